@@ -1,0 +1,252 @@
+/* voxplane_b200 — C ABI of the B200-native voxel-map / plane-segmentation path.
+ *
+ * Drop-in for the hot path of the reference C++ library `voxplane`
+ * (/root/reference/proj/core): the per-frame update
+ *   clear_rays -> integrate_frame -> recenter -> estimate_normals ->
+ *   classify_steppable -> build_adjacency + label_components ->
+ *   filter_clusters -> fit_planes -> refine_plane -> make_polygon
+ * driven by run_frames (pipeline.cpp:199-213) and voxel_frame_polygons
+ * (pipeline.cpp:43-85). Every entry point below names the reference
+ * interface it replaces. Plain pointers and sizes only; no C++ or torch types.
+ *
+ * Conventions
+ *   - return value: VP_OK or a VP_E* code; vp_last_error() gives the message
+ *     (thread-local). VP_EINVAL corresponds to the reference's
+ *     std::invalid_argument, VP_EEMPTY to estimate_normals on an empty grid.
+ *   - rotations are 9 doubles row-major (r00 r01 r02 r10 ...), translations 3.
+ *   - points are n x 3 float32 sensor-frame xyz (SensorFrame::points).
+ *   - voxel indices are window (logical) coordinates, as the reference's.
+ *   - arrays returned through vp_*_t** are owned by the library; free them
+ *     with the matching vp_*_free.
+ *   - every call is synchronous on return (the grid's CUDA stream is drained).
+ */
+#ifndef VOXPLANE_B200_H
+#define VOXPLANE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VP_OK 0
+#define VP_EINVAL 1    /* std::invalid_argument in the reference            */
+#define VP_EEMPTY 2    /* estimate_normals: empty grid (segmentation.cpp:22) */
+#define VP_ENOMEM 3    /* device allocation failed                          */
+#define VP_ECUDA 4     /* CUDA runtime / launch error                       */
+#define VP_ENODEV 5    /* no usable sm_100 device                           */
+
+typedef struct vp_grid vp_grid;         /* VoxelGrid (voxel_grid.hpp:17-91)  */
+typedef struct vp_pipeline vp_pipeline; /* run_frames state (pipeline.cpp:157-245) */
+
+/* types.hpp:63-76 */
+typedef struct { uint64_t voxels_touched, points_discarded; } vp_update_stats;
+typedef struct { uint64_t voxels_cleared, voxels_freed; } vp_clear_stats;
+typedef struct { int32_t shift[3]; uint64_t voxels_dropped; } vp_shift_stats;
+
+/* SegmentationParams (segmentation.hpp:11-19) */
+typedef struct {
+  int32_t neighbor_radius;     /* 1 */
+  int32_t min_neighbors;       /* 3 */
+  double max_angle_deg;        /* 15 */
+  double adjacency_angle_deg;  /* 15 */
+  double distance_th;          /* 0.05 */
+  int32_t min_cluster_size;    /* 30 */
+  double up[3];                /* (0,0,1) */
+} vp_seg_params;
+
+/* RansacParams (plane_fit.hpp:28-34); execution: 0 ClusterParallel, 1 PerClusterSerial */
+typedef struct {
+  int32_t iterations;  /* 100 */
+  double inlier_eps;   /* 0.01 */
+  uint64_t seed;       /* 0 (RunConfig.seed is synced in by the config loader) */
+  double up[3];
+  int32_t execution;
+} vp_ransac_params;
+
+/* Everything voxel_frame_polygons reads from PipelineConfig (pipeline.cpp:43-85). */
+typedef struct {
+  vp_seg_params seg;
+  vp_ransac_params ransac;
+  int32_t refine;            /* RunConfig.refine, default 1 */
+  double min_polygon_area;   /* OutputConfig.min_polygon_area, default 0.002 */
+  int32_t refine_exact;      /* 1: sequential refine sums (bit-identical to the
+                                reference); 0: deterministic tree reduction
+                                (within the 1e-4 rad / 1e-4 m tolerance) */
+} vp_pipeline_params;
+
+/* PlaneModel (plane_fit.hpp:13-18) */
+typedef struct {
+  double normal[3];
+  double offset;
+  int32_t inlier_count;
+  int32_t cluster_label;
+} vp_plane;
+
+/* PlanePolygon (polygonize.hpp:49-54) */
+typedef struct {
+  vp_plane plane;
+  uint32_t nverts;
+  const double* v2d; /* nverts x 2 */
+  const double* v3d; /* nverts x 3 */
+  double area;
+} vp_polygon;
+
+typedef struct {
+  size_t count;
+  vp_polygon* polys;
+} vp_polygons_t;
+
+/* OccupiedVoxel list (types.hpp:19-24), lexicographic window order */
+typedef struct {
+  size_t count;
+  int32_t* idx;     /* count x 3 */
+  double* mean;     /* count x 3 */
+  uint32_t* npts;   /* count     */
+  uint8_t* status;  /* count     */
+} vp_occupied_t;
+
+/* SurfaceEstimate list (segmentation.hpp:24-31) */
+typedef struct {
+  size_t count;
+  int32_t* idx;            /* count x 3 */
+  double* mean;            /* count x 3 */
+  double* normal;          /* count x 3 */
+  int32_t* neighbor_count;
+  double* angle_to_up_deg; /* host libm acos of normal.up (segmentation.cpp:62-63) */
+  uint8_t* valid;
+} vp_estimates_t;
+
+/* SteppablePoint list (segmentation.hpp:33-42), ordinal = position */
+typedef struct {
+  size_t count;
+  int32_t* idx;    /* count x 3 */
+  double* mean;    /* count x 3 */
+  double* normal;  /* count x 3 */
+} vp_steppable_t;
+
+/* ClusterFit list (plane_fit.hpp:36-39); inliers of fit f are
+   inliers[offsets[f] .. offsets[f+1]) (x3 doubles) */
+typedef struct {
+  size_t count;
+  vp_plane* models;
+  uint64_t* offsets;  /* count + 1 */
+  double* inliers;
+  uint64_t clusters_skipped_small; /* FitStats (plane_fit.hpp:41-44) */
+  uint64_t clusters_unfit;
+} vp_fits_t;
+
+/* FrameTiming stage spans (metrics.hpp:51-62), CUDA-event milliseconds */
+typedef struct {
+  double mapping_ms, classify_ms, cluster_ms, ransac_ms, hull_ms, total_ms;
+  uint64_t points, voxels, clusters;
+} vp_frame_timing;
+
+const char* vp_last_error(void);
+const char* vp_version(void);
+
+/* ---- defaults (segmentation.hpp:11-19, plane_fit.hpp:28-34, config.hpp:13-28) */
+void vp_default_params(vp_pipeline_params* p);
+
+/* ---- VoxelGrid ------------------------------------------------------- */
+/* VoxelGrid::VoxelGrid (voxel_grid.cpp:19-25); throws invalid_argument -> VP_EINVAL */
+int vp_grid_create(double resolution, const int32_t extent[3], const double center[3],
+                   int device, vp_grid** out);
+void vp_grid_destroy(vp_grid* g);
+/* origin() / extent() / resolution() / occupied_count() (voxel_grid.hpp:32-52) */
+int vp_grid_info(const vp_grid* g, double origin[3], int32_t extent[3], double* resolution,
+                 uint64_t* occupied_count);
+/* VoxelGrid::integrate_frame (voxel_grid.cpp:59-115) */
+int vp_integrate_frame(vp_grid* g, const float* xyz, uint64_t n, const double rotation[9],
+                       const double translation[3], vp_update_stats* stats);
+/* VoxelGrid::clear_rays (voxel_grid.cpp:182-215) */
+int vp_clear_rays(vp_grid* g, const float* xyz, uint64_t n, const double rotation[9],
+                  const double translation[3], vp_clear_stats* stats);
+/* VoxelGrid::recenter (voxel_grid.cpp:217-252) */
+int vp_recenter(vp_grid* g, const double new_center[3], vp_shift_stats* stats);
+/* VoxelGrid::merge_point (voxel_grid.cpp:49-57), idx in window coordinates */
+int vp_merge_point(vp_grid* g, const int32_t idx[3], const double p[3]);
+/* VoxelGrid::cell(idx) (voxel_grid.hpp:49): sums, count, status of one cell */
+int vp_get_cell(vp_grid* g, const int32_t idx[3], double sum[3], uint32_t* count,
+                uint8_t* status);
+/* VoxelGrid::set_status (voxel_grid.hpp:78) */
+int vp_set_status(vp_grid* g, const int32_t idx[3], uint8_t status);
+/* VoxelGrid::occupied_voxels (voxel_grid.cpp:254-263) */
+int vp_occupied_voxels(vp_grid* g, vp_occupied_t** out);
+void vp_occupied_free(vp_occupied_t* o);
+
+/* ---- segmentation.hpp -------------------------------------------------- */
+/* estimate_normals (segmentation.cpp:19-67) */
+int vp_estimate_normals(vp_grid* g, const vp_seg_params* p, vp_estimates_t** out);
+void vp_estimates_free(vp_estimates_t* e);
+/* classify_steppable (segmentation.cpp:69-85) on the grid's current estimates
+   (fused on device with estimate_normals); writes statuses back to the grid.
+   objects_idx (optional) receives V_obj x 3 indices. */
+int vp_classify_steppable(vp_grid* g, const vp_seg_params* p, vp_steppable_t** steppable,
+                          int32_t** objects_idx, size_t* n_objects);
+void vp_steppable_free(vp_steppable_t* s);
+void vp_free(void* p);
+/* build_adjacency + label_components (segmentation.cpp:87-194) for a host
+   steppable list: labels[i] = canonical component minimum ordinal. */
+int vp_label_components(const vp_steppable_t* steppable, const vp_seg_params* p,
+                        double resolution, int device, int32_t* labels);
+/* build_adjacency (segmentation.cpp:87-132) materialised as CSR (ascending
+   neighbour lists) for API completeness; not used on the fused path. */
+int vp_build_adjacency(const vp_steppable_t* steppable, const vp_seg_params* p,
+                       double resolution, int device, uint64_t** row_offsets,
+                       int32_t** cols, uint64_t* n_edges);
+
+/* ---- plane_fit.hpp / polygonize.hpp ------------------------------------ */
+/* fit_planes (plane_fit.cpp:55-131). Clusters in CSR form: cluster c has
+   label labels[c] and member means means[offsets[c] .. offsets[c+1]) (x3). */
+int vp_fit_planes(size_t n_clusters, const int32_t* labels, const uint64_t* offsets,
+                  const double* means, const vp_ransac_params* p, int device,
+                  vp_fits_t** out);
+void vp_fits_free(vp_fits_t* f);
+/* refine_plane (plane_fit.cpp:133-154) for every fit; exact!=0 reproduces
+   the sequential sums bit-for-bit. */
+int vp_refine_planes(const vp_fits_t* fits, const double up[3], int exact, int device,
+                     vp_plane* refined);
+/* make_polygon (polygonize.cpp:166-182) for every (plane, inlier set);
+   polygons that are nullopt in the reference come back with nverts == 0. */
+int vp_make_polygons(size_t n, const vp_plane* planes, const uint64_t* offsets,
+                     const double* inliers, int filter_directions, int device,
+                     vp_polygons_t** out);
+void vp_polygons_free(vp_polygons_t* p);
+
+/* ---- composite ----------------------------------------------------------- */
+/* segment(): voxel_frame_polygons (pipeline.cpp:43-85) on the device-resident
+   grid: polygons in ascending cluster-label order, area-filtered. */
+int vp_segment(vp_grid* g, const vp_pipeline_params* p, vp_polygons_t** out,
+               vp_frame_timing* timing);
+
+/* run_frames state: a grid plus the global-cell recenter trigger
+   (pipeline.cpp:165, 174, 199-213). */
+int vp_pipeline_create(double resolution, const int32_t extent[3],
+                       const double start_center[3], const vp_pipeline_params* p,
+                       int device, vp_pipeline** out);
+void vp_pipeline_destroy(vp_pipeline* pl);
+vp_grid* vp_pipeline_grid(vp_pipeline* pl);
+/* One frame of run_frames: clear_rays, integrate_frame, recenter-if-moved,
+   voxel_frame_polygons. out may be NULL (polygons stay on the device). */
+int vp_pipeline_frame(vp_pipeline* pl, const float* xyz, uint64_t n, const double rotation[9],
+                      const double translation[3], vp_polygons_t** out,
+                      vp_frame_timing* timing);
+/* Same frame step, device-resident input (xyz_dev is a device pointer). */
+int vp_pipeline_frame_device(vp_pipeline* pl, const float* xyz_dev, uint64_t n,
+                             const double rotation[9], const double translation[3],
+                             vp_polygons_t** out, vp_frame_timing* timing);
+/* Same frame step, returning the stage trace (voxplane_trace.h); buf is
+   freed with vp_free. */
+int vp_pipeline_frame_trace(vp_pipeline* pl, const float* xyz, uint64_t n,
+                            const double rotation[9], const double translation[3],
+                            uint8_t** buf, uint64_t* len);
+
+/* Count of this library's kernel launches since process start (bench evidence). */
+uint64_t vp_kernel_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif
