@@ -1,0 +1,418 @@
+"""ctypes binding of the C ABI in include/voxplane_b200.h.
+
+This is the Python harness's view of the product library
+(`paper_2510_01592_b200/lib/libvoxplane_b200.so`, hand-written sm_100a
+kernels + host runtime). There is no fallback: if the library is missing or
+no B200 is visible, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "lib", "libvoxplane_b200.so")
+
+VP_OK, VP_EINVAL, VP_EEMPTY, VP_ENOMEM, VP_ECUDA, VP_ENODEV = range(6)
+
+
+class VpError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"voxplane_b200 error {code}: {msg}")
+        self.code = code
+
+
+class InvalidArgument(VpError, ValueError):
+    """std::invalid_argument in the reference."""
+
+
+class SegParams(C.Structure):
+    _fields_ = [("neighbor_radius", C.c_int32), ("min_neighbors", C.c_int32),
+                ("max_angle_deg", C.c_double), ("adjacency_angle_deg", C.c_double),
+                ("distance_th", C.c_double), ("min_cluster_size", C.c_int32),
+                ("up", C.c_double * 3)]
+
+
+class RansacParams(C.Structure):
+    _fields_ = [("iterations", C.c_int32), ("inlier_eps", C.c_double), ("seed", C.c_uint64),
+                ("up", C.c_double * 3), ("execution", C.c_int32)]
+
+
+class PipelineParams(C.Structure):
+    _fields_ = [("seg", SegParams), ("ransac", RansacParams), ("refine", C.c_int32),
+                ("min_polygon_area", C.c_double), ("refine_exact", C.c_int32)]
+
+
+class UpdateStats(C.Structure):
+    _fields_ = [("voxels_touched", C.c_uint64), ("points_discarded", C.c_uint64)]
+
+
+class ClearStats(C.Structure):
+    _fields_ = [("voxels_cleared", C.c_uint64), ("voxels_freed", C.c_uint64)]
+
+
+class ShiftStats(C.Structure):
+    _fields_ = [("shift", C.c_int32 * 3), ("voxels_dropped", C.c_uint64)]
+
+
+class Plane(C.Structure):
+    _fields_ = [("normal", C.c_double * 3), ("offset", C.c_double), ("inlier_count", C.c_int32),
+                ("cluster_label", C.c_int32)]
+
+
+class Polygon(C.Structure):
+    _fields_ = [("plane", Plane), ("nverts", C.c_uint32), ("v2d", C.POINTER(C.c_double)),
+                ("v3d", C.POINTER(C.c_double)), ("area", C.c_double)]
+
+
+class Polygons(C.Structure):
+    _fields_ = [("count", C.c_size_t), ("polys", C.POINTER(Polygon))]
+
+
+class Occupied(C.Structure):
+    _fields_ = [("count", C.c_size_t), ("idx", C.POINTER(C.c_int32)), ("mean", C.POINTER(C.c_double)),
+                ("npts", C.POINTER(C.c_uint32)), ("status", C.POINTER(C.c_uint8))]
+
+
+class Estimates(C.Structure):
+    _fields_ = [("count", C.c_size_t), ("idx", C.POINTER(C.c_int32)), ("mean", C.POINTER(C.c_double)),
+                ("normal", C.POINTER(C.c_double)), ("neighbor_count", C.POINTER(C.c_int32)),
+                ("angle_to_up_deg", C.POINTER(C.c_double)), ("valid", C.POINTER(C.c_uint8))]
+
+
+class Steppable(C.Structure):
+    _fields_ = [("count", C.c_size_t), ("idx", C.POINTER(C.c_int32)), ("mean", C.POINTER(C.c_double)),
+                ("normal", C.POINTER(C.c_double))]
+
+
+class Fits(C.Structure):
+    _fields_ = [("count", C.c_size_t), ("models", C.POINTER(Plane)), ("offsets", C.POINTER(C.c_uint64)),
+                ("inliers", C.POINTER(C.c_double)), ("clusters_skipped_small", C.c_uint64),
+                ("clusters_unfit", C.c_uint64)]
+
+
+class FrameTiming(C.Structure):
+    _fields_ = [("mapping_ms", C.c_double), ("classify_ms", C.c_double), ("cluster_ms", C.c_double),
+                ("ransac_ms", C.c_double), ("hull_ms", C.c_double), ("total_ms", C.c_double),
+                ("points", C.c_uint64), ("voxels", C.c_uint64), ("clusters", C.c_uint64)]
+
+
+def default_params(seed: int = 0, refine: bool = True, min_area: float = 0.002,
+                   refine_exact: bool = False) -> PipelineParams:
+    """SegmentationParams / RansacParams / RunConfig / OutputConfig defaults."""
+    p = PipelineParams()
+    s = p.seg
+    s.neighbor_radius, s.min_neighbors = 1, 3
+    s.max_angle_deg = s.adjacency_angle_deg = 15.0
+    s.distance_th, s.min_cluster_size = 0.05, 30
+    s.up[:] = (0.0, 0.0, 1.0)
+    r = p.ransac
+    r.iterations, r.inlier_eps, r.seed, r.execution = 100, 0.01, seed, 0
+    r.up[:] = (0.0, 0.0, 1.0)
+    p.refine = 1 if refine else 0
+    p.min_polygon_area = min_area
+    p.refine_exact = 1 if refine_exact else 0
+    return p
+
+
+_lib = None
+
+
+def lib():
+    """Load the product library (raises if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run __graft_entry__.build()")
+        L = C.CDLL(LIB_PATH)
+        L.vp_last_error.restype = C.c_char_p
+        L.vp_version.restype = C.c_char_p
+        L.vp_pipeline_grid.restype = C.c_void_p
+        L.vp_kernel_launch_count.restype = C.c_uint64
+        _lib = L
+    return _lib
+
+
+def check(rc):
+    if rc != VP_OK:
+        msg = lib().vp_last_error().decode(errors="replace")
+        if rc == VP_EINVAL:
+            raise InvalidArgument(rc, msg)
+        raise VpError(rc, msg)
+
+
+def _p(a, t):
+    return a.ctypes.data_as(C.POINTER(t))
+
+
+def _pose(R, t):
+    R = np.ascontiguousarray(R, np.float64).reshape(9)
+    t = np.ascontiguousarray(t, np.float64).reshape(3)
+    return R, t
+
+
+def polygons_to_py(pp) -> list[dict]:
+    out = []
+    P = pp.contents
+    for i in range(P.count):
+        q = P.polys[i]
+        nv = q.nverts
+        v2 = np.ctypeslib.as_array(q.v2d, (nv, 2)).copy() if nv else np.zeros((0, 2))
+        v3 = np.ctypeslib.as_array(q.v3d, (nv, 3)).copy() if nv else np.zeros((0, 3))
+        out.append(dict(normal=np.array(q.plane.normal[:]), offset=q.plane.offset,
+                        inlier_count=q.plane.inlier_count, label=q.plane.cluster_label,
+                        v2d=v2, v3d=v3, area=q.area))
+    lib().vp_polygons_free(pp)
+    return out
+
+
+class Pipeline:
+    """run_frames state on the device (vp_pipeline_*)."""
+
+    def __init__(self, res, extent, start_center, params: PipelineParams | None = None, device=0):
+        self.params = params or default_params()
+        ext = np.asarray(extent, np.int32)
+        c = np.asarray(start_center, np.float64)
+        self.h = C.c_void_p()
+        check(lib().vp_pipeline_create(C.c_double(res), _p(ext, C.c_int32), _p(c, C.c_double),
+                                       C.byref(self.params), C.c_int(device), C.byref(self.h)))
+
+    def frame(self, pts, R, t, want_polygons=True):
+        pts = np.ascontiguousarray(pts, np.float32)
+        R, t = _pose(R, t)
+        out = C.POINTER(Polygons)()
+        tm = FrameTiming()
+        check(lib().vp_pipeline_frame(self.h, _p(pts, C.c_float), C.c_uint64(len(pts)),
+                                      _p(R, C.c_double), _p(t, C.c_double),
+                                      C.byref(out) if want_polygons else None, C.byref(tm)))
+        return (polygons_to_py(out) if want_polygons else None), tm
+
+    def frame_device(self, pts_dev_ptr: int, n: int, R, t, want_polygons=False):
+        R, t = _pose(R, t)
+        out = C.POINTER(Polygons)()
+        tm = FrameTiming()
+        check(lib().vp_pipeline_frame_device(self.h, C.c_void_p(pts_dev_ptr), C.c_uint64(n),
+                                             _p(R, C.c_double), _p(t, C.c_double),
+                                             C.byref(out) if want_polygons else None, C.byref(tm)))
+        return (polygons_to_py(out) if want_polygons else None), tm
+
+    def frame_trace_raw(self, pts, R, t) -> bytes:
+        pts = np.ascontiguousarray(pts, np.float32)
+        R, t = _pose(R, t)
+        buf = C.POINTER(C.c_uint8)()
+        n = C.c_uint64()
+        check(lib().vp_pipeline_frame_trace(self.h, _p(pts, C.c_float), C.c_uint64(len(pts)),
+                                            _p(R, C.c_double), _p(t, C.c_double), C.byref(buf),
+                                            C.byref(n)))
+        data = C.string_at(buf, n.value)
+        lib().vp_free(buf)
+        return data
+
+    def frame_trace(self, pts, R, t):
+        from .trace import parse_trace
+        return parse_trace(self.frame_trace_raw(pts, R, t))
+
+    @property
+    def grid(self) -> "Grid":
+        return Grid._borrow(lib().vp_pipeline_grid(self.h))
+
+    def close(self):
+        if self.h:
+            lib().vp_pipeline_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Grid:
+    """VoxelGrid (voxel_grid.hpp:17-91) on the device."""
+
+    def __init__(self, res, extent, center, device=0):
+        ext = np.asarray(extent, np.int32)
+        c = np.asarray(center, np.float64)
+        self.h = C.c_void_p()
+        self.owned = True
+        check(lib().vp_grid_create(C.c_double(res), _p(ext, C.c_int32), _p(c, C.c_double),
+                                   C.c_int(device), C.byref(self.h)))
+
+    @classmethod
+    def _borrow(cls, h):
+        g = cls.__new__(cls)
+        g.h = C.c_void_p(h)
+        g.owned = False
+        return g
+
+    def info(self):
+        o = np.zeros(3)
+        e = np.zeros(3, np.int32)
+        r = C.c_double()
+        n = C.c_uint64()
+        check(lib().vp_grid_info(self.h, _p(o, C.c_double), _p(e, C.c_int32), C.byref(r), C.byref(n)))
+        return dict(origin=o, extent=e, resolution=r.value, occupied_count=n.value)
+
+    def integrate_frame(self, pts, R, t):
+        pts = np.ascontiguousarray(pts, np.float32)
+        R, t = _pose(R, t)
+        st = UpdateStats()
+        check(lib().vp_integrate_frame(self.h, _p(pts, C.c_float), C.c_uint64(len(pts)),
+                                       _p(R, C.c_double), _p(t, C.c_double), C.byref(st)))
+        return st.voxels_touched, st.points_discarded
+
+    def clear_rays(self, pts, R, t):
+        pts = np.ascontiguousarray(pts, np.float32)
+        R, t = _pose(R, t)
+        st = ClearStats()
+        check(lib().vp_clear_rays(self.h, _p(pts, C.c_float), C.c_uint64(len(pts)),
+                                  _p(R, C.c_double), _p(t, C.c_double), C.byref(st)))
+        return st.voxels_cleared, st.voxels_freed
+
+    def recenter(self, c):
+        c = np.ascontiguousarray(c, np.float64)
+        st = ShiftStats()
+        check(lib().vp_recenter(self.h, _p(c, C.c_double), C.byref(st)))
+        return tuple(st.shift[:]), st.voxels_dropped
+
+    def merge_point(self, idx, p):
+        i = np.asarray(idx, np.int32)
+        q = np.asarray(p, np.float64)
+        check(lib().vp_merge_point(self.h, _p(i, C.c_int32), _p(q, C.c_double)))
+
+    def cell(self, idx):
+        i = np.asarray(idx, np.int32)
+        s = np.zeros(3)
+        n = C.c_uint32()
+        st = C.c_uint8()
+        check(lib().vp_get_cell(self.h, _p(i, C.c_int32), _p(s, C.c_double), C.byref(n), C.byref(st)))
+        return s, n.value, st.value
+
+    def set_status(self, idx, status):
+        i = np.asarray(idx, np.int32)
+        check(lib().vp_set_status(self.h, _p(i, C.c_int32), C.c_uint8(status)))
+
+    def occupied_voxels(self):
+        o = C.POINTER(Occupied)()
+        check(lib().vp_occupied_voxels(self.h, C.byref(o)))
+        O = o.contents
+        n = O.count
+        res = dict(idx=np.ctypeslib.as_array(O.idx, (n, 3)).copy() if n else np.zeros((0, 3), np.int32),
+                   mean=np.ctypeslib.as_array(O.mean, (n, 3)).copy() if n else np.zeros((0, 3)),
+                   count=np.ctypeslib.as_array(O.npts, (n,)).copy() if n else np.zeros(0, np.uint32),
+                   status=np.ctypeslib.as_array(O.status, (n,)).copy() if n else np.zeros(0, np.uint8))
+        lib().vp_occupied_free(o)
+        return res
+
+    def estimate_normals(self, seg: SegParams):
+        e = C.POINTER(Estimates)()
+        check(lib().vp_estimate_normals(self.h, C.byref(seg), C.byref(e)))
+        E = e.contents
+        n = E.count
+
+        def arr(p, shape, dt):
+            return np.ctypeslib.as_array(p, shape).copy() if n else np.zeros(shape, dt)
+        res = dict(idx=arr(E.idx, (n, 3), np.int32), mean=arr(E.mean, (n, 3), float),
+                   normal=arr(E.normal, (n, 3), float), neighbor_count=arr(E.neighbor_count, (n,), np.int32),
+                   angle=arr(E.angle_to_up_deg, (n,), float), valid=arr(E.valid, (n,), np.uint8))
+        lib().vp_estimates_free(e)
+        return res
+
+    def segment(self, params: PipelineParams):
+        out = C.POINTER(Polygons)()
+        tm = FrameTiming()
+        check(lib().vp_segment(self.h, C.byref(params), C.byref(out), C.byref(tm)))
+        return polygons_to_py(out), tm
+
+    def close(self):
+        if self.h and self.owned:
+            lib().vp_grid_destroy(self.h)
+        self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def label_components(st_idx, st_mean, st_normal, seg: SegParams, res: float, device=0):
+    n = len(st_idx)
+    s = Steppable()
+    idx = np.ascontiguousarray(st_idx, np.int32)
+    mean = np.ascontiguousarray(st_mean, np.float64)
+    nrm = np.ascontiguousarray(st_normal, np.float64)
+    s.count = n
+    s.idx, s.mean, s.normal = _p(idx, C.c_int32), _p(mean, C.c_double), _p(nrm, C.c_double)
+    labels = np.zeros(n, np.int32)
+    check(lib().vp_label_components(C.byref(s), C.byref(seg), C.c_double(res), C.c_int(device),
+                                    _p(labels, C.c_int32)))
+    return labels
+
+
+def fit_planes(labels, offsets, means, rp: RansacParams, device=0):
+    labels = np.ascontiguousarray(labels, np.int32)
+    offsets = np.ascontiguousarray(offsets, np.uint64)
+    means = np.ascontiguousarray(means, np.float64)
+    f = C.POINTER(Fits)()
+    check(lib().vp_fit_planes(C.c_size_t(len(labels)), _p(labels, C.c_int32), _p(offsets, C.c_uint64),
+                              _p(means, C.c_double), C.byref(rp), C.c_int(device), C.byref(f)))
+    F = f.contents
+    n = F.count
+    offs = np.ctypeslib.as_array(F.offsets, (n + 1,)).copy()
+    tot = int(offs[-1]) if n else 0
+    inl = np.ctypeslib.as_array(F.inliers, (tot, 3)).copy() if tot else np.zeros((0, 3))
+    models = [dict(normal=np.array(F.models[i].normal[:]), offset=F.models[i].offset,
+                   inlier_count=F.models[i].inlier_count, label=F.models[i].cluster_label,
+                   inliers=inl[offs[i]:offs[i + 1]]) for i in range(n)]
+    stats = (F.clusters_skipped_small, F.clusters_unfit)
+    lib().vp_fits_free(f)
+    return models, stats
+
+
+def make_polygons(planes, inlier_sets, directions=16, device=0):
+    n = len(planes)
+    arr = (Plane * max(n, 1))()
+    for i, p in enumerate(planes):
+        arr[i].normal[:] = tuple(p["normal"])
+        arr[i].offset = p["offset"]
+        arr[i].inlier_count = p.get("inlier_count", 0)
+        arr[i].cluster_label = p.get("label", -1)
+    offs = np.zeros(n + 1, np.uint64)
+    offs[1:] = np.cumsum([len(s) for s in inlier_sets])
+    pts = np.ascontiguousarray(np.concatenate(inlier_sets) if n else np.zeros((0, 3)), np.float64)
+    out = C.POINTER(Polygons)()
+    check(lib().vp_make_polygons(C.c_size_t(n), arr, _p(offs, C.c_uint64), _p(pts, C.c_double),
+                                 C.c_int(directions), C.c_int(device), C.byref(out)))
+    return polygons_to_py(out)
+
+
+def refine_planes(fits_models, up=(0.0, 0.0, 1.0), exact=False, device=0):
+    """refine_plane for a list of dict(normal, offset, inlier_count, label, inliers)."""
+    n = len(fits_models)
+    f = Fits()
+    models = (Plane * max(n, 1))()
+    for i, m in enumerate(fits_models):
+        models[i].normal[:] = tuple(m["normal"])
+        models[i].offset = m["offset"]
+        models[i].inlier_count = m["inlier_count"]
+        models[i].cluster_label = m["label"]
+    offs = np.zeros(n + 1, np.uint64)
+    offs[1:] = np.cumsum([len(m["inliers"]) for m in fits_models])
+    pts = np.ascontiguousarray(np.concatenate([m["inliers"] for m in fits_models]) if n else np.zeros((0, 3)))
+    f.count = n
+    f.models = C.cast(models, C.POINTER(Plane))
+    f.offsets = _p(offs, C.c_uint64)
+    f.inliers = _p(pts, C.c_double)
+    out = (Plane * max(n, 1))()
+    u = np.asarray(up, np.float64)
+    check(lib().vp_refine_planes(C.byref(f), _p(u, C.c_double), C.c_int(1 if exact else 0),
+                                 C.c_int(device), out))
+    return [(np.array(out[i].normal[:]), out[i].offset) for i in range(n)]
+
+
+def kernel_launch_count() -> int:
+    return int(lib().vp_kernel_launch_count())
