@@ -1,0 +1,414 @@
+"""Benchmark: segmentation update rate of the full per-frame update
+(clear -> integrate -> recenter -> normals/classify -> CCL -> RANSAC -> refine
+-> hull) on BASELINE.json configs[1] (C2: Stair5 + stepping stones, 30-frame
+640x480 depth stream, 0.01 m voxels, 500^3 window), one B200 per rank.
+
+A step = one pass over the 30-frame stream from an empty map (the map is reset
+between steps, untimed, together with an L2 flush). `value` = frames/s with
+every frame already resident in HBM (device time, CUDA events on the
+library's stream, max over ranks); `e2e` = the same through the public C ABI
+with pinned-host inputs (H2D inside) and the polygons read back every frame.
+
+--impl reference times the reference's own CPU implementation (oracle/_ref:
+the unmodified /root/reference sources) on the host cores over a bounded
+sample of the same stream.
+
+N > 1: the path is a per-robot map; without slab decomposition (SURVEY §8(e),
+not built yet) ranks run independent replicas of the stream (weak scaling, no
+data-path collective); only the timing barrier / max use torch.distributed.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "segmentation update rate (Hz, ms/frame) at 0.01 m; points/s integrated; HBM GB/s"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if len(r) > 8 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 8 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) > 8 for i in range(4)
+                          if r[5 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# --------------------------------------------------------------- workload
+def load_workload(name):
+    from paper_2510_01592_b200 import scenes
+    t = time.time()
+    wl = scenes.workload(name)
+    log(f"[bench] workload {name}: {len(wl.frames)} frames, {wl.points} points, "
+        f"rendered in {time.time() - t:.1f}s")
+    return wl
+
+
+def algorithmic_bytes(c, n_points):
+    """SURVEY.md §8(d) unique-touch byte model, per kernel, from one frame's counters.
+    c = vp_pipeline_counters: cleared freed touched discarded dropped occupied V S K
+    fits padded inliers poolv newly groups overflow."""
+    cleared, freed, touched, _, dropped, _, V, S, K, F, padded, inl, poolv = c[:13]
+    return {
+        "k_clear_walk": 12 * n_points + cleared / 8,           # points in, clear marks out
+        "k_clear_apply": 2 * C_BITS + 32 * freed,              # clr (+occ) scan, freed cells
+        "k_integrate_hash": 12 * n_points + 8 * n_points,
+        "k_integrate_fold": 64 * touched + 12 * n_points,      # cell RMW + points
+        "k_recenter": 3 * C_BITS + 32 * dropped,
+        "k_bitmap_count": C_BITS,
+        "k_bitmap_emit": C_BITS + 4 * V,
+        "k_normals": 32 * V + 4 * V + 72 * V,                  # cells, list in, estimate out
+        "k_ccl_union": 56 * S,                                 # mean+normal+ordinal per voxel
+        "k_ccl_flatten": 12 * S,
+        "k_ransac_count": 24 * padded,
+        "k_ransac_extract": 24 * padded + 24 * inl,
+        "k_refine": 2 * 24 * inl,
+        "k_polygon": 24 * inl + 64 * poolv,
+    }
+
+
+C_BITS = 0  # set from the grid size (cells / 8)
+
+
+# ------------------------------------------------------------------- ours
+def run_ours(args, rank, world, dist):
+    import numpy as np
+    import torch
+
+    from paper_2510_01592_b200 import native
+
+    global C_BITS
+    dev = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(dev)
+    wl = load_workload(args.workload)
+    nx, ny, nz = wl.extent
+    C_BITS = nx * ny * nz // 8
+    frames = wl.frames
+    nf = len(frames)
+    npts = [len(f.points) for f in frames]
+    params = native.default_params(seed=wl.seed)
+    pl = native.Pipeline(wl.resolution, wl.extent, frames[0].translation, params, device=dev)
+    L = native.lib()
+    L.vp_pipeline_stream.restype = C.c_void_p
+    stream = torch.cuda.ExternalStream(L.vp_pipeline_stream(pl.h))
+    start = np.ascontiguousarray(frames[0].translation, np.float64)
+
+    def reset():
+        native.check(L.vp_pipeline_reset(pl.h, start.ctypes.data_as(C.POINTER(C.c_double))))
+
+    dev_pts = [torch.from_numpy(f.points).to(f"cuda:{dev}") for f in frames]
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{dev}")
+    torch.cuda.synchronize()
+
+    def device_step():
+        for f, d in zip(frames, dev_pts):
+            pl.frame_device(d.data_ptr(), len(f.points), f.rotation, f.translation)
+
+    # warm-up
+    for _ in range(args.warmup):
+        reset()
+        device_step()
+    torch.cuda.synchronize()
+
+    # timed: device-resident inputs
+    launches0 = native.kernel_launch_count()
+    times = []
+    with ClockSampler(dev) as clk:
+        for _ in range(args.steps):
+            reset()
+            flush.fill_(1.0)  # > L2: evict the previous step's working set
+            torch.cuda.synchronize()
+            if dist:
+                dist.barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            device_step()
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+    launches = native.kernel_launch_count() - launches0
+    counters = np.zeros(16, np.uint64)
+    L.vp_pipeline_counters(pl.h, counters.ctypes.data_as(C.POINTER(C.c_uint64)))
+    step_ms = sum(times) / len(times)
+    if dist:
+        t = torch.tensor([sum(times)], device=f"cuda:{dev}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    else:
+        total_ms = sum(times)
+    value = world * nf * args.steps / (total_ms / 1e3)
+
+    # e2e through the public API: pinned host points, H2D + D2H inside
+    host_pts = [torch.from_numpy(f.points).pin_memory() for f in frames]
+    e2e_times = []
+    d2h_bytes = 0
+    for s in range(max(1, args.steps)):
+        reset()
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        nbytes = 0
+        for f, hp in zip(frames, host_pts):
+            polys, _ = pl.frame_ptr(hp.data_ptr(), len(f.points), f.rotation, f.translation)
+            nbytes += sum(40 + 8 + 40 * len(p["v3d"]) for p in polys) + 128
+        e2e_times.append(time.perf_counter() - t0)
+        d2h_bytes = nbytes
+    e2e_total = sum(e2e_times)
+    if dist:
+        t = torch.tensor([e2e_total], device=f"cuda:{dev}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_total = float(t.item())
+    e2e_value = world * nf * len(e2e_times) / e2e_total
+
+    # per-kernel profile of one step (serialised launches; shares only)
+    L.vp_profile_read.restype = C.c_int
+    reset()
+    L.vp_profile_enable(1)
+    per_frame_counters = []
+    for f, d in zip(frames, dev_pts):
+        pl.frame_device(d.data_ptr(), len(f.points), f.rotation, f.translation)
+        cc = np.zeros(16, np.uint64)
+        L.vp_pipeline_counters(pl.h, cc.ctypes.data_as(C.POINTER(C.c_uint64)))
+        per_frame_counters.append(cc.astype(np.float64))
+    names = (C.c_char_p * 128)()
+    ms = (C.c_double * 128)()
+    calls = (C.c_uint64 * 128)()
+    nk = L.vp_profile_read(names, ms, calls, 128)
+    L.vp_profile_enable(0)
+    prof = {names[i].decode(): (ms[i], calls[i]) for i in range(nk)}
+    prof_total = sum(v[0] for v in prof.values())
+    top = max(prof, key=lambda k: prof[k][0])
+    # algorithmic bytes of the top kernel, summed over the step's frames
+    alg = sum(algorithmic_bytes(c, n).get(top, 0.0) for c, n in zip(per_frame_counters, npts))
+    top_ms, top_calls = prof[top]
+    per_launch_bytes = alg / top_calls
+    per_launch_s = top_ms / top_calls / 1e3
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    achieved = per_launch_bytes / per_launch_s / 1e9
+    # whole-step algorithmic bytes (the survey's frame formula)
+    step_bytes = 0.0
+    for c, n in zip(per_frame_counters, npts):
+        cleared, freed, touched, _, dropped, _, V, S, K, F, padded, inl, poolv = c[:13]
+        step_bytes += (12 * n + 64 * touched + 32 * freed + C_BITS + 72 * V + 56 * S + 24 * padded
+                       + 48 * inl + 64 * poolv)
+    out = {
+        "metric": METRIC,
+        "value": round(value, 3),
+        "unit": "Hz",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(total_ms / args.steps, 4),
+        "ms_per_frame": round(step_ms / nf, 4),
+        "points_per_s": round(world * sum(npts) * args.steps / (total_ms / 1e3), 1),
+        "hbm_gbs_step": round(step_bytes / (step_ms / 1e3) / 1e9, 2),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (library frame source = reference render_frame, byte-identical)",
+        "config": {"workload": "C2: stair5+stepping stones, 30x640x480 depth frames, 0.01 m, 500^3",
+                   "frames_per_step": nf, "points_per_step": sum(npts), "resolution_m": wl.resolution,
+                   "extent": list(wl.extent), "seed": wl.seed, "l2": "flushed (256 MiB write) between steps",
+                   "parallelism": f"replicas x{world}" if world > 1 else "single"},
+        "gpu_launches": int(launches),
+        "e2e": {"value": round(e2e_value, 3), "unit": "Hz",
+                "h2d_bytes_per_step": int(12 * sum(npts)), "d2h_bytes_per_step": int(d2h_bytes)},
+        "roofline": {"bound": "hbm", "kernel": top, "achieved": round(achieved, 2), "peak": peak,
+                     "unit": "GB/s", "frac": round(achieved / peak, 5), "traffic": None,
+                     "share_of_step": round(top_ms / prof_total, 4),
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650"},
+        "kernels": {k: {"ms_per_step": round(v[0], 4), "calls": int(v[1])}
+                    for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])},
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(wl, args.cpu_frames)
+    return out
+
+
+# ------------------------------------------------------- reference (CPU)
+def ref_lib():
+    path = os.path.join(ROOT, "oracle", "_ref", "libvoxplane_ref.so")
+    kind = "reference"
+    if not os.path.exists(path):
+        raise FileNotFoundError(path)
+    L = C.CDLL(path)
+    L.ref_session_create.restype = C.c_void_p
+    return L, kind
+
+
+def cpu_baseline(wl, nframes):
+    """oracle/_ref (unmodified reference sources) on the host cores: the first
+    `nframes` frames of the stream from an empty map, all host threads."""
+    import numpy as np
+
+    from paper_2510_01592_b200 import native
+    L, kind = ref_lib()
+    cores = os.cpu_count()
+    L.ref_set_threads(cores)
+    p = native.default_params(seed=wl.seed)
+    ext = np.asarray(wl.extent, np.int32)
+    c = np.ascontiguousarray(wl.frames[0].translation, np.float64)
+    s = L.ref_session_create(C.c_double(wl.resolution), ext.ctypes.data_as(C.POINTER(C.c_int32)),
+                             c.ctypes.data_as(C.POINTER(C.c_double)), C.byref(p))
+    total = 0.0
+    for f in wl.frames[:nframes]:
+        ms = C.c_double()
+        npoly = C.c_uint64()
+        pts = np.ascontiguousarray(f.points)
+        R = np.ascontiguousarray(f.rotation, np.float64).reshape(9)
+        t = np.ascontiguousarray(f.translation, np.float64)
+        L.ref_session_step(C.c_void_p(s), pts.ctypes.data_as(C.POINTER(C.c_float)), C.c_uint64(len(pts)),
+                           R.ctypes.data_as(C.POINTER(C.c_double)), t.ctypes.data_as(C.POINTER(C.c_double)),
+                           C.byref(ms), C.byref(npoly))
+        total += ms.value
+    L.ref_session_destroy(C.c_void_p(s))
+    return {"value": round(nframes / (total / 1e3), 4), "unit": "Hz", "cores": cores, "kind": kind,
+            "sample": f"first {nframes} frames of the C2 stream from an empty 500^3 map "
+                      f"({total / 1e3:.1f} s, run_frames body, VOXPLANE threads={cores})"}
+
+
+def run_reference(args):
+    import numpy as np
+
+    from paper_2510_01592_b200 import native
+    wl = load_workload(args.workload)
+    L, kind = ref_lib()
+    cores = os.cpu_count()
+    L.ref_set_threads(cores)
+    p = native.default_params(seed=wl.seed)
+    ext = np.asarray(wl.extent, np.int32)
+    c = np.ascontiguousarray(wl.frames[0].translation, np.float64)
+    s = L.ref_session_create(C.c_double(wl.resolution), ext.ctypes.data_as(C.POINTER(C.c_int32)),
+                             c.ctypes.data_as(C.POINTER(C.c_double)), C.byref(p))
+    # one step = one frame of the stream (cycling), on a persistent map
+    nf = len(wl.frames)
+    times = []
+    for i in range(args.warmup + args.steps):
+        f = wl.frames[i % nf]
+        ms = C.c_double()
+        npoly = C.c_uint64()
+        pts = np.ascontiguousarray(f.points)
+        R = np.ascontiguousarray(f.rotation, np.float64).reshape(9)
+        t = np.ascontiguousarray(f.translation, np.float64)
+        L.ref_session_step(C.c_void_p(s), pts.ctypes.data_as(C.POINTER(C.c_float)), C.c_uint64(len(pts)),
+                           R.ctypes.data_as(C.POINTER(C.c_double)), t.ctypes.data_as(C.POINTER(C.c_double)),
+                           C.byref(ms), C.byref(npoly))
+        if i >= args.warmup:
+            times.append(ms.value)
+    L.ref_session_destroy(C.c_void_p(s))
+    total = sum(times) / 1e3
+    value = len(times) / total
+    return {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "Hz", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * total / len(times), 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (same frames as the B200 arm)",
+        "config": {"workload": "C2: stair5+stepping stones, 30x640x480 depth frames, 0.01 m, 500^3",
+                   "step": "one frame update of the stream on a persistent map"},
+        "cpu_baseline": {"value": round(value, 4), "unit": "Hz", "cores": cores, "kind": kind,
+                         "sample": f"frames {args.warmup}..{args.warmup + args.steps - 1} (mod {nf}) of C2"},
+        "e2e": {"value": round(value, 4), "unit": "Hz", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c2")
+    ap.add_argument("--cpu-frames", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        try:
+            out = run_reference(args)
+        except FileNotFoundError as e:
+            out = {"impl": "reference", "unavailable": f"reference build missing: {e}"}
+        print(json.dumps(out))
+        return 0
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as tdist
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        tdist.init_process_group("nccl")
+        dist = tdist
+    out = run_ours(args, rank, world, dist)
+    if rank == 0:
+        print(json.dumps(out))
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

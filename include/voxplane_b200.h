@@ -227,7 +227,16 @@ int vp_pipeline_create(double resolution, const int32_t extent[3],
                        const double start_center[3], const vp_pipeline_params* p,
                        int device, vp_pipeline** out);
 void vp_pipeline_destroy(vp_pipeline* pl);
+/* Empty the map and re-centre it (the state of a freshly constructed
+   VoxelGrid plus run_frames' last_cell), keeping every device allocation. */
+int vp_pipeline_reset(vp_pipeline* pl, const double start_center[3]);
 vp_grid* vp_pipeline_grid(vp_pipeline* pl);
+/* The cudaStream_t the pipeline's kernels run on (for external event timing). */
+void* vp_pipeline_stream(vp_pipeline* pl);
+/* Counters of the last frame: cleared, freed, touched, discarded, dropped,
+   occupied, V_occ, V_step, clusters, fits, padded members, inliers,
+   polygon vertices, newly occupied, touched groups, overflow flags. */
+int vp_pipeline_counters(vp_pipeline* pl, uint64_t out[16]);
 /* One frame of run_frames: clear_rays, integrate_frame, recenter-if-moved,
    voxel_frame_polygons. out may be NULL (polygons stay on the device). */
 int vp_pipeline_frame(vp_pipeline* pl, const float* xyz, uint64_t n, const double rotation[9],
@@ -245,6 +254,10 @@ int vp_pipeline_frame_trace(vp_pipeline* pl, const float* xyz, uint64_t n,
 
 /* Count of this library's kernel launches since process start (bench evidence). */
 uint64_t vp_kernel_launch_count(void);
+/* Per-kernel CUDA-event timing of every launch (serialising; for profiling
+   runs only). vp_profile_read returns the kernel count and fills up to cap. */
+void vp_profile_enable(int on);
+int vp_profile_read(const char** names, double* ms, uint64_t* calls, int cap);
 
 #ifdef __cplusplus
 }

@@ -251,6 +251,54 @@ int ref_session_frame(void* sp, const float* xyz, uint64_t n, const double R[9],
   }
 }
 
+// One run_frames iteration (pipeline.cpp:199-213) without serialisation:
+// the CPU-baseline step. Returns wall milliseconds in *ms.
+int ref_session_step(void* sp, const float* xyz, uint64_t n, const double R[9], const double t[3],
+                     double* ms, uint64_t* npolys) {
+  auto* s = static_cast<Session*>(sp);
+  try {
+    const SensorFrame frame = make_frame(xyz, n, R, t);
+    StageTimer timer;
+    timer.start();
+    s->grid.clear_rays(frame);
+    s->grid.integrate_frame(frame);
+    const Vec3i cell = global_cell(frame.pose.translation, s->grid.resolution());
+    if (cell != s->last_cell) {
+      s->grid.recenter(frame.pose.translation);
+      s->last_cell = cell;
+    }
+    std::vector<PlanePolygon> polygons;
+    const vp_pipeline_params& P = s->params;
+    if (s->grid.occupied_count() > 0) {  // voxel_frame_polygons (pipeline.cpp:43-85)
+      const SegmentationParams seg = seg_from(P.seg);
+      const RansacParams rp = ransac_from(P.ransac);
+      const std::vector<SurfaceEstimate> est = estimate_normals(s->grid, seg);
+      const SteppablePartition part = classify_steppable(s->grid, est, seg);
+      const Adjacency adj = build_adjacency(part.steppable, seg, s->grid.resolution());
+      const ClusterSet set = label_components(part.steppable, adj);
+      const std::vector<Cluster> clusters = filter_clusters(set, seg.min_cluster_size);
+      const std::vector<ClusterFit> fits = fit_planes(clusters, rp);
+      for (const ClusterFit& fit : fits) {
+        PlaneModel model = fit.model;
+        if (P.refine) {
+          model = refine_plane(fit.inliers, model, rp.up);
+          model.inlier_count = fit.model.inlier_count;
+          model.cluster_label = fit.model.cluster_label;
+        }
+        auto poly = make_polygon(model, fit.inliers);
+        if (poly && poly->area >= P.min_polygon_area) polygons.push_back(std::move(*poly));
+      }
+    }
+    *ms = timer.stop_ms();
+    if (npolys) *npolys = polygons.size();
+    s->frame++;
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return VP_EINVAL;
+  }
+}
+
 // Raw grid state for state-parity tests on small windows: sums (C x 3),
 // counts (C), statuses (C), window (logical) x-major order.
 int ref_session_cells(void* sp, double* sums, uint32_t* counts, uint8_t* status) {

@@ -1,0 +1,958 @@
+// Segmentation kernels: normals + steppability, CCL, cluster gather, RANSAC,
+// refine, polygon. Reference: /root/reference/proj/core/src/{segmentation,
+// jacobi,plane_fit,polygonize}.cpp and pipeline.cpp:43-85.
+#include "vp_kernels.cuh"
+
+namespace vp {
+
+// ---------------------------------------------------------------------------
+// estimate_normals + classify_steppable (segmentation.cpp:19-85), fused.
+// One thread per occupied voxel; the (2r+1)^3 window is probed in the
+// reference's dx -> dy -> dz order through the logical occupancy bitmap, and
+// only occupied neighbours' 32-byte cells are read. The angle predicate
+// acos(d)*kRadToDeg <= theta is evaluated as d >= d*, with d* found on the host
+// by bisection over the host libm acos (exact; A.3).
+// ---------------------------------------------------------------------------
+__global__ void k_normals(GridDesc g, const FrameParams* __restrict__ fp, Counters* ctr, SegDev sp,
+                          SegBufs b, int write_status) {
+  if (blockIdx.x == 0 && threadIdx.x == 0 && ctr->V > b.Vcap) atomicOr(&ctr->overflow, kOverflowOcc);
+  const uint32_t V = min(ctr->V, b.Vcap);
+  const uint32_t* occ = fp->occ_post;
+  const int32_t* off = fp->off_post;
+  const int r = sp.radius;
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x) {
+    const uint32_t flat = b.occ_list[v];
+    const int z = static_cast<int>(flat % static_cast<uint32_t>(g.ez));
+    const uint32_t rr = flat / static_cast<uint32_t>(g.ez);
+    const int y = static_cast<int>(rr % static_cast<uint32_t>(g.ey));
+    const int x = static_cast<int>(rr / static_cast<uint32_t>(g.ey));
+    Cell* own = g.cells + phys_index(g, off, x, y, z);
+    const uint32_t oc = own->count;
+    const double ocd = static_cast<double>(oc);
+    const d3 om = mk3(own->sx / ocd, own->sy / ocd, own->sz / ocd);
+    const uint8_t ostatus = own->status;
+
+    d3 sum = mk3(0.0, 0.0, 0.0);
+    double s00 = 0.0, s01 = 0.0, s02 = 0.0, s11 = 0.0, s12 = 0.0, s22 = 0.0;
+    int n = 0;
+    for (int dx = -r; dx <= r; ++dx) {
+      const int X = x + dx;
+      if (X < 0 || X >= g.ex) continue;
+      for (int dy = -r; dy <= r; ++dy) {
+        const int Y = y + dy;
+        if (Y < 0 || Y >= g.ey) continue;
+        const uint32_t* row = occ + (static_cast<uint64_t>(X) * g.ey + Y) * g.W;
+        for (int dz = -r; dz <= r; ++dz) {
+          const int Z = z + dz;
+          if (Z < 0 || Z >= g.ez) continue;
+          if (!((row[Z >> 5] >> (Z & 31)) & 1u)) continue;
+          const Cell* c = g.cells + phys_index(g, off, X, Y, Z);
+          const double cd = static_cast<double>(c->count);
+          const d3 m = mk3(c->sx / cd, c->sy / cd, c->sz / cd);
+          sum = add3(sum, m);
+          s00 = s00 + m.x * m.x;
+          s01 = s01 + m.y * m.x;
+          s02 = s02 + m.z * m.x;
+          s11 = s11 + m.y * m.y;
+          s12 = s12 + m.z * m.y;
+          s22 = s22 + m.z * m.z;
+          ++n;
+        }
+      }
+    }
+    bool valid = false;
+    d3 nrm = mk3(0.0, 0.0, 0.0);
+    if (n >= 3) {
+      const double dn = static_cast<double>(n);
+      const d3 mean = div3(sum, dn);
+      double cov[3][3];
+      cov[0][0] = s00 / dn - mean.x * mean.x;
+      cov[0][1] = s01 / dn - mean.y * mean.x;
+      cov[0][2] = s02 / dn - mean.z * mean.x;
+      cov[1][0] = s01 / dn - mean.x * mean.y;
+      cov[1][1] = s11 / dn - mean.y * mean.y;
+      cov[1][2] = s12 / dn - mean.z * mean.y;
+      cov[2][0] = s02 / dn - mean.x * mean.z;
+      cov[2][1] = s12 / dn - mean.y * mean.z;
+      cov[2][2] = s22 / dn - mean.z * mean.z;
+      const Eig3 e = jacobi3(cov);
+      if (!(e.val[1] <= 1e-12 + 1e-9 * fabs(e.val[2]))) {
+        nrm = orient_up(normalized3(e.vec[0]), sp.up);
+        valid = true;
+      }
+    }
+    double d = valid ? dot3(nrm, sp.up) : 0.0;
+    d = d < 0.0 ? 0.0 : (1.0 < d ? 1.0 : d);  // std::clamp(d, 0, 1)
+    const bool step = valid && n >= sp.min_neighbors && d >= sp.dstar;
+    if (write_status) own->status = step ? 2 : 1;  // VoxelStatus::Steppable / Occupied
+    b.est_normal[3 * v] = nrm.x;
+    b.est_normal[3 * v + 1] = nrm.y;
+    b.est_normal[3 * v + 2] = nrm.z;
+    b.est_ncount[v] = n;
+    b.est_valid[v] = valid ? 1 : 0;
+    b.own_mean[3 * v] = om.x;
+    b.own_mean[3 * v + 1] = om.y;
+    b.own_mean[3 * v + 2] = om.z;
+    b.own_count[v] = oc;
+    b.own_status[v] = ostatus;
+    b.step_flag[v] = step ? 1 : 0;
+  }
+}
+
+// Steppable list in occupied (lexicographic) order -> ordinals; fills the
+// ordinal map used by the CCL window search.
+__global__ void k_step_emit(GridDesc g, Counters* ctr, SegBufs b, MapDesc m) {
+  const uint32_t V = min(ctr->V, b.Vcap);
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x) {
+    if (!b.step_flag[v]) continue;
+    const uint32_t s = b.step_pos[v];
+    if (s >= b.Scap) {
+      atomicOr(&ctr->overflow, kOverflowStep);
+      continue;
+    }
+    const uint32_t flat = b.occ_list[v];
+    const int z = static_cast<int>(flat % static_cast<uint32_t>(g.ez));
+    const uint32_t rr = flat / static_cast<uint32_t>(g.ez);
+    const int y = static_cast<int>(rr % static_cast<uint32_t>(g.ey));
+    const int x = static_cast<int>(rr / static_cast<uint32_t>(g.ey));
+    b.st_idx[3 * s] = x;
+    b.st_idx[3 * s + 1] = y;
+    b.st_idx[3 * s + 2] = z;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      b.st_mean[3 * s + k] = b.own_mean[3 * v + k];
+      b.st_normal[3 * s + k] = b.est_normal[3 * v + k];
+    }
+    m.map[m.slot(x, y, z)] = static_cast<int32_t>(s);
+  }
+}
+
+// Host-provided steppable list (vp_label_components): fill the map only.
+__global__ void k_map_fill(Counters* ctr, SegBufs b, MapDesc m) {
+  const uint32_t S = min(ctr->S, b.Scap);
+  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < S; s += gridDim.x * blockDim.x)
+    m.map[m.slot(b.st_idx[3 * s], b.st_idx[3 * s + 1], b.st_idx[3 * s + 2])] = static_cast<int32_t>(s);
+}
+
+__global__ void k_ccl_init(Counters* ctr, SegBufs b) {
+  const uint32_t S = min(ctr->S, b.Scap);
+  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < S; s += gridDim.x * blockDim.x) {
+    b.parent[s] = static_cast<int32_t>(s);
+    b.cnt[s] = 0;
+    b.cid[s] = -1;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// build_adjacency + label_components (segmentation.cpp:87-194).
+// The reference materialises every adjacency list and propagates minimum
+// labels until quiet. Here the edge predicate is evaluated on the fly over
+// the forward half of the (2w+1)^3 window (ordinals are lexicographic, so
+// "forward in (x,y,z)" == "j > i"), and each edge is a union-find union that
+// always hooks the larger root under the smaller (atomicCAS), so every root is
+// its component's minimum ordinal: the canonical label, bit-exact.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int uf_find(volatile int32_t* parent, int v) {
+  int par = parent[v];
+  if (par != v) {
+    int next, prev = v;
+    while (par > (next = parent[par])) {
+      parent[prev] = next;  // pointer jumping; parent[x] <= x always holds
+      prev = par;
+      par = next;
+    }
+  }
+  return par;
+}
+
+__device__ __forceinline__ void uf_union(volatile int32_t* parent, int a, int b) {
+  int ra = uf_find(parent, a), rb = uf_find(parent, b);
+  while (ra != rb) {
+    const int lo = ra < rb ? ra : rb;
+    const int hi = ra < rb ? rb : ra;
+    const int ret = atomicCAS(const_cast<int32_t*>(parent) + hi, hi, lo);
+    if (ret == hi) break;
+    if (ra == hi) ra = ret; else rb = ret;
+  }
+}
+
+__global__ void k_ccl_union(Counters* ctr, SegDev sp, SegBufs b, MapDesc m) {
+  const uint32_t S = min(ctr->S, b.Scap);
+  const int w = sp.w;
+  volatile int32_t* parent = b.parent;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < S; i += gridDim.x * blockDim.x) {
+    const int x = b.st_idx[3 * i], y = b.st_idx[3 * i + 1], z = b.st_idx[3 * i + 2];
+    const d3 mi = mk3(b.st_mean[3 * i], b.st_mean[3 * i + 1], b.st_mean[3 * i + 2]);
+    const d3 ni = mk3(b.st_normal[3 * i], b.st_normal[3 * i + 1], b.st_normal[3 * i + 2]);
+    const int xhi = min(x + w, m.lo[0] + m.dims[0] - 1);
+    for (int X = x; X <= xhi; ++X) {
+      const int ylo = (X == x) ? y : max(y - w, m.lo[1]);
+      const int yhi = min(y + w, m.lo[1] + m.dims[1] - 1);
+      for (int Y = ylo; Y <= yhi; ++Y) {
+        const int zlo = (X == x && Y == y) ? z + 1 : max(z - w, m.lo[2]);
+        const int zhi = min(z + w, m.lo[2] + m.dims[2] - 1);
+        if (zlo > zhi) continue;
+        const int32_t* row = m.map + m.slot(X, Y, zlo);
+        for (int Z = zlo; Z <= zhi; ++Z) {
+          const int j = __ldg(row + (Z - zlo));
+          if (j < 0) continue;
+          const d3 mj = mk3(__ldg(b.st_mean + 3 * j), __ldg(b.st_mean + 3 * j + 1),
+                            __ldg(b.st_mean + 3 * j + 2));
+          if (sqn3(sub3(mi, mj)) >= sp.d2_th) continue;
+          const d3 nj = mk3(__ldg(b.st_normal + 3 * j), __ldg(b.st_normal + 3 * j + 1),
+                            __ldg(b.st_normal + 3 * j + 2));
+          if (dot3(ni, nj) <= sp.cos_th) continue;
+          uf_union(parent, static_cast<int>(i), j);
+        }
+      }
+    }
+  }
+}
+
+// build_adjacency materialised (segmentation.cpp:112-130) for the API:
+// pass 1 (cols == nullptr) counts, pass 2 fills rows in ascending ordinal order.
+__global__ void k_adjacency(Counters* ctr, SegDev sp, SegBufs b, MapDesc m, const uint64_t* rows,
+                            uint32_t* counts, int32_t* cols) {
+  const uint32_t S = min(ctr->S, b.Scap);
+  const int w = sp.w;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < S; i += gridDim.x * blockDim.x) {
+    const int x = b.st_idx[3 * i], y = b.st_idx[3 * i + 1], z = b.st_idx[3 * i + 2];
+    const d3 mi = mk3(b.st_mean[3 * i], b.st_mean[3 * i + 1], b.st_mean[3 * i + 2]);
+    const d3 ni = mk3(b.st_normal[3 * i], b.st_normal[3 * i + 1], b.st_normal[3 * i + 2]);
+    uint64_t k = cols ? rows[i] : 0;
+    uint32_t c = 0;
+    for (int X = max(x - w, m.lo[0]); X <= min(x + w, m.lo[0] + m.dims[0] - 1); ++X)
+      for (int Y = max(y - w, m.lo[1]); Y <= min(y + w, m.lo[1] + m.dims[1] - 1); ++Y)
+        for (int Z = max(z - w, m.lo[2]); Z <= min(z + w, m.lo[2] + m.dims[2] - 1); ++Z) {
+          const int j = m.map[m.slot(X, Y, Z)];
+          if (j < 0 || j == static_cast<int>(i)) continue;
+          const d3 mj = mk3(b.st_mean[3 * j], b.st_mean[3 * j + 1], b.st_mean[3 * j + 2]);
+          if (sqn3(sub3(mi, mj)) >= sp.d2_th) continue;
+          const d3 nj = mk3(b.st_normal[3 * j], b.st_normal[3 * j + 1], b.st_normal[3 * j + 2]);
+          if (dot3(ni, nj) <= sp.cos_th) continue;
+          if (cols) cols[k++] = j;
+          ++c;
+        }
+    if (!cols) counts[i] = c;
+  }
+}
+
+// OccupiedVoxel materialisation (voxel_grid.cpp:254-263) for the API.
+__global__ void k_occ_gather(GridDesc g, const FrameParams* __restrict__ fp, Counters* ctr,
+                             SegBufs b) {
+  const uint32_t V = min(ctr->V, b.Vcap);
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x) {
+    const uint32_t flat = b.occ_list[v];
+    const int z = static_cast<int>(flat % static_cast<uint32_t>(g.ez));
+    const uint32_t rr = flat / static_cast<uint32_t>(g.ez);
+    const int y = static_cast<int>(rr % static_cast<uint32_t>(g.ey));
+    const int x = static_cast<int>(rr / static_cast<uint32_t>(g.ey));
+    const Cell* c = g.cells + phys_index(g, fp->off_post, x, y, z);
+    const double cd = static_cast<double>(c->count);
+    b.own_mean[3 * v] = c->sx / cd;
+    b.own_mean[3 * v + 1] = c->sy / cd;
+    b.own_mean[3 * v + 2] = c->sz / cd;
+    b.own_count[v] = c->count;
+    b.own_status[v] = c->status;
+  }
+}
+
+// Final labels (component minimum), member counts per root, map reset.
+__global__ void k_ccl_flatten(Counters* ctr, SegBufs b, MapDesc m) {
+  const uint32_t S = min(ctr->S, b.Scap);
+  volatile int32_t* parent = b.parent;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < S; i += gridDim.x * blockDim.x) {
+    const int r = uf_find(parent, static_cast<int>(i));
+    b.label[i] = r;
+    atomicAdd(&b.cnt[r], 1u);
+    m.map[m.slot(b.st_idx[3 * i], b.st_idx[3 * i + 1], b.st_idx[3 * i + 2])] = -1;
+  }
+}
+
+// filter_clusters (segmentation.cpp:196-201): roots with >= min_cluster members.
+__global__ void k_cluster_flags(Counters* ctr, SegDev sp, SegBufs b) {
+  const uint32_t S = min(ctr->S, b.Scap);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < S; i += gridDim.x * blockDim.x)
+    b.big_flag[i] = (b.label[i] == static_cast<int32_t>(i) &&
+                     static_cast<long long>(b.cnt[i]) >= static_cast<long long>(sp.min_cluster))
+                        ? 1
+                        : 0;
+}
+
+__global__ void k_cluster_assign(Counters* ctr, SegBufs b) {
+  const uint32_t S = min(ctr->S, b.Scap);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < S; i += gridDim.x * blockDim.x) {
+    if (!b.big_flag[i]) continue;
+    const uint32_t k = b.big_pos[i];
+    if (k < static_cast<uint32_t>(kClusterBins)) {
+      b.klabel[k] = static_cast<int32_t>(i);
+      b.cid[i] = static_cast<int32_t>(k);
+    }
+  }
+}
+
+// Single block: sizes and warp-padded member offsets of the K clusters.
+__global__ void k_cluster_setup(Counters* ctr, SegBufs b) {
+  __shared__ uint32_t carry;
+  if (threadIdx.x == 0) {
+    carry = 0;
+    if (ctr->K > static_cast<uint32_t>(kClusterBins)) atomicOr(&ctr->overflow, kOverflowClusters);
+  }
+  __syncthreads();
+  const uint32_t K = min(ctr->K, static_cast<uint32_t>(kClusterBins));
+  for (uint32_t base = 0; base < K; base += blockDim.x) {
+    const uint32_t k = base + threadIdx.x;
+    uint32_t padded = 0;
+    if (k < K) {
+      const uint32_t s = b.cnt[b.klabel[k]];
+      b.ksize[k] = s;
+      padded = (s + 31u) & ~31u;
+    }
+    const uint32_t ex = block_exclusive_u32(padded);
+    const uint32_t c = carry;
+    if (k < K) b.kpoff[k] = c + ex;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = c + ex + padded;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    b.kpoff[K] = carry;
+    ctr->padded_members = carry;
+    if (carry > b.Mcap) atomicOr(&ctr->overflow, kOverflowMembers);
+  }
+}
+
+// Stable counting sort of cluster members by cluster index (ascending
+// ordinal inside each cluster = segmentation.cpp:182-193 grouping order).
+// One warp per chunk of kChunk ordinals.
+__global__ void k_member_hist(Counters* ctr, SegBufs b, uint32_t hstride) {
+  __shared__ uint32_t hist[kClusterBins];
+  const uint32_t S = min(ctr->S, b.Scap);
+  const uint32_t K = min(ctr->K, static_cast<uint32_t>(kClusterBins));
+  const uint32_t nch = (S + kChunk - 1) / kChunk;
+  for (uint32_t c = blockIdx.x; c < nch; c += gridDim.x) {
+    for (uint32_t k = threadIdx.x; k < K; k += blockDim.x) hist[k] = 0;
+    __syncwarp();
+    const uint32_t e1 = min(S, (c + 1) * kChunk);
+    for (uint32_t e = c * kChunk + threadIdx.x; e < e1; e += blockDim.x) {
+      const int32_t k = b.cid[b.label[e]];
+      if (k >= 0) atomicAdd(&hist[k], 1u);
+    }
+    __syncwarp();
+    for (uint32_t k = threadIdx.x; k < K; k += blockDim.x) b.H[k * hstride + c] = hist[k];
+    __syncwarp();
+  }
+}
+
+__global__ void k_member_hscan(Counters* ctr, SegBufs b, uint32_t hstride) {
+  const uint32_t S = min(ctr->S, b.Scap);
+  const uint32_t K = min(ctr->K, static_cast<uint32_t>(kClusterBins));
+  const uint32_t nch = (S + kChunk - 1) / kChunk;
+  const unsigned lane = lane_id();
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarp = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t k = warp; k < K; k += nwarp) {
+    uint32_t run = b.kpoff[k];
+    for (uint32_t c0 = 0; c0 < nch; c0 += 32) {
+      const uint32_t c = c0 + lane;
+      const uint32_t v = c < nch ? b.H[k * hstride + c] : 0u;
+      uint32_t incl = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (static_cast<int>(lane) >= o) incl += t;
+      }
+      if (c < nch) b.H[k * hstride + c] = run + incl - v;
+      run += __shfl_sync(0xffffffffu, incl, 31);
+    }
+  }
+}
+
+__global__ void k_member_scatter(Counters* ctr, SegBufs b, uint32_t hstride) {
+  __shared__ uint32_t run[kClusterBins];
+  const uint32_t S = min(ctr->S, b.Scap);
+  const uint32_t K = min(ctr->K, static_cast<uint32_t>(kClusterBins));
+  const uint32_t nch = (S + kChunk - 1) / kChunk;
+  const bool ok = !(ctr->overflow & kOverflowMembers);
+  const unsigned lane = lane_id();
+  for (uint32_t c = blockIdx.x; c < nch; c += gridDim.x) {
+    for (uint32_t k = lane; k < K; k += 32) run[k] = b.H[k * hstride + c];
+    __syncwarp();
+    const uint32_t e1 = min(S, (c + 1) * kChunk);
+    for (uint32_t e0 = c * kChunk; e0 < e1; e0 += 32) {
+      const uint32_t e = e0 + lane;
+      const int32_t k = e < e1 ? b.cid[b.label[e]] : -1;
+      const unsigned peers = __match_any_sync(0xffffffffu, k);
+      const int leader = __ffs(peers) - 1;
+      const uint32_t base = k >= 0 ? run[k] : 0u;
+      __syncwarp();
+      if (k >= 0 && static_cast<int>(lane) == leader) run[k] = base + __popc(peers);
+      __syncwarp();
+      if (k >= 0 && ok) {
+        const uint32_t pos = base + __popc(peers & lanemask_lt());
+        b.mx[pos] = b.st_mean[3 * e];
+        b.my[pos] = b.st_mean[3 * e + 1];
+        b.mz[pos] = b.st_mean[3 * e + 2];
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// fit_planes (plane_fit.cpp:55-131), cluster-parallel.
+// (a) one thread per (cluster, iteration): CounterRng(seed, label, it) draws,
+//     cross product, area gate, orient_up -> candidate (bit-exact);
+// (b) one warp per 32-member segment: every candidate's predicate over the
+//     segment, __ballot_sync + __popc, integer atomics (order independent);
+// (c) one warp per cluster: argmax, ties to the lowest iteration;
+//     ordered inlier extraction (block scan) in member order.
+// ---------------------------------------------------------------------------
+__global__ void k_ransac_hyp(Counters* ctr, RansacDev rp, SegBufs b) {
+  const uint32_t K = min(ctr->K, static_cast<uint32_t>(kClusterBins));
+  const uint32_t I = static_cast<uint32_t>(rp.iterations);
+  const uint64_t total = static_cast<uint64_t>(K) * I;
+  if (ctr->overflow & kOverflowMembers) return;
+  for (uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
+       t += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t k = static_cast<uint32_t>(t / I), it = static_cast<uint32_t>(t % I);
+    const uint32_t M = b.ksize[k];
+    b.cand_cnt[t] = -1;
+    if (M < 3) continue;
+    CounterRng rng(rp.seed, static_cast<uint64_t>(static_cast<uint32_t>(b.klabel[k])),
+                   static_cast<uint64_t>(it));
+    const uint32_t ia = rng.below(M);
+    uint32_t ib = rng.below(M);
+    while (ib == ia) ib = rng.below(M);
+    uint32_t ic = rng.below(M);
+    while (ic == ia || ic == ib) ic = rng.below(M);
+    const uint32_t o = b.kpoff[k];
+    const d3 p0 = mk3(b.mx[o + ia], b.my[o + ia], b.mz[o + ia]);
+    const d3 e1 = sub3(mk3(b.mx[o + ib], b.my[o + ib], b.mz[o + ib]), p0);
+    const d3 e2 = sub3(mk3(b.mx[o + ic], b.my[o + ic], b.mz[o + ic]), p0);
+    const d3 cr = cross3(e1, e2);
+    const double norm = sqrt(sqn3(cr));
+    if (0.5 * norm <= 1e-10) continue;  // area gate (plane_fit.cpp:38)
+    const d3 n = orient_up(div3(cr, norm), rp.up);
+    b.cand[4 * t] = n.x;
+    b.cand[4 * t + 1] = n.y;
+    b.cand[4 * t + 2] = n.z;
+    b.cand[4 * t + 3] = dot3(n, p0);
+    b.cand_cnt[t] = 0;
+  }
+}
+
+__global__ void k_ransac_count(Counters* ctr, RansacDev rp, SegBufs b) {
+  const uint32_t K = min(ctr->K, static_cast<uint32_t>(kClusterBins));
+  if (K == 0 || (ctr->overflow & kOverflowMembers)) return;
+  const uint32_t nseg = b.kpoff[K] >> 5;
+  const uint32_t I = static_cast<uint32_t>(rp.iterations);
+  const unsigned lane = lane_id();
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarp = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t sg = warp; sg < nseg; sg += nwarp) {
+    const uint32_t start = sg << 5;
+    uint32_t lo = 0, hi = K;  // largest k with kpoff[k] <= start
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (b.kpoff[mid] <= start) lo = mid; else hi = mid;
+    }
+    const uint32_t k = lo;
+    const uint32_t M = b.ksize[k];
+    if (M < 3) continue;
+    const uint32_t j = start + lane - b.kpoff[k];
+    const bool in = j < M;
+    const d3 p = in ? mk3(b.mx[start + lane], b.my[start + lane], b.mz[start + lane])
+                    : mk3(0.0, 0.0, 0.0);
+    const uint64_t cbase = static_cast<uint64_t>(k) * I;
+    for (uint32_t c0 = 0; c0 < I; c0 += 32) {
+      uint32_t mine = 0;
+      const uint32_t cend = min(32u, I - c0);
+      for (uint32_t q = 0; q < cend; ++q) {
+        const uint64_t t = cbase + c0 + q;
+        if (b.cand_cnt[t] < 0) continue;  // degenerate sample: warp-uniform
+        const d3 n = mk3(b.cand[4 * t], b.cand[4 * t + 1], b.cand[4 * t + 2]);
+        const double off = b.cand[4 * t + 3];
+        const bool pred = in && fabs(dot3(n, p) - off) <= rp.eps;
+        const uint32_t c = __popc(__ballot_sync(0xffffffffu, pred));
+        if (lane == q) mine = c;
+      }
+      if (mine) atomicAdd(&b.cand_cnt[cbase + c0 + lane], static_cast<int32_t>(mine));
+    }
+  }
+}
+
+__global__ void k_ransac_select(Counters* ctr, RansacDev rp, SegBufs b) {
+  const uint32_t K = min(ctr->K, static_cast<uint32_t>(kClusterBins));
+  const int I = rp.iterations;
+  const unsigned lane = lane_id();
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarp = (gridDim.x * blockDim.x) >> 5;
+  const bool bad = (ctr->overflow & kOverflowMembers) != 0;
+  for (uint32_t k = warp; k < K; k += nwarp) {
+    if (bad || b.ksize[k] < 3) {
+      if (lane == 0) {
+        b.win_it[k] = -2;  // clusters_skipped_small (plane_fit.cpp:60-61)
+        b.win_cnt[k] = 0;
+      }
+      continue;
+    }
+    int best = -1, bc = -1;
+    for (int it = static_cast<int>(lane); it < I; it += 32) {
+      const int c = b.cand_cnt[static_cast<uint64_t>(k) * I + it];
+      if (c > bc) {  // strict: ties keep the lowest iteration
+        bc = c;
+        best = it;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const int oc = __shfl_down_sync(0xffffffffu, bc, o);
+      const int ob = __shfl_down_sync(0xffffffffu, best, o);
+      if (oc > bc || (oc == bc && ob >= 0 && (best < 0 || ob < best))) {
+        bc = oc;
+        best = ob;
+      }
+    }
+    if (lane == 0) {
+      b.win_it[k] = bc >= 0 ? best : -1;
+      b.win_cnt[k] = bc >= 0 ? bc : 0;
+    }
+  }
+}
+
+// Single block: fit list in cluster order, inlier offsets, FitStats.
+__global__ void k_fit_setup(Counters* ctr, RansacDev rp, SegBufs b) {
+  __shared__ uint32_t carry_f, carry_i, n_skip, n_unfit;
+  if (threadIdx.x == 0) carry_f = carry_i = n_skip = n_unfit = 0;
+  __syncthreads();
+  const uint32_t K = min(ctr->K, static_cast<uint32_t>(kClusterBins));
+  for (uint32_t base = 0; base < K; base += blockDim.x) {
+    const uint32_t k = base + threadIdx.x;
+    int w = -3;
+    if (k < K) w = b.win_it[k];
+    const uint32_t fitted = (w >= 0) ? 1u : 0u;
+    const uint32_t cnt = fitted ? static_cast<uint32_t>(b.win_cnt[k]) : 0u;
+    if (w == -2) atomicAdd(&n_skip, 1u);
+    if (w == -1) atomicAdd(&n_unfit, 1u);
+    const uint32_t ef = block_exclusive_u32(fitted);
+    const uint32_t ei = block_exclusive_u32(cnt);
+    const uint32_t cf = carry_f, ci = carry_i;
+    if (k < K) {
+      b.fid[k] = fitted ? static_cast<int32_t>(cf + ef) : -1;
+      if (fitted) {
+        const uint32_t f = cf + ef;
+        const uint64_t t = static_cast<uint64_t>(k) * rp.iterations + w;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) b.fit_model[4 * f + q] = b.cand[4 * t + q];
+        b.fit_meta[2 * f] = b.win_cnt[k];
+        b.fit_meta[2 * f + 1] = b.klabel[k];
+        b.fit_cluster[f] = k;
+        b.ioff[f] = ci + ei;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) {
+      carry_f = cf + ef + fitted;
+      carry_i = ci + ei + cnt;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    ctr->nfits = carry_f;
+    ctr->inliers = carry_i;
+    b.ioff[carry_f] = carry_i;
+    ctr->skipped = n_skip;
+    ctr->unfit = n_unfit;
+    if (carry_i > b.Icap) atomicOr(&ctr->overflow, kOverflowFits);
+  }
+}
+
+// Ordered inlier extraction (plane_fit.cpp:102-104), one block per fit.
+__global__ void k_ransac_extract(Counters* ctr, RansacDev rp, SegBufs b) {
+  const uint32_t F = ctr->nfits;
+  if (ctr->overflow & (kOverflowFits | kOverflowMembers)) return;
+  __shared__ uint32_t run;
+  for (uint32_t f = blockIdx.x; f < F; f += gridDim.x) {
+    const uint32_t k = b.fit_cluster[f];
+    const uint32_t M = b.ksize[k], o = b.kpoff[k];
+    const d3 n = mk3(b.fit_model[4 * f], b.fit_model[4 * f + 1], b.fit_model[4 * f + 2]);
+    const double off = b.fit_model[4 * f + 3];
+    const uint32_t dst0 = b.ioff[f];
+    if (threadIdx.x == 0) run = 0;
+    __syncthreads();
+    for (uint32_t base = 0; base < M; base += blockDim.x) {
+      const uint32_t j = base + threadIdx.x;
+      d3 p = mk3(0.0, 0.0, 0.0);
+      bool pred = false;
+      if (j < M) {
+        p = mk3(b.mx[o + j], b.my[o + j], b.mz[o + j]);
+        pred = fabs(dot3(n, p) - off) <= rp.eps;
+      }
+      const uint32_t ex = block_exclusive_u32(pred ? 1u : 0u);
+      const uint32_t r0 = run;
+      if (pred) {
+        const uint64_t d = static_cast<uint64_t>(dst0) + r0 + ex;
+        b.inl[3 * d] = p.x;
+        b.inl[3 * d + 1] = p.y;
+        b.inl[3 * d + 2] = p.z;
+      }
+      __syncthreads();
+      if (threadIdx.x == blockDim.x - 1) run = r0 + ex + (pred ? 1u : 0u);
+      __syncthreads();
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// refine_plane (plane_fit.cpp:133-154) via pipeline.cpp:74-78.
+// exact = 1: the reference's sequential sums (one thread, bit-identical).
+// exact = 0: deterministic fixed-shape tree reduction (256 strided partials,
+//            pairwise tree), within the stated 1e-4 rad / 1e-4 m tolerance.
+// ---------------------------------------------------------------------------
+__device__ void refine_finish(double cov[3][3], d3 cen, const double* init, d3 up, double* out) {
+  const Eig3 e = jacobi3(cov);
+  if (e.val[1] <= 1e-12 + 1e-9 * fabs(e.val[2])) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) out[q] = init[q];
+    return;
+  }
+  const d3 n = orient_up(normalized3(e.vec[0]), up);
+  out[0] = n.x;
+  out[1] = n.y;
+  out[2] = n.z;
+  out[3] = dot3(n, cen);
+}
+
+__global__ void k_refine(Counters* ctr, SegBufs b, d3 up, int refine, int exact) {
+  constexpr int B = 256;
+  __shared__ double red[6][B];
+  __shared__ double cen_s[3];
+  const uint32_t F = ctr->nfits;
+  if (ctr->overflow & (kOverflowFits | kOverflowMembers)) return;
+  for (uint32_t f = blockIdx.x; f < F; f += gridDim.x) {
+    const uint64_t o = b.ioff[f];
+    const uint32_t n = b.ioff[f + 1] - b.ioff[f];
+    const double* init = b.fit_model + 4 * f;
+    double* out = b.ref_model + 4 * f;
+    if (!refine || n < 3) {
+      if (threadIdx.x < 4) out[threadIdx.x] = init[threadIdx.x];
+      __syncthreads();
+      continue;
+    }
+    const double* P = b.inl + 3 * o;
+    if (exact) {
+      if (threadIdx.x == 0) {
+        d3 s = mk3(0.0, 0.0, 0.0);
+        for (uint32_t i = 0; i < n; ++i) s = add3(s, mk3(P[3 * i], P[3 * i + 1], P[3 * i + 2]));
+        const d3 cen = div3(s, static_cast<double>(n));
+        double c[3][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
+        for (uint32_t i = 0; i < n; ++i) {
+          const d3 d = sub3(mk3(P[3 * i], P[3 * i + 1], P[3 * i + 2]), cen);
+          const double dv[3] = {d.x, d.y, d.z};
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int q = 0; q < 3; ++q) c[a][q] = c[a][q] + dv[q] * dv[a];
+        }
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+          for (int q = 0; q < 3; ++q) c[a][q] = c[a][q] / static_cast<double>(n);
+        refine_finish(c, cen, init, up, out);
+      }
+      __syncthreads();
+      continue;
+    }
+    // tree: centroid
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    for (uint32_t i = threadIdx.x; i < n; i += B) {
+      s0 += P[3 * i];
+      s1 += P[3 * i + 1];
+      s2 += P[3 * i + 2];
+    }
+    red[0][threadIdx.x] = s0;
+    red[1][threadIdx.x] = s1;
+    red[2][threadIdx.x] = s2;
+    __syncthreads();
+    for (int h = B / 2; h > 0; h >>= 1) {
+      if (static_cast<int>(threadIdx.x) < h)
+        for (int q = 0; q < 3; ++q) red[q][threadIdx.x] = red[q][threadIdx.x] + red[q][threadIdx.x + h];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      const double dn = static_cast<double>(n);
+      cen_s[0] = red[0][0] / dn;
+      cen_s[1] = red[1][0] / dn;
+      cen_s[2] = red[2][0] / dn;
+    }
+    __syncthreads();
+    const d3 cen = mk3(cen_s[0], cen_s[1], cen_s[2]);
+    double c00 = 0.0, c01 = 0.0, c02 = 0.0, c11 = 0.0, c12 = 0.0, c22 = 0.0;
+    for (uint32_t i = threadIdx.x; i < n; i += B) {
+      const d3 d = sub3(mk3(P[3 * i], P[3 * i + 1], P[3 * i + 2]), cen);
+      c00 += d.x * d.x;
+      c01 += d.y * d.x;
+      c02 += d.z * d.x;
+      c11 += d.y * d.y;
+      c12 += d.z * d.y;
+      c22 += d.z * d.z;
+    }
+    __syncthreads();
+    red[0][threadIdx.x] = c00;
+    red[1][threadIdx.x] = c01;
+    red[2][threadIdx.x] = c02;
+    red[3][threadIdx.x] = c11;
+    red[4][threadIdx.x] = c12;
+    red[5][threadIdx.x] = c22;
+    __syncthreads();
+    for (int h = B / 2; h > 0; h >>= 1) {
+      if (static_cast<int>(threadIdx.x) < h)
+        for (int q = 0; q < 6; ++q) red[q][threadIdx.x] = red[q][threadIdx.x] + red[q][threadIdx.x + h];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      const double dn = static_cast<double>(n);
+      double c[3][3];
+      c[0][0] = red[0][0] / dn;
+      c[0][1] = c[1][0] = red[1][0] / dn;
+      c[0][2] = c[2][0] = red[2][0] / dn;
+      c[1][1] = red[3][0] / dn;
+      c[1][2] = c[2][1] = red[4][0] / dn;
+      c[2][2] = red[5][0] / dn;
+      refine_finish(c, cen, init, up, out);
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// make_polygon (polygonize.cpp:166-182): plane_basis, projection, 16-direction
+// hull_filter (extremes with the lexicographic tie-break, inner polygon),
+// lexicographic sort of the survivors (shared-memory bitonic), unique,
+// monotone chain, lift, shoelace. One block per fit.
+// ---------------------------------------------------------------------------
+struct P2 {
+  double x, y;
+};
+__device__ __forceinline__ bool lex_less(P2 a, P2 b) { return a.x < b.x || (a.x == b.x && a.y < b.y); }
+__device__ __forceinline__ double cross2(P2 o, P2 a, P2 b) {
+  return (a.x - o.x) * (b.y - o.y) - (a.y - o.y) * (b.x - o.x);
+}
+
+// Monotone chain over sorted, deduplicated points (polygonize.cpp:116-139);
+// returns hull size (0 if < 3). h has room for 2n points.
+__device__ uint32_t chain_sorted(const P2* pts, uint32_t n, P2* h) {
+  if (n < 3) return 0;
+  uint32_t k = 0;
+  for (uint32_t i = 0; i < n; ++i) {
+    while (k >= 2 && cross2(h[k - 2], h[k - 1], pts[i]) <= 0.0) --k;
+    h[k++] = pts[i];
+  }
+  const uint32_t lower = k + 1;
+  for (uint32_t i = n - 1; i-- > 0;) {
+    while (k >= lower && cross2(h[k - 2], h[k - 1], pts[i]) <= 0.0) --k;
+    h[k++] = pts[i];
+  }
+  const uint32_t m = k - 1;
+  return m < 3 ? 0 : m;
+}
+
+// In-place bitonic sort (lexicographic) of n (power of two) points by a block.
+__device__ void bitonic_sort(P2* a, uint32_t n) {
+  for (uint32_t k = 2; k <= n; k <<= 1) {
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const uint32_t l = i ^ j;
+        if (l > i) {
+          const bool up = (i & k) == 0;
+          const P2 x = a[i], y = a[l];
+          const bool sw = up ? lex_less(y, x) : lex_less(x, y);
+          if (sw) {
+            a[i] = y;
+            a[l] = x;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+__global__ void k_polygon(Counters* ctr, SegBufs b, const double* dirtab, int directions,
+                          double min_area) {
+  extern __shared__ P2 sm_pts[];  // kHullSmem points
+  __shared__ double ex_dot[256];
+  __shared__ P2 ex_pt[256];
+  __shared__ P2 extremes[64];
+  __shared__ P2 inner[130];
+  __shared__ uint32_t n_inner, n_surv, n_uniq;
+  __shared__ double basis[9];
+  const uint32_t F = ctr->nfits;
+  if (ctr->overflow & (kOverflowFits | kOverflowMembers)) return;
+  for (uint32_t f = blockIdx.x; f < F; f += gridDim.x) {
+    const uint64_t o = b.ioff[f];
+    const uint32_t n = b.ioff[f + 1] - b.ioff[f];
+    const double* pl = b.ref_model + 4 * f;
+    double* rd = b.prec_d + 8 * f;
+    int32_t* ri = b.prec_i + 4 * f;
+    if (threadIdx.x == 0) {
+      rd[0] = pl[0];
+      rd[1] = pl[1];
+      rd[2] = pl[2];
+      rd[3] = pl[3];
+      rd[4] = 0.0;
+      ri[0] = b.fit_meta[2 * f];
+      ri[1] = b.fit_meta[2 * f + 1];
+      ri[2] = 0;
+      ri[3] = 0;
+    }
+    if (n < 3) {
+      __syncthreads();
+      continue;
+    }
+    const d3 nrm = mk3(pl[0], pl[1], pl[2]);
+    if (threadIdx.x == 0) {  // plane_basis (polygonize.cpp:21-34)
+      int least = 0;
+      const double an[3] = {fabs(nrm.x), fabs(nrm.y), fabs(nrm.z)};
+      if (an[1] < an[least]) least = 1;
+      if (an[2] < an[least]) least = 2;
+      const d3 axis = mk3(least == 0 ? 1.0 : 0.0, least == 1 ? 1.0 : 0.0, least == 2 ? 1.0 : 0.0);
+      const d3 u = normalized3(sub3(axis, scl3(dot3(nrm, axis), nrm)));
+      const d3 v = cross3(nrm, u);
+      const d3 org = scl3(pl[3], nrm);
+      basis[0] = u.x; basis[1] = u.y; basis[2] = u.z;
+      basis[3] = v.x; basis[4] = v.y; basis[5] = v.z;
+      basis[6] = org.x; basis[7] = org.y; basis[8] = org.z;
+      n_surv = 0;
+    }
+    __syncthreads();
+    const d3 u = mk3(basis[0], basis[1], basis[2]);
+    const d3 v = mk3(basis[3], basis[4], basis[5]);
+    const d3 org = mk3(basis[6], basis[7], basis[8]);
+    const double* Pin = b.inl + 3 * o;
+    P2* proj = reinterpret_cast<P2*>(b.proj) + o;
+    P2* surv = reinterpret_cast<P2*>(b.surv) + 2 * o;  // 2n slots
+    P2* hullg = reinterpret_cast<P2*>(b.hull) + 2 * o;  // 2n slots
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {  // project_to_plane (:36-44)
+      const d3 d = sub3(mk3(Pin[3 * i], Pin[3 * i + 1], Pin[3 * i + 2]), org);
+      proj[i] = P2{dot3(d, u), dot3(d, v)};
+    }
+    __syncthreads();
+    // hull_filter (:50-114)
+    bool filter = n > 3 && directions >= 3;
+    if (filter) {
+      for (int j = 0; j < directions; ++j) {
+        const double dx = dirtab[2 * j], dy = dirtab[2 * j + 1];
+        double best = -CUDART_INF;
+        P2 bp = P2{0.0, 0.0};
+        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+          const P2 q = proj[i];
+          const double dd = q.x * dx + q.y * dy;
+          if (dd > best || (dd == best && lex_less(q, bp))) {
+            best = dd;
+            bp = q;
+          }
+        }
+        ex_dot[threadIdx.x] = best;
+        ex_pt[threadIdx.x] = bp;
+        __syncthreads();
+        for (uint32_t h = blockDim.x / 2; h > 0; h >>= 1) {
+          if (threadIdx.x < h) {
+            const double od = ex_dot[threadIdx.x + h];
+            const P2 op = ex_pt[threadIdx.x + h];
+            if (od > ex_dot[threadIdx.x] || (od == ex_dot[threadIdx.x] && lex_less(op, ex_pt[threadIdx.x]))) {
+              ex_dot[threadIdx.x] = od;
+              ex_pt[threadIdx.x] = op;
+            }
+          }
+          __syncthreads();
+        }
+        if (threadIdx.x == 0) extremes[j] = ex_pt[0];
+        __syncthreads();
+      }
+      if (threadIdx.x == 0) {  // inner = monotone_chain(extremes)
+        P2 e[64];
+        for (int j = 0; j < directions; ++j) e[j] = extremes[j];
+        for (int a = 1; a < directions; ++a) {  // insertion sort (lex)
+          const P2 t = e[a];
+          int c = a;
+          while (c > 0 && lex_less(t, e[c - 1])) {
+            e[c] = e[c - 1];
+            --c;
+          }
+          e[c] = t;
+        }
+        uint32_t m = 0;
+        for (int j = 0; j < directions; ++j)
+          if (m == 0 || !(e[j].x == e[m - 1].x && e[j].y == e[m - 1].y)) e[m++] = e[j];
+        n_inner = chain_sorted(e, m, inner);
+      }
+      __syncthreads();
+      if (n_inner < 3) filter = false;
+    }
+    const uint32_t ni = filter ? n_inner : 0;
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+      const P2 q = proj[i];
+      bool keep = !filter;
+      for (uint32_t e = 0; e < ni && !keep; ++e)
+        if (cross2(inner[e], inner[(e + 1) % ni], q) <= 0.0) keep = true;
+      if (keep) surv[atomicAdd(&n_surv, 1u)] = q;
+    }
+    __syncthreads();
+    const uint32_t ns = n_surv;
+    uint32_t np2 = 1;
+    while (np2 < ns) np2 <<= 1;
+    const bool in_smem = np2 <= static_cast<uint32_t>(kHullSmem);
+    P2* arr = in_smem ? sm_pts : surv;
+    for (uint32_t i = threadIdx.x; i < np2; i += blockDim.x)
+      arr[i] = i < ns ? surv[i] : P2{CUDART_INF, CUDART_INF};
+    __syncthreads();
+    bitonic_sort(arr, np2);
+    if (threadIdx.x == 0) {
+      uint32_t m = 0;  // std::unique
+      for (uint32_t i = 0; i < ns; ++i)
+        if (m == 0 || !(arr[i].x == arr[m - 1].x && arr[i].y == arr[m - 1].y)) arr[m++] = arr[i];
+      n_uniq = chain_sorted(arr, m, hullg);
+    }
+    __syncthreads();
+    const uint32_t m = n_uniq;
+    if (m >= 3) {
+      __shared__ uint32_t voff;
+      __shared__ double area_s;
+      if (threadIdx.x == 0) {
+        double twice = 0.0;  // polygon_area (:146-154)
+        for (uint32_t i = 0; i < m; ++i) {
+          const P2 a = hullg[i], c = hullg[(i + 1) % m];
+          twice += a.x * c.y - c.x * a.y;
+        }
+        area_s = 0.5 * twice;
+        voff = 0xffffffffu;
+        if (area_s >= min_area) {
+          const uint32_t at = atomicAdd(&ctr->pool_used, m);
+          if (at + m <= b.pool_cap) voff = at;
+          else atomicOr(&ctr->overflow, kOverflowPool);
+        }
+        rd[4] = area_s;
+        ri[2] = (voff != 0xffffffffu) ? static_cast<int32_t>(m) : 0;
+        ri[3] = static_cast<int32_t>(voff == 0xffffffffu ? 0 : voff);
+      }
+      __syncthreads();
+      if (voff != 0xffffffffu) {
+        for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {  // lift_from_plane (:46-48)
+          const P2 q = hullg[i];
+          const d3 p3 = add3(add3(org, scl3(q.x, u)), scl3(q.y, v));
+          double* dst = b.pool + 5 * (static_cast<uint64_t>(voff) + i);
+          dst[0] = q.x;
+          dst[1] = q.y;
+          dst[2] = p3.x;
+          dst[3] = p3.y;
+          dst[4] = p3.z;
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace vp

@@ -1,0 +1,1668 @@
+// Host runtime and C ABI (include/voxplane_b200.h).
+//
+// One vp_grid owns its device buffers and one CUDA stream. A frame update
+// (clear -> integrate -> recenter -> segment) is a fixed sequence of kernels
+// whose data-dependent sizes live in device counters, so the host never waits
+// mid-frame; it synchronises once to read the result records.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstddef>
+#include <cstring>
+#include <limits>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "voxplane_b200.h"
+#include "voxplane_trace.h"
+#include "vp_kernels.cuh"
+
+using namespace vp;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
+
+constexpr double kRadToDeg = 57.295779513082320876798;
+constexpr double kDegToRad = 0.017453292519943295769237;
+constexpr double kPi = 3.14159265358979323846;  // == glibc M_PI
+constexpr int kThreads = 256;
+
+struct VpFail {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw VpFail{code, msg}; }
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(VP_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// Optional per-kernel profiling (vp_profile_enable): every launch is bracketed
+// by CUDA events on its stream and the elapsed time is accumulated per kernel.
+struct ProfEntry {
+  std::string name;
+  double ms = 0.0;
+  uint64_t calls = 0;
+};
+std::vector<ProfEntry> g_prof;
+bool g_prof_on = false;
+cudaEvent_t g_prof_ev[2] = {nullptr, nullptr};
+
+void prof_begin(cudaStream_t s) {
+  if (!g_prof_ev[0]) {
+    cudaEventCreate(&g_prof_ev[0]);
+    cudaEventCreate(&g_prof_ev[1]);
+  }
+  cudaEventRecord(g_prof_ev[0], s);
+}
+void prof_end(cudaStream_t s, const char* name) {
+  cudaEventRecord(g_prof_ev[1], s);
+  cudaEventSynchronize(g_prof_ev[1]);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, g_prof_ev[0], g_prof_ev[1]);
+  for (auto& e : g_prof)
+    if (e.name == name) {
+      e.ms += ms;
+      ++e.calls;
+      return;
+    }
+  g_prof.push_back(ProfEntry{name, ms, 1});
+}
+
+#define LAUNCH(kernel, grid, block, smem, stream, ...)                         \
+  do {                                                                         \
+    if (g_prof_on) prof_begin(stream);                                         \
+    kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);               \
+    ck(cudaGetLastError(), #kernel);                                           \
+    g_launches.fetch_add(1, std::memory_order_relaxed);                        \
+    if (g_prof_on) prof_end(stream, #kernel);                                  \
+  } while (0)
+
+template <typename T>
+T* dalloc(size_t n) {
+  if (n == 0) n = 1;
+  void* p = nullptr;
+  const cudaError_t e = cudaMalloc(&p, n * sizeof(T));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    fail(VP_ENOMEM, "cudaMalloc " + std::to_string(n * sizeof(T)) + " bytes: " + cudaGetErrorString(e));
+  }
+  return static_cast<T*>(p);
+}
+
+template <typename T>
+void dfree(T*& p) {
+  if (p) cudaFree(p);
+  p = nullptr;
+}
+
+int grid_for(uint64_t n, int cap = 148 * 16) {
+  const uint64_t b = (n + kThreads - 1) / kThreads;
+  return static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(b, static_cast<uint64_t>(cap))));
+}
+constexpr int kWide = 148 * 8;  // grid-stride width for device-sized loops
+
+// voxel_grid.cpp:13-17 (r^T r in the shim's product order; tolerance 1e-6)
+bool is_valid_rotation(const double* R) {
+  double t[3][3], p[3][3];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) t[i][j] = R[3 * j + i];
+  for (int j = 0; j < 3; ++j)
+    for (int i = 0; i < 3; ++i)
+      p[i][j] = i < 2 ? (t[i][0] * R[j] + t[i][1] * R[3 + j]) + t[i][2] * R[6 + j]
+                      : t[i][0] * R[j] + (t[i][1] * R[3 + j] + t[i][2] * R[6 + j]);
+  double mx = 0.0;
+  bool first = true;
+  for (int j = 0; j < 3; ++j)
+    for (int i = 0; i < 3; ++i) {
+      double v = p[i][j] - (i == j ? 1.0 : 0.0);
+      v = v < 0.0 ? -v : v;
+      if (first || mx < v) mx = v;
+      first = false;
+    }
+  if (mx > 1e-6) return false;
+  auto m = [&](int r, int c) { return R[3 * r + c]; };
+  auto h = [&](int a, int b, int c) { return m(0, a) * (m(1, b) * m(2, c) - m(1, c) * m(2, b)); };
+  const double det = h(0, 1, 2) - h(1, 0, 2) + h(2, 0, 1);
+  return std::abs(det - 1.0) <= 1e-6;
+}
+
+// Smallest d in [0,1] with acos(d)*kRadToDeg <= theta (segmentation.cpp:62-63,
+// 74-75), by bisection over the IEEE bit patterns with the host libm.
+double angle_threshold(double theta) {
+  auto ok = [&](double d) { return std::acos(d) * kRadToDeg <= theta; };
+  if (!ok(1.0)) return std::numeric_limits<double>::infinity();
+  if (ok(0.0)) return 0.0;
+  uint64_t lo, hi;
+  double z = 0.0, o = 1.0;
+  std::memcpy(&lo, &z, 8);
+  std::memcpy(&hi, &o, 8);
+  while (hi - lo > 1) {
+    const uint64_t mid = lo + (hi - lo) / 2;
+    double d;
+    std::memcpy(&d, &mid, 8);
+    if (ok(d)) hi = mid; else lo = mid;
+  }
+  double d;
+  std::memcpy(&d, &hi, 8);
+  return d;
+}
+
+SegDev make_segdev(const vp_seg_params& p, double res) {
+  SegDev s;
+  s.radius = p.neighbor_radius;
+  s.min_neighbors = p.min_neighbors;
+  s.dstar = angle_threshold(p.max_angle_deg);
+  s.up = d3{p.up[0], p.up[1], p.up[2]};
+  s.w = std::max(1, static_cast<int>(std::ceil(p.distance_th / res)));
+  s.d2_th = p.distance_th * p.distance_th;
+  s.cos_th = std::cos(p.adjacency_angle_deg * kDegToRad);
+  s.min_cluster = p.min_cluster_size;
+  return s;
+}
+
+RansacDev make_ransacdev(const vp_ransac_params& r) {
+  RansacDev d;
+  d.iterations = r.iterations;
+  d.eps = r.inlier_eps;
+  d.seed = r.seed;
+  d.up = d3{r.up[0], r.up[1], r.up[2]};
+  return d;
+}
+
+void check_device(int device) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    fail(VP_ENODEV, "no CUDA device visible");
+  }
+  if (device < 0 || device >= n) fail(VP_ENODEV, "device index out of range");
+  cudaDeviceProp prop;
+  ck(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+  if (prop.major != 10) fail(VP_ENODEV, std::string("sm_100a build needs a B200-class device, got ") + prop.name);
+  ck(cudaSetDevice(device), "cudaSetDevice");
+}
+
+// Segmentation scratch sized by capacities; grows on overflow.
+struct Seg {
+  SegBufs b{};
+  uint32_t* bsum = nullptr;  // scan block sums
+  uint32_t bsum_cap = 0;
+  double* dirtab = nullptr;
+  int dir_n = -1;
+  uint32_t hstride = 0;
+
+  void release() {
+    void* ptrs[] = {b.occ_list, b.est_normal, b.est_ncount, b.est_valid, b.own_mean, b.own_count,
+                    b.own_status, b.step_flag, b.step_pos, b.st_idx, b.st_mean, b.st_normal,
+                    b.parent, b.label, b.cnt, b.cid, b.big_flag, b.big_pos, b.klabel, b.ksize,
+                    b.kpoff, b.H, b.mx, b.my, b.mz, b.cand, b.cand_cnt, b.win_it, b.win_cnt,
+                    b.fid, b.fit_cluster, b.ioff, b.fit_model, b.fit_meta, b.ref_model, b.inl,
+                    b.proj, b.surv, b.hull, b.prec_d, b.prec_i, b.pool, bsum, dirtab};
+    for (void* p : ptrs)
+      if (p) cudaFree(p);
+    b = SegBufs{};
+    bsum = nullptr;
+    dirtab = nullptr;
+    dir_n = -1;
+  }
+
+  void ensure(uint32_t vcap, uint32_t scap, uint32_t icap, int iterations, uint64_t nwords) {
+    const uint32_t mcap = scap + 32u * kClusterBins;
+    const bool need = !b.occ_list || vcap > b.Vcap || scap > b.Scap || icap > b.Icap ||
+                      static_cast<uint64_t>(iterations) * kClusterBins > cand_cap;
+    const uint64_t need_bsum = std::max<uint64_t>({(nwords + kScanPerBlock - 1) / kScanPerBlock,
+                                                   (vcap + kScanPerBlock - 1) / kScanPerBlock,
+                                                   (scap + kScanPerBlock - 1) / kScanPerBlock}) + 1;
+    if (need) {
+      release();
+      b.Vcap = vcap;
+      b.Scap = scap;
+      b.Mcap = mcap;
+      b.Icap = icap;
+      cand_cap = static_cast<uint64_t>(std::max(iterations, 1)) * kClusterBins;
+      b.occ_list = dalloc<uint32_t>(vcap);
+      b.est_normal = dalloc<double>(3ull * vcap);
+      b.est_ncount = dalloc<int32_t>(vcap);
+      b.est_valid = dalloc<uint8_t>(vcap);
+      b.own_mean = dalloc<double>(3ull * vcap);
+      b.own_count = dalloc<uint32_t>(vcap);
+      b.own_status = dalloc<uint8_t>(vcap);
+      b.step_flag = dalloc<uint8_t>(vcap);
+      b.step_pos = dalloc<uint32_t>(vcap);
+      b.st_idx = dalloc<int32_t>(3ull * scap);
+      b.st_mean = dalloc<double>(3ull * scap);
+      b.st_normal = dalloc<double>(3ull * scap);
+      b.parent = dalloc<int32_t>(scap);
+      b.label = dalloc<int32_t>(scap);
+      b.cnt = dalloc<uint32_t>(scap);
+      b.cid = dalloc<int32_t>(scap);
+      b.big_flag = dalloc<uint8_t>(scap);
+      b.big_pos = dalloc<uint32_t>(scap);
+      b.klabel = dalloc<int32_t>(kClusterBins);
+      b.ksize = dalloc<uint32_t>(kClusterBins);
+      b.kpoff = dalloc<uint32_t>(kClusterBins + 1);
+      hstride = (scap + kChunk - 1) / kChunk;
+      b.H = dalloc<uint32_t>(static_cast<size_t>(kClusterBins) * hstride);
+      b.mx = dalloc<double>(mcap);
+      b.my = dalloc<double>(mcap);
+      b.mz = dalloc<double>(mcap);
+      b.cand = dalloc<double>(4 * cand_cap);
+      b.cand_cnt = dalloc<int32_t>(cand_cap);
+      b.win_it = dalloc<int32_t>(kClusterBins);
+      b.win_cnt = dalloc<int32_t>(kClusterBins);
+      b.fid = dalloc<int32_t>(kClusterBins);
+      b.fit_cluster = dalloc<uint32_t>(kClusterBins);
+      b.ioff = dalloc<uint32_t>(kClusterBins + 1);
+      b.fit_model = dalloc<double>(4 * kClusterBins);
+      b.fit_meta = dalloc<int32_t>(2 * kClusterBins);
+      b.ref_model = dalloc<double>(4 * kClusterBins);
+      b.inl = dalloc<double>(3ull * icap);
+      b.proj = dalloc<double>(2ull * icap);
+      b.surv = dalloc<double>(4ull * icap);
+      b.hull = dalloc<double>(4ull * icap);
+      b.prec_d = dalloc<double>(8 * kClusterBins);
+      b.prec_i = dalloc<int32_t>(4 * kClusterBins);
+      b.pool_cap = icap;
+      b.pool = dalloc<double>(5ull * icap);
+      bsum_cap = static_cast<uint32_t>(need_bsum);
+      bsum = dalloc<uint32_t>(2ull * need_bsum);
+    } else if (need_bsum > bsum_cap) {
+      dfree(bsum);
+      bsum_cap = static_cast<uint32_t>(need_bsum);
+      bsum = dalloc<uint32_t>(2ull * need_bsum);
+    }
+  }
+
+  void ensure_dirs(int n, cudaStream_t s) {
+    if (n == dir_n) return;
+    if (n > 64) fail(VP_EINVAL, "make_polygon: at most 64 filter directions supported");
+    std::vector<double> t(2 * 64, 0.0);
+    for (int j = 0; j < n; ++j) {  // polygonize.cpp:59-63
+      const double a = 2.0 * kPi * j / n;
+      t[2 * j] = std::cos(a);
+      t[2 * j + 1] = std::sin(a);
+    }
+    if (!dirtab) dirtab = dalloc<double>(128);
+    ck(cudaMemcpyAsync(dirtab, t.data(), 128 * sizeof(double), cudaMemcpyHostToDevice, s), "dirtab");
+    ck(cudaStreamSynchronize(s), "dirtab sync");
+    dir_n = n;
+  }
+
+  uint64_t cand_cap = 0;
+};
+
+// Host image of the per-fit records written by k_polygon.
+struct HostPolys {
+  std::vector<vp_polygon> polys;
+  std::vector<double> verts;  // 5 per vertex (u v x y z)
+};
+
+}  // namespace
+
+// ===========================================================================
+struct vp_grid {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  GridDesc gd{};
+  double origin[3];
+  int32_t ext[3];
+  int32_t off[3] = {0, 0, 0};
+  uint32_t* occ[2] = {nullptr, nullptr};
+  int cur = 0;
+  Counters* ctr = nullptr;
+  Counters* h_ctr = nullptr;  // pinned
+  FrameParams* d_fp = nullptr;
+  FrameParams* h_fp = nullptr;  // pinned
+  uint64_t host_occupied = 0;
+  // integrate scratch
+  uint64_t pcap = 0;
+  float* d_pts = nullptr;
+  uint32_t* hkey = nullptr;
+  uint32_t* hcnt = nullptr;
+  uint32_t* hoff = nullptr;
+  uint32_t hmask = 0;
+  uint32_t* groups = nullptr;
+  uint32_t* pslot = nullptr;
+  uint32_t* prank = nullptr;
+  uint32_t* sorted = nullptr;
+  Seg seg;
+  cudaEvent_t ev[8];
+  // trace scratch for the occupied-list view
+  bool status_written_this_frame = false;
+
+  ~vp_grid() {
+    if (stream) cudaStreamSynchronize(stream);
+    seg.release();
+    for (auto* p : {occ[0], occ[1]}) if (p) cudaFree(p);
+    if (gd.cells) cudaFree(gd.cells);
+    if (gd.clr) cudaFree(gd.clr);
+    if (gd.ordmap) cudaFree(gd.ordmap);
+    if (ctr) cudaFree(ctr);
+    if (d_fp) cudaFree(d_fp);
+    if (h_ctr) cudaFreeHost(h_ctr);
+    if (h_fp) cudaFreeHost(h_fp);
+    for (void* p : {(void*)d_pts, (void*)hkey, (void*)hcnt, (void*)hoff, (void*)groups,
+                    (void*)pslot, (void*)prank, (void*)sorted})
+      if (p) cudaFree(p);
+    for (auto& e : ev) if (e) cudaEventDestroy(e);
+    if (stream) cudaStreamDestroy(stream);
+  }
+
+  // ------------------------------------------------------------ set-up
+  void init(double res, const int32_t* e, const double* c, int dev) {
+    if (!(res > 0.0) || e[0] <= 0 || e[1] <= 0 || e[2] <= 0)  // voxel_grid.cpp:21-22
+      fail(VP_EINVAL, "VoxelGrid: resolution and extents must be positive");
+    const uint64_t C = static_cast<uint64_t>(e[0]) * e[1] * e[2];
+    if (C >= (1ull << 32)) fail(VP_EINVAL, "VoxelGrid: more than 2^32 cells per grid (use slabs)");
+    check_device(dev);
+    device = dev;
+    for (int k = 0; k < 3; ++k) {
+      ext[k] = e[k];
+      origin[k] = c[k] - static_cast<double>(e[k]) * (0.5 * res);  // voxel_grid.cpp:23
+    }
+    ck(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "stream");
+    for (auto& x : ev) ck(cudaEventCreate(&x), "event");
+    gd.ex = e[0];
+    gd.ey = e[1];
+    gd.ez = e[2];
+    gd.W = (e[2] + 31) / 32;
+    gd.res = res;
+    gd.ncells = C;
+    gd.nwords = static_cast<uint64_t>(e[0]) * e[1] * gd.W;
+    gd.cells = dalloc<Cell>(C);
+    gd.clr = dalloc<uint32_t>(gd.nwords);
+    gd.ordmap = dalloc<int32_t>(C);
+    occ[0] = dalloc<uint32_t>(gd.nwords);
+    occ[1] = dalloc<uint32_t>(gd.nwords);
+    ck(cudaMemsetAsync(gd.cells, 0, C * sizeof(Cell), stream), "memset cells");
+    ck(cudaMemsetAsync(gd.clr, 0, gd.nwords * 4, stream), "memset clr");
+    ck(cudaMemsetAsync(occ[0], 0, gd.nwords * 4, stream), "memset occ");
+    ck(cudaMemsetAsync(occ[1], 0, gd.nwords * 4, stream), "memset occ");
+    ck(cudaMemsetAsync(gd.ordmap, 0xff, C * 4, stream), "memset ordmap");
+    ctr = dalloc<Counters>(1);
+    ck(cudaMemsetAsync(ctr, 0, sizeof(Counters), stream), "memset ctr");
+    d_fp = dalloc<FrameParams>(1);
+    ck(cudaMallocHost(&h_ctr, sizeof(Counters)), "pinned");
+    ck(cudaMallocHost(&h_fp, sizeof(FrameParams)), "pinned");
+    std::memset(h_fp, 0, sizeof(FrameParams));
+    const uint32_t vcap = static_cast<uint32_t>(std::min<uint64_t>(C, 1u << 22));
+    seg.ensure(vcap, vcap, vcap, 100, gd.nwords);
+    ck(cudaFuncSetAttribute(k_polygon, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            kHullSmem * 16), "smem attr");
+    ck(cudaStreamSynchronize(stream), "init sync");
+  }
+
+  // Back to an empty window centred on c (VoxelGrid constructor state): zero
+  // the occupied cells (bitmap-guided, O(occupied)) and the bitmaps.
+  void reset(const double* c) {
+    fill_static_params();
+    h_fp->n = 0;
+    // drop everything: a shift larger than the window zeroes every occupied cell
+    for (int k = 0; k < 3; ++k) h_fp->shift[k] = ext[k] + 1;
+    h_fp->do_shift = 1;
+    h_fp->occ_post = occ[cur ^ 1];
+    upload_params();
+    reset_frame_counters();
+    launch_recenter();
+    ck(cudaMemsetAsync(occ[0], 0, gd.nwords * 4, stream), "occ");
+    ck(cudaMemsetAsync(occ[1], 0, gd.nwords * 4, stream), "occ");
+    ck(cudaMemsetAsync(ctr, 0, sizeof(Counters), stream), "ctr");
+    ck(cudaStreamSynchronize(stream), "reset sync");
+    cur = 0;
+    host_occupied = 0;
+    for (int k = 0; k < 3; ++k) {
+      off[k] = 0;
+      origin[k] = c[k] - static_cast<double>(ext[k]) * (0.5 * gd.res);
+    }
+  }
+
+  void ensure_points(uint64_t n) {
+    if (n <= pcap && d_pts) return;
+    uint64_t cap = std::max<uint64_t>(n, 1 << 16);
+    cap = std::max<uint64_t>(cap, pcap * 2);
+    for (void* p : {(void*)d_pts, (void*)hkey, (void*)hcnt, (void*)hoff, (void*)groups,
+                    (void*)pslot, (void*)prank, (void*)sorted})
+      if (p) cudaFree(p);
+    uint64_t hs = 1;
+    while (hs < 2 * cap) hs <<= 1;
+    d_pts = dalloc<float>(3 * cap);
+    hkey = dalloc<uint32_t>(hs);
+    hcnt = dalloc<uint32_t>(hs);
+    hoff = dalloc<uint32_t>(hs);
+    groups = dalloc<uint32_t>(cap);
+    pslot = dalloc<uint32_t>(cap);
+    prank = dalloc<uint32_t>(cap);
+    sorted = dalloc<uint32_t>(cap);
+    ck(cudaMemsetAsync(hkey, 0xff, hs * 4, stream), "hkey");
+    ck(cudaMemsetAsync(hcnt, 0, hs * 4, stream), "hcnt");
+    hmask = static_cast<uint32_t>(hs - 1);
+    pcap = cap;
+  }
+
+  // ------------------------------------------------------------ frame params
+  void set_pose(const double* R, const double* t) {
+    std::memcpy(h_fp->R, R, 9 * sizeof(double));
+    std::memcpy(h_fp->t, t, 3 * sizeof(double));
+  }
+  void fill_static_params() {
+    for (int k = 0; k < 3; ++k) {
+      h_fp->origin_pre[k] = h_fp->origin_post[k] = origin[k];
+      h_fp->off_pre[k] = h_fp->off_post[k] = off[k];
+      h_fp->shift[k] = 0;
+    }
+    h_fp->do_shift = 0;
+    h_fp->occ_pre = h_fp->occ_post = occ[cur];
+  }
+  // Host part of recenter (voxel_grid.cpp:217-223) -> post-shift state.
+  bool plan_recenter(const double* c, vp_shift_stats* st) {
+    const double res = gd.res;
+    int32_t s[3];
+    for (int k = 0; k < 3; ++k) {
+      const double wc = origin[k] + static_cast<double>(ext[k]) * (0.5 * res);  // world_center
+      s[k] = static_cast<int32_t>(std::llround((c[k] - wc) / res));
+    }
+    if (st) {
+      std::memcpy(st->shift, s, sizeof s);
+      st->voxels_dropped = 0;
+    }
+    if (s[0] == 0 && s[1] == 0 && s[2] == 0) return false;
+    for (int k = 0; k < 3; ++k) {
+      origin[k] += static_cast<double>(s[k]) * res;
+      int64_t o = (static_cast<int64_t>(off[k]) + s[k]) % ext[k];
+      if (o < 0) o += ext[k];
+      off[k] = static_cast<int32_t>(o);
+      h_fp->origin_post[k] = origin[k];
+      h_fp->off_post[k] = off[k];
+      h_fp->shift[k] = s[k];
+    }
+    h_fp->do_shift = 1;
+    h_fp->occ_post = occ[cur ^ 1];
+    cur ^= 1;
+    return true;
+  }
+  void upload_params() {
+    ck(cudaMemcpyAsync(d_fp, h_fp, sizeof(FrameParams), cudaMemcpyHostToDevice, stream), "params");
+  }
+  void reset_frame_counters() {
+    ck(cudaMemsetAsync(reinterpret_cast<char*>(ctr) + sizeof(unsigned long long), 0,
+                       sizeof(Counters) - sizeof(unsigned long long), stream),
+       "ctr reset");
+  }
+  void read_counters() {
+    ck(cudaMemcpyAsync(h_ctr, ctr, sizeof(Counters), cudaMemcpyDeviceToHost, stream), "ctr d2h");
+    ck(cudaStreamSynchronize(stream), "sync");
+    host_occupied = h_ctr->occupied;
+  }
+
+  // ------------------------------------------------------------ kernels
+  void launch_clear(uint64_t n) {
+    if (n == 0) return;
+    LAUNCH(k_clear_walk, grid_for(n, 148 * 32), kThreads, 0, stream, gd, d_fp);
+    LAUNCH(k_clear_apply, grid_for(gd.nwords), kThreads, 0, stream, gd, d_fp, ctr);
+  }
+  void launch_integrate(uint64_t n) {
+    if (n == 0) return;
+    const int gp = grid_for(n);
+    LAUNCH(k_integrate_hash, gp, kThreads, 0, stream, gd, d_fp, ctr, hkey, hcnt, hmask, groups,
+           pslot, prank);
+    LAUNCH(k_integrate_offsets, gp, kThreads, 0, stream, ctr, groups, hcnt, hoff);
+    LAUNCH(k_integrate_scatter, gp, kThreads, 0, stream, d_fp, pslot, prank, hoff, sorted);
+    LAUNCH(k_integrate_fold, gp, kThreads, 0, stream, gd, d_fp, ctr, groups, hkey, hcnt, hoff,
+           sorted);
+  }
+  void launch_recenter() {
+    LAUNCH(k_recenter, grid_for(gd.nwords), kThreads, 0, stream, gd, d_fp, ctr);
+  }
+  void launch_finalize() { LAUNCH(k_map_finalize, 1, 1, 0, stream, ctr); }
+
+  // Occupied scan of the post-recenter bitmap into seg.b.occ_list; ctr->V.
+  void launch_occupied_scan() {
+    const uint32_t nb = static_cast<uint32_t>((gd.nwords + kScanPerBlock - 1) / kScanPerBlock);
+    uint32_t* occ_now = h_fp->occ_post;
+    LAUNCH(k_bitmap_count, nb, kScanThreads, 0, stream, occ_now, gd.nwords, seg.bsum);
+    LAUNCH(k_scan_exclusive, 1, 1024, 0, stream, seg.bsum, nb, nullptr, &ctr->V, nullptr);
+    LAUNCH(k_bitmap_emit, nb, kScanThreads, 0, stream, occ_now, gd.nwords, gd.W, gd.ez, seg.bsum,
+           seg.b.occ_list, seg.b.Vcap);
+  }
+
+  // flags[0..*n) -> positions, total into *total
+  void launch_flag_scan(const uint8_t* flags, const uint32_t* n_ptr, uint32_t cap, uint32_t* pos,
+                        uint32_t* total) {
+    const uint32_t nb = (cap + kScanPerBlock - 1) / kScanPerBlock;
+    uint32_t* bs = seg.bsum + seg.bsum_cap;
+    LAUNCH(k_flags_count, nb, kScanThreads, 0, stream, flags, n_ptr, cap, bs);
+    LAUNCH(k_scan_exclusive, 1, 1024, 0, stream, bs, nb, nullptr, total, nullptr);
+    LAUNCH(k_flags_positions, nb, kScanThreads, 0, stream, flags, n_ptr, cap, bs, pos);
+  }
+
+  MapDesc grid_map() {
+    MapDesc m;
+    m.map = gd.ordmap;
+    m.lo[0] = m.lo[1] = m.lo[2] = 0;
+    m.dims[0] = ext[0];
+    m.dims[1] = ext[1];
+    m.dims[2] = ext[2];
+    return m;
+  }
+
+  // normals + classify + steppable list (+ ordinal map)
+  void launch_classify(const SegDev& sd, int write_status) {
+    LAUNCH(k_normals, kWide, kThreads, 0, stream, gd, d_fp, ctr, sd, seg.b, write_status);
+    launch_flag_scan(seg.b.step_flag, &ctr->V, seg.b.Vcap, seg.b.step_pos, &ctr->S);
+  }
+  void launch_step_emit(const MapDesc& m) {
+    LAUNCH(k_step_emit, kWide, kThreads, 0, stream, gd, ctr, seg.b, m);
+  }
+  // union-find over the steppable list in seg.b (ctr->S set)
+  void launch_ccl(const SegDev& sd, const MapDesc& m) {
+    LAUNCH(k_ccl_init, kWide, kThreads, 0, stream, ctr, seg.b);
+    LAUNCH(k_ccl_union, kWide, kThreads, 0, stream, ctr, sd, seg.b, m);
+    LAUNCH(k_ccl_flatten, kWide, kThreads, 0, stream, ctr, seg.b, m);
+  }
+  void launch_clusters(const SegDev& sd) {
+    LAUNCH(k_cluster_flags, kWide, kThreads, 0, stream, ctr, sd, seg.b);
+    launch_flag_scan(seg.b.big_flag, &ctr->S, seg.b.Scap, seg.b.big_pos, &ctr->K);
+    LAUNCH(k_cluster_assign, kWide, kThreads, 0, stream, ctr, seg.b);
+    LAUNCH(k_cluster_setup, 1, 1024, 0, stream, ctr, seg.b);
+    const int nch = static_cast<int>(seg.hstride);
+    LAUNCH(k_member_hist, nch, 32, 0, stream, ctr, seg.b, seg.hstride);
+    LAUNCH(k_member_hscan, kWide, kThreads, 0, stream, ctr, seg.b, seg.hstride);
+    LAUNCH(k_member_scatter, nch, 32, 0, stream, ctr, seg.b, seg.hstride);
+  }
+  void launch_ransac(const RansacDev& rd) {
+    LAUNCH(k_ransac_hyp, kWide, kThreads, 0, stream, ctr, rd, seg.b);
+    LAUNCH(k_ransac_count, kWide, kThreads, 0, stream, ctr, rd, seg.b);
+    LAUNCH(k_ransac_select, kWide, kThreads, 0, stream, ctr, rd, seg.b);
+    LAUNCH(k_fit_setup, 1, 1024, 0, stream, ctr, rd, seg.b);
+    LAUNCH(k_ransac_extract, 148 * 2, kThreads, 0, stream, ctr, rd, seg.b);
+  }
+  void launch_refine(const double* up, int refine, int exact) {
+    LAUNCH(k_refine, 148 * 2, 256, 0, stream, ctr, seg.b, d3{up[0], up[1], up[2]}, refine, exact);
+  }
+  void launch_polygon(int dirs, double min_area) {
+    seg.ensure_dirs(dirs, stream);
+    LAUNCH(k_polygon, 148 * 2, 256, kHullSmem * 16, stream, ctr, seg.b, seg.dirtab, dirs, min_area);
+  }
+
+  // The fused segment(): voxel_frame_polygons (pipeline.cpp:43-85) on device.
+  void launch_segment(const vp_pipeline_params& p, bool timing) {
+    const SegDev sd = make_segdev(p.seg, gd.res);
+    const RansacDev rd = make_ransacdev(p.ransac);
+    if (static_cast<uint64_t>(p.ransac.iterations) * kClusterBins > seg.cand_cap)
+      seg.ensure(seg.b.Vcap, seg.b.Scap, seg.b.Icap, p.ransac.iterations, gd.nwords);
+    if (timing) ck(cudaEventRecord(ev[1], stream), "ev");
+    launch_occupied_scan();
+    launch_classify(sd, 1);
+    if (timing) ck(cudaEventRecord(ev[2], stream), "ev");
+    launch_step_emit(grid_map());
+    launch_ccl(sd, grid_map());
+    launch_clusters(sd);
+    if (timing) ck(cudaEventRecord(ev[3], stream), "ev");
+    launch_ransac(rd);
+    if (timing) ck(cudaEventRecord(ev[4], stream), "ev");
+    launch_refine(p.ransac.up, p.refine, p.refine_exact);
+    launch_polygon(16, p.min_polygon_area);
+    if (timing) ck(cudaEventRecord(ev[5], stream), "ev");
+  }
+
+  // Grow capacities after an overflow (the frame's segmentation is re-run).
+  bool grow_if_overflow(int iterations) {
+    const uint32_t of = h_ctr->overflow;
+    if (!of) return false;
+    if (of & kOverflowClusters)
+      fail(VP_ENOMEM, "more than 2048 clusters >= min_cluster_size in one frame");
+    uint32_t vcap = seg.b.Vcap, scap = seg.b.Scap, icap = seg.b.Icap;
+    const uint64_t C = gd.ncells;
+    if (of & kOverflowOcc) vcap = static_cast<uint32_t>(std::min<uint64_t>(C, std::max<uint64_t>(2ull * vcap, h_ctr->V)));
+    if (of & (kOverflowStep | kOverflowOcc)) scap = std::max(scap, std::min<uint32_t>(vcap, std::max(2 * scap, h_ctr->S)));
+    if (of & kOverflowMembers) scap = std::min<uint32_t>(static_cast<uint32_t>(std::min<uint64_t>(C, 4ull * scap)), std::max(2 * scap, h_ctr->padded_members));
+    if (of & (kOverflowFits | kOverflowPool)) icap = std::max(2 * icap, scap);
+    seg.ensure(std::max(vcap, seg.b.Vcap), std::max(scap, seg.b.Scap), std::max(icap, seg.b.Icap),
+               iterations, gd.nwords);
+    return true;
+  }
+
+  // Download polygon records of the last segment() into host vectors.
+  void download_polygons(HostPolys& hp, bool keep_nullopt) {
+    const uint32_t F = h_ctr->nfits;
+    std::vector<double> rd(8ull * F);
+    std::vector<int32_t> ri(4ull * F);
+    if (F) {
+      ck(cudaMemcpyAsync(rd.data(), seg.b.prec_d, rd.size() * 8, cudaMemcpyDeviceToHost, stream), "prec");
+      ck(cudaMemcpyAsync(ri.data(), seg.b.prec_i, ri.size() * 4, cudaMemcpyDeviceToHost, stream), "prec");
+    }
+    const uint32_t pu = h_ctr->pool_used;
+    hp.verts.resize(5ull * pu);
+    if (pu)
+      ck(cudaMemcpyAsync(hp.verts.data(), seg.b.pool, hp.verts.size() * 8, cudaMemcpyDeviceToHost,
+                         stream), "pool");
+    ck(cudaStreamSynchronize(stream), "sync");
+    hp.polys.clear();
+    for (uint32_t f = 0; f < F; ++f) {
+      const int32_t nv = ri[4 * f + 2];
+      if (nv <= 0 && !keep_nullopt) continue;
+      vp_polygon q{};
+      q.plane.normal[0] = rd[8 * f];
+      q.plane.normal[1] = rd[8 * f + 1];
+      q.plane.normal[2] = rd[8 * f + 2];
+      q.plane.offset = rd[8 * f + 3];
+      q.plane.inlier_count = ri[4 * f];
+      q.plane.cluster_label = ri[4 * f + 1];
+      q.nverts = nv > 0 ? static_cast<uint32_t>(nv) : 0u;
+      q.area = rd[8 * f + 4];
+      // stash the pool offset in v2d temporarily
+      q.v2d = reinterpret_cast<const double*>(static_cast<uintptr_t>(ri[4 * f + 3]));
+      hp.polys.push_back(q);
+    }
+  }
+};
+
+namespace {
+
+vp_polygons_t* make_polygons_out(const HostPolys& hp) {
+  size_t nv = 0;
+  for (const auto& q : hp.polys) nv += q.nverts;
+  const size_t bytes = sizeof(vp_polygons_t) + hp.polys.size() * sizeof(vp_polygon) + nv * 5 * sizeof(double);
+  char* mem = static_cast<char*>(std::malloc(bytes));
+  if (!mem) fail(VP_ENOMEM, "host allocation");
+  auto* out = reinterpret_cast<vp_polygons_t*>(mem);
+  out->count = hp.polys.size();
+  out->polys = reinterpret_cast<vp_polygon*>(mem + sizeof(vp_polygons_t));
+  double* vbase = reinterpret_cast<double*>(mem + sizeof(vp_polygons_t) + hp.polys.size() * sizeof(vp_polygon));
+  for (size_t i = 0; i < hp.polys.size(); ++i) {
+    vp_polygon q = hp.polys[i];
+    const size_t voff = static_cast<size_t>(reinterpret_cast<uintptr_t>(q.v2d));
+    double* v2 = vbase;
+    double* v3 = vbase + 2 * q.nverts;
+    for (uint32_t k = 0; k < q.nverts; ++k) {
+      const double* src = hp.verts.data() + 5 * (voff + k);
+      v2[2 * k] = src[0];
+      v2[2 * k + 1] = src[1];
+      v3[3 * k] = src[2];
+      v3[3 * k + 1] = src[3];
+      v3[3 * k + 2] = src[4];
+    }
+    q.v2d = q.nverts ? v2 : nullptr;
+    q.v3d = q.nverts ? v3 : nullptr;
+    vbase += 5 * q.nverts;
+    out->polys[i] = q;
+  }
+  return out;
+}
+
+template <typename F>
+int guard(F&& f) {
+  try {
+    f();
+    return VP_OK;
+  } catch (const VpFail& e) {
+    g_err = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "host allocation failed";
+    return VP_ENOMEM;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return VP_ECUDA;
+  }
+}
+
+// ------------------------------------------------------------- frame steps
+// pipeline.cpp:37-41
+void global_cell(const double* t, double res, int32_t* c) {
+  for (int k = 0; k < 3; ++k) c[k] = static_cast<int32_t>(std::floor(t[k] / res));
+}
+
+void stage_points(vp_grid* g, const float* xyz, uint64_t n, bool device_ptr) {
+  if (device_ptr) {
+    g->h_fp->pts = xyz;
+  } else {
+    g->ensure_points(n);
+    if (n)
+      ck(cudaMemcpyAsync(g->d_pts, xyz, n * 12, cudaMemcpyHostToDevice, g->stream), "points h2d");
+    g->h_fp->pts = g->d_pts;
+  }
+  g->h_fp->n = n;
+}
+
+}  // namespace
+
+struct vp_pipeline {
+  vp_grid* grid = nullptr;
+  vp_pipeline_params p{};
+  int32_t last_cell[3] = {0, 0, 0};
+  uint32_t frame = 0;
+  ~vp_pipeline() { delete grid; }
+};
+
+namespace {
+
+// One run_frames iteration up to the end of segmentation (no host sync).
+// Returns whether the grid was recentered.
+bool pipeline_enqueue(vp_pipeline* pl, const float* xyz, uint64_t n, const double* R,
+                      const double* t, bool device_ptr, vp_shift_stats* ss) {
+  vp_grid* g = pl->grid;
+  if (!is_valid_rotation(R))  // voxel_grid.cpp:60-61, 183-184
+    fail(VP_EINVAL, "clear_rays: pose rotation is not orthonormal");
+  if (device_ptr) g->ensure_points(n);
+  g->set_pose(R, t);
+  g->fill_static_params();
+  stage_points(g, xyz, n, device_ptr);
+  int32_t cell[3];
+  global_cell(t, g->gd.res, cell);
+  bool rec = false;
+  std::memset(ss, 0, sizeof *ss);
+  if (cell[0] != pl->last_cell[0] || cell[1] != pl->last_cell[1] || cell[2] != pl->last_cell[2]) {
+    g->plan_recenter(t, ss);
+    std::memcpy(pl->last_cell, cell, sizeof cell);
+    rec = true;
+  }
+  ck(cudaEventRecord(g->ev[0], g->stream), "ev");
+  g->upload_params();
+  g->reset_frame_counters();
+  g->launch_clear(n);
+  g->launch_integrate(n);
+  g->launch_recenter();
+  g->launch_finalize();
+  g->launch_segment(pl->p, true);
+  return rec;
+}
+
+void fill_timing(vp_grid* g, vp_frame_timing* tm, uint64_t n) {
+  if (!tm) return;
+  float ms[5];
+  for (int i = 0; i < 5; ++i) ck(cudaEventElapsedTime(&ms[i], g->ev[i], g->ev[i + 1]), "elapsed");
+  tm->mapping_ms = ms[0];
+  tm->classify_ms = ms[1];
+  tm->cluster_ms = ms[2];
+  tm->ransac_ms = ms[3];
+  tm->hull_ms = ms[4];
+  float tot;
+  ck(cudaEventElapsedTime(&tot, g->ev[0], g->ev[5]), "elapsed");
+  tm->total_ms = tot;
+  tm->points = n;
+  tm->voxels = g->h_ctr->occupied;
+  tm->clusters = g->h_ctr->K;
+}
+
+// Re-run only the segmentation part after growing capacities.
+void rerun_segment_until_fits(vp_grid* g, const vp_pipeline_params& p) {
+  for (int tries = 0; tries < 6 && g->grow_if_overflow(p.ransac.iterations); ++tries) {
+    // restore the post-map state: the recenter was already applied, so the
+    // segmentation reads the post bitmap/offsets; make pre == post.
+    for (int k = 0; k < 3; ++k) {
+      g->h_fp->origin_pre[k] = g->h_fp->origin_post[k];
+      g->h_fp->off_pre[k] = g->h_fp->off_post[k];
+      g->h_fp->shift[k] = 0;
+    }
+    g->h_fp->occ_pre = g->h_fp->occ_post;
+    g->h_fp->do_shift = 0;
+    g->h_fp->n = 0;
+    const unsigned long long occ = g->h_ctr->occupied;
+    g->upload_params();
+    g->reset_frame_counters();
+    ck(cudaEventRecord(g->ev[0], g->stream), "ev");
+    g->launch_segment(p, true);
+    g->read_counters();
+    (void)occ;
+  }
+  if (g->h_ctr->overflow) fail(VP_ENOMEM, "segmentation capacity overflow persists");
+}
+
+struct TraceW {
+  std::vector<uint8_t> b;
+  template <typename T>
+  void put(const T& v) {
+    const auto* p = reinterpret_cast<const uint8_t*>(&v);
+    b.insert(b.end(), p, p + sizeof(T));
+  }
+  void raw(const void* p, size_t n) {
+    const auto* q = static_cast<const uint8_t*>(p);
+    b.insert(b.end(), q, q + n);
+  }
+};
+
+template <typename T>
+std::vector<T> d2h(const T* src, size_t n, cudaStream_t s) {
+  std::vector<T> v(n);
+  if (n) ck(cudaMemcpyAsync(v.data(), src, n * sizeof(T), cudaMemcpyDeviceToHost, s), "d2h");
+  return v;
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+const char* vp_last_error(void) { return g_err.c_str(); }
+const char* vp_version(void) { return "voxplane_b200 0.1 (sm_100a)"; }
+uint64_t vp_kernel_launch_count(void) { return g_launches.load(); }
+
+void vp_profile_enable(int on) {
+  g_prof_on = on != 0;
+  if (on) g_prof.clear();
+}
+
+// Accumulated per-kernel device time since vp_profile_enable(1): returns the
+// number of kernels; fills up to cap entries (name pointers stay valid until
+// the next vp_profile_enable).
+int vp_profile_read(const char** names, double* ms, uint64_t* calls, int cap) {
+  const int n = static_cast<int>(g_prof.size());
+  for (int i = 0; i < n && i < cap; ++i) {
+    names[i] = g_prof[i].name.c_str();
+    ms[i] = g_prof[i].ms;
+    calls[i] = g_prof[i].calls;
+  }
+  return n;
+}
+void vp_free(void* p) { std::free(p); }
+
+void vp_default_params(vp_pipeline_params* p) {
+  std::memset(p, 0, sizeof *p);
+  p->seg.neighbor_radius = 1;
+  p->seg.min_neighbors = 3;
+  p->seg.max_angle_deg = 15.0;
+  p->seg.adjacency_angle_deg = 15.0;
+  p->seg.distance_th = 0.05;
+  p->seg.min_cluster_size = 30;
+  p->seg.up[2] = 1.0;
+  p->ransac.iterations = 100;
+  p->ransac.inlier_eps = 0.01;
+  p->ransac.seed = 0;
+  p->ransac.up[2] = 1.0;
+  p->refine = 1;
+  p->min_polygon_area = 0.002;
+  p->refine_exact = 0;
+}
+
+int vp_grid_create(double res, const int32_t extent[3], const double center[3], int device,
+                   vp_grid** out) {
+  *out = nullptr;
+  return guard([&] {
+    auto* g = new vp_grid();
+    try {
+      g->init(res, extent, center, device);
+    } catch (...) {
+      delete g;
+      throw;
+    }
+    *out = g;
+  });
+}
+
+void vp_grid_destroy(vp_grid* g) { delete g; }
+
+int vp_grid_info(const vp_grid* g, double origin[3], int32_t extent[3], double* resolution,
+                 uint64_t* occupied_count) {
+  return guard([&] {
+    for (int k = 0; k < 3; ++k) {
+      if (origin) origin[k] = g->origin[k];
+      if (extent) extent[k] = g->ext[k];
+    }
+    if (resolution) *resolution = g->gd.res;
+    if (occupied_count) *occupied_count = g->host_occupied;
+  });
+}
+
+int vp_integrate_frame(vp_grid* g, const float* xyz, uint64_t n, const double R[9],
+                       const double t[3], vp_update_stats* st) {
+  return guard([&] {
+    if (!is_valid_rotation(R)) fail(VP_EINVAL, "integrate_frame: pose rotation is not orthonormal");
+    g->set_pose(R, t);
+    g->fill_static_params();
+    stage_points(g, xyz, n, false);
+    g->upload_params();
+    g->reset_frame_counters();
+    g->launch_integrate(n);
+    g->launch_finalize();
+    g->read_counters();
+    if (st) {
+      st->voxels_touched = g->h_ctr->touched;
+      st->points_discarded = g->h_ctr->discarded;
+    }
+  });
+}
+
+int vp_clear_rays(vp_grid* g, const float* xyz, uint64_t n, const double R[9], const double t[3],
+                  vp_clear_stats* st) {
+  return guard([&] {
+    if (!is_valid_rotation(R)) fail(VP_EINVAL, "clear_rays: pose rotation is not orthonormal");
+    g->set_pose(R, t);
+    g->fill_static_params();
+    stage_points(g, xyz, n, false);
+    g->upload_params();
+    g->reset_frame_counters();
+    g->launch_clear(n);
+    g->launch_finalize();
+    g->read_counters();
+    if (st) {
+      st->voxels_cleared = g->h_ctr->cleared;
+      st->voxels_freed = g->h_ctr->freed;
+    }
+  });
+}
+
+int vp_recenter(vp_grid* g, const double c[3], vp_shift_stats* st) {
+  return guard([&] {
+    vp_shift_stats tmp;
+    g->fill_static_params();
+    g->h_fp->n = 0;
+    if (!g->plan_recenter(c, st ? st : &tmp)) return;
+    g->upload_params();
+    g->reset_frame_counters();
+    g->launch_recenter();
+    g->launch_finalize();
+    g->read_counters();
+    if (st) st->voxels_dropped = g->h_ctr->dropped;
+  });
+}
+
+int vp_merge_point(vp_grid* g, const int32_t idx[3], const double p[3]) {
+  return guard([&] {
+    if (idx[0] < 0 || idx[1] < 0 || idx[2] < 0 || idx[0] >= g->ext[0] || idx[1] >= g->ext[1] ||
+        idx[2] >= g->ext[2])
+      fail(VP_EINVAL, "merge_point: index out of bounds");
+    g->fill_static_params();
+    g->h_fp->n = 0;
+    g->upload_params();
+    LAUNCH(k_merge_point, 1, 1, 0, g->stream, g->gd, g->d_fp, g->ctr, idx[0], idx[1], idx[2], p[0],
+           p[1], p[2]);
+    g->read_counters();
+  });
+}
+
+static uint64_t host_phys(const vp_grid* g, const int32_t* idx) {
+  int64_t p[3];
+  for (int k = 0; k < 3; ++k) p[k] = (static_cast<int64_t>(idx[k]) + g->off[k]) % g->ext[k];
+  return (static_cast<uint64_t>(p[0]) * g->ext[1] + p[1]) * g->ext[2] + p[2];
+}
+
+int vp_get_cell(vp_grid* g, const int32_t idx[3], double sum[3], uint32_t* count, uint8_t* status) {
+  return guard([&] {
+    if (idx[0] < 0 || idx[1] < 0 || idx[2] < 0 || idx[0] >= g->ext[0] || idx[1] >= g->ext[1] ||
+        idx[2] >= g->ext[2])
+      fail(VP_EINVAL, "cell: index out of bounds");
+    Cell c;
+    ck(cudaMemcpyAsync(&c, g->gd.cells + host_phys(g, idx), sizeof(Cell), cudaMemcpyDeviceToHost,
+                       g->stream), "cell");
+    ck(cudaStreamSynchronize(g->stream), "sync");
+    if (sum) {
+      sum[0] = c.sx;
+      sum[1] = c.sy;
+      sum[2] = c.sz;
+    }
+    if (count) *count = c.count;
+    if (status) *status = c.status;
+  });
+}
+
+int vp_set_status(vp_grid* g, const int32_t idx[3], uint8_t status) {
+  return guard([&] {
+    if (idx[0] < 0 || idx[1] < 0 || idx[2] < 0 || idx[0] >= g->ext[0] || idx[1] >= g->ext[1] ||
+        idx[2] >= g->ext[2])
+      fail(VP_EINVAL, "set_status: index out of bounds");
+    Cell* c = g->gd.cells + host_phys(g, idx);
+    ck(cudaMemcpyAsync(&c->status, &status, 1, cudaMemcpyHostToDevice, g->stream), "status");
+    ck(cudaStreamSynchronize(g->stream), "sync");
+  });
+}
+
+int vp_occupied_voxels(vp_grid* g, vp_occupied_t** out) {
+  *out = nullptr;
+  return guard([&] {
+    for (int tries = 0;; ++tries) {
+      g->fill_static_params();
+      g->h_fp->n = 0;
+      g->upload_params();
+      g->reset_frame_counters();
+      g->launch_occupied_scan();
+      LAUNCH(k_occ_gather, kWide, kThreads, 0, g->stream, g->gd, g->d_fp, g->ctr, g->seg.b);
+      g->read_counters();
+      if (g->h_ctr->V <= g->seg.b.Vcap || tries > 4) break;
+      g->seg.ensure(static_cast<uint32_t>(std::min<uint64_t>(g->gd.ncells, 2ull * g->h_ctr->V)),
+                    g->seg.b.Scap, g->seg.b.Icap, 100, g->gd.nwords);
+    }
+    const uint32_t V = g->h_ctr->V;
+    auto flat = d2h(g->seg.b.occ_list, V, g->stream);
+    auto mean = d2h(g->seg.b.own_mean, 3ull * V, g->stream);
+    auto cnt = d2h(g->seg.b.own_count, V, g->stream);
+    auto st = d2h(g->seg.b.own_status, V, g->stream);
+    ck(cudaStreamSynchronize(g->stream), "sync");
+    auto* o = static_cast<vp_occupied_t*>(std::calloc(1, sizeof(vp_occupied_t)));
+    o->count = V;
+    o->idx = static_cast<int32_t*>(std::malloc(12ull * V + 1));
+    o->mean = static_cast<double*>(std::malloc(24ull * V + 1));
+    o->npts = static_cast<uint32_t*>(std::malloc(4ull * V + 1));
+    o->status = static_cast<uint8_t*>(std::malloc(V + 1));
+    for (uint32_t v = 0; v < V; ++v) {
+      const uint32_t f = flat[v];
+      o->idx[3 * v + 2] = static_cast<int32_t>(f % g->ext[2]);
+      o->idx[3 * v + 1] = static_cast<int32_t>((f / g->ext[2]) % g->ext[1]);
+      o->idx[3 * v] = static_cast<int32_t>(f / g->ext[2] / g->ext[1]);
+    }
+    std::memcpy(o->mean, mean.data(), 24ull * V);
+    std::memcpy(o->npts, cnt.data(), 4ull * V);
+    std::memcpy(o->status, st.data(), V);
+    *out = o;
+  });
+}
+
+void vp_occupied_free(vp_occupied_t* o) {
+  if (!o) return;
+  std::free(o->idx);
+  std::free(o->mean);
+  std::free(o->npts);
+  std::free(o->status);
+  std::free(o);
+}
+
+// estimate_normals (+ optional classify) on the current grid state.
+static void run_normals(vp_grid* g, const vp_seg_params* p, int write_status) {
+  const SegDev sd = make_segdev(*p, g->gd.res);
+  for (int tries = 0;; ++tries) {
+    g->fill_static_params();
+    g->h_fp->n = 0;
+    g->upload_params();
+    g->reset_frame_counters();
+    g->launch_occupied_scan();
+    g->launch_classify(sd, write_status);
+    g->read_counters();
+    if (!(g->h_ctr->overflow & kOverflowOcc) || tries > 4) break;
+    g->seg.ensure(static_cast<uint32_t>(std::min<uint64_t>(g->gd.ncells, 2ull * g->h_ctr->V)),
+                  static_cast<uint32_t>(std::min<uint64_t>(g->gd.ncells, 2ull * g->h_ctr->V)),
+                  g->seg.b.Icap, 100, g->gd.nwords);
+  }
+  if (g->h_ctr->V == 0) fail(VP_EEMPTY, "estimate_normals: empty grid");
+}
+
+int vp_estimate_normals(vp_grid* g, const vp_seg_params* p, vp_estimates_t** out) {
+  *out = nullptr;
+  return guard([&] {
+    run_normals(g, p, 0);
+    LAUNCH(k_occ_gather, kWide, kThreads, 0, g->stream, g->gd, g->d_fp, g->ctr, g->seg.b);
+    const uint32_t V = g->h_ctr->V;
+    auto flat = d2h(g->seg.b.occ_list, V, g->stream);
+    auto mean = d2h(g->seg.b.own_mean, 3ull * V, g->stream);
+    auto nrm = d2h(g->seg.b.est_normal, 3ull * V, g->stream);
+    auto nc = d2h(g->seg.b.est_ncount, V, g->stream);
+    auto va = d2h(g->seg.b.est_valid, V, g->stream);
+    ck(cudaStreamSynchronize(g->stream), "sync");
+    auto* e = static_cast<vp_estimates_t*>(std::calloc(1, sizeof(vp_estimates_t)));
+    e->count = V;
+    e->idx = static_cast<int32_t*>(std::malloc(12ull * V + 1));
+    e->mean = static_cast<double*>(std::malloc(24ull * V + 1));
+    e->normal = static_cast<double*>(std::malloc(24ull * V + 1));
+    e->neighbor_count = static_cast<int32_t*>(std::malloc(4ull * V + 1));
+    e->angle_to_up_deg = static_cast<double*>(std::malloc(8ull * V + 1));
+    e->valid = static_cast<uint8_t*>(std::malloc(V + 1));
+    for (uint32_t v = 0; v < V; ++v) {
+      const uint32_t f = flat[v];
+      e->idx[3 * v + 2] = static_cast<int32_t>(f % g->ext[2]);
+      e->idx[3 * v + 1] = static_cast<int32_t>((f / g->ext[2]) % g->ext[1]);
+      e->idx[3 * v] = static_cast<int32_t>(f / g->ext[2] / g->ext[1]);
+      e->angle_to_up_deg[v] = 0.0;
+      if (va[v]) {  // segmentation.cpp:62-63 with the host libm
+        const double d0 = (nrm[3 * v] * p->up[0] + nrm[3 * v + 1] * p->up[1]) + nrm[3 * v + 2] * p->up[2];
+        const double d = std::clamp(d0, 0.0, 1.0);
+        e->angle_to_up_deg[v] = std::acos(d) * kRadToDeg;
+      }
+    }
+    std::memcpy(e->mean, mean.data(), 24ull * V);
+    std::memcpy(e->normal, nrm.data(), 24ull * V);
+    std::memcpy(e->neighbor_count, nc.data(), 4ull * V);
+    std::memcpy(e->valid, va.data(), V);
+    *out = e;
+  });
+}
+
+void vp_estimates_free(vp_estimates_t* e) {
+  if (!e) return;
+  std::free(e->idx);
+  std::free(e->mean);
+  std::free(e->normal);
+  std::free(e->neighbor_count);
+  std::free(e->angle_to_up_deg);
+  std::free(e->valid);
+  std::free(e);
+}
+
+int vp_classify_steppable(vp_grid* g, const vp_seg_params* p, vp_steppable_t** steppable,
+                          int32_t** objects_idx, size_t* n_objects) {
+  *steppable = nullptr;
+  return guard([&] {
+    run_normals(g, p, 1);
+    const uint32_t V = g->h_ctr->V;
+    const uint32_t S = g->h_ctr->S;
+    auto flat = d2h(g->seg.b.occ_list, V, g->stream);
+    auto flag = d2h(g->seg.b.step_flag, V, g->stream);
+    auto mean = d2h(g->seg.b.own_mean, 3ull * V, g->stream);
+    auto nrm = d2h(g->seg.b.est_normal, 3ull * V, g->stream);
+    ck(cudaStreamSynchronize(g->stream), "sync");
+    auto* s = static_cast<vp_steppable_t*>(std::calloc(1, sizeof(vp_steppable_t)));
+    s->count = S;
+    s->idx = static_cast<int32_t*>(std::malloc(12ull * S + 1));
+    s->mean = static_cast<double*>(std::malloc(24ull * S + 1));
+    s->normal = static_cast<double*>(std::malloc(24ull * S + 1));
+    std::vector<int32_t> obj;
+    uint32_t k = 0;
+    for (uint32_t v = 0; v < V; ++v) {
+      const uint32_t f = flat[v];
+      const int32_t xyz[3] = {static_cast<int32_t>(f / g->ext[2] / g->ext[1]),
+                              static_cast<int32_t>((f / g->ext[2]) % g->ext[1]),
+                              static_cast<int32_t>(f % g->ext[2])};
+      if (flag[v]) {
+        std::memcpy(s->idx + 3 * k, xyz, 12);
+        std::memcpy(s->mean + 3 * k, mean.data() + 3 * v, 24);
+        std::memcpy(s->normal + 3 * k, nrm.data() + 3 * v, 24);
+        ++k;
+      } else {
+        obj.insert(obj.end(), xyz, xyz + 3);
+      }
+    }
+    *steppable = s;
+    if (objects_idx) {
+      *objects_idx = static_cast<int32_t*>(std::malloc(obj.size() * 4 + 1));
+      std::memcpy(*objects_idx, obj.data(), obj.size() * 4);
+    }
+    if (n_objects) *n_objects = obj.size() / 3;
+  });
+}
+
+void vp_steppable_free(vp_steppable_t* s) {
+  if (!s) return;
+  std::free(s->idx);
+  std::free(s->mean);
+  std::free(s->normal);
+  std::free(s);
+}
+
+}  // extern "C"
+
+// ---- host-list entry points share a per-device scratch grid (1^3 window) --
+namespace {
+struct Scratch {
+  vp_grid* g = nullptr;
+  int device = -1;
+};
+thread_local Scratch t_scratch;
+
+vp_grid* scratch_grid(int device) {
+  if (t_scratch.g && t_scratch.device == device) return t_scratch.g;
+  delete t_scratch.g;
+  t_scratch.g = nullptr;
+  auto* g = new vp_grid();
+  const int32_t e[3] = {1, 1, 32};
+  const double c[3] = {0, 0, 0};
+  try {
+    g->init(1.0, e, c, device);
+  } catch (...) {
+    delete g;
+    throw;
+  }
+  t_scratch.g = g;
+  t_scratch.device = device;
+  return g;
+}
+
+template <typename T>
+void h2d(T* dst, const T* src, size_t n, cudaStream_t s) {
+  if (n) ck(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyHostToDevice, s), "h2d");
+}
+
+void set_counter_u32(vp_grid* g, size_t field_offset, uint32_t v) {
+  ck(cudaMemcpyAsync(reinterpret_cast<char*>(g->ctr) + field_offset, &v, 4, cudaMemcpyHostToDevice,
+                     g->stream), "ctr set");
+  ck(cudaStreamSynchronize(g->stream), "sync");
+}
+
+// Temporary dense ordinal volume over the steppable bounding box
+// (segmentation.cpp:96-110).
+struct BoxMap {
+  MapDesc m{};
+  int32_t* buf = nullptr;
+  ~BoxMap() { if (buf) cudaFree(buf); }
+};
+
+void upload_steppable(vp_grid* g, const vp_steppable_t* s, BoxMap& bm) {
+  const uint32_t S = static_cast<uint32_t>(s->count);
+  g->seg.ensure(std::max(g->seg.b.Vcap, S), std::max(g->seg.b.Scap, S), g->seg.b.Icap, 100, g->gd.nwords);
+  int lo[3], hi[3];
+  for (int k = 0; k < 3; ++k) lo[k] = hi[k] = S ? s->idx[k] : 0;
+  for (uint32_t i = 0; i < S; ++i)
+    for (int k = 0; k < 3; ++k) {
+      lo[k] = std::min(lo[k], s->idx[3 * i + k]);
+      hi[k] = std::max(hi[k], s->idx[3 * i + k]);
+    }
+  uint64_t vol = 1;
+  for (int k = 0; k < 3; ++k) {
+    bm.m.lo[k] = lo[k];
+    bm.m.dims[k] = hi[k] - lo[k] + 1;
+    vol *= static_cast<uint64_t>(bm.m.dims[k]);
+  }
+  bm.buf = dalloc<int32_t>(vol);
+  ck(cudaMemsetAsync(bm.buf, 0xff, vol * 4, g->stream), "map");
+  bm.m.map = bm.buf;
+  h2d(g->seg.b.st_idx, s->idx, 3ull * S, g->stream);
+  h2d(g->seg.b.st_mean, s->mean, 3ull * S, g->stream);
+  h2d(g->seg.b.st_normal, s->normal, 3ull * S, g->stream);
+  g->reset_frame_counters();
+  set_counter_u32(g, offsetof(Counters, S), S);
+  LAUNCH(k_map_fill, kWide, kThreads, 0, g->stream, g->ctr, g->seg.b, bm.m);
+}
+}  // namespace
+
+extern "C" {
+
+
+int vp_label_components(const vp_steppable_t* s, const vp_seg_params* p, double resolution,
+                        int device, int32_t* labels) {
+  return guard([&] {
+    if (s->count == 0) return;
+    vp_grid* g = scratch_grid(device);
+    BoxMap bm;
+    upload_steppable(g, s, bm);
+    const SegDev sd = make_segdev(*p, resolution);
+    g->launch_ccl(sd, bm.m);
+    ck(cudaMemcpyAsync(labels, g->seg.b.label, 4 * s->count, cudaMemcpyDeviceToHost, g->stream), "labels");
+    ck(cudaStreamSynchronize(g->stream), "sync");
+  });
+}
+
+int vp_build_adjacency(const vp_steppable_t* s, const vp_seg_params* p, double resolution,
+                       int device, uint64_t** row_offsets, int32_t** cols, uint64_t* n_edges) {
+  return guard([&] {
+    const uint32_t S = static_cast<uint32_t>(s->count);
+    *row_offsets = static_cast<uint64_t*>(std::calloc(S + 1, 8));
+    *cols = nullptr;
+    *n_edges = 0;
+    if (S == 0) return;
+    vp_grid* g = scratch_grid(device);
+    BoxMap bm;
+    upload_steppable(g, s, bm);
+    const SegDev sd = make_segdev(*p, resolution);
+    uint32_t* cnt = dalloc<uint32_t>(S);
+    LAUNCH(k_adjacency, kWide, kThreads, 0, g->stream, g->ctr, sd, g->seg.b, bm.m, nullptr, cnt, nullptr);
+    auto c = d2h(cnt, S, g->stream);
+    ck(cudaStreamSynchronize(g->stream), "sync");
+    std::vector<uint64_t> rows(S + 1, 0);
+    for (uint32_t i = 0; i < S; ++i) rows[i + 1] = rows[i] + c[i];
+    uint64_t* drows = dalloc<uint64_t>(S + 1);
+    int32_t* dcols = dalloc<int32_t>(rows[S]);
+    h2d(drows, rows.data(), S + 1, g->stream);
+    LAUNCH(k_adjacency, kWide, kThreads, 0, g->stream, g->ctr, sd, g->seg.b, bm.m, drows, cnt, dcols);
+    *cols = static_cast<int32_t*>(std::malloc(rows[S] * 4 + 1));
+    if (rows[S]) ck(cudaMemcpyAsync(*cols, dcols, rows[S] * 4, cudaMemcpyDeviceToHost, g->stream), "cols");
+    ck(cudaStreamSynchronize(g->stream), "sync");
+    std::memcpy(*row_offsets, rows.data(), 8ull * (S + 1));
+    *n_edges = rows[S];
+    cudaFree(cnt);
+    cudaFree(drows);
+    cudaFree(dcols);
+  });
+}
+
+int vp_fit_planes(size_t n_clusters, const int32_t* labels, const uint64_t* offsets,
+                  const double* means, const vp_ransac_params* p, int device, vp_fits_t** out) {
+  *out = nullptr;
+  return guard([&] {
+    vp_grid* g = scratch_grid(device);
+    const RansacDev rd = make_ransacdev(*p);
+    std::vector<vp_plane> models;
+    std::vector<uint64_t> offs{0};
+    std::vector<double> inl;
+    uint64_t skipped = 0, unfit = 0;
+    for (size_t c0 = 0; c0 < n_clusters; c0 += kClusterBins) {
+      const uint32_t K = static_cast<uint32_t>(std::min<size_t>(kClusterBins, n_clusters - c0));
+      std::vector<uint32_t> ksize(K), kpoff(K + 1, 0);
+      uint64_t tot = 0, maxm = 0;
+      for (uint32_t k = 0; k < K; ++k) {
+        ksize[k] = static_cast<uint32_t>(offsets[c0 + k + 1] - offsets[c0 + k]);
+        kpoff[k] = static_cast<uint32_t>(tot);
+        tot += (ksize[k] + 31u) & ~31u;
+        maxm += ksize[k];
+      }
+      kpoff[K] = static_cast<uint32_t>(tot);
+      const uint32_t need = static_cast<uint32_t>(std::max<uint64_t>(tot, maxm));
+      g->seg.ensure(g->seg.b.Vcap, std::max(g->seg.b.Scap, need), std::max(g->seg.b.Icap, need),
+                    std::max(p->iterations, 1), g->gd.nwords);
+      std::vector<double> mx(tot, 0.0), my(tot, 0.0), mz(tot, 0.0);
+      for (uint32_t k = 0; k < K; ++k)
+        for (uint32_t j = 0; j < ksize[k]; ++j) {
+          const double* q = means + 3 * (offsets[c0 + k] + j);
+          mx[kpoff[k] + j] = q[0];
+          my[kpoff[k] + j] = q[1];
+          mz[kpoff[k] + j] = q[2];
+        }
+      h2d(g->seg.b.klabel, labels + c0, K, g->stream);
+      h2d(g->seg.b.ksize, ksize.data(), K, g->stream);
+      h2d(g->seg.b.kpoff, kpoff.data(), K + 1, g->stream);
+      h2d(g->seg.b.mx, mx.data(), tot, g->stream);
+      h2d(g->seg.b.my, my.data(), tot, g->stream);
+      h2d(g->seg.b.mz, mz.data(), tot, g->stream);
+      g->reset_frame_counters();
+      set_counter_u32(g, offsetof(Counters, K), K);
+      g->launch_ransac(rd);
+      g->read_counters();
+      const uint32_t F = g->h_ctr->nfits;
+      skipped += g->h_ctr->skipped;
+      unfit += g->h_ctr->unfit;
+      auto fm = d2h(g->seg.b.fit_model, 4ull * F, g->stream);
+      auto meta = d2h(g->seg.b.fit_meta, 2ull * F, g->stream);
+      auto io = d2h(g->seg.b.ioff, F + 1ull, g->stream);
+      ck(cudaStreamSynchronize(g->stream), "sync");
+      auto in = d2h(g->seg.b.inl, 3ull * io[F], g->stream);
+      ck(cudaStreamSynchronize(g->stream), "sync");
+      for (uint32_t f = 0; f < F; ++f) {
+        vp_plane pl{};
+        for (int q = 0; q < 3; ++q) pl.normal[q] = fm[4 * f + q];
+        pl.offset = fm[4 * f + 3];
+        pl.inlier_count = meta[2 * f];
+        pl.cluster_label = meta[2 * f + 1];
+        models.push_back(pl);
+        offs.push_back(offs.back() + (io[f + 1] - io[f]));
+      }
+      inl.insert(inl.end(), in.begin(), in.end());
+    }
+    auto* f = static_cast<vp_fits_t*>(std::calloc(1, sizeof(vp_fits_t)));
+    f->count = models.size();
+    f->models = static_cast<vp_plane*>(std::malloc(models.size() * sizeof(vp_plane) + 1));
+    std::memcpy(f->models, models.data(), models.size() * sizeof(vp_plane));
+    f->offsets = static_cast<uint64_t*>(std::malloc(offs.size() * 8));
+    std::memcpy(f->offsets, offs.data(), offs.size() * 8);
+    f->inliers = static_cast<double*>(std::malloc(inl.size() * 8 + 1));
+    std::memcpy(f->inliers, inl.data(), inl.size() * 8);
+    f->clusters_skipped_small = skipped;
+    f->clusters_unfit = unfit;
+    *out = f;
+  });
+}
+
+void vp_fits_free(vp_fits_t* f) {
+  if (!f) return;
+  std::free(f->models);
+  std::free(f->offsets);
+  std::free(f->inliers);
+  std::free(f);
+}
+
+}  // extern "C"
+
+namespace {
+// Upload (plane, inlier set) batches as "fits" of the scratch grid.
+void upload_fit_batch(vp_grid* g, size_t f0, uint32_t F, const vp_plane* planes,
+                      const uint64_t* offsets, const double* inliers, double* model_dst) {
+  std::vector<double> fm(4ull * F);
+  std::vector<int32_t> meta(2ull * F);
+  std::vector<uint32_t> io(F + 1);
+  const uint64_t base = offsets[f0];
+  for (uint32_t f = 0; f < F; ++f) {
+    for (int q = 0; q < 3; ++q) fm[4 * f + q] = planes[f0 + f].normal[q];
+    fm[4 * f + 3] = planes[f0 + f].offset;
+    meta[2 * f] = planes[f0 + f].inlier_count;
+    meta[2 * f + 1] = planes[f0 + f].cluster_label;
+    io[f] = static_cast<uint32_t>(offsets[f0 + f] - base);
+  }
+  io[F] = static_cast<uint32_t>(offsets[f0 + F] - base);
+  const uint32_t tot = io[F];
+  g->seg.ensure(g->seg.b.Vcap, g->seg.b.Scap, std::max(g->seg.b.Icap, tot), 100, g->gd.nwords);
+  h2d(model_dst == nullptr ? g->seg.b.fit_model : model_dst, fm.data(), fm.size(), g->stream);
+  h2d(g->seg.b.fit_meta, meta.data(), meta.size(), g->stream);
+  h2d(g->seg.b.ioff, io.data(), io.size(), g->stream);
+  h2d(g->seg.b.inl, inliers + 3 * base, 3ull * tot, g->stream);
+  g->reset_frame_counters();
+  set_counter_u32(g, offsetof(Counters, nfits), F);
+}
+}  // namespace
+
+extern "C" {
+
+
+int vp_refine_planes(const vp_fits_t* fits, const double up[3], int exact, int device,
+                     vp_plane* refined) {
+  return guard([&] {
+    vp_grid* g = scratch_grid(device);
+    for (size_t f0 = 0; f0 < fits->count; f0 += kClusterBins) {
+      const uint32_t F = static_cast<uint32_t>(std::min<size_t>(kClusterBins, fits->count - f0));
+      upload_fit_batch(g, f0, F, fits->models, fits->offsets, fits->inliers, nullptr);
+      g->launch_refine(up, 1, exact);
+      auto rm = d2h(g->seg.b.ref_model, 4ull * F, g->stream);
+      ck(cudaStreamSynchronize(g->stream), "sync");
+      for (uint32_t f = 0; f < F; ++f) {
+        refined[f0 + f] = fits->models[f0 + f];  // pipeline.cpp:76-77 keep count/label
+        for (int q = 0; q < 3; ++q) refined[f0 + f].normal[q] = rm[4 * f + q];
+        refined[f0 + f].offset = rm[4 * f + 3];
+      }
+    }
+  });
+}
+
+int vp_make_polygons(size_t n, const vp_plane* planes, const uint64_t* offsets,
+                     const double* inliers, int filter_directions, int device, vp_polygons_t** out) {
+  *out = nullptr;
+  return guard([&] {
+    vp_grid* g = scratch_grid(device);
+    HostPolys all;
+    std::vector<double> verts;
+    for (size_t f0 = 0; f0 < n || (f0 == 0 && n == 0); f0 += kClusterBins) {
+      if (n == 0) break;
+      const uint32_t F = static_cast<uint32_t>(std::min<size_t>(kClusterBins, n - f0));
+      upload_fit_batch(g, f0, F, planes, offsets, inliers, g->seg.b.ref_model);
+      g->launch_polygon(filter_directions, -std::numeric_limits<double>::infinity());
+      g->read_counters();
+      if (g->h_ctr->overflow & kOverflowPool) fail(VP_ENOMEM, "polygon vertex pool overflow");
+      HostPolys hp;
+      g->download_polygons(hp, true);
+      const size_t vbase = all.verts.size() / 5;
+      for (auto q : hp.polys) {
+        q.v2d = reinterpret_cast<const double*>(reinterpret_cast<uintptr_t>(q.v2d) + vbase);
+        all.polys.push_back(q);
+      }
+      all.verts.insert(all.verts.end(), hp.verts.begin(), hp.verts.end());
+    }
+    *out = make_polygons_out(all);
+  });
+}
+
+void vp_polygons_free(vp_polygons_t* p) { std::free(p); }
+
+int vp_segment(vp_grid* g, const vp_pipeline_params* p, vp_polygons_t** out,
+               vp_frame_timing* timing) {
+  if (out) *out = nullptr;
+  return guard([&] {
+    g->fill_static_params();
+    g->h_fp->n = 0;
+    g->upload_params();
+    g->reset_frame_counters();
+    ck(cudaEventRecord(g->ev[0], g->stream), "ev");
+    g->launch_segment(*p, true);
+    g->read_counters();
+    rerun_segment_until_fits(g, *p);
+    fill_timing(g, timing, 0);
+    if (timing) timing->mapping_ms = 0.0;
+    HostPolys hp;
+    g->download_polygons(hp, false);
+    if (out) *out = make_polygons_out(hp);
+  });
+}
+
+int vp_pipeline_create(double res, const int32_t extent[3], const double start_center[3],
+                       const vp_pipeline_params* p, int device, vp_pipeline** out) {
+  *out = nullptr;
+  return guard([&] {
+    auto* pl = new vp_pipeline();
+    try {
+      pl->grid = new vp_grid();
+      pl->grid->init(res, extent, start_center, device);
+    } catch (...) {
+      delete pl;
+      throw;
+    }
+    if (p) pl->p = *p; else vp_default_params(&pl->p);
+    global_cell(start_center, res, pl->last_cell);  // pipeline.cpp:174
+    *out = pl;
+  });
+}
+
+void vp_pipeline_destroy(vp_pipeline* pl) { delete pl; }
+
+int vp_pipeline_reset(vp_pipeline* pl, const double start_center[3]) {
+  return guard([&] { pl->grid->reset(start_center); global_cell(start_center, pl->grid->gd.res, pl->last_cell); pl->frame = 0; });
+}
+
+vp_grid* vp_pipeline_grid(vp_pipeline* pl) { return pl->grid; }
+
+void* vp_pipeline_stream(vp_pipeline* pl) { return pl->grid->stream; }
+
+int vp_pipeline_counters(vp_pipeline* pl, uint64_t out[16]) {
+  return guard([&] {
+    const Counters& c = *pl->grid->h_ctr;
+    const uint64_t v[16] = {c.cleared, c.freed, c.touched, c.discarded, c.dropped, c.occupied,
+                            c.V, c.S, c.K, c.nfits, c.padded_members, c.inliers, c.pool_used,
+                            c.newly, c.ngroups, c.overflow};
+    std::memcpy(out, v, sizeof v);
+  });
+}
+
+static int pipeline_frame_impl(vp_pipeline* pl, const float* xyz, uint64_t n, const double* R,
+                               const double* t, bool device_ptr, vp_polygons_t** out,
+                               vp_frame_timing* timing) {
+  if (out) *out = nullptr;
+  return guard([&] {
+    vp_shift_stats ss;
+    pipeline_enqueue(pl, xyz, n, R, t, device_ptr, &ss);
+    vp_grid* g = pl->grid;
+    g->read_counters();
+    if (g->h_ctr->overflow) rerun_segment_until_fits(g, pl->p);
+    fill_timing(g, timing, n);
+    if (out) {
+      HostPolys hp;
+      g->download_polygons(hp, false);
+      *out = make_polygons_out(hp);
+    }
+    ++pl->frame;
+  });
+}
+
+int vp_pipeline_frame(vp_pipeline* pl, const float* xyz, uint64_t n, const double R[9],
+                      const double t[3], vp_polygons_t** out, vp_frame_timing* timing) {
+  return pipeline_frame_impl(pl, xyz, n, R, t, false, out, timing);
+}
+
+int vp_pipeline_frame_device(vp_pipeline* pl, const float* xyz_dev, uint64_t n, const double R[9],
+                             const double t[3], vp_polygons_t** out, vp_frame_timing* timing) {
+  return pipeline_frame_impl(pl, xyz_dev, n, R, t, true, out, timing);
+}
+
+int vp_pipeline_frame_trace(vp_pipeline* pl, const float* xyz, uint64_t n, const double R[9],
+                            const double t[3], uint8_t** buf, uint64_t* len) {
+  *buf = nullptr;
+  *len = 0;
+  return guard([&] {
+    vp_shift_stats ss;
+    const bool rec = pipeline_enqueue(pl, xyz, n, R, t, false, &ss);
+    vp_grid* g = pl->grid;
+    g->read_counters();
+    if (g->h_ctr->overflow) rerun_segment_until_fits(g, pl->p);
+    const Counters c = *g->h_ctr;
+    TraceW w;
+    w.raw("VPTR", 4);
+    w.put<uint32_t>(VP_TRACE_VERSION);
+    w.put<uint32_t>(pl->frame++);
+    w.put<uint64_t>(c.cleared);
+    w.put<uint64_t>(c.freed);
+    w.put<uint64_t>(c.touched);
+    w.put<uint64_t>(c.discarded);
+    w.put<uint8_t>(rec ? 1 : 0);
+    w.raw(ss.shift, 12);
+    w.put<uint64_t>(c.dropped);
+    w.raw(g->origin, 24);
+    w.put<uint64_t>(c.occupied);
+    if (c.occupied == 0) {
+      for (int k = 0; k < 7; ++k) w.put<uint64_t>(0);
+    } else {
+      const uint32_t V = c.V, S = c.S, K = std::min<uint32_t>(c.K, kClusterBins), F = c.nfits;
+      auto flat = d2h(g->seg.b.occ_list, V, g->stream);
+      auto mean = d2h(g->seg.b.own_mean, 3ull * V, g->stream);
+      auto cnt = d2h(g->seg.b.own_count, V, g->stream);
+      auto st = d2h(g->seg.b.own_status, V, g->stream);
+      auto nrm = d2h(g->seg.b.est_normal, 3ull * V, g->stream);
+      auto nc = d2h(g->seg.b.est_ncount, V, g->stream);
+      auto va = d2h(g->seg.b.est_valid, V, g->stream);
+      auto sidx = d2h(g->seg.b.st_idx, 3ull * S, g->stream);
+      auto smean = d2h(g->seg.b.st_mean, 3ull * S, g->stream);
+      auto snrm = d2h(g->seg.b.st_normal, 3ull * S, g->stream);
+      auto lab = d2h(g->seg.b.label, S, g->stream);
+      auto kl = d2h(g->seg.b.klabel, K, g->stream);
+      auto ks = d2h(g->seg.b.ksize, K, g->stream);
+      auto fm = d2h(g->seg.b.fit_model, 4ull * F, g->stream);
+      auto meta = d2h(g->seg.b.fit_meta, 2ull * F, g->stream);
+      auto io = d2h(g->seg.b.ioff, F + 1ull, g->stream);
+      auto rm = d2h(g->seg.b.ref_model, 4ull * F, g->stream);
+      ck(cudaStreamSynchronize(g->stream), "sync");
+      auto in = d2h(g->seg.b.inl, 3ull * io[F], g->stream);
+      ck(cudaStreamSynchronize(g->stream), "sync");
+      w.put<uint64_t>(V);
+      for (uint32_t v = 0; v < V; ++v) {
+        const uint32_t f = flat[v];
+        w.put<int32_t>(static_cast<int32_t>(f / g->ext[2] / g->ext[1]));
+        w.put<int32_t>(static_cast<int32_t>((f / g->ext[2]) % g->ext[1]));
+        w.put<int32_t>(static_cast<int32_t>(f % g->ext[2]));
+      }
+      w.raw(mean.data(), 24ull * V);
+      w.raw(cnt.data(), 4ull * V);
+      w.raw(st.data(), V);
+      w.raw(nrm.data(), 24ull * V);
+      w.raw(nc.data(), 4ull * V);
+      w.raw(va.data(), V);
+      w.put<uint64_t>(S);
+      w.raw(sidx.data(), 12ull * S);
+      w.raw(smean.data(), 24ull * S);
+      w.raw(snrm.data(), 24ull * S);
+      w.raw(lab.data(), 4ull * S);
+      w.put<uint64_t>(K);
+      for (uint32_t k = 0; k < K; ++k) {
+        w.put<int32_t>(kl[k]);
+        w.put<uint64_t>(ks[k]);
+      }
+      w.put<uint64_t>(c.skipped);
+      w.put<uint64_t>(c.unfit);
+      w.put<uint64_t>(F);
+      for (uint32_t f = 0; f < F; ++f) {
+        w.raw(&fm[4 * f], 32);
+        w.put<int32_t>(meta[2 * f]);
+        w.put<int32_t>(meta[2 * f + 1]);
+        const uint64_t m = io[f + 1] - io[f];
+        w.put<uint64_t>(m);
+        w.raw(in.data() + 3ull * io[f], 24 * m);
+      }
+      for (uint32_t f = 0; f < F; ++f) w.raw(&rm[4 * f], 32);
+      HostPolys hp;
+      g->download_polygons(hp, false);
+      w.put<uint64_t>(hp.polys.size());
+      for (const auto& q : hp.polys) {
+        w.raw(q.plane.normal, 24);
+        w.put<double>(q.plane.offset);
+        w.put<int32_t>(q.plane.inlier_count);
+        w.put<int32_t>(q.plane.cluster_label);
+        w.put<uint64_t>(q.nverts);
+        const size_t voff = static_cast<size_t>(reinterpret_cast<uintptr_t>(q.v2d));
+        for (uint32_t k = 0; k < q.nverts; ++k) w.raw(&hp.verts[5 * (voff + k)], 16);
+        for (uint32_t k = 0; k < q.nverts; ++k) w.raw(&hp.verts[5 * (voff + k) + 2], 24);
+        w.put<double>(q.area);
+      }
+    }
+    *buf = static_cast<uint8_t*>(std::malloc(w.b.size()));
+    std::memcpy(*buf, w.b.data(), w.b.size());
+    *len = w.b.size();
+  });
+}
+
+}  // extern "C"

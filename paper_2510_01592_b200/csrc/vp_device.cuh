@@ -1,0 +1,288 @@
+// Device-side data layout and arithmetic shared by the sm_100a kernels.
+//
+// HBM layout:
+//   cells    Cell[C] (32 B, one DRAM sector) in PHYSICAL toroidal order:
+//            phys(l) = (l + off) mod extent per axis, x-major. recenter()
+//            (voxel_grid.cpp:217-252) only rotates `off` and zeroes the cells
+//            that fall off the window, instead of moving all C cells.
+//   occ      occupancy bitmap, 1 bit per cell, LOGICAL (window) order, rows of
+//            W = ceil(ez/32) words: word((x,y,z)) = (x*ey + y)*W + z/32.
+//            Bit set <=> count > 0 <=> the cell record is non-zero, so free
+//            cells are never touched.
+//   clr      clear_rays dedup mask (voxel_grid.cpp:188), same layout as occ.
+//   ordmap   int32 per cell (logical), steppable ordinal or -1; written and
+//            reset per frame for the steppable voxels only.
+//
+// Arithmetic: the whole library is compiled with -fmad=false; every FP64
+// expression below is written in the reference's evaluation order (see
+// oracle/eigen_shim/Eigen/Dense for the Eigen 3.4 order this follows), so
+// keys, sums, normals, labels and RANSAC candidates are bit-identical.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace vp {
+
+struct __align__(32) Cell {  // voxel_grid.hpp:19-23
+  double sx, sy, sz;
+  uint32_t count;
+  uint8_t status;
+  uint8_t pad[3];
+};
+static_assert(sizeof(Cell) == 32, "Cell must be one 32-byte sector");
+
+constexpr uint32_t kEmptyKey = 0xffffffffu;
+
+// Dynamic per-frame state, written by the host into device memory before the
+// frame's kernels run (so the whole frame can be replayed as a CUDA graph).
+struct FrameParams {
+  double R[9];          // pose rotation, row-major
+  double t[3];          // pose translation (= sensor origin for clear_rays)
+  const float* pts;     // device xyz (n x 3)
+  uint64_t n;
+  double origin_pre[3];   // window origin during clear/integrate
+  double origin_post[3];  // after recenter
+  int32_t off_pre[3];     // toroidal offsets during clear/integrate
+  int32_t off_post[3];
+  int32_t shift[3];
+  int32_t do_shift;
+  uint32_t* occ_pre;   // occupancy bitmap before recenter
+  uint32_t* occ_post;  // after recenter (== occ_pre when no shift)
+};
+
+// Static grid description (pointers fixed at creation).
+struct GridDesc {
+  Cell* cells;
+  uint32_t* clr;
+  int32_t* ordmap;
+  int32_t ex, ey, ez, W;  // extent and words per (x,y) row
+  double res;
+  uint64_t ncells;
+  uint64_t nwords;
+};
+
+// Device counters (one struct in device memory, zeroed per frame except
+// `occupied`, which persists like VoxelGrid::occupied_).
+struct Counters {
+  unsigned long long occupied;
+  unsigned long long cleared, freed, touched, discarded, dropped;
+  unsigned long long newly;  // newly occupied by integrate
+  uint32_t ngroups, group_cursor;
+  uint32_t V, S, K, nfits;
+  uint32_t skipped, unfit;
+  uint32_t pool_used;
+  uint32_t overflow;  // bit flags, see kOverflow*
+  uint32_t padded_members;
+  uint32_t inliers;
+};
+
+constexpr uint32_t kOverflowOcc = 1u;
+constexpr uint32_t kOverflowStep = 2u;
+constexpr uint32_t kOverflowClusters = 4u;
+constexpr uint32_t kOverflowMembers = 8u;
+constexpr uint32_t kOverflowFits = 16u;
+constexpr uint32_t kOverflowPool = 32u;
+constexpr uint32_t kOverflowHull = 64u;
+
+// ------------------------------------------------------------- arithmetic
+struct d3 {
+  double x, y, z;
+};
+
+__device__ __forceinline__ d3 mk3(double a, double b, double c) { return d3{a, b, c}; }
+__device__ __forceinline__ d3 add3(d3 a, d3 b) { return mk3(a.x + b.x, a.y + b.y, a.z + b.z); }
+__device__ __forceinline__ d3 sub3(d3 a, d3 b) { return mk3(a.x - b.x, a.y - b.y, a.z - b.z); }
+__device__ __forceinline__ d3 scl3(double s, d3 a) { return mk3(s * a.x, s * a.y, s * a.z); }
+__device__ __forceinline__ d3 div3(d3 a, double s) { return mk3(a.x / s, a.y / s, a.z / s); }
+__device__ __forceinline__ d3 neg3(d3 a) { return mk3(-a.x, -a.y, -a.z); }
+// Eigen 3.4 vectorised redux over 3 coefficients: (e0 + e1) + e2
+__device__ __forceinline__ double dot3(d3 a, d3 b) { return (a.x * b.x + a.y * b.y) + a.z * b.z; }
+__device__ __forceinline__ double sqn3(d3 a) { return dot3(a, a); }
+__device__ __forceinline__ d3 cross3(d3 a, d3 b) {
+  return mk3(a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x);
+}
+__device__ __forceinline__ d3 normalized3(d3 a) {
+  const double z = sqn3(a);
+  return z > 0.0 ? div3(a, sqrt(z)) : a;
+}
+// types.hpp:43-52
+__device__ __forceinline__ d3 orient_up(d3 n, d3 up) {
+  const double d = dot3(n, up);
+  if (d < 0.0) return neg3(n);
+  if (d > 0.0) return n;
+  if (n.x > 0.0) return n;
+  if (n.x < 0.0) return neg3(n);
+  if (n.y > 0.0) return n;
+  if (n.y < 0.0) return neg3(n);
+  if (n.z > 0.0) return n;
+  if (n.z < 0.0) return neg3(n);
+  return n;
+}
+
+// Pose::apply (types.hpp:31): R * p (rows 0,1 packet order, row 2 halving
+// order; Eigen 3.4 lazy product) then + t.
+__device__ __forceinline__ d3 pose_apply(const double* R, const double* t, double px, double py,
+                                         double pz) {
+  const double q0 = (R[0] * px + R[1] * py) + R[2] * pz;
+  const double q1 = (R[3] * px + R[4] * py) + R[5] * pz;
+  const double q2 = R[6] * px + (R[7] * py + R[8] * pz);
+  return mk3(q0 + t[0], q1 + t[1], q2 + t[2]);
+}
+
+__device__ __forceinline__ bool finite3(d3 p) {
+  return isfinite(p.x) && isfinite(p.y) && isfinite(p.z);
+}
+
+// voxel_grid.cpp:31-35
+__device__ __forceinline__ int w2i(double p, double o, double res) {
+  return static_cast<int>(floor((p - o) / res));
+}
+
+// Symmetric 3x3 cyclic Jacobi (jacobi.cpp:13-81), register resident.
+struct Eig3 {
+  double val[3];
+  d3 vec[3];  // column k
+};
+
+__device__ __forceinline__ void jacobi_rotate(double a[3][3], double v[3][3], int p, int q) {
+  const double apq = a[p][q];
+  if (apq == 0.0) return;
+  const double theta = (a[q][q] - a[p][p]) / (2.0 * apq);
+  const double t = copysign(1.0, theta) / (fabs(theta) + sqrt(theta * theta + 1.0));
+  const double c = 1.0 / sqrt(t * t + 1.0);
+  const double s = t * c;
+  const double app = a[p][p], aqq = a[q][q];
+  a[p][p] = app - t * apq;
+  a[q][q] = aqq + t * apq;
+  a[p][q] = 0.0;
+  a[q][p] = 0.0;
+  const int r = 3 - p - q;
+  const double arp = a[r][p], arq = a[r][q];
+  a[r][p] = a[p][r] = c * arp - s * arq;
+  a[r][q] = a[q][r] = s * arp + c * arq;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const double vip = v[i][p], viq = v[i][q];
+    v[i][p] = c * vip - s * viq;
+    v[i][q] = s * vip + c * viq;
+  }
+}
+
+__device__ __forceinline__ Eig3 jacobi3(const double in[3][3]) {
+  double a[3][3];
+  a[0][0] = in[0][0];
+  a[0][1] = 0.5 * (in[0][1] + in[1][0]);
+  a[0][2] = 0.5 * (in[0][2] + in[2][0]);
+  a[1][1] = in[1][1];
+  a[1][2] = 0.5 * (in[1][2] + in[2][1]);
+  a[2][2] = in[2][2];
+  a[1][0] = a[0][1];
+  a[2][0] = a[0][2];
+  a[2][1] = a[1][2];
+  double v[3][3] = {{1.0, 0.0, 0.0}, {0.0, 1.0, 0.0}, {0.0, 0.0, 1.0}};
+  for (int sweep = 0; sweep < 30; ++sweep) {
+    const double off =
+        sqrt(2.0 * (a[0][1] * a[0][1] + a[0][2] * a[0][2] + a[1][2] * a[1][2]));
+    if (!(off >= 1e-10)) break;
+    jacobi_rotate(a, v, 0, 1);
+    jacobi_rotate(a, v, 0, 2);
+    jacobi_rotate(a, v, 1, 2);
+  }
+  const double ev[3] = {a[0][0], a[1][1], a[2][2]};
+  int o[3] = {0, 1, 2};
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = i + 1; j < 3; ++j)
+      if (ev[o[j]] < ev[o[i]]) {
+        const int s = o[i];
+        o[i] = o[j];
+        o[j] = s;
+      }
+  Eig3 r;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    r.val[k] = ev[o[k]];
+    r.vec[k] = mk3(v[0][o[k]], v[1][o[k]], v[2][o[k]]);
+  }
+  // determinant of [vec0 vec1 vec2] (bruteforce_det3_helper order)
+  const double m00 = r.vec[0].x, m01 = r.vec[1].x, m02 = r.vec[2].x;
+  const double m10 = r.vec[0].y, m11 = r.vec[1].y, m12 = r.vec[2].y;
+  const double m20 = r.vec[0].z, m21 = r.vec[1].z, m22 = r.vec[2].z;
+  const double det = m00 * (m11 * m22 - m12 * m21) - m10 * (m01 * m22 - m02 * m21) +
+                     m20 * (m01 * m12 - m02 * m11);
+  if (det < 0.0) r.vec[2] = neg3(r.vec[2]);
+  return r;
+}
+
+// ------------------------------------------------------------ grid helpers
+__device__ __forceinline__ uint64_t phys_index(const GridDesc& g, const int32_t* off, int x, int y,
+                                               int z) {
+  int px = x + off[0];
+  if (px >= g.ex) px -= g.ex;
+  int py = y + off[1];
+  if (py >= g.ey) py -= g.ey;
+  int pz = z + off[2];
+  if (pz >= g.ez) pz -= g.ez;
+  return (static_cast<uint64_t>(px) * g.ey + py) * g.ez + pz;
+}
+
+__device__ __forceinline__ uint64_t word_of(const GridDesc& g, int x, int y, int z) {
+  return (static_cast<uint64_t>(x) * g.ey + y) * g.W + (z >> 5);
+}
+
+__device__ __forceinline__ bool in_bounds(const GridDesc& g, int x, int y, int z) {
+  return x >= 0 && y >= 0 && z >= 0 && x < g.ex && y < g.ey && z < g.ez;
+}
+
+// ------------------------------------------------------------ warp helpers
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Warp-aggregated atomicAdd of a per-lane value to one counter (all lanes
+// of the warp must call it).
+__device__ __forceinline__ void warp_add_u64(unsigned long long* c, unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if (lane_id() == 0 && v) atomicAdd(c, v);
+}
+
+__device__ __forceinline__ uint32_t hash_u32(uint32_t k) {
+  k ^= k >> 16;
+  k *= 0x7feb352dU;
+  k ^= k >> 15;
+  k *= 0x846ca68bU;
+  k ^= k >> 16;
+  return k;
+}
+
+// CounterRng (rng.hpp:13-64): splitmix64 keyed stream, integer only.
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+struct CounterRng {
+  uint64_t s;
+  __device__ __forceinline__ CounterRng(uint64_t seed, uint64_t k1, uint64_t k2) {
+    s = mix64(seed + 0x9e3779b97f4a7c15ULL);
+    s = mix64(s ^ mix64(k1 + 0xbf58476d1ce4e5b9ULL));
+    s = mix64(s ^ mix64(k2 + 0x94d049bb133111ebULL));
+  }
+  __device__ __forceinline__ uint64_t next() {
+    s += 0x9e3779b97f4a7c15ULL;
+    return mix64(s);
+  }
+  // (unsigned __int128(x) * n) >> 64
+  __device__ __forceinline__ uint32_t below(uint32_t n) {
+    return static_cast<uint32_t>(__umul64hi(next(), static_cast<uint64_t>(n)));
+  }
+};
+
+}  // namespace vp

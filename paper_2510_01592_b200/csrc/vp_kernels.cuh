@@ -1,0 +1,205 @@
+// Kernel declarations and block-level primitives.
+#pragma once
+
+#include <math_constants.h>
+
+#include "vp_device.cuh"
+
+namespace vp {
+
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 8;
+constexpr int kScanPerBlock = kScanThreads * kScanItems;  // 2048
+constexpr int kClusterBins = 2048;  // clusters handled by the counting sort per pass
+constexpr int kChunk = 2048;        // ordinals per counting-sort chunk
+constexpr int kHullSmem = 4096;     // survivors sorted in shared memory
+
+// Block-wide exclusive prefix sum (any blockDim multiple of 32, <= 1024).
+__device__ __forceinline__ uint32_t block_exclusive_u32(uint32_t v) {
+  __shared__ uint32_t wt[32];
+  const unsigned lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+  const unsigned nw = (blockDim.x + 31) >> 5;
+  uint32_t incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (static_cast<int>(lane) >= o) incl += t;
+  }
+  if (lane == 31) wt[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    uint32_t t = lane < nw ? wt[lane] : 0u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, t, o);
+      if (static_cast<int>(lane) >= o) t += u;
+    }
+    wt[lane] = t;
+  }
+  __syncthreads();
+  const uint32_t r = (wid ? wt[wid - 1] : 0u) + incl - v;
+  __syncthreads();
+  return r;
+}
+
+__device__ __forceinline__ uint32_t block_sum_u32(uint32_t v) {
+  __shared__ uint32_t ws[32];
+  __shared__ uint32_t tot;
+  const unsigned lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+  const unsigned nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if (lane == 0) ws[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    uint32_t t = lane < nw ? ws[lane] : 0u;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
+    if (lane == 0) tot = t;
+  }
+  __syncthreads();
+  const uint32_t r = tot;
+  __syncthreads();
+  return r;
+}
+
+// Segmentation parameters resolved on the host (thresholds computed with the
+// host libm exactly as the reference computes them).
+struct SegDev {
+  int radius;          // SegmentationParams.neighbor_radius
+  int min_neighbors;
+  double dstar;        // smallest d with acos(d)*kRadToDeg <= max_angle_deg (host libm)
+  d3 up;
+  int w;               // max(1, ceil(distance_th / resolution))   segmentation.cpp:89
+  double d2_th;        // distance_th^2                             segmentation.cpp:90
+  double cos_th;       // cos(adjacency_angle_deg * kDegToRad)      segmentation.cpp:91
+  int min_cluster;     // min_cluster_size
+};
+
+struct RansacDev {
+  int iterations;
+  double eps;
+  uint64_t seed;
+  d3 up;
+};
+
+// Dense ordinal lookup volume for the CCL window search (segmentation.cpp:96-110):
+// the grid's logical extent on the fused path, the steppable bounding box for a
+// host-provided list.
+struct MapDesc {
+  int32_t* map;
+  int lo[3];
+  int dims[3];
+  __device__ __forceinline__ uint64_t slot(int x, int y, int z) const {
+    return (static_cast<uint64_t>(x - lo[0]) * dims[1] + (y - lo[1])) * dims[2] + (z - lo[2]);
+  }
+};
+
+// Buffers of the segmentation stage.
+struct SegBufs {
+  // occupied list (Vcap)
+  uint32_t* occ_list;
+  double* est_normal;    // 3*Vcap
+  int32_t* est_ncount;
+  uint8_t* est_valid;
+  double* own_mean;      // 3*Vcap
+  uint32_t* own_count;
+  uint8_t* own_status;
+  uint8_t* step_flag;
+  uint32_t* step_pos;
+  // steppable (Scap)
+  int32_t* st_idx;       // 3*Scap window indices
+  double* st_mean;       // 3*Scap
+  double* st_normal;     // 3*Scap
+  int32_t* parent;       // union-find
+  int32_t* label;        // canonical labels
+  uint32_t* cnt;         // members per root
+  int32_t* cid;          // cluster index of a big root, else -1
+  uint8_t* big_flag;
+  uint32_t* big_pos;
+  // clusters (kClusterBins)
+  int32_t* klabel;       // cluster label (= root ordinal)
+  uint32_t* ksize;
+  uint32_t* kpoff;       // K+1 warp-padded member offsets
+  uint32_t* H;           // K x nchunks histogram / offsets
+  // members (padded, Mcap)
+  double* mx;
+  double* my;
+  double* mz;
+  // RANSAC candidates (kClusterBins x iterations)
+  double* cand;          // 4 per candidate: n.x n.y n.z offset
+  int32_t* cand_cnt;     // -1 degenerate
+  int32_t* win_it;       // per cluster: winner, -1 unfit, -2 skipped small
+  int32_t* win_cnt;
+  int32_t* fid;          // fit index of a cluster or -1
+  uint32_t* fit_cluster; // cluster of a fit
+  uint32_t* ioff;        // per fit inlier offsets (nfits+1)
+  double* fit_model;     // 4 per fit (normal, offset): RANSAC winner
+  int32_t* fit_meta;     // 2 per fit (inlier_count, label)
+  double* ref_model;     // 4 per fit: refined
+  double* inl;           // 3 * Icap inliers (fit order)
+  double* proj;          // 2 * Icap
+  double* surv;          // 2 * 2Icap
+  double* hull;          // 2 * 2Icap
+  // polygon records (kClusterBins) + vertex pool
+  double* prec_d;        // 8 per fit: normal(3) offset area
+  int32_t* prec_i;       // 4 per fit: inlier_count label nv voff
+  double* pool;          // 5 per vertex: u v x y z
+  uint32_t pool_cap;
+  uint32_t Vcap, Scap, Mcap, Icap;
+};
+
+// ---- kernels (k_map.cu)
+__global__ void k_integrate_hash(GridDesc g, const FrameParams* fp, Counters* ctr, uint32_t* hkey,
+                                 uint32_t* hcnt, uint32_t hmask, uint32_t* groups, uint32_t* pslot,
+                                 uint32_t* prank);
+__global__ void k_integrate_offsets(Counters* ctr, const uint32_t* groups, const uint32_t* hcnt,
+                                    uint32_t* hoff);
+__global__ void k_integrate_scatter(const FrameParams* fp, const uint32_t* pslot,
+                                    const uint32_t* prank, const uint32_t* hoff, uint32_t* sorted);
+__global__ void k_integrate_fold(GridDesc g, const FrameParams* fp, Counters* ctr,
+                                 const uint32_t* groups, uint32_t* hkey, uint32_t* hcnt,
+                                 const uint32_t* hoff, uint32_t* sorted);
+__global__ void k_clear_walk(GridDesc g, const FrameParams* fp);
+__global__ void k_clear_apply(GridDesc g, const FrameParams* fp, Counters* ctr);
+__global__ void k_recenter(GridDesc g, const FrameParams* fp, Counters* ctr);
+__global__ void k_map_finalize(Counters* ctr);
+__global__ void k_bitmap_count(const uint32_t* bits, uint64_t nwords, uint32_t* bsum);
+__global__ void k_bitmap_emit(const uint32_t* bits, uint64_t nwords, int W, int ez,
+                              const uint32_t* boff, uint32_t* out, uint32_t cap);
+__global__ void k_flags_count(const uint8_t* flags, const uint32_t* n_ptr, uint32_t cap,
+                              uint32_t* bsum);
+__global__ void k_flags_positions(const uint8_t* flags, const uint32_t* n_ptr, uint32_t cap,
+                                  const uint32_t* boff, uint32_t* pos_out);
+__global__ void k_merge_point(GridDesc g, const FrameParams* fp, Counters* ctr, int x, int y, int z,
+                              double px, double py, double pz);
+__global__ void k_scan_exclusive(uint32_t* a, uint32_t n_static, const uint32_t* n_ptr,
+                                 uint32_t* total, uint32_t* total2);
+
+// ---- kernels (k_segment.cu)
+__global__ void k_normals(GridDesc g, const FrameParams* fp, Counters* ctr, SegDev sp, SegBufs b,
+                          int write_status);
+__global__ void k_adjacency(Counters* ctr, SegDev sp, SegBufs b, MapDesc m, const uint64_t* rows,
+                            uint32_t* counts, int32_t* cols);
+__global__ void k_step_emit(GridDesc g, Counters* ctr, SegBufs b, MapDesc m);
+__global__ void k_map_fill(Counters* ctr, SegBufs b, MapDesc m);
+__global__ void k_occ_gather(GridDesc g, const FrameParams* fp, Counters* ctr, SegBufs b);
+__global__ void k_ccl_init(Counters* ctr, SegBufs b);
+__global__ void k_ccl_union(Counters* ctr, SegDev sp, SegBufs b, MapDesc m);
+__global__ void k_ccl_flatten(Counters* ctr, SegBufs b, MapDesc m);
+__global__ void k_cluster_flags(Counters* ctr, SegDev sp, SegBufs b);
+__global__ void k_cluster_assign(Counters* ctr, SegBufs b);
+__global__ void k_cluster_setup(Counters* ctr, SegBufs b);
+__global__ void k_member_hist(Counters* ctr, SegBufs b, uint32_t hstride);
+__global__ void k_member_hscan(Counters* ctr, SegBufs b, uint32_t hstride);
+__global__ void k_member_scatter(Counters* ctr, SegBufs b, uint32_t hstride);
+__global__ void k_ransac_hyp(Counters* ctr, RansacDev rp, SegBufs b);
+__global__ void k_ransac_count(Counters* ctr, RansacDev rp, SegBufs b);
+__global__ void k_ransac_select(Counters* ctr, RansacDev rp, SegBufs b);
+__global__ void k_fit_setup(Counters* ctr, RansacDev rp, SegBufs b);
+__global__ void k_ransac_extract(Counters* ctr, RansacDev rp, SegBufs b);
+__global__ void k_refine(Counters* ctr, SegBufs b, d3 up, int refine, int exact);
+__global__ void k_polygon(Counters* ctr, SegBufs b, const double* dirtab, int directions,
+                          double min_area);
+
+}  // namespace vp

@@ -189,6 +189,25 @@ class Pipeline:
                                       C.byref(out) if want_polygons else None, C.byref(tm)))
         return (polygons_to_py(out) if want_polygons else None), tm
 
+    def frame_ptr(self, pts_host_ptr: int, n: int, R, t, want_polygons=True):
+        """vp_pipeline_frame on a raw host pointer (e.g. pinned memory)."""
+        R, t = _pose(R, t)
+        out = C.POINTER(Polygons)()
+        tm = FrameTiming()
+        check(lib().vp_pipeline_frame(self.h, C.c_void_p(pts_host_ptr), C.c_uint64(n),
+                                      _p(R, C.c_double), _p(t, C.c_double),
+                                      C.byref(out) if want_polygons else None, C.byref(tm)))
+        return (polygons_to_py(out) if want_polygons else None), tm
+
+    def reset(self, start_center):
+        c = np.ascontiguousarray(start_center, np.float64)
+        check(lib().vp_pipeline_reset(self.h, _p(c, C.c_double)))
+
+    def counters(self):
+        out = np.zeros(16, np.uint64)
+        check(lib().vp_pipeline_counters(self.h, _p(out, C.c_uint64)))
+        return out
+
     def frame_device(self, pts_dev_ptr: int, n: int, R, t, want_polygons=False):
         R, t = _pose(R, t)
         out = C.POINTER(Polygons)()

@@ -1,0 +1,164 @@
+"""GPU tier: the B200 pipeline against the CPU oracle, stage by stage.
+
+Bit-exact bar (integer / index / FP64-ordered work): occupancy, sums, counts,
+statuses, occupied list, normals, steppable list, canonical labels, clusters,
+RANSAC candidates / winners / inlier sets. With refine_exact the refine sums are
+sequential too, so the whole trace (and the golden files) must be byte-equal.
+With the default tree-reduced refine the tolerance of north_star applies:
+plane normals within 1e-4 rad, offsets within 1e-4 m, hull vertices within
+1e-5 m (symmetric Hausdorff).
+"""
+import numpy as np
+import pytest
+
+from cpu_oracles import CpuSession
+from paper_2510_01592_b200 import native, scenes
+from paper_2510_01592_b200.trace import format_polygons, parse_trace
+from workloads import golden_text, run_config
+
+pytestmark = pytest.mark.gpu
+
+NORMAL_TOL = 1e-4   # rad
+OFFSET_TOL = 1e-4   # m
+VERTEX_TOL = 1e-5   # m
+
+
+def sessions(name_or_frames, res=None, ext=None, seed=None, exact=True, params=None):
+    if isinstance(name_or_frames, str):
+        frames, res, ext, seed, _ = run_config(name_or_frames)
+    else:
+        frames = name_or_frames
+    p = params or native.default_params(seed=seed, refine_exact=exact)
+    gpu = native.Pipeline(res, ext, frames[0].translation, p)
+    ora = CpuSession("oracle", res, ext, frames[0].translation, p)
+    return frames, gpu, ora
+
+
+def diff_sections(a, b):
+    """Names of trace fields that differ (for diagnostics)."""
+    out = []
+    for k in ("cleared", "freed", "touched", "discarded", "recentered", "shift", "dropped", "origin",
+              "occupied_count", "skipped", "unfit"):
+        if getattr(a, k) != getattr(b, k):
+            out.append(f"{k}: gpu={getattr(a, k)} oracle={getattr(b, k)}")
+    for k in ("occ_idx", "occ_mean", "occ_count", "occ_status", "normal", "ncount", "valid", "st_idx",
+              "st_mean", "st_normal", "labels"):
+        x, y = getattr(a, k), getattr(b, k)
+        if x.shape != y.shape:
+            out.append(f"{k}: shape {x.shape} vs {y.shape}")
+        elif x.tobytes() != y.tobytes():
+            bad = np.nonzero((x != y).reshape(len(x), -1).any(axis=1))[0]
+            out.append(f"{k}: {len(bad)} rows differ, first {bad[:5].tolist()}")
+    if a.clusters != b.clusters:
+        out.append(f"clusters: {a.clusters[:6]} vs {b.clusters[:6]}")
+    if len(a.fits) != len(b.fits):
+        out.append(f"fits: {len(a.fits)} vs {len(b.fits)}")
+    else:
+        for i, (x, y) in enumerate(zip(a.fits, b.fits)):
+            if (x["inlier_count"], x["label"]) != (y["inlier_count"], y["label"]) or \
+                    x["normal"].tobytes() != y["normal"].tobytes() or x["offset"] != y["offset"] or \
+                    x["inliers"].tobytes() != y["inliers"].tobytes():
+                out.append(f"fit {i} differs")
+    return out
+
+
+def check_bit_exact(frames, gpu, ora):
+    for i, f in enumerate(frames):
+        a = gpu.frame_trace_raw(f.points, f.rotation, f.translation)
+        b = ora.frame_raw(f.points, f.rotation, f.translation)
+        if a != b:
+            d = diff_sections(parse_trace(a), parse_trace(b))
+            pytest.fail(f"frame {i}: trace differs: {d}")
+    return parse_trace(a)
+
+
+@pytest.mark.parametrize("name", ["t1", "smallobs"])
+def test_trace_bit_exact_and_golden(name):
+    frames, gpu, ora = sessions(name)
+    last = check_bit_exact(frames, gpu, ora)
+    assert format_polygons(last.polygons) == golden_text(run_config(name)[4])
+
+
+@pytest.mark.parametrize("name", ["stair", "rosette"])
+def test_golden_files_reproduced(name):
+    frames, res, ext, seed, run = run_config(name)
+    gpu = native.Pipeline(res, ext, frames[0].translation, native.default_params(seed=seed, refine_exact=True))
+    polys = None
+    for f in frames:
+        polys, _ = gpu.frame(f.points, f.rotation, f.translation)
+    assert format_polygons(polys) == golden_text(run)
+
+
+def test_stair_every_stage_bit_exact():
+    frames, gpu, ora = sessions("stair")
+    check_bit_exact(frames[:12], gpu, ora)
+
+
+def hausdorff(a, b):
+    d = np.linalg.norm(a[:, None, :] - b[None, :, :], axis=2)
+    return max(d.min(axis=1).max(), d.min(axis=0).max())
+
+
+def check_tolerance(ta, tb):
+    # everything up to the RANSAC fits is bit-exact in either refine mode
+    assert diff_sections(ta, tb) == []
+    for (na, oa), (nb, ob) in zip(ta.refined, tb.refined):
+        ang = np.arccos(np.clip(np.dot(na, nb), -1.0, 1.0))
+        assert ang <= NORMAL_TOL and abs(oa - ob) <= OFFSET_TOL
+    assert [(p["label"], p["inlier_count"]) for p in ta.polygons] == \
+           [(p["label"], p["inlier_count"]) for p in tb.polygons]
+    for pa, pb in zip(ta.polygons, tb.polygons):
+        assert hausdorff(pa["v3d"], pb["v3d"]) <= VERTEX_TOL
+        assert abs(pa["area"] - pb["area"]) <= 1e-4 * max(1.0, pb["area"])
+
+
+@pytest.mark.parametrize("name", ["t1", "stair"])
+def test_tree_refine_within_tolerance(name):
+    frames, gpu, ora = sessions(name, exact=False)
+    for f in frames:
+        ta = gpu.frame_trace(f.points, f.rotation, f.translation)
+        tb = ora.frame(f.points, f.rotation, f.translation)
+        check_tolerance(ta, tb)
+
+
+def test_stepping_stones_reduced_window_bit_exact():
+    # C2 scene and sensor, 0.01 m, a 240^3 window so the oracle stays fast
+    wl = scenes.workload("c2", frames=8)
+    frames, gpu, ora = sessions(wl.frames, 0.01, (240, 240, 240), 2025)
+    last = check_bit_exact(frames, gpu, ora)
+    assert len(last.polygons) >= 2
+
+
+def test_c2_full_size_first_frames_bit_exact():
+    # BASELINE configs[1] at its full 500^3 window: first frames vs the oracle
+    wl = scenes.workload("c2", frames=30)
+    frames, gpu, ora = sessions(wl.frames[:3], 0.01, (500, 500, 500), 2025)
+    check_bit_exact(frames, gpu, ora)
+
+
+def test_c2_full_stream_properties_and_determinism():
+    # size-independent properties over the whole 30-frame stream at 500^3:
+    # run-to-run bitwise determinism, label canonicality, polygon invariants.
+    wl = scenes.workload("c2")
+    p = native.default_params(seed=2025)
+    runs = []
+    for _ in range(2):
+        gpu = native.Pipeline(0.01, (500, 500, 500), wl.frames[0].translation, p)
+        traces = [gpu.frame_trace_raw(f.points, f.rotation, f.translation) for f in wl.frames]
+        runs.append(traces)
+        gpu.close()
+    assert runs[0] == runs[1]
+    t = parse_trace(runs[0][-1])
+    assert t.occupied_count == len(t.occ_idx)
+    flat = (t.occ_idx[:, 0].astype(np.int64) * 500 + t.occ_idx[:, 1]) * 500 + t.occ_idx[:, 2]
+    assert np.all(np.diff(flat) > 0)                    # lexicographic order
+    lab = t.labels
+    assert np.all(lab <= np.arange(len(lab)))           # label = component minimum ordinal
+    assert np.all(lab[lab] == lab)                      # roots are fixed points
+    labels = [p["label"] for p in t.polygons]
+    assert labels == sorted(labels) and len(labels) >= 6
+    for poly in t.polygons:
+        assert poly["area"] >= 0.002
+        v = poly["v2d"]
+        cr = np.cross(np.roll(v, -1, 0) - v, np.roll(v, -2, 0) - np.roll(v, -1, 0))
+        assert np.all(cr > 0)                           # strictly convex, CCW
