@@ -112,28 +112,82 @@ __global__ void k_integrate_scatter(const FrameParams* __restrict__ fp, const ui
   }
 }
 
-__global__ void k_integrate_fold(GridDesc g, const FrameParams* __restrict__ fp, Counters* ctr,
-                                 const uint32_t* groups, uint32_t* hkey, uint32_t* hcnt,
-                                 const uint32_t* hoff, uint32_t* sorted) {
+// One warp per touched voxel: the point indices are staged in shared memory,
+// ranked (indices are distinct, so rank = number of smaller indices), the
+// points are transformed in parallel, and lane 0 performs the reference's
+// sequential FP64 fold (voxel_grid.cpp:104-110) in ascending point index.
+constexpr int kFoldMax = 128;
+constexpr int kFoldWarps = 8;
+
+__device__ __forceinline__ void fold_cell(const GridDesc& g, const FrameParams* fp, uint32_t key,
+                                          const d3* w, uint32_t cnt, unsigned long long& fresh) {
+  const uint32_t z = key % static_cast<uint32_t>(g.ez);
+  const uint32_t r = key / static_cast<uint32_t>(g.ez);
+  const uint32_t y = r % static_cast<uint32_t>(g.ey);
+  const uint32_t x = r / static_cast<uint32_t>(g.ey);
+  Cell* c = g.cells + phys_index(g, fp->off_pre, x, y, z);
+  double sx = c->sx, sy = c->sy, sz = c->sz;
+  const uint32_t count = c->count;
+  for (uint32_t a = 0; a < cnt; ++a) {
+    sx += w[a].x;
+    sy += w[a].y;
+    sz += w[a].z;
+  }
+  c->sx = sx;
+  c->sy = sy;
+  c->sz = sz;
+  c->count = count + cnt;
+  c->status = 1;  // VoxelStatus::Occupied
+  if (count == 0) {
+    atomicOr(fp->occ_pre + word_of(g, x, y, z), 1u << (z & 31));
+    ++fresh;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_integrate_fold(GridDesc g, const FrameParams* __restrict__ fp,
+                                                        Counters* ctr, const uint32_t* groups,
+                                                        uint32_t* hkey, uint32_t* hcnt,
+                                                        const uint32_t* hoff, uint32_t* sorted) {
+  __shared__ uint32_t raw[kFoldWarps][kFoldMax];
+  __shared__ uint32_t srt[kFoldMax * kFoldWarps];
+  __shared__ d3 sw[kFoldWarps][kFoldMax];
   const uint32_t ng = ctr->ngroups;
+  const unsigned lane = lane_id(), wid = threadIdx.x >> 5;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarp = (gridDim.x * blockDim.x) >> 5;
   unsigned long long fresh = 0;
-  uint32_t* occ = fp->occ_pre;
-  for (uint32_t i0 = blockIdx.x * blockDim.x; i0 < ng; i0 += gridDim.x * blockDim.x) {
-    const uint32_t gi = i0 + threadIdx.x;
-    if (gi < ng) {
-      const uint32_t slot = groups[gi];
-      const uint32_t key = hkey[slot];
-      const uint32_t cnt = hcnt[slot];
-      uint32_t* lst = sorted + hoff[slot];
-      // ascending point index (ranks are lane-ordered, so this is ~linear)
+  for (uint32_t gi = warp; gi < ng; gi += nwarp) {
+    const uint32_t slot = groups[gi];
+    const uint32_t key = hkey[slot];
+    const uint32_t cnt = hcnt[slot];
+    uint32_t* lst = sorted + hoff[slot];
+    if (cnt <= static_cast<uint32_t>(kFoldMax)) {
+      for (uint32_t k = lane; k < cnt; k += 32) raw[wid][k] = lst[k];
+      __syncwarp();
+      for (uint32_t k = lane; k < cnt; k += 32) {
+        const uint32_t v = raw[wid][k];
+        uint32_t rank = 0;
+        for (uint32_t q = 0; q < cnt; ++q) rank += raw[wid][q] < v ? 1u : 0u;
+        srt[wid * kFoldMax + rank] = v;
+      }
+      __syncwarp();
+      for (uint32_t k = lane; k < cnt; k += 32) {
+        const float* p = fp->pts + 3 * static_cast<uint64_t>(srt[wid * kFoldMax + k]);
+        sw[wid][k] = pose_apply(fp->R, fp->t, static_cast<double>(p[0]), static_cast<double>(p[1]),
+                                static_cast<double>(p[2]));
+      }
+      __syncwarp();
+      if (lane == 0) fold_cell(g, fp, key, sw[wid], cnt, fresh);
+      __syncwarp();
+    } else if (lane == 0) {  // rare very dense voxel: in-place sort + streamed fold
       for (uint32_t a = 1; a < cnt; ++a) {
         const uint32_t v = lst[a];
-        uint32_t b = a;
-        while (b > 0 && lst[b - 1] > v) {
-          lst[b] = lst[b - 1];
-          --b;
+        uint32_t q = a;
+        while (q > 0 && lst[q - 1] > v) {
+          lst[q] = lst[q - 1];
+          --q;
         }
-        lst[b] = v;
+        lst[q] = v;
       }
       const uint32_t z = key % static_cast<uint32_t>(g.ez);
       const uint32_t r = key / static_cast<uint32_t>(g.ez);
@@ -141,8 +195,7 @@ __global__ void k_integrate_fold(GridDesc g, const FrameParams* __restrict__ fp,
       const uint32_t x = r / static_cast<uint32_t>(g.ey);
       Cell* c = g.cells + phys_index(g, fp->off_pre, x, y, z);
       double sx = c->sx, sy = c->sy, sz = c->sz;
-      uint32_t count = c->count;
-      const bool was_free = count == 0;
+      const uint32_t count = c->count;
       for (uint32_t a = 0; a < cnt; ++a) {
         const float* p = fp->pts + 3 * static_cast<uint64_t>(lst[a]);
         const d3 w = pose_apply(fp->R, fp->t, static_cast<double>(p[0]), static_cast<double>(p[1]),
@@ -150,17 +203,18 @@ __global__ void k_integrate_fold(GridDesc g, const FrameParams* __restrict__ fp,
         sx += w.x;
         sy += w.y;
         sz += w.z;
-        ++count;
       }
       c->sx = sx;
       c->sy = sy;
       c->sz = sz;
-      c->count = count;
-      c->status = 1;  // VoxelStatus::Occupied
-      if (was_free) {
-        atomicOr(occ + word_of(g, x, y, z), 1u << (z & 31));
+      c->count = count + cnt;
+      c->status = 1;
+      if (count == 0) {
+        atomicOr(fp->occ_pre + word_of(g, x, y, z), 1u << (z & 31));
         ++fresh;
       }
+    }
+    if (lane == 0) {
       hkey[slot] = kEmptyKey;
       hcnt[slot] = 0;
     }
@@ -175,85 +229,112 @@ __global__ void k_integrate_fold(GridDesc g, const FrameParams* __restrict__ fp,
 // cells next to the sensor from serialising on L2 atomics); k_clear_apply
 // then counts unique cells, frees occupied ones and zeroes the mask.
 // ---------------------------------------------------------------------------
-__global__ void k_clear_walk(GridDesc g, const FrameParams* __restrict__ fp) {
+// Mark one traversed interior cell. Lanes of a warp that step through the same
+// cell in the same iteration (adjacent pixels near the sensor) are merged with
+// __match_any_sync so only one fire-and-forget RED.OR per distinct cell is
+// issued; nothing in the loop waits on memory.
+__device__ __forceinline__ void mark_cell(const GridDesc& g, int x, int y, int z) {
+  const uint64_t w = word_of(g, x, y, z);
+  const unsigned active = __activemask();
+  const unsigned long long key = (w << 5) | static_cast<unsigned>(z & 31);
+  const unsigned peers = __match_any_sync(active, key);
+  if ((__ffs(peers) - 1) == static_cast<int>(lane_id())) atomicOr(g.clr + w, 1u << (z & 31));
+}
+
+__global__ void __launch_bounds__(256) k_clear_walk(GridDesc g, const FrameParams* __restrict__ fp) {
   const uint64_t n = fp->n;
   const double res = g.res;
-  const double* lo = fp->origin_pre;
-  double hi[3];
-  hi[0] = lo[0] + static_cast<double>(g.ex) * res;
-  hi[1] = lo[1] + static_cast<double>(g.ey) * res;
-  hi[2] = lo[2] + static_cast<double>(g.ez) * res;
-  const int ext[3] = {g.ex, g.ey, g.ez};
-  const d3 a = mk3(fp->t[0], fp->t[1], fp->t[2]);
-  const int oc0 = w2i(a.x, lo[0], res), oc1 = w2i(a.y, lo[1], res), oc2 = w2i(a.z, lo[2], res);
+  const double lo0 = fp->origin_pre[0], lo1 = fp->origin_pre[1], lo2 = fp->origin_pre[2];
+  const double hi0 = lo0 + static_cast<double>(g.ex) * res;
+  const double hi1 = lo1 + static_cast<double>(g.ey) * res;
+  const double hi2 = lo2 + static_cast<double>(g.ez) * res;
+  const double a0 = fp->t[0], a1 = fp->t[1], a2 = fp->t[2];
+  const int oc0 = w2i(a0, lo0, res), oc1 = w2i(a1, lo1, res), oc2 = w2i(a2, lo2, res);
   const int max_steps = g.ex + g.ey + g.ez + 4;
   for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const float* pp = fp->pts + 3 * i;
-    const d3 b = pose_apply(fp->R, fp->t, static_cast<double>(pp[0]), static_cast<double>(pp[1]),
-                            static_cast<double>(pp[2]));
-    if (!finite3(b)) continue;
-    const double d[3] = {b.x - a.x, b.y - a.y, b.z - a.z};
-    const double av[3] = {a.x, a.y, a.z};
+    const d3 bw = pose_apply(fp->R, fp->t, static_cast<double>(pp[0]), static_cast<double>(pp[1]),
+                             static_cast<double>(pp[2]));
+    if (!finite3(bw)) continue;
+    const double d0 = bw.x - a0, d1 = bw.y - a1, d2 = bw.z - a2;
+    // clip [t0, t1] to the window (voxel_grid.cpp:130-142)
     double t0 = 0.0, t1 = 1.0;
     bool skip = false;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      if (d[k] == 0.0) {
-        if (av[k] < lo[k] || av[k] >= hi[k]) skip = true;
-        continue;
-      }
-      double ta = (lo[k] - av[k]) / d[k];
-      double tb = (hi[k] - av[k]) / d[k];
-      if (ta > tb) {
-        const double s = ta;
-        ta = tb;
-        tb = s;
-      }
-      t0 = (t0 < ta) ? ta : t0;  // std::max(t0, ta)
-      t1 = (tb < t1) ? tb : t1;  // std::min(t1, tb)
-      if (t0 > t1) skip = true;
-      if (skip) break;
+#define VP_CLIP(dk, ak, lok, hik)                         \
+    if (!skip) {                                         \
+      if (dk == 0.0) {                                   \
+        if (ak < lok || ak >= hik) skip = true;          \
+      } else {                                           \
+        double ta = (lok - ak) / dk;                     \
+        double tb = (hik - ak) / dk;                     \
+        if (ta > tb) {                                   \
+          const double sw = ta;                          \
+          ta = tb;                                       \
+          tb = sw;                                       \
+        }                                                \
+        t0 = (t0 < ta) ? ta : t0;                        \
+        t1 = (tb < t1) ? tb : t1;                        \
+        if (t0 > t1) skip = true;                        \
+      }                                                  \
     }
+    VP_CLIP(d0, a0, lo0, hi0)
+    VP_CLIP(d1, a1, lo1, hi1)
+    VP_CLIP(d2, a2, lo2, hi2)
+#undef VP_CLIP
     if (skip) continue;
-    const int ec0 = w2i(b.x, lo[0], res), ec1 = w2i(b.y, lo[1], res), ec2 = w2i(b.z, lo[2], res);
-    const double entry[3] = {av[0] + t0 * d[0], av[1] + t0 * d[1], av[2] + t0 * d[2]};
-    int cell[3];
-    int step[3];
-    double tmax[3], tdelta[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      int c = w2i(entry[k], lo[k], res);
-      c = c < 0 ? 0 : (ext[k] - 1 < c ? ext[k] - 1 : c);  // std::clamp
-      cell[k] = c;
-      step[k] = 0;
-      tmax[k] = CUDART_INF;
-      tdelta[k] = CUDART_INF;
-      if (d[k] > 0.0) {
-        step[k] = 1;
-        tmax[k] = t0 + (lo[k] + static_cast<double>(c + 1) * res - entry[k]) / d[k];
-        tdelta[k] = res / d[k];
-      } else if (d[k] < 0.0) {
-        step[k] = -1;
-        tmax[k] = t0 + (lo[k] + static_cast<double>(c) * res - entry[k]) / d[k];
-        tdelta[k] = res / -d[k];
-      }
+    const int ec0 = w2i(bw.x, lo0, res), ec1 = w2i(bw.y, lo1, res), ec2 = w2i(bw.z, lo2, res);
+    const double e0 = a0 + t0 * d0, e1 = a1 + t0 * d1, e2 = a2 + t0 * d2;
+    int c0 = w2i(e0, lo0, res), c1 = w2i(e1, lo1, res), c2 = w2i(e2, lo2, res);
+    c0 = c0 < 0 ? 0 : (g.ex - 1 < c0 ? g.ex - 1 : c0);  // std::clamp
+    c1 = c1 < 0 ? 0 : (g.ey - 1 < c1 ? g.ey - 1 : c1);
+    c2 = c2 < 0 ? 0 : (g.ez - 1 < c2 ? g.ez - 1 : c2);
+    int s0 = 0, s1 = 0, s2 = 0;
+    double tm0 = CUDART_INF, tm1 = CUDART_INF, tm2 = CUDART_INF;
+    double td0 = CUDART_INF, td1 = CUDART_INF, td2 = CUDART_INF;
+#define VP_INIT(dk, ck, lok, ek, sk, tmk, tdk)                                        \
+    if (dk > 0.0) {                                                                   \
+      sk = 1;                                                                         \
+      tmk = t0 + (lok + static_cast<double>(ck + 1) * res - ek) / dk;                 \
+      tdk = res / dk;                                                                 \
+    } else if (dk < 0.0) {                                                            \
+      sk = -1;                                                                        \
+      tmk = t0 + (lok + static_cast<double>(ck) * res - ek) / dk;                     \
+      tdk = res / -dk;                                                                \
     }
+    VP_INIT(d0, c0, lo0, e0, s0, tm0, td0)
+    VP_INIT(d1, c1, lo1, e1, s1, tm1, td1)
+    VP_INIT(d2, c2, lo2, e2, s2, tm2, td2)
+#undef VP_INIT
     for (int s = 0; s < max_steps; ++s) {
-      const bool is_o = cell[0] == oc0 && cell[1] == oc1 && cell[2] == oc2;
-      const bool is_e = cell[0] == ec0 && cell[1] == ec1 && cell[2] == ec2;
-      if (!is_o && !is_e) {
-        uint32_t* wp = g.clr + word_of(g, cell[0], cell[1], cell[2]);
-        const uint32_t bit = 1u << (cell[2] & 31);
-        if (!(__ldcg(wp) & bit)) atomicOr(wp, bit);
-      }
+      const bool is_o = c0 == oc0 && c1 == oc1 && c2 == oc2;
+      const bool is_e = c0 == ec0 && c1 == ec1 && c2 == ec2;
+      if (!is_o && !is_e) mark_cell(g, c0, c1, c2);
+      // m = argmin t_max, ties to the lower axis (voxel_grid.cpp:170-172)
       int m = 0;
-      if (tmax[1] < tmax[m]) m = 1;
-      if (tmax[2] < tmax[m]) m = 2;
-      if (tmax[m] >= t1) break;
-      cell[m] += step[m];
-      if (cell[m] < 0 || cell[m] >= ext[m]) break;
-      tmax[m] += tdelta[m];
+      double tm = tm0;
+      if (tm1 < tm) {
+        m = 1;
+        tm = tm1;
+      }
+      if (tm2 < tm) {
+        m = 2;
+        tm = tm2;
+      }
+      if (tm >= t1) break;
+      if (m == 0) {
+        c0 += s0;
+        if (c0 < 0 || c0 >= g.ex) break;
+        tm0 += td0;
+      } else if (m == 1) {
+        c1 += s1;
+        if (c1 < 0 || c1 >= g.ey) break;
+        tm1 += td1;
+      } else {
+        c2 += s2;
+        if (c2 < 0 || c2 >= g.ez) break;
+        tm2 += td2;
+      }
     }
   }
 }
@@ -381,7 +462,8 @@ __global__ void k_map_finalize(Counters* ctr) {
 // bitmap (x, y, z lexicographic) into logical flat indices.
 // 256 threads x 8 words per block.
 // ---------------------------------------------------------------------------
-__global__ void k_bitmap_count(const uint32_t* __restrict__ bits, uint64_t nwords, uint32_t* bsum) {
+__global__ void k_bitmap_count(const FrameParams* __restrict__ fp, uint64_t nwords, uint32_t* bsum) {
+  const uint32_t* __restrict__ bits = fp->occ_post;
   const uint64_t w0 = (static_cast<uint64_t>(blockIdx.x) * kScanThreads + threadIdx.x) * kScanItems;
   uint32_t c = 0;
 #pragma unroll
@@ -391,8 +473,9 @@ __global__ void k_bitmap_count(const uint32_t* __restrict__ bits, uint64_t nword
   if (threadIdx.x == 0) bsum[blockIdx.x] = c;
 }
 
-__global__ void k_bitmap_emit(const uint32_t* __restrict__ bits, uint64_t nwords, int W, int ez,
+__global__ void k_bitmap_emit(const FrameParams* __restrict__ fp, uint64_t nwords, int W, int ez,
                               const uint32_t* boff, uint32_t* out, uint32_t cap) {
+  const uint32_t* __restrict__ bits = fp->occ_post;
   const uint64_t w0 = (static_cast<uint64_t>(blockIdx.x) * kScanThreads + threadIdx.x) * kScanItems;
   uint32_t v[kScanItems];
   uint32_t c = 0;

@@ -124,14 +124,18 @@ __global__ void k_step_emit(GridDesc g, Counters* ctr, SegBufs b, MapDesc m) {
       b.st_normal[3 * s + k] = b.est_normal[3 * v + k];
     }
     m.map[m.slot(x, y, z)] = static_cast<int32_t>(s);
+    atomicOr(m.bits + m.word(x, y, z), 1u << ((z - m.lo[2]) & 31));
   }
 }
 
 // Host-provided steppable list (vp_label_components): fill the map only.
 __global__ void k_map_fill(Counters* ctr, SegBufs b, MapDesc m) {
   const uint32_t S = min(ctr->S, b.Scap);
-  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < S; s += gridDim.x * blockDim.x)
-    m.map[m.slot(b.st_idx[3 * s], b.st_idx[3 * s + 1], b.st_idx[3 * s + 2])] = static_cast<int32_t>(s);
+  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < S; s += gridDim.x * blockDim.x) {
+    const int x = b.st_idx[3 * s], y = b.st_idx[3 * s + 1], z = b.st_idx[3 * s + 2];
+    m.map[m.slot(x, y, z)] = static_cast<int32_t>(s);
+    atomicOr(m.bits + m.word(x, y, z), 1u << ((z - m.lo[2]) & 31));
+  }
 }
 
 __global__ void k_ccl_init(Counters* ctr, SegBufs b) {
@@ -152,12 +156,17 @@ __global__ void k_ccl_init(Counters* ctr, SegBufs b) {
 // always hooks the larger root under the smaller (atomicCAS), so every root is
 // its component's minimum ordinal: the canonical label, bit-exact.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ int uf_find(volatile int32_t* parent, int v) {
-  int par = parent[v];
+// Parent pointers only ever move to an ancestor (hooks: root -> smaller root;
+// pointer jumping: node -> grandparent), so every value a thread can observe
+// is an ancestor of the node. Reads go through L2 (ld.cg): a stale value is
+// still an ancestor, so "same root" answers are always right and a wrong
+// "different roots" answer is corrected by the atomicCAS retry.
+__device__ __forceinline__ int uf_find(int32_t* parent, int v) {
+  int par = __ldcg(parent + v);
   if (par != v) {
     int next, prev = v;
-    while (par > (next = parent[par])) {
-      parent[prev] = next;  // pointer jumping; parent[x] <= x always holds
+    while (par > (next = __ldcg(parent + par))) {
+      __stcg(parent + prev, next);  // pointer jumping; parent[x] <= x always holds
       prev = par;
       par = next;
     }
@@ -165,45 +174,145 @@ __device__ __forceinline__ int uf_find(volatile int32_t* parent, int v) {
   return par;
 }
 
-__device__ __forceinline__ void uf_union(volatile int32_t* parent, int a, int b) {
-  int ra = uf_find(parent, a), rb = uf_find(parent, b);
+// Link two roots (larger under smaller); returns the surviving root.
+__device__ __forceinline__ int uf_link(int32_t* parent, int ra, int rb) {
   while (ra != rb) {
     const int lo = ra < rb ? ra : rb;
     const int hi = ra < rb ? rb : ra;
-    const int ret = atomicCAS(const_cast<int32_t*>(parent) + hi, hi, lo);
-    if (ret == hi) break;
-    if (ra == hi) ra = ret; else rb = ret;
+    const int ret = atomicCAS(parent + hi, hi, lo);
+    if (ret == hi) return lo;
+    if (ra == hi) ra = ret; else rb = ret;  // hi was hooked meanwhile: climb
+  }
+  return ra;
+}
+
+__device__ __forceinline__ void uf_union(int32_t* parent, int a, int b) {
+  uf_link(parent, uf_find(parent, a), uf_find(parent, b));
+}
+
+// Edge predicate of build_adjacency (segmentation.cpp:124-125), evaluated in
+// the reference's arithmetic: squaredNorm of the mean difference, normal dot.
+__device__ __forceinline__ bool adjacent(const SegBufs& b, const SegDev& sp, d3 mi, d3 ni, int j) {
+  const d3 mj = mk3(__ldg(b.st_mean + 3 * j), __ldg(b.st_mean + 3 * j + 1), __ldg(b.st_mean + 3 * j + 2));
+  if (sqn3(sub3(mi, mj)) >= sp.d2_th) return false;
+  const d3 nj = mk3(__ldg(b.st_normal + 3 * j), __ldg(b.st_normal + 3 * j + 1),
+                    __ldg(b.st_normal + 3 * j + 2));
+  return dot3(ni, nj) > sp.cos_th;
+}
+
+// Window rows of voxel i: forward half (dx = 0: dy = 0..w with dz > 0 on
+// dy = 0; dx = 1..w: dy = -w..w) or, with backward = true, its mirror image.
+__device__ __forceinline__ bool window_row(int r, int w, int span, bool backward, int& dx, int& dy) {
+  if (r <= w) {
+    dx = 0;
+    dy = r;
+  } else {
+    const int q = r - (w + 1);
+    dx = 1 + q / span;
+    dy = q % span - w;
+  }
+  if (backward) {
+    dx = -dx;
+    dy = -dy;
+  }
+  return true;
+}
+
+// CCL phase 1 (ECL-CC style initial hooking, no atomics): parent[i] = the
+// smallest ordinal j < i adjacent to i, else i. Each node writes only its own
+// parent and j < i keeps parent[x] <= x, so this is a valid set of unions.
+// One warp per voxel; the steppable bitmap turns each window row into one
+// word load, and only present voxels are probed.
+__global__ void __launch_bounds__(256) k_ccl_hook(Counters* ctr, SegDev sp, SegBufs b, MapDesc m) {
+  const uint32_t S = min(ctr->S, b.Scap);
+  const int w = sp.w, span = 2 * w + 1;
+  const int nrows = (w + 1) + w * span;
+  const unsigned lane = lane_id();
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarp = (gridDim.x * blockDim.x) >> 5;
+  const int xlo = m.lo[0], ylo = m.lo[1], yhi = m.lo[1] + m.dims[1] - 1;
+  const int zlo_m = m.lo[2], zhi_m = m.lo[2] + m.dims[2] - 1;
+  for (uint32_t i = warp; i < S; i += nwarp) {
+    const int x = __ldg(b.st_idx + 3 * i), y = __ldg(b.st_idx + 3 * i + 1), z = __ldg(b.st_idx + 3 * i + 2);
+    const d3 mi = mk3(__ldg(b.st_mean + 3 * i), __ldg(b.st_mean + 3 * i + 1), __ldg(b.st_mean + 3 * i + 2));
+    const d3 ni = mk3(__ldg(b.st_normal + 3 * i), __ldg(b.st_normal + 3 * i + 1),
+                      __ldg(b.st_normal + 3 * i + 2));
+    int best = static_cast<int>(i);
+    for (int r = static_cast<int>(lane); r < nrows; r += 32) {
+      int dx, dy;
+      window_row(r, w, span, true, dx, dy);
+      const int X = x + dx, Y = y + dy;
+      if (X < xlo || Y < ylo || Y > yhi) continue;
+      const int z0 = max(z - w, zlo_m);
+      const int z1 = (dx == 0 && dy == 0) ? z - 1 : min(z + w, zhi_m);
+      if (z0 > z1) continue;
+      uint32_t bits = m.row_span(X, Y, z0, z1 - z0 + 1);
+      while (bits) {
+        const int t = __ffs(bits) - 1;
+        bits &= bits - 1;
+        const int j = __ldg(m.map + m.slot(X, Y, z0 + t));
+        if (j < best && adjacent(b, sp, mi, ni, j)) best = j;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+    if (lane == 0) {
+      b.parent[i] = best;
+      b.cnt[i] = 0;
+      b.cid[i] = -1;
+    }
   }
 }
 
-__global__ void k_ccl_union(Counters* ctr, SegDev sp, SegBufs b, MapDesc m) {
+// Pointer jumping to the root for every node (ld.cg: roots written by other
+// SMs in k_ccl_hook are visible; no node changes its own value concurrently
+// except through jumps to an ancestor, which keeps the result a root).
+__global__ void k_ccl_compress(Counters* ctr, SegBufs b) {
   const uint32_t S = min(ctr->S, b.Scap);
-  const int w = sp.w;
-  volatile int32_t* parent = b.parent;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < S; i += gridDim.x * blockDim.x) {
-    const int x = b.st_idx[3 * i], y = b.st_idx[3 * i + 1], z = b.st_idx[3 * i + 2];
-    const d3 mi = mk3(b.st_mean[3 * i], b.st_mean[3 * i + 1], b.st_mean[3 * i + 2]);
-    const d3 ni = mk3(b.st_normal[3 * i], b.st_normal[3 * i + 1], b.st_normal[3 * i + 2]);
-    const int xhi = min(x + w, m.lo[0] + m.dims[0] - 1);
-    for (int X = x; X <= xhi; ++X) {
-      const int ylo = (X == x) ? y : max(y - w, m.lo[1]);
-      const int yhi = min(y + w, m.lo[1] + m.dims[1] - 1);
-      for (int Y = ylo; Y <= yhi; ++Y) {
-        const int zlo = (X == x && Y == y) ? z + 1 : max(z - w, m.lo[2]);
-        const int zhi = min(z + w, m.lo[2] + m.dims[2] - 1);
-        if (zlo > zhi) continue;
-        const int32_t* row = m.map + m.slot(X, Y, zlo);
-        for (int Z = zlo; Z <= zhi; ++Z) {
-          const int j = __ldg(row + (Z - zlo));
-          if (j < 0) continue;
-          const d3 mj = mk3(__ldg(b.st_mean + 3 * j), __ldg(b.st_mean + 3 * j + 1),
-                            __ldg(b.st_mean + 3 * j + 2));
-          if (sqn3(sub3(mi, mj)) >= sp.d2_th) continue;
-          const d3 nj = mk3(__ldg(b.st_normal + 3 * j), __ldg(b.st_normal + 3 * j + 1),
-                            __ldg(b.st_normal + 3 * j + 2));
-          if (dot3(ni, nj) <= sp.cos_th) continue;
-          uf_union(parent, static_cast<int>(i), j);
-        }
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < S; i += gridDim.x * blockDim.x)
+    __stcg(b.parent + i, uf_find(b.parent, static_cast<int>(i)));
+}
+
+// CCL phase 2: every forward edge (i, j > i) as a union. The 4-byte parent[j]
+// is checked against i's cached root before the 48-byte predicate loads, so
+// edges inside an already-joined tree cost one load.
+__global__ void __launch_bounds__(256) k_ccl_union(Counters* ctr, SegDev sp, SegBufs b, MapDesc m) {
+  const uint32_t S = min(ctr->S, b.Scap);
+  const int w = sp.w, span = 2 * w + 1;
+  const int nrows = (w + 1) + w * span;
+  int32_t* parent = b.parent;
+  const unsigned lane = lane_id();
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarp = (gridDim.x * blockDim.x) >> 5;
+  const int xmax = m.lo[0] + m.dims[0] - 1, ymin = m.lo[1], ymax = m.lo[1] + m.dims[1] - 1;
+  const int zmin = m.lo[2], zmax = m.lo[2] + m.dims[2] - 1;
+  for (uint32_t i = warp; i < S; i += nwarp) {
+    const int x = __ldg(b.st_idx + 3 * i), y = __ldg(b.st_idx + 3 * i + 1), z = __ldg(b.st_idx + 3 * i + 2);
+    const d3 mi = mk3(__ldg(b.st_mean + 3 * i), __ldg(b.st_mean + 3 * i + 1), __ldg(b.st_mean + 3 * i + 2));
+    const d3 ni = mk3(__ldg(b.st_normal + 3 * i), __ldg(b.st_normal + 3 * i + 1),
+                      __ldg(b.st_normal + 3 * i + 2));
+    int ri = -1;
+    if (lane == 0) ri = uf_find(parent, static_cast<int>(i));
+    ri = __shfl_sync(0xffffffffu, ri, 0);
+    for (int r = static_cast<int>(lane); r < nrows; r += 32) {
+      int dx, dy;
+      window_row(r, w, span, false, dx, dy);
+      const int X = x + dx, Y = y + dy;
+      if (X > xmax || Y < ymin || Y > ymax) continue;
+      const int z0 = (dx == 0 && dy == 0) ? z + 1 : max(z - w, zmin);
+      const int z1 = min(z + w, zmax);
+      if (z0 > z1) continue;
+      uint32_t bits = m.row_span(X, Y, z0, z1 - z0 + 1);
+      while (bits) {
+        const int t = __ffs(bits) - 1;
+        bits &= bits - 1;
+        const int j = __ldg(m.map + m.slot(X, Y, z0 + t));
+        const int pj = __ldcg(parent + j);
+        if (pj == ri) continue;  // already in i's tree
+        if (!adjacent(b, sp, mi, ni, j)) continue;
+        const int rj = uf_find(parent, j);
+        if (rj == ri) continue;
+        ri = uf_link(parent, ri, rj);
       }
     }
   }
@@ -260,12 +369,14 @@ __global__ void k_occ_gather(GridDesc g, const FrameParams* __restrict__ fp, Cou
 // Final labels (component minimum), member counts per root, map reset.
 __global__ void k_ccl_flatten(Counters* ctr, SegBufs b, MapDesc m) {
   const uint32_t S = min(ctr->S, b.Scap);
-  volatile int32_t* parent = b.parent;
+  int32_t* parent = b.parent;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < S; i += gridDim.x * blockDim.x) {
     const int r = uf_find(parent, static_cast<int>(i));
     b.label[i] = r;
     atomicAdd(&b.cnt[r], 1u);
-    m.map[m.slot(b.st_idx[3 * i], b.st_idx[3 * i + 1], b.st_idx[3 * i + 2])] = -1;
+    const int x = b.st_idx[3 * i], y = b.st_idx[3 * i + 1], z = b.st_idx[3 * i + 2];
+    m.map[m.slot(x, y, z)] = -1;
+    m.bits[m.word(x, y, z)] = 0u;  // every bit of the word belongs to a steppable voxel being reset
   }
 }
 
@@ -782,14 +893,17 @@ __device__ void bitonic_sort(P2* a, uint32_t n) {
 __global__ void k_polygon(Counters* ctr, SegBufs b, const double* dirtab, int directions,
                           double min_area) {
   extern __shared__ P2 sm_pts[];  // kHullSmem points
-  __shared__ double ex_dot[256];
-  __shared__ P2 ex_pt[256];
+  __shared__ double ex_dot[8 * 16];
+  __shared__ int ex_idx[8 * 16];
+  __shared__ double sdir[128];
   __shared__ P2 extremes[64];
   __shared__ P2 inner[130];
   __shared__ uint32_t n_inner, n_surv, n_uniq;
   __shared__ double basis[9];
   const uint32_t F = ctr->nfits;
   if (ctr->overflow & (kOverflowFits | kOverflowMembers)) return;
+  for (int j = threadIdx.x; j < 2 * directions && j < 128; j += blockDim.x) sdir[j] = dirtab[j];
+  __syncthreads();
   for (uint32_t f = blockIdx.x; f < F; f += gridDim.x) {
     const uint64_t o = b.ioff[f];
     const uint32_t n = b.ioff[f + 1] - b.ioff[f];
@@ -839,36 +953,65 @@ __global__ void k_polygon(Counters* ctr, SegBufs b, const double* dirtab, int di
       proj[i] = P2{dot3(d, u), dot3(d, v)};
     }
     __syncthreads();
-    // hull_filter (:50-114)
+    // hull_filter (:50-114): extreme point along each direction (larger dot,
+    // ties to the lexicographically smaller point) -- all directions of a
+    // chunk in one pass over the points, then a warp-shuffle + smem reduction.
     bool filter = n > 3 && directions >= 3;
     if (filter) {
-      for (int j = 0; j < directions; ++j) {
-        const double dx = dirtab[2 * j], dy = dirtab[2 * j + 1];
-        double best = -CUDART_INF;
-        P2 bp = P2{0.0, 0.0};
-        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-          const P2 q = proj[i];
-          const double dd = q.x * dx + q.y * dy;
-          if (dd > best || (dd == best && lex_less(q, bp))) {
-            best = dd;
-            bp = q;
-          }
+      for (int j0 = 0; j0 < directions; j0 += 16) {
+        const int nd = min(16, directions - j0);
+        double bd[16];
+        int bi[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          bd[q] = -CUDART_INF;
+          bi[q] = -1;
         }
-        ex_dot[threadIdx.x] = best;
-        ex_pt[threadIdx.x] = bp;
-        __syncthreads();
-        for (uint32_t h = blockDim.x / 2; h > 0; h >>= 1) {
-          if (threadIdx.x < h) {
-            const double od = ex_dot[threadIdx.x + h];
-            const P2 op = ex_pt[threadIdx.x + h];
-            if (od > ex_dot[threadIdx.x] || (od == ex_dot[threadIdx.x] && lex_less(op, ex_pt[threadIdx.x]))) {
-              ex_dot[threadIdx.x] = od;
-              ex_pt[threadIdx.x] = op;
+        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+          const P2 q2 = proj[i];
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            if (q < nd) {
+              const double dd = q2.x * sdir[2 * (j0 + q)] + q2.y * sdir[2 * (j0 + q) + 1];
+              if (dd > bd[q] || (dd == bd[q] && bi[q] >= 0 && lex_less(q2, proj[bi[q]]))) {
+                bd[q] = dd;
+                bi[q] = static_cast<int>(i);
+              }
             }
           }
-          __syncthreads();
         }
-        if (threadIdx.x == 0) extremes[j] = ex_pt[0];
+        const unsigned lane = lane_id(), wid = threadIdx.x >> 5;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            const double od = __shfl_down_sync(0xffffffffu, bd[q], o);
+            const int oi = __shfl_down_sync(0xffffffffu, bi[q], o);
+            if (oi >= 0 && (bi[q] < 0 || od > bd[q] || (od == bd[q] && lex_less(proj[oi], proj[bi[q]])))) {
+              bd[q] = od;
+              bi[q] = oi;
+            }
+          }
+          if (lane == 0) {
+            ex_dot[wid * 16 + q] = bd[q];
+            ex_idx[wid * 16 + q] = bi[q];
+          }
+        }
+        __syncthreads();
+        if (threadIdx.x < static_cast<unsigned>(nd)) {
+          const int q = static_cast<int>(threadIdx.x);
+          double best = -CUDART_INF;
+          int bix = -1;
+          for (unsigned w2 = 0; w2 < (blockDim.x >> 5); ++w2) {
+            const double od = ex_dot[w2 * 16 + q];
+            const int oi = ex_idx[w2 * 16 + q];
+            if (oi >= 0 && (bix < 0 || od > best || (od == best && lex_less(proj[oi], proj[bix])))) {
+              best = od;
+              bix = oi;
+            }
+          }
+          extremes[j0 + q] = bix >= 0 ? proj[bix] : P2{0.0, 0.0};
+        }
         __syncthreads();
       }
       if (threadIdx.x == 0) {  // inner = monotone_chain(extremes)

@@ -222,6 +222,7 @@ struct Seg {
                                                    (vcap + kScanPerBlock - 1) / kScanPerBlock,
                                                    (scap + kScanPerBlock - 1) / kScanPerBlock}) + 1;
     if (need) {
+      ++gen;
       release();
       b.Vcap = vcap;
       b.Scap = scap;
@@ -275,6 +276,7 @@ struct Seg {
       bsum_cap = static_cast<uint32_t>(need_bsum);
       bsum = dalloc<uint32_t>(2ull * need_bsum);
     } else if (need_bsum > bsum_cap) {
+      ++gen;
       dfree(bsum);
       bsum_cap = static_cast<uint32_t>(need_bsum);
       bsum = dalloc<uint32_t>(2ull * need_bsum);
@@ -297,6 +299,7 @@ struct Seg {
   }
 
   uint64_t cand_cap = 0;
+  uint64_t gen = 0;  // bumped on reallocation (invalidates captured graphs)
 };
 
 // Host image of the per-fit records written by k_polygon.
@@ -335,8 +338,9 @@ struct vp_grid {
   uint32_t* sorted = nullptr;
   Seg seg;
   cudaEvent_t ev[8];
-  // trace scratch for the occupied-list view
-  bool status_written_this_frame = false;
+  // CUDA graph of one pipeline frame (see pipeline_enqueue)
+  bool capturing = false;
+  uint64_t gen = 1;  // bumped whenever a buffer the graph references is reallocated
 
   ~vp_grid() {
     if (stream) cudaStreamSynchronize(stream);
@@ -345,6 +349,7 @@ struct vp_grid {
     if (gd.cells) cudaFree(gd.cells);
     if (gd.clr) cudaFree(gd.clr);
     if (gd.ordmap) cudaFree(gd.ordmap);
+    if (gd.stbits) cudaFree(gd.stbits);
     if (ctr) cudaFree(ctr);
     if (d_fp) cudaFree(d_fp);
     if (h_ctr) cudaFreeHost(h_ctr);
@@ -380,6 +385,7 @@ struct vp_grid {
     gd.cells = dalloc<Cell>(C);
     gd.clr = dalloc<uint32_t>(gd.nwords);
     gd.ordmap = dalloc<int32_t>(C);
+    gd.stbits = dalloc<uint32_t>(gd.nwords);
     occ[0] = dalloc<uint32_t>(gd.nwords);
     occ[1] = dalloc<uint32_t>(gd.nwords);
     ck(cudaMemsetAsync(gd.cells, 0, C * sizeof(Cell), stream), "memset cells");
@@ -387,6 +393,7 @@ struct vp_grid {
     ck(cudaMemsetAsync(occ[0], 0, gd.nwords * 4, stream), "memset occ");
     ck(cudaMemsetAsync(occ[1], 0, gd.nwords * 4, stream), "memset occ");
     ck(cudaMemsetAsync(gd.ordmap, 0xff, C * 4, stream), "memset ordmap");
+    ck(cudaMemsetAsync(gd.stbits, 0, gd.nwords * 4, stream), "memset stbits");
     ctr = dalloc<Counters>(1);
     ck(cudaMemsetAsync(ctr, 0, sizeof(Counters), stream), "memset ctr");
     d_fp = dalloc<FrameParams>(1);
@@ -445,6 +452,7 @@ struct vp_grid {
     ck(cudaMemsetAsync(hcnt, 0, hs * 4, stream), "hcnt");
     hmask = static_cast<uint32_t>(hs - 1);
     pcap = cap;
+    ++gen;
   }
 
   // ------------------------------------------------------------ frame params
@@ -503,14 +511,16 @@ struct vp_grid {
   }
 
   // ------------------------------------------------------------ kernels
+  // Grids are sized by the points capacity (grid-stride loops read n from
+  // the device params), so the same launches can be replayed as a graph.
   void launch_clear(uint64_t n) {
-    if (n == 0) return;
-    LAUNCH(k_clear_walk, grid_for(n, 148 * 32), kThreads, 0, stream, gd, d_fp);
+    if (n == 0 && !capturing) return;
+    LAUNCH(k_clear_walk, grid_for(capturing ? pcap : n, 148 * 32), kThreads, 0, stream, gd, d_fp);
     LAUNCH(k_clear_apply, grid_for(gd.nwords), kThreads, 0, stream, gd, d_fp, ctr);
   }
   void launch_integrate(uint64_t n) {
-    if (n == 0) return;
-    const int gp = grid_for(n);
+    if (n == 0 && !capturing) return;
+    const int gp = grid_for(capturing ? pcap : n);
     LAUNCH(k_integrate_hash, gp, kThreads, 0, stream, gd, d_fp, ctr, hkey, hcnt, hmask, groups,
            pslot, prank);
     LAUNCH(k_integrate_offsets, gp, kThreads, 0, stream, ctr, groups, hcnt, hoff);
@@ -526,10 +536,9 @@ struct vp_grid {
   // Occupied scan of the post-recenter bitmap into seg.b.occ_list; ctr->V.
   void launch_occupied_scan() {
     const uint32_t nb = static_cast<uint32_t>((gd.nwords + kScanPerBlock - 1) / kScanPerBlock);
-    uint32_t* occ_now = h_fp->occ_post;
-    LAUNCH(k_bitmap_count, nb, kScanThreads, 0, stream, occ_now, gd.nwords, seg.bsum);
+    LAUNCH(k_bitmap_count, nb, kScanThreads, 0, stream, d_fp, gd.nwords, seg.bsum);
     LAUNCH(k_scan_exclusive, 1, 1024, 0, stream, seg.bsum, nb, nullptr, &ctr->V, nullptr);
-    LAUNCH(k_bitmap_emit, nb, kScanThreads, 0, stream, occ_now, gd.nwords, gd.W, gd.ez, seg.bsum,
+    LAUNCH(k_bitmap_emit, nb, kScanThreads, 0, stream, d_fp, gd.nwords, gd.W, gd.ez, seg.bsum,
            seg.b.occ_list, seg.b.Vcap);
   }
 
@@ -546,6 +555,8 @@ struct vp_grid {
   MapDesc grid_map() {
     MapDesc m;
     m.map = gd.ordmap;
+    m.bits = gd.stbits;
+    m.W = gd.W;
     m.lo[0] = m.lo[1] = m.lo[2] = 0;
     m.dims[0] = ext[0];
     m.dims[1] = ext[1];
@@ -563,7 +574,8 @@ struct vp_grid {
   }
   // union-find over the steppable list in seg.b (ctr->S set)
   void launch_ccl(const SegDev& sd, const MapDesc& m) {
-    LAUNCH(k_ccl_init, kWide, kThreads, 0, stream, ctr, seg.b);
+    LAUNCH(k_ccl_hook, kWide, kThreads, 0, stream, ctr, sd, seg.b, m);
+    LAUNCH(k_ccl_compress, kWide, kThreads, 0, stream, ctr, seg.b);
     LAUNCH(k_ccl_union, kWide, kThreads, 0, stream, ctr, sd, seg.b, m);
     LAUNCH(k_ccl_flatten, kWide, kThreads, 0, stream, ctr, seg.b, m);
   }
@@ -593,24 +605,29 @@ struct vp_grid {
   }
 
   // The fused segment(): voxel_frame_polygons (pipeline.cpp:43-85) on device.
+  void record(cudaEvent_t e) {
+    ck(cudaEventRecordWithFlags(e, stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault),
+       "event record");
+  }
+
   void launch_segment(const vp_pipeline_params& p, bool timing) {
     const SegDev sd = make_segdev(p.seg, gd.res);
     const RansacDev rd = make_ransacdev(p.ransac);
-    if (static_cast<uint64_t>(p.ransac.iterations) * kClusterBins > seg.cand_cap)
+    if (!capturing && static_cast<uint64_t>(p.ransac.iterations) * kClusterBins > seg.cand_cap)
       seg.ensure(seg.b.Vcap, seg.b.Scap, seg.b.Icap, p.ransac.iterations, gd.nwords);
-    if (timing) ck(cudaEventRecord(ev[1], stream), "ev");
+    if (timing) record(ev[1]);
     launch_occupied_scan();
     launch_classify(sd, 1);
-    if (timing) ck(cudaEventRecord(ev[2], stream), "ev");
+    if (timing) record(ev[2]);
     launch_step_emit(grid_map());
     launch_ccl(sd, grid_map());
     launch_clusters(sd);
-    if (timing) ck(cudaEventRecord(ev[3], stream), "ev");
+    if (timing) record(ev[3]);
     launch_ransac(rd);
-    if (timing) ck(cudaEventRecord(ev[4], stream), "ev");
+    if (timing) record(ev[4]);
     launch_refine(p.ransac.up, p.refine, p.refine_exact);
     launch_polygon(16, p.min_polygon_area);
-    if (timing) ck(cudaEventRecord(ev[5], stream), "ev");
+    if (timing) record(ev[5]);
   }
 
   // Grow capacities after an overflow (the frame's segmentation is re-run).
@@ -740,19 +757,76 @@ struct vp_pipeline {
   vp_pipeline_params p{};
   int32_t last_cell[3] = {0, 0, 0};
   uint32_t frame = 0;
-  ~vp_pipeline() { delete grid; }
+  // one frame of work as a CUDA graph (params H2D, counter reset, every
+  // kernel, stage events, counters D2H)
+  cudaGraphExec_t gexec = nullptr;
+  uint64_t graph_key = 0;
+  uint64_t graph_kernels = 0;
+  ~vp_pipeline() {
+    if (gexec) cudaGraphExecDestroy(gexec);
+    delete grid;
+  }
 };
 
 namespace {
 
-// One run_frames iteration up to the end of segmentation (no host sync).
-// Returns whether the grid was recentered.
+// The device work of one frame, in stream order. With capture == true the
+// same sequence is recorded into a CUDA graph (every argument is frame
+// invariant; per-frame values live in the device FrameParams).
+void enqueue_frame_work(vp_pipeline* pl, uint64_t n) {
+  vp_grid* g = pl->grid;
+  const unsigned evflag = g->capturing ? cudaEventRecordExternal : cudaEventRecordDefault;
+  ck(cudaMemcpyAsync(g->d_fp, g->h_fp, sizeof(FrameParams), cudaMemcpyHostToDevice, g->stream), "params");
+  g->reset_frame_counters();
+  ck(cudaEventRecordWithFlags(g->ev[0], g->stream, evflag), "ev");
+  g->launch_clear(n);
+  g->launch_integrate(n);
+  g->launch_recenter();
+  g->launch_finalize();
+  g->launch_segment(pl->p, true);
+  ck(cudaMemcpyAsync(g->h_ctr, g->ctr, sizeof(Counters), cudaMemcpyDeviceToHost, g->stream), "ctr d2h");
+}
+
+void run_frame_graph(vp_pipeline* pl) {
+  vp_grid* g = pl->grid;
+  const uint64_t key = (g->gen << 32) ^ g->seg.gen;
+  if (!pl->gexec || pl->graph_key != key) {
+    if (pl->gexec) cudaGraphExecDestroy(pl->gexec);
+    pl->gexec = nullptr;
+    cudaGraph_t graph;
+    const uint64_t before = g_launches.load();
+    g->capturing = true;
+    ck(cudaStreamBeginCapture(g->stream, cudaStreamCaptureModeThreadLocal), "capture begin");
+    try {
+      enqueue_frame_work(pl, g->pcap);
+    } catch (...) {
+      cudaStreamEndCapture(g->stream, &graph);
+      g->capturing = false;
+      throw;
+    }
+    ck(cudaStreamEndCapture(g->stream, &graph), "capture end");
+    g->capturing = false;
+    pl->graph_kernels = g_launches.load() - before;
+    g_launches.fetch_sub(pl->graph_kernels);
+    ck(cudaGraphInstantiate(&pl->gexec, graph, 0), "graph instantiate");
+    cudaGraphDestroy(graph);
+    pl->graph_key = key;
+  }
+  ck(cudaGraphLaunch(pl->gexec, g->stream), "graph launch");
+  g_launches.fetch_add(pl->graph_kernels);
+}
+
+// One run_frames iteration (pipeline.cpp:199-213) through segmentation;
+// returns whether the window was recentered. The caller waits on the stream.
 bool pipeline_enqueue(vp_pipeline* pl, const float* xyz, uint64_t n, const double* R,
                       const double* t, bool device_ptr, vp_shift_stats* ss) {
   vp_grid* g = pl->grid;
   if (!is_valid_rotation(R))  // voxel_grid.cpp:60-61, 183-184
     fail(VP_EINVAL, "clear_rays: pose rotation is not orthonormal");
-  if (device_ptr) g->ensure_points(n);
+  g->ensure_points(n);
+  if (static_cast<uint64_t>(pl->p.ransac.iterations) * kClusterBins > g->seg.cand_cap)
+    g->seg.ensure(g->seg.b.Vcap, g->seg.b.Scap, g->seg.b.Icap, pl->p.ransac.iterations, g->gd.nwords);
+  g->seg.ensure_dirs(16, g->stream);
   g->set_pose(R, t);
   g->fill_static_params();
   stage_points(g, xyz, n, device_ptr);
@@ -765,15 +839,17 @@ bool pipeline_enqueue(vp_pipeline* pl, const float* xyz, uint64_t n, const doubl
     std::memcpy(pl->last_cell, cell, sizeof cell);
     rec = true;
   }
-  ck(cudaEventRecord(g->ev[0], g->stream), "ev");
-  g->upload_params();
-  g->reset_frame_counters();
-  g->launch_clear(n);
-  g->launch_integrate(n);
-  g->launch_recenter();
-  g->launch_finalize();
-  g->launch_segment(pl->p, true);
+  if (g_prof_on || std::getenv("VP_NO_GRAPH")) {
+    enqueue_frame_work(pl, n);
+  } else {
+    run_frame_graph(pl);
+  }
   return rec;
+}
+
+void wait_frame(vp_grid* g) {
+  ck(cudaStreamSynchronize(g->stream), "frame sync");
+  g->host_occupied = g->h_ctr->occupied;
 }
 
 void fill_timing(vp_grid* g, vp_frame_timing* tm, uint64_t n) {
@@ -1228,7 +1304,11 @@ void set_counter_u32(vp_grid* g, size_t field_offset, uint32_t v) {
 struct BoxMap {
   MapDesc m{};
   int32_t* buf = nullptr;
-  ~BoxMap() { if (buf) cudaFree(buf); }
+  uint32_t* bits = nullptr;
+  ~BoxMap() {
+    if (buf) cudaFree(buf);
+    if (bits) cudaFree(bits);
+  }
 };
 
 void upload_steppable(vp_grid* g, const vp_steppable_t* s, BoxMap& bm) {
@@ -1250,6 +1330,11 @@ void upload_steppable(vp_grid* g, const vp_steppable_t* s, BoxMap& bm) {
   bm.buf = dalloc<int32_t>(vol);
   ck(cudaMemsetAsync(bm.buf, 0xff, vol * 4, g->stream), "map");
   bm.m.map = bm.buf;
+  bm.m.W = (bm.m.dims[2] + 31) / 32;
+  const uint64_t nw = static_cast<uint64_t>(bm.m.dims[0]) * bm.m.dims[1] * bm.m.W;
+  bm.bits = dalloc<uint32_t>(nw);
+  ck(cudaMemsetAsync(bm.bits, 0, nw * 4, g->stream), "bits");
+  bm.m.bits = bm.bits;
   h2d(g->seg.b.st_idx, s->idx, 3ull * S, g->stream);
   h2d(g->seg.b.st_mean, s->mean, 3ull * S, g->stream);
   h2d(g->seg.b.st_normal, s->normal, 3ull * S, g->stream);
@@ -1539,7 +1624,7 @@ static int pipeline_frame_impl(vp_pipeline* pl, const float* xyz, uint64_t n, co
     vp_shift_stats ss;
     pipeline_enqueue(pl, xyz, n, R, t, device_ptr, &ss);
     vp_grid* g = pl->grid;
-    g->read_counters();
+    wait_frame(g);
     if (g->h_ctr->overflow) rerun_segment_until_fits(g, pl->p);
     fill_timing(g, timing, n);
     if (out) {
@@ -1569,7 +1654,7 @@ int vp_pipeline_frame_trace(vp_pipeline* pl, const float* xyz, uint64_t n, const
     vp_shift_stats ss;
     const bool rec = pipeline_enqueue(pl, xyz, n, R, t, false, &ss);
     vp_grid* g = pl->grid;
-    g->read_counters();
+    wait_frame(g);
     if (g->h_ctr->overflow) rerun_segment_until_fits(g, pl->p);
     const Counters c = *g->h_ctr;
     TraceW w;

@@ -56,6 +56,7 @@ struct GridDesc {
   Cell* cells;
   uint32_t* clr;
   int32_t* ordmap;
+  uint32_t* stbits;  // steppable presence bitmap (logical, occ layout)
   int32_t ex, ey, ez, W;  // extent and words per (x,y) row
   double res;
   uint64_t ncells;

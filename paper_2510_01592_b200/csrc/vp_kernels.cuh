@@ -87,11 +87,26 @@ struct RansacDev {
 // the grid's logical extent on the fused path, the steppable bounding box for a
 // host-provided list.
 struct MapDesc {
-  int32_t* map;
+  int32_t* map;    // ordinal or -1 per slot
+  uint32_t* bits;  // 1 bit per slot (steppable present), rows of W words
   int lo[3];
   int dims[3];
+  int W;
   __device__ __forceinline__ uint64_t slot(int x, int y, int z) const {
     return (static_cast<uint64_t>(x - lo[0]) * dims[1] + (y - lo[1])) * dims[2] + (z - lo[2]);
+  }
+  __device__ __forceinline__ uint64_t word(int x, int y, int z) const {
+    return (static_cast<uint64_t>(x - lo[0]) * dims[1] + (y - lo[1])) * W + ((z - lo[2]) >> 5);
+  }
+  // `count` (<= 32) presence bits of row (x, y) starting at z0
+  __device__ __forceinline__ uint32_t row_span(int x, int y, int z0, int count) const {
+    const uint32_t* row = bits + (static_cast<uint64_t>(x - lo[0]) * dims[1] + (y - lo[1])) * W;
+    const int b0 = z0 - lo[2];
+    const int wl = b0 >> 5, sh = b0 & 31;
+    const uint32_t a = __ldg(row + wl);
+    const uint32_t hi = (sh && wl + 1 < W) ? __ldg(row + wl + 1) : 0u;
+    const uint32_t v = sh ? ((a >> sh) | (hi << (32 - sh))) : a;
+    return count >= 32 ? v : (v & ((1u << count) - 1u));
   }
 };
 
@@ -164,8 +179,8 @@ __global__ void k_clear_walk(GridDesc g, const FrameParams* fp);
 __global__ void k_clear_apply(GridDesc g, const FrameParams* fp, Counters* ctr);
 __global__ void k_recenter(GridDesc g, const FrameParams* fp, Counters* ctr);
 __global__ void k_map_finalize(Counters* ctr);
-__global__ void k_bitmap_count(const uint32_t* bits, uint64_t nwords, uint32_t* bsum);
-__global__ void k_bitmap_emit(const uint32_t* bits, uint64_t nwords, int W, int ez,
+__global__ void k_bitmap_count(const FrameParams* fp, uint64_t nwords, uint32_t* bsum);
+__global__ void k_bitmap_emit(const FrameParams* fp, uint64_t nwords, int W, int ez,
                               const uint32_t* boff, uint32_t* out, uint32_t cap);
 __global__ void k_flags_count(const uint8_t* flags, const uint32_t* n_ptr, uint32_t cap,
                               uint32_t* bsum);
@@ -186,6 +201,8 @@ __global__ void k_map_fill(Counters* ctr, SegBufs b, MapDesc m);
 __global__ void k_occ_gather(GridDesc g, const FrameParams* fp, Counters* ctr, SegBufs b);
 __global__ void k_ccl_init(Counters* ctr, SegBufs b);
 __global__ void k_ccl_union(Counters* ctr, SegDev sp, SegBufs b, MapDesc m);
+__global__ void k_ccl_hook(Counters* ctr, SegDev sp, SegBufs b, MapDesc m);
+__global__ void k_ccl_compress(Counters* ctr, SegBufs b);
 __global__ void k_ccl_flatten(Counters* ctr, SegBufs b, MapDesc m);
 __global__ void k_cluster_flags(Counters* ctr, SegDev sp, SegBufs b);
 __global__ void k_cluster_assign(Counters* ctr, SegBufs b);
