@@ -419,10 +419,16 @@ __global__ void k_recenter(GridDesc g, const FrameParams* __restrict__ fp, Count
       if (xd < 0 || xd >= g.ex || yd < 0 || yd >= g.ey) {
         drop = ov;
       } else {
+        // keep bits b with 0 <= 32*wz + b - sz < ez, i.e. b in [blo, bhi)
+        const long long blo = static_cast<long long>(sz) - 32ll * wz;
+        const long long bhi = static_cast<long long>(g.ez) + sz - 32ll * wz;
+        const int lo_b = static_cast<int>(blo < 0 ? 0 : (blo > 32 ? 32 : blo));
+        const int hi_b = static_cast<int>(bhi < 0 ? 0 : (bhi > 32 ? 32 : bhi));
         uint32_t keep = 0;
-        for (int b = 0; b < 32; ++b) {
-          const long long zd = static_cast<long long>(wz) * 32 + b - sz;
-          if (zd >= 0 && zd < g.ez) keep |= 1u << b;
+        if (hi_b > lo_b) {
+          const uint32_t upto_hi = hi_b >= 32 ? 0xffffffffu : ((1u << hi_b) - 1u);
+          const uint32_t below_lo = lo_b >= 32 ? 0xffffffffu : ((1u << lo_b) - 1u);
+          keep = upto_hi & ~below_lo;
         }
         drop = ov & ~keep;
       }

@@ -577,16 +577,32 @@ __global__ void k_ransac_count(Counters* ctr, RansacDev rp, SegBufs b) {
                     : mk3(0.0, 0.0, 0.0);
     const uint64_t cbase = static_cast<uint64_t>(k) * I;
     for (uint32_t c0 = 0; c0 < I; c0 += 32) {
+      // candidate c0 + lane held by this lane, broadcast by shuffles
+      const uint32_t mine_t = c0 + lane;
+      int valid = 0;
+      double cx = 0.0, cy = 0.0, cz = 0.0, cd = 0.0;
+      if (mine_t < I) {
+        const uint64_t t = cbase + mine_t;
+        valid = b.cand_cnt[t] >= 0;
+        if (valid) {
+          cx = b.cand[4 * t];
+          cy = b.cand[4 * t + 1];
+          cz = b.cand[4 * t + 2];
+          cd = b.cand[4 * t + 3];
+        }
+      }
+      const unsigned vmask = __ballot_sync(0xffffffffu, valid);
       uint32_t mine = 0;
-      const uint32_t cend = min(32u, I - c0);
-      for (uint32_t q = 0; q < cend; ++q) {
-        const uint64_t t = cbase + c0 + q;
-        if (b.cand_cnt[t] < 0) continue;  // degenerate sample: warp-uniform
-        const d3 n = mk3(b.cand[4 * t], b.cand[4 * t + 1], b.cand[4 * t + 2]);
-        const double off = b.cand[4 * t + 3];
+      unsigned rem = vmask;
+      while (rem) {  // degenerate samples skipped (warp-uniform)
+        const int q = __ffs(rem) - 1;
+        rem &= rem - 1;
+        const d3 n = mk3(__shfl_sync(0xffffffffu, cx, q), __shfl_sync(0xffffffffu, cy, q),
+                         __shfl_sync(0xffffffffu, cz, q));
+        const double off = __shfl_sync(0xffffffffu, cd, q);
         const bool pred = in && fabs(dot3(n, p) - off) <= rp.eps;
         const uint32_t c = __popc(__ballot_sync(0xffffffffu, pred));
-        if (lane == q) mine = c;
+        if (static_cast<int>(lane) == q) mine = c;
       }
       if (mine) atomicAdd(&b.cand_cnt[cbase + c0 + lane], static_cast<int32_t>(mine));
     }
@@ -890,22 +906,238 @@ __device__ void bitonic_sort(P2* a, uint32_t n) {
   }
 }
 
-__global__ void k_polygon(Counters* ctr, SegBufs b, const double* dirtab, int directions,
-                          double min_area) {
-  extern __shared__ P2 sm_pts[];  // kHullSmem points
+// Polygon stage as five kernels so the large fits use the whole GPU:
+//  setup   (1 block)        plane_basis per fit, chunk table (kPolyChunk points)
+//  extremes(block / chunk)  project_to_plane + per-chunk extremes per direction
+//  inner   (block / fit)    final extremes (larger dot, ties lexicographic) and
+//                           the inner polygon = monotone_chain(extremes)
+//  keep    (block / chunk)  survivors: not strictly inside the inner polygon
+//  hull    (block / fit)    lexicographic bitonic sort, unique, monotone chain,
+//                           lift, shoelace, area filter, output record
+__device__ __forceinline__ bool ext_better(double od, int oi, double bd, int bi, const P2* proj) {
+  return oi >= 0 && (bi < 0 || od > bd || (od == bd && lex_less(proj[oi], proj[bi])));
+}
+
+__device__ __forceinline__ uint32_t poly_fit_of_chunk(const SegBufs& b, uint32_t F, uint32_t c) {
+  uint32_t lo = 0, hi = F;  // largest f with pch_off[f] <= c
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (b.pch_off[mid] <= c) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void k_poly_setup(Counters* ctr, SegBufs b) {
+  __shared__ uint32_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const uint32_t F = (ctr->overflow & (kOverflowFits | kOverflowMembers)) ? 0u : ctr->nfits;
+  for (uint32_t base = 0; base < F; base += blockDim.x) {
+    const uint32_t f = base + threadIdx.x;
+    uint32_t nch = 0;
+    if (f < F) {
+      const uint32_t n = b.ioff[f + 1] - b.ioff[f];
+      nch = n >= 3 ? (n + kPolyChunk - 1) / kPolyChunk : 0u;
+      b.nsurv[f] = 0;
+      const double* pl = b.ref_model + 4 * f;
+      const d3 nrm = mk3(pl[0], pl[1], pl[2]);
+      int least = 0;  // plane_basis (polygonize.cpp:21-34)
+      const double an[3] = {fabs(nrm.x), fabs(nrm.y), fabs(nrm.z)};
+      if (an[1] < an[least]) least = 1;
+      if (an[2] < an[least]) least = 2;
+      const d3 axis = mk3(least == 0 ? 1.0 : 0.0, least == 1 ? 1.0 : 0.0, least == 2 ? 1.0 : 0.0);
+      const d3 u = normalized3(sub3(axis, scl3(dot3(nrm, axis), nrm)));
+      const d3 v = cross3(nrm, u);
+      const d3 org = scl3(pl[3], nrm);
+      double* bs = b.basis + 9 * f;
+      bs[0] = u.x; bs[1] = u.y; bs[2] = u.z;
+      bs[3] = v.x; bs[4] = v.y; bs[5] = v.z;
+      bs[6] = org.x; bs[7] = org.y; bs[8] = org.z;
+    }
+    const uint32_t ex = block_exclusive_u32(nch);
+    const uint32_t c0 = carry;
+    if (f < F) b.pch_off[f] = c0 + ex;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = c0 + ex + nch;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    b.pch_off[F] = carry;
+    ctr->poly_chunks = carry;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_poly_extremes(Counters* ctr, SegBufs b, const double* dirtab,
+                                                       int directions) {
+  __shared__ double sdir[128];
   __shared__ double ex_dot[8 * 16];
   __shared__ int ex_idx[8 * 16];
-  __shared__ double sdir[128];
-  __shared__ P2 extremes[64];
-  __shared__ P2 inner[130];
-  __shared__ uint32_t n_inner, n_surv, n_uniq;
-  __shared__ double basis[9];
-  const uint32_t F = ctr->nfits;
-  if (ctr->overflow & (kOverflowFits | kOverflowMembers)) return;
+  const uint32_t F = ctr->nfits, nchunks = ctr->poly_chunks;
   for (int j = threadIdx.x; j < 2 * directions && j < 128; j += blockDim.x) sdir[j] = dirtab[j];
   __syncthreads();
+  P2* proj = reinterpret_cast<P2*>(b.proj);
+  const unsigned lane = lane_id(), wid = threadIdx.x >> 5;
+  for (uint32_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    const uint32_t f = poly_fit_of_chunk(b, F, c);
+    const uint32_t n = b.ioff[f + 1] - b.ioff[f];
+    const uint64_t i0 = b.ioff[f] + static_cast<uint64_t>(c - b.pch_off[f]) * kPolyChunk;
+    const uint64_t i1 = min(static_cast<uint64_t>(b.ioff[f + 1]), i0 + kPolyChunk);
+    const double* bs = b.basis + 9 * f;
+    const d3 u = mk3(bs[0], bs[1], bs[2]), v = mk3(bs[3], bs[4], bs[5]), org = mk3(bs[6], bs[7], bs[8]);
+    for (uint64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {  // project_to_plane (:36-44)
+      const d3 d = sub3(mk3(b.inl[3 * i], b.inl[3 * i + 1], b.inl[3 * i + 2]), org);
+      proj[i] = P2{dot3(d, u), dot3(d, v)};
+    }
+    __syncthreads();
+    if (n > 3 && directions >= 3) {
+      for (int j0 = 0; j0 < directions; j0 += 16) {
+        const int nd = min(16, directions - j0);
+        double bd[16];
+        int bi[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          bd[q] = -CUDART_INF;
+          bi[q] = -1;
+        }
+        for (uint64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+          const P2 q2 = proj[i];
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            if (q < nd) {
+              const double dd = q2.x * sdir[2 * (j0 + q)] + q2.y * sdir[2 * (j0 + q) + 1];
+              if (dd > bd[q] || (dd == bd[q] && bi[q] >= 0 && lex_less(q2, proj[bi[q]]))) {
+                bd[q] = dd;
+                bi[q] = static_cast<int>(i);
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            const double od = __shfl_down_sync(0xffffffffu, bd[q], o);
+            const int oi = __shfl_down_sync(0xffffffffu, bi[q], o);
+            if (ext_better(od, oi, bd[q], bi[q], proj)) {
+              bd[q] = od;
+              bi[q] = oi;
+            }
+          }
+          if (lane == 0) {
+            ex_dot[wid * 16 + q] = bd[q];
+            ex_idx[wid * 16 + q] = bi[q];
+          }
+        }
+        __syncthreads();
+        if (threadIdx.x < static_cast<unsigned>(nd)) {
+          const int q = static_cast<int>(threadIdx.x);
+          double best = -CUDART_INF;
+          int bix = -1;
+          for (unsigned w2 = 0; w2 < (blockDim.x >> 5); ++w2)
+            if (ext_better(ex_dot[w2 * 16 + q], ex_idx[w2 * 16 + q], best, bix, proj)) {
+              best = ex_dot[w2 * 16 + q];
+              bix = ex_idx[w2 * 16 + q];
+            }
+          b.pext_dot[static_cast<uint64_t>(c) * 64 + j0 + q] = best;
+          b.pext_idx[static_cast<uint64_t>(c) * 64 + j0 + q] = bix;
+        }
+        __syncthreads();
+      }
+    }
+  }
+}
+
+__global__ void k_poly_inner(Counters* ctr, SegBufs b, int directions) {
+  __shared__ P2 ext[64];
+  const uint32_t F = ctr->nfits;
+  const P2* proj = reinterpret_cast<const P2*>(b.proj);
   for (uint32_t f = blockIdx.x; f < F; f += gridDim.x) {
-    const uint64_t o = b.ioff[f];
+    const uint32_t n = b.ioff[f + 1] - b.ioff[f];
+    const bool filter = n > 3 && directions >= 3;
+    if (filter && threadIdx.x < static_cast<unsigned>(directions)) {
+      const int j = static_cast<int>(threadIdx.x);
+      double best = -CUDART_INF;
+      int bix = -1;
+      for (uint32_t c = b.pch_off[f]; c < b.pch_off[f + 1]; ++c) {
+        const double od = b.pext_dot[static_cast<uint64_t>(c) * 64 + j];
+        const int oi = b.pext_idx[static_cast<uint64_t>(c) * 64 + j];
+        if (ext_better(od, oi, best, bix, proj)) {
+          best = od;
+          bix = oi;
+        }
+      }
+      ext[j] = bix >= 0 ? proj[bix] : P2{0.0, 0.0};
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t ni = 0;
+      if (filter) {  // inner = monotone_chain(extremes)
+        P2 e[64];
+        for (int j = 0; j < directions; ++j) e[j] = ext[j];
+        for (int a = 1; a < directions; ++a) {
+          const P2 t = e[a];
+          int q = a;
+          while (q > 0 && lex_less(t, e[q - 1])) {
+            e[q] = e[q - 1];
+            --q;
+          }
+          e[q] = t;
+        }
+        uint32_t m = 0;
+        for (int j = 0; j < directions; ++j)
+          if (m == 0 || !(e[j].x == e[m - 1].x && e[j].y == e[m - 1].y)) e[m++] = e[j];
+        ni = chain_sorted(e, m, reinterpret_cast<P2*>(b.inner) + 130 * f);
+      }
+      b.ninner[f] = ni;  // < 3: no filtering (hull_filter returns all points)
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(256) k_poly_keep(Counters* ctr, SegBufs b) {
+  __shared__ P2 inner[130];
+  __shared__ uint32_t ni_s;
+  const uint32_t F = ctr->nfits, nchunks = ctr->poly_chunks;
+  const P2* proj = reinterpret_cast<const P2*>(b.proj);
+  for (uint32_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    const uint32_t f = poly_fit_of_chunk(b, F, c);
+    if (threadIdx.x == 0) ni_s = b.ninner[f];
+    __syncthreads();
+    const uint32_t ni = ni_s >= 3 ? ni_s : 0u;
+    for (uint32_t k = threadIdx.x; k < ni; k += blockDim.x) inner[k] = reinterpret_cast<const P2*>(b.inner)[130 * f + k];
+    __syncthreads();
+    const uint64_t i0 = b.ioff[f] + static_cast<uint64_t>(c - b.pch_off[f]) * kPolyChunk;
+    const uint64_t i1 = min(static_cast<uint64_t>(b.ioff[f + 1]), i0 + kPolyChunk);
+    P2* surv = reinterpret_cast<P2*>(b.surv) + 2 * static_cast<uint64_t>(b.ioff[f]);
+    for (uint64_t base = i0; base < i1; base += blockDim.x) {
+      const uint64_t i = base + threadIdx.x;
+      bool keep = false;
+      P2 q{0.0, 0.0};
+      if (i < i1) {
+        q = proj[i];
+        keep = ni == 0;
+        for (uint32_t e = 0; e < ni && !keep; ++e)
+          if (cross2(inner[e], inner[(e + 1) % ni], q) <= 0.0) keep = true;
+      }
+      const unsigned km = __ballot_sync(0xffffffffu, keep);
+      uint32_t at = 0;
+      if (km) {
+        const int first = __ffs(km) - 1;
+        if (static_cast<int>(lane_id()) == first) at = atomicAdd(&b.nsurv[f], static_cast<uint32_t>(__popc(km)));
+        at = __shfl_sync(0xffffffffu, at, first);
+      }
+      if (keep) surv[at + __popc(km & lanemask_lt())] = q;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void k_poly_hull(Counters* ctr, SegBufs b, double min_area) {
+  extern __shared__ P2 sm_pts[];  // kHullSmem points
+  __shared__ uint32_t n_uniq, voff;
+  __shared__ double area_s;
+  const uint32_t F = (ctr->overflow & (kOverflowFits | kOverflowMembers)) ? 0u : ctr->nfits;
+  for (uint32_t f = blockIdx.x; f < F; f += gridDim.x) {
     const uint32_t n = b.ioff[f + 1] - b.ioff[f];
     const double* pl = b.ref_model + 4 * f;
     double* rd = b.prec_d + 8 * f;
@@ -921,129 +1153,13 @@ __global__ void k_polygon(Counters* ctr, SegBufs b, const double* dirtab, int di
       ri[2] = 0;
       ri[3] = 0;
     }
-    if (n < 3) {
+    if (n < 3) {  // make_polygon: nullopt
       __syncthreads();
       continue;
     }
-    const d3 nrm = mk3(pl[0], pl[1], pl[2]);
-    if (threadIdx.x == 0) {  // plane_basis (polygonize.cpp:21-34)
-      int least = 0;
-      const double an[3] = {fabs(nrm.x), fabs(nrm.y), fabs(nrm.z)};
-      if (an[1] < an[least]) least = 1;
-      if (an[2] < an[least]) least = 2;
-      const d3 axis = mk3(least == 0 ? 1.0 : 0.0, least == 1 ? 1.0 : 0.0, least == 2 ? 1.0 : 0.0);
-      const d3 u = normalized3(sub3(axis, scl3(dot3(nrm, axis), nrm)));
-      const d3 v = cross3(nrm, u);
-      const d3 org = scl3(pl[3], nrm);
-      basis[0] = u.x; basis[1] = u.y; basis[2] = u.z;
-      basis[3] = v.x; basis[4] = v.y; basis[5] = v.z;
-      basis[6] = org.x; basis[7] = org.y; basis[8] = org.z;
-      n_surv = 0;
-    }
-    __syncthreads();
-    const d3 u = mk3(basis[0], basis[1], basis[2]);
-    const d3 v = mk3(basis[3], basis[4], basis[5]);
-    const d3 org = mk3(basis[6], basis[7], basis[8]);
-    const double* Pin = b.inl + 3 * o;
-    P2* proj = reinterpret_cast<P2*>(b.proj) + o;
-    P2* surv = reinterpret_cast<P2*>(b.surv) + 2 * o;  // 2n slots
-    P2* hullg = reinterpret_cast<P2*>(b.hull) + 2 * o;  // 2n slots
-    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {  // project_to_plane (:36-44)
-      const d3 d = sub3(mk3(Pin[3 * i], Pin[3 * i + 1], Pin[3 * i + 2]), org);
-      proj[i] = P2{dot3(d, u), dot3(d, v)};
-    }
-    __syncthreads();
-    // hull_filter (:50-114): extreme point along each direction (larger dot,
-    // ties to the lexicographically smaller point) -- all directions of a
-    // chunk in one pass over the points, then a warp-shuffle + smem reduction.
-    bool filter = n > 3 && directions >= 3;
-    if (filter) {
-      for (int j0 = 0; j0 < directions; j0 += 16) {
-        const int nd = min(16, directions - j0);
-        double bd[16];
-        int bi[16];
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          bd[q] = -CUDART_INF;
-          bi[q] = -1;
-        }
-        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-          const P2 q2 = proj[i];
-#pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            if (q < nd) {
-              const double dd = q2.x * sdir[2 * (j0 + q)] + q2.y * sdir[2 * (j0 + q) + 1];
-              if (dd > bd[q] || (dd == bd[q] && bi[q] >= 0 && lex_less(q2, proj[bi[q]]))) {
-                bd[q] = dd;
-                bi[q] = static_cast<int>(i);
-              }
-            }
-          }
-        }
-        const unsigned lane = lane_id(), wid = threadIdx.x >> 5;
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            const double od = __shfl_down_sync(0xffffffffu, bd[q], o);
-            const int oi = __shfl_down_sync(0xffffffffu, bi[q], o);
-            if (oi >= 0 && (bi[q] < 0 || od > bd[q] || (od == bd[q] && lex_less(proj[oi], proj[bi[q]])))) {
-              bd[q] = od;
-              bi[q] = oi;
-            }
-          }
-          if (lane == 0) {
-            ex_dot[wid * 16 + q] = bd[q];
-            ex_idx[wid * 16 + q] = bi[q];
-          }
-        }
-        __syncthreads();
-        if (threadIdx.x < static_cast<unsigned>(nd)) {
-          const int q = static_cast<int>(threadIdx.x);
-          double best = -CUDART_INF;
-          int bix = -1;
-          for (unsigned w2 = 0; w2 < (blockDim.x >> 5); ++w2) {
-            const double od = ex_dot[w2 * 16 + q];
-            const int oi = ex_idx[w2 * 16 + q];
-            if (oi >= 0 && (bix < 0 || od > best || (od == best && lex_less(proj[oi], proj[bix])))) {
-              best = od;
-              bix = oi;
-            }
-          }
-          extremes[j0 + q] = bix >= 0 ? proj[bix] : P2{0.0, 0.0};
-        }
-        __syncthreads();
-      }
-      if (threadIdx.x == 0) {  // inner = monotone_chain(extremes)
-        P2 e[64];
-        for (int j = 0; j < directions; ++j) e[j] = extremes[j];
-        for (int a = 1; a < directions; ++a) {  // insertion sort (lex)
-          const P2 t = e[a];
-          int c = a;
-          while (c > 0 && lex_less(t, e[c - 1])) {
-            e[c] = e[c - 1];
-            --c;
-          }
-          e[c] = t;
-        }
-        uint32_t m = 0;
-        for (int j = 0; j < directions; ++j)
-          if (m == 0 || !(e[j].x == e[m - 1].x && e[j].y == e[m - 1].y)) e[m++] = e[j];
-        n_inner = chain_sorted(e, m, inner);
-      }
-      __syncthreads();
-      if (n_inner < 3) filter = false;
-    }
-    const uint32_t ni = filter ? n_inner : 0;
-    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-      const P2 q = proj[i];
-      bool keep = !filter;
-      for (uint32_t e = 0; e < ni && !keep; ++e)
-        if (cross2(inner[e], inner[(e + 1) % ni], q) <= 0.0) keep = true;
-      if (keep) surv[atomicAdd(&n_surv, 1u)] = q;
-    }
-    __syncthreads();
-    const uint32_t ns = n_surv;
+    const uint32_t ns = b.nsurv[f];
+    P2* surv = reinterpret_cast<P2*>(b.surv) + 2 * static_cast<uint64_t>(b.ioff[f]);  // 2n slots
+    P2* hullg = reinterpret_cast<P2*>(b.hull) + 2 * static_cast<uint64_t>(b.ioff[f]);
     uint32_t np2 = 1;
     while (np2 < ns) np2 <<= 1;
     const bool in_smem = np2 <= static_cast<uint32_t>(kHullSmem);
@@ -1057,41 +1173,40 @@ __global__ void k_polygon(Counters* ctr, SegBufs b, const double* dirtab, int di
       for (uint32_t i = 0; i < ns; ++i)
         if (m == 0 || !(arr[i].x == arr[m - 1].x && arr[i].y == arr[m - 1].y)) arr[m++] = arr[i];
       n_uniq = chain_sorted(arr, m, hullg);
-    }
-    __syncthreads();
-    const uint32_t m = n_uniq;
-    if (m >= 3) {
-      __shared__ uint32_t voff;
-      __shared__ double area_s;
-      if (threadIdx.x == 0) {
+      voff = 0xffffffffu;
+      area_s = 0.0;
+      const uint32_t mh = n_uniq;
+      if (mh >= 3) {
         double twice = 0.0;  // polygon_area (:146-154)
-        for (uint32_t i = 0; i < m; ++i) {
-          const P2 a = hullg[i], c = hullg[(i + 1) % m];
+        for (uint32_t i = 0; i < mh; ++i) {
+          const P2 a = hullg[i], c = hullg[(i + 1) % mh];
           twice += a.x * c.y - c.x * a.y;
         }
         area_s = 0.5 * twice;
-        voff = 0xffffffffu;
         if (area_s >= min_area) {
-          const uint32_t at = atomicAdd(&ctr->pool_used, m);
-          if (at + m <= b.pool_cap) voff = at;
+          const uint32_t at = atomicAdd(&ctr->pool_used, mh);
+          if (at + mh <= b.pool_cap) voff = at;
           else atomicOr(&ctr->overflow, kOverflowPool);
         }
-        rd[4] = area_s;
-        ri[2] = (voff != 0xffffffffu) ? static_cast<int32_t>(m) : 0;
-        ri[3] = static_cast<int32_t>(voff == 0xffffffffu ? 0 : voff);
       }
-      __syncthreads();
-      if (voff != 0xffffffffu) {
-        for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {  // lift_from_plane (:46-48)
-          const P2 q = hullg[i];
-          const d3 p3 = add3(add3(org, scl3(q.x, u)), scl3(q.y, v));
-          double* dst = b.pool + 5 * (static_cast<uint64_t>(voff) + i);
-          dst[0] = q.x;
-          dst[1] = q.y;
-          dst[2] = p3.x;
-          dst[3] = p3.y;
-          dst[4] = p3.z;
-        }
+      rd[4] = area_s;
+      ri[2] = (voff != 0xffffffffu) ? static_cast<int32_t>(mh) : 0;
+      ri[3] = static_cast<int32_t>(voff == 0xffffffffu ? 0 : voff);
+    }
+    __syncthreads();
+    const uint32_t m = n_uniq;
+    if (voff != 0xffffffffu) {
+      const double* bs = b.basis + 9 * f;
+      const d3 u = mk3(bs[0], bs[1], bs[2]), v = mk3(bs[3], bs[4], bs[5]), org = mk3(bs[6], bs[7], bs[8]);
+      for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {  // lift_from_plane (:46-48)
+        const P2 q = hullg[i];
+        const d3 p3 = add3(add3(org, scl3(q.x, u)), scl3(q.y, v));
+        double* dst = b.pool + 5 * (static_cast<uint64_t>(voff) + i);
+        dst[0] = q.x;
+        dst[1] = q.y;
+        dst[2] = p3.x;
+        dst[3] = p3.y;
+        dst[4] = p3.z;
       }
     }
     __syncthreads();

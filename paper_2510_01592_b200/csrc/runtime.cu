@@ -205,7 +205,8 @@ struct Seg {
                     b.parent, b.label, b.cnt, b.cid, b.big_flag, b.big_pos, b.klabel, b.ksize,
                     b.kpoff, b.H, b.mx, b.my, b.mz, b.cand, b.cand_cnt, b.win_it, b.win_cnt,
                     b.fid, b.fit_cluster, b.ioff, b.fit_model, b.fit_meta, b.ref_model, b.inl,
-                    b.proj, b.surv, b.hull, b.prec_d, b.prec_i, b.pool, bsum, dirtab};
+                    b.proj, b.surv, b.hull, b.basis, b.pch_off, b.pext_dot, b.pext_idx, b.inner,
+                    b.ninner, b.nsurv, b.prec_d, b.prec_i, b.pool, bsum, dirtab};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     b = SegBufs{};
@@ -269,6 +270,14 @@ struct Seg {
       b.proj = dalloc<double>(2ull * icap);
       b.surv = dalloc<double>(4ull * icap);
       b.hull = dalloc<double>(4ull * icap);
+      b.basis = dalloc<double>(9 * kClusterBins);
+      b.pch_off = dalloc<uint32_t>(kClusterBins + 1);
+      b.pch_cap = icap / kPolyChunk + kClusterBins + 1;
+      b.pext_dot = dalloc<double>(64ull * b.pch_cap);
+      b.pext_idx = dalloc<int32_t>(64ull * b.pch_cap);
+      b.inner = dalloc<double>(2ull * 130 * kClusterBins);
+      b.ninner = dalloc<uint32_t>(kClusterBins);
+      b.nsurv = dalloc<uint32_t>(kClusterBins);
       b.prec_d = dalloc<double>(8 * kClusterBins);
       b.prec_i = dalloc<int32_t>(4 * kClusterBins);
       b.pool_cap = icap;
@@ -402,7 +411,7 @@ struct vp_grid {
     std::memset(h_fp, 0, sizeof(FrameParams));
     const uint32_t vcap = static_cast<uint32_t>(std::min<uint64_t>(C, 1u << 22));
     seg.ensure(vcap, vcap, vcap, 100, gd.nwords);
-    ck(cudaFuncSetAttribute(k_polygon, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    ck(cudaFuncSetAttribute(k_poly_hull, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             kHullSmem * 16), "smem attr");
     ck(cudaStreamSynchronize(stream), "init sync");
   }
@@ -585,9 +594,9 @@ struct vp_grid {
     LAUNCH(k_cluster_assign, kWide, kThreads, 0, stream, ctr, seg.b);
     LAUNCH(k_cluster_setup, 1, 1024, 0, stream, ctr, seg.b);
     const int nch = static_cast<int>(seg.hstride);
-    LAUNCH(k_member_hist, nch, 32, 0, stream, ctr, seg.b, seg.hstride);
+    LAUNCH(k_member_hist, std::min(nch, 148 * 16), 32, 0, stream, ctr, seg.b, seg.hstride);
     LAUNCH(k_member_hscan, kWide, kThreads, 0, stream, ctr, seg.b, seg.hstride);
-    LAUNCH(k_member_scatter, nch, 32, 0, stream, ctr, seg.b, seg.hstride);
+    LAUNCH(k_member_scatter, std::min(nch, 148 * 16), 32, 0, stream, ctr, seg.b, seg.hstride);
   }
   void launch_ransac(const RansacDev& rd) {
     LAUNCH(k_ransac_hyp, kWide, kThreads, 0, stream, ctr, rd, seg.b);
@@ -601,7 +610,11 @@ struct vp_grid {
   }
   void launch_polygon(int dirs, double min_area) {
     seg.ensure_dirs(dirs, stream);
-    LAUNCH(k_polygon, 148 * 2, 256, kHullSmem * 16, stream, ctr, seg.b, seg.dirtab, dirs, min_area);
+    LAUNCH(k_poly_setup, 1, 1024, 0, stream, ctr, seg.b);
+    LAUNCH(k_poly_extremes, kWide, 256, 0, stream, ctr, seg.b, seg.dirtab, dirs);
+    LAUNCH(k_poly_inner, 148 * 2, 64, 0, stream, ctr, seg.b, dirs);
+    LAUNCH(k_poly_keep, kWide, 256, 0, stream, ctr, seg.b);
+    LAUNCH(k_poly_hull, 148 * 2, 256, kHullSmem * 16, stream, ctr, seg.b, min_area);
   }
 
   // The fused segment(): voxel_frame_polygons (pipeline.cpp:43-85) on device.

@@ -76,6 +76,7 @@ struct Counters {
   uint32_t overflow;  // bit flags, see kOverflow*
   uint32_t padded_members;
   uint32_t inliers;
+  uint32_t poly_chunks;
 };
 
 constexpr uint32_t kOverflowOcc = 1u;

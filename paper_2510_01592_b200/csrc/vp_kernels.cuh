@@ -11,8 +11,9 @@ constexpr int kScanThreads = 256;
 constexpr int kScanItems = 8;
 constexpr int kScanPerBlock = kScanThreads * kScanItems;  // 2048
 constexpr int kClusterBins = 2048;  // clusters handled by the counting sort per pass
-constexpr int kChunk = 2048;        // ordinals per counting-sort chunk
+constexpr int kChunk = 256;         // ordinals per counting-sort chunk (one warp)
 constexpr int kHullSmem = 4096;     // survivors sorted in shared memory
+constexpr int kPolyChunk = 1024;    // inlier points per polygon-stage block
 
 // Block-wide exclusive prefix sum (any blockDim multiple of 32, <= 1024).
 __device__ __forceinline__ uint32_t block_exclusive_u32(uint32_t v) {
@@ -157,6 +158,14 @@ struct SegBufs {
   double* surv;          // 2 * 2Icap
   double* hull;          // 2 * 2Icap
   // polygon records (kClusterBins) + vertex pool
+  double* basis;         // 9 per fit: u, v, origin (plane_basis)
+  uint32_t* pch_off;     // per fit chunk offsets (nfits+1)
+  double* pext_dot;      // 64 per chunk: per-direction extreme dot
+  int32_t* pext_idx;     // 64 per chunk: its point index
+  double* inner;         // 2*130 per fit: inner polygon
+  uint32_t* ninner;
+  uint32_t* nsurv;       // survivors per fit
+  uint32_t pch_cap;
   double* prec_d;        // 8 per fit: normal(3) offset area
   int32_t* prec_i;       // 4 per fit: inlier_count label nv voff
   double* pool;          // 5 per vertex: u v x y z
@@ -216,7 +225,10 @@ __global__ void k_ransac_select(Counters* ctr, RansacDev rp, SegBufs b);
 __global__ void k_fit_setup(Counters* ctr, RansacDev rp, SegBufs b);
 __global__ void k_ransac_extract(Counters* ctr, RansacDev rp, SegBufs b);
 __global__ void k_refine(Counters* ctr, SegBufs b, d3 up, int refine, int exact);
-__global__ void k_polygon(Counters* ctr, SegBufs b, const double* dirtab, int directions,
-                          double min_area);
+__global__ void k_poly_setup(Counters* ctr, SegBufs b);
+__global__ void k_poly_extremes(Counters* ctr, SegBufs b, const double* dirtab, int directions);
+__global__ void k_poly_inner(Counters* ctr, SegBufs b, int directions);
+__global__ void k_poly_keep(Counters* ctr, SegBufs b);
+__global__ void k_poly_hull(Counters* ctr, SegBufs b, double min_area);
 
 }  // namespace vp
