@@ -235,7 +235,7 @@ vp_grid* vp_pipeline_grid(vp_pipeline* pl);
 void* vp_pipeline_stream(vp_pipeline* pl);
 /* Counters of the last frame: cleared, freed, touched, discarded, dropped,
    occupied, V_occ, V_step, clusters, fits, padded members, inliers,
-   polygon vertices, newly occupied, touched groups, overflow flags. */
+   polygon vertices, newly occupied, largest hull-survivor set, overflow flags. */
 int vp_pipeline_counters(vp_pipeline* pl, uint64_t out[16]);
 /* One frame of run_frames: clear_rays, integrate_frame, recenter-if-moved,
    voxel_frame_polygons. out may be NULL (polygons stay on the device). */

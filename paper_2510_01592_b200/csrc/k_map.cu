@@ -229,18 +229,12 @@ __global__ void __launch_bounds__(256) k_integrate_fold(GridDesc g, const FrameP
 // cells next to the sensor from serialising on L2 atomics); k_clear_apply
 // then counts unique cells, frees occupied ones and zeroes the mask.
 // ---------------------------------------------------------------------------
-// Mark one traversed interior cell. Lanes of a warp that step through the same
-// cell in the same iteration (adjacent pixels near the sensor) are merged with
-// __match_any_sync so only one fire-and-forget RED.OR per distinct cell is
-// issued; nothing in the loop waits on memory.
-__device__ __forceinline__ void mark_cell(const GridDesc& g, int x, int y, int z) {
-  const uint64_t w = word_of(g, x, y, z);
-  const unsigned active = __activemask();
-  const unsigned long long key = (w << 5) | static_cast<unsigned>(z & 31);
-  const unsigned peers = __match_any_sync(active, key);
-  if ((__ffs(peers) - 1) == static_cast<int>(lane_id())) atomicOr(g.clr + w, 1u << (z & 31));
-}
-
+// One thread per ray (voxel_grid.cpp:122-178, the reference's DDA arithmetic
+// verbatim). The loop keeps the cell's 32-bit bitmap word index incrementally
+// and selects the stepped axis without branches; each traversed interior cell
+// is marked with a fire-and-forget RED.OR, after lanes of the warp standing in
+// the same cell this iteration (adjacent pixels near the sensor) are merged
+// with a 32-bit __match_any_sync. Nothing in the loop waits on memory.
 __global__ void __launch_bounds__(256) k_clear_walk(GridDesc g, const FrameParams* __restrict__ fp) {
   const uint64_t n = fp->n;
   const double res = g.res;
@@ -251,6 +245,10 @@ __global__ void __launch_bounds__(256) k_clear_walk(GridDesc g, const FrameParam
   const double a0 = fp->t[0], a1 = fp->t[1], a2 = fp->t[2];
   const int oc0 = w2i(a0, lo0, res), oc1 = w2i(a1, lo1, res), oc2 = w2i(a2, lo2, res);
   const int max_steps = g.ex + g.ey + g.ez + 4;
+  const uint32_t xstride = static_cast<uint32_t>(g.ey) * static_cast<uint32_t>(g.W);
+  const uint32_t ystride = static_cast<uint32_t>(g.W);
+  uint32_t* __restrict__ clr = g.clr;
+  const unsigned lane = lane_id();
   for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const float* pp = fp->pts + 3 * i;
@@ -306,35 +304,36 @@ __global__ void __launch_bounds__(256) k_clear_walk(GridDesc g, const FrameParam
     VP_INIT(d1, c1, lo1, e1, s1, tm1, td1)
     VP_INIT(d2, c2, lo2, e2, s2, tm2, td2)
 #undef VP_INIT
+    uint32_t row = static_cast<uint32_t>(c0) * xstride + static_cast<uint32_t>(c1) * ystride;
+    const int dx_row = s0 * static_cast<int>(xstride), dy_row = s1 * static_cast<int>(ystride);
     for (int s = 0; s < max_steps; ++s) {
       const bool is_o = c0 == oc0 && c1 == oc1 && c2 == oc2;
       const bool is_e = c0 == ec0 && c1 == ec1 && c2 == ec2;
-      if (!is_o && !is_e) mark_cell(g, c0, c1, c2);
+      if (!is_o && !is_e) {
+        const uint32_t w = row + (static_cast<uint32_t>(c2) >> 5);
+        const uint32_t key = (w << 5) | (static_cast<uint32_t>(c2) & 31u);
+        const unsigned peers = __match_any_sync(__activemask(), key);
+        if (static_cast<unsigned>(__ffs(peers) - 1) == lane) atomicOr(clr + w, 1u << (c2 & 31));
+      }
       // m = argmin t_max, ties to the lower axis (voxel_grid.cpp:170-172)
-      int m = 0;
-      double tm = tm0;
-      if (tm1 < tm) {
-        m = 1;
-        tm = tm1;
-      }
-      if (tm2 < tm) {
-        m = 2;
-        tm = tm2;
-      }
+      const bool m1 = tm1 < tm0;
+      const double tm01 = m1 ? tm1 : tm0;
+      const bool m2 = tm2 < tm01;
+      const double tm = m2 ? tm2 : tm01;
       if (tm >= t1) break;
-      if (m == 0) {
-        c0 += s0;
-        if (c0 < 0 || c0 >= g.ex) break;
-        tm0 += td0;
-      } else if (m == 1) {
-        c1 += s1;
-        if (c1 < 0 || c1 >= g.ey) break;
-        tm1 += td1;
-      } else {
-        c2 += s2;
-        if (c2 < 0 || c2 >= g.ez) break;
-        tm2 += td2;
-      }
+      const bool m0 = !m1 && !m2;
+      const bool m1s = m1 && !m2;
+      c0 += m0 ? s0 : 0;
+      c1 += m1s ? s1 : 0;
+      c2 += m2 ? s2 : 0;
+      if (static_cast<unsigned>(c0) >= static_cast<unsigned>(g.ex) ||
+          static_cast<unsigned>(c1) >= static_cast<unsigned>(g.ey) ||
+          static_cast<unsigned>(c2) >= static_cast<unsigned>(g.ez))
+        break;
+      row += m0 ? dx_row : (m1s ? dy_row : 0);
+      tm0 = m0 ? tm0 + td0 : tm0;
+      tm1 = m1s ? tm1 + td1 : tm1;
+      tm2 = m2 ? tm2 + td2 : tm2;
     }
   }
 }
@@ -395,11 +394,12 @@ __global__ void k_recenter(GridDesc g, const FrameParams* __restrict__ fp, Count
   uint32_t* newb = fp->occ_post;
   const int sx = fp->shift[0], sy = fp->shift[1], sz = fp->shift[2];
   unsigned long long dropped = 0;
-  for (uint64_t u = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; u < g.nwords;
-       u += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const uint64_t row = u / g.W;
-    const int wz = static_cast<int>(u % g.W);
-    const int y = static_cast<int>(row % g.ey), x = static_cast<int>(row / g.ey);
+  const uint32_t nw = static_cast<uint32_t>(g.nwords);  // < 2^32 (grid creation check)
+  const uint32_t W = static_cast<uint32_t>(g.W), ey = static_cast<uint32_t>(g.ey);
+  for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < nw; u += gridDim.x * blockDim.x) {
+    const uint32_t row = u / W;
+    const int wz = static_cast<int>(u - row * W);
+    const int y = static_cast<int>(row % ey), x = static_cast<int>(row / ey);
     // new word: destination (x,y,z) reads source (x+sx, y+sy, z+sz)
     const long long xs = static_cast<long long>(x) + sx, ys = static_cast<long long>(y) + sy;
     uint32_t nv = 0;

@@ -689,37 +689,76 @@ __global__ void k_fit_setup(Counters* ctr, RansacDev rp, SegBufs b) {
     ctr->nfits = carry_f;
     ctr->inliers = carry_i;
     b.ioff[carry_f] = carry_i;
+    // member chunks of the fits (for the multi-block ordered extraction)
+    uint32_t ch = 0;
+    for (uint32_t f = 0; f < carry_f; ++f) {
+      b.fch_off[f] = ch;
+      ch += (b.ksize[b.fit_cluster[f]] + kPolyChunk - 1) / kPolyChunk;
+    }
+    b.fch_off[carry_f] = ch;
+    ctr->fit_chunks = ch;
     ctr->skipped = n_skip;
     ctr->unfit = n_unfit;
     if (carry_i > b.Icap) atomicOr(&ctr->overflow, kOverflowFits);
   }
 }
 
-// Ordered inlier extraction (plane_fit.cpp:102-104), one block per fit.
-__global__ void k_ransac_extract(Counters* ctr, RansacDev rp, SegBufs b) {
-  const uint32_t F = ctr->nfits;
+// Ordered inlier extraction (plane_fit.cpp:102-104) over member chunks of
+// kPolyChunk: count per chunk, one exclusive scan over all chunks (fits and
+// their inliers are both concatenated in fit order), then a block-ordered
+// write per chunk.
+__device__ __forceinline__ uint32_t fit_of_chunk(const SegBufs& b, uint32_t F, uint32_t c) {
+  uint32_t lo = 0, hi = F;
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (b.fch_off[mid] <= c) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void k_extract_count(Counters* ctr, RansacDev rp, SegBufs b) {
   if (ctr->overflow & (kOverflowFits | kOverflowMembers)) return;
-  __shared__ uint32_t run;
-  for (uint32_t f = blockIdx.x; f < F; f += gridDim.x) {
+  const uint32_t F = ctr->nfits, nch = ctr->fit_chunks;
+  for (uint32_t c = blockIdx.x; c < nch; c += gridDim.x) {
+    const uint32_t f = fit_of_chunk(b, F, c);
     const uint32_t k = b.fit_cluster[f];
     const uint32_t M = b.ksize[k], o = b.kpoff[k];
+    const uint32_t j0 = (c - b.fch_off[f]) * kPolyChunk, j1 = min(M, j0 + kPolyChunk);
     const d3 n = mk3(b.fit_model[4 * f], b.fit_model[4 * f + 1], b.fit_model[4 * f + 2]);
     const double off = b.fit_model[4 * f + 3];
-    const uint32_t dst0 = b.ioff[f];
-    if (threadIdx.x == 0) run = 0;
+    uint32_t cnt = 0;
+    for (uint32_t j = j0 + threadIdx.x; j < j1; j += blockDim.x)
+      cnt += fabs(dot3(n, mk3(b.mx[o + j], b.my[o + j], b.mz[o + j])) - off) <= rp.eps ? 1u : 0u;
+    cnt = block_sum_u32(cnt);
+    if (threadIdx.x == 0) b.ccount[c] = cnt;
+  }
+}
+
+__global__ void k_extract_emit(Counters* ctr, RansacDev rp, SegBufs b) {
+  if (ctr->overflow & (kOverflowFits | kOverflowMembers)) return;
+  __shared__ uint32_t run;
+  const uint32_t F = ctr->nfits, nch = ctr->fit_chunks;
+  for (uint32_t c = blockIdx.x; c < nch; c += gridDim.x) {
+    const uint32_t f = fit_of_chunk(b, F, c);
+    const uint32_t k = b.fit_cluster[f];
+    const uint32_t M = b.ksize[k], o = b.kpoff[k];
+    const uint32_t j0 = (c - b.fch_off[f]) * kPolyChunk, j1 = min(M, j0 + kPolyChunk);
+    const d3 n = mk3(b.fit_model[4 * f], b.fit_model[4 * f + 1], b.fit_model[4 * f + 2]);
+    const double off = b.fit_model[4 * f + 3];
+    if (threadIdx.x == 0) run = b.ccount[c];  // exclusive-scanned: first inlier slot
     __syncthreads();
-    for (uint32_t base = 0; base < M; base += blockDim.x) {
+    for (uint32_t base = j0; base < j1; base += blockDim.x) {
       const uint32_t j = base + threadIdx.x;
       d3 p = mk3(0.0, 0.0, 0.0);
       bool pred = false;
-      if (j < M) {
+      if (j < j1) {
         p = mk3(b.mx[o + j], b.my[o + j], b.mz[o + j]);
         pred = fabs(dot3(n, p) - off) <= rp.eps;
       }
       const uint32_t ex = block_exclusive_u32(pred ? 1u : 0u);
       const uint32_t r0 = run;
       if (pred) {
-        const uint64_t d = static_cast<uint64_t>(dst0) + r0 + ex;
+        const uint64_t d = static_cast<uint64_t>(r0) + ex;
         b.inl[3 * d] = p.x;
         b.inl[3 * d + 1] = p.y;
         b.inl[3 * d + 2] = p.z;
@@ -1158,6 +1197,7 @@ __global__ void k_poly_hull(Counters* ctr, SegBufs b, double min_area) {
       continue;
     }
     const uint32_t ns = b.nsurv[f];
+    if (threadIdx.x == 0) atomicMax(&ctr->surv_max, ns);
     P2* surv = reinterpret_cast<P2*>(b.surv) + 2 * static_cast<uint64_t>(b.ioff[f]);  // 2n slots
     P2* hullg = reinterpret_cast<P2*>(b.hull) + 2 * static_cast<uint64_t>(b.ioff[f]);
     uint32_t np2 = 1;

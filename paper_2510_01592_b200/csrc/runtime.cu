@@ -204,7 +204,7 @@ struct Seg {
                     b.own_status, b.step_flag, b.step_pos, b.st_idx, b.st_mean, b.st_normal,
                     b.parent, b.label, b.cnt, b.cid, b.big_flag, b.big_pos, b.klabel, b.ksize,
                     b.kpoff, b.H, b.mx, b.my, b.mz, b.cand, b.cand_cnt, b.win_it, b.win_cnt,
-                    b.fid, b.fit_cluster, b.ioff, b.fit_model, b.fit_meta, b.ref_model, b.inl,
+                    b.fid, b.fit_cluster, b.ioff, b.fch_off, b.ccount, b.fit_model, b.fit_meta, b.ref_model, b.inl,
                     b.proj, b.surv, b.hull, b.basis, b.pch_off, b.pext_dot, b.pext_idx, b.inner,
                     b.ninner, b.nsurv, b.prec_d, b.prec_i, b.pool, bsum, dirtab};
     for (void* p : ptrs)
@@ -263,6 +263,9 @@ struct Seg {
       b.fid = dalloc<int32_t>(kClusterBins);
       b.fit_cluster = dalloc<uint32_t>(kClusterBins);
       b.ioff = dalloc<uint32_t>(kClusterBins + 1);
+      b.fch_off = dalloc<uint32_t>(kClusterBins + 1);
+      b.cch_cap = mcap / kPolyChunk + kClusterBins + 1;
+      b.ccount = dalloc<uint32_t>(b.cch_cap);
       b.fit_model = dalloc<double>(4 * kClusterBins);
       b.fit_meta = dalloc<int32_t>(2 * kClusterBins);
       b.ref_model = dalloc<double>(4 * kClusterBins);
@@ -603,7 +606,9 @@ struct vp_grid {
     LAUNCH(k_ransac_count, kWide, kThreads, 0, stream, ctr, rd, seg.b);
     LAUNCH(k_ransac_select, kWide, kThreads, 0, stream, ctr, rd, seg.b);
     LAUNCH(k_fit_setup, 1, 1024, 0, stream, ctr, rd, seg.b);
-    LAUNCH(k_ransac_extract, 148 * 2, kThreads, 0, stream, ctr, rd, seg.b);
+    LAUNCH(k_extract_count, kWide, kThreads, 0, stream, ctr, rd, seg.b);
+    LAUNCH(k_scan_exclusive, 1, 1024, 0, stream, seg.b.ccount, 0u, &ctr->fit_chunks, nullptr, nullptr);
+    LAUNCH(k_extract_emit, kWide, kThreads, 0, stream, ctr, rd, seg.b);
   }
   void launch_refine(const double* up, int refine, int exact) {
     LAUNCH(k_refine, 148 * 2, 256, 0, stream, ctr, seg.b, d3{up[0], up[1], up[2]}, refine, exact);
@@ -1624,7 +1629,7 @@ int vp_pipeline_counters(vp_pipeline* pl, uint64_t out[16]) {
     const Counters& c = *pl->grid->h_ctr;
     const uint64_t v[16] = {c.cleared, c.freed, c.touched, c.discarded, c.dropped, c.occupied,
                             c.V, c.S, c.K, c.nfits, c.padded_members, c.inliers, c.pool_used,
-                            c.newly, c.ngroups, c.overflow};
+                            c.newly, c.surv_max, c.overflow};
     std::memcpy(out, v, sizeof v);
   });
 }

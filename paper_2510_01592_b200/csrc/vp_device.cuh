@@ -77,6 +77,8 @@ struct Counters {
   uint32_t padded_members;
   uint32_t inliers;
   uint32_t poly_chunks;
+  uint32_t fit_chunks;
+  uint32_t surv_max;     // largest hull-survivor set of the frame (diagnostic)
 };
 
 constexpr uint32_t kOverflowOcc = 1u;

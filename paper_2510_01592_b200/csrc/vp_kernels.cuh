@@ -150,6 +150,9 @@ struct SegBufs {
   int32_t* fid;          // fit index of a cluster or -1
   uint32_t* fit_cluster; // cluster of a fit
   uint32_t* ioff;        // per fit inlier offsets (nfits+1)
+  uint32_t* fch_off;     // per fit member-chunk offsets (nfits+1)
+  uint32_t* ccount;      // per member chunk: inlier count, then exclusive offset
+  uint32_t cch_cap;
   double* fit_model;     // 4 per fit (normal, offset): RANSAC winner
   int32_t* fit_meta;     // 2 per fit (inlier_count, label)
   double* ref_model;     // 4 per fit: refined
@@ -223,7 +226,8 @@ __global__ void k_ransac_hyp(Counters* ctr, RansacDev rp, SegBufs b);
 __global__ void k_ransac_count(Counters* ctr, RansacDev rp, SegBufs b);
 __global__ void k_ransac_select(Counters* ctr, RansacDev rp, SegBufs b);
 __global__ void k_fit_setup(Counters* ctr, RansacDev rp, SegBufs b);
-__global__ void k_ransac_extract(Counters* ctr, RansacDev rp, SegBufs b);
+__global__ void k_extract_count(Counters* ctr, RansacDev rp, SegBufs b);
+__global__ void k_extract_emit(Counters* ctr, RansacDev rp, SegBufs b);
 __global__ void k_refine(Counters* ctr, SegBufs b, d3 up, int refine, int exact);
 __global__ void k_poly_setup(Counters* ctr, SegBufs b);
 __global__ void k_poly_extremes(Counters* ctr, SegBufs b, const double* dirtab, int directions);

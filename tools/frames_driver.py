@@ -21,7 +21,7 @@ def main():
     wl = scenes.workload(a.workload)
     pl = native.Pipeline(wl.resolution, wl.extent, wl.frames[0].translation, native.default_params(seed=wl.seed))
     dev = [torch.from_numpy(f.points).cuda() for f in wl.frames]
-    names = "cleared freed touched discarded dropped occupied V S K fits padded inliers poolv newly groups overflow".split()
+    names = "cleared freed touched discarded dropped occupied V S K fits padded inliers poolv newly surv_max overflow".split()
     for k in range(a.frames):
         f = wl.frames[k % len(wl.frames)]
         if k and k % len(wl.frames) == 0:
