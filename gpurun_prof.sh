@@ -3,5 +3,5 @@ mkdir -p gpurun_out
 timeout 300 python tools/frames_driver.py --frames 30 --counters > gpurun_out/counters.txt 2>&1
 timeout 900 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.log
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python tools/frames_driver.py --frames 12 > gpurun_out/ncu_launch.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:'^k_(ccl_union|polygon|integrate_fold|clear_walk)$' -s 40 -c 4 -o gpurun_out/prof_top python tools/frames_driver.py --frames 12 > gpurun_out/ncu_full.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:'^k_(ccl_union|ccl_hook|poly_hull|clear_walk|normals)$' -s 50 -c 5 -o gpurun_out/prof_top python tools/frames_driver.py --frames 12 > gpurun_out/ncu_full.log 2>&1
 ls -la gpurun_out

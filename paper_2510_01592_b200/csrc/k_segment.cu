@@ -35,6 +35,46 @@ __global__ void k_normals(GridDesc g, const FrameParams* __restrict__ fp, Counte
     d3 sum = mk3(0.0, 0.0, 0.0);
     double s00 = 0.0, s01 = 0.0, s02 = 0.0, s11 = 0.0, s12 = 0.0, s22 = 0.0;
     int n = 0;
+    if (r == 1) {
+      // default 3x3x3 window, fully unrolled: the 9 row words and the occupied
+      // neighbours' cells are independent loads; the sums stay in dx,dy,dz order
+      const int za = z - 1, zb = z + 1;
+      uint32_t occ3[9];
+#pragma unroll
+      for (int q = 0; q < 9; ++q) {
+        const int X = x + q / 3 - 1, Y = y + q % 3 - 1;
+        uint32_t bits = 0;
+        if (X >= 0 && X < g.ex && Y >= 0 && Y < g.ey) {
+          const uint32_t* row = occ + (static_cast<uint64_t>(X) * g.ey + Y) * g.W;
+          const uint32_t wlo = za >= 0 ? __ldg(row + (za >> 5)) : 0u;
+          const uint32_t whi = (zb < g.ez && (zb >> 5) != (z >> 5)) ? __ldg(row + (zb >> 5)) : 0u;
+          const uint32_t wmid = ((z >> 5) == (za >> 5) && za >= 0) ? wlo : __ldg(row + (z >> 5));
+          const uint32_t b0 = za >= 0 ? ((((za >> 5) == (z >> 5)) ? wmid : wlo) >> (za & 31)) & 1u : 0u;
+          const uint32_t b1 = (wmid >> (z & 31)) & 1u;
+          const uint32_t b2 = zb < g.ez ? ((((zb >> 5) == (z >> 5)) ? wmid : whi) >> (zb & 31)) & 1u : 0u;
+          bits = b0 | (b1 << 1) | (b2 << 2);
+        }
+        occ3[q] = bits;
+      }
+#pragma unroll
+      for (int q = 0; q < 27; ++q) {
+        if ((occ3[q / 3] >> (q % 3)) & 1u) {
+          const Cell* c = g.cells + phys_index(g, off, x + q / 9 - 1, y + (q / 3) % 3 - 1, z + q % 3 - 1);
+          const double2 sxy = __ldg(reinterpret_cast<const double2*>(c));
+          const double szz = __ldg(&c->sz);
+          const double cd = static_cast<double>(__ldg(&c->count));
+          const d3 m = mk3(sxy.x / cd, sxy.y / cd, szz / cd);
+          sum = add3(sum, m);
+          s00 = s00 + m.x * m.x;
+          s01 = s01 + m.y * m.x;
+          s02 = s02 + m.z * m.x;
+          s11 = s11 + m.y * m.y;
+          s12 = s12 + m.z * m.y;
+          s22 = s22 + m.z * m.z;
+          ++n;
+        }
+      }
+    } else
     for (int dx = -r; dx <= r; ++dx) {
       const int X = x + dx;
       if (X < 0 || X >= g.ex) continue;
@@ -247,11 +287,12 @@ __global__ void __launch_bounds__(256) k_ccl_hook(Counters* ctr, SegDev sp, SegB
       const int z1 = (dx == 0 && dy == 0) ? z - 1 : min(z + w, zhi_m);
       if (z0 > z1) continue;
       uint32_t bits = m.row_span(X, Y, z0, z1 - z0 + 1);
-      while (bits) {
-        const int t = __ffs(bits) - 1;
+      if (!bits) continue;
+      // voxels of one (X, Y) column are consecutive ordinals: one map load
+      const int j0 = __ldg(m.map + m.slot(X, Y, z0 + __ffs(bits) - 1));
+      for (int j = j0; bits && j < best; ++j) {
         bits &= bits - 1;
-        const int j = __ldg(m.map + m.slot(X, Y, z0 + t));
-        if (j < best && adjacent(b, sp, mi, ni, j)) best = j;
+        if (adjacent(b, sp, mi, ni, j)) best = j;
       }
     }
 #pragma unroll
@@ -303,10 +344,12 @@ __global__ void __launch_bounds__(256) k_ccl_union(Counters* ctr, SegDev sp, Seg
       const int z1 = min(z + w, zmax);
       if (z0 > z1) continue;
       uint32_t bits = m.row_span(X, Y, z0, z1 - z0 + 1);
+      if (!bits) continue;
+      // voxels of one (X, Y) column are consecutive ordinals: one map load
+      int j = __ldg(m.map + m.slot(X, Y, z0 + __ffs(bits) - 1)) - 1;
       while (bits) {
-        const int t = __ffs(bits) - 1;
         bits &= bits - 1;
-        const int j = __ldg(m.map + m.slot(X, Y, z0 + t));
+        ++j;
         const int pj = __ldcg(parent + j);
         if (pj == ri) continue;  // already in i's tree
         if (!adjacent(b, sp, mi, ni, j)) continue;
