@@ -232,10 +232,10 @@ __global__ void __launch_bounds__(256) k_integrate_fold(GridDesc g, const FrameP
 // One thread per ray (voxel_grid.cpp:122-178, the reference's DDA arithmetic
 // verbatim). The loop keeps the cell's 32-bit bitmap word index incrementally
 // and selects the stepped axis without branches; each traversed interior cell
-// is marked with a fire-and-forget RED.OR, after lanes of the warp standing in
-// the same cell this iteration (adjacent pixels near the sensor) are merged
-// with a 32-bit __match_any_sync. Nothing in the loop waits on memory.
-__global__ void __launch_bounds__(256) k_clear_walk(GridDesc g, const FrameParams* __restrict__ fp) {
+// is marked with a fire-and-forget RED.OR; lanes of the warp standing in the
+// same cell as their left neighbour this iteration (adjacent pixels near the
+// sensor) skip it. Nothing in the loop waits on memory.
+__global__ void __launch_bounds__(256, 4) k_clear_walk(GridDesc g, const FrameParams* __restrict__ fp) {
   const uint64_t n = fp->n;
   const double res = g.res;
   const double lo0 = fp->origin_pre[0], lo1 = fp->origin_pre[1], lo2 = fp->origin_pre[2];
@@ -312,8 +312,12 @@ __global__ void __launch_bounds__(256) k_clear_walk(GridDesc g, const FrameParam
       if (!is_o && !is_e) {
         const uint32_t w = row + (static_cast<uint32_t>(c2) >> 5);
         const uint32_t key = (w << 5) | (static_cast<uint32_t>(c2) & 31u);
-        const unsigned peers = __match_any_sync(__activemask(), key);
-        if (static_cast<unsigned>(__ffs(peers) - 1) == lane) atomicOr(clr + w, 1u << (c2 & 31));
+        // adjacent pixels stand in the same cell as runs of lanes: only the
+        // first lane of each run issues the RED
+        const unsigned act = __activemask();
+        const uint32_t prev = __shfl_up_sync(act, key, 1);
+        const bool dup = lane > 0 && ((act >> (lane - 1)) & 1u) && prev == key;
+        if (!dup) atomicOr(clr + w, 1u << (c2 & 31));
       }
       // m = argmin t_max, ties to the lower axis (voxel_grid.cpp:170-172)
       const bool m1 = tm1 < tm0;

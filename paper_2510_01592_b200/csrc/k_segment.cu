@@ -1131,6 +1131,7 @@ __global__ void __launch_bounds__(256) k_poly_extremes(Counters* ctr, SegBufs b,
 
 __global__ void k_poly_inner(Counters* ctr, SegBufs b, int directions) {
   __shared__ P2 ext[64];
+  __shared__ P2 hull_s[130];
   const uint32_t F = ctr->nfits;
   const P2* proj = reinterpret_cast<const P2*>(b.proj);
   for (uint32_t f = blockIdx.x; f < F; f += gridDim.x) {
@@ -1168,7 +1169,8 @@ __global__ void k_poly_inner(Counters* ctr, SegBufs b, int directions) {
         uint32_t m = 0;
         for (int j = 0; j < directions; ++j)
           if (m == 0 || !(e[j].x == e[m - 1].x && e[j].y == e[m - 1].y)) e[m++] = e[j];
-        ni = chain_sorted(e, m, reinterpret_cast<P2*>(b.inner) + 130 * f);
+        ni = chain_sorted(e, m, hull_s);
+        for (uint32_t k = 0; k < ni; ++k) reinterpret_cast<P2*>(b.inner)[130 * f + k] = hull_s[k];
       }
       b.ninner[f] = ni;  // < 3: no filtering (hull_filter returns all points)
     }
@@ -1242,11 +1244,14 @@ __global__ void k_poly_hull(Counters* ctr, SegBufs b, double min_area) {
     const uint32_t ns = b.nsurv[f];
     if (threadIdx.x == 0) atomicMax(&ctr->surv_max, ns);
     P2* surv = reinterpret_cast<P2*>(b.surv) + 2 * static_cast<uint64_t>(b.ioff[f]);  // 2n slots
-    P2* hullg = reinterpret_cast<P2*>(b.hull) + 2 * static_cast<uint64_t>(b.ioff[f]);
     uint32_t np2 = 1;
     while (np2 < ns) np2 <<= 1;
     const bool in_smem = np2 <= static_cast<uint32_t>(kHullSmem);
     P2* arr = in_smem ? sm_pts : surv;
+    // the chain's stack (<= 2 ns points) lives in shared memory too when it
+    // fits: its pops are a serial dependent loop
+    P2* hullg = in_smem ? sm_pts + kHullSmem
+                        : reinterpret_cast<P2*>(b.hull) + 2 * static_cast<uint64_t>(b.ioff[f]);
     for (uint32_t i = threadIdx.x; i < np2; i += blockDim.x)
       arr[i] = i < ns ? surv[i] : P2{CUDART_INF, CUDART_INF};
     __syncthreads();
