@@ -967,6 +967,35 @@ __device__ uint32_t chain_sorted(const P2* pts, uint32_t n, P2* h) {
   return m < 3 ? 0 : m;
 }
 
+// The two halves of Andrew's monotone chain as independent stacks
+// (polygonize.cpp:116-139): the lower chain over pts[0..n) and the upper chain
+// over pts[n-1], pts[n-2], .., pts[0] starting from the stack [pts[n-1]],
+// popping while it holds >= 2 points. The reference's single-array loop pops
+// the upper part only down to `lower`, i.e. never below pts[n-1], so
+// hull = L + U[1 .. |U|-1) is exactly its output. The top two stack entries
+// live in registers (the pop loop is a serial dependency chain).
+__device__ uint32_t half_chain(const P2* pts, uint32_t n, bool upper, P2* h) {
+  uint32_t k = 0;
+  P2 a{0.0, 0.0}, t{0.0, 0.0};
+  if (upper) {
+    t = pts[n - 1];
+    h[k++] = t;
+  }
+  const uint32_t m = upper ? n - 1 : n;
+  for (uint32_t q = 0; q < m; ++q) {
+    const P2 p = upper ? pts[n - 2 - q] : pts[q];
+    while (k >= 2 && cross2(a, t, p) <= 0.0) {
+      --k;
+      t = a;
+      if (k >= 2) a = h[k - 2];
+    }
+    h[k++] = p;
+    a = t;
+    t = p;
+  }
+  return k;
+}
+
 // In-place bitonic sort (lexicographic) of n (power of two) points by a block.
 __device__ void bitonic_sort(P2* a, uint32_t n) {
   for (uint32_t k = 2; k <= n; k <<= 1) {
@@ -1248,19 +1277,61 @@ __global__ void k_poly_hull(Counters* ctr, SegBufs b, double min_area) {
     while (np2 < ns) np2 <<= 1;
     const bool in_smem = np2 <= static_cast<uint32_t>(kHullSmem);
     P2* arr = in_smem ? sm_pts : surv;
-    // the chain's stack (<= 2 ns points) lives in shared memory too when it
-    // fits: its pops are a serial dependent loop
-    P2* hullg = in_smem ? sm_pts + kHullSmem
+    // the final ring (<= 2 ns points) stays in shared memory when it fits
+    P2* hullg = in_smem ? sm_pts + 4 * kHullSmem
                         : reinterpret_cast<P2*>(b.hull) + 2 * static_cast<uint64_t>(b.ioff[f]);
     for (uint32_t i = threadIdx.x; i < np2; i += blockDim.x)
       arr[i] = i < ns ? surv[i] : P2{CUDART_INF, CUDART_INF};
     __syncthreads();
     bitonic_sort(arr, np2);
+    if (in_smem) {
+      // std::unique as an ordered block compaction, then the two chains on
+      // two threads of different warps
+      P2* uq = sm_pts + kHullSmem;
+      P2* lo_st = sm_pts + 2 * kHullSmem;
+      P2* up_st = sm_pts + 3 * kHullSmem;
+      constexpr int kPer = kHullSmem / 256;
+      uint32_t keep_mask = 0, cnt = 0;
+      const uint32_t i0 = threadIdx.x * kPer;
+#pragma unroll
+      for (int q = 0; q < kPer; ++q) {
+        const uint32_t i = i0 + q;
+        const bool k = i < ns && (i == 0 || !(arr[i].x == arr[i - 1].x && arr[i].y == arr[i - 1].y));
+        keep_mask |= (k ? 1u : 0u) << q;
+        cnt += k ? 1u : 0u;
+      }
+      uint32_t pos = block_exclusive_u32(cnt);
+      if (threadIdx.x == blockDim.x - 1) n_uniq = pos + cnt;
+#pragma unroll
+      for (int q = 0; q < kPer; ++q)
+        if ((keep_mask >> q) & 1u) uq[pos++] = arr[i0 + q];
+      __syncthreads();
+      const uint32_t mu = n_uniq;
+      if (mu >= 3 && (threadIdx.x == 0 || threadIdx.x == 32)) {
+        const bool upper = threadIdx.x == 32;
+        const uint32_t k = half_chain(uq, mu, upper, upper ? up_st : lo_st);
+        if (upper) voff = k; else area_s = static_cast<double>(k);  // stash sizes
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        uint32_t mh = 0;
+        if (mu >= 3) {
+          const uint32_t kl = static_cast<uint32_t>(area_s), ku = voff;
+          for (uint32_t i = 0; i < kl; ++i) hullg[mh++] = lo_st[i];
+          for (uint32_t i = 1; i + 1 < ku; ++i) hullg[mh++] = up_st[i];
+          if (mh < 3) mh = 0;
+        }
+        n_uniq = mh;
+      }
+      __syncthreads();
+    }
     if (threadIdx.x == 0) {
-      uint32_t m = 0;  // std::unique
-      for (uint32_t i = 0; i < ns; ++i)
-        if (m == 0 || !(arr[i].x == arr[m - 1].x && arr[i].y == arr[m - 1].y)) arr[m++] = arr[i];
-      n_uniq = chain_sorted(arr, m, hullg);
+      if (!in_smem) {
+        uint32_t m = 0;  // std::unique
+        for (uint32_t i = 0; i < ns; ++i)
+          if (m == 0 || !(arr[i].x == arr[m - 1].x && arr[i].y == arr[m - 1].y)) arr[m++] = arr[i];
+        n_uniq = chain_sorted(arr, m, hullg);
+      }
       voff = 0xffffffffu;
       area_s = 0.0;
       const uint32_t mh = n_uniq;

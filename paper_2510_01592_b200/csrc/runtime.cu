@@ -415,7 +415,7 @@ struct vp_grid {
     const uint32_t vcap = static_cast<uint32_t>(std::min<uint64_t>(C, 1u << 22));
     seg.ensure(vcap, vcap, vcap, 100, gd.nwords);
     ck(cudaFuncSetAttribute(k_poly_hull, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            kHullSmem * 16 * 3), "smem attr");
+                            kHullSmem * 16 * 6), "smem attr");
     ck(cudaStreamSynchronize(stream), "init sync");
   }
 
@@ -619,7 +619,7 @@ struct vp_grid {
     LAUNCH(k_poly_extremes, kWide, 256, 0, stream, ctr, seg.b, seg.dirtab, dirs);
     LAUNCH(k_poly_inner, 148 * 2, 64, 0, stream, ctr, seg.b, dirs);
     LAUNCH(k_poly_keep, kWide, 256, 0, stream, ctr, seg.b);
-    LAUNCH(k_poly_hull, 148, 256, kHullSmem * 16 * 3, stream, ctr, seg.b, min_area);
+    LAUNCH(k_poly_hull, 148, 256, kHullSmem * 16 * 6, stream, ctr, seg.b, min_area);
   }
 
   // The fused segment(): voxel_frame_polygons (pipeline.cpp:43-85) on device.
