@@ -586,8 +586,12 @@ struct vp_grid {
   }
   // union-find over the steppable list in seg.b (ctr->S set)
   void launch_ccl(const SegDev& sd, const MapDesc& m) {
-    LAUNCH(k_ccl_hook, kWide, kThreads, 0, stream, ctr, sd, seg.b, m);
-    LAUNCH(k_ccl_compress, kWide, kThreads, 0, stream, ctr, seg.b);
+    if (std::getenv("VP_CCL_HOOK")) {  // ECL-style pre-hooking (measured: no net gain on C2)
+      LAUNCH(k_ccl_hook, kWide, kThreads, 0, stream, ctr, sd, seg.b, m);
+      LAUNCH(k_ccl_compress, kWide, kThreads, 0, stream, ctr, seg.b);
+    } else {
+      LAUNCH(k_ccl_init, kWide, kThreads, 0, stream, ctr, seg.b);
+    }
     LAUNCH(k_ccl_union, kWide, kThreads, 0, stream, ctr, sd, seg.b, m);
     LAUNCH(k_ccl_flatten, kWide, kThreads, 0, stream, ctr, seg.b, m);
   }

@@ -12,7 +12,7 @@ constexpr int kScanItems = 8;
 constexpr int kScanPerBlock = kScanThreads * kScanItems;  // 2048
 constexpr int kClusterBins = 2048;  // clusters handled by the counting sort per pass
 constexpr int kChunk = 256;         // ordinals per counting-sort chunk (one warp)
-constexpr int kHullSmem = 2048;     // survivors sorted in shared memory (6 regions of this size)
+constexpr int kHullSmem = 512;      // survivors sorted in shared memory (6 regions of this size)
 constexpr int kPolyChunk = 1024;    // inlier points per polygon-stage block
 
 // Block-wide exclusive prefix sum (any blockDim multiple of 32, <= 1024).
