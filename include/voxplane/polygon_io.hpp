@@ -1,0 +1,4 @@
+// Reference-compatible include path (voxplane/polygon_io.hpp): the B200 API lives in
+// voxplane/voxplane.hpp.
+#pragma once
+#include "voxplane/voxplane.hpp"

@@ -172,6 +172,8 @@ int vp_get_cell(vp_grid* g, const int32_t idx[3], double sum[3], uint32_t* count
                 uint8_t* status);
 /* VoxelGrid::set_status (voxel_grid.hpp:78) */
 int vp_set_status(vp_grid* g, const int32_t idx[3], uint8_t status);
+/* set_status for n voxels (idx n x 3) in one transfer (classify_steppable writeback) */
+int vp_set_statuses(vp_grid* g, const int32_t* idx, const uint8_t* status, size_t n);
 /* VoxelGrid::occupied_voxels (voxel_grid.cpp:254-263) */
 int vp_occupied_voxels(vp_grid* g, vp_occupied_t** out);
 void vp_occupied_free(vp_occupied_t* o);

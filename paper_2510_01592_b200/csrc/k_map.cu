@@ -462,6 +462,16 @@ __global__ void k_merge_point(GridDesc g, const FrameParams* __restrict__ fp, Co
   c->status = 1;
 }
 
+// Batch VoxelGrid::set_status (window indices, current toroidal offsets).
+__global__ void k_set_statuses(GridDesc g, const FrameParams* __restrict__ fp, const int32_t* idx,
+                               const uint8_t* st, uint64_t n) {
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const int x = idx[3 * i], y = idx[3 * i + 1], z = idx[3 * i + 2];
+    if (in_bounds(g, x, y, z)) g.cells[phys_index(g, fp->off_pre, x, y, z)].status = st[i];
+  }
+}
+
 __global__ void k_map_finalize(Counters* ctr) {
   ctr->occupied = ctr->occupied + ctr->newly - ctr->freed - ctr->dropped;
   ctr->touched = ctr->ngroups;

@@ -191,6 +191,8 @@ __global__ void k_clear_walk(GridDesc g, const FrameParams* fp);
 __global__ void k_clear_apply(GridDesc g, const FrameParams* fp, Counters* ctr);
 __global__ void k_recenter(GridDesc g, const FrameParams* fp, Counters* ctr);
 __global__ void k_map_finalize(Counters* ctr);
+__global__ void k_set_statuses(GridDesc g, const FrameParams* fp, const int32_t* idx, const uint8_t* st,
+                               uint64_t n);
 __global__ void k_bitmap_count(const FrameParams* fp, uint64_t nwords, uint32_t* bsum);
 __global__ void k_bitmap_emit(const FrameParams* fp, uint64_t nwords, int W, int ez,
                               const uint32_t* boff, uint32_t* out, uint32_t cap);
