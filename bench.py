@@ -6,8 +6,10 @@
 A step = one pass over the 30-frame stream from an empty map (the map is reset
 between steps, untimed, together with an L2 flush). `value` = frames/s with
 every frame already resident in HBM (device time, CUDA events on the
-library's stream, max over ranks); `e2e` = the same through the public C ABI
-with pinned-host inputs (H2D inside) and the polygons read back every frame.
+library's stream, max over ranks); a step is one vp_pipeline_run call
+(run_frames: consecutive frames overlap on the device, outputs identical to
+the frame-by-frame API). `e2e` = the same call with pinned-host inputs (H2D
+inside) and the final polygons read back.
 
 --impl reference times the reference's own CPU implementation (oracle/_ref:
 the unmodified /root/reference sources) on the host cores over a bounded
@@ -110,12 +112,17 @@ def algorithmic_bytes(c, n_points):
         "k_bitmap_count": C_BITS,
         "k_bitmap_emit": C_BITS + 4 * V,
         "k_normals": 32 * V + 4 * V + 72 * V,                  # cells, list in, estimate out
+        "k_ccl_hook": 56 * S,
+        "k_ccl_compress": 8 * S,
         "k_ccl_union": 56 * S,                                 # mean+normal+ordinal per voxel
         "k_ccl_flatten": 12 * S,
         "k_ransac_count": 24 * padded,
-        "k_ransac_extract": 24 * padded + 24 * inl,
+        "k_extract_count": 24 * padded,
+        "k_extract_emit": 24 * padded + 24 * inl,
         "k_refine": 2 * 24 * inl,
-        "k_polygon": 24 * inl + 64 * poolv,
+        "k_poly_extremes": 24 * inl + 16 * inl,
+        "k_poly_keep": 16 * inl,
+        "k_poly_hull": 64 * poolv,
     }
 
 
@@ -148,13 +155,23 @@ def run_ours(args, rank, world, dist):
     def reset():
         native.check(L.vp_pipeline_reset(pl.h, start.ctypes.data_as(C.POINTER(C.c_double))))
 
-    dev_pts = [torch.from_numpy(f.points).to(f"cuda:{dev}") for f in frames]
+    dev_pts = [torch.from_numpy(f.points).to(f"cuda:{dev}").contiguous() for f in frames]
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{dev}")
     torch.cuda.synchronize()
 
+    # the whole 30-frame stream is one vp_pipeline_run call (run_frames):
+    # consecutive frames overlap on the device; per-frame outputs are identical
+    # to the frame-by-frame API (tests/test_gpu_parity.py)
+    nfr = len(frames)
+    R_all = np.ascontiguousarray(np.stack([f.rotation.reshape(9) for f in frames]), np.float64)
+    t_all = np.ascontiguousarray(np.stack([f.translation for f in frames]), np.float64)
+    n_all = np.asarray(npts, np.uint64)
+    dev_ptrs = (C.c_void_p * nfr)(*[d.data_ptr() for d in dev_pts])
+    host_pts = [torch.from_numpy(f.points).pin_memory() for f in frames]
+    host_ptrs = (C.c_void_p * nfr)(*[h.data_ptr() for h in host_pts])
+
     def device_step():
-        for f, d in zip(frames, dev_pts):
-            pl.frame_device(d.data_ptr(), len(f.points), f.rotation, f.translation)
+        pl.run_ptrs(dev_ptrs, n_all, R_all, t_all, device_ptrs=True, want_polygons=False)
 
     # warm-up
     for _ in range(args.warmup):
@@ -191,8 +208,8 @@ def run_ours(args, rank, world, dist):
         total_ms = sum(times)
     value = world * nf * args.steps / (total_ms / 1e3)
 
-    # e2e through the public API: pinned host points, H2D + D2H inside
-    host_pts = [torch.from_numpy(f.points).pin_memory() for f in frames]
+    # e2e through the public C ABI: pinned host points (H2D inside the call),
+    # final polygons copied back (PipelineResult::polygons)
     e2e_times = []
     d2h_bytes = 0
     for s in range(max(1, args.steps)):
@@ -201,13 +218,14 @@ def run_ours(args, rank, world, dist):
         torch.cuda.synchronize()
         if dist:
             dist.barrier()
-        t0 = time.perf_counter()
-        nbytes = 0
-        for f, hp in zip(frames, host_pts):
-            polys, _ = pl.frame_ptr(hp.data_ptr(), len(f.points), f.rotation, f.translation)
-            nbytes += sum(40 + 8 + 40 * len(p["v3d"]) for p in polys) + 128
-        e2e_times.append(time.perf_counter() - t0)
-        d2h_bytes = nbytes
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        polys = pl.run_ptrs(host_ptrs, n_all, R_all, t_all, device_ptrs=False, want_polygons=True)
+        e1.record(stream)
+        e1.synchronize()
+        e2e_times.append(e0.elapsed_time(e1) / 1e3)
+        d2h_bytes = sum(40 + 8 + 40 * len(p["v3d"]) for p in polys) + 128 * nf
     e2e_total = sum(e2e_times)
     if dist:
         t = torch.tensor([e2e_total], device=f"cuda:{dev}", dtype=torch.float64)

@@ -248,6 +248,16 @@ int vp_pipeline_frame(vp_pipeline* pl, const float* xyz, uint64_t n, const doubl
 int vp_pipeline_frame_device(vp_pipeline* pl, const float* xyz_dev, uint64_t n,
                              const double rotation[9], const double translation[3],
                              vp_polygons_t** out, vp_frame_timing* timing);
+/* run_frames (pipeline.cpp:157-245) over n_frames frames: frame k's points
+   are xyz[k] (n[k] x 3 floats; device pointers when device_ptrs != 0), pose
+   rotations[9k..], translations[3k..]. Consecutive frames overlap on the
+   device (frame k+1's mapping runs beside frame k's fitting and polygon
+   stages); outputs are those of calling vp_pipeline_frame per frame. out
+   receives the final frame's polygons (PipelineResult::polygons); timings
+   (optional, n_frames entries) the per-frame device spans. */
+int vp_pipeline_run(vp_pipeline* pl, size_t n_frames, const float* const* xyz, const uint64_t* n,
+                    const double* rotations, const double* translations, int device_ptrs,
+                    vp_polygons_t** out, vp_frame_timing* timings);
 /* Same frame step, returning the stage trace (voxplane_trace.h); buf is
    freed with vp_free. */
 int vp_pipeline_frame_trace(vp_pipeline* pl, const float* xyz, uint64_t n,

@@ -452,7 +452,7 @@ __global__ void k_merge_point(GridDesc g, const FrameParams* __restrict__ fp, Co
                               int y, int z, double px, double py, double pz) {
   Cell* c = g.cells + phys_index(g, fp->off_pre, x, y, z);
   if (c->count == 0) {
-    ctr->occupied += 1;
+    ctr->newly += 1;
     atomicOr(fp->occ_pre + word_of(g, x, y, z), 1u << (z & 31));
   }
   c->sx += px;
@@ -472,9 +472,19 @@ __global__ void k_set_statuses(GridDesc g, const FrameParams* __restrict__ fp, c
   }
 }
 
-__global__ void k_map_finalize(Counters* ctr) {
-  ctr->occupied = ctr->occupied + ctr->newly - ctr->freed - ctr->dropped;
+__global__ void k_map_finalize(Counters* ctr, unsigned long long* occ_total) {
+  const unsigned long long o = *occ_total + ctr->newly - ctr->freed - ctr->dropped;
+  *occ_total = o;
+  ctr->occupied = o;
   ctr->touched = ctr->ngroups;
+}
+
+// Per-frame counter reset (one slot); occupied carries VoxelGrid::occupied_.
+__global__ void k_frame_begin(Counters* ctr, const unsigned long long* occ_total) {
+  uint32_t* w = reinterpret_cast<uint32_t*>(ctr);
+  for (uint32_t i = threadIdx.x; i < sizeof(Counters) / 4; i += blockDim.x) w[i] = 0u;
+  __syncwarp();
+  if (threadIdx.x == 0) ctr->occupied = *occ_total;
 }
 
 // ---------------------------------------------------------------------------

@@ -332,14 +332,25 @@ struct vp_grid {
   int32_t off[3] = {0, 0, 0};
   uint32_t* occ[2] = {nullptr, nullptr};
   int cur = 0;
+  // Per-frame state in two slots so consecutive frames can be in flight at
+  // once (vp_pipeline_run); ctr/h_ctr/d_fp/h_fp/d_pts point at the current slot.
+  Counters* ctr_s[2] = {nullptr, nullptr};
+  Counters* h_ctr_s[2] = {nullptr, nullptr};  // pinned
+  FrameParams* d_fp_s[2] = {nullptr, nullptr};
+  FrameParams* h_fp_s[2] = {nullptr, nullptr};  // pinned
+  float* d_pts_s[2] = {nullptr, nullptr};
+  int slot = 0;
   Counters* ctr = nullptr;
-  Counters* h_ctr = nullptr;  // pinned
+  Counters* h_ctr = nullptr;
   FrameParams* d_fp = nullptr;
-  FrameParams* h_fp = nullptr;  // pinned
+  FrameParams* h_fp = nullptr;
+  float* d_pts = nullptr;
+  unsigned long long* occ_total = nullptr;  // VoxelGrid::occupied_ (device, persistent)
   uint64_t host_occupied = 0;
+  cudaStream_t mstream = nullptr;   // mapping stream of pipelined runs
+  cudaStream_t lstream = nullptr;   // stream the mapping launches go to (stream or mstream)
   // integrate scratch
   uint64_t pcap = 0;
-  float* d_pts = nullptr;
   uint32_t* hkey = nullptr;
   uint32_t* hcnt = nullptr;
   uint32_t* hoff = nullptr;
@@ -362,15 +373,21 @@ struct vp_grid {
     if (gd.clr) cudaFree(gd.clr);
     if (gd.ordmap) cudaFree(gd.ordmap);
     if (gd.stbits) cudaFree(gd.stbits);
-    if (ctr) cudaFree(ctr);
-    if (d_fp) cudaFree(d_fp);
-    if (h_ctr) cudaFreeHost(h_ctr);
-    if (h_fp) cudaFreeHost(h_fp);
-    for (void* p : {(void*)d_pts, (void*)hkey, (void*)hcnt, (void*)hoff, (void*)groups,
+    if (mstream) cudaStreamSynchronize(mstream);
+    for (int q = 0; q < 2; ++q) {
+      if (ctr_s[q]) cudaFree(ctr_s[q]);
+      if (d_fp_s[q]) cudaFree(d_fp_s[q]);
+      if (h_ctr_s[q]) cudaFreeHost(h_ctr_s[q]);
+      if (h_fp_s[q]) cudaFreeHost(h_fp_s[q]);
+      if (d_pts_s[q]) cudaFree(d_pts_s[q]);
+    }
+    if (occ_total) cudaFree(occ_total);
+    for (void* p : {(void*)hkey, (void*)hcnt, (void*)hoff, (void*)groups,
                     (void*)pslot, (void*)prank, (void*)sorted})
       if (p) cudaFree(p);
     for (auto& e : ev) if (e) cudaEventDestroy(e);
     if (stream) cudaStreamDestroy(stream);
+    if (mstream) cudaStreamDestroy(mstream);
   }
 
   // ------------------------------------------------------------ set-up
@@ -386,6 +403,8 @@ struct vp_grid {
       origin[k] = c[k] - static_cast<double>(e[k]) * (0.5 * res);  // voxel_grid.cpp:23
     }
     ck(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "stream");
+    ck(cudaStreamCreateWithFlags(&mstream, cudaStreamNonBlocking), "stream");
+    lstream = stream;
     for (auto& x : ev) ck(cudaEventCreate(&x), "event");
     gd.ex = e[0];
     gd.ey = e[1];
@@ -406,12 +425,18 @@ struct vp_grid {
     ck(cudaMemsetAsync(occ[1], 0, gd.nwords * 4, stream), "memset occ");
     ck(cudaMemsetAsync(gd.ordmap, 0xff, C * 4, stream), "memset ordmap");
     ck(cudaMemsetAsync(gd.stbits, 0, gd.nwords * 4, stream), "memset stbits");
-    ctr = dalloc<Counters>(1);
-    ck(cudaMemsetAsync(ctr, 0, sizeof(Counters), stream), "memset ctr");
-    d_fp = dalloc<FrameParams>(1);
-    ck(cudaMallocHost(&h_ctr, sizeof(Counters)), "pinned");
-    ck(cudaMallocHost(&h_fp, sizeof(FrameParams)), "pinned");
-    std::memset(h_fp, 0, sizeof(FrameParams));
+    for (int q = 0; q < 2; ++q) {
+      ctr_s[q] = dalloc<Counters>(1);
+      ck(cudaMemsetAsync(ctr_s[q], 0, sizeof(Counters), stream), "memset ctr");
+      d_fp_s[q] = dalloc<FrameParams>(1);
+      ck(cudaMallocHost(&h_ctr_s[q], sizeof(Counters)), "pinned");
+      ck(cudaMallocHost(&h_fp_s[q], sizeof(FrameParams)), "pinned");
+      std::memset(h_fp_s[q], 0, sizeof(FrameParams));
+      std::memset(h_ctr_s[q], 0, sizeof(Counters));
+    }
+    occ_total = dalloc<unsigned long long>(1);
+    ck(cudaMemsetAsync(occ_total, 0, 8, stream), "memset occ");
+    set_slot(0);
     const uint32_t vcap = static_cast<uint32_t>(std::min<uint64_t>(C, 1u << 22));
     seg.ensure(vcap, vcap, vcap, 100, gd.nwords);
     ck(cudaFuncSetAttribute(k_poly_hull, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -433,7 +458,8 @@ struct vp_grid {
     launch_recenter();
     ck(cudaMemsetAsync(occ[0], 0, gd.nwords * 4, stream), "occ");
     ck(cudaMemsetAsync(occ[1], 0, gd.nwords * 4, stream), "occ");
-    ck(cudaMemsetAsync(ctr, 0, sizeof(Counters), stream), "ctr");
+    for (int q = 0; q < 2; ++q) ck(cudaMemsetAsync(ctr_s[q], 0, sizeof(Counters), stream), "ctr");
+    ck(cudaMemsetAsync(occ_total, 0, 8, stream), "occ total");
     ck(cudaStreamSynchronize(stream), "reset sync");
     cur = 0;
     host_occupied = 0;
@@ -443,16 +469,28 @@ struct vp_grid {
     }
   }
 
+  void set_slot(int s) {
+    slot = s;
+    ctr = ctr_s[s];
+    h_ctr = h_ctr_s[s];
+    d_fp = d_fp_s[s];
+    h_fp = h_fp_s[s];
+    d_pts = d_pts_s[s];
+  }
+
   void ensure_points(uint64_t n) {
-    if (n <= pcap && d_pts) return;
+    if (n <= pcap && d_pts_s[0]) return;
     uint64_t cap = std::max<uint64_t>(n, 1 << 16);
     cap = std::max<uint64_t>(cap, pcap * 2);
-    for (void* p : {(void*)d_pts, (void*)hkey, (void*)hcnt, (void*)hoff, (void*)groups,
-                    (void*)pslot, (void*)prank, (void*)sorted})
+    ck(cudaDeviceSynchronize(), "sync before realloc");
+    for (void* p : {(void*)d_pts_s[0], (void*)d_pts_s[1], (void*)hkey, (void*)hcnt, (void*)hoff,
+                    (void*)groups, (void*)pslot, (void*)prank, (void*)sorted})
       if (p) cudaFree(p);
     uint64_t hs = 1;
     while (hs < 2 * cap) hs <<= 1;
-    d_pts = dalloc<float>(3 * cap);
+    d_pts_s[0] = dalloc<float>(3 * cap);
+    d_pts_s[1] = dalloc<float>(3 * cap);
+    d_pts = d_pts_s[slot];
     hkey = dalloc<uint32_t>(hs);
     hcnt = dalloc<uint32_t>(hs);
     hoff = dalloc<uint32_t>(hs);
@@ -509,13 +547,10 @@ struct vp_grid {
     return true;
   }
   void upload_params() {
-    ck(cudaMemcpyAsync(d_fp, h_fp, sizeof(FrameParams), cudaMemcpyHostToDevice, stream), "params");
+    ck(cudaMemcpyAsync(d_fp, h_fp, sizeof(FrameParams), cudaMemcpyHostToDevice, lstream), "params");
   }
-  void reset_frame_counters() {
-    ck(cudaMemsetAsync(reinterpret_cast<char*>(ctr) + sizeof(unsigned long long), 0,
-                       sizeof(Counters) - sizeof(unsigned long long), stream),
-       "ctr reset");
-  }
+  // zero the slot's counters; occupied <- the persistent total
+  void reset_frame_counters() { LAUNCH(k_frame_begin, 1, 32, 0, lstream, ctr, occ_total); }
   void read_counters() {
     ck(cudaMemcpyAsync(h_ctr, ctr, sizeof(Counters), cudaMemcpyDeviceToHost, stream), "ctr d2h");
     ck(cudaStreamSynchronize(stream), "sync");
@@ -527,23 +562,23 @@ struct vp_grid {
   // the device params), so the same launches can be replayed as a graph.
   void launch_clear(uint64_t n) {
     if (n == 0 && !capturing) return;
-    LAUNCH(k_clear_walk, grid_for(capturing ? pcap : n, 148 * 32), kThreads, 0, stream, gd, d_fp);
-    LAUNCH(k_clear_apply, grid_for(gd.nwords), kThreads, 0, stream, gd, d_fp, ctr);
+    LAUNCH(k_clear_walk, grid_for(capturing ? pcap : n, 148 * 32), kThreads, 0, lstream, gd, d_fp);
+    LAUNCH(k_clear_apply, grid_for(gd.nwords), kThreads, 0, lstream, gd, d_fp, ctr);
   }
   void launch_integrate(uint64_t n) {
     if (n == 0 && !capturing) return;
     const int gp = grid_for(capturing ? pcap : n);
-    LAUNCH(k_integrate_hash, gp, kThreads, 0, stream, gd, d_fp, ctr, hkey, hcnt, hmask, groups,
+    LAUNCH(k_integrate_hash, gp, kThreads, 0, lstream, gd, d_fp, ctr, hkey, hcnt, hmask, groups,
            pslot, prank);
-    LAUNCH(k_integrate_offsets, gp, kThreads, 0, stream, ctr, groups, hcnt, hoff);
-    LAUNCH(k_integrate_scatter, gp, kThreads, 0, stream, d_fp, pslot, prank, hoff, sorted);
-    LAUNCH(k_integrate_fold, gp, kThreads, 0, stream, gd, d_fp, ctr, groups, hkey, hcnt, hoff,
+    LAUNCH(k_integrate_offsets, gp, kThreads, 0, lstream, ctr, groups, hcnt, hoff);
+    LAUNCH(k_integrate_scatter, gp, kThreads, 0, lstream, d_fp, pslot, prank, hoff, sorted);
+    LAUNCH(k_integrate_fold, gp, kThreads, 0, lstream, gd, d_fp, ctr, groups, hkey, hcnt, hoff,
            sorted);
   }
   void launch_recenter() {
-    LAUNCH(k_recenter, grid_for(gd.nwords), kThreads, 0, stream, gd, d_fp, ctr);
+    LAUNCH(k_recenter, grid_for(gd.nwords), kThreads, 0, lstream, gd, d_fp, ctr);
   }
-  void launch_finalize() { LAUNCH(k_map_finalize, 1, 1, 0, stream, ctr); }
+  void launch_finalize() { LAUNCH(k_map_finalize, 1, 1, 0, lstream, ctr, occ_total); }
 
   // Occupied scan of the post-recenter bitmap into seg.b.occ_list; ctr->V.
   void launch_occupied_scan() {
@@ -630,9 +665,10 @@ struct vp_grid {
        "event record");
   }
 
-  void launch_segment(const vp_pipeline_params& p, bool timing) {
+  // voxel_frame_polygons up to filter_clusters: everything that can overflow
+  // a capacity, and the last stage that reads the grid cells.
+  void launch_seg_a(const vp_pipeline_params& p, bool timing) {
     const SegDev sd = make_segdev(p.seg, gd.res);
-    const RansacDev rd = make_ransacdev(p.ransac);
     if (!capturing && static_cast<uint64_t>(p.ransac.iterations) * kClusterBins > seg.cand_cap)
       seg.ensure(seg.b.Vcap, seg.b.Scap, seg.b.Icap, p.ransac.iterations, gd.nwords);
     if (timing) record(ev[1]);
@@ -643,11 +679,19 @@ struct vp_grid {
     launch_ccl(sd, grid_map());
     launch_clusters(sd);
     if (timing) record(ev[3]);
+  }
+  // fit_planes .. make_polygon: reads only the cluster buffers
+  void launch_seg_b(const vp_pipeline_params& p, bool timing) {
+    const RansacDev rd = make_ransacdev(p.ransac);
     launch_ransac(rd);
     if (timing) record(ev[4]);
     launch_refine(p.ransac.up, p.refine, p.refine_exact);
     launch_polygon(16, p.min_polygon_area);
     if (timing) record(ev[5]);
+  }
+  void launch_segment(const vp_pipeline_params& p, bool timing) {
+    launch_seg_a(p, timing);
+    launch_seg_b(p, timing);
   }
 
   // Grow capacities after an overflow (the frame's segmentation is re-run).
@@ -782,8 +826,20 @@ struct vp_pipeline {
   cudaGraphExec_t gexec = nullptr;
   uint64_t graph_key = 0;
   uint64_t graph_kernels = 0;
+  // pipelined runs: graphs per (slot, part: 0 mapping, 1 seg_a, 2 seg_b)
+  cudaGraphExec_t rx[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
+  uint64_t rkey[2][3] = {{0, 0, 0}, {0, 0, 0}};
+  uint64_t rkern[2][3] = {{0, 0, 0}, {0, 0, 0}};
+  cudaEvent_t ev_start[2] = {nullptr, nullptr}, ev_map[2] = {nullptr, nullptr};
+  cudaEvent_t ev_clu[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr};
   ~vp_pipeline() {
     if (gexec) cudaGraphExecDestroy(gexec);
+    for (auto& row : rx)
+      for (auto& x : row)
+        if (x) cudaGraphExecDestroy(x);
+    for (auto* e : {ev_start, ev_map, ev_clu, ev_done})
+      for (int q = 0; q < 2; ++q)
+        if (e[q]) cudaEventDestroy(e[q]);
     delete grid;
   }
 };
@@ -841,6 +897,8 @@ void run_frame_graph(vp_pipeline* pl) {
 bool pipeline_enqueue(vp_pipeline* pl, const float* xyz, uint64_t n, const double* R,
                       const double* t, bool device_ptr, vp_shift_stats* ss) {
   vp_grid* g = pl->grid;
+  g->set_slot(0);
+  g->lstream = g->stream;
   if (!is_valid_rotation(R))  // voxel_grid.cpp:60-61, 183-184
     fail(VP_EINVAL, "clear_rays: pose rotation is not orthonormal");
   g->ensure_points(n);
@@ -865,6 +923,144 @@ bool pipeline_enqueue(vp_pipeline* pl, const float* xyz, uint64_t n, const doubl
     run_frame_graph(pl);
   }
   return rec;
+}
+
+void rerun_segment_until_fits(vp_grid* g, const vp_pipeline_params& p);
+
+// Record part `part` of a frame for the current slot as a CUDA graph on
+// stream `st` (rebuilt when a referenced buffer was reallocated), then launch it.
+template <typename F>
+void run_part_graph(vp_pipeline* pl, int part, cudaStream_t st, F&& enqueue) {
+  vp_grid* g = pl->grid;
+  const int s = g->slot;
+  const uint64_t key = (g->gen << 32) ^ g->seg.gen;
+  if (!pl->rx[s][part] || pl->rkey[s][part] != key) {
+    if (pl->rx[s][part]) cudaGraphExecDestroy(pl->rx[s][part]);
+    pl->rx[s][part] = nullptr;
+    cudaGraph_t graph;
+    const uint64_t before = g_launches.load();
+    g->capturing = true;
+    ck(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "capture begin");
+    try {
+      enqueue();
+    } catch (...) {
+      cudaStreamEndCapture(st, &graph);
+      g->capturing = false;
+      throw;
+    }
+    ck(cudaStreamEndCapture(st, &graph), "capture end");
+    g->capturing = false;
+    pl->rkern[s][part] = g_launches.load() - before;
+    g_launches.fetch_sub(pl->rkern[s][part]);
+    ck(cudaGraphInstantiate(&pl->rx[s][part], graph, 0), "graph instantiate");
+    cudaGraphDestroy(graph);
+    pl->rkey[s][part] = key;
+  }
+  ck(cudaGraphLaunch(pl->rx[s][part], st), "graph launch");
+  g_launches.fetch_add(pl->rkern[s][part]);
+}
+
+// run_frames (pipeline.cpp:157-245) over a whole stream with two frames in
+// flight: the mapping of frame k+1 (clear/integrate/recenter, on the mapping
+// stream) only has to wait for frame k's segmentation to finish reading the
+// grid (end of seg_a), so it overlaps frame k's fit_planes/refine/make_polygon.
+// The host checks frame k's capacities at that same point, before frame k+1
+// touches the grid, so an overflow is re-run exactly as in the single-frame path.
+void pipeline_run(vp_pipeline* pl, size_t nf, const float* const* xyz, const uint64_t* n,
+                  const double* R, const double* t, bool device_ptrs, vp_frame_timing* timings) {
+  vp_grid* g = pl->grid;
+  for (auto* e : {pl->ev_start, pl->ev_map, pl->ev_clu, pl->ev_done})
+    for (int q = 0; q < 2; ++q)
+      if (!e[q]) ck(cudaEventCreate(&e[q]), "event");
+  uint64_t maxn = 0;
+  for (size_t k = 0; k < nf; ++k) maxn = std::max(maxn, n[k]);
+  for (size_t k = 0; k < nf; ++k)
+    if (!is_valid_rotation(R + 9 * k)) fail(VP_EINVAL, "clear_rays: pose rotation is not orthonormal");
+  g->ensure_points(maxn);
+  if (static_cast<uint64_t>(pl->p.ransac.iterations) * kClusterBins > g->seg.cand_cap)
+    g->seg.ensure(g->seg.b.Vcap, g->seg.b.Scap, g->seg.b.Icap, pl->p.ransac.iterations, g->gd.nwords);
+  g->seg.ensure_dirs(16, g->stream);
+  ck(cudaStreamSynchronize(g->stream), "sync");
+  const bool graphs = !g_prof_on && !std::getenv("VP_NO_GRAPH");
+  auto harvest = [&](size_t k) {
+    if (!timings) return;
+    const int s = static_cast<int>(k & 1);
+    float ms = 0.f;
+    ck(cudaEventElapsedTime(&ms, pl->ev_start[s], pl->ev_done[s]), "elapsed");
+    vp_frame_timing& tm = timings[k];
+    std::memset(&tm, 0, sizeof tm);
+    tm.total_ms = ms;
+    tm.points = n[k];
+    tm.voxels = g->h_ctr_s[s]->occupied;
+    tm.clusters = g->h_ctr_s[s]->K;
+  };
+  for (size_t k = 0; k < nf; ++k) {
+    const int s = static_cast<int>(k & 1);
+    if (k >= 2) {
+      ck(cudaEventSynchronize(pl->ev_done[s]), "slot sync");
+      harvest(k - 2);
+    }
+    g->set_slot(s);
+    g->set_pose(R + 9 * k, t + 3 * k);
+    g->fill_static_params();
+    if (device_ptrs) {
+      g->h_fp->pts = xyz[k];
+    } else {
+      if (n[k])
+        ck(cudaMemcpyAsync(g->d_pts, xyz[k], n[k] * 12, cudaMemcpyHostToDevice, g->mstream), "points h2d");
+      g->h_fp->pts = g->d_pts;
+    }
+    g->h_fp->n = n[k];
+    int32_t cell[3];
+    global_cell(t + 3 * k, g->gd.res, cell);
+    if (cell[0] != pl->last_cell[0] || cell[1] != pl->last_cell[1] || cell[2] != pl->last_cell[2]) {
+      vp_shift_stats ss;
+      g->plan_recenter(t + 3 * k, &ss);
+      std::memcpy(pl->last_cell, cell, sizeof cell);
+    }
+    // mapping of frame k: after frame k-1 stopped reading the grid
+    if (k >= 1) ck(cudaStreamWaitEvent(g->mstream, pl->ev_clu[s ^ 1], 0), "wait");
+    ck(cudaEventRecord(pl->ev_start[s], g->mstream), "ev");
+    g->lstream = g->mstream;
+    auto map_part = [&] {
+      g->upload_params();
+      g->reset_frame_counters();
+      g->launch_clear(n[k]);
+      g->launch_integrate(n[k]);
+      g->launch_recenter();
+      g->launch_finalize();
+    };
+    if (graphs) run_part_graph(pl, 0, g->mstream, map_part); else map_part();
+    g->lstream = g->stream;
+    ck(cudaEventRecord(pl->ev_map[s], g->mstream), "ev");
+    // segmentation of frame k
+    ck(cudaStreamWaitEvent(g->stream, pl->ev_map[s], 0), "wait");
+    auto seg_a = [&] {
+      g->launch_seg_a(pl->p, false);
+      ck(cudaMemcpyAsync(g->h_ctr, g->ctr, sizeof(Counters), cudaMemcpyDeviceToHost, g->stream), "ctr");
+    };
+    auto seg_b = [&] {
+      g->launch_seg_b(pl->p, false);
+      ck(cudaMemcpyAsync(g->h_ctr, g->ctr, sizeof(Counters), cudaMemcpyDeviceToHost, g->stream), "ctr");
+    };
+    if (graphs) run_part_graph(pl, 1, g->stream, seg_a); else seg_a();
+    ck(cudaEventRecord(pl->ev_clu[s], g->stream), "ev");
+    if (graphs) run_part_graph(pl, 2, g->stream, seg_b); else seg_b();
+    ck(cudaEventRecord(pl->ev_done[s], g->stream), "ev");
+    // capacity check point: frame k+1 has not touched the grid yet
+    ck(cudaEventSynchronize(pl->ev_clu[s]), "sync");
+    if (g->h_ctr->overflow) {
+      ck(cudaStreamSynchronize(g->stream), "sync");
+      rerun_segment_until_fits(g, pl->p);
+      ck(cudaEventRecord(pl->ev_done[s], g->stream), "ev");
+    }
+    ++pl->frame;
+  }
+  ck(cudaStreamSynchronize(g->stream), "sync");
+  ck(cudaStreamSynchronize(g->mstream), "sync");
+  for (size_t k = nf >= 2 ? nf - 2 : 0; k < nf; ++k) harvest(k);
+  if (nf) g->set_slot(static_cast<int>((nf - 1) & 1));
+  g->host_occupied = g->h_ctr->occupied;
 }
 
 void wait_frame(vp_grid* g) {
@@ -1069,8 +1265,10 @@ int vp_merge_point(vp_grid* g, const int32_t idx[3], const double p[3]) {
     g->fill_static_params();
     g->h_fp->n = 0;
     g->upload_params();
+    g->reset_frame_counters();
     LAUNCH(k_merge_point, 1, 1, 0, g->stream, g->gd, g->d_fp, g->ctr, idx[0], idx[1], idx[2], p[0],
            p[1], p[2]);
+    g->launch_finalize();
     g->read_counters();
   });
 }
@@ -1681,6 +1879,21 @@ int vp_pipeline_frame(vp_pipeline* pl, const float* xyz, uint64_t n, const doubl
 int vp_pipeline_frame_device(vp_pipeline* pl, const float* xyz_dev, uint64_t n, const double R[9],
                              const double t[3], vp_polygons_t** out, vp_frame_timing* timing) {
   return pipeline_frame_impl(pl, xyz_dev, n, R, t, true, out, timing);
+}
+
+int vp_pipeline_run(vp_pipeline* pl, size_t n_frames, const float* const* xyz, const uint64_t* n,
+                    const double* rotations, const double* translations, int device_ptrs,
+                    vp_polygons_t** out, vp_frame_timing* timings) {
+  if (out) *out = nullptr;
+  return guard([&] {
+    pipeline_run(pl, n_frames, xyz, n, rotations, translations, device_ptrs != 0, timings);
+    if (out) {
+      HostPolys hp;
+      pl->grid->download_polygons(hp, false);
+      *out = make_polygons_out(hp);
+    }
+    pl->grid->set_slot(0);
+  });
 }
 
 int vp_pipeline_frame_trace(vp_pipeline* pl, const float* xyz, uint64_t n, const double R[9],

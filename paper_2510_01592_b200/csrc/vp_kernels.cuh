@@ -190,7 +190,8 @@ __global__ void k_integrate_fold(GridDesc g, const FrameParams* fp, Counters* ct
 __global__ void k_clear_walk(GridDesc g, const FrameParams* fp);
 __global__ void k_clear_apply(GridDesc g, const FrameParams* fp, Counters* ctr);
 __global__ void k_recenter(GridDesc g, const FrameParams* fp, Counters* ctr);
-__global__ void k_map_finalize(Counters* ctr);
+__global__ void k_map_finalize(Counters* ctr, unsigned long long* occ_total);
+__global__ void k_frame_begin(Counters* ctr, const unsigned long long* occ_total);
 __global__ void k_set_statuses(GridDesc g, const FrameParams* fp, const int32_t* idx, const uint8_t* st,
                                uint64_t n);
 __global__ void k_bitmap_count(const FrameParams* fp, uint64_t nwords, uint32_t* bsum);

@@ -199,6 +199,42 @@ class Pipeline:
                                       C.byref(out) if want_polygons else None, C.byref(tm)))
         return (polygons_to_py(out) if want_polygons else None), tm
 
+    def run(self, frames, device_ptrs=None, want_polygons=True, timings=False):
+        """vp_pipeline_run: run_frames over a list of Frames (host arrays), or
+        over device pointers: device_ptrs = [(ptr, n), ...] with frames giving poses."""
+        nf = len(frames)
+        R = np.ascontiguousarray(np.stack([np.asarray(f.rotation, np.float64).reshape(9) for f in frames]))
+        t = np.ascontiguousarray(np.stack([np.asarray(f.translation, np.float64).reshape(3) for f in frames]))
+        ptrs = (C.c_void_p * max(nf, 1))()
+        ns = np.zeros(max(nf, 1), np.uint64)
+        keep = []
+        if device_ptrs is not None:
+            for k, (ptr, n) in enumerate(device_ptrs):
+                ptrs[k] = ptr
+                ns[k] = n
+        else:
+            for k, f in enumerate(frames):
+                a = np.ascontiguousarray(f.points, np.float32)
+                keep.append(a)
+                ptrs[k] = a.ctypes.data
+                ns[k] = len(a)
+        out = C.POINTER(Polygons)()
+        tms = (FrameTiming * max(nf, 1))()
+        check(lib().vp_pipeline_run(self.h, C.c_size_t(nf), ptrs, _p(ns, C.c_uint64), _p(R, C.c_double),
+                                    _p(t, C.c_double), C.c_int(1 if device_ptrs is not None else 0),
+                                    C.byref(out) if want_polygons else None, tms if timings else None))
+        polys = polygons_to_py(out) if want_polygons else None
+        return (polys, [tms[k] for k in range(nf)]) if timings else polys
+
+    def run_ptrs(self, ptr_array, n_array, R_array, t_array, device_ptrs, want_polygons):
+        """Low-overhead vp_pipeline_run on prebuilt ctypes arrays (bench)."""
+        out = C.POINTER(Polygons)()
+        check(lib().vp_pipeline_run(self.h, C.c_size_t(len(n_array)), ptr_array, _p(n_array, C.c_uint64),
+                                    _p(R_array, C.c_double), _p(t_array, C.c_double),
+                                    C.c_int(1 if device_ptrs else 0),
+                                    C.byref(out) if want_polygons else None, None))
+        return polygons_to_py(out) if want_polygons else None
+
     def reset(self, start_center):
         c = np.ascontiguousarray(start_center, np.float64)
         check(lib().vp_pipeline_reset(self.h, _p(c, C.c_double)))

@@ -160,5 +160,45 @@ def test_c2_full_stream_properties_and_determinism():
     for poly in t.polygons:
         assert poly["area"] >= 0.002
         v = poly["v2d"]
-        cr = np.cross(np.roll(v, -1, 0) - v, np.roll(v, -2, 0) - np.roll(v, -1, 0))
+        a, b = np.roll(v, -1, 0) - v, np.roll(v, -2, 0) - np.roll(v, -1, 0)
+        cr = a[:, 0] * b[:, 1] - a[:, 1] * b[:, 0]
         assert np.all(cr > 0)                           # strictly convex, CCW
+
+
+@pytest.mark.parametrize("name", ["t1", "stair"])
+def test_pipelined_run_equals_per_frame(name):
+    # vp_pipeline_run overlaps consecutive frames; outputs must equal the
+    # frame-by-frame path and the golden file (exact refine)
+    frames, res, ext, seed, run = run_config(name)
+    p = native.default_params(seed=seed, refine_exact=True)
+    a = native.Pipeline(res, ext, frames[0].translation, p)
+    polys_run = a.run(frames)
+    b = native.Pipeline(res, ext, frames[0].translation, p)
+    for f in frames:
+        polys_frame, _ = b.frame(f.points, f.rotation, f.translation)
+    assert format_polygons(polys_run) == format_polygons(polys_frame) == golden_text(run)
+    oa, ob = a.grid.occupied_voxels(), b.grid.occupied_voxels()
+    for k in oa:
+        assert oa[k].tobytes() == ob[k].tobytes()
+
+
+def test_pipelined_run_c2_matches_frames_and_device_inputs():
+    import torch
+    wl = scenes.workload("c2", frames=12)
+    p = native.default_params(seed=wl.seed)
+    a = native.Pipeline(wl.resolution, wl.extent, wl.frames[0].translation, p)
+    dev = [torch.from_numpy(f.points).cuda() for f in wl.frames]
+    polys_dev, tms = a.run(wl.frames, device_ptrs=[(d.data_ptr(), len(d)) for d in dev], timings=True)
+    assert all(t.total_ms > 0 for t in tms)
+    b = native.Pipeline(wl.resolution, wl.extent, wl.frames[0].translation, p)
+    polys_host = b.run(wl.frames)
+    c = native.Pipeline(wl.resolution, wl.extent, wl.frames[0].translation, p)
+    for f in wl.frames:
+        polys_frame, _ = c.frame(f.points, f.rotation, f.translation)
+    assert format_polygons(polys_dev) == format_polygons(polys_host) == format_polygons(polys_frame)
+    # a second run continues from the map state, like further run_frames iterations
+    more = scenes.workload("c2", frames=30).frames[12:16]
+    a2 = a.run(more, device_ptrs=None)
+    for f in more:
+        polys_frame, _ = c.frame(f.points, f.rotation, f.translation)
+    assert format_polygons(a2) == format_polygons(polys_frame)
