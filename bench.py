@@ -263,6 +263,12 @@ def run_ours(args, rank, world, dist):
         pass
     peak = float(peaks.get("hbm_gbs", 6650.0))
     achieved = per_launch_bytes / per_launch_s / 1e9
+    traffic = None
+    try:  # DRAM bytes of the same kernel from the committed ncu --set full capture
+        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))["dram_bytes_per_launch"]
+        traffic = tr.get(top)
+    except Exception:
+        pass
     # whole-step algorithmic bytes (the survey's frame formula)
     step_bytes = 0.0
     for c, n in zip(per_frame_counters, npts):
@@ -293,7 +299,8 @@ def run_ours(args, rank, world, dist):
         "e2e": {"value": round(e2e_value, 3), "unit": "Hz",
                 "h2d_bytes_per_step": int(12 * sum(npts)), "d2h_bytes_per_step": int(d2h_bytes)},
         "roofline": {"bound": "hbm", "kernel": top, "achieved": round(achieved, 2), "peak": peak,
-                     "unit": "GB/s", "frac": round(achieved / peak, 5), "traffic": None,
+                     "unit": "GB/s", "frac": round(achieved / peak, 5), "traffic": traffic,
+                     "alg_bytes_per_launch": round(per_launch_bytes), "us_per_launch": round(per_launch_s * 1e6, 2),
                      "share_of_step": round(top_ms / prof_total, 4),
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650"},
         "kernels": {k: {"ms_per_step": round(v[0], 4), "calls": int(v[1])}
