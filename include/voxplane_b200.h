@@ -163,6 +163,10 @@ int vp_integrate_frame(vp_grid* g, const float* xyz, uint64_t n, const double ro
 /* VoxelGrid::clear_rays (voxel_grid.cpp:182-215) */
 int vp_clear_rays(vp_grid* g, const float* xyz, uint64_t n, const double rotation[9],
                   const double translation[3], vp_clear_stats* stats);
+/* clear_rays followed by integrate_frame on one frame (pipeline.cpp:200-201)
+   with a single staging of the points; xyz may be a host or device pointer. */
+int vp_update_frame(vp_grid* g, const float* xyz, uint64_t n, const double rotation[9],
+                    const double translation[3], vp_clear_stats* cleared, vp_update_stats* updated);
 /* VoxelGrid::recenter (voxel_grid.cpp:217-252) */
 int vp_recenter(vp_grid* g, const double new_center[3], vp_shift_stats* stats);
 /* VoxelGrid::merge_point (voxel_grid.cpp:49-57), idx in window coordinates */
@@ -222,6 +226,34 @@ void vp_polygons_free(vp_polygons_t* p);
    grid: polygons in ascending cluster-label order, area-filtered. */
 int vp_segment(vp_grid* g, const vp_pipeline_params* p, vp_polygons_t** out,
                vp_frame_timing* timing);
+
+/* ---- spatial slabs --------------------------------------
+   A window of window_extent voxels is split along x; a slab grid owns window
+   x in [x_begin, x_end) and stores one halo plane on each side. Clear and
+   integrate run on every slab with the full window's arithmetic (rays are
+   clipped to the whole window and walked from their start) and keep only
+   owned cells and points; halo planes are filled from the neighbours
+   (vp_grid_plane) before estimate_normals; the per-slab steppable lists,
+   concatenated in slab order, are exactly the single-grid list (ordinals
+   are x-major), and vp_segment_steppable runs CCL .. make_polygon on it.
+   Slab windows are fixed (no recenter), as for SURVEY §8(d) C5. */
+int vp_slab_create(double resolution, const int32_t window_extent[3], const double center[3],
+                   int32_t x_begin, int32_t x_end, int device, vp_grid** out);
+/* Device pointers to the cell records and occupancy-bitmap words of window
+   plane x (owned or halo) of a grid; the halo exchange copies owned boundary
+   planes of one slab onto the halo planes of its neighbour. */
+int vp_grid_plane(vp_grid* g, int32_t window_x, void** cells, uint64_t* cell_bytes, void** bits,
+                  uint64_t* bit_bytes);
+/* estimate_normals + classify_steppable over the owned voxels; returns the
+   steppable list (window indices) as device arrays owned by the grid, valid
+   until the next call on it. */
+int vp_slab_steppable(vp_grid* g, const vp_seg_params* p, uint64_t* count, int32_t** idx,
+                      double** mean, double** normal);
+/* build_adjacency .. make_polygon (voxel_frame_polygons after classify) on a
+   steppable list in window coordinates (device or host arrays). */
+int vp_segment_steppable(vp_grid* g, const vp_pipeline_params* p, uint64_t n, const int32_t* idx,
+                         const double* mean, const double* normal, int device_ptrs,
+                         vp_polygons_t** out);
 
 /* run_frames state: a grid plus the global-cell recenter trigger
    (pipeline.cpp:165, 174, 199-213). */

@@ -15,18 +15,22 @@ namespace vp {
 // ordered) index list and performs the ordered FP64 fold, so the sums are
 // bit-identical to the sequential reference.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ bool point_key(const GridDesc& g, const FrameParams* fp, uint64_t i,
-                                          uint32_t* key) {
+// 0: discarded (non-finite or outside the window), 1: inserted into *key,
+// 2: inside the window but owned by another slab.
+__device__ __forceinline__ int point_key(const GridDesc& g, const FrameParams* fp, uint64_t i,
+                                         uint32_t* key) {
   const float* p = fp->pts + 3 * i;
   const d3 w = pose_apply(fp->R, fp->t, static_cast<double>(p[0]), static_cast<double>(p[1]),
                           static_cast<double>(p[2]));
-  if (!finite3(w)) return false;
-  const int ix = w2i(w.x, fp->origin_pre[0], g.res);
+  if (!finite3(w)) return 0;
+  const int ix = w2i(w.x, fp->origin_pre[0], g.res);  // window coordinates
   const int iy = w2i(w.y, fp->origin_pre[1], g.res);
   const int iz = w2i(w.z, fp->origin_pre[2], g.res);
-  if (!in_bounds(g, ix, iy, iz)) return false;
-  *key = static_cast<uint32_t>((static_cast<uint64_t>(ix) * g.ey + iy) * g.ez + iz);
-  return true;
+  if (ix < 0 || iy < 0 || iz < 0 || ix >= g.gex || iy >= g.ey || iz >= g.ez) return 0;
+  const int lx = ix - g.xoff;
+  if (lx < g.own_lo || lx >= g.own_hi) return 2;
+  *key = static_cast<uint32_t>((static_cast<uint64_t>(lx) * g.ey + iy) * g.ez + iz);
+  return 1;
 }
 
 __global__ void k_integrate_hash(GridDesc g, const FrameParams* __restrict__ fp, Counters* ctr,
@@ -41,8 +45,10 @@ __global__ void k_integrate_hash(GridDesc g, const FrameParams* __restrict__ fp,
     uint32_t key = kEmptyKey;
     bool valid = false;
     if (i < n) {
-      valid = point_key(g, fp, i, &key);
-      if (!valid) ++disc;
+      const int r = point_key(g, fp, i, &key);
+      valid = r == 1;
+      if (r == 0) ++disc;
+      if (r == 2) key = kEmptyKey;
     }
     const unsigned peers = __match_any_sync(0xffffffffu, key);
     const int leader = __ffs(peers) - 1;
@@ -239,12 +245,13 @@ __global__ void __launch_bounds__(256, 4) k_clear_walk(GridDesc g, const FramePa
   const uint64_t n = fp->n;
   const double res = g.res;
   const double lo0 = fp->origin_pre[0], lo1 = fp->origin_pre[1], lo2 = fp->origin_pre[2];
-  const double hi0 = lo0 + static_cast<double>(g.ex) * res;
+  const double hi0 = lo0 + static_cast<double>(g.gex) * res;
   const double hi1 = lo1 + static_cast<double>(g.ey) * res;
   const double hi2 = lo2 + static_cast<double>(g.ez) * res;
   const double a0 = fp->t[0], a1 = fp->t[1], a2 = fp->t[2];
   const int oc0 = w2i(a0, lo0, res), oc1 = w2i(a1, lo1, res), oc2 = w2i(a2, lo2, res);
-  const int max_steps = g.ex + g.ey + g.ez + 4;
+  const int max_steps = g.gex + g.ey + g.ez + 4;
+  const int own0 = g.xoff + g.own_lo, own1 = g.xoff + g.own_hi;  // window x owned here
   const uint32_t xstride = static_cast<uint32_t>(g.ey) * static_cast<uint32_t>(g.W);
   const uint32_t ystride = static_cast<uint32_t>(g.W);
   uint32_t* __restrict__ clr = g.clr;
@@ -284,7 +291,7 @@ __global__ void __launch_bounds__(256, 4) k_clear_walk(GridDesc g, const FramePa
     const int ec0 = w2i(bw.x, lo0, res), ec1 = w2i(bw.y, lo1, res), ec2 = w2i(bw.z, lo2, res);
     const double e0 = a0 + t0 * d0, e1 = a1 + t0 * d1, e2 = a2 + t0 * d2;
     int c0 = w2i(e0, lo0, res), c1 = w2i(e1, lo1, res), c2 = w2i(e2, lo2, res);
-    c0 = c0 < 0 ? 0 : (g.ex - 1 < c0 ? g.ex - 1 : c0);  // std::clamp
+    c0 = c0 < 0 ? 0 : (g.gex - 1 < c0 ? g.gex - 1 : c0);  // std::clamp
     c1 = c1 < 0 ? 0 : (g.ey - 1 < c1 ? g.ey - 1 : c1);
     c2 = c2 < 0 ? 0 : (g.ez - 1 < c2 ? g.ez - 1 : c2);
     int s0 = 0, s1 = 0, s2 = 0;
@@ -304,12 +311,16 @@ __global__ void __launch_bounds__(256, 4) k_clear_walk(GridDesc g, const FramePa
     VP_INIT(d1, c1, lo1, e1, s1, tm1, td1)
     VP_INIT(d2, c2, lo2, e2, s2, tm2, td2)
 #undef VP_INIT
-    uint32_t row = static_cast<uint32_t>(c0) * xstride + static_cast<uint32_t>(c1) * ystride;
+    // local row of the current cell (meaningful while c0 is owned here)
+    uint32_t row = static_cast<uint32_t>(c0 - g.xoff) * xstride + static_cast<uint32_t>(c1) * ystride;
     const int dx_row = s0 * static_cast<int>(xstride), dy_row = s1 * static_cast<int>(ystride);
     for (int s = 0; s < max_steps; ++s) {
       const bool is_o = c0 == oc0 && c1 == oc1 && c2 == oc2;
       const bool is_e = c0 == ec0 && c1 == ec1 && c2 == ec2;
-      if (!is_o && !is_e) {
+      // a slab never sees the ray again once it left the owned x-range in
+      // its stepping direction (the DDA is monotone per axis)
+      if ((s0 > 0 && c0 >= own1) || (s0 < 0 && c0 < own0) || (s0 == 0 && (c0 < own0 || c0 >= own1))) break;
+      if (!is_o && !is_e && c0 >= own0) {
         const uint32_t w = row + (static_cast<uint32_t>(c2) >> 5);
         const uint32_t key = (w << 5) | (static_cast<uint32_t>(c2) & 31u);
         // adjacent pixels stand in the same cell as runs of lanes: only the
@@ -330,7 +341,7 @@ __global__ void __launch_bounds__(256, 4) k_clear_walk(GridDesc g, const FramePa
       c0 += m0 ? s0 : 0;
       c1 += m1s ? s1 : 0;
       c2 += m2 ? s2 : 0;
-      if (static_cast<unsigned>(c0) >= static_cast<unsigned>(g.ex) ||
+      if (static_cast<unsigned>(c0) >= static_cast<unsigned>(g.gex) ||
           static_cast<unsigned>(c1) >= static_cast<unsigned>(g.ey) ||
           static_cast<unsigned>(c2) >= static_cast<unsigned>(g.ez))
         break;
@@ -492,8 +503,9 @@ __global__ void k_frame_begin(Counters* ctr, const unsigned long long* occ_total
 // bitmap (x, y, z lexicographic) into logical flat indices.
 // 256 threads x 8 words per block.
 // ---------------------------------------------------------------------------
-__global__ void k_bitmap_count(const FrameParams* __restrict__ fp, uint64_t nwords, uint32_t* bsum) {
-  const uint32_t* __restrict__ bits = fp->occ_post;
+__global__ void k_bitmap_count(const FrameParams* __restrict__ fp, uint64_t w_lo, uint64_t nwords,
+                               uint32_t* bsum) {
+  const uint32_t* __restrict__ bits = fp->occ_post + w_lo;
   const uint64_t w0 = (static_cast<uint64_t>(blockIdx.x) * kScanThreads + threadIdx.x) * kScanItems;
   uint32_t c = 0;
 #pragma unroll
@@ -503,9 +515,9 @@ __global__ void k_bitmap_count(const FrameParams* __restrict__ fp, uint64_t nwor
   if (threadIdx.x == 0) bsum[blockIdx.x] = c;
 }
 
-__global__ void k_bitmap_emit(const FrameParams* __restrict__ fp, uint64_t nwords, int W, int ez,
-                              const uint32_t* boff, uint32_t* out, uint32_t cap) {
-  const uint32_t* __restrict__ bits = fp->occ_post;
+__global__ void k_bitmap_emit(const FrameParams* __restrict__ fp, uint64_t w_lo, uint64_t nwords, int W,
+                              int ez, const uint32_t* boff, uint32_t* out, uint32_t cap) {
+  const uint32_t* __restrict__ bits = fp->occ_post + w_lo;
   const uint64_t w0 = (static_cast<uint64_t>(blockIdx.x) * kScanThreads + threadIdx.x) * kScanItems;
   uint32_t v[kScanItems];
   uint32_t c = 0;
@@ -520,7 +532,7 @@ __global__ void k_bitmap_emit(const FrameParams* __restrict__ fp, uint64_t nword
     uint32_t b = v[k];
     if (!b) continue;
     const uint64_t w = w0 + k;
-    const uint64_t row = w / W;
+    const uint64_t row = (w + w_lo) / W;
     const uint32_t zb = static_cast<uint32_t>(w % W) * 32;
     while (b) {
       const int t = __ffs(b) - 1;

@@ -141,7 +141,7 @@ __global__ void k_normals(GridDesc g, const FrameParams* __restrict__ fp, Counte
 
 // Steppable list in occupied (lexicographic) order -> ordinals; fills the
 // ordinal map used by the CCL window search.
-__global__ void k_step_emit(GridDesc g, Counters* ctr, SegBufs b, MapDesc m) {
+__global__ void k_step_emit(GridDesc g, Counters* ctr, SegBufs b, MapDesc m, int xadd) {
   const uint32_t V = min(ctr->V, b.Vcap);
   for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x) {
     if (!b.step_flag[v]) continue;
@@ -155,7 +155,7 @@ __global__ void k_step_emit(GridDesc g, Counters* ctr, SegBufs b, MapDesc m) {
     const uint32_t rr = flat / static_cast<uint32_t>(g.ez);
     const int y = static_cast<int>(rr % static_cast<uint32_t>(g.ey));
     const int x = static_cast<int>(rr / static_cast<uint32_t>(g.ey));
-    b.st_idx[3 * s] = x;
+    b.st_idx[3 * s] = x + xadd;  // xadd: slab -> window x (0 for a plain grid)
     b.st_idx[3 * s + 1] = y;
     b.st_idx[3 * s + 2] = z;
 #pragma unroll
@@ -163,8 +163,10 @@ __global__ void k_step_emit(GridDesc g, Counters* ctr, SegBufs b, MapDesc m) {
       b.st_mean[3 * s + k] = b.own_mean[3 * v + k];
       b.st_normal[3 * s + k] = b.est_normal[3 * v + k];
     }
-    m.map[m.slot(x, y, z)] = static_cast<int32_t>(s);
-    atomicOr(m.bits + m.word(x, y, z), 1u << ((z - m.lo[2]) & 31));
+    if (m.map) {
+      m.map[m.slot(x, y, z)] = static_cast<int32_t>(s);
+      atomicOr(m.bits + m.word(x, y, z), 1u << ((z - m.lo[2]) & 31));
+    }
   }
 }
 

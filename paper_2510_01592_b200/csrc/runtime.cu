@@ -361,6 +361,9 @@ struct vp_grid {
   uint32_t* sorted = nullptr;
   Seg seg;
   cudaEvent_t ev[8];
+  // window-sized ordinal map for segmenting a gathered slab steppable list
+  int32_t* gmap = nullptr;
+  uint32_t* gbits = nullptr;
   // CUDA graph of one pipeline frame (see pipeline_enqueue)
   bool capturing = false;
   uint64_t gen = 1;  // bumped whenever a buffer the graph references is reallocated
@@ -373,6 +376,8 @@ struct vp_grid {
     if (gd.clr) cudaFree(gd.clr);
     if (gd.ordmap) cudaFree(gd.ordmap);
     if (gd.stbits) cudaFree(gd.stbits);
+    if (gmap) cudaFree(gmap);
+    if (gbits) cudaFree(gbits);
     if (mstream) cudaStreamSynchronize(mstream);
     for (int q = 0; q < 2; ++q) {
       if (ctr_s[q]) cudaFree(ctr_s[q]);
@@ -413,6 +418,10 @@ struct vp_grid {
     gd.res = res;
     gd.ncells = C;
     gd.nwords = static_cast<uint64_t>(e[0]) * e[1] * gd.W;
+    gd.xoff = 0;
+    gd.own_lo = 0;
+    gd.own_hi = e[0];
+    gd.gex = e[0];
     gd.cells = dalloc<Cell>(C);
     gd.clr = dalloc<uint32_t>(gd.nwords);
     gd.ordmap = dalloc<int32_t>(C);
@@ -442,6 +451,40 @@ struct vp_grid {
     ck(cudaFuncSetAttribute(k_poly_hull, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             kHullSmem * 16 * 6), "smem attr");
     ck(cudaStreamSynchronize(stream), "init sync");
+  }
+
+  // Slab of a window with global extent ge centred on c, owning window x in
+  // [xb, xe): local storage [xb - 1, xe + 1) (one halo plane per side).
+  void init_slab(double res, const int32_t* ge, const double* c, int32_t xb, int32_t xe, int dev) {
+    if (!(res > 0.0) || ge[0] <= 0 || ge[1] <= 0 || ge[2] <= 0 || xb < 0 || xe > ge[0] || xb >= xe)
+      fail(VP_EINVAL, "slab: bad window or x range");
+    const int32_t le[3] = {xe - xb + 2, ge[1], ge[2]};
+    init(res, le, c, dev);
+    origin[0] = c[0] - static_cast<double>(ge[0]) * (0.5 * res);  // the window's origin
+    gd.xoff = xb - 1;
+    gd.own_lo = 1;
+    gd.own_hi = 1 + (xe - xb);
+    gd.gex = ge[0];
+  }
+
+  MapDesc window_map() {
+    const uint64_t C = static_cast<uint64_t>(gd.gex) * gd.ey * gd.ez;
+    const uint64_t nw = static_cast<uint64_t>(gd.gex) * gd.ey * gd.W;
+    if (!gmap) {
+      gmap = dalloc<int32_t>(C);
+      gbits = dalloc<uint32_t>(nw);
+      ck(cudaMemsetAsync(gmap, 0xff, C * 4, stream), "gmap");
+      ck(cudaMemsetAsync(gbits, 0, nw * 4, stream), "gbits");
+    }
+    MapDesc m{};
+    m.map = gmap;
+    m.bits = gbits;
+    m.lo[0] = m.lo[1] = m.lo[2] = 0;
+    m.dims[0] = gd.gex;
+    m.dims[1] = gd.ey;
+    m.dims[2] = gd.ez;
+    m.W = gd.W;
+    return m;
   }
 
   // Back to an empty window centred on c (VoxelGrid constructor state): zero
@@ -522,6 +565,15 @@ struct vp_grid {
   // Host part of recenter (voxel_grid.cpp:217-223) -> post-shift state.
   bool plan_recenter(const double* c, vp_shift_stats* st) {
     const double res = gd.res;
+    if (gd.gex != gd.ex || gd.xoff != 0) {
+      // slab windows are fixed; a shift would move cells between ranks
+      for (int k = 0; k < 3; ++k) {
+        const double wc = origin[k] + static_cast<double>(k == 0 ? gd.gex : ext[k]) * (0.5 * res);
+        if (std::llround((c[k] - wc) / res) != 0) fail(VP_EINVAL, "recenter: slab windows are fixed");
+      }
+      if (st) std::memset(st, 0, sizeof *st);
+      return false;
+    }
     int32_t s[3];
     for (int k = 0; k < 3; ++k) {
       const double wc = origin[k] + static_cast<double>(ext[k]) * (0.5 * res);  // world_center
@@ -583,9 +635,11 @@ struct vp_grid {
   // Occupied scan of the post-recenter bitmap into seg.b.occ_list; ctr->V.
   void launch_occupied_scan() {
     const uint32_t nb = static_cast<uint32_t>((gd.nwords + kScanPerBlock - 1) / kScanPerBlock);
-    LAUNCH(k_bitmap_count, nb, kScanThreads, 0, stream, d_fp, gd.nwords, seg.bsum);
+    const uint64_t w_lo = static_cast<uint64_t>(gd.own_lo) * gd.ey * gd.W;
+    const uint64_t w_n = static_cast<uint64_t>(gd.own_hi - gd.own_lo) * gd.ey * gd.W;
+    LAUNCH(k_bitmap_count, nb, kScanThreads, 0, stream, d_fp, w_lo, w_n, seg.bsum);
     LAUNCH(k_scan_exclusive, 1, 1024, 0, stream, seg.bsum, nb, nullptr, &ctr->V, nullptr);
-    LAUNCH(k_bitmap_emit, nb, kScanThreads, 0, stream, d_fp, gd.nwords, gd.W, gd.ez, seg.bsum,
+    LAUNCH(k_bitmap_emit, nb, kScanThreads, 0, stream, d_fp, w_lo, w_n, gd.W, gd.ez, seg.bsum,
            seg.b.occ_list, seg.b.Vcap);
   }
 
@@ -616,8 +670,8 @@ struct vp_grid {
     LAUNCH(k_normals, kWide, kThreads, 0, stream, gd, d_fp, ctr, sd, seg.b, write_status);
     launch_flag_scan(seg.b.step_flag, &ctr->V, seg.b.Vcap, seg.b.step_pos, &ctr->S);
   }
-  void launch_step_emit(const MapDesc& m) {
-    LAUNCH(k_step_emit, kWide, kThreads, 0, stream, gd, ctr, seg.b, m);
+  void launch_step_emit(const MapDesc& m, int xadd = 0) {
+    LAUNCH(k_step_emit, kWide, kThreads, 0, stream, gd, ctr, seg.b, m, xadd);
   }
   // union-find over the steppable list in seg.b (ctr->S set)
   void launch_ccl(const SegDev& sd, const MapDesc& m) {
@@ -807,8 +861,8 @@ void stage_points(vp_grid* g, const float* xyz, uint64_t n, bool device_ptr) {
     g->h_fp->pts = xyz;
   } else {
     g->ensure_points(n);
-    if (n)
-      ck(cudaMemcpyAsync(g->d_pts, xyz, n * 12, cudaMemcpyHostToDevice, g->stream), "points h2d");
+    if (n)  // cudaMemcpyDefault: host (pageable or pinned) or device source
+      ck(cudaMemcpyAsync(g->d_pts, xyz, n * 12, cudaMemcpyDefault, g->stream), "points h2d");
     g->h_fp->pts = g->d_pts;
   }
   g->h_fp->n = n;
@@ -1242,6 +1296,32 @@ int vp_clear_rays(vp_grid* g, const float* xyz, uint64_t n, const double R[9], c
   });
 }
 
+int vp_update_frame(vp_grid* g, const float* xyz, uint64_t n, const double R[9], const double t[3],
+                    vp_clear_stats* cs, vp_update_stats* us) {
+  return guard([&] {
+    if (!is_valid_rotation(R)) fail(VP_EINVAL, "clear_rays: pose rotation is not orthonormal");
+    g->set_slot(0);
+    g->lstream = g->stream;
+    g->set_pose(R, t);
+    g->fill_static_params();
+    stage_points(g, xyz, n, false);
+    g->upload_params();
+    g->reset_frame_counters();
+    g->launch_clear(n);
+    g->launch_integrate(n);
+    g->launch_finalize();
+    g->read_counters();
+    if (cs) {
+      cs->voxels_cleared = g->h_ctr->cleared;
+      cs->voxels_freed = g->h_ctr->freed;
+    }
+    if (us) {
+      us->voxels_touched = g->h_ctr->touched;
+      us->points_discarded = g->h_ctr->discarded;
+    }
+  });
+}
+
 int vp_recenter(vp_grid* g, const double c[3], vp_shift_stats* st) {
   return guard([&] {
     vp_shift_stats tmp;
@@ -1275,13 +1355,15 @@ int vp_merge_point(vp_grid* g, const int32_t idx[3], const double p[3]) {
 
 static uint64_t host_phys(const vp_grid* g, const int32_t* idx) {
   int64_t p[3];
-  for (int k = 0; k < 3; ++k) p[k] = (static_cast<int64_t>(idx[k]) + g->off[k]) % g->ext[k];
+  int32_t l[3] = {idx[0] - g->gd.xoff, idx[1], idx[2]};  // slab: window x -> local x
+  for (int k = 0; k < 3; ++k) p[k] = (static_cast<int64_t>(l[k]) + g->off[k]) % g->ext[k];
   return (static_cast<uint64_t>(p[0]) * g->ext[1] + p[1]) * g->ext[2] + p[2];
 }
 
 int vp_get_cell(vp_grid* g, const int32_t idx[3], double sum[3], uint32_t* count, uint8_t* status) {
   return guard([&] {
-    if (idx[0] < 0 || idx[1] < 0 || idx[2] < 0 || idx[0] >= g->ext[0] || idx[1] >= g->ext[1] ||
+    const int32_t lx = idx[0] - g->gd.xoff;
+    if (lx < 0 || idx[1] < 0 || idx[2] < 0 || lx >= g->ext[0] || idx[1] >= g->ext[1] ||
         idx[2] >= g->ext[2])
       fail(VP_EINVAL, "cell: index out of bounds");
     Cell c;
@@ -1300,7 +1382,8 @@ int vp_get_cell(vp_grid* g, const int32_t idx[3], double sum[3], uint32_t* count
 
 int vp_set_status(vp_grid* g, const int32_t idx[3], uint8_t status) {
   return guard([&] {
-    if (idx[0] < 0 || idx[1] < 0 || idx[2] < 0 || idx[0] >= g->ext[0] || idx[1] >= g->ext[1] ||
+    const int32_t lx = idx[0] - g->gd.xoff;
+    if (lx < 0 || idx[1] < 0 || idx[2] < 0 || lx >= g->ext[0] || idx[1] >= g->ext[1] ||
         idx[2] >= g->ext[2])
       fail(VP_EINVAL, "set_status: index out of bounds");
     Cell* c = g->gd.cells + host_phys(g, idx);
@@ -1792,6 +1875,106 @@ int vp_make_polygons(size_t n, const vp_plane* planes, const uint64_t* offsets,
 }
 
 void vp_polygons_free(vp_polygons_t* p) { std::free(p); }
+
+int vp_slab_create(double res, const int32_t window_extent[3], const double center[3],
+                   int32_t x_begin, int32_t x_end, int device, vp_grid** out) {
+  *out = nullptr;
+  return guard([&] {
+    auto* g = new vp_grid();
+    try {
+      g->init_slab(res, window_extent, center, x_begin, x_end, device);
+    } catch (...) {
+      delete g;
+      throw;
+    }
+    *out = g;
+  });
+}
+
+int vp_grid_plane(vp_grid* g, int32_t window_x, void** cells, uint64_t* cell_bytes, void** bits,
+                  uint64_t* bit_bytes) {
+  return guard([&] {
+    const int32_t lx = window_x - g->gd.xoff;
+    if (lx < 0 || lx >= g->gd.ex) fail(VP_EINVAL, "grid_plane: x outside this grid");
+    if (g->off[0] || g->off[1] || g->off[2]) fail(VP_EINVAL, "grid_plane: window was recentered");
+    const uint64_t plane = static_cast<uint64_t>(g->gd.ey) * g->gd.ez;
+    const uint64_t wplane = static_cast<uint64_t>(g->gd.ey) * g->gd.W;
+    *cells = g->gd.cells + lx * plane;
+    *cell_bytes = plane * sizeof(Cell);
+    *bits = g->occ[g->cur] + lx * wplane;
+    *bit_bytes = wplane * 4;
+  });
+}
+
+int vp_slab_steppable(vp_grid* g, const vp_seg_params* p, uint64_t* count, int32_t** idx,
+                      double** mean, double** normal) {
+  return guard([&] {
+    const SegDev sd = make_segdev(*p, g->gd.res);
+    MapDesc none{};
+    for (int tries = 0;; ++tries) {
+      g->fill_static_params();
+      g->h_fp->n = 0;
+      g->upload_params();
+      g->reset_frame_counters();
+      g->launch_occupied_scan();
+      g->launch_classify(sd, 1);
+      g->launch_step_emit(none, g->gd.xoff);
+      g->read_counters();
+      if (!(g->h_ctr->overflow & (kOverflowOcc | kOverflowStep)) || tries > 4) break;
+      const uint32_t need = static_cast<uint32_t>(std::min<uint64_t>(g->gd.ncells, 2ull * g->h_ctr->V));
+      g->seg.ensure(std::max(need, g->seg.b.Vcap), std::max(need, g->seg.b.Scap), g->seg.b.Icap,
+                    100, g->gd.nwords);
+    }
+    *count = g->h_ctr->S;
+    *idx = g->seg.b.st_idx;
+    *mean = g->seg.b.st_mean;
+    *normal = g->seg.b.st_normal;
+  });
+}
+
+int vp_segment_steppable(vp_grid* g, const vp_pipeline_params* p, uint64_t S, const int32_t* idx,
+                         const double* mean, const double* normal, int device_ptrs,
+                         vp_polygons_t** out) {
+  if (out) *out = nullptr;
+  return guard([&] {
+    const uint32_t n = static_cast<uint32_t>(S);
+    const SegDev sd = make_segdev(p->seg, g->gd.res);
+    const RansacDev rd = make_ransacdev(p->ransac);
+    g->seg.ensure(std::max(n, g->seg.b.Vcap), std::max(n, g->seg.b.Scap), std::max(n, g->seg.b.Icap),
+                  p->ransac.iterations, g->gd.nwords);
+    g->seg.ensure_dirs(16, g->stream);
+    const cudaMemcpyKind kind = device_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    if (S && idx != g->seg.b.st_idx) {
+      ck(cudaMemcpyAsync(g->seg.b.st_idx, idx, 12 * S, kind, g->stream), "st idx");
+      ck(cudaMemcpyAsync(g->seg.b.st_mean, mean, 24 * S, kind, g->stream), "st mean");
+      ck(cudaMemcpyAsync(g->seg.b.st_normal, normal, 24 * S, kind, g->stream), "st normal");
+    }
+    const MapDesc m = g->window_map();
+    for (int tries = 0;; ++tries) {
+      g->fill_static_params();
+      g->h_fp->n = 0;
+      g->upload_params();
+      g->reset_frame_counters();
+      set_counter_u32(g, offsetof(Counters, S), n);
+      LAUNCH(k_map_fill, kWide, kThreads, 0, g->stream, g->ctr, g->seg.b, m);
+      g->launch_ccl(sd, m);
+      g->launch_clusters(sd);
+      g->launch_ransac(rd);
+      g->launch_refine(p->ransac.up, p->refine, p->refine_exact);
+      g->launch_polygon(16, p->min_polygon_area);
+      g->read_counters();
+      if (!g->h_ctr->overflow || tries > 4) break;
+      if (g->h_ctr->overflow & kOverflowClusters)
+        fail(VP_ENOMEM, "more than 2048 clusters >= min_cluster_size in one frame");
+      g->seg.ensure(g->seg.b.Vcap, g->seg.b.Scap, 2 * g->seg.b.Icap, p->ransac.iterations, g->gd.nwords);
+    }
+    if (out) {
+      HostPolys hp;
+      g->download_polygons(hp, false);
+      *out = make_polygons_out(hp);
+    }
+  });
+}
 
 int vp_segment(vp_grid* g, const vp_pipeline_params* p, vp_polygons_t** out,
                vp_frame_timing* timing) {

@@ -57,10 +57,16 @@ struct GridDesc {
   uint32_t* clr;
   int32_t* ordmap;
   uint32_t* stbits;  // steppable presence bitmap (logical, occ layout)
-  int32_t ex, ey, ez, W;  // extent and words per (x,y) row
+  int32_t ex, ey, ez, W;  // (local) extent and words per (x,y) row
   double res;
   uint64_t ncells;
   uint64_t nwords;
+  // Spatial slab: this grid stores window x in
+  // [xoff, xoff + ex) and owns [xoff + own_lo, xoff + own_hi); the rest are
+  // halo planes filled from the neighbouring slabs. gex is the window's full
+  // x extent (ray clipping and point bounds use the whole window). A plain
+  // grid has xoff = 0, own = [0, ex), gex = ex.
+  int32_t xoff, own_lo, own_hi, gex;
 };
 
 // Device counters (one struct in device memory, zeroed per frame except

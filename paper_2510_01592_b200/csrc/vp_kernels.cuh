@@ -194,8 +194,8 @@ __global__ void k_map_finalize(Counters* ctr, unsigned long long* occ_total);
 __global__ void k_frame_begin(Counters* ctr, const unsigned long long* occ_total);
 __global__ void k_set_statuses(GridDesc g, const FrameParams* fp, const int32_t* idx, const uint8_t* st,
                                uint64_t n);
-__global__ void k_bitmap_count(const FrameParams* fp, uint64_t nwords, uint32_t* bsum);
-__global__ void k_bitmap_emit(const FrameParams* fp, uint64_t nwords, int W, int ez,
+__global__ void k_bitmap_count(const FrameParams* fp, uint64_t w_lo, uint64_t nwords, uint32_t* bsum);
+__global__ void k_bitmap_emit(const FrameParams* fp, uint64_t w_lo, uint64_t nwords, int W, int ez,
                               const uint32_t* boff, uint32_t* out, uint32_t cap);
 __global__ void k_flags_count(const uint8_t* flags, const uint32_t* n_ptr, uint32_t cap,
                               uint32_t* bsum);
@@ -211,7 +211,7 @@ __global__ void k_normals(GridDesc g, const FrameParams* fp, Counters* ctr, SegD
                           int write_status);
 __global__ void k_adjacency(Counters* ctr, SegDev sp, SegBufs b, MapDesc m, const uint64_t* rows,
                             uint32_t* counts, int32_t* cols);
-__global__ void k_step_emit(GridDesc g, Counters* ctr, SegBufs b, MapDesc m);
+__global__ void k_step_emit(GridDesc g, Counters* ctr, SegBufs b, MapDesc m, int xadd);
 __global__ void k_map_fill(Counters* ctr, SegBufs b, MapDesc m);
 __global__ void k_occ_gather(GridDesc g, const FrameParams* fp, Counters* ctr, SegBufs b);
 __global__ void k_ccl_init(Counters* ctr, SegBufs b);

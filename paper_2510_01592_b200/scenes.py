@@ -221,4 +221,42 @@ def workload(name: str, frames: int | None = None) -> Workload:
         sensor = SensorSpec(kind=1, pattern=spherical_pattern(2_000_000), max_range=10.0, rate_hz=30.0)
         poses = default_trajectory(STAIR5, n, 30.0)
         return Workload(name, render(s, sensor, poses, 2025), 0.01, (500, 500, 500), 2025)
+    if name == "c5":
+        return c5_workload(frames or 6)
     raise ValueError(name)
+
+
+def c5_scene() -> Scene:
+    """C5: 20 x 20 m floor, 20 x 10 m mezzanine at 1.5 m, two 9-step box stairs
+    up to it, ten 1.2 x 0.8 m tables at 0.75 m."""
+    s = Scene()
+    s.rects.append(horizontal_rect((0.0, 0.0, 0.0), 10.0, 10.0))
+    s.rects.append(horizontal_rect((0.0, 5.0, 1.5), 10.0, 5.0))
+    rise, run, width = 1.5 / 9.0, 0.3, 1.2
+    for x0 in (-6.0, 5.0):
+        y0 = -9 * run
+        for k in range(9):
+            s.boxes.append(((x0, y0 + k * run, 0.0), (x0 + width, y0 + (k + 1) * run, (k + 1) * rise)))
+    for i in range(5):
+        for j in range(2):
+            s.rects.append(horizontal_rect((-8.0 + 3.5 * i, -6.0 + 4.0 * j, 0.75), 0.6, 0.4))
+    return s
+
+
+C5_EXTENT = (2000, 2000, 300)
+C5_CENTER = (0.0, 0.0, 1.45)
+
+
+def c5_workload(frames: int, rays: int = 1_000_000) -> Workload:
+    """Sphere LiDAR (1M rays, 10 m) along a lawnmower path at 0.6 m over the
+    C5 scene; fixed 2000 x 2000 x 300 window at 0.01 m."""
+    poses = []
+    for k in range(frames):
+        lane = k // 4
+        u = (k % 4) / 3.0
+        x = -7.0 + 14.0 * (u if lane % 2 == 0 else 1.0 - u)
+        y = -7.0 + 3.0 * lane
+        R = np.eye(3)
+        poses.append(np.concatenate([R.reshape(9), [x, y, 0.6]]))
+    sensor = SensorSpec(kind=1, pattern=spherical_pattern(rays), max_range=10.0, rate_hz=10.0)
+    return Workload("c5", render(c5_scene(), sensor, np.array(poses), 2025), 0.01, C5_EXTENT, 2025)
