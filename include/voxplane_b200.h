@@ -271,6 +271,9 @@ void* vp_pipeline_stream(vp_pipeline* pl);
    occupied, V_occ, V_step, clusters, fits, padded members, inliers,
    polygon vertices, newly occupied, largest hull-survivor set, overflow flags. */
 int vp_pipeline_counters(vp_pipeline* pl, uint64_t out[16]);
+/* The same counters for a grid driven through the grid / slab entry points
+   (values of the last call that read them back). */
+int vp_grid_counters(vp_grid* g, uint64_t out[16]);
 /* One frame of run_frames: clear_rays, integrate_frame, recenter-if-moved,
    voxel_frame_polygons. out may be NULL (polygons stay on the device). */
 int vp_pipeline_frame(vp_pipeline* pl, const float* xyz, uint64_t n, const double rotation[9],

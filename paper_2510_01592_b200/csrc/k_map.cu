@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(256, 4) k_clear_walk(GridDesc g, const FramePa
       // a slab never sees the ray again once it left the owned x-range in
       // its stepping direction (the DDA is monotone per axis)
       if ((s0 > 0 && c0 >= own1) || (s0 < 0 && c0 < own0) || (s0 == 0 && (c0 < own0 || c0 >= own1))) break;
-      if (!is_o && !is_e && c0 >= own0) {
+      if (!is_o && !is_e && c0 >= own0 && c0 < own1) {  // not yet entered: skip
         const uint32_t w = row + (static_cast<uint32_t>(c2) >> 5);
         const uint32_t key = (w << 5) | (static_cast<uint32_t>(c2) & 31u);
         // adjacent pixels stand in the same cell as runs of lanes: only the

@@ -1940,17 +1940,34 @@ int vp_segment_steppable(vp_grid* g, const vp_pipeline_params* p, uint64_t S, co
     const uint32_t n = static_cast<uint32_t>(S);
     const SegDev sd = make_segdev(p->seg, g->gd.res);
     const RansacDev rd = make_ransacdev(p->ransac);
+    cudaMemcpyKind kind = device_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    // the lists may be this grid's own steppable buffers (vp_slab_steppable),
+    // which a capacity retry below reallocates: stage them aside first
+    int32_t* stage = nullptr;
+    if (S && idx == g->seg.b.st_idx) {
+      stage = dalloc<int32_t>(15 * S);
+      ck(cudaMemcpyAsync(stage, idx, 12 * S, cudaMemcpyDeviceToDevice, g->stream), "stage idx");
+      ck(cudaMemcpyAsync(stage + 3 * S, mean, 24 * S, cudaMemcpyDeviceToDevice, g->stream), "stage mean");
+      ck(cudaMemcpyAsync(stage + 9 * S, normal, 24 * S, cudaMemcpyDeviceToDevice, g->stream), "stage nrm");
+      idx = stage;
+      mean = reinterpret_cast<const double*>(stage + 3 * S);
+      normal = reinterpret_cast<const double*>(stage + 9 * S);
+      kind = cudaMemcpyDeviceToDevice;
+    }
+    struct Free {
+      int32_t* p;
+      ~Free() { if (p) cudaFree(p); }
+    } free_stage{stage};
     g->seg.ensure(std::max(n, g->seg.b.Vcap), std::max(n, g->seg.b.Scap), std::max(n, g->seg.b.Icap),
                   p->ransac.iterations, g->gd.nwords);
     g->seg.ensure_dirs(16, g->stream);
-    const cudaMemcpyKind kind = device_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-    if (S && idx != g->seg.b.st_idx) {
-      ck(cudaMemcpyAsync(g->seg.b.st_idx, idx, 12 * S, kind, g->stream), "st idx");
-      ck(cudaMemcpyAsync(g->seg.b.st_mean, mean, 24 * S, kind, g->stream), "st mean");
-      ck(cudaMemcpyAsync(g->seg.b.st_normal, normal, 24 * S, kind, g->stream), "st normal");
-    }
     const MapDesc m = g->window_map();
     for (int tries = 0;; ++tries) {
+      if (S) {  // (re)load the lists: a retry's ensure() reallocated the buffers
+        ck(cudaMemcpyAsync(g->seg.b.st_idx, idx, 12 * S, kind, g->stream), "st idx");
+        ck(cudaMemcpyAsync(g->seg.b.st_mean, mean, 24 * S, kind, g->stream), "st mean");
+        ck(cudaMemcpyAsync(g->seg.b.st_normal, normal, 24 * S, kind, g->stream), "st normal");
+      }
       g->fill_static_params();
       g->h_fp->n = 0;
       g->upload_params();
@@ -2023,6 +2040,16 @@ int vp_pipeline_reset(vp_pipeline* pl, const double start_center[3]) {
 vp_grid* vp_pipeline_grid(vp_pipeline* pl) { return pl->grid; }
 
 void* vp_pipeline_stream(vp_pipeline* pl) { return pl->grid->stream; }
+
+int vp_grid_counters(vp_grid* g, uint64_t out[16]) {
+  return guard([&] {
+    const Counters& c = *g->h_ctr;
+    const uint64_t v[16] = {c.cleared, c.freed, c.touched, c.discarded, c.dropped, c.occupied,
+                            c.V, c.S, c.K, c.nfits, c.padded_members, c.inliers, c.pool_used,
+                            c.newly, c.surv_max, c.overflow};
+    std::memcpy(out, v, sizeof v);
+  });
+}
 
 int vp_pipeline_counters(vp_pipeline* pl, uint64_t out[16]) {
   return guard([&] {

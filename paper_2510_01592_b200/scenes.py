@@ -116,7 +116,8 @@ def rosette_pattern(n: int, cone_deg=70.0, freq_ratio=7.96) -> np.ndarray:
     return out
 
 
-def render(scene: Scene, sensor: SensorSpec, poses: np.ndarray, seed: int, threads: int = 0) -> list[Frame]:
+def render(scene: Scene, sensor: SensorSpec, poses: np.ndarray, seed: int, threads: int = 0,
+           first_index: int = 0) -> list[Frame]:
     """render_frame (scene_sim.cpp:186-236) for each pose, frame index = position."""
     B, nb, R, nr = scene.ctypes()
     s = Sensor()
@@ -139,7 +140,7 @@ def render(scene: Scene, sensor: SensorSpec, poses: np.ndarray, seed: int, threa
         native.check(_L().vp_render_frame(B, C.c_size_t(nb), R, C.c_size_t(nr), C.byref(s),
                                           Rm.ctypes.data_as(C.POINTER(C.c_double)),
                                           t.ctypes.data_as(C.POINTER(C.c_double)), C.c_uint64(seed),
-                                          C.c_uint64(fi), C.c_int(threads), C.byref(pts), C.byref(n),
+                                          C.c_uint64(fi + first_index), C.c_int(threads), C.byref(pts), C.byref(n),
                                           qR.ctypes.data_as(C.POINTER(C.c_double)),
                                           qt.ctypes.data_as(C.POINTER(C.c_double))))
         arr = np.ctypeslib.as_array(pts, (n.value, 3)).copy() if n.value else np.zeros((0, 3), np.float32)
@@ -247,9 +248,18 @@ C5_EXTENT = (2000, 2000, 300)
 C5_CENTER = (0.0, 0.0, 1.45)
 
 
-def c5_workload(frames: int, rays: int = 1_000_000) -> Workload:
+def c5_workload(frames: int, rays: int = 1_000_000, first: int = 0) -> Workload:
     """Sphere LiDAR (1M rays, 10 m) along a lawnmower path at 0.6 m over the
-    C5 scene; fixed 2000 x 2000 x 300 window at 0.01 m."""
+    C5 scene; fixed 2000 x 2000 x 300 window at 0.01 m. Frame indices
+    first .. first + frames - 1 of the path."""
+    poses = c5_poses(first + frames)[first:]
+    sensor = SensorSpec(kind=1, pattern=spherical_pattern(rays), max_range=10.0, rate_hz=10.0)
+    out = render(c5_scene(), sensor, poses, 2025, first_index=first)
+    return Workload("c5", out, 0.01, C5_EXTENT, 2025)
+
+
+def c5_poses(frames: int) -> np.ndarray:
+    """Lawnmower path: lanes of 4 poses along x, 3 m apart in y."""
     poses = []
     for k in range(frames):
         lane = k // 4
@@ -258,5 +268,4 @@ def c5_workload(frames: int, rays: int = 1_000_000) -> Workload:
         y = -7.0 + 3.0 * lane
         R = np.eye(3)
         poses.append(np.concatenate([R.reshape(9), [x, y, 0.6]]))
-    sensor = SensorSpec(kind=1, pattern=spherical_pattern(rays), max_range=10.0, rate_hz=10.0)
-    return Workload("c5", render(c5_scene(), sensor, np.array(poses), 2025), 0.01, C5_EXTENT, 2025)
+    return np.array(poses)

@@ -100,6 +100,13 @@ class Slab:
                                          C.c_void_p(nrm_t.data_ptr() if S else 0), C.c_int(1), C.byref(out)))
         return polygons_to_py(out)
 
+    def counters(self):
+        """vp_grid_counters: cleared freed touched discarded dropped occupied V S K fits padded
+        inliers poolv newly surv_max overflow, as of the last call that read them back."""
+        out = np.zeros(16, np.uint64)
+        check(lib().vp_grid_counters(self.h, _p(out, C.c_uint64)))
+        return out
+
     def close(self):
         if self.h:
             lib().vp_grid_destroy(self.h)
@@ -201,13 +208,21 @@ class DistComm:
 
 def slab_frame(slabs, comm, pts_t, R, t, params: native.PipelineParams):
     """One frame over the local slabs; returns the polygons on rank 0 (else None)."""
+    import torch
+    # the library runs on its own streams and returns synchronised; whatever
+    # torch (or NCCL, which torch's stream waits on) produced is fenced with a
+    # stream synchronise before the library reads it
+    sync = torch.cuda.current_stream().synchronize if pts_t.is_cuda else (lambda: None)
     pts_t = comm.broadcast_frame(pts_t)
+    sync()
     n = pts_t.numel() // 12 if pts_t.dtype.itemsize == 1 else pts_t.numel() // 3
     for s in slabs:
         s.clear_integrate_device(pts_t.data_ptr(), n, R, t)
     comm.halo_exchange(slabs)
+    sync()
     parts = [s.steppable(params.seg) for s in slabs]
     S, idx, mean, nrm = comm.gather_steppable(parts)
     if idx is None:
         return None
+    sync()
     return slabs[0].segment(params, S, idx, mean, nrm)
