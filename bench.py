@@ -393,20 +393,11 @@ def run_slabs(args, rank, world, dist):
     L.vp_profile_enable(1)
     i = W + K - 1
     R, t = rot(i)
-    pts_t = comm.broadcast_frame(dev_pts[i] if rank == 0 else empty)
-    torch.cuda.synchronize()
-    slab.clear_integrate_device(pts_t.data_ptr(), pts_t.numel() // 3, R, t)
-    c_map = slab.counters().astype(np.float64)
-    comm.halo_exchange([slab])
-    torch.cuda.synchronize()
-    part = slab.steppable(params.seg)
-    c_step = slab.counters().astype(np.float64)
-    S, idx, mean, nrm = comm.gather_steppable([part])
-    c_seg = np.zeros(16)
-    if idx is not None:
-        torch.cuda.synchronize()
-        slab.segment(params, S, idx, mean, nrm)
-        c_seg = slab.counters().astype(np.float64)
+    stages = {}
+    slabs.slab_frame([slab], comm, dev_pts[i] if rank == 0 else empty, R, t, params, stages=stages)
+    c_map = stages["c_map"].astype(np.float64)
+    c_step = stages["c_step"].astype(np.float64)
+    c_seg = stages["c_seg"].astype(np.float64)
     names = (C.c_char_p * 128)()
     ms = (C.c_double * 128)()
     calls = (C.c_uint64 * 128)()
@@ -461,7 +452,8 @@ def run_slabs(args, rank, world, dist):
                    "slabs": [list(r) for r in slabs.split_x(ext[0], world)], "timed_frames": f"{W}..{W + K - 1}",
                    "e2e_frames": f"{W}..{W + K - 1} again (revisit)", "points_per_frame": round(timed_pts / K),
                    "l2": "flushed (256 MiB write) between steps; window 38.4 GB >> L2",
-                   "parallelism": f"x-slabs x{world} (halo planes + steppable gather over NCCL)"
+                   "parallelism": f"x-slabs x{world} (halo planes, halo steppable lists, boundary-label "
+                                  "merge and cluster gather to the owner over NCCL)"
                    if world > 1 else "single slab"},
         "gpu_launches": int(launches),
         "e2e": {"value": round(K / (e2e_ms / 1e3), 3), "unit": "Hz",

@@ -255,6 +255,60 @@ int vp_segment_steppable(vp_grid* g, const vp_pipeline_params* p, uint64_t n, co
                          const double* mean, const double* normal, int device_ptrs,
                          vp_polygons_t** out);
 
+/* ---- distributed segmentation over slabs -----------------
+   build_adjacency + label_components (segmentation.cpp:87-194) run per slab
+   on its own steppable voxels plus the w = max(1, ceil(distance_th / res))
+   planes either side (segmentation.cpp:89), received from the slabs that own
+   them; a boundary-label merge makes the labels the single-grid canonical
+   ones (component-minimum global ordinal); every cluster's members are sent
+   to the slab owning its label, which runs filter_clusters .. make_polygon
+   (pipeline.cpp:43-85) for the clusters it owns. Per frame, after
+   vp_slab_steppable:
+     vp_slab_plane_counts -> (all-gather) -> vp_slab_extend -> (halo lists)
+     -> vp_slab_label -> (all-gather of triples) -> vp_slab_merge
+     -> vp_slab_export -> (members to owners) -> vp_slab_segment_owned
+   All arrays are device arrays owned by the grid unless stated. */
+typedef struct {
+  int32_t n_slabs;
+  const int32_t* x_begin;        /* n_slabs + 1: first window x of every slab, then window extent x */
+  const uint32_t* plane_counts;  /* window_extent[0]: steppable voxels per window x-plane, all slabs */
+} vp_slab_layout;
+/* A cluster member on its way to the slab that owns the cluster (32 B). */
+typedef struct {
+  double mean[3];
+  int32_t label;   /* canonical label = global ordinal of the cluster's minimum */
+  int32_t pad;
+} vp_member_rec;
+
+/* segmentation.cpp:89 */
+int vp_adjacency_window(const vp_seg_params* p, double resolution, int32_t* w);
+/* Steppable voxels per owned x-plane (n_planes = owned planes), from the
+   last vp_slab_steppable. */
+int vp_slab_plane_counts(vp_grid* g, uint32_t** counts, int32_t* n_planes);
+/* Extended list of window planes [x_lo, x_hi) = owned planes +- w (clipped):
+   the own list is copied into place; the caller fills the halo entries
+   (entries of plane x start at index P[x] - P[x_lo], P = prefix sum of the
+   layout's plane counts) from the owning slabs' lists. */
+int vp_slab_extend(vp_grid* g, const vp_seg_params* p, const vp_slab_layout* layout, int32_t** idx,
+                   double** mean, double** normal, uint64_t* n_ext, int32_t* x_lo, int32_t* x_hi);
+/* Local union-find over the extended list; returns this slab's boundary
+   triples (3 x int32: zone index of an entry in the boundary zone, zone
+   index of its local component's smallest zone entry, local label) and the
+   zone size (same on every slab). */
+int vp_slab_label(vp_grid* g, const vp_seg_params* p, int32_t** triples, uint64_t* n_triples,
+                  uint64_t* zone_size);
+/* Merge the triples of all slabs (device; triples with a negative first
+   entry are padding); labels = canonical label of every owned entry. */
+int vp_slab_merge(vp_grid* g, const int32_t* triples, uint64_t n_triples, int32_t** labels);
+/* Members of clusters owned by lower slabs, sorted by destination slab
+   (ascending ordinal within each); dest_counts (host, n_slabs entries). */
+int vp_slab_export(vp_grid* g, uint64_t* dest_counts, void** records);
+/* filter_clusters .. make_polygon for the clusters this slab owns: its own
+   members followed by the records received from the higher slabs in slab
+   order (device vp_member_rec array). Polygons in ascending label order. */
+int vp_slab_segment_owned(vp_grid* g, const vp_pipeline_params* p, const void* recv, uint64_t n_recv,
+                          vp_polygons_t** out);
+
 /* run_frames state: a grid plus the global-cell recenter trigger
    (pipeline.cpp:165, 174, 199-213). */
 int vp_pipeline_create(double resolution, const int32_t extent[3],

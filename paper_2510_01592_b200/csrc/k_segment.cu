@@ -198,40 +198,6 @@ __global__ void k_ccl_init(Counters* ctr, SegBufs b) {
 // always hooks the larger root under the smaller (atomicCAS), so every root is
 // its component's minimum ordinal: the canonical label, bit-exact.
 // ---------------------------------------------------------------------------
-// Parent pointers only ever move to an ancestor (hooks: root -> smaller root;
-// pointer jumping: node -> grandparent), so every value a thread can observe
-// is an ancestor of the node. Reads go through L2 (ld.cg): a stale value is
-// still an ancestor, so "same root" answers are always right and a wrong
-// "different roots" answer is corrected by the atomicCAS retry.
-__device__ __forceinline__ int uf_find(int32_t* parent, int v) {
-  int par = __ldcg(parent + v);
-  if (par != v) {
-    int next, prev = v;
-    while (par > (next = __ldcg(parent + par))) {
-      __stcg(parent + prev, next);  // pointer jumping; parent[x] <= x always holds
-      prev = par;
-      par = next;
-    }
-  }
-  return par;
-}
-
-// Link two roots (larger under smaller); returns the surviving root.
-__device__ __forceinline__ int uf_link(int32_t* parent, int ra, int rb) {
-  while (ra != rb) {
-    const int lo = ra < rb ? ra : rb;
-    const int hi = ra < rb ? rb : ra;
-    const int ret = atomicCAS(parent + hi, hi, lo);
-    if (ret == hi) return lo;
-    if (ra == hi) ra = ret; else rb = ret;  // hi was hooked meanwhile: climb
-  }
-  return ra;
-}
-
-__device__ __forceinline__ void uf_union(int32_t* parent, int a, int b) {
-  uf_link(parent, uf_find(parent, a), uf_find(parent, b));
-}
-
 // Edge predicate of build_adjacency (segmentation.cpp:124-125), evaluated in
 // the reference's arithmetic: squaredNorm of the mean difference, normal dot.
 __device__ __forceinline__ bool adjacent(const SegBufs& b, const SegDev& sp, d3 mi, d3 ni, int j) {
@@ -429,7 +395,7 @@ __global__ void k_ccl_flatten(Counters* ctr, SegBufs b, MapDesc m) {
 __global__ void k_cluster_flags(Counters* ctr, SegDev sp, SegBufs b) {
   const uint32_t S = min(ctr->S, b.Scap);
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < S; i += gridDim.x * blockDim.x)
-    b.big_flag[i] = (b.label[i] == static_cast<int32_t>(i) &&
+    b.big_flag[i] = (b.label[i] == static_cast<int32_t>(i) && b.cnt[i] > 0u &&
                      static_cast<long long>(b.cnt[i]) >= static_cast<long long>(sp.min_cluster))
                         ? 1
                         : 0;

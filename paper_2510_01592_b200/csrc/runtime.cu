@@ -314,6 +314,53 @@ struct Seg {
   uint64_t gen = 0;  // bumped on reallocation (invalidates captured graphs)
 };
 
+// Per-frame layout and buffers of a slab's distributed segmentation.
+struct SlabSeg {
+  // layout (vp_slab_extend)
+  int n = 0, me = -1;              // slabs, this slab's index
+  std::vector<int32_t> xb;         // x_begin of every slab + window x extent
+  std::vector<uint64_t> P;         // global plane prefix (gex + 1)
+  int w = 1;
+  int32_t x_lo = 0, x_hi = 0;      // extended list planes
+  uint64_t n_left = 0, n_own = 0, n_ext = 0, zone_size = 0;
+  int64_t base = 0, own_base = 0;
+  ZoneDesc zone{};
+  RankDesc rd{};
+  bool labelled = false, merged = false;
+  // buffers
+  uint64_t xcap = 0;
+  int32_t* xidx = nullptr;
+  double* xmean = nullptr;
+  double* xnrm = nullptr;
+  int32_t* bmin = nullptr;
+  int32_t* flabel = nullptr;
+  uint64_t tcap = 0;
+  int32_t* triples = nullptr;
+  uint32_t* ntrip = nullptr;       // device counter
+  uint64_t zcap = 0;
+  int32_t* zparent = nullptr;
+  int32_t* zminlab = nullptr;
+  uint32_t* pcounts = nullptr;     // per owned plane
+  int32_t pcap = 0;
+  uint64_t hcap = 0;
+  uint32_t* H = nullptr;
+  uint32_t* dcount = nullptr;      // kMaxSlabs
+  uint64_t ecap = 0;
+  MemberRec* exp = nullptr;
+  // dense ordinal map over the extended planes
+  int32_t* xmap = nullptr;
+  uint32_t* xbits = nullptr;
+  uint64_t xmap_slots = 0, xmap_words = 0;
+
+  void release() {
+    void* ptrs[] = {xidx, xmean, xnrm, bmin, flabel, triples, ntrip, zparent, zminlab, pcounts, H,
+                    dcount, exp, xmap, xbits};
+    for (void* q : ptrs)
+      if (q) cudaFree(q);
+    *this = SlabSeg{};
+  }
+};
+
 // Host image of the per-fit records written by k_polygon.
 struct HostPolys {
   std::vector<vp_polygon> polys;
@@ -364,6 +411,8 @@ struct vp_grid {
   // window-sized ordinal map for segmenting a gathered slab steppable list
   int32_t* gmap = nullptr;
   uint32_t* gbits = nullptr;
+  // distributed segmentation of a slab (vp_slab_extend .. vp_slab_segment_owned)
+  SlabSeg sl;
   // CUDA graph of one pipeline frame (see pipeline_enqueue)
   bool capturing = false;
   uint64_t gen = 1;  // bumped whenever a buffer the graph references is reallocated
@@ -378,6 +427,7 @@ struct vp_grid {
     if (gd.stbits) cudaFree(gd.stbits);
     if (gmap) cudaFree(gmap);
     if (gbits) cudaFree(gbits);
+    sl.release();
     if (mstream) cudaStreamSynchronize(mstream);
     for (int q = 0; q < 2; ++q) {
       if (ctr_s[q]) cudaFree(ctr_s[q]);
@@ -674,19 +724,22 @@ struct vp_grid {
     LAUNCH(k_step_emit, kWide, kThreads, 0, stream, gd, ctr, seg.b, m, xadd);
   }
   // union-find over the steppable list in seg.b (ctr->S set)
-  void launch_ccl(const SegDev& sd, const MapDesc& m) {
+  void launch_ccl(const SegDev& sd, const MapDesc& m) { launch_ccl(sd, m, seg.b); }
+  void launch_ccl(const SegDev& sd, const MapDesc& m, const SegBufs& sb) {
     // ECL-style atomic-free pre-hooking + compression: most unions then end at
     // the one-load parent check (C2: union pass 400 us -> 80 us)
-    LAUNCH(k_ccl_hook, kWide, kThreads, 0, stream, ctr, sd, seg.b, m);
-    LAUNCH(k_ccl_compress, kWide, kThreads, 0, stream, ctr, seg.b);
-    LAUNCH(k_ccl_union, kWide, kThreads, 0, stream, ctr, sd, seg.b, m);
-    LAUNCH(k_ccl_flatten, kWide, kThreads, 0, stream, ctr, seg.b, m);
+    LAUNCH(k_ccl_hook, kWide, kThreads, 0, stream, ctr, sd, sb, m);
+    LAUNCH(k_ccl_compress, kWide, kThreads, 0, stream, ctr, sb);
+    LAUNCH(k_ccl_union, kWide, kThreads, 0, stream, ctr, sd, sb, m);
+    LAUNCH(k_ccl_flatten, kWide, kThreads, 0, stream, ctr, sb, m);
   }
-  void launch_clusters(const SegDev& sd) {
+  // label_base: global ordinal of list entry 0 (slab owners), else 0
+  void launch_clusters(const SegDev& sd, int64_t label_base = 0) {
     LAUNCH(k_cluster_flags, kWide, kThreads, 0, stream, ctr, sd, seg.b);
     launch_flag_scan(seg.b.big_flag, &ctr->S, seg.b.Scap, seg.b.big_pos, &ctr->K);
     LAUNCH(k_cluster_assign, kWide, kThreads, 0, stream, ctr, seg.b);
     LAUNCH(k_cluster_setup, 1, 1024, 0, stream, ctr, seg.b);
+    if (label_base) LAUNCH(k_klabel_rebase, 8, 256, 0, stream, ctr, seg.b, label_base);
     const int nch = static_cast<int>(seg.hstride);
     LAUNCH(k_member_hist, std::min(nch, 148 * 16), 32, 0, stream, ctr, seg.b, seg.hstride);
     LAUNCH(k_member_hscan, kWide, kThreads, 0, stream, ctr, seg.b, seg.hstride);
@@ -1985,6 +2038,294 @@ int vp_segment_steppable(vp_grid* g, const vp_pipeline_params* p, uint64_t S, co
         fail(VP_ENOMEM, "more than 2048 clusters >= min_cluster_size in one frame");
       g->seg.ensure(g->seg.b.Vcap, g->seg.b.Scap, 2 * g->seg.b.Icap, p->ransac.iterations, g->gd.nwords);
     }
+    if (out) {
+      HostPolys hp;
+      g->download_polygons(hp, false);
+      *out = make_polygons_out(hp);
+    }
+  });
+}
+
+static_assert(sizeof(vp_member_rec) == sizeof(MemberRec), "vp_member_rec must match MemberRec");
+
+int vp_adjacency_window(const vp_seg_params* p, double resolution, int32_t* w) {
+  return guard([&] {
+    // segmentation.cpp:89
+    *w = std::max(1, static_cast<int>(std::ceil(p->distance_th / resolution)));
+  });
+}
+
+int vp_slab_plane_counts(vp_grid* g, uint32_t** counts, int32_t* n_planes) {
+  return guard([&] {
+    SlabSeg& L = g->sl;
+    const int32_t np = g->gd.own_hi - g->gd.own_lo;
+    if (np > L.pcap) {
+      dfree(L.pcounts);
+      L.pcounts = dalloc<uint32_t>(np);
+      L.pcap = np;
+    }
+    LAUNCH(k_plane_counts, grid_for(np), kThreads, 0, g->stream, g->ctr, g->seg.b.st_idx, g->seg.b.Scap,
+           g->gd.xoff + g->gd.own_lo, np, L.pcounts);
+    ck(cudaStreamSynchronize(g->stream), "sync");
+    *counts = L.pcounts;
+    *n_planes = np;
+  });
+}
+
+int vp_slab_extend(vp_grid* g, const vp_seg_params* p, const vp_slab_layout* lay, int32_t** idx,
+                   double** mean, double** normal, uint64_t* n_ext, int32_t* x_lo, int32_t* x_hi) {
+  return guard([&] {
+    SlabSeg& L = g->sl;
+    const int n = lay->n_slabs;
+    if (n < 1 || n > kMaxSlabs) fail(VP_EINVAL, "slab layout: 1..64 slabs");
+    const int32_t gex = g->gd.gex;
+    if (lay->x_begin[0] != 0 || lay->x_begin[n] != gex) fail(VP_EINVAL, "slab layout: x ranges must tile the window");
+    L.n = n;
+    L.xb.assign(lay->x_begin, lay->x_begin + n + 1);
+    const int32_t my_xb = g->gd.xoff + g->gd.own_lo, my_xe = g->gd.xoff + g->gd.own_hi;
+    L.me = -1;
+    for (int k = 0; k < n; ++k) {
+      if (L.xb[k] >= L.xb[k + 1]) fail(VP_EINVAL, "slab layout: empty or unordered x range");
+      if (L.xb[k] == my_xb && L.xb[k + 1] == my_xe) L.me = k;
+    }
+    if (L.me < 0) fail(VP_EINVAL, "slab layout: this slab's x range is not in the layout");
+    L.P.assign(gex + 1, 0);
+    for (int32_t x = 0; x < gex; ++x) L.P[x + 1] = L.P[x] + lay->plane_counts[x];
+    if (L.P[gex] >= (1ull << 31)) fail(VP_ENOMEM, "more than 2^31 steppable voxels in the window");
+    L.w = std::max(1, static_cast<int>(std::ceil(p->distance_th / g->gd.res)));  // segmentation.cpp:89
+    L.x_lo = std::max(0, my_xb - L.w);
+    L.x_hi = std::min(gex, my_xe + L.w);
+    L.base = static_cast<int64_t>(L.P[L.x_lo]);
+    L.own_base = static_cast<int64_t>(L.P[my_xb]);
+    L.n_left = L.P[my_xb] - L.P[L.x_lo];
+    L.n_own = L.P[my_xe] - L.P[my_xb];
+    L.n_ext = L.P[L.x_hi] - L.P[L.x_lo];
+    if (L.n_own != g->h_ctr->S) fail(VP_EINVAL, "slab layout: plane counts disagree with this slab's steppable list");
+    // boundary zone: [B - w, B + w) around every internal boundary, merged
+    L.zone = ZoneDesc{};
+    L.zone_size = 0;
+    for (int k = 1; k < n; ++k) {
+      const int32_t a = std::max(0, L.xb[k] - L.w), b = std::min(gex, L.xb[k] + L.w);
+      ZoneDesc& z = L.zone;
+      if (z.n && a <= z.xhi[z.n - 1]) {
+        z.xhi[z.n - 1] = std::max(z.xhi[z.n - 1], b);
+      } else {
+        z.xlo[z.n] = a;
+        z.xhi[z.n] = b;
+        ++z.n;
+      }
+    }
+    for (int k = 0; k < L.zone.n; ++k) {
+      L.zone.olo[k] = static_cast<int64_t>(L.P[L.zone.xlo[k]]);
+      L.zone.dbase[k] = static_cast<int64_t>(L.zone_size);
+      L.zone_size += L.P[L.zone.xhi[k]] - L.P[L.zone.xlo[k]];
+    }
+    L.rd = RankDesc{};
+    L.rd.n = n;
+    for (int k = 0; k < n; ++k) L.rd.ord_lo[k] = static_cast<int64_t>(L.P[L.xb[k]]);
+    // extended list buffers; the own list moves in before any seg realloc
+    if (L.n_ext > L.xcap) {
+      const uint64_t cap = std::max<uint64_t>(L.n_ext + L.n_ext / 4, 1 << 16);
+      for (void* q : {(void*)L.xidx, (void*)L.xmean, (void*)L.xnrm, (void*)L.bmin, (void*)L.flabel})
+        if (q) cudaFree(q);
+      L.xidx = dalloc<int32_t>(3 * cap);
+      L.xmean = dalloc<double>(3 * cap);
+      L.xnrm = dalloc<double>(3 * cap);
+      L.bmin = dalloc<int32_t>(cap);
+      L.flabel = dalloc<int32_t>(cap);
+      L.xcap = cap;
+    }
+    if (L.n_own) {
+      ck(cudaMemcpyAsync(L.xidx + 3 * L.n_left, g->seg.b.st_idx, 12 * L.n_own, cudaMemcpyDeviceToDevice, g->stream), "ext idx");
+      ck(cudaMemcpyAsync(L.xmean + 3 * L.n_left, g->seg.b.st_mean, 24 * L.n_own, cudaMemcpyDeviceToDevice, g->stream), "ext mean");
+      ck(cudaMemcpyAsync(L.xnrm + 3 * L.n_left, g->seg.b.st_normal, 24 * L.n_own, cudaMemcpyDeviceToDevice, g->stream), "ext nrm");
+    }
+    ck(cudaStreamSynchronize(g->stream), "sync");
+    const uint32_t need = static_cast<uint32_t>(L.n_ext);
+    if (need > g->seg.b.Scap)
+      g->seg.ensure(g->seg.b.Vcap, need, std::max(g->seg.b.Icap, need), 100, g->gd.nwords);
+    // dense ordinal map over the extended planes
+    const uint64_t slots = static_cast<uint64_t>(L.x_hi - L.x_lo) * g->gd.ey * g->gd.ez;
+    const uint64_t words = static_cast<uint64_t>(L.x_hi - L.x_lo) * g->gd.ey * g->gd.W;
+    if (slots > L.xmap_slots) {
+      dfree(L.xmap);
+      dfree(L.xbits);
+      L.xmap = dalloc<int32_t>(slots);
+      L.xbits = dalloc<uint32_t>(words);
+      ck(cudaMemsetAsync(L.xmap, 0xff, slots * 4, g->stream), "xmap");
+      ck(cudaMemsetAsync(L.xbits, 0, words * 4, g->stream), "xbits");
+      ck(cudaStreamSynchronize(g->stream), "sync");
+      L.xmap_slots = slots;
+      L.xmap_words = words;
+    }
+    L.labelled = L.merged = false;
+    *idx = L.xidx;
+    *mean = L.xmean;
+    *normal = L.xnrm;
+    *n_ext = L.n_ext;
+    *x_lo = L.x_lo;
+    *x_hi = L.x_hi;
+  });
+}
+
+int vp_slab_label(vp_grid* g, const vp_seg_params* p, int32_t** triples, uint64_t* n_triples,
+                  uint64_t* zone_size) {
+  return guard([&] {
+    SlabSeg& L = g->sl;
+    if (L.me < 0) fail(VP_EINVAL, "slab_label: call vp_slab_extend first");
+    const SegDev sd = make_segdev(*p, g->gd.res);
+    SegBufs sb = g->seg.b;
+    sb.st_idx = L.xidx;
+    sb.st_mean = L.xmean;
+    sb.st_normal = L.xnrm;
+    sb.Scap = static_cast<uint32_t>(std::min<uint64_t>(L.xcap, g->seg.b.Scap));
+    MapDesc m{};
+    m.map = L.xmap;
+    m.bits = L.xbits;
+    m.lo[0] = L.x_lo;
+    m.lo[1] = m.lo[2] = 0;
+    m.dims[0] = L.x_hi - L.x_lo;
+    m.dims[1] = g->gd.ey;
+    m.dims[2] = g->gd.ez;
+    m.W = g->gd.W;
+    // count of zone entries bounds the triples
+    uint64_t zent = 0;
+    for (int k = 0; k < L.zone.n; ++k) {
+      const int32_t a = std::max(L.zone.xlo[k], L.x_lo), b = std::min(L.zone.xhi[k], L.x_hi);
+      if (a < b) zent += L.P[b] - L.P[a];
+    }
+    if (zent > L.tcap || !L.triples) {
+      dfree(L.triples);
+      L.tcap = std::max<uint64_t>(zent + zent / 4, 1 << 12);
+      L.triples = dalloc<int32_t>(3 * L.tcap);
+      if (!L.ntrip) L.ntrip = dalloc<uint32_t>(1);
+    }
+    g->reset_frame_counters();
+    set_counter_u32(g, offsetof(Counters, S), static_cast<uint32_t>(L.n_ext));
+    if (L.n_ext) {
+      LAUNCH(k_map_fill, kWide, kThreads, 0, g->stream, g->ctr, sb, m);
+      g->launch_ccl(sd, m, sb);
+      LAUNCH(k_fill_i32, grid_for(L.n_ext), kThreads, 0, g->stream, L.bmin, L.n_ext, 0x7fffffff);
+    }
+    ck(cudaMemsetAsync(L.ntrip, 0, 4, g->stream), "ntrip");
+    if (L.n_ext && L.zone.n) {
+      LAUNCH(k_zone_bmin, kWide, kThreads, 0, g->stream, g->ctr, sb, L.zone, L.bmin);
+      LAUNCH(k_zone_triples, kWide, kThreads, 0, g->stream, g->ctr, sb, L.zone, L.base, L.bmin, L.triples,
+             L.ntrip);
+    }
+    uint32_t nt = 0;
+    ck(cudaMemcpyAsync(&nt, L.ntrip, 4, cudaMemcpyDeviceToHost, g->stream), "ntrip");
+    ck(cudaStreamSynchronize(g->stream), "sync");
+    if (nt != zent) fail(VP_ECUDA, "slab_label: zone entry count mismatch");
+    L.labelled = true;
+    *triples = L.triples;
+    *n_triples = nt;
+    *zone_size = L.zone_size;
+  });
+}
+
+int vp_slab_merge(vp_grid* g, const int32_t* triples, uint64_t n_triples, int32_t** labels) {
+  return guard([&] {
+    SlabSeg& L = g->sl;
+    if (!L.labelled) fail(VP_EINVAL, "slab_merge: call vp_slab_label first");
+    if (L.zone_size > L.zcap || !L.zparent) {
+      dfree(L.zparent);
+      dfree(L.zminlab);
+      L.zcap = std::max<uint64_t>(L.zone_size + L.zone_size / 4, 1 << 12);
+      L.zparent = dalloc<int32_t>(L.zcap);
+      L.zminlab = dalloc<int32_t>(L.zcap);
+    }
+    if (L.zone_size) {
+      LAUNCH(k_zone_init, grid_for(L.zone_size), kThreads, 0, g->stream, L.zparent, L.zminlab, L.zone_size);
+      if (n_triples) {
+        LAUNCH(k_zone_union, grid_for(n_triples), kThreads, 0, g->stream, triples, n_triples, L.zparent);
+        LAUNCH(k_zone_minlab, grid_for(n_triples), kThreads, 0, g->stream, triples, n_triples, L.zparent,
+               L.zminlab);
+      }
+    }
+    SegBufs sb = g->seg.b;
+    sb.st_idx = L.xidx;
+    if (L.n_own)
+      LAUNCH(k_slab_relabel, grid_for(L.n_own), kThreads, 0, g->stream, sb, L.zone, L.base,
+             static_cast<uint32_t>(L.n_left), static_cast<uint32_t>(L.n_own), L.bmin, L.zparent, L.zminlab,
+             L.flabel);
+    ck(cudaStreamSynchronize(g->stream), "sync");
+    L.merged = true;
+    *labels = L.flabel;
+  });
+}
+
+int vp_slab_export(vp_grid* g, uint64_t* dest_counts, void** records) {
+  return guard([&] {
+    SlabSeg& L = g->sl;
+    if (!L.merged) fail(VP_EINVAL, "slab_export: call vp_slab_merge first");
+    const uint32_t n_own = static_cast<uint32_t>(L.n_own);
+    const uint32_t nch = std::max<uint32_t>(1, (n_own + kChunk - 1) / kChunk);
+    const uint64_t hn = static_cast<uint64_t>(L.n) * nch;
+    if (hn > L.hcap || !L.H) {
+      dfree(L.H);
+      L.hcap = std::max<uint64_t>(hn + hn / 4, 1 << 12);
+      L.H = dalloc<uint32_t>(L.hcap);
+      if (!L.dcount) L.dcount = dalloc<uint32_t>(kMaxSlabs);
+    }
+    ck(cudaMemsetAsync(L.dcount, 0, 4 * kMaxSlabs, g->stream), "dcount");
+    ck(cudaMemsetAsync(L.H, 0, 4 * hn, g->stream), "H");
+    const int blocks = static_cast<int>(std::min<uint32_t>(nch, 148 * 16));
+    if (n_own)
+      LAUNCH(k_export_hist, blocks, 32, 0, g->stream, n_own, L.flabel, L.rd, L.me, L.H, nch, L.dcount);
+    uint32_t dc[kMaxSlabs];
+    ck(cudaMemcpyAsync(dc, L.dcount, 4 * kMaxSlabs, cudaMemcpyDeviceToHost, g->stream), "dcount");
+    ck(cudaStreamSynchronize(g->stream), "sync");
+    uint64_t tot = 0;
+    for (int k = 0; k < L.n; ++k) {
+      dest_counts[k] = dc[k];
+      tot += dc[k];
+    }
+    if (tot > L.ecap || !L.exp) {
+      dfree(L.exp);
+      L.ecap = std::max<uint64_t>(tot + tot / 4, 1 << 12);
+      L.exp = dalloc<MemberRec>(L.ecap);
+    }
+    if (tot) {
+      if (hn > 0xffffffffull) fail(VP_ENOMEM, "slab_export: histogram too large");
+      LAUNCH(k_scan_exclusive, 1, 1024, 0, g->stream, L.H, static_cast<uint32_t>(hn), nullptr, nullptr, nullptr);
+      LAUNCH(k_export_scatter, blocks, 32, 0, g->stream, n_own, L.flabel, L.xmean + 3 * L.n_left, L.rd, L.me,
+             L.H, nch, L.exp);
+    }
+    ck(cudaStreamSynchronize(g->stream), "sync");
+    *records = L.exp;
+  });
+}
+
+int vp_slab_segment_owned(vp_grid* g, const vp_pipeline_params* p, const void* recv, uint64_t n_recv,
+                          vp_polygons_t** out) {
+  if (out) *out = nullptr;
+  return guard([&] {
+    SlabSeg& L = g->sl;
+    if (!L.merged) fail(VP_EINVAL, "slab_segment_owned: call vp_slab_merge first");
+    const uint32_t n = static_cast<uint32_t>(L.n_own + n_recv);
+    const SegDev sd = make_segdev(p->seg, g->gd.res);
+    const RansacDev rd = make_ransacdev(p->ransac);
+    g->seg.ensure(g->seg.b.Vcap, std::max(n, g->seg.b.Scap), std::max(n, g->seg.b.Icap), p->ransac.iterations,
+                  g->gd.nwords);
+    g->seg.ensure_dirs(16, g->stream);
+    for (int tries = 0;; ++tries) {
+      g->reset_frame_counters();
+      set_counter_u32(g, offsetof(Counters, S), n);
+      if (n) {
+        LAUNCH(k_owner_init, grid_for(n), kThreads, 0, g->stream, n, g->seg.b);
+        LAUNCH(k_owner_prep, grid_for(n), kThreads, 0, g->stream, static_cast<uint32_t>(L.n_own),
+               static_cast<uint32_t>(n_recv), L.own_base, L.xmean + 3 * L.n_left, L.flabel,
+               static_cast<const MemberRec*>(recv), g->seg.b);
+      }
+      g->launch_clusters(sd, L.own_base);  // cluster labels = global ordinals
+      g->launch_ransac(rd);
+      g->launch_refine(p->ransac.up, p->refine, p->refine_exact);
+      g->launch_polygon(16, p->min_polygon_area);
+      g->read_counters();
+      if (tries > 4 || !g->grow_if_overflow(p->ransac.iterations)) break;
+    }
+    if (g->h_ctr->overflow) fail(VP_ENOMEM, "segmentation capacity overflow persists");
     if (out) {
       HostPolys hp;
       g->download_polygons(hp, false);

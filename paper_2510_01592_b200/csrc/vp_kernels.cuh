@@ -64,6 +64,41 @@ __device__ __forceinline__ uint32_t block_sum_u32(uint32_t v) {
   return r;
 }
 
+// Union-find over int32 parent arrays (CCL and the slab boundary merge).
+// Parent pointers only ever move to an ancestor (hooks: root -> smaller root;
+// pointer jumping: node -> grandparent), so every value a thread can observe
+// is an ancestor of the node. Reads go through L2 (ld.cg): a stale value is
+// still an ancestor, so "same root" answers are always right and a wrong
+// "different roots" answer is corrected by the atomicCAS retry.
+__device__ __forceinline__ int uf_find(int32_t* parent, int v) {
+  int par = __ldcg(parent + v);
+  if (par != v) {
+    int next, prev = v;
+    while (par > (next = __ldcg(parent + par))) {
+      __stcg(parent + prev, next);  // pointer jumping; parent[x] <= x always holds
+      prev = par;
+      par = next;
+    }
+  }
+  return par;
+}
+
+// Link two roots (larger under smaller); returns the surviving root.
+__device__ __forceinline__ int uf_link(int32_t* parent, int ra, int rb) {
+  while (ra != rb) {
+    const int lo = ra < rb ? ra : rb;
+    const int hi = ra < rb ? rb : ra;
+    const int ret = atomicCAS(parent + hi, hi, lo);
+    if (ret == hi) return lo;
+    if (ra == hi) ra = ret; else rb = ret;  // hi was hooked meanwhile: climb
+  }
+  return ra;
+}
+
+__device__ __forceinline__ void uf_union(int32_t* parent, int a, int b) {
+  uf_link(parent, uf_find(parent, a), uf_find(parent, b));
+}
+
 // Segmentation parameters resolved on the host (thresholds computed with the
 // host libm exactly as the reference computes them).
 struct SegDev {
@@ -176,6 +211,30 @@ struct SegBufs {
   uint32_t Vcap, Scap, Mcap, Icap;
 };
 
+// ---- spatial slabs (k_slab.cu)
+constexpr int kMaxSlabs = 64;
+
+// Boundary zone: window x intervals [xlo, xhi) within w of an internal slab
+// boundary; zone index of ordinal o in interval k = dbase[k] + (o - olo[k]).
+struct ZoneDesc {
+  int n;
+  int32_t xlo[kMaxSlabs], xhi[kMaxSlabs];
+  int64_t olo[kMaxSlabs], dbase[kMaxSlabs];
+};
+
+// First global ordinal of every slab (slab k owns [ord_lo[k], ord_lo[k+1])).
+struct RankDesc {
+  int n;
+  int64_t ord_lo[kMaxSlabs];
+};
+
+// A cluster member sent to the slab that owns its cluster (32 B).
+struct MemberRec {
+  double m[3];
+  int32_t label;
+  int32_t pad;
+};
+
 // ---- kernels (k_map.cu)
 __global__ void k_integrate_hash(GridDesc g, const FrameParams* fp, Counters* ctr, uint32_t* hkey,
                                  uint32_t* hcnt, uint32_t hmask, uint32_t* groups, uint32_t* pslot,
@@ -237,5 +296,26 @@ __global__ void k_poly_extremes(Counters* ctr, SegBufs b, const double* dirtab, 
 __global__ void k_poly_inner(Counters* ctr, SegBufs b, int directions);
 __global__ void k_poly_keep(Counters* ctr, SegBufs b);
 __global__ void k_poly_hull(Counters* ctr, SegBufs b, double min_area);
+
+// ---- kernels (k_slab.cu)
+__global__ void k_plane_counts(const Counters* ctr, const int32_t* st_idx, uint32_t cap, int32_t x0,
+                               int32_t nplanes, uint32_t* counts);
+__global__ void k_fill_i32(int32_t* a, uint64_t n, int32_t v);
+__global__ void k_zone_bmin(const Counters* ctr, SegBufs b, ZoneDesc z, int32_t* bmin);
+__global__ void k_zone_triples(const Counters* ctr, SegBufs b, ZoneDesc z, int64_t base,
+                               const int32_t* bmin, int32_t* out, uint32_t* nout);
+__global__ void k_zone_init(int32_t* parent, int32_t* minlab, uint64_t Z);
+__global__ void k_zone_union(const int32_t* t, uint64_t n, int32_t* parent);
+__global__ void k_zone_minlab(const int32_t* t, uint64_t n, int32_t* parent, int32_t* minlab);
+__global__ void k_slab_relabel(SegBufs b, ZoneDesc z, int64_t base, uint32_t n_left, uint32_t n_own,
+                               const int32_t* bmin, int32_t* parent, const int32_t* minlab, int32_t* flabel);
+__global__ void k_export_hist(uint32_t n_own, const int32_t* flabel, RankDesc rd, int me, uint32_t* H,
+                              uint32_t nch, uint32_t* dcount);
+__global__ void k_export_scatter(uint32_t n_own, const int32_t* flabel, const double* mean, RankDesc rd,
+                                 int me, const uint32_t* H, uint32_t nch, MemberRec* out);
+__global__ void k_owner_init(uint32_t n, SegBufs b);
+__global__ void k_owner_prep(uint32_t n_own, uint32_t n_recv, int64_t own_base, const double* own_mean,
+                             const int32_t* flabel, const MemberRec* recv, SegBufs b);
+__global__ void k_klabel_rebase(const Counters* ctr, SegBufs b, int64_t base);
 
 }  // namespace vp

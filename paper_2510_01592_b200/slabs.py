@@ -11,14 +11,26 @@ flat index, voxel_grid.hpp:43-46), one slab per rank. Per frame:
    bits) is sent onto the halo planes of its neighbours (the 1-cell window of
    estimate_normals, segmentation.cpp:36-51);
 4. estimate_normals + classify_steppable on owned voxels (library);
-5. the steppable lists are gathered to rank 0 in slab order -- ordinals are
-   x-major, so the concatenation IS the single-grid list -- and rank 0 runs
-   build_adjacency .. make_polygon (vp_segment_steppable).
+5. per-plane steppable counts are all-gathered: ordinals are x-major, so every
+   slab owns a contiguous global ordinal range and every plane's first ordinal
+   is known everywhere (SlabLayout);
+6. each slab receives the steppable voxels of the w planes either side of it
+   (w = adjacency window, segmentation.cpp:89) and runs build_adjacency +
+   label_components locally (library, vp_slab_label);
+7. boundary-label merge: the slabs' boundary triples are all-gathered and a
+   union-find over the boundary zone (replicated, on device) gives every
+   owned voxel its canonical label = the component's minimum global ordinal
+   (vp_slab_merge) -- the single-grid label, bit-exact;
+8. cluster gather: members of clusters whose label lies in a lower slab are
+   sent to that owner (vp_slab_export); each owner runs filter_clusters ..
+   make_polygon on its clusters, members in global ordinal order
+   (vp_slab_segment_owned);
+9. polygons are gathered to rank 0 in slab order (= ascending label order).
 
-The same phase functions drive N virtual slabs in one process (LocalComm,
-exchange = device copies; used by the single-GPU parity tests) or one slab
-per rank under torch.distributed (DistComm: NCCL send/recv of the halo
-planes, gather of the steppable lists).
+The same phase functions drive N virtual slabs in one process (LocalComm:
+exchanges are device copies; used by the single-GPU parity tests) or one slab
+per rank under torch.distributed (DistComm: NCCL broadcast / all-gather /
+send-recv on B200s, gloo in the CPU tests).
 """
 from __future__ import annotations
 
@@ -28,6 +40,8 @@ import numpy as np
 
 from . import native
 from .native import _p, _pose, check, lib, polygons_to_py
+
+MEMBER_REC_BYTES = 32  # vp_member_rec
 
 
 class DeviceBuffer:
@@ -43,6 +57,17 @@ class DeviceBuffer:
         return torch.as_tensor(self, device=f"cuda:{self.device}")
 
 
+def _dev_bytes(ptr, nbytes, device):
+    import torch
+    if nbytes == 0 or not ptr:
+        return torch.empty(0, dtype=torch.uint8, device=f"cuda:{device}")
+    return DeviceBuffer(ptr, nbytes, device).tensor()
+
+
+def _addr(p):
+    return C.cast(p, C.c_void_p).value or 0
+
+
 def split_x(extent_x: int, world: int):
     """Balanced contiguous x ranges [(x_begin, x_end)] for `world` slabs."""
     base, rem = divmod(extent_x, world)
@@ -54,6 +79,79 @@ def split_x(extent_x: int, world: int):
     return out
 
 
+def adjacency_window(seg: native.SegParams, res: float) -> int:
+    """w = max(1, ceil(distance_th / resolution)) (segmentation.cpp:89), from the library."""
+    w = C.c_int32()
+    check(lib().vp_adjacency_window(C.byref(seg), C.c_double(res), C.byref(w)))
+    return w.value
+
+
+class SlabLayout:
+    """One frame's global view of the slabs (host arithmetic only; mirrors
+    vp_slab_extend): P[x] = global ordinal of the first steppable voxel of
+    window plane x, slab k owns ordinals [P[xb_k], P[xb_{k+1})), its extended
+    list covers planes [max(0, xb_k - w), min(gex, xb_{k+1} + w))."""
+
+    def __init__(self, ranges, plane_counts, w: int):
+        self.ranges = [tuple(int(v) for v in r) for r in ranges]
+        self.n = len(self.ranges)
+        self.gex = self.ranges[-1][1]
+        counts = np.asarray(plane_counts, np.int64)
+        assert counts.shape == (self.gex,)
+        self.P = np.zeros(self.gex + 1, np.int64)
+        np.cumsum(counts, out=self.P[1:])
+        self.w = int(w)
+        self.x_begin = np.asarray([a for a, _ in self.ranges] + [self.gex], np.int32)
+        self.counts_u32 = np.ascontiguousarray(counts, np.uint32)
+
+    def ext(self, k):
+        a, b = self.ranges[k]
+        return max(0, a - self.w), min(self.gex, b + self.w)
+
+    def n_own(self, k):
+        a, b = self.ranges[k]
+        return int(self.P[b] - self.P[a])
+
+    def n_left(self, k):
+        lo, _ = self.ext(k)
+        return int(self.P[self.ranges[k][0]] - self.P[lo])
+
+    def n_ext(self, k):
+        lo, hi = self.ext(k)
+        return int(self.P[hi] - self.P[lo])
+
+    def transfers(self):
+        """Halo lists: (src, dst, src_start, count, dst_start) -- entries of
+        slab src's own list [src_start, +count) land at [dst_start, +count) of
+        slab dst's extended list. Same list on every rank."""
+        out = []
+        for d in range(self.n):
+            lo, hi = self.ext(d)
+            for s in range(self.n):
+                if s == d:
+                    continue
+                a, b = self.ranges[s]
+                x0, x1 = max(lo, a), min(hi, b)
+                if x0 >= x1:
+                    continue
+                cnt = int(self.P[x1] - self.P[x0])
+                if cnt:
+                    out.append((s, d, int(self.P[x0] - self.P[a]), cnt, int(self.P[x0] - self.P[lo])))
+        return out
+
+    def c_struct(self):
+        lay = VpSlabLayout()
+        lay.n_slabs = self.n
+        lay.x_begin = _p(self.x_begin, C.c_int32)
+        lay.plane_counts = _p(self.counts_u32, C.c_uint32)
+        return lay
+
+
+class VpSlabLayout(C.Structure):
+    _fields_ = [("n_slabs", C.c_int32), ("x_begin", C.POINTER(C.c_int32)),
+                ("plane_counts", C.POINTER(C.c_uint32))]
+
+
 class Slab:
     """One slab grid (vp_slab_create) owning window x in [x_begin, x_end)."""
 
@@ -61,6 +159,7 @@ class Slab:
         ext = np.asarray(window_extent, np.int32)
         c = np.asarray(center, np.float64)
         self.h = C.c_void_p()
+        self.res = res
         self.x_begin, self.x_end, self.device = x_begin, x_end, device
         self.window_extent = tuple(int(v) for v in window_extent)
         check(lib().vp_slab_create(C.c_double(res), _p(ext, C.c_int32), _p(c, C.c_double),
@@ -82,17 +181,75 @@ class Slab:
         return (cs.voxels_cleared, cs.voxels_freed), (us.voxels_touched, us.points_discarded)
 
     def steppable(self, seg: native.SegParams):
+        """estimate_normals + classify_steppable on the owned voxels: (S, (idx, mean, normal) byte views)."""
         n = C.c_uint64()
         idx, mean, nrm = C.POINTER(C.c_int32)(), C.POINTER(C.c_double)(), C.POINTER(C.c_double)()
         check(lib().vp_slab_steppable(self.h, C.byref(seg), C.byref(n), C.byref(idx), C.byref(mean),
                                       C.byref(nrm)))
         S = n.value
-        addr = lambda p: C.cast(p, C.c_void_p).value or 0  # noqa: E731
-        return S, (DeviceBuffer(addr(idx), 12 * S, self.device).tensor(),
-                   DeviceBuffer(addr(mean), 24 * S, self.device).tensor(),
-                   DeviceBuffer(addr(nrm), 24 * S, self.device).tensor())
+        return S, (_dev_bytes(_addr(idx), 12 * S, self.device), _dev_bytes(_addr(mean), 24 * S, self.device),
+                   _dev_bytes(_addr(nrm), 24 * S, self.device))
 
-    def segment(self, params: native.PipelineParams, S, idx_t, mean_t, nrm_t):
+    def plane_counts(self):
+        """Steppable voxels per owned plane (device uint32 view)."""
+        import torch
+        ptr = C.POINTER(C.c_uint32)()
+        n = C.c_int32()
+        check(lib().vp_slab_plane_counts(self.h, C.byref(ptr), C.byref(n)))
+        return _dev_bytes(_addr(ptr), 4 * n.value, self.device).view(torch.int32)
+
+    def extend(self, seg: native.SegParams, layout: SlabLayout):
+        """Extended list buffers (idx 12 B, mean 24 B, normal 24 B per entry) with the own list in place."""
+        lay = layout.c_struct()
+        idx, mean, nrm = C.POINTER(C.c_int32)(), C.POINTER(C.c_double)(), C.POINTER(C.c_double)()
+        n, lo, hi = C.c_uint64(), C.c_int32(), C.c_int32()
+        check(lib().vp_slab_extend(self.h, C.byref(seg), C.byref(lay), C.byref(idx), C.byref(mean), C.byref(nrm),
+                                   C.byref(n), C.byref(lo), C.byref(hi)))
+        N = n.value
+        k = layout.ranges.index((self.x_begin, self.x_end))
+        self.n_own = layout.n_own(k)
+        self.ext_lists = (_dev_bytes(_addr(idx), 12 * N, self.device), _dev_bytes(_addr(mean), 24 * N, self.device),
+                          _dev_bytes(_addr(nrm), 24 * N, self.device))
+        return self.ext_lists
+
+    def label(self, seg: native.SegParams):
+        """Local CCL on the extended list: (boundary triples as an int32 (n, 3) view, zone size)."""
+        import torch
+        t = C.POINTER(C.c_int32)()
+        n, z = C.c_uint64(), C.c_uint64()
+        check(lib().vp_slab_label(self.h, C.byref(seg), C.byref(t), C.byref(n), C.byref(z)))
+        return _dev_bytes(_addr(t), 12 * n.value, self.device).view(torch.int32).view(-1, 3), z.value
+
+    def merge(self, triples):
+        """Canonical labels (global ordinals) of the owned entries (device int32 view)."""
+        import torch
+        out = C.POINTER(C.c_int32)()
+        n = triples.shape[0] if triples is not None else 0
+        check(lib().vp_slab_merge(self.h, C.c_void_p(triples.data_ptr() if n else 0), C.c_uint64(n),
+                                  C.byref(out)))
+        self._labels = _dev_bytes(_addr(out), 4 * self.n_own, self.device).view(torch.int32)
+        return self._labels
+
+    def merge_labels(self):
+        """The labels of the last vp_slab_merge (device int32 view of the owned entries)."""
+        return self._labels
+
+    def export(self, n_slabs):
+        """Members of clusters owned by lower slabs: (per-destination counts, 32-byte records view)."""
+        counts = np.zeros(n_slabs, np.uint64)
+        rec = C.c_void_p()
+        check(lib().vp_slab_export(self.h, _p(counts, C.c_uint64), C.byref(rec)))
+        tot = int(counts.sum())
+        return counts.astype(np.int64), _dev_bytes(rec.value or 0, MEMBER_REC_BYTES * tot, self.device)
+
+    def segment_owned(self, params: native.PipelineParams, recv, n_recv):
+        out = C.POINTER(native.Polygons)()
+        check(lib().vp_slab_segment_owned(self.h, C.byref(params), C.c_void_p(recv.data_ptr() if n_recv else 0),
+                                          C.c_uint64(n_recv), C.byref(out)))
+        return polygons_to_py(out)
+
+    def segment_gathered(self, params: native.PipelineParams, S, idx_t, mean_t, nrm_t):
+        """Segment a whole steppable list on this grid (vp_segment_steppable)."""
         out = C.POINTER(native.Polygons)()
         check(lib().vp_segment_steppable(self.h, C.byref(params), C.c_uint64(S),
                                          C.c_void_p(idx_t.data_ptr() if S else 0),
@@ -113,11 +270,16 @@ class Slab:
             self.h = None
 
 
+# ------------------------------------------------------------------ comms
 class LocalComm:
     """N virtual slabs in one process: the exchanges are device copies."""
 
     def __init__(self, world):
         self.world = world
+        self.rank = 0
+
+    def slab_index(self, i):
+        return i
 
     def broadcast_frame(self, pts_t):
         return pts_t
@@ -135,14 +297,41 @@ class LocalComm:
                 dst[0].copy_(src[0])
                 dst[1].copy_(src[1])
 
-    def gather_steppable(self, parts):
+    def allgather_plane_counts(self, counts):
         import torch
-        S = sum(p[0] for p in parts)
-        if S == 0:
-            e = torch.empty(0, dtype=torch.uint8, device="cuda")
-            return 0, e, e, e
-        return S, torch.cat([p[1][0] for p in parts]), torch.cat([p[1][1] for p in parts]), \
-            torch.cat([p[1][2] for p in parts])
+        return torch.cat(counts).cpu().numpy() if counts else np.zeros(0, np.int32)
+
+    def exchange_steppable(self, layout, ext_lists):
+        """ext_lists[k] = (idx, mean, normal) byte views of slab k's extended list."""
+        for s, d, s0, cnt, d0 in layout.transfers():
+            ls = layout.n_left(s)
+            for src, dst, w in zip(ext_lists[s], ext_lists[d], (12, 24, 24)):
+                dst[d0 * w:(d0 + cnt) * w].copy_(src[(ls + s0) * w:(ls + s0 + cnt) * w])
+
+    def allgather_triples(self, parts):
+        import torch
+        return torch.cat(parts) if parts else None
+
+    def exchange_members(self, exports):
+        """exports[k] = (dest_counts, records): returns per slab the records
+        received from the higher slabs, in slab order."""
+        import torch
+        out = []
+        n = len(exports)
+        offs = [np.concatenate([[0], np.cumsum(c)]) for c, _ in exports]
+        for d in range(n):
+            parts = []
+            for s in range(d + 1, n):
+                c = int(exports[s][0][d])
+                if c:
+                    o = int(offs[s][d])
+                    parts.append(exports[s][1][o * MEMBER_REC_BYTES:(o + c) * MEMBER_REC_BYTES])
+            recv = torch.cat(parts) if parts else None
+            out.append((recv, sum(p.numel() for p in parts) // MEMBER_REC_BYTES))
+        return out
+
+    def gather_polygons(self, per_slab):
+        return [p for polys in per_slab for p in polys]
 
 
 class DistComm:
@@ -153,6 +342,9 @@ class DistComm:
         self.rank, self.world = dist.get_rank(), dist.get_world_size()
         self.device = device
 
+    def slab_index(self, i):
+        return self.rank
+
     def broadcast_frame(self, pts_t):
         import torch
         n = torch.tensor([pts_t.numel() if self.rank == 0 else 0], dtype=torch.int64, device=pts_t.device)
@@ -161,6 +353,11 @@ class DistComm:
             pts_t = torch.empty(int(n.item()), dtype=pts_t.dtype, device=pts_t.device)
         self.dist.broadcast(pts_t, 0)
         return pts_t
+
+    def _p2p(self, ops):
+        if ops:
+            for req in self.dist.batch_isend_irecv(ops):
+                req.wait()
 
     def halo_exchange(self, slabs):
         (s,) = slabs
@@ -174,40 +371,85 @@ class DistComm:
             mine, halo = s.plane(s.x_end - 1), s.plane(s.x_end)
             ops += [P2P(self.dist.isend, mine[0], self.rank + 1), P2P(self.dist.isend, mine[1], self.rank + 1),
                     P2P(self.dist.irecv, halo[0], self.rank + 1), P2P(self.dist.irecv, halo[1], self.rank + 1)]
-        if ops:
-            for req in self.dist.batch_isend_irecv(ops):
-                req.wait()
+        self._p2p(ops)
 
-    def gather_steppable(self, parts):
+    def _allgather_var(self, t):
+        """All-gather of 1-D tensors of different lengths, concatenated in rank order."""
         import torch
-        ((S, arrs),) = parts
-        mine = torch.tensor([S], dtype=torch.int64, device=arrs[0].device)
+        n = torch.tensor([t.numel()], dtype=torch.int64, device=t.device)
+        ns = [torch.zeros_like(n) for _ in range(self.world)]
+        self.dist.all_gather(ns, n)
+        ns = [int(v.item()) for v in ns]
+        m = max(ns)
+        if m == 0:
+            return t[:0]
+        buf = torch.zeros(m, dtype=t.dtype, device=t.device)
+        buf[:t.numel()] = t
+        outs = [torch.empty_like(buf) for _ in range(self.world)]
+        self.dist.all_gather(outs, buf)
+        return torch.cat([o[:k] for o, k in zip(outs, ns)])
+
+    def allgather_plane_counts(self, counts):
+        (c,) = counts
+        return self._allgather_var(c).cpu().numpy()
+
+    def exchange_steppable(self, layout, ext_lists):
+        (mine,) = ext_lists
+        ops = []
+        P2P = self.dist.P2POp
+        ls = layout.n_left(self.rank)
+        for s, d, s0, cnt, d0 in layout.transfers():
+            if s == self.rank:
+                for src, w in zip(mine, (12, 24, 24)):
+                    ops.append(P2P(self.dist.isend, src[(ls + s0) * w:(ls + s0 + cnt) * w], d))
+            elif d == self.rank:
+                for dst, w in zip(mine, (12, 24, 24)):
+                    ops.append(P2P(self.dist.irecv, dst[d0 * w:(d0 + cnt) * w], s))
+        self._p2p(ops)
+
+    def allgather_triples(self, parts):
+        (t,) = parts
+        return self._allgather_var(t.reshape(-1)).view(-1, 3)
+
+    def exchange_members(self, exports):
+        import torch
+        ((counts, rec),) = exports
+        mine = torch.as_tensor(np.asarray(counts, np.int64), device=rec.device if rec.numel() else self.device)
         allc = [torch.zeros_like(mine) for _ in range(self.world)]
         self.dist.all_gather(allc, mine)
-        counts = [int(c.item()) for c in allc]
-        total = sum(counts)
+        M = np.stack([a.cpu().numpy() for a in allc])  # M[s][d] = records s sends to d
+        offs = np.concatenate([[0], np.cumsum(M[self.rank])])
+        ops = []
+        P2P = self.dist.P2POp
+        for d in range(self.rank):  # my foreign members go to lower slabs
+            c = int(M[self.rank][d])
+            if c:
+                o = int(offs[d])
+                ops.append(P2P(self.dist.isend, rec[o * MEMBER_REC_BYTES:(o + c) * MEMBER_REC_BYTES], d))
+        total = int(M[self.rank + 1:, self.rank].sum())
+        recv = torch.empty(total * MEMBER_REC_BYTES, dtype=torch.uint8, device=mine.device)
+        o = 0
+        for s in range(self.rank + 1, self.world):
+            c = int(M[s][self.rank])
+            if c:
+                ops.append(P2P(self.dist.irecv, recv[o * MEMBER_REC_BYTES:(o + c) * MEMBER_REC_BYTES], s))
+                o += c
+        self._p2p(ops)
+        return [(recv if total else None, total)]
+
+    def gather_polygons(self, per_slab):
+        (polys,) = per_slab
+        out = [None] * self.world if self.rank == 0 else None
+        self.dist.gather_object(polys, out, dst=0)
         if self.rank != 0:
-            for a in arrs:
-                if S:
-                    self.dist.send(a, 0)
-            return total, None, None, None
-        out = [torch.empty(total * w, dtype=torch.uint8, device=arrs[0].device) for w in (12, 24, 24)]
-        off = 0
-        for r, n in enumerate(counts):
-            for o, a, w in zip(out, arrs, (12, 24, 24)):
-                view = o[off * w:(off + n) * w]
-                if n == 0:
-                    continue
-                if r == 0:
-                    view.copy_(a)
-                else:
-                    self.dist.recv(view, r)
-            off += n
-        return total, out[0], out[1], out[2]
+            return None
+        return [p for part in out for p in part]
 
 
-def slab_frame(slabs, comm, pts_t, R, t, params: native.PipelineParams):
-    """One frame over the local slabs; returns the polygons on rank 0 (else None)."""
+# ------------------------------------------------------------------ frame
+def slab_frame(slabs, comm, pts_t, R, t, params: native.PipelineParams, stages=None):
+    """One frame over the local slabs; returns the polygons on rank 0 (else None).
+    `stages` (optional dict) receives per-phase counts for the bench."""
     import torch
     # the library runs on its own streams and returns synchronised; whatever
     # torch (or NCCL, which torch's stream waits on) produced is fenced with a
@@ -218,11 +460,53 @@ def slab_frame(slabs, comm, pts_t, R, t, params: native.PipelineParams):
     n = pts_t.numel() // 12 if pts_t.dtype.itemsize == 1 else pts_t.numel() // 3
     for s in slabs:
         s.clear_integrate_device(pts_t.data_ptr(), n, R, t)
+    if stages is not None:
+        stages["c_map"] = slabs[0].counters()
     comm.halo_exchange(slabs)
     sync()
-    parts = [s.steppable(params.seg) for s in slabs]
-    S, idx, mean, nrm = comm.gather_steppable(parts)
-    if idx is None:
-        return None
+    seg = params.seg
+    for s in slabs:
+        s.steppable(seg)
+    if stages is not None:
+        stages["c_step"] = slabs[0].counters()
+    counts = comm.allgather_plane_counts([s.plane_counts() for s in slabs])
+    ranges = [s_range for s_range in _ranges(slabs, comm)]
+    layout = SlabLayout(ranges, counts, adjacency_window(seg, slabs[0].res))
+    ext = [s.extend(seg, layout) for s in slabs]
+    comm.exchange_steppable(layout, ext)
     sync()
-    return slabs[0].segment(params, S, idx, mean, nrm)
+    parts, zsize = [], 0
+    for s in slabs:
+        tr, zsize = s.label(seg)
+        parts.append(tr)
+    triples = comm.allgather_triples(parts)
+    sync()
+    for s in slabs:
+        s.merge(triples)
+    exports = [s.export(layout.n) for s in slabs]
+    recv = comm.exchange_members(exports)
+    sync()
+    polys = [s.segment_owned(params, r, nr) for s, (r, nr) in zip(slabs, recv)]
+    if stages is not None:
+        stages["c_seg"] = slabs[0].counters()
+        stages.update(steppable=int(layout.P[-1]), zone=int(zsize), triples=int(triples.shape[0]),
+                      exported=int(sum(int(c.sum()) for c, _ in exports)))
+    return comm.gather_polygons(polys)
+
+
+_RANGES_CACHE: dict = {}
+
+
+def _ranges(slabs, comm):
+    """x ranges of all slabs of the decomposition (all ranks for DistComm)."""
+    if isinstance(comm, DistComm):
+        key = (comm.world, slabs[0].window_extent[0])
+        if key not in _RANGES_CACHE:
+            import torch
+            mine = torch.tensor([slabs[0].x_begin, slabs[0].x_end], dtype=torch.int64,
+                                device=f"cuda:{slabs[0].device}" if comm.device is not None else "cpu")
+            allr = [torch.zeros_like(mine) for _ in range(comm.world)]
+            comm.dist.all_gather(allr, mine)
+            _RANGES_CACHE[key] = [tuple(int(v) for v in a.tolist()) for a in allr]
+        return _RANGES_CACHE[key]
+    return [(s.x_begin, s.x_end) for s in slabs]

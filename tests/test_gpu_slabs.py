@@ -3,7 +3,9 @@
 A fixed window driven with clear_rays + integrate_frame per frame and then
 segmented must give the same steppable list (bit-exact) and the same polygons
 whether it lives in one grid or in N slab grids with halo exchange and the
-rank-0 gather -- the multi-GPU path's correctness argument, checked on 1 GPU."""
+distributed segmentation (local CCL + boundary-label merge + cluster gather
+to the owning slab) -- the multi-GPU path's correctness argument, checked on
+1 GPU. The merged labels must equal the single-grid canonical labels."""
 import numpy as np
 import pytest
 import torch
@@ -34,6 +36,19 @@ def one_grid(frames, params):
     return g, polys
 
 
+def steppable_normals(g, params):
+    from ctypes import POINTER, byref, c_size_t, c_int32
+    st = POINTER(native.Steppable)()
+    objs = POINTER(c_int32)()
+    nobj = c_size_t()
+    native.check(native.lib().vp_classify_steppable(g.h, byref(params.seg), byref(st), byref(objs), byref(nobj)))
+    S = st.contents.count
+    nrm = np.ctypeslib.as_array(st.contents.normal, (S, 3)).copy()
+    native.lib().vp_steppable_free(st)
+    native.lib().vp_free(objs)
+    return nrm
+
+
 def steppable_of_grid(g, params):
     from ctypes import POINTER, byref, c_size_t, c_int32
     st = POINTER(native.Steppable)()
@@ -48,7 +63,9 @@ def steppable_of_grid(g, params):
     return idx, mean
 
 
-@pytest.mark.parametrize("ranges", [[(0, 300)], [(0, 150), (150, 300)], [(0, 37), (37, 150), (150, 151), (151, 300)]])
+@pytest.mark.parametrize("ranges", [[(0, 300)], [(0, 150), (150, 300)], [(0, 37), (37, 150), (150, 151), (151, 300)],
+                                    [(0, 100), (100, 102), (102, 104), (104, 200), (200, 300)],
+                                    [(a, a + 38) for a in range(0, 266, 38)] + [(266, 300)]])
 def test_virtual_slabs_equal_one_grid(ranges):
     frames = scenes.stair_frames(10)
     params = native.default_params(seed=5, refine_exact=True)
@@ -60,11 +77,15 @@ def test_virtual_slabs_equal_one_grid(ranges):
     for f in frames:
         pts = torch.from_numpy(np.ascontiguousarray(f.points)).cuda()
         polys = slabs.slab_frame(sl, comm, pts, f.rotation, f.translation, params)
+    # the merged labels of the last frame (kept by each slab) == single-grid canonical labels
+    labels = np.concatenate([s.merge_labels().cpu().numpy() for s in sl])
     parts = [s.steppable(params.seg) for s in sl]
     S = sum(p[0] for p in parts)
     idx = torch.cat([p[1][0] for p in parts]).cpu().numpy().view(np.int32).reshape(S, 3)
     mean = torch.cat([p[1][1] for p in parts]).cpu().numpy().view(np.float64).reshape(S, 3)
     assert np.array_equal(idx, ref_idx) and mean.tobytes() == ref_mean.tobytes()
+    ref_labels = native.label_components(ref_idx, ref_mean, steppable_normals(g, params), params.seg, RES)
+    assert np.array_equal(labels, ref_labels)
     assert len(ref_polys) >= 3
     assert format_polygons(polys) == format_polygons(ref_polys)
 
