@@ -353,6 +353,11 @@ int vp_pipeline_frame_trace(vp_pipeline* pl, const float* xyz, uint64_t n,
                             const double rotation[9], const double translation[3],
                             uint8_t** buf, uint64_t* len);
 
+/* label_components algorithm (identical labels): 0 = min-neighbour hooking +
+   forward-window unions (default), 1 = neighbour-sampling unions + whole-window
+   unions outside the sampled giant component, 2 = hooking + the same giant
+   skip. Set before creating pipelines (captured graphs keep their variant). */
+int vp_set_ccl_mode(int mode);
 /* Count of this library's kernel launches since process start (bench evidence). */
 uint64_t vp_kernel_launch_count(void);
 /* Per-kernel CUDA-event timing of every launch (serialising; for profiling

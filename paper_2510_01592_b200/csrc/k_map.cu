@@ -241,7 +241,18 @@ __global__ void __launch_bounds__(256) k_integrate_fold(GridDesc g, const FrameP
 // is marked with a fire-and-forget RED.OR; lanes of the warp standing in the
 // same cell as their left neighbour this iteration (adjacent pixels near the
 // sensor) skip it. Nothing in the loop waits on memory.
-__global__ void __launch_bounds__(256, 4) k_clear_walk(GridDesc g, const FrameParams* __restrict__ fp) {
+//
+// Per-step work is kept minimal (the kernel is issue/FP64-bound, not
+// memory-bound): the reference loop "visit unless origin or end cell; argmin;
+// step; bounds; t_max[m] += t_delta[m]" is rotated so the origin test runs
+// once (the DDA is monotone per axis: once it left the first cell it never
+// returns, and the first cell is the origin cell whenever the origin lies in
+// the window), the end-cell test is one compare of the cell's bitmap key
+// (word << 5 | bit, injective over the grid's cells), and only the stepped
+// axis' t_max is advanced (one DADD). kSlab adds the owned-x-range logic of a
+// spatial slab.
+template <bool kSlab>
+__device__ __forceinline__ void clear_walk_body(const GridDesc& g, const FrameParams* __restrict__ fp) {
   const uint64_t n = fp->n;
   const double res = g.res;
   const double lo0 = fp->origin_pre[0], lo1 = fp->origin_pre[1], lo2 = fp->origin_pre[2];
@@ -256,6 +267,7 @@ __global__ void __launch_bounds__(256, 4) k_clear_walk(GridDesc g, const FramePa
   const uint32_t ystride = static_cast<uint32_t>(g.W);
   uint32_t* __restrict__ clr = g.clr;
   const unsigned lane = lane_id();
+  const unsigned left = lane ? (1u << (lane - 1)) : 0u;  // the lane to my left
   for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const float* pp = fp->pts + 3 * i;
@@ -311,46 +323,71 @@ __global__ void __launch_bounds__(256, 4) k_clear_walk(GridDesc g, const FramePa
     VP_INIT(d1, c1, lo1, e1, s1, tm1, td1)
     VP_INIT(d2, c2, lo2, e2, s2, tm2, td2)
 #undef VP_INIT
-    // local row of the current cell (meaningful while c0 is owned here)
+    // bitmap key of a cell of this grid: word << 5 | bit (meaningful while c0
+    // is stored here; the end cell's key only when it is owned here)
+    const bool e_here = ec0 >= own0 && ec0 < own1 && static_cast<unsigned>(ec1) < static_cast<unsigned>(g.ey) &&
+                        static_cast<unsigned>(ec2) < static_cast<unsigned>(g.ez);
+    const uint32_t key_e =
+        e_here ? (((static_cast<uint32_t>(ec0 - g.xoff) * xstride + static_cast<uint32_t>(ec1) * ystride +
+                    (static_cast<uint32_t>(ec2) >> 5)) << 5) | (static_cast<uint32_t>(ec2) & 31u))
+               : 0xffffffffu;
     uint32_t row = static_cast<uint32_t>(c0 - g.xoff) * xstride + static_cast<uint32_t>(c1) * ystride;
     const int dx_row = s0 * static_cast<int>(xstride), dy_row = s1 * static_cast<int>(ystride);
+    bool mark = !(c0 == oc0 && c1 == oc1 && c2 == oc2);  // origin cell: first cell only
     for (int s = 0; s < max_steps; ++s) {
-      const bool is_o = c0 == oc0 && c1 == oc1 && c2 == oc2;
-      const bool is_e = c0 == ec0 && c1 == ec1 && c2 == ec2;
-      // a slab never sees the ray again once it left the owned x-range in
-      // its stepping direction (the DDA is monotone per axis)
-      if ((s0 > 0 && c0 >= own1) || (s0 < 0 && c0 < own0) || (s0 == 0 && (c0 < own0 || c0 >= own1))) break;
-      if (!is_o && !is_e && c0 >= own0 && c0 < own1) {  // not yet entered: skip
-        const uint32_t w = row + (static_cast<uint32_t>(c2) >> 5);
-        const uint32_t key = (w << 5) | (static_cast<uint32_t>(c2) & 31u);
+      if (s > 0) {
+        // m = argmin t_max, ties to the lower axis (voxel_grid.cpp:170-172)
+        const bool m1 = tm1 < tm0;
+        const double tm01 = m1 ? tm1 : tm0;
+        const bool m2 = tm2 < tm01;
+        const double tm = m2 ? tm2 : tm01;
+        if (tm >= t1) break;
+        // the stepped axis as an integer (the FP64 predicates are not re-evaluated)
+        const int m = m2 ? 2 : (m1 ? 1 : 0);
+        c0 += m == 0 ? s0 : 0;
+        c1 += m == 1 ? s1 : 0;
+        c2 += m == 2 ? s2 : 0;
+        if (static_cast<unsigned>(c0) >= static_cast<unsigned>(g.gex) ||
+            static_cast<unsigned>(c1) >= static_cast<unsigned>(g.ey) ||
+            static_cast<unsigned>(c2) >= static_cast<unsigned>(g.ez))
+          break;
+        int drow = m == 0 ? dx_row : 0;
+        drow = m == 1 ? dy_row : drow;
+        row += drow;
+        double tdm = m == 0 ? td0 : td1;
+        tdm = m == 2 ? td2 : tdm;
+        const double tn = tm + tdm;  // t_max[m] += t_delta[m]
+        tm0 = m == 0 ? tn : tm0;
+        tm1 = m == 1 ? tn : tm1;
+        tm2 = m == 2 ? tn : tm2;
+        mark = true;
+      }
+      bool here = true;
+      if (kSlab) {
+        // a slab never sees the ray again once it left the owned x-range in
+        // its stepping direction (the DDA is monotone per axis)
+        if ((s0 > 0 && c0 >= own1) || (s0 < 0 && c0 < own0) || (s0 == 0 && (c0 < own0 || c0 >= own1))) break;
+        here = c0 >= own0 && c0 < own1;  // not yet entered: skip
+      }
+      const uint32_t w = row + (static_cast<uint32_t>(c2) >> 5);
+      const uint32_t key = (w << 5) | (static_cast<uint32_t>(c2) & 31u);
+      if (mark && here && key != key_e) {
         // adjacent pixels stand in the same cell as runs of lanes: only the
         // first lane of each run issues the RED
         const unsigned act = __activemask();
         const uint32_t prev = __shfl_up_sync(act, key, 1);
-        const bool dup = lane > 0 && ((act >> (lane - 1)) & 1u) && prev == key;
+        const bool dup = (act & left) && prev == key;
         if (!dup) atomicOr(clr + w, 1u << (c2 & 31));
       }
-      // m = argmin t_max, ties to the lower axis (voxel_grid.cpp:170-172)
-      const bool m1 = tm1 < tm0;
-      const double tm01 = m1 ? tm1 : tm0;
-      const bool m2 = tm2 < tm01;
-      const double tm = m2 ? tm2 : tm01;
-      if (tm >= t1) break;
-      const bool m0 = !m1 && !m2;
-      const bool m1s = m1 && !m2;
-      c0 += m0 ? s0 : 0;
-      c1 += m1s ? s1 : 0;
-      c2 += m2 ? s2 : 0;
-      if (static_cast<unsigned>(c0) >= static_cast<unsigned>(g.gex) ||
-          static_cast<unsigned>(c1) >= static_cast<unsigned>(g.ey) ||
-          static_cast<unsigned>(c2) >= static_cast<unsigned>(g.ez))
-        break;
-      row += m0 ? dx_row : (m1s ? dy_row : 0);
-      tm0 = m0 ? tm0 + td0 : tm0;
-      tm1 = m1s ? tm1 + td1 : tm1;
-      tm2 = m2 ? tm2 + td2 : tm2;
     }
   }
+}
+
+__global__ void __launch_bounds__(256, 4) k_clear_walk(GridDesc g, const FrameParams* __restrict__ fp) {
+  clear_walk_body<false>(g, fp);
+}
+__global__ void __launch_bounds__(256, 4) k_clear_walk_slab(GridDesc g, const FrameParams* __restrict__ fp) {
+  clear_walk_body<true>(g, fp);
 }
 
 __device__ __forceinline__ void zero_cell(Cell* c) {

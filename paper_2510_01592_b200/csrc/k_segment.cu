@@ -329,6 +329,147 @@ __global__ void __launch_bounds__(256) k_ccl_union(Counters* ctr, SegDev sp, Seg
   }
 }
 
+// ---------------------------------------------------------------------------
+// Sampling CCL (Afforest-style) for large planar components:
+//  1. k_ccl_lattice  each voxel unions with its first adjacent voxel in the
+//                    +z, +y and +x neighbour columns -- on a surface sampled
+//                    at the voxel pitch this already joins almost every
+//                    voxel of a plane into one tree;
+//  2. k_ccl_compress pointer jumping;
+//  3. k_ccl_giant    the most frequent root among 1024 evenly spaced voxels;
+//  4. k_ccl_full     every voxel NOT in that component unions with every
+//                    adjacent voxel of its whole (2w+1)^3 window.
+// Edges with both ends in the giant component are redundant (sets only
+// grow); every other edge has an end that scans its whole window, and the
+// predicate is symmetric, so every edge of build_adjacency is applied. The
+// link rule (larger root under smaller) keeps every root the minimum ordinal
+// of its set: labels stay canonical and bit-exact.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_ccl_lattice(Counters* ctr, SegDev sp, SegBufs b, MapDesc m) {
+  const uint32_t S = min(ctr->S, b.Scap);
+  int32_t* parent = b.parent;
+  const int xmax = m.lo[0] + m.dims[0] - 1, ymax = m.lo[1] + m.dims[1] - 1;
+  const int zmin = m.lo[2], zmax = m.lo[2] + m.dims[2] - 1;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < S; i += gridDim.x * blockDim.x) {
+    const int x = __ldg(b.st_idx + 3 * i), y = __ldg(b.st_idx + 3 * i + 1), z = __ldg(b.st_idx + 3 * i + 2);
+    const d3 mi = mk3(__ldg(b.st_mean + 3 * i), __ldg(b.st_mean + 3 * i + 1), __ldg(b.st_mean + 3 * i + 2));
+    const d3 ni = mk3(__ldg(b.st_normal + 3 * i), __ldg(b.st_normal + 3 * i + 1),
+                      __ldg(b.st_normal + 3 * i + 2));
+    // neighbour sampling: at most one union per direction (+z, +y, +x), with
+    // the first adjacent voxel of the 3-cell column (z-1..z+1) that way -- a
+    // surface sampled at the voxel pitch is then one spanning structure
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const int X = x + (r == 2 ? 1 : 0), Y = y + (r == 1 ? 1 : 0);
+      if (X > xmax || Y > ymax) continue;
+      const int z0 = r == 0 ? z + 1 : max(z - 1, zmin);
+      const int z1 = min(z + 1, zmax);
+      if (z0 > z1) continue;
+      uint32_t bits = m.row_span(X, Y, z0, z1 - z0 + 1);
+      if (!bits) continue;
+      int j = __ldg(m.map + m.slot(X, Y, z0 + __ffs(bits) - 1)) - 1;
+      while (bits) {
+        bits &= bits - 1;
+        ++j;
+        if (adjacent(b, sp, mi, ni, j)) {
+          uf_union(parent, static_cast<int>(i), j);
+          break;
+        }
+      }
+    }
+  }
+}
+
+// Single block: the most frequent root among up to 1024 evenly spaced voxels
+// (ties to the smaller root) -> ctr->ccl_giant (-1 if there are no voxels).
+__global__ void __launch_bounds__(1024) k_ccl_giant(Counters* ctr, SegBufs b) {
+  __shared__ int32_t v[1024];
+  __shared__ unsigned long long best;
+  const uint32_t S = min(ctr->S, b.Scap);
+  const uint32_t k = min(S, 1024u);
+  const uint32_t t = threadIdx.x;
+  if (t == 0) best = ~0ull;
+  v[t] = t < k ? __ldcg(b.parent + static_cast<uint32_t>((static_cast<uint64_t>(t) * S) / k)) : 0x7fffffff;
+  __syncthreads();
+  for (uint32_t q = 2; q <= 1024; q <<= 1) {  // bitonic sort, ascending
+    for (uint32_t j = q >> 1; j > 0; j >>= 1) {
+      const uint32_t l = t ^ j;
+      if (l > t) {
+        const int32_t a = v[t], c = v[l];
+        if (((t & q) == 0) ? (a > c) : (a < c)) {
+          v[t] = c;
+          v[l] = a;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (t < k && (t == 0 || v[t - 1] != v[t])) {  // run start: its length by binary search
+    uint32_t lo = t, hi = k;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (v[mid] == v[t]) lo = mid + 1; else hi = mid;
+    }
+    // max count, then min root: pack (1024 - count) in the high bits
+    const unsigned long long key = (static_cast<unsigned long long>(1024u - (lo - t)) << 32) |
+                                   static_cast<uint32_t>(v[t]);
+    atomicMin(&best, key);
+  }
+  __syncthreads();
+  if (t == 0) ctr->ccl_giant = k ? static_cast<int32_t>(best & 0xffffffffu) : -1;
+}
+
+// Whole-window unions of every voxel outside the giant component (one warp
+// per voxel, one window row per lane).
+__global__ void __launch_bounds__(256) k_ccl_full(Counters* ctr, SegDev sp, SegBufs b, MapDesc m) {
+  const uint32_t S = min(ctr->S, b.Scap);
+  const int w = sp.w, span = 2 * w + 1;
+  const int nrows = span * span;
+  const int32_t giant = ctr->ccl_giant;
+  int32_t* parent = b.parent;
+  const unsigned lane = lane_id();
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarp = (gridDim.x * blockDim.x) >> 5;
+  const int xmin = m.lo[0], xmax = m.lo[0] + m.dims[0] - 1, ymin = m.lo[1], ymax = m.lo[1] + m.dims[1] - 1;
+  const int zmin = m.lo[2], zmax = m.lo[2] + m.dims[2] - 1;
+  for (uint32_t i = warp; i < S; i += nwarp) {
+    // the skip test must be warp-uniform (lanes arrive here at different
+    // times while other warps relink i): lane 0 decides for the warp
+    int pi = 0;
+    if (lane == 0) pi = __ldcg(parent + i);
+    if (__shfl_sync(0xffffffffu, pi, 0) == giant) continue;
+    const int x = __ldg(b.st_idx + 3 * i), y = __ldg(b.st_idx + 3 * i + 1), z = __ldg(b.st_idx + 3 * i + 2);
+    const d3 mi = mk3(__ldg(b.st_mean + 3 * i), __ldg(b.st_mean + 3 * i + 1), __ldg(b.st_mean + 3 * i + 2));
+    const d3 ni = mk3(__ldg(b.st_normal + 3 * i), __ldg(b.st_normal + 3 * i + 1),
+                      __ldg(b.st_normal + 3 * i + 2));
+    int ri = -1;
+    if (lane == 0) ri = uf_find(parent, static_cast<int>(i));
+    ri = __shfl_sync(0xffffffffu, ri, 0);
+    for (int r = static_cast<int>(lane); r < nrows; r += 32) {
+      const int dx = r / span - w, dy = r % span - w;
+      const int X = x + dx, Y = y + dy;
+      if (X < xmin || X > xmax || Y < ymin || Y > ymax) continue;
+      const int z0 = max(z - w, zmin);
+      const int z1 = min(z + w, zmax);
+      uint32_t bits = m.row_span(X, Y, z0, z1 - z0 + 1);
+      if (!bits) continue;
+      // voxels of one (X, Y) column are consecutive ordinals: one map load
+      int j = __ldg(m.map + m.slot(X, Y, z0 + __ffs(bits) - 1)) - 1;
+      while (bits) {
+        bits &= bits - 1;
+        ++j;
+        if (j == static_cast<int>(i)) continue;
+        const int pj = __ldcg(parent + j);
+        if (pj == ri) continue;  // already in i's tree
+        if (!adjacent(b, sp, mi, ni, j)) continue;
+        const int rj = uf_find(parent, j);
+        if (rj == ri) continue;
+        ri = uf_link(parent, ri, rj);
+      }
+    }
+  }
+}
+
 // build_adjacency materialised (segmentation.cpp:112-130) for the API:
 // pass 1 (cols == nullptr) counts, pass 2 fills rows in ascending ordinal order.
 __global__ void k_adjacency(Counters* ctr, SegDev sp, SegBufs b, MapDesc m, const uint64_t* rows,
@@ -384,7 +525,7 @@ __global__ void k_ccl_flatten(Counters* ctr, SegBufs b, MapDesc m) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < S; i += gridDim.x * blockDim.x) {
     const int r = uf_find(parent, static_cast<int>(i));
     b.label[i] = r;
-    atomicAdd(&b.cnt[r], 1u);
+    atomic_inc_agg(b.cnt, r);
     const int x = b.st_idx[3 * i], y = b.st_idx[3 * i + 1], z = b.st_idx[3 * i + 2];
     m.map[m.slot(x, y, z)] = -1;
     m.bits[m.word(x, y, z)] = 0u;  // every bit of the word belongs to a steppable voxel being reset

@@ -72,7 +72,12 @@ __global__ void k_fill_i32(int32_t* a, uint64_t n, int32_t v) {
 __global__ void k_zone_bmin(const Counters* ctr, SegBufs b, ZoneDesc z, int32_t* bmin) {
   const uint32_t S = min(ctr->S, b.Scap);
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < S; i += gridDim.x * blockDim.x)
-    if (zone_of(z, __ldg(b.st_idx + 3ull * i)) >= 0) atomicMin(bmin + b.label[i], static_cast<int32_t>(i));
+    if (zone_of(z, __ldg(b.st_idx + 3ull * i)) >= 0) {
+      const int32_t r = b.label[i];
+      const unsigned peers = __match_any_sync(__activemask(), r);
+      const int32_t m = static_cast<int32_t>(__reduce_min_sync(peers, i));
+      if (static_cast<int>(lane_id()) == __ffs(peers) - 1) atomicMin(bmin + r, m);
+    }
 }
 
 // One triple per zone entry: (zone(ordinal), zone(component's smallest zone
@@ -124,7 +129,10 @@ __global__ void k_zone_minlab(const int32_t* __restrict__ t, uint64_t n, int32_t
   for (uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
        j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     if (__ldg(t + 3 * j) < 0) continue;
-    atomicMin(minlab + uf_find(parent, __ldg(t + 3 * j + 1)), __ldg(t + 3 * j + 2));
+    const int32_t r = uf_find(parent, __ldg(t + 3 * j + 1));
+    const unsigned peers = __match_any_sync(__activemask(), r);
+    const int32_t m = __reduce_min_sync(peers, __ldg(t + 3 * j + 2));
+    if (static_cast<int>(lane_id()) == __ffs(peers) - 1) atomicMin(minlab + r, m);
   }
 }
 
@@ -236,12 +244,9 @@ __global__ void k_owner_prep(uint32_t n_own, uint32_t n_recv, int64_t own_base,
     b.st_mean[3ull * e + 1] = m1;
     b.st_mean[3ull * e + 2] = m2;
     const int64_t local = static_cast<int64_t>(L) - own_base;
-    if (local >= 0 && local < static_cast<int64_t>(n_own)) {
-      b.label[e] = static_cast<int32_t>(local);
-      atomicAdd(b.cnt + local, 1u);
-    } else {
-      b.label[e] = static_cast<int32_t>(e);
-    }
+    const bool mine = local >= 0 && local < static_cast<int64_t>(n_own);
+    b.label[e] = mine ? static_cast<int32_t>(local) : static_cast<int32_t>(e);
+    if (mine) atomic_inc_agg(b.cnt, static_cast<int>(local));
   }
 }
 

@@ -26,6 +26,9 @@ using namespace vp;
 namespace {
 
 thread_local std::string g_err;
+// CCL variant: 0 = min-neighbour hook + forward-window unions (default),
+// 1 = neighbour sampling + giant skip, 2 = hook + giant skip (same labels)
+int g_ccl_mode = 0;
 std::atomic<uint64_t> g_launches{0};
 
 constexpr double kRadToDeg = 57.295779513082320876798;
@@ -450,7 +453,8 @@ struct vp_grid {
     if (!(res > 0.0) || e[0] <= 0 || e[1] <= 0 || e[2] <= 0)  // voxel_grid.cpp:21-22
       fail(VP_EINVAL, "VoxelGrid: resolution and extents must be positive");
     const uint64_t C = static_cast<uint64_t>(e[0]) * e[1] * e[2];
-    if (C >= (1ull << 32)) fail(VP_EINVAL, "VoxelGrid: more than 2^32 cells per grid (use slabs)");
+    if (C >= (1ull << 32) || static_cast<uint64_t>(e[0]) * e[1] * ((e[2] + 31) / 32) * 32 >= 0xffffffffull)
+      fail(VP_EINVAL, "VoxelGrid: more than 2^32 cells per grid (use slabs)");
     check_device(dev);
     device = dev;
     for (int k = 0; k < 3; ++k) {
@@ -664,7 +668,10 @@ struct vp_grid {
   // the device params), so the same launches can be replayed as a graph.
   void launch_clear(uint64_t n) {
     if (n == 0 && !capturing) return;
-    LAUNCH(k_clear_walk, grid_for(capturing ? pcap : n, 148 * 32), kThreads, 0, lstream, gd, d_fp);
+    if (gd.xoff != 0 || gd.gex != gd.ex)
+      LAUNCH(k_clear_walk_slab, grid_for(capturing ? pcap : n, 148 * 32), kThreads, 0, lstream, gd, d_fp);
+    else
+      LAUNCH(k_clear_walk, grid_for(capturing ? pcap : n, 148 * 32), kThreads, 0, lstream, gd, d_fp);
     LAUNCH(k_clear_apply, grid_for(gd.nwords), kThreads, 0, lstream, gd, d_fp, ctr);
   }
   void launch_integrate(uint64_t n) {
@@ -726,11 +733,26 @@ struct vp_grid {
   // union-find over the steppable list in seg.b (ctr->S set)
   void launch_ccl(const SegDev& sd, const MapDesc& m) { launch_ccl(sd, m, seg.b); }
   void launch_ccl(const SegDev& sd, const MapDesc& m, const SegBufs& sb) {
-    // ECL-style atomic-free pre-hooking + compression: most unions then end at
-    // the one-load parent check (C2: union pass 400 us -> 80 us)
-    LAUNCH(k_ccl_hook, kWide, kThreads, 0, stream, ctr, sd, sb, m);
-    LAUNCH(k_ccl_compress, kWide, kThreads, 0, stream, ctr, sb);
-    LAUNCH(k_ccl_union, kWide, kThreads, 0, stream, ctr, sd, sb, m);
+    if (g_ccl_mode == 0) {
+      // ECL-style atomic-free pre-hooking + compression: most unions then end at
+      // the one-load parent check (C2: union pass 400 us -> 80 us)
+      LAUNCH(k_ccl_hook, kWide, kThreads, 0, stream, ctr, sd, sb, m);
+      LAUNCH(k_ccl_compress, kWide, kThreads, 0, stream, ctr, sb);
+      LAUNCH(k_ccl_union, kWide, kThreads, 0, stream, ctr, sd, sb, m);
+    } else {
+      // sampling variants (measured slower on C2 and C5):
+      // 1 = neighbour-sampling unions, 2 = min-neighbour hooking; then
+      // whole-window unions of the voxels outside the sampled giant tree
+      if (g_ccl_mode == 1) {
+        LAUNCH(k_ccl_init, kWide, kThreads, 0, stream, ctr, sb);
+        LAUNCH(k_ccl_lattice, kWide, kThreads, 0, stream, ctr, sd, sb, m);
+      } else {
+        LAUNCH(k_ccl_hook, kWide, kThreads, 0, stream, ctr, sd, sb, m);
+      }
+      LAUNCH(k_ccl_compress, kWide, kThreads, 0, stream, ctr, sb);
+      LAUNCH(k_ccl_giant, 1, 1024, 0, stream, ctr, sb);
+      LAUNCH(k_ccl_full, kWide, kThreads, 0, stream, ctr, sd, sb, m);
+    }
     LAUNCH(k_ccl_flatten, kWide, kThreads, 0, stream, ctr, sb, m);
   }
   // label_base: global ordinal of list entry 0 (slab owners), else 0
@@ -1244,6 +1266,11 @@ extern "C" {
 const char* vp_last_error(void) { return g_err.c_str(); }
 const char* vp_version(void) { return "voxplane_b200 0.1 (sm_100a)"; }
 uint64_t vp_kernel_launch_count(void) { return g_launches.load(); }
+int vp_set_ccl_mode(int mode) {
+  if (mode < 0 || mode > 2) return VP_EINVAL;
+  g_ccl_mode = mode;
+  return VP_OK;
+}
 
 void vp_profile_enable(int on) {
   g_prof_on = on != 0;
@@ -2125,7 +2152,8 @@ int vp_slab_extend(vp_grid* g, const vp_seg_params* p, const vp_slab_layout* lay
     for (int k = 0; k < n; ++k) L.rd.ord_lo[k] = static_cast<int64_t>(L.P[L.xb[k]]);
     // extended list buffers; the own list moves in before any seg realloc
     if (L.n_ext > L.xcap) {
-      const uint64_t cap = std::max<uint64_t>(L.n_ext + L.n_ext / 4, 1 << 16);
+      // generous first size (the list grows with the map): no cudaMalloc in steady state
+      const uint64_t cap = std::max<uint64_t>({L.n_ext + L.n_ext / 2, 2 * L.xcap, g->seg.b.Scap, 1 << 16});
       for (void* q : {(void*)L.xidx, (void*)L.xmean, (void*)L.xnrm, (void*)L.bmin, (void*)L.flabel})
         if (q) cudaFree(q);
       L.xidx = dalloc<int32_t>(3 * cap);
@@ -2196,7 +2224,7 @@ int vp_slab_label(vp_grid* g, const vp_seg_params* p, int32_t** triples, uint64_
     }
     if (zent > L.tcap || !L.triples) {
       dfree(L.triples);
-      L.tcap = std::max<uint64_t>(zent + zent / 4, 1 << 12);
+      L.tcap = std::max<uint64_t>({zent + zent / 2, 2 * L.tcap, 1 << 20});
       L.triples = dalloc<int32_t>(3 * L.tcap);
       if (!L.ntrip) L.ntrip = dalloc<uint32_t>(1);
     }
@@ -2231,7 +2259,7 @@ int vp_slab_merge(vp_grid* g, const int32_t* triples, uint64_t n_triples, int32_
     if (L.zone_size > L.zcap || !L.zparent) {
       dfree(L.zparent);
       dfree(L.zminlab);
-      L.zcap = std::max<uint64_t>(L.zone_size + L.zone_size / 4, 1 << 12);
+      L.zcap = std::max<uint64_t>({L.zone_size + L.zone_size / 2, 2 * L.zcap, 1 << 20});
       L.zparent = dalloc<int32_t>(L.zcap);
       L.zminlab = dalloc<int32_t>(L.zcap);
     }
@@ -2264,7 +2292,7 @@ int vp_slab_export(vp_grid* g, uint64_t* dest_counts, void** records) {
     const uint64_t hn = static_cast<uint64_t>(L.n) * nch;
     if (hn > L.hcap || !L.H) {
       dfree(L.H);
-      L.hcap = std::max<uint64_t>(hn + hn / 4, 1 << 12);
+      L.hcap = std::max<uint64_t>({hn + hn / 2, 2 * L.hcap, 1 << 18});
       L.H = dalloc<uint32_t>(L.hcap);
       if (!L.dcount) L.dcount = dalloc<uint32_t>(kMaxSlabs);
     }
@@ -2283,7 +2311,7 @@ int vp_slab_export(vp_grid* g, uint64_t* dest_counts, void** records) {
     }
     if (tot > L.ecap || !L.exp) {
       dfree(L.exp);
-      L.ecap = std::max<uint64_t>(tot + tot / 4, 1 << 12);
+      L.ecap = std::max<uint64_t>({tot + tot / 2, 2 * L.ecap, 1 << 20});
       L.exp = dalloc<MemberRec>(L.ecap);
     }
     if (tot) {

@@ -85,6 +85,7 @@ struct Counters {
   uint32_t poly_chunks;
   uint32_t fit_chunks;
   uint32_t surv_max;     // largest hull-survivor set of the frame (diagnostic)
+  int32_t ccl_giant;     // root of the sampled largest component after the lattice links
 };
 
 constexpr uint32_t kOverflowOcc = 1u;
@@ -257,6 +258,14 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 
 // Warp-aggregated atomicAdd of a per-lane value to one counter (all lanes
 // of the warp must call it).
+// atomicAdd(base + idx, 1) with the lanes that hit the same idx combined
+// (one atomic per distinct idx per warp: big components otherwise serialise
+// on one counter).
+__device__ __forceinline__ void atomic_inc_agg(uint32_t* base, int idx) {
+  const unsigned peers = __match_any_sync(__activemask(), idx);
+  if (static_cast<int>(lane_id()) == __ffs(peers) - 1) atomicAdd(base + idx, static_cast<uint32_t>(__popc(peers)));
+}
+
 __device__ __forceinline__ void warp_add_u64(unsigned long long* c, unsigned long long v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);

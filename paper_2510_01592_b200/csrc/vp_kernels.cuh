@@ -247,6 +247,7 @@ __global__ void k_integrate_fold(GridDesc g, const FrameParams* fp, Counters* ct
                                  const uint32_t* groups, uint32_t* hkey, uint32_t* hcnt,
                                  const uint32_t* hoff, uint32_t* sorted);
 __global__ void k_clear_walk(GridDesc g, const FrameParams* fp);
+__global__ void k_clear_walk_slab(GridDesc g, const FrameParams* fp);
 __global__ void k_clear_apply(GridDesc g, const FrameParams* fp, Counters* ctr);
 __global__ void k_recenter(GridDesc g, const FrameParams* fp, Counters* ctr);
 __global__ void k_map_finalize(Counters* ctr, unsigned long long* occ_total);
@@ -277,6 +278,9 @@ __global__ void k_ccl_init(Counters* ctr, SegBufs b);
 __global__ void k_ccl_union(Counters* ctr, SegDev sp, SegBufs b, MapDesc m);
 __global__ void k_ccl_hook(Counters* ctr, SegDev sp, SegBufs b, MapDesc m);
 __global__ void k_ccl_compress(Counters* ctr, SegBufs b);
+__global__ void k_ccl_lattice(Counters* ctr, SegDev sp, SegBufs b, MapDesc m);
+__global__ void k_ccl_giant(Counters* ctr, SegBufs b);
+__global__ void k_ccl_full(Counters* ctr, SegDev sp, SegBufs b, MapDesc m);
 __global__ void k_ccl_flatten(Counters* ctr, SegBufs b, MapDesc m);
 __global__ void k_cluster_flags(Counters* ctr, SegDev sp, SegBufs b);
 __global__ void k_cluster_assign(Counters* ctr, SegBufs b);

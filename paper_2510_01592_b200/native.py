@@ -469,5 +469,11 @@ def refine_planes(fits_models, up=(0.0, 0.0, 1.0), exact=False, device=0):
     return [(np.array(out[i].normal[:]), out[i].offset) for i in range(n)]
 
 
+def set_ccl_mode(mode: int) -> None:
+    """0 = hook + forward-window unions (default), 1 = neighbour sampling + giant
+    skip, 2 = hook + giant skip (identical labels)."""
+    check(lib().vp_set_ccl_mode(C.c_int(mode)))
+
+
 def kernel_launch_count() -> int:
     return int(lib().vp_kernel_launch_count())

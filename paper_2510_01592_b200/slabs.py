@@ -450,7 +450,16 @@ class DistComm:
 def slab_frame(slabs, comm, pts_t, R, t, params: native.PipelineParams, stages=None):
     """One frame over the local slabs; returns the polygons on rank 0 (else None).
     `stages` (optional dict) receives per-phase counts for the bench."""
+    import time
+
     import torch
+    clock = [time.perf_counter()]
+
+    def phase(name):  # wall time per phase (library calls return synchronised)
+        if stages is not None:
+            now = time.perf_counter()
+            stages.setdefault("phase_ms", {})[name] = round(1e3 * (now - clock[0]), 3)
+            clock[0] = now
     # the library runs on its own streams and returns synchronised; whatever
     # torch (or NCCL, which torch's stream waits on) produced is fenced with a
     # stream synchronise before the library reads it
@@ -460,6 +469,7 @@ def slab_frame(slabs, comm, pts_t, R, t, params: native.PipelineParams, stages=N
     n = pts_t.numel() // 12 if pts_t.dtype.itemsize == 1 else pts_t.numel() // 3
     for s in slabs:
         s.clear_integrate_device(pts_t.data_ptr(), n, R, t)
+    phase("broadcast+clear+integrate")
     if stages is not None:
         stages["c_map"] = slabs[0].counters()
     comm.halo_exchange(slabs)
@@ -467,31 +477,40 @@ def slab_frame(slabs, comm, pts_t, R, t, params: native.PipelineParams, stages=N
     seg = params.seg
     for s in slabs:
         s.steppable(seg)
+    phase("halo planes+normals+classify")
     if stages is not None:
         stages["c_step"] = slabs[0].counters()
     counts = comm.allgather_plane_counts([s.plane_counts() for s in slabs])
     ranges = [s_range for s_range in _ranges(slabs, comm)]
     layout = SlabLayout(ranges, counts, adjacency_window(seg, slabs[0].res))
+    phase("plane counts+layout")
     ext = [s.extend(seg, layout) for s in slabs]
     comm.exchange_steppable(layout, ext)
     sync()
+    phase("halo lists")
     parts, zsize = [], 0
     for s in slabs:
         tr, zsize = s.label(seg)
         parts.append(tr)
+    phase("local ccl")
     triples = comm.allgather_triples(parts)
     sync()
     for s in slabs:
         s.merge(triples)
+    phase("label merge")
     exports = [s.export(layout.n) for s in slabs]
     recv = comm.exchange_members(exports)
     sync()
+    phase("cluster gather")
     polys = [s.segment_owned(params, r, nr) for s, (r, nr) in zip(slabs, recv)]
+    phase("fit+refine+polygon")
     if stages is not None:
         stages["c_seg"] = slabs[0].counters()
         stages.update(steppable=int(layout.P[-1]), zone=int(zsize), triples=int(triples.shape[0]),
                       exported=int(sum(int(c.sum()) for c, _ in exports)))
-    return comm.gather_polygons(polys)
+    out = comm.gather_polygons(polys)
+    phase("polygon gather")
+    return out
 
 
 _RANGES_CACHE: dict = {}

@@ -154,10 +154,17 @@ def random_steppable(rng, n, spread):
     return idx, mean, nrm
 
 
+@pytest.fixture(params=[0, 1, 2], ids=["hook_ccl", "sampling_ccl", "hook_giant_ccl"])
+def ccl_mode(request):
+    native.set_ccl_mode(request.param)
+    yield request.param
+    native.set_ccl_mode(0)
+
+
 @pytest.mark.parametrize("seed", range(6))
-def test_label_components_matches_oracle(seed):
+def test_label_components_matches_oracle(seed, ccl_mode):
     rng = np.random.default_rng(seed)
-    idx, mean, nrm = random_steppable(rng, 3000, 30)
+    idx, mean, nrm = random_steppable(rng, 3000 if seed < 3 else 12000, 30)
     seg = native.default_params().seg
     got = native.label_components(idx, mean, nrm, seg, 0.01)
     L = CpuSession.load("oracle")
@@ -166,6 +173,39 @@ def test_label_components_matches_oracle(seed):
                               mean.ctypes.data_as(C.POINTER(C.c_double)),
                               nrm.ctypes.data_as(C.POINTER(C.c_double)), C.byref(seg), C.c_double(0.01),
                               exp.ctypes.data_as(C.POINTER(C.c_int32)))
+    assert np.array_equal(got, exp)
+
+
+def planar_steppable(rng):
+    """~300k voxels: a 520 x 520 noisy floor with holes, a raised 200 x 120 table
+    patch and clutter -- a giant component plus many small ones."""
+    fx, fy = np.meshgrid(np.arange(520), np.arange(520), indexing="ij")
+    keep = rng.random(fx.shape) > 0.12
+    fz = 40 + (rng.random(fx.shape) < 0.2).astype(int)
+    floor = np.stack([fx[keep], fy[keep], fz[keep]], 1)
+    tx, ty = np.meshgrid(np.arange(100, 300), np.arange(50, 170), indexing="ij")
+    table = np.stack([tx.ravel(), ty.ravel(), np.full(tx.size, 115)], 1)
+    clutter = np.stack([rng.integers(0, 520, 4000), rng.integers(0, 520, 4000), rng.integers(60, 110, 4000)], 1)
+    idx = np.unique(np.concatenate([floor, table, clutter]).astype(np.int32), axis=0)
+    mean = (idx + 0.5) * 0.01 + rng.normal(0, 0.002, idx.shape)
+    nrm = np.tile([0.0, 0.0, 1.0], (len(idx), 1)) + rng.normal(0, 0.05, idx.shape)
+    nrm /= np.linalg.norm(nrm, axis=1, keepdims=True)
+    return idx, mean, nrm
+
+
+def test_label_components_large_planar_matches_oracle(ccl_mode):
+    # the sampling CCL's giant-component path at scale (C5 has ~1M steppable voxels)
+    rng = np.random.default_rng(11)
+    idx, mean, nrm = planar_steppable(rng)
+    seg = native.default_params().seg
+    got = native.label_components(idx, mean, nrm, seg, 0.01)
+    L = CpuSession.load("oracle")
+    exp = np.zeros(len(idx), np.int32)
+    L.oracle_label_components(C.c_size_t(len(idx)), idx.ctypes.data_as(C.POINTER(C.c_int32)),
+                              mean.ctypes.data_as(C.POINTER(C.c_double)),
+                              nrm.ctypes.data_as(C.POINTER(C.c_double)), C.byref(seg), C.c_double(0.01),
+                              exp.ctypes.data_as(C.POINTER(C.c_int32)))
+    assert len(np.unique(exp)) > 100
     assert np.array_equal(got, exp)
 
 

@@ -89,9 +89,14 @@ def test_golden_files_reproduced(name):
     assert format_polygons(polys) == golden_text(run)
 
 
-def test_stair_every_stage_bit_exact():
-    frames, gpu, ora = sessions("stair")
-    check_bit_exact(frames[:12], gpu, ora)
+@pytest.mark.parametrize("ccl_mode", [0, 1, 2], ids=["hook_ccl", "sampling_ccl", "hook_giant_ccl"])
+def test_stair_every_stage_bit_exact(ccl_mode):
+    native.set_ccl_mode(ccl_mode)
+    try:
+        frames, gpu, ora = sessions("stair")
+        check_bit_exact(frames[:12], gpu, ora)
+    finally:
+        native.set_ccl_mode(0)
 
 
 def hausdorff(a, b):

@@ -25,9 +25,11 @@ def run(wl, k, params):
         pts = torch.from_numpy(f.points).cuda()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        out = slabs.slab_frame(ss, comm, pts, f.rotation, f.translation, params)
+        st = {}
+        out = slabs.slab_frame(ss, comm, pts, f.rotation, f.translation, params, stages=st)
         torch.cuda.synchronize()
-        print(f"slabs={k} frame {i}: {len(f.points)} pts, {len(out)} polygons, {1e3 * (time.perf_counter() - t0):.2f} ms",
+        print(f"slabs={k} frame {i}: {len(f.points)} pts, {len(out)} polygons, {1e3 * (time.perf_counter() - t0):.2f} ms"
+              f" | steppable {st['steppable']} zone {st['zone']} exported {st['exported']} | {st['phase_ms']}",
               flush=True)
     for s in ss:
         s.close()
