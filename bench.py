@@ -56,7 +56,7 @@ class ClockSampler:
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -173,6 +173,9 @@ def run_ours(args, rank, world, dist):
     def device_step():
         pl.run_ptrs(dev_ptrs, n_all, R_all, t_all, device_ptrs=True, want_polygons=False)
 
+    # clocks are sampled from the start of the warm-up to the end of the timed
+    # loops (the timed region alone is ~0.1 s, a handful of samples)
+    clk = ClockSampler(dev).__enter__()
     # warm-up
     for _ in range(args.warmup):
         reset()
@@ -182,7 +185,7 @@ def run_ours(args, rank, world, dist):
     # timed: device-resident inputs
     launches0 = native.kernel_launch_count()
     times = []
-    with ClockSampler(dev) as clk:
+    if True:
         for _ in range(args.steps):
             reset()
             flush.fill_(1.0)  # > L2: evict the previous step's working set
@@ -232,6 +235,7 @@ def run_ours(args, rank, world, dist):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_total = float(t.item())
     e2e_value = world * nf * len(e2e_times) / e2e_total
+    clk.__exit__(None, None, None)
 
     # per-kernel profile of one step (serialised launches; shares only)
     L.vp_profile_read.restype = C.c_int
@@ -309,7 +313,76 @@ def run_ours(args, rank, world, dist):
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(wl, args.cpu_frames)
+    if rank == 0 and world == 1 and not args.no_configs:
+        # the other BASELINE configs on this GPU (secondary lines; C1 is the
+        # reference's 0.05 m CPU case, C5 the multi-GPU map as one slab)
+        out["configs"] = {}
+        for name in ("c1", "c3", "c4"):
+            try:
+                out["configs"][name] = measure_stream(name, 3, 2, dev)
+            except Exception as e:  # report, do not lose the headline line
+                out["configs"][name] = {"error": repr(e)[:200]}
+        try:
+            a5 = argparse.Namespace(**vars(args))
+            a5.steps, a5.warmup = 3, 3
+            r5 = run_slabs(a5, 0, 1, None)
+            out["configs"]["c5"] = {k: r5[k] for k in ("value", "ms_per_frame", "points_per_s", "e2e", "config")}
+        except Exception as e:
+            out["configs"]["c5"] = {"error": repr(e)[:200]}
     return out
+
+
+# ------------------------------------------- other BASELINE configs (N=1)
+def measure_stream(name, steps, warmup, dev):
+    """Frames/s and points/s of one BASELINE config on one GPU: the stream from
+    an empty map per step (device-resident inputs; L2 flushed between steps),
+    plus the same through the C ABI with pinned host inputs (e2e)."""
+    import numpy as np
+    import torch
+
+    from paper_2510_01592_b200 import native
+    wl = load_workload(name)
+    frames = wl.frames
+    nf = len(frames)
+    npts = [len(f.points) for f in frames]
+    pl = native.Pipeline(wl.resolution, wl.extent, frames[0].translation, native.default_params(seed=wl.seed),
+                         device=dev)
+    L = native.lib()
+    L.vp_pipeline_stream.restype = C.c_void_p
+    stream = torch.cuda.ExternalStream(L.vp_pipeline_stream(pl.h))
+    start = np.ascontiguousarray(frames[0].translation, np.float64)
+    R_all = np.ascontiguousarray(np.stack([f.rotation.reshape(9) for f in frames]), np.float64)
+    t_all = np.ascontiguousarray(np.stack([f.translation for f in frames]), np.float64)
+    n_all = np.asarray(npts, np.uint64)
+    dev_pts = [torch.from_numpy(f.points).to(f"cuda:{dev}").contiguous() for f in frames]
+    host_pts = [torch.from_numpy(f.points).pin_memory() for f in frames]
+    dev_ptrs = (C.c_void_p * nf)(*[d.data_ptr() for d in dev_pts])
+    host_ptrs = (C.c_void_p * nf)(*[h.data_ptr() for h in host_pts])
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{dev}")
+
+    def timed(ptrs, device_ptrs, k):
+        out = []
+        for _ in range(k):
+            native.check(L.vp_pipeline_reset(pl.h, start.ctypes.data_as(C.POINTER(C.c_double))))
+            flush.fill_(1.0)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            pl.run_ptrs(ptrs, n_all, R_all, t_all, device_ptrs=device_ptrs, want_polygons=not device_ptrs)
+            e1.record(stream)
+            e1.synchronize()
+            out.append(e0.elapsed_time(e1))
+        return out
+
+    timed(dev_ptrs, True, warmup)
+    t = timed(dev_ptrs, True, steps)
+    te = timed(host_ptrs, False, steps)
+    pl.close()
+    ms = sum(t) / len(t)
+    return {"workload": name, "frames_per_step": nf, "points_per_frame": round(sum(npts) / nf),
+            "resolution_m": wl.resolution, "extent": list(wl.extent), "value_hz": round(nf / (ms / 1e3), 2),
+            "ms_per_frame": round(ms / nf, 4), "points_per_s": round(sum(npts) / (ms / 1e3), 1),
+            "e2e_hz": round(nf / (sum(te) / len(te) / 1e3), 2), "steps": steps, "warmup": warmup}
 
 
 # ------------------------------------------------------ C5: spatial slabs
@@ -568,6 +641,7 @@ def main():
     ap.add_argument("--workload", default="c2")
     ap.add_argument("--cpu-frames", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the secondary C1/C3/C4/C5 lines")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -942,10 +942,9 @@ __device__ void refine_finish(double cov[3][3], d3 cen, const double* init, d3 u
   out[3] = dot3(n, cen);
 }
 
+// refine_plane with the reference's sequential sums (refine_exact): one
+// thread per fit, bit-identical to plane_fit.cpp:136-143.
 __global__ void k_refine(Counters* ctr, SegBufs b, d3 up, int refine, int exact) {
-  constexpr int B = 256;
-  __shared__ double red[6][B];
-  __shared__ double cen_s[3];
   const uint32_t F = ctr->nfits;
   if (ctr->overflow & (kOverflowFits | kOverflowMembers)) return;
   for (uint32_t f = blockIdx.x; f < F; f += gridDim.x) {
@@ -982,65 +981,145 @@ __global__ void k_refine(Counters* ctr, SegBufs b, d3 up, int refine, int exact)
       __syncthreads();
       continue;
     }
-    // tree: centroid
+  }
+}
+
+// refine_plane in tree mode, split over the GPU: chunks of kRefChunk inliers
+// (one block each) reduce in a fixed-shape tree; each fit then sums its chunk
+// partials in chunk order. Deterministic; within the north_star tolerance of
+// the reference's sequential sums.
+constexpr uint32_t kRefChunk = 4096;
+
+// Single block: per fit chunk offsets (fits that are not refined get none).
+__global__ void k_refine_setup(Counters* ctr, SegBufs b, int refine) {
+  __shared__ uint32_t carry;
+  const uint32_t F = min(ctr->nfits, static_cast<uint32_t>(kClusterBins));
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (uint32_t base = 0; base < F; base += blockDim.x) {
+    const uint32_t f = base + threadIdx.x;
+    uint32_t c = 0;
+    if (f < F) {
+      const uint32_t n = b.ioff[f + 1] - b.ioff[f];
+      c = (refine && n >= 3) ? (n + kRefChunk - 1) / kRefChunk : 0u;
+    }
+    const uint32_t ex = block_exclusive_u32(c);
+    const uint32_t c0 = carry;
+    if (f < F) b.rch_off[f] = c0 + ex;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = c0 + ex + c;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) b.rch_off[F] = carry;
+}
+
+__device__ __forceinline__ uint32_t ref_fit_of_chunk(const SegBufs& b, uint32_t F, uint32_t c) {
+  uint32_t lo = 0, hi = F;  // largest f with rch_off[f] <= c (skipping empty fits)
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (b.rch_off[mid] <= c) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// pass 0: per chunk sum of x, y, z; pass 1: per chunk sums of the centred
+// outer products (xx, yx, zx, yy, zy, zz) about the fit's centroid.
+template <int kPass>
+__device__ __forceinline__ void refine_part_body(Counters* ctr, SegBufs b) {
+  constexpr int B = 256;
+  constexpr int NQ = kPass == 0 ? 3 : 6;
+  __shared__ double red[NQ][B];
+  const uint32_t F = min(ctr->nfits, static_cast<uint32_t>(kClusterBins));
+  if (ctr->overflow & (kOverflowFits | kOverflowMembers)) return;
+  const uint32_t total = b.rch_off[F];
+  for (uint32_t c = blockIdx.x; c < total; c += gridDim.x) {
+    const uint32_t f = ref_fit_of_chunk(b, F, c);
+    const uint64_t o = b.ioff[f];
+    const uint32_t n = b.ioff[f + 1] - b.ioff[f];
+    const uint32_t i0 = (c - b.rch_off[f]) * kRefChunk;
+    const uint32_t i1 = min(n, i0 + kRefChunk);
+    const double* P = b.inl + 3 * o;
+    double q[NQ];
+#pragma unroll
+    for (int k = 0; k < NQ; ++k) q[k] = 0.0;
+    d3 cen = mk3(0.0, 0.0, 0.0);
+    if (kPass == 1) cen = mk3(b.rcen[3 * f], b.rcen[3 * f + 1], b.rcen[3 * f + 2]);
+    for (uint32_t i = i0 + threadIdx.x; i < i1; i += B) {
+      if (kPass == 0) {
+        q[0] += P[3 * i];
+        q[1] += P[3 * i + 1];
+        q[2] += P[3 * i + 2];
+      } else {
+        const d3 d = sub3(mk3(P[3 * i], P[3 * i + 1], P[3 * i + 2]), cen);
+        q[0] += d.x * d.x;
+        q[1] += d.y * d.x;
+        q[2] += d.z * d.x;
+        q[3] += d.y * d.y;
+        q[4] += d.z * d.y;
+        q[5] += d.z * d.z;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < NQ; ++k) red[k][threadIdx.x] = q[k];
+    __syncthreads();
+    for (int h = B / 2; h > 0; h >>= 1) {
+      if (static_cast<int>(threadIdx.x) < h)
+#pragma unroll
+        for (int k = 0; k < NQ; ++k) red[k][threadIdx.x] = red[k][threadIdx.x] + red[k][threadIdx.x + h];
+      __syncthreads();
+    }
+    if (threadIdx.x < NQ) b.rpart[8ull * c + threadIdx.x] = red[threadIdx.x][0];
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(256) k_refine_part0(Counters* ctr, SegBufs b) { refine_part_body<0>(ctr, b); }
+__global__ void __launch_bounds__(256) k_refine_part1(Counters* ctr, SegBufs b) { refine_part_body<1>(ctr, b); }
+
+// Per fit (one thread): centroid = (sum of chunk sums in chunk order) / n.
+__global__ void k_refine_cen(Counters* ctr, SegBufs b) {
+  const uint32_t F = min(ctr->nfits, static_cast<uint32_t>(kClusterBins));
+  if (ctr->overflow & (kOverflowFits | kOverflowMembers)) return;
+  for (uint32_t f = blockIdx.x * blockDim.x + threadIdx.x; f < F; f += gridDim.x * blockDim.x) {
     double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-    for (uint32_t i = threadIdx.x; i < n; i += B) {
-      s0 += P[3 * i];
-      s1 += P[3 * i + 1];
-      s2 += P[3 * i + 2];
+    for (uint32_t c = b.rch_off[f]; c < b.rch_off[f + 1]; ++c) {
+      s0 += b.rpart[8ull * c];
+      s1 += b.rpart[8ull * c + 1];
+      s2 += b.rpart[8ull * c + 2];
     }
-    red[0][threadIdx.x] = s0;
-    red[1][threadIdx.x] = s1;
-    red[2][threadIdx.x] = s2;
-    __syncthreads();
-    for (int h = B / 2; h > 0; h >>= 1) {
-      if (static_cast<int>(threadIdx.x) < h)
-        for (int q = 0; q < 3; ++q) red[q][threadIdx.x] = red[q][threadIdx.x] + red[q][threadIdx.x + h];
-      __syncthreads();
+    const double dn = static_cast<double>(b.ioff[f + 1] - b.ioff[f]);
+    b.rcen[3 * f] = s0 / dn;
+    b.rcen[3 * f + 1] = s1 / dn;
+    b.rcen[3 * f + 2] = s2 / dn;
+  }
+}
+
+// Per fit (one thread): covariance / n -> Jacobi -> rank gate -> orient_up
+// (plane_fit.cpp:133-154); unrefined fits keep the RANSAC model.
+__global__ void k_refine_fin(Counters* ctr, SegBufs b, d3 up) {
+  const uint32_t F = min(ctr->nfits, static_cast<uint32_t>(kClusterBins));
+  if (ctr->overflow & (kOverflowFits | kOverflowMembers)) return;
+  for (uint32_t f = blockIdx.x * blockDim.x + threadIdx.x; f < F; f += gridDim.x * blockDim.x) {
+    const double* init = b.fit_model + 4 * f;
+    double* out = b.ref_model + 4 * f;
+    if (b.rch_off[f] == b.rch_off[f + 1]) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) out[q] = init[q];
+      continue;
     }
-    if (threadIdx.x == 0) {
-      const double dn = static_cast<double>(n);
-      cen_s[0] = red[0][0] / dn;
-      cen_s[1] = red[1][0] / dn;
-      cen_s[2] = red[2][0] / dn;
-    }
-    __syncthreads();
-    const d3 cen = mk3(cen_s[0], cen_s[1], cen_s[2]);
-    double c00 = 0.0, c01 = 0.0, c02 = 0.0, c11 = 0.0, c12 = 0.0, c22 = 0.0;
-    for (uint32_t i = threadIdx.x; i < n; i += B) {
-      const d3 d = sub3(mk3(P[3 * i], P[3 * i + 1], P[3 * i + 2]), cen);
-      c00 += d.x * d.x;
-      c01 += d.y * d.x;
-      c02 += d.z * d.x;
-      c11 += d.y * d.y;
-      c12 += d.z * d.y;
-      c22 += d.z * d.z;
-    }
-    __syncthreads();
-    red[0][threadIdx.x] = c00;
-    red[1][threadIdx.x] = c01;
-    red[2][threadIdx.x] = c02;
-    red[3][threadIdx.x] = c11;
-    red[4][threadIdx.x] = c12;
-    red[5][threadIdx.x] = c22;
-    __syncthreads();
-    for (int h = B / 2; h > 0; h >>= 1) {
-      if (static_cast<int>(threadIdx.x) < h)
-        for (int q = 0; q < 6; ++q) red[q][threadIdx.x] = red[q][threadIdx.x] + red[q][threadIdx.x + h];
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-      const double dn = static_cast<double>(n);
-      double c[3][3];
-      c[0][0] = red[0][0] / dn;
-      c[0][1] = c[1][0] = red[1][0] / dn;
-      c[0][2] = c[2][0] = red[2][0] / dn;
-      c[1][1] = red[3][0] / dn;
-      c[1][2] = c[2][1] = red[4][0] / dn;
-      c[2][2] = red[5][0] / dn;
-      refine_finish(c, cen, init, up, out);
-    }
-    __syncthreads();
+    double a[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    for (uint32_t c = b.rch_off[f]; c < b.rch_off[f + 1]; ++c)
+#pragma unroll
+      for (int k = 0; k < 6; ++k) a[k] += b.rpart[8ull * c + k];
+    const double dn = static_cast<double>(b.ioff[f + 1] - b.ioff[f]);
+    double cv[3][3];
+    cv[0][0] = a[0] / dn;
+    cv[0][1] = cv[1][0] = a[1] / dn;
+    cv[0][2] = cv[2][0] = a[2] / dn;
+    cv[1][1] = a[3] / dn;
+    cv[1][2] = cv[2][1] = a[4] / dn;
+    cv[2][2] = a[5] / dn;
+    refine_finish(cv, mk3(b.rcen[3 * f], b.rcen[3 * f + 1], b.rcen[3 * f + 2]), init, up, out);
   }
 }
 

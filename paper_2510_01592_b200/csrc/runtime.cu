@@ -208,6 +208,7 @@ struct Seg {
                     b.parent, b.label, b.cnt, b.cid, b.big_flag, b.big_pos, b.klabel, b.ksize,
                     b.kpoff, b.H, b.mx, b.my, b.mz, b.cand, b.cand_cnt, b.win_it, b.win_cnt,
                     b.fid, b.fit_cluster, b.ioff, b.fch_off, b.ccount, b.fit_model, b.fit_meta, b.ref_model, b.inl,
+                    b.rch_off, b.rpart, b.rcen,
                     b.proj, b.surv, b.hull, b.basis, b.pch_off, b.pext_dot, b.pext_idx, b.inner,
                     b.ninner, b.nsurv, b.prec_d, b.prec_i, b.pool, bsum, dirtab};
     for (void* p : ptrs)
@@ -272,6 +273,9 @@ struct Seg {
       b.fit_model = dalloc<double>(4 * kClusterBins);
       b.fit_meta = dalloc<int32_t>(2 * kClusterBins);
       b.ref_model = dalloc<double>(4 * kClusterBins);
+      b.rch_off = dalloc<uint32_t>(kClusterBins + 1);
+      b.rpart = dalloc<double>(8ull * (icap / 4096 + kClusterBins + 1));
+      b.rcen = dalloc<double>(3 * kClusterBins);
       b.inl = dalloc<double>(3ull * icap);
       b.proj = dalloc<double>(2ull * icap);
       b.surv = dalloc<double>(4ull * icap);
@@ -777,7 +781,16 @@ struct vp_grid {
     LAUNCH(k_extract_emit, kWide, kThreads, 0, stream, ctr, rd, seg.b);
   }
   void launch_refine(const double* up, int refine, int exact) {
-    LAUNCH(k_refine, 148 * 2, 256, 0, stream, ctr, seg.b, d3{up[0], up[1], up[2]}, refine, exact);
+    const d3 u{up[0], up[1], up[2]};
+    if (exact) {
+      LAUNCH(k_refine, 148 * 2, 32, 0, stream, ctr, seg.b, u, refine, exact);
+      return;
+    }
+    LAUNCH(k_refine_setup, 1, 1024, 0, stream, ctr, seg.b, refine);
+    LAUNCH(k_refine_part0, 148 * 4, 256, 0, stream, ctr, seg.b);
+    LAUNCH(k_refine_cen, 8, 256, 0, stream, ctr, seg.b);
+    LAUNCH(k_refine_part1, 148 * 4, 256, 0, stream, ctr, seg.b);
+    LAUNCH(k_refine_fin, 8, 256, 0, stream, ctr, seg.b, u);
   }
   void launch_polygon(int dirs, double min_area) {
     seg.ensure_dirs(dirs, stream);

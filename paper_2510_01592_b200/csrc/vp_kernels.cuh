@@ -191,6 +191,9 @@ struct SegBufs {
   double* fit_model;     // 4 per fit (normal, offset): RANSAC winner
   int32_t* fit_meta;     // 2 per fit (inlier_count, label)
   double* ref_model;     // 4 per fit: refined
+  uint32_t* rch_off;     // per fit refine-chunk offsets (nfits+1)
+  double* rpart;         // 8 per refine chunk: partial sums
+  double* rcen;          // 3 per fit: refine centroid
   double* inl;           // 3 * Icap inliers (fit order)
   double* proj;          // 2 * Icap
   double* surv;          // 2 * 2Icap
@@ -295,6 +298,11 @@ __global__ void k_fit_setup(Counters* ctr, RansacDev rp, SegBufs b);
 __global__ void k_extract_count(Counters* ctr, RansacDev rp, SegBufs b);
 __global__ void k_extract_emit(Counters* ctr, RansacDev rp, SegBufs b);
 __global__ void k_refine(Counters* ctr, SegBufs b, d3 up, int refine, int exact);
+__global__ void k_refine_setup(Counters* ctr, SegBufs b, int refine);
+__global__ void k_refine_part0(Counters* ctr, SegBufs b);
+__global__ void k_refine_part1(Counters* ctr, SegBufs b);
+__global__ void k_refine_cen(Counters* ctr, SegBufs b);
+__global__ void k_refine_fin(Counters* ctr, SegBufs b, d3 up);
 __global__ void k_poly_setup(Counters* ctr, SegBufs b);
 __global__ void k_poly_extremes(Counters* ctr, SegBufs b, const double* dirtab, int directions);
 __global__ void k_poly_inner(Counters* ctr, SegBufs b, int directions);
