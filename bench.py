@@ -15,9 +15,16 @@ inside) and the final polygons read back.
 the unmodified /root/reference sources) on the host cores over a bounded
 sample of the same stream.
 
-N > 1: the path is a per-robot map; without slab decomposition (SURVEY §8(e),
-not built yet) ranks run independent replicas of the stream (weak scaling, no
+N > 1 (default C2): the path is a per-robot map whose 5 m window needs no
+slabbing, so ranks run independent replicas of the stream (weak scaling, no
 data-path collective); only the timing barrier / max use torch.distributed.
+--workload c5 runs BASELINE configs[4], one 2000x2000x300 window split into
+x-slabs across the ranks (paper_2510_01592_b200/slabs.py: halo
+planes, halo steppable lists, boundary-label merge, cluster gather to the
+owning slab, all over NCCL; strong scaling).
+
+At N = 1 the line also carries secondary `configs` (C1, C3, C4 and C5 as one
+slab) measured the same way.
 """
 from __future__ import annotations
 

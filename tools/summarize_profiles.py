@@ -11,6 +11,7 @@ import sys
 from collections import defaultdict
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+LAUNCH_CMD = os.environ.get("LAUNCH_CMD", "python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-configs (C2)")
 
 
 def launches(path):
@@ -68,7 +69,7 @@ def main(tag):
     tot = sum(v[0] for v in agg.values())
     with open(os.path.join(dst, f"{tag}_kernel_shares.txt"), "w") as f:
         f.write(f"# ncu launch list (gpu__time_duration.sum, --clock-control none, serialised, cold): "
-                f"tools/frames_driver.py --frames 12 on C2; {sum(v[1] for v in agg.values())} launches\n")
+                f"{LAUNCH_CMD}; {sum(v[1] for v in agg.values())} launches\n")
         f.write(f"{'kernel':28s} {'launches':>8s} {'total_us':>10s} {'us/launch':>10s} {'share':>7s}\n")
         for k, (t, n) in sorted(agg.items(), key=lambda kv: -kv[1][0]):
             f.write(f"{k:28s} {n:8d} {t / 1e3:10.1f} {t / 1e3 / n:10.2f} {100 * t / tot:6.1f}%\n")
