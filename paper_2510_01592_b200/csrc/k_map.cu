@@ -122,7 +122,6 @@ __global__ void k_integrate_scatter(const FrameParams* __restrict__ fp, const ui
 // ranked (indices are distinct, so rank = number of smaller indices), the
 // points are transformed in parallel, and lane 0 performs the reference's
 // sequential FP64 fold (voxel_grid.cpp:104-110) in ascending point index.
-constexpr int kFoldMax = 128;
 constexpr int kFoldWarps = 8;
 
 __device__ __forceinline__ void fold_cell(const GridDesc& g, const FrameParams* fp, uint32_t key,
@@ -153,7 +152,8 @@ __device__ __forceinline__ void fold_cell(const GridDesc& g, const FrameParams* 
 __global__ void __launch_bounds__(256) k_integrate_fold(GridDesc g, const FrameParams* __restrict__ fp,
                                                         Counters* ctr, const uint32_t* groups,
                                                         uint32_t* hkey, uint32_t* hcnt,
-                                                        const uint32_t* hoff, uint32_t* sorted) {
+                                                        const uint32_t* hoff, uint32_t* sorted,
+                                                        uint32_t* dense) {
   __shared__ uint32_t raw[kFoldWarps][kFoldMax];
   __shared__ uint32_t srt[kFoldMax * kFoldWarps];
   __shared__ d3 sw[kFoldWarps][kFoldMax];
@@ -185,40 +185,9 @@ __global__ void __launch_bounds__(256) k_integrate_fold(GridDesc g, const FrameP
       __syncwarp();
       if (lane == 0) fold_cell(g, fp, key, sw[wid], cnt, fresh);
       __syncwarp();
-    } else if (lane == 0) {  // rare very dense voxel: in-place sort + streamed fold
-      for (uint32_t a = 1; a < cnt; ++a) {
-        const uint32_t v = lst[a];
-        uint32_t q = a;
-        while (q > 0 && lst[q - 1] > v) {
-          lst[q] = lst[q - 1];
-          --q;
-        }
-        lst[q] = v;
-      }
-      const uint32_t z = key % static_cast<uint32_t>(g.ez);
-      const uint32_t r = key / static_cast<uint32_t>(g.ez);
-      const uint32_t y = r % static_cast<uint32_t>(g.ey);
-      const uint32_t x = r / static_cast<uint32_t>(g.ey);
-      Cell* c = g.cells + phys_index(g, fp->off_pre, x, y, z);
-      double sx = c->sx, sy = c->sy, sz = c->sz;
-      const uint32_t count = c->count;
-      for (uint32_t a = 0; a < cnt; ++a) {
-        const float* p = fp->pts + 3 * static_cast<uint64_t>(lst[a]);
-        const d3 w = pose_apply(fp->R, fp->t, static_cast<double>(p[0]), static_cast<double>(p[1]),
-                                static_cast<double>(p[2]));
-        sx += w.x;
-        sy += w.y;
-        sz += w.z;
-      }
-      c->sx = sx;
-      c->sy = sy;
-      c->sz = sz;
-      c->count = count + cnt;
-      c->status = 1;
-      if (count == 0) {
-        atomicOr(fp->occ_pre + word_of(g, x, y, z), 1u << (z & 31));
-        ++fresh;
-      }
+    } else {  // dense voxel: k_integrate_fold_dense (block per voxel)
+      if (lane == 0) dense[atomicAdd(&ctr->ndense, 1u)] = slot;
+      continue;
     }
     if (lane == 0) {
       hkey[slot] = kEmptyKey;
@@ -226,6 +195,126 @@ __global__ void __launch_bounds__(256) k_integrate_fold(GridDesc g, const FrameP
     }
   }
   warp_add_u64(&ctr->newly, fresh);
+}
+
+// Voxels with more than kFoldMax points (coarse grids, points next to the
+// sensor): one block per voxel. Up to kDenseSort indices are bitonic-sorted
+// in shared memory; larger groups are gathered in index order by streaming
+// the whole frame's point->slot table (no sort, any size). The points are
+// transformed by the block 1024 at a time and thread 0 folds them in
+// ascending index (voxel_grid.cpp:104-110), bit-exact.
+__global__ void __launch_bounds__(1024) k_integrate_fold_dense(GridDesc g, const FrameParams* __restrict__ fp,
+                                                               Counters* ctr, uint32_t* hkey, uint32_t* hcnt,
+                                                               const uint32_t* hoff, const uint32_t* sorted,
+                                                               const uint32_t* pslot, const uint32_t* dense) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  d3* w = reinterpret_cast<d3*>(smem);                          // 1024 transformed points
+  uint32_t* keys = reinterpret_cast<uint32_t*>(smem + 1024 * sizeof(d3));  // kDenseSort indices
+  __shared__ uint32_t wcount[32];
+  __shared__ uint32_t run_base;
+  const uint32_t nd = ctr->ndense;
+  const uint32_t t = threadIdx.x;
+  for (uint32_t di = blockIdx.x; di < nd; di += gridDim.x) {
+    const uint32_t slot = dense[di];
+    const uint32_t key = hkey[slot];
+    const uint32_t cnt = hcnt[slot];
+    const uint32_t z = key % static_cast<uint32_t>(g.ez);
+    const uint32_t r = key / static_cast<uint32_t>(g.ez);
+    const uint32_t y = r % static_cast<uint32_t>(g.ey);
+    const uint32_t x = r / static_cast<uint32_t>(g.ey);
+    Cell* c = g.cells + phys_index(g, fp->off_pre, x, y, z);
+    double sx = 0.0, sy = 0.0, sz = 0.0;
+    uint32_t count = 0;
+    if (t == 0) {
+      sx = c->sx;
+      sy = c->sy;
+      sz = c->sz;
+      count = c->count;
+    }
+    if (cnt <= kDenseSort) {
+      uint32_t np = 1;
+      while (np < cnt) np <<= 1;
+      const uint32_t* lst = sorted + hoff[slot];
+      for (uint32_t k = t; k < np; k += blockDim.x) keys[k] = k < cnt ? lst[k] : 0xffffffffu;
+      __syncthreads();
+      for (uint32_t q = 2; q <= np; q <<= 1)
+        for (uint32_t j = q >> 1; j > 0; j >>= 1) {
+          for (uint32_t i = t; i < np; i += blockDim.x) {
+            const uint32_t l = i ^ j;
+            if (l > i) {
+              const uint32_t a = keys[i], b = keys[l];
+              if (((i & q) == 0) ? (a > b) : (a < b)) {
+                keys[i] = b;
+                keys[l] = a;
+              }
+            }
+          }
+          __syncthreads();
+        }
+      for (uint32_t c0 = 0; c0 < cnt; c0 += 1024) {
+        const uint32_t m = min(1024u, cnt - c0);
+        if (t < m) {
+          const float* p = fp->pts + 3 * static_cast<uint64_t>(keys[c0 + t]);
+          w[t] = pose_apply(fp->R, fp->t, static_cast<double>(p[0]), static_cast<double>(p[1]),
+                            static_cast<double>(p[2]));
+        }
+        __syncthreads();
+        if (t == 0)
+          for (uint32_t a = 0; a < m; ++a) {
+            sx += w[a].x;
+            sy += w[a].y;
+            sz += w[a].z;
+          }
+        __syncthreads();
+      }
+    } else {
+      // stream the frame in index order; keep the points of this slot
+      const uint64_t n = fp->n;
+      if (t == 0) run_base = 0;
+      __syncthreads();
+      for (uint64_t i0 = 0; i0 < n; i0 += 1024) {
+        const uint64_t i = i0 + t;
+        const bool mine = i < n && pslot[i] == slot;
+        const unsigned bal = __ballot_sync(0xffffffffu, mine);
+        if ((t & 31) == 0) wcount[t >> 5] = __popc(bal);
+        __syncthreads();
+        uint32_t before = run_base;
+        for (uint32_t q = 0; q < (t >> 5); ++q) before += wcount[q];
+        if (mine) {
+          const float* p = fp->pts + 3 * i;
+          w[before - run_base + __popc(bal & lanemask_lt())] =
+              pose_apply(fp->R, fp->t, static_cast<double>(p[0]), static_cast<double>(p[1]),
+                         static_cast<double>(p[2]));
+        }
+        __syncthreads();
+        if (t == 0) {
+          uint32_t m = 0;
+          for (uint32_t q = 0; q < 32; ++q) m += wcount[q];
+          for (uint32_t a = 0; a < m; ++a) {
+            sx += w[a].x;
+            sy += w[a].y;
+            sz += w[a].z;
+          }
+          run_base += m;
+        }
+        __syncthreads();
+      }
+    }
+    if (t == 0) {
+      c->sx = sx;
+      c->sy = sy;
+      c->sz = sz;
+      c->count = count + cnt;
+      c->status = 1;
+      if (count == 0) {
+        atomicOr(fp->occ_pre + word_of(g, x, y, z), 1u << (z & 31));
+        atomicAdd(&ctr->newly, 1ull);
+      }
+      hkey[slot] = kEmptyKey;
+      hcnt[slot] = 0;
+    }
+    __syncthreads();
+  }
 }
 
 // ---------------------------------------------------------------------------

@@ -413,6 +413,7 @@ struct vp_grid {
   uint32_t* pslot = nullptr;
   uint32_t* prank = nullptr;
   uint32_t* sorted = nullptr;
+  uint32_t* dense = nullptr;  // slots of integrate groups > kFoldMax points
   Seg seg;
   cudaEvent_t ev[8];
   // window-sized ordinal map for segmenting a gathered slab steppable list
@@ -445,7 +446,7 @@ struct vp_grid {
     }
     if (occ_total) cudaFree(occ_total);
     for (void* p : {(void*)hkey, (void*)hcnt, (void*)hoff, (void*)groups,
-                    (void*)pslot, (void*)prank, (void*)sorted})
+                    (void*)pslot, (void*)prank, (void*)sorted, (void*)dense})
       if (p) cudaFree(p);
     for (auto& e : ev) if (e) cudaEventDestroy(e);
     if (stream) cudaStreamDestroy(stream);
@@ -508,6 +509,8 @@ struct vp_grid {
     seg.ensure(vcap, vcap, vcap, 100, gd.nwords);
     ck(cudaFuncSetAttribute(k_poly_hull, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             kHullSmem * 16 * 6), "smem attr");
+    ck(cudaFuncSetAttribute(k_integrate_fold_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, kDenseSmem),
+       "smem attr");
     ck(cudaStreamSynchronize(stream), "init sync");
   }
 
@@ -585,7 +588,7 @@ struct vp_grid {
     cap = std::max<uint64_t>(cap, pcap * 2);
     ck(cudaDeviceSynchronize(), "sync before realloc");
     for (void* p : {(void*)d_pts_s[0], (void*)d_pts_s[1], (void*)hkey, (void*)hcnt, (void*)hoff,
-                    (void*)groups, (void*)pslot, (void*)prank, (void*)sorted})
+                    (void*)groups, (void*)pslot, (void*)prank, (void*)sorted, (void*)dense})
       if (p) cudaFree(p);
     uint64_t hs = 1;
     while (hs < 2 * cap) hs <<= 1;
@@ -599,6 +602,7 @@ struct vp_grid {
     pslot = dalloc<uint32_t>(cap);
     prank = dalloc<uint32_t>(cap);
     sorted = dalloc<uint32_t>(cap);
+    dense = dalloc<uint32_t>(cap / (kFoldMax + 1) + 1);
     ck(cudaMemsetAsync(hkey, 0xff, hs * 4, stream), "hkey");
     ck(cudaMemsetAsync(hcnt, 0, hs * 4, stream), "hcnt");
     hmask = static_cast<uint32_t>(hs - 1);
@@ -686,7 +690,9 @@ struct vp_grid {
     LAUNCH(k_integrate_offsets, gp, kThreads, 0, lstream, ctr, groups, hcnt, hoff);
     LAUNCH(k_integrate_scatter, gp, kThreads, 0, lstream, d_fp, pslot, prank, hoff, sorted);
     LAUNCH(k_integrate_fold, gp, kThreads, 0, lstream, gd, d_fp, ctr, groups, hkey, hcnt, hoff,
-           sorted);
+           sorted, dense);
+    LAUNCH(k_integrate_fold_dense, 148, 1024, kDenseSmem, lstream, gd, d_fp, ctr, hkey, hcnt, hoff, sorted,
+           pslot, dense);
   }
   void launch_recenter() {
     LAUNCH(k_recenter, grid_for(gd.nwords), kThreads, 0, lstream, gd, d_fp, ctr);

@@ -86,6 +86,7 @@ struct Counters {
   uint32_t fit_chunks;
   uint32_t surv_max;     // largest hull-survivor set of the frame (diagnostic)
   int32_t ccl_giant;     // root of the sampled largest component after the lattice links
+  uint32_t ndense;       // integrate groups with more than kFoldMax points (k_integrate_fold_dense)
 };
 
 constexpr uint32_t kOverflowOcc = 1u;

@@ -14,6 +14,8 @@ constexpr int kClusterBins = 2048;  // clusters handled by the counting sort per
 constexpr int kChunk = 256;         // ordinals per counting-sort chunk (one warp)
 constexpr int kHullSmem = 512;      // survivors sorted in shared memory (6 regions of this size)
 constexpr int kPolyChunk = 1024;    // inlier points per polygon-stage block
+constexpr int kFoldMax = 128;       // integrate: points per voxel folded by one warp
+constexpr uint32_t kDenseSort = 16384;  // denser voxels: indices bitonic-sorted in shared memory
 
 // Block-wide exclusive prefix sum (any blockDim multiple of 32, <= 1024).
 __device__ __forceinline__ uint32_t block_exclusive_u32(uint32_t v) {
@@ -248,7 +250,11 @@ __global__ void k_integrate_scatter(const FrameParams* fp, const uint32_t* pslot
                                     const uint32_t* prank, const uint32_t* hoff, uint32_t* sorted);
 __global__ void k_integrate_fold(GridDesc g, const FrameParams* fp, Counters* ctr,
                                  const uint32_t* groups, uint32_t* hkey, uint32_t* hcnt,
-                                 const uint32_t* hoff, uint32_t* sorted);
+                                 const uint32_t* hoff, uint32_t* sorted, uint32_t* dense);
+__global__ void k_integrate_fold_dense(GridDesc g, const FrameParams* fp, Counters* ctr, uint32_t* hkey,
+                                       uint32_t* hcnt, const uint32_t* hoff, const uint32_t* sorted,
+                                       const uint32_t* pslot, const uint32_t* dense);
+constexpr int kDenseSmem = 1024 * 24 + 16384 * 4;  // k_integrate_fold_dense dynamic shared memory
 __global__ void k_clear_walk(GridDesc g, const FrameParams* fp);
 __global__ void k_clear_walk_slab(GridDesc g, const FrameParams* fp);
 __global__ void k_clear_apply(GridDesc g, const FrameParams* fp, Counters* ctr);

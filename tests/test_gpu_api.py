@@ -81,6 +81,34 @@ def test_random_rays_match_oracle_grid_state():
         assert a == b, f"frame {k}"
 
 
+@pytest.mark.parametrize("dense", [3000, 20000])
+def test_dense_voxels_fold_in_index_order(dense):
+    # voxels with > 128 points (k_integrate_fold_dense: shared-memory sort up to
+    # 16384 points, ordered stream beyond) must fold in ascending point index
+    rng = np.random.default_rng(dense)
+    parts = [rng.uniform(0.25, 0.30, (dense, 3)), rng.uniform([0.10, 0.15, 0.20], [0.15, 0.20, 0.25], (700, 3)),
+             rng.uniform(0.35, 0.40, (150, 3)), rng.uniform(0.0, 0.5, (60, 3))]
+    pts = np.concatenate(parts).astype(np.float32)
+    pts = pts[rng.permutation(len(pts))]
+    p = native.default_params()
+    g = native.Pipeline(0.05, (10, 10, 10), (0.25, 0.25, 0.25), p)
+    o = CpuSession("oracle", 0.05, (10, 10, 10), (0.25, 0.25, 0.25), p)
+    t = np.array([0.26, 0.27, 0.28])
+    for k in range(2):
+        assert g.frame_trace_raw(pts, I3, t) == o.frame_raw(pts, I3, t), f"frame {k}"
+
+
+def test_c1_frame_bit_exact():
+    # BASELINE configs[0]: Stair5 640x480 at 0.05 m (~160 points per voxel)
+    from paper_2510_01592_b200 import scenes
+    wl = scenes.workload("c1")
+    f = wl.frames[0]
+    p = native.default_params(seed=wl.seed, refine_exact=True)
+    g = native.Pipeline(wl.resolution, wl.extent, f.translation, p)
+    o = CpuSession("oracle", wl.resolution, wl.extent, f.translation, p)
+    assert g.frame_trace_raw(f.points, f.rotation, f.translation) == o.frame_raw(f.points, f.rotation, f.translation)
+
+
 def test_recenter_shift_and_drop():
     # test_voxel_grid.cpp:225-237: shift (3,0,0) moves cell (10,5,5) to (7,5,5)
     g = small_grid()
