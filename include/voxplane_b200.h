@@ -353,6 +353,40 @@ int vp_pipeline_frame_trace(vp_pipeline* pl, const float* xyz, uint64_t n,
                             const double rotation[9], const double translation[3],
                             uint8_t** buf, uint64_t* len);
 
+/* ---- cluster-parallel ablation (pipeline.cpp:304-381, Fig. 9) -------------
+   Per trial (trial-major, alternating mode order as the reference): M drawn
+   from CounterRng(seed, count, trial) in [points_min, points_max], `count`
+   clusters of exactly M synthetic points (the reference's generator, bit for
+   bit, on the host), staged on the device, then fit_planes timed with CUDA
+   events in both RansacExecution modes; the two modes' fits must be
+   bitwise identical (checked every measurement; VP_ECUDA otherwise). Rows:
+   10 % trimmed means and medians over trials. */
+typedef struct {
+  const int32_t* cluster_counts;
+  int32_t n_counts;
+  int32_t trials;
+  int32_t points_min, points_max;
+  uint64_t seed;
+  int32_t iterations;
+  double inlier_eps;
+  int32_t device;
+} vp_ablation_config;
+typedef struct {
+  int32_t clusters, trials;
+  double parallel_ms, serial_ms, parallel_median_ms, serial_median_ms;
+} vp_ablation_row;
+/* AblationConfig defaults (pipeline.hpp:65-74): counts {1,2,4,8,16} need the
+   caller's array; trials 1000, M in [10000, 30000], seed 1234, 100
+   iterations, eps 0.01. */
+void vp_default_ablation_config(vp_ablation_config* c);
+int vp_run_ablation(const vp_ablation_config* c, vp_ablation_row* rows);
+/* The synthetic clusters of one (trial, count): *m points per cluster,
+   points = count * m * 3 doubles (host, free with vp_free). */
+int vp_ablation_clusters(const vp_ablation_config* c, int32_t trial, int32_t count, int32_t* m,
+                         double** points);
+/* write_ablation_csv (pipeline.cpp:383-396). */
+int vp_write_ablation_csv(const char* path, const vp_ablation_row* rows, size_t n);
+
 /* label_components algorithm (identical labels): 0 = min-neighbour hooking +
    forward-window unions (default), 1 = neighbour-sampling unions + whole-window
    unions outside the sampled giant component, 2 = hooking + the same giant

@@ -15,6 +15,7 @@
 #include <new>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "voxplane_b200.h"
@@ -368,6 +369,24 @@ struct SlabSeg {
   }
 };
 
+// Per-cluster views for fit_planes' PerClusterSerial execution mode
+// (plane_fit.cpp:113-119): cluster c runs the same kernels alone with its own
+// counters, a [0, padded) member offset pair and private output slots.
+struct SerialFitBufs {
+  uint32_t cap = 0;
+  uint32_t* kp1 = nullptr;     // 2 per cluster: 0, padded size
+  Counters* ctrs = nullptr;    // 1 per cluster (K = 1)
+  double* fm = nullptr;        // 4 per cluster: winning model
+  int32_t* fmeta = nullptr;    // 2 per cluster: inlier_count, label
+  uint32_t* io1 = nullptr;     // 2 per cluster: inlier offsets
+  void release() {
+    void* ptrs[] = {kp1, ctrs, fm, fmeta, io1};
+    for (void* q : ptrs)
+      if (q) cudaFree(q);
+    *this = SerialFitBufs{};
+  }
+};
+
 // Host image of the per-fit records written by k_polygon.
 struct HostPolys {
   std::vector<vp_polygon> polys;
@@ -421,6 +440,8 @@ struct vp_grid {
   uint32_t* gbits = nullptr;
   // distributed segmentation of a slab (vp_slab_extend .. vp_slab_segment_owned)
   SlabSeg sl;
+  // fit_planes PerClusterSerial views (vp_fit_planes, vp_run_ablation)
+  SerialFitBufs sf;
   // CUDA graph of one pipeline frame (see pipeline_enqueue)
   bool capturing = false;
   uint64_t gen = 1;  // bumped whenever a buffer the graph references is reallocated
@@ -436,6 +457,7 @@ struct vp_grid {
     if (gmap) cudaFree(gmap);
     if (gbits) cudaFree(gbits);
     sl.release();
+    sf.release();
     if (mstream) cudaStreamSynchronize(mstream);
     for (int q = 0; q < 2; ++q) {
       if (ctr_s[q]) cudaFree(ctr_s[q]);
@@ -777,14 +799,18 @@ struct vp_grid {
     LAUNCH(k_member_hscan, kWide, kThreads, 0, stream, ctr, seg.b, seg.hstride);
     LAUNCH(k_member_scatter, std::min(nch, 148 * 16), 32, 0, stream, ctr, seg.b, seg.hstride);
   }
-  void launch_ransac(const RansacDev& rd) {
-    LAUNCH(k_ransac_hyp, kWide, kThreads, 0, stream, ctr, rd, seg.b);
-    LAUNCH(k_ransac_count, kWide, kThreads, 0, stream, ctr, rd, seg.b);
-    LAUNCH(k_ransac_select, kWide, kThreads, 0, stream, ctr, rd, seg.b);
-    LAUNCH(k_fit_setup, 1, 1024, 0, stream, ctr, rd, seg.b);
-    LAUNCH(k_extract_count, kWide, kThreads, 0, stream, ctr, rd, seg.b);
-    LAUNCH(k_scan_exclusive, 1, 1024, 0, stream, seg.b.ccount, 0u, &ctr->fit_chunks, nullptr, nullptr);
-    LAUNCH(k_extract_emit, kWide, kThreads, 0, stream, ctr, rd, seg.b);
+  void launch_ransac(const RansacDev& rd) { launch_ransac(rd, ctr, seg.b); }
+  // fit_planes on the clusters described by b (counters c): the same kernels
+  // serve the cluster-parallel pass and, with single-cluster views, the
+  // per-cluster-serial execution mode (plane_fit.cpp:107-119)
+  void launch_ransac(const RansacDev& rd, Counters* c, const SegBufs& b) {
+    LAUNCH(k_ransac_hyp, kWide, kThreads, 0, stream, c, rd, b);
+    LAUNCH(k_ransac_count, kWide, kThreads, 0, stream, c, rd, b);
+    LAUNCH(k_ransac_select, kWide, kThreads, 0, stream, c, rd, b);
+    LAUNCH(k_fit_setup, 1, 1024, 0, stream, c, rd, b);
+    LAUNCH(k_extract_count, kWide, kThreads, 0, stream, c, rd, b);
+    LAUNCH(k_scan_exclusive, 1, 1024, 0, stream, b.ccount, 0u, &c->fit_chunks, nullptr, nullptr);
+    LAUNCH(k_extract_emit, kWide, kThreads, 0, stream, c, rd, b);
   }
   void launch_refine(const double* up, int refine, int exact) {
     const d3 u{up[0], up[1], up[2]};
@@ -1759,6 +1785,236 @@ void upload_steppable(vp_grid* g, const vp_steppable_t* s, BoxMap& bm) {
   set_counter_u32(g, offsetof(Counters, S), S);
   LAUNCH(k_map_fill, kWide, kThreads, 0, g->stream, g->ctr, g->seg.b, bm.m);
 }
+
+// ---- fit_planes on host-provided clusters (vp_fit_planes, vp_run_ablation)
+struct FitResult {
+  std::vector<vp_plane> models;
+  std::vector<uint64_t> offsets{0};
+  std::vector<double> inliers;
+  uint64_t skipped = 0, unfit = 0;
+};
+
+void append_fits(FitResult& all, const FitResult& r) {
+  const uint64_t base = all.offsets.back();
+  all.models.insert(all.models.end(), r.models.begin(), r.models.end());
+  for (size_t i = 1; i < r.offsets.size(); ++i) all.offsets.push_back(base + r.offsets[i]);
+  all.inliers.insert(all.inliers.end(), r.inliers.begin(), r.inliers.end());
+  all.skipped += r.skipped;
+  all.unfit += r.unfit;
+}
+
+// Stage K clusters (sizes, labels, contiguous member means) in the
+// cluster-parallel layout (warp-padded SoA) and set the counters; returns kpoff.
+std::vector<uint32_t> stage_clusters(vp_grid* g, uint32_t K, const int32_t* labels, const uint32_t* ksize,
+                                     const double* means, int iterations) {
+  std::vector<uint32_t> kpoff(K + 1, 0);
+  uint64_t tot = 0, maxm = 0;
+  for (uint32_t k = 0; k < K; ++k) {
+    kpoff[k] = static_cast<uint32_t>(tot);
+    tot += (ksize[k] + 31u) & ~31u;
+    maxm += ksize[k];
+  }
+  kpoff[K] = static_cast<uint32_t>(tot);
+  const uint32_t need = static_cast<uint32_t>(std::max<uint64_t>(tot, maxm));
+  // inliers: [0, tot) for the cluster-parallel pass, [tot, 2 tot) for the serial views
+  g->seg.ensure(g->seg.b.Vcap, std::max(g->seg.b.Scap, need), std::max(g->seg.b.Icap, 2 * need),
+                std::max(iterations, 1), g->gd.nwords);
+  std::vector<double> mx(tot, 0.0), my(tot, 0.0), mz(tot, 0.0);
+  uint64_t src = 0;
+  for (uint32_t k = 0; k < K; ++k)
+    for (uint32_t j = 0; j < ksize[k]; ++j, ++src) {
+      mx[kpoff[k] + j] = means[3 * src];
+      my[kpoff[k] + j] = means[3 * src + 1];
+      mz[kpoff[k] + j] = means[3 * src + 2];
+    }
+  h2d(g->seg.b.klabel, labels, K, g->stream);
+  h2d(g->seg.b.ksize, ksize, K, g->stream);
+  h2d(g->seg.b.kpoff, kpoff.data(), K + 1, g->stream);
+  h2d(g->seg.b.mx, mx.data(), tot, g->stream);
+  h2d(g->seg.b.my, my.data(), tot, g->stream);
+  h2d(g->seg.b.mz, mz.data(), tot, g->stream);
+  g->reset_frame_counters();
+  set_counter_u32(g, offsetof(Counters, K), K);
+  return kpoff;
+}
+
+void serial_prepare(vp_grid* g, const std::vector<uint32_t>& ksize, const std::vector<uint32_t>& kpoff) {
+  SerialFitBufs& sf = g->sf;
+  const uint32_t K = static_cast<uint32_t>(ksize.size());
+  if (K > sf.cap) {
+    sf.release();
+    sf.cap = std::max<uint32_t>(K, 64);
+    sf.kp1 = dalloc<uint32_t>(2ull * sf.cap);
+    sf.ctrs = dalloc<Counters>(sf.cap);
+    sf.fm = dalloc<double>(4ull * sf.cap);
+    sf.fmeta = dalloc<int32_t>(2ull * sf.cap);
+    sf.io1 = dalloc<uint32_t>(2ull * sf.cap);
+  }
+  std::vector<uint32_t> kp1(2ull * K);
+  std::vector<Counters> c(K);
+  std::memset(c.data(), 0, K * sizeof(Counters));
+  for (uint32_t k = 0; k < K; ++k) {
+    kp1[2 * k] = 0;
+    kp1[2 * k + 1] = kpoff[k + 1] - kpoff[k];
+    c[k].K = 1;
+  }
+  h2d(sf.kp1, kp1.data(), kp1.size(), g->stream);
+  h2d(sf.ctrs, c.data(), K, g->stream);
+  ck(cudaStreamSynchronize(g->stream), "sync");
+}
+
+void serial_launch(vp_grid* g, const RansacDev& rd, const std::vector<uint32_t>& kpoff) {
+  SerialFitBufs& sf = g->sf;
+  const uint32_t K = static_cast<uint32_t>(kpoff.size() - 1);
+  for (uint32_t k = 0; k < K; ++k) {
+    SegBufs v = g->seg.b;
+    v.klabel += k;
+    v.ksize += k;
+    v.kpoff = sf.kp1 + 2 * k;
+    v.mx += kpoff[k];
+    v.my += kpoff[k];
+    v.mz += kpoff[k];
+    v.fit_model = sf.fm + 4 * k;
+    v.fit_meta = sf.fmeta + 2 * k;
+    v.ioff = sf.io1 + 2 * k;
+    v.inl = g->seg.b.inl + 3ull * (kpoff[K] + kpoff[k]);
+    v.Icap = kpoff[k + 1] - kpoff[k];
+    g->launch_ransac(rd, sf.ctrs + k, v);
+  }
+}
+
+FitResult parallel_results(vp_grid* g) {
+  g->read_counters();
+  FitResult r;
+  const uint32_t F = g->h_ctr->nfits;
+  r.skipped = g->h_ctr->skipped;
+  r.unfit = g->h_ctr->unfit;
+  if (g->h_ctr->overflow) fail(VP_ENOMEM, "fit_planes: capacity overflow");
+  auto fm = d2h(g->seg.b.fit_model, 4ull * F, g->stream);
+  auto meta = d2h(g->seg.b.fit_meta, 2ull * F, g->stream);
+  auto io = d2h(g->seg.b.ioff, F + 1ull, g->stream);
+  ck(cudaStreamSynchronize(g->stream), "sync");
+  r.inliers = d2h(g->seg.b.inl, 3ull * io[F], g->stream);
+  ck(cudaStreamSynchronize(g->stream), "sync");
+  for (uint32_t f = 0; f < F; ++f) {
+    vp_plane pl{};
+    for (int q = 0; q < 3; ++q) pl.normal[q] = fm[4 * f + q];
+    pl.offset = fm[4 * f + 3];
+    pl.inlier_count = meta[2 * f];
+    pl.cluster_label = meta[2 * f + 1];
+    r.models.push_back(pl);
+    r.offsets.push_back(io[f + 1]);
+  }
+  return r;
+}
+
+FitResult serial_results(vp_grid* g, const std::vector<uint32_t>& ksize, const std::vector<uint32_t>& kpoff) {
+  SerialFitBufs& sf = g->sf;
+  const uint32_t K = static_cast<uint32_t>(ksize.size());
+  auto c = d2h(sf.ctrs, K, g->stream);
+  auto fm = d2h(sf.fm, 4ull * K, g->stream);
+  auto meta = d2h(sf.fmeta, 2ull * K, g->stream);
+  auto io = d2h(sf.io1, 2ull * K, g->stream);
+  ck(cudaStreamSynchronize(g->stream), "sync");
+  FitResult r;
+  for (uint32_t k = 0; k < K; ++k) {
+    if (c[k].overflow) fail(VP_ENOMEM, "fit_planes: capacity overflow");
+    r.skipped += c[k].skipped;
+    r.unfit += c[k].unfit;
+    if (c[k].nfits == 0) continue;
+    vp_plane pl{};
+    for (int q = 0; q < 3; ++q) pl.normal[q] = fm[4 * k + q];
+    pl.offset = fm[4 * k + 3];
+    pl.inlier_count = meta[2 * k];
+    pl.cluster_label = meta[2 * k + 1];
+    r.models.push_back(pl);
+    const uint32_t n = io[2 * k + 1];
+    auto in = d2h(g->seg.b.inl + 3ull * (kpoff[K] + kpoff[k]), 3ull * n, g->stream);
+    ck(cudaStreamSynchronize(g->stream), "sync");
+    r.inliers.insert(r.inliers.end(), in.begin(), in.end());
+    r.offsets.push_back(r.offsets.back() + n);
+  }
+  return r;
+}
+
+bool same_fits(const FitResult& a, const FitResult& b) {
+  return a.models.size() == b.models.size() && a.offsets == b.offsets && a.skipped == b.skipped &&
+         a.unfit == b.unfit && std::memcmp(a.models.data(), b.models.data(), a.models.size() * sizeof(vp_plane)) == 0 &&
+         a.inliers.size() == b.inliers.size() &&
+         std::memcmp(a.inliers.data(), b.inliers.data(), a.inliers.size() * 8) == 0;
+}
+
+// ---- Fig.-9 ablation (pipeline.cpp:304-381) --------------------------------
+// CounterRng (rng.hpp:13-64) on the host: the reference's synthetic clusters
+// bit for bit (std::log / std::sin / std::cos as in the reference build).
+struct HostRng {
+  uint64_t st;
+  double cached = 0.0;
+  bool has = false;
+  static uint64_t mix(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+  }
+  HostRng(uint64_t seed, uint64_t k1, uint64_t k2) {
+    st = mix(seed + 0x9e3779b97f4a7c15ULL);
+    st = mix(st ^ mix(k1 + 0xbf58476d1ce4e5b9ULL));
+    st = mix(st ^ mix(k2 + 0x94d049bb133111ebULL));
+  }
+  uint64_t next() {
+    st += 0x9e3779b97f4a7c15ULL;
+    return mix(st);
+  }
+  double uniform() { return static_cast<double>(next() >> 11) * 0x1.0p-53; }
+  double uniform(double lo, double hi) { return lo + (hi - lo) * uniform(); }
+  uint32_t below(uint32_t n) {
+    return static_cast<uint32_t>((static_cast<unsigned __int128>(next()) * n) >> 64);
+  }
+  double normal() {
+    if (has) {
+      has = false;
+      return cached;
+    }
+    double u1 = uniform();
+    while (u1 <= 0.0) u1 = uniform();
+    const double u2 = uniform();
+    const double r = std::sqrt(-2.0 * std::log(u1));
+    const double a = 6.283185307179586476925286766559 * u2;
+    cached = r * std::sin(a);
+    has = true;
+    return r * std::cos(a);
+  }
+};
+
+// M for (trial, count) and the count x M synthetic members (pipeline.cpp:330-347).
+int ablation_points(const vp_ablation_config& c, int trial, int count) {
+  HostRng tr(c.seed, static_cast<uint64_t>(count), static_cast<uint64_t>(trial));
+  return c.points_min + static_cast<int>(tr.below(static_cast<uint32_t>(c.points_max - c.points_min + 1)));
+}
+
+void ablation_clusters(const vp_ablation_config& c, int trial, int count, int m, double* out) {
+  auto one = [&](int k) {
+    HostRng rng(c.seed ^ 0x5eedULL, static_cast<uint64_t>(trial) << 8 | static_cast<uint64_t>(k), 7);
+    const double z0 = rng.uniform(0.0, 0.5);
+    double* o = out + 3ull * k * m;
+    for (int i = 0; i < m; ++i) {
+      const double x = rng.uniform(-0.5, 0.5);
+      const double y = rng.uniform(-0.5, 0.5);
+      const double z = z0 + 0.004 * rng.normal();
+      o[3 * i] = x;
+      o[3 * i + 1] = y;
+      o[3 * i + 2] = z;
+    }
+  };
+  const int nt = std::min<int>(count, std::max(1u, std::thread::hardware_concurrency()));
+  std::vector<std::thread> th;
+  for (int w = 0; w < nt; ++w)
+    th.emplace_back([&, w] {
+      for (int k = w; k < count; k += nt) one(k);
+    });
+  for (auto& t : th) t.join();
+}
+
 }  // namespace
 
 extern "C" {
@@ -1817,73 +2073,144 @@ int vp_fit_planes(size_t n_clusters, const int32_t* labels, const uint64_t* offs
   return guard([&] {
     vp_grid* g = scratch_grid(device);
     const RansacDev rd = make_ransacdev(*p);
-    std::vector<vp_plane> models;
-    std::vector<uint64_t> offs{0};
-    std::vector<double> inl;
-    uint64_t skipped = 0, unfit = 0;
+    FitResult all;
     for (size_t c0 = 0; c0 < n_clusters; c0 += kClusterBins) {
       const uint32_t K = static_cast<uint32_t>(std::min<size_t>(kClusterBins, n_clusters - c0));
-      std::vector<uint32_t> ksize(K), kpoff(K + 1, 0);
-      uint64_t tot = 0, maxm = 0;
-      for (uint32_t k = 0; k < K; ++k) {
-        ksize[k] = static_cast<uint32_t>(offsets[c0 + k + 1] - offsets[c0 + k]);
-        kpoff[k] = static_cast<uint32_t>(tot);
-        tot += (ksize[k] + 31u) & ~31u;
-        maxm += ksize[k];
+      std::vector<uint32_t> ksize(K);
+      for (uint32_t k = 0; k < K; ++k) ksize[k] = static_cast<uint32_t>(offsets[c0 + k + 1] - offsets[c0 + k]);
+      const std::vector<uint32_t> kpoff =
+          stage_clusters(g, K, labels + c0, ksize.data(), means + 3 * offsets[c0], p->iterations);
+      if (p->execution == 1) {
+        serial_prepare(g, ksize, kpoff);
+        serial_launch(g, rd, kpoff);
+      } else {
+        g->launch_ransac(rd);
       }
-      kpoff[K] = static_cast<uint32_t>(tot);
-      const uint32_t need = static_cast<uint32_t>(std::max<uint64_t>(tot, maxm));
-      g->seg.ensure(g->seg.b.Vcap, std::max(g->seg.b.Scap, need), std::max(g->seg.b.Icap, need),
-                    std::max(p->iterations, 1), g->gd.nwords);
-      std::vector<double> mx(tot, 0.0), my(tot, 0.0), mz(tot, 0.0);
-      for (uint32_t k = 0; k < K; ++k)
-        for (uint32_t j = 0; j < ksize[k]; ++j) {
-          const double* q = means + 3 * (offsets[c0 + k] + j);
-          mx[kpoff[k] + j] = q[0];
-          my[kpoff[k] + j] = q[1];
-          mz[kpoff[k] + j] = q[2];
-        }
-      h2d(g->seg.b.klabel, labels + c0, K, g->stream);
-      h2d(g->seg.b.ksize, ksize.data(), K, g->stream);
-      h2d(g->seg.b.kpoff, kpoff.data(), K + 1, g->stream);
-      h2d(g->seg.b.mx, mx.data(), tot, g->stream);
-      h2d(g->seg.b.my, my.data(), tot, g->stream);
-      h2d(g->seg.b.mz, mz.data(), tot, g->stream);
-      g->reset_frame_counters();
-      set_counter_u32(g, offsetof(Counters, K), K);
-      g->launch_ransac(rd);
-      g->read_counters();
-      const uint32_t F = g->h_ctr->nfits;
-      skipped += g->h_ctr->skipped;
-      unfit += g->h_ctr->unfit;
-      auto fm = d2h(g->seg.b.fit_model, 4ull * F, g->stream);
-      auto meta = d2h(g->seg.b.fit_meta, 2ull * F, g->stream);
-      auto io = d2h(g->seg.b.ioff, F + 1ull, g->stream);
       ck(cudaStreamSynchronize(g->stream), "sync");
-      auto in = d2h(g->seg.b.inl, 3ull * io[F], g->stream);
-      ck(cudaStreamSynchronize(g->stream), "sync");
-      for (uint32_t f = 0; f < F; ++f) {
-        vp_plane pl{};
-        for (int q = 0; q < 3; ++q) pl.normal[q] = fm[4 * f + q];
-        pl.offset = fm[4 * f + 3];
-        pl.inlier_count = meta[2 * f];
-        pl.cluster_label = meta[2 * f + 1];
-        models.push_back(pl);
-        offs.push_back(offs.back() + (io[f + 1] - io[f]));
-      }
-      inl.insert(inl.end(), in.begin(), in.end());
+      append_fits(all, p->execution == 1 ? serial_results(g, ksize, kpoff) : parallel_results(g));
     }
     auto* f = static_cast<vp_fits_t*>(std::calloc(1, sizeof(vp_fits_t)));
-    f->count = models.size();
-    f->models = static_cast<vp_plane*>(std::malloc(models.size() * sizeof(vp_plane) + 1));
-    std::memcpy(f->models, models.data(), models.size() * sizeof(vp_plane));
-    f->offsets = static_cast<uint64_t*>(std::malloc(offs.size() * 8));
-    std::memcpy(f->offsets, offs.data(), offs.size() * 8);
-    f->inliers = static_cast<double*>(std::malloc(inl.size() * 8 + 1));
-    std::memcpy(f->inliers, inl.data(), inl.size() * 8);
-    f->clusters_skipped_small = skipped;
-    f->clusters_unfit = unfit;
+    f->count = all.models.size();
+    f->models = static_cast<vp_plane*>(std::malloc(all.models.size() * sizeof(vp_plane) + 1));
+    std::memcpy(f->models, all.models.data(), all.models.size() * sizeof(vp_plane));
+    f->offsets = static_cast<uint64_t*>(std::malloc(all.offsets.size() * 8));
+    std::memcpy(f->offsets, all.offsets.data(), all.offsets.size() * 8);
+    f->inliers = static_cast<double*>(std::malloc(all.inliers.size() * 8 + 1));
+    std::memcpy(f->inliers, all.inliers.data(), all.inliers.size() * 8);
+    f->clusters_skipped_small = all.skipped;
+    f->clusters_unfit = all.unfit;
     *out = f;
+  });
+}
+
+void vp_default_ablation_config(vp_ablation_config* c) {
+  std::memset(c, 0, sizeof *c);
+  c->trials = 1000;
+  c->points_min = 10000;
+  c->points_max = 30000;
+  c->seed = 1234;
+  c->iterations = 100;
+  c->inlier_eps = 0.01;
+}
+
+int vp_ablation_clusters(const vp_ablation_config* c, int32_t trial, int32_t count, int32_t* m,
+                         double** points) {
+  *points = nullptr;
+  return guard([&] {
+    if (count <= 0 || c->points_max < c->points_min || c->points_min < 0)
+      fail(VP_EINVAL, "ablation: bad cluster count or point range");
+    *m = ablation_points(*c, trial, count);
+    *points = static_cast<double*>(std::malloc(3ull * count * *m * sizeof(double) + 8));
+    if (!*points) fail(VP_ENOMEM, "host allocation");
+    ablation_clusters(*c, trial, count, *m, *points);
+  });
+}
+
+int vp_run_ablation(const vp_ablation_config* c, vp_ablation_row* rows) {
+  return guard([&] {
+    if (c->trials <= 0) return;  // pipeline.cpp:309
+    if (c->points_max < c->points_min || c->points_min < 0 || c->n_counts < 0)
+      fail(VP_EINVAL, "ablation: bad configuration");
+    vp_grid* g = scratch_grid(c->device);
+    vp_ransac_params rp{};
+    rp.iterations = c->iterations;
+    rp.inlier_eps = c->inlier_eps;
+    rp.seed = c->seed;
+    rp.up[2] = 1.0;
+    const RansacDev rd = make_ransacdev(rp);
+    std::vector<std::vector<double>> par(c->n_counts), ser(c->n_counts);
+    cudaEvent_t e0, e1;
+    ck(cudaEventCreate(&e0), "event");
+    ck(cudaEventCreate(&e1), "event");
+    std::vector<double> pts;
+    for (int trial = 0; trial < c->trials; ++trial) {
+      for (int ci = 0; ci < c->n_counts; ++ci) {
+        const int count = c->cluster_counts[ci];
+        if (count <= 0 || count > kClusterBins) fail(VP_EINVAL, "ablation: 1..2048 clusters per row");
+        const int m = ablation_points(*c, trial, count);
+        pts.resize(3ull * count * m);
+        ablation_clusters(*c, trial, count, m, pts.data());
+        std::vector<int32_t> labels(count);
+        std::vector<uint32_t> ksize(count, static_cast<uint32_t>(m));
+        for (int k = 0; k < count; ++k) labels[k] = k;
+        const std::vector<uint32_t> kpoff = stage_clusters(g, count, labels.data(), ksize.data(), pts.data(),
+                                                           c->iterations);
+        serial_prepare(g, ksize, kpoff);
+        auto time_mode = [&](bool serial) {
+          ck(cudaEventRecord(e0, g->stream), "event");
+          if (serial) serial_launch(g, rd, kpoff); else g->launch_ransac(rd);
+          ck(cudaEventRecord(e1, g->stream), "event");
+          ck(cudaEventSynchronize(e1), "sync");
+          float ms = 0.f;
+          ck(cudaEventElapsedTime(&ms, e0, e1), "elapsed");
+          return static_cast<double>(ms);
+        };
+        if (trial % 2 == 0) {
+          par[ci].push_back(time_mode(false));
+          ser[ci].push_back(time_mode(true));
+        } else {
+          ser[ci].push_back(time_mode(true));
+          par[ci].push_back(time_mode(false));
+        }
+        const FitResult a = parallel_results(g), b = serial_results(g, ksize, kpoff);
+        if (a.models.size() != static_cast<size_t>(count))
+          fail(VP_ECUDA, "ablation: cluster dropped during timing");  // pipeline.cpp:353-354
+        if (!same_fits(a, b)) fail(VP_ECUDA, "ablation: execution modes disagree");
+      }
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    auto trimmed_mean = [](std::vector<double>& v) {  // pipeline.cpp:366-372
+      std::sort(v.begin(), v.end());
+      const size_t trim = v.size() / 10;
+      double sum = 0.0;
+      for (size_t i = trim; i < v.size() - trim; ++i) sum += v[i];
+      return sum / static_cast<double>(v.size() - 2 * trim);
+    };
+    for (int ci = 0; ci < c->n_counts; ++ci) {
+      vp_ablation_row& r = rows[ci];
+      r.clusters = c->cluster_counts[ci];
+      r.trials = c->trials;
+      r.parallel_ms = trimmed_mean(par[ci]);
+      r.serial_ms = trimmed_mean(ser[ci]);
+      r.parallel_median_ms = par[ci][par[ci].size() / 2];
+      r.serial_median_ms = ser[ci][ser[ci].size() / 2];
+    }
+  });
+}
+
+int vp_write_ablation_csv(const char* path, const vp_ablation_row* rows, size_t n) {
+  return guard([&] {
+    FILE* f = std::fopen(path, "w");
+    if (!f) fail(VP_EINVAL, std::string("ablation csv: cannot open for write: ") + path);
+    std::fputs("clusters,trials,parallel_ms,serial_ms,ratio,parallel_median_ms,serial_median_ms\n", f);
+    for (size_t i = 0; i < n; ++i) {
+      const vp_ablation_row& r = rows[i];
+      std::fprintf(f, "%d,%d,%.4f,%.4f,%.4f,%.4f,%.4f\n", r.clusters, r.trials, r.parallel_ms, r.serial_ms,
+                   r.serial_ms > 0.0 ? r.parallel_ms / r.serial_ms : 0.0, r.parallel_median_ms,
+                   r.serial_median_ms);
+    }
+    std::fclose(f);
   });
 }
 

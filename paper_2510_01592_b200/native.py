@@ -131,6 +131,7 @@ def lib():
         L.vp_version.restype = C.c_char_p
         L.vp_pipeline_grid.restype = C.c_void_p
         L.vp_kernel_launch_count.restype = C.c_uint64
+        L.vp_default_ablation_config.restype = None
         _lib = L
     return _lib
 
@@ -426,6 +427,50 @@ def fit_planes(labels, offsets, means, rp: RansacParams, device=0):
     stats = (F.clusters_skipped_small, F.clusters_unfit)
     lib().vp_fits_free(f)
     return models, stats
+
+
+class AblationConfig(C.Structure):
+    _fields_ = [("cluster_counts", C.POINTER(C.c_int32)), ("n_counts", C.c_int32), ("trials", C.c_int32),
+                ("points_min", C.c_int32), ("points_max", C.c_int32), ("seed", C.c_uint64),
+                ("iterations", C.c_int32), ("inlier_eps", C.c_double), ("device", C.c_int32)]
+
+
+class AblationRow(C.Structure):
+    _fields_ = [("clusters", C.c_int32), ("trials", C.c_int32), ("parallel_ms", C.c_double),
+                ("serial_ms", C.c_double), ("parallel_median_ms", C.c_double), ("serial_median_ms", C.c_double)]
+
+
+def ablation_config(counts=(1, 2, 4, 8, 16), **kw):
+    """AblationConfig (pipeline.hpp:65-74) defaults, overridden by keywords."""
+    c = AblationConfig()
+    lib().vp_default_ablation_config(C.byref(c))
+    c._counts = np.ascontiguousarray(counts, np.int32)  # keep alive
+    c.cluster_counts = _p(c._counts, C.c_int32)
+    c.n_counts = len(counts)
+    for k, v in kw.items():
+        setattr(c, k, v)
+    return c
+
+
+def run_ablation(cfg: AblationConfig, csv_path: str | None = None):
+    """run_ablation (pipeline.cpp:304-381) on the device; optional write_ablation_csv."""
+    rows = (AblationRow * max(cfg.n_counts, 1))()
+    check(lib().vp_run_ablation(C.byref(cfg), rows))
+    if csv_path:
+        check(lib().vp_write_ablation_csv(csv_path.encode(), rows, C.c_size_t(cfg.n_counts)))
+    return [dict(clusters=r.clusters, trials=r.trials, parallel_ms=r.parallel_ms, serial_ms=r.serial_ms,
+                 parallel_median_ms=r.parallel_median_ms, serial_median_ms=r.serial_median_ms)
+            for r in rows[:cfg.n_counts]]
+
+
+def ablation_clusters(cfg: AblationConfig, trial: int, count: int):
+    """The synthetic clusters of one (trial, count): array (count, M, 3)."""
+    m = C.c_int32()
+    pts = C.POINTER(C.c_double)()
+    check(lib().vp_ablation_clusters(C.byref(cfg), C.c_int32(trial), C.c_int32(count), C.byref(m), C.byref(pts)))
+    out = np.ctypeslib.as_array(pts, (count, m.value, 3)).copy()
+    lib().vp_free(pts)
+    return out
 
 
 def make_polygons(planes, inlier_sets, directions=16, device=0):
