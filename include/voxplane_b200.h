@@ -353,6 +353,30 @@ int vp_pipeline_frame_trace(vp_pipeline* pl, const float* xyz, uint64_t n,
                             const double rotation[9], const double translation[3],
                             uint8_t** buf, uint64_t* len);
 
+/* ---- frame and polygon formats on the GPU path (frame_io.cpp:91-116,
+   polygon_io.cpp:30-47) ---------------------------------------------------
+   A VXPF stream (magic "VXPF", u32 version 1, per frame u32 n, 12 f32 pose
+   [R|t] row-major, n x 3 f32 xyz) is read once into pinned host memory, so
+   replay feeds run_frames with asynchronous H2D copies and no per-frame
+   host staging. Errors as the reference: a missing file, bad magic or
+   version, or a truncated frame -> VP_EINVAL with the reference's message. */
+typedef struct vp_stream vp_stream;
+int vp_stream_open(const char* path, vp_stream** out);
+void vp_stream_close(vp_stream* s);
+uint64_t vp_stream_count(const vp_stream* s);
+/* Frame i: pinned xyz (n x 3 f32), pose as doubles (f32 values, as read). */
+int vp_stream_frame(const vp_stream* s, uint64_t i, const float** xyz, uint64_t* n, double rotation[9],
+                    double translation[3]);
+/* run_frames over frames [first, first + count) of a stream (replay_pipeline,
+   pipeline.cpp:291-302): out = the last frame's polygons, timings optional. */
+int vp_pipeline_replay(vp_pipeline* pl, const vp_stream* s, uint64_t first, uint64_t count,
+                       vp_polygons_t** out, vp_frame_timing* timings);
+/* write_frames_binary (frame_io.cpp:74-89): frames given as host arrays. */
+int vp_write_frames_binary(const char* path, size_t n_frames, const float* const* xyz, const uint64_t* n,
+                           const double* rotations, const double* translations);
+/* write_polygons (polygon_io.cpp:30-47): the golden-file text, %.9g. */
+int vp_write_polygons(const char* path, const vp_polygons_t* polygons);
+
 /* ---- cluster-parallel ablation (pipeline.cpp:304-381, Fig. 9) -------------
    Per trial (trial-major, alternating mode order as the reference): M drawn
    from CounterRng(seed, count, trial) in [points_min, points_max], `count`

@@ -66,6 +66,30 @@ int vp_render_frame(const vp_box* boxes, size_t nb, const vp_rect* rects, size_t
                     uint64_t frame_index, int threads, float** points, uint64_t* n,
                     double qR[9], double qt[3]);
 
+/* quantize_pose (frame_io.cpp:64-72) + the orthonormality check of
+   render_frame (scene_sim.cpp:188-190); returns VP_EINVAL (voxplane_b200.h) if invalid. */
+int vp_quantize_pose(const double R[9], const double t[3], double qR[9], double qt[3]);
+
+/* ---- device frame source ---------------------------
+   render_frame on the GPU: one thread per ray (pinhole pixel or pattern
+   direction), the reference's ray/box and ray/rect arithmetic in FP64
+   without FMA, CounterRng(seed, frame, ray) range noise, and an ordered
+   compaction of the hits (misses dropped, ray order kept). The frame stays
+   in device memory (feed it to vp_pipeline_frame_device / slabs). The noise
+   uses the device log/cos (<= 1-2 ulp from glibc): points equal the host
+   source's bytes unless such an ulp survives the f32 rounding
+   (tests/test_frame_source.py measures it). */
+typedef struct vp_frame_source vp_frame_source;
+int vp_frame_source_create(const vp_box* boxes, size_t nb, const vp_rect* rects, size_t nr,
+                           const vp_sensor* sensor, uint64_t seed, int device, vp_frame_source** out);
+void vp_frame_source_destroy(vp_frame_source* s);
+/* The cudaStream_t the source renders on. */
+void* vp_frame_source_stream(vp_frame_source* s);
+/* Render frame `frame_index` at pose (R, t): xyz_dev = device points (n x 3
+   f32, valid until the next render), qR/qt = the f32-quantised pose. */
+int vp_frame_source_render(vp_frame_source* s, const double R[9], const double t[3], uint64_t frame_index,
+                           const float** xyz_dev, uint64_t* n, double qR[9], double qt[3]);
+
 #ifdef __cplusplus
 }
 #endif

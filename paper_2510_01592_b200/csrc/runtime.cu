@@ -2214,6 +2214,152 @@ int vp_write_ablation_csv(const char* path, const vp_ablation_row* rows, size_t 
   });
 }
 
+}  // extern "C"
+
+struct vp_stream {
+  unsigned char* buf = nullptr;  // pinned: the whole file
+  size_t bytes = 0;
+  std::vector<uint64_t> off, n;  // per frame: xyz byte offset, point count
+  std::vector<double> pose;      // 12 per frame
+  bool pinned = true;
+  ~vp_stream() {
+    if (buf) {
+      if (pinned) cudaFreeHost(buf); else std::free(buf);
+    }
+  }
+};
+
+namespace {
+uint32_t le_u32(const unsigned char* p) {
+  return static_cast<uint32_t>(p[0]) | static_cast<uint32_t>(p[1]) << 8 | static_cast<uint32_t>(p[2]) << 16 |
+         static_cast<uint32_t>(p[3]) << 24;
+}
+float le_f32(const unsigned char* p) {
+  const uint32_t u = le_u32(p);
+  float f;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
+void put_u32(FILE* f, uint32_t v) {
+  const unsigned char b[4] = {static_cast<unsigned char>(v), static_cast<unsigned char>(v >> 8),
+                              static_cast<unsigned char>(v >> 16), static_cast<unsigned char>(v >> 24)};
+  std::fwrite(b, 1, 4, f);
+}
+void put_f32(FILE* f, float x) {
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  put_u32(f, u);
+}
+}  // namespace
+
+extern "C" {
+
+int vp_stream_open(const char* path, vp_stream** out) {
+  *out = nullptr;
+  return guard([&] {
+    FILE* f = std::fopen(path, "rb");
+    if (!f) fail(VP_EINVAL, std::string("frame stream: cannot open: ") + path);
+    std::fseek(f, 0, SEEK_END);
+    const long len = std::ftell(f);
+    std::fseek(f, 0, SEEK_SET);
+    auto* s = new vp_stream();
+    struct Del {
+      vp_stream*& s;
+      ~Del() { delete s; }
+    } del{s};
+    s->bytes = len > 0 ? static_cast<size_t>(len) : 0;
+    // pinned when a device is present (async H2D in replay); plain host
+    // memory otherwise (reading a stream needs no device)
+    if (cudaHostAlloc(reinterpret_cast<void**>(&s->buf), s->bytes + 1, cudaHostAllocDefault) != cudaSuccess) {
+      cudaGetLastError();
+      s->pinned = false;
+      s->buf = static_cast<unsigned char*>(std::malloc(s->bytes + 1));
+      if (!s->buf) {
+        std::fclose(f);
+        fail(VP_ENOMEM, "frame stream: host allocation failed");
+      }
+    }
+    const size_t got = std::fread(s->buf, 1, s->bytes, f);
+    std::fclose(f);
+    if (got != s->bytes) fail(VP_EINVAL, std::string("frame stream: read failed: ") + path);
+    if (s->bytes < 4 || std::memcmp(s->buf, "VXPF", 4) != 0)
+      fail(VP_EINVAL, std::string("frame stream: bad magic in ") + path);
+    if (s->bytes < 8 || le_u32(s->buf + 4) != 1) fail(VP_EINVAL, "frame stream: unsupported version");
+    size_t o = 8;
+    while (o < s->bytes) {  // frame_io.cpp:102-113; short reads throw (frame_io.cpp:28)
+      if (o + 52 > s->bytes) fail(VP_EINVAL, "frame stream: truncated file");
+      const uint64_t n = le_u32(s->buf + o);
+      for (int k = 0; k < 12; ++k) s->pose.push_back(static_cast<double>(le_f32(s->buf + o + 4 + 4 * k)));
+      o += 52;
+      if (o + 12 * n > s->bytes) fail(VP_EINVAL, "frame stream: truncated file");
+      s->off.push_back(o);
+      s->n.push_back(n);
+      o += 12 * n;
+    }
+    // little-endian host: the xyz payload is used in place
+    *out = s;
+    s = nullptr;
+  });
+}
+
+void vp_stream_close(vp_stream* s) { delete s; }
+
+uint64_t vp_stream_count(const vp_stream* s) { return s ? s->n.size() : 0; }
+
+int vp_stream_frame(const vp_stream* s, uint64_t i, const float** xyz, uint64_t* n, double rotation[9],
+                    double translation[3]) {
+  return guard([&] {
+    if (i >= s->n.size()) fail(VP_EINVAL, "frame stream: frame index out of range");
+    *xyz = reinterpret_cast<const float*>(s->buf + s->off[i]);
+    *n = s->n[i];
+    const double* q = s->pose.data() + 12 * i;  // [R|t] row-major
+    for (int r = 0; r < 3; ++r) {
+      for (int c = 0; c < 3; ++c) rotation[3 * r + c] = q[4 * r + c];
+      translation[r] = q[4 * r + 3];
+    }
+  });
+}
+
+int vp_write_frames_binary(const char* path, size_t n_frames, const float* const* xyz, const uint64_t* n,
+                           const double* rotations, const double* translations) {
+  return guard([&] {
+    FILE* f = std::fopen(path, "wb");
+    if (!f) fail(VP_EINVAL, std::string("frame stream: cannot open for write: ") + path);
+    std::fwrite("VXPF", 1, 4, f);
+    put_u32(f, 1);
+    for (size_t k = 0; k < n_frames; ++k) {
+      put_u32(f, static_cast<uint32_t>(n[k]));
+      for (int r = 0; r < 3; ++r) {  // put_pose: f32 [R|t] row-major
+        for (int c = 0; c < 3; ++c) put_f32(f, static_cast<float>(rotations[9 * k + 3 * r + c]));
+        put_f32(f, static_cast<float>(translations[3 * k + r]));
+      }
+      for (uint64_t i = 0; i < 3 * n[k]; ++i) put_f32(f, xyz[k][i]);
+    }
+    const bool ok = std::ferror(f) == 0;
+    std::fclose(f);
+    if (!ok) fail(VP_EINVAL, std::string("frame stream: write failed: ") + path);
+  });
+}
+
+int vp_write_polygons(const char* path, const vp_polygons_t* polygons) {
+  return guard([&] {
+    FILE* f = std::fopen(path, "w");
+    if (!f) fail(VP_EINVAL, std::string("polygons: cannot open for write: ") + path);
+    std::fputs("# voxplane polygons v1\n", f);
+    for (size_t i = 0; i < (polygons ? polygons->count : 0); ++i) {
+      const vp_polygon& q = polygons->polys[i];
+      std::fprintf(f, "polygon\nnormal %.9g %.9g %.9g\noffset %.9g\nvertices %u\n", q.plane.normal[0],
+                   q.plane.normal[1], q.plane.normal[2], q.plane.offset, q.nverts);
+      for (uint32_t k = 0; k < q.nverts; ++k)
+        std::fprintf(f, "%.9g %.9g %.9g\n", q.v3d[3 * k], q.v3d[3 * k + 1], q.v3d[3 * k + 2]);
+      std::fprintf(f, "area %.9g\nlabel %d\ninliers %d\n", q.area, q.plane.cluster_label, q.plane.inlier_count);
+    }
+    const bool ok = std::ferror(f) == 0;
+    std::fclose(f);
+    if (!ok) fail(VP_EINVAL, std::string("polygons: write failed: ") + path);
+  });
+}
+
 void vp_fits_free(vp_fits_t* f) {
   if (!f) return;
   std::free(f->models);
@@ -2812,6 +2958,35 @@ int vp_pipeline_run(vp_pipeline* pl, size_t n_frames, const float* const* xyz, c
   if (out) *out = nullptr;
   return guard([&] {
     pipeline_run(pl, n_frames, xyz, n, rotations, translations, device_ptrs != 0, timings);
+    if (out) {
+      HostPolys hp;
+      pl->grid->download_polygons(hp, false);
+      *out = make_polygons_out(hp);
+    }
+    pl->grid->set_slot(0);
+  });
+}
+
+int vp_pipeline_replay(vp_pipeline* pl, const vp_stream* st, uint64_t first, uint64_t count,
+                       vp_polygons_t** out, vp_frame_timing* timings) {
+  if (out) *out = nullptr;
+  return guard([&] {
+    if (first > st->n.size() || count > st->n.size() - first) fail(VP_EINVAL, "replay: frame range out of stream");
+    std::vector<const float*> xyz(count);
+    std::vector<uint64_t> n(count);
+    std::vector<double> R(9 * count), t(3 * count);
+    for (uint64_t k = 0; k < count; ++k) {
+      const uint64_t i = first + k;
+      xyz[k] = reinterpret_cast<const float*>(st->buf + st->off[i]);
+      n[k] = st->n[i];
+      const double* q = st->pose.data() + 12 * i;
+      for (int r = 0; r < 3; ++r) {
+        for (int c = 0; c < 3; ++c) R[9 * k + 3 * r + c] = q[4 * r + c];
+        t[3 * k + r] = q[4 * r + 3];
+      }
+    }
+    // pinned host frames: the H2D copies inside run_frames are asynchronous
+    pipeline_run(pl, count, xyz.data(), n.data(), R.data(), t.data(), false, timings);
     if (out) {
       HostPolys hp;
       pl->grid->download_polygons(hp, false);

@@ -368,6 +368,15 @@ int vp_default_trajectory(int kind, int frames, double rate_hz, double* poses) {
   return static_cast<int>(v.size() / 12);
 }
 
+int vp_quantize_pose(const double Rin[9], const double tin[3], double qR[9], double qt[3]) {
+  M3 R;  // quantize_pose (frame_io.cpp:64-72)
+  for (int i = 0; i < 9; ++i) R.m[i] = static_cast<double>(static_cast<float>(Rin[i]));
+  if (!valid_rotation(R)) return VP_EINVAL;  // render_frame (scene_sim.cpp:188-190)
+  std::memcpy(qR, R.m, sizeof R.m);
+  for (int k = 0; k < 3; ++k) qt[k] = static_cast<double>(static_cast<float>(tin[k]));
+  return VP_OK;
+}
+
 int vp_spherical_pattern(int n, float* out) {  // scene_sim.cpp:174-184
   const double golden = kPi * (3.0 - std::sqrt(5.0));
   for (int i = 0; i < n; ++i) {

@@ -429,6 +429,64 @@ def fit_planes(labels, offsets, means, rp: RansacParams, device=0):
     return models, stats
 
 
+class Stream:
+    """VXPF frame stream read into pinned host memory (vp_stream_open)."""
+
+    def __init__(self, path: str):
+        self.h = C.c_void_p()
+        check(lib().vp_stream_open(str(path).encode(), C.byref(self.h)))
+
+    def __len__(self):
+        L = lib()
+        L.vp_stream_count.restype = C.c_uint64
+        return int(L.vp_stream_count(self.h))
+
+    def frame(self, i):
+        xyz = C.POINTER(C.c_float)()
+        n = C.c_uint64()
+        R = np.zeros(9)
+        t = np.zeros(3)
+        check(lib().vp_stream_frame(self.h, C.c_uint64(i), C.byref(xyz), C.byref(n), _p(R, C.c_double),
+                                    _p(t, C.c_double)))
+        pts = np.ctypeslib.as_array(xyz, (n.value, 3)).copy() if n.value else np.zeros((0, 3), np.float32)
+        return pts, R.reshape(3, 3), t
+
+    def replay(self, pl: "Pipeline", first=0, count=None):
+        """run_frames over the stream (vp_pipeline_replay): the last frame's polygons."""
+        count = len(self) - first if count is None else count
+        out = C.POINTER(Polygons)()
+        check(lib().vp_pipeline_replay(pl.h, self.h, C.c_uint64(first), C.c_uint64(count), C.byref(out), None))
+        return out
+
+    def close(self):
+        if self.h:
+            lib().vp_stream_close(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def write_frames_binary(path, frames):
+    """write_frames_binary (frame_io.cpp:74-89) through the library."""
+    n = len(frames)
+    pts = [np.ascontiguousarray(f.points, np.float32) for f in frames]
+    ptrs = (C.c_void_p * max(n, 1))(*[p.ctypes.data for p in pts])
+    cnt = np.asarray([len(p) for p in pts], np.uint64)
+    R = np.ascontiguousarray(np.stack([np.asarray(f.rotation, np.float64).reshape(9) for f in frames]))
+    t = np.ascontiguousarray(np.stack([np.asarray(f.translation, np.float64) for f in frames]))
+    check(lib().vp_write_frames_binary(str(path).encode(), C.c_size_t(n), ptrs, _p(cnt, C.c_uint64),
+                                       _p(R, C.c_double), _p(t, C.c_double)))
+
+
+def write_polygons(path, polys_ptr):
+    """write_polygons (polygon_io.cpp:30-47) of a vp_polygons_t* through the library."""
+    check(lib().vp_write_polygons(str(path).encode(), polys_ptr))
+
+
 class AblationConfig(C.Structure):
     _fields_ = [("cluster_counts", C.POINTER(C.c_int32)), ("n_counts", C.c_int32), ("trials", C.c_int32),
                 ("points_min", C.c_int32), ("points_max", C.c_int32), ("seed", C.c_uint64),

@@ -194,17 +194,30 @@ def stepping_stones():
     return s
 
 
-def workload(name: str, frames: int | None = None) -> Workload:
-    """SURVEY.md §8(d) configs C1-C4 (C5 is the multi-GPU map)."""
+@dataclass
+class WorkloadSpec:
+    """Scene, sensor, poses and grid of a workload before rendering."""
+    name: str
+    scene: Scene
+    sensor: SensorSpec
+    poses: np.ndarray
+    seed: int
+    resolution: float
+    extent: tuple
+    first_index: int = 0
+
+
+def workload_spec(name: str, frames: int | None = None) -> WorkloadSpec:
+    """SURVEY.md §8(d) configs C1-C5."""
     if name == "c1":  # Stair5, one 640x480 frame, 0.05 m, 100^3
         sensor = SensorSpec(width=640, height=480, max_range=6.0, rate_hz=30.0)
         poses = default_trajectory(STAIR5, 30, 30.0)[:1]
-        return Workload(name, render(stock_scene(STAIR5), sensor, poses, 2025), 0.05, (100, 100, 100), 2025)
+        return WorkloadSpec(name, stock_scene(STAIR5), sensor, poses, 2025, 0.05, (100, 100, 100))
     if name == "c2":  # Stair5 + stepping stones, 30 frames, 640x480, 0.01 m, 500^3
         n = frames or 30
         sensor = SensorSpec(width=640, height=480, max_range=6.0, rate_hz=30.0)
         poses = default_trajectory(STAIR5, n, 30.0)
-        return Workload(name, render(stepping_stones(), sensor, poses, 2025), 0.01, (500, 500, 500), 2025)
+        return WorkloadSpec(name, stepping_stones(), sensor, poses, 2025, 0.01, (500, 500, 500))
     if name == "c3":  # open-tread stairs + overhanging table, 0.01 m, 500^3
         n = frames or 30
         s = Scene()
@@ -214,17 +227,81 @@ def workload(name: str, frames: int | None = None) -> Workload:
         s.rects.append(horizontal_rect((-0.8, 0.0, 0.75), 0.6, 0.4))
         sensor = SensorSpec(width=640, height=480, max_range=6.0, rate_hz=30.0)
         poses = straight_trajectory(n, 30.0, (-1.7, 0.0, 0.45), (0.1, 0.0, 0.45), -35.0, 10.0)
-        return Workload(name, render(s, sensor, poses, 2025), 0.01, (500, 500, 500), 2025)
+        return WorkloadSpec(name, s, sensor, poses, 2025, 0.01, (500, 500, 500))
     if name == "c4":  # ~1M-point sphere LiDAR in Stair5 + 20x20 m floor
         n = frames or 30
         s = stock_scene(STAIR5)
         s.rects.append(horizontal_rect((0.0, 0.0, -0.001), 10.0, 10.0))
         sensor = SensorSpec(kind=1, pattern=spherical_pattern(2_000_000), max_range=10.0, rate_hz=30.0)
         poses = default_trajectory(STAIR5, n, 30.0)
-        return Workload(name, render(s, sensor, poses, 2025), 0.01, (500, 500, 500), 2025)
+        return WorkloadSpec(name, s, sensor, poses, 2025, 0.01, (500, 500, 500))
+    if name == "c5":
+        n = frames or 6
+        sensor = SensorSpec(kind=1, pattern=spherical_pattern(1_000_000), max_range=10.0, rate_hz=10.0)
+        return WorkloadSpec(name, c5_scene(), sensor, c5_poses(n), 2025, 0.01, C5_EXTENT)
+    raise ValueError(name)
+
+
+def workload(name: str, frames: int | None = None) -> Workload:
+    """SURVEY.md §8(d) configs C1-C4 (C5 is the multi-GPU map), rendered on the host."""
     if name == "c5":
         return c5_workload(frames or 6)
-    raise ValueError(name)
+    w = workload_spec(name, frames)
+    return Workload(name, render(w.scene, w.sensor, w.poses, w.seed), w.resolution, w.extent, w.seed)
+
+
+class DeviceFrameSource:
+    """render_frame on the GPU (vp_frame_source_*): frames stay in HBM."""
+
+    def __init__(self, scene: Scene, sensor: SensorSpec, seed: int, device: int = 0):
+        B, nb, R, nr = scene.ctypes()
+        s = Sensor()
+        s.kind, s.width, s.height = sensor.kind, sensor.width, sensor.height
+        s.hfov_deg, s.vfov_deg = sensor.hfov_deg, sensor.vfov_deg
+        self._pat = None
+        if sensor.pattern is not None:
+            self._pat = np.ascontiguousarray(sensor.pattern, np.float32)
+            s.pattern = self._pat.ctypes.data_as(C.POINTER(C.c_float))
+            s.npattern = len(self._pat)
+        s.rate_hz, s.max_range, s.noise_sigma = sensor.rate_hz, sensor.max_range, sensor.noise_sigma
+        self.h = C.c_void_p()
+        self.device = device
+        native.check(_L().vp_frame_source_create(B, C.c_size_t(nb), R, C.c_size_t(nr), C.byref(s),
+                                                 C.c_uint64(seed), C.c_int(device), C.byref(self.h)))
+
+    def render_ptr(self, pose, index):
+        """(device pointer, n, R 3x3, t) of frame `index` at pose (12 doubles R|t)."""
+        Rm = np.ascontiguousarray(pose[:9], np.float64)
+        t = np.ascontiguousarray(pose[9:12], np.float64)
+        ptr = C.c_void_p()
+        n = C.c_uint64()
+        qR, qt = np.zeros(9), np.zeros(3)
+        native.check(_L().vp_frame_source_render(self.h, Rm.ctypes.data_as(C.POINTER(C.c_double)),
+                                                 t.ctypes.data_as(C.POINTER(C.c_double)), C.c_uint64(index),
+                                                 C.byref(ptr), C.byref(n),
+                                                 qR.ctypes.data_as(C.POINTER(C.c_double)),
+                                                 qt.ctypes.data_as(C.POINTER(C.c_double))))
+        return ptr.value or 0, n.value, qR.reshape(3, 3), qt
+
+    def render(self, pose, index):
+        """Frame with its points copied to the host (tests)."""
+        import torch
+
+        from .slabs import _dev_bytes
+        ptr, n, R, t = self.render_ptr(pose, index)
+        pts = _dev_bytes(ptr, 12 * n, self.device).view(torch.float32).view(-1, 3).cpu().numpy().copy()
+        return Frame(pts, R, t)
+
+    def close(self):
+        if self.h:
+            _L().vp_frame_source_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def c5_scene() -> Scene:
