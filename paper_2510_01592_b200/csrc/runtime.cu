@@ -421,6 +421,14 @@ struct vp_grid {
   unsigned long long* occ_total = nullptr;  // VoxelGrid::occupied_ (device, persistent)
   uint64_t host_occupied = 0;
   cudaStream_t mstream = nullptr;   // mapping stream of pipelined runs
+  // Second segmentation context (pipelined runs): frame k's CCL .. polygon
+  // chain runs on its own stream with its own scratch and ordinal map while
+  // frame k+1 is mapped and starts its own chain. use_seg(s) swaps it in.
+  Seg seg_alt;
+  cudaStream_t stream_alt = nullptr;
+  int32_t* ordmap_alt = nullptr;
+  uint32_t* stbits_alt = nullptr;
+  int seg_slot = 0;
   cudaStream_t lstream = nullptr;   // stream the mapping launches go to (stream or mstream)
   // integrate scratch
   uint64_t pcap = 0;
@@ -452,8 +460,12 @@ struct vp_grid {
     for (auto* p : {occ[0], occ[1]}) if (p) cudaFree(p);
     if (gd.cells) cudaFree(gd.cells);
     if (gd.clr) cudaFree(gd.clr);
+    if (stream_alt) cudaStreamSynchronize(stream_alt);
     if (gd.ordmap) cudaFree(gd.ordmap);
     if (gd.stbits) cudaFree(gd.stbits);
+    if (ordmap_alt) cudaFree(ordmap_alt);
+    if (stbits_alt) cudaFree(stbits_alt);
+    seg_alt.release();
     if (gmap) cudaFree(gmap);
     if (gbits) cudaFree(gbits);
     sl.release();
@@ -473,6 +485,7 @@ struct vp_grid {
     for (auto& e : ev) if (e) cudaEventDestroy(e);
     if (stream) cudaStreamDestroy(stream);
     if (mstream) cudaStreamDestroy(mstream);
+    if (stream_alt) cudaStreamDestroy(stream_alt);
   }
 
   // ------------------------------------------------------------ set-up
@@ -595,6 +608,32 @@ struct vp_grid {
     }
   }
 
+  // Segmentation context of pipeline slot s (scratch, ordinal map, stream).
+  void use_seg(int s) {
+    if (s == seg_slot) return;
+    std::swap(seg, seg_alt);
+    std::swap(gd.ordmap, ordmap_alt);
+    std::swap(gd.stbits, stbits_alt);
+    std::swap(stream, stream_alt);
+    seg_slot = s;
+  }
+  // The second context, with the first one's capacities.
+  void ensure_alt(int iterations) {
+    if (!stream_alt) {
+      ck(cudaStreamCreateWithFlags(&stream_alt, cudaStreamNonBlocking), "stream");
+      const uint64_t C = gd.ncells;
+      ordmap_alt = dalloc<int32_t>(C);
+      stbits_alt = dalloc<uint32_t>(gd.nwords);
+      ck(cudaMemsetAsync(ordmap_alt, 0xff, C * 4, stream_alt), "memset ordmap");
+      ck(cudaMemsetAsync(stbits_alt, 0, gd.nwords * 4, stream_alt), "memset stbits");
+    }
+    Seg& a = seg_slot == 0 ? seg_alt : seg;
+    const Seg& m = seg_slot == 0 ? seg : seg_alt;
+    a.ensure(std::max(a.b.Vcap, m.b.Vcap), std::max(a.b.Scap, m.b.Scap), std::max(a.b.Icap, m.b.Icap), iterations,
+             gd.nwords);
+    a.ensure_dirs(16, seg_slot == 0 ? stream_alt : stream);
+    ck(cudaStreamSynchronize(stream_alt), "sync");
+  }
   void set_slot(int s) {
     slot = s;
     ctr = ctr_s[s];
@@ -842,6 +881,12 @@ struct vp_grid {
   // voxel_frame_polygons up to filter_clusters: everything that can overflow
   // a capacity, and the last stage that reads the grid cells.
   void launch_seg_a(const vp_pipeline_params& p, bool timing) {
+    launch_seg_a1(p, timing);
+    launch_seg_a2(p, timing);
+  }
+  // occupied_voxels .. classify_steppable + ordinal map: the last stage that
+  // reads the grid (cells, occupancy) -- everything that can overflow
+  void launch_seg_a1(const vp_pipeline_params& p, bool timing) {
     const SegDev sd = make_segdev(p.seg, gd.res);
     if (!capturing && static_cast<uint64_t>(p.ransac.iterations) * kClusterBins > seg.cand_cap)
       seg.ensure(seg.b.Vcap, seg.b.Scap, seg.b.Icap, p.ransac.iterations, gd.nwords);
@@ -850,6 +895,11 @@ struct vp_grid {
     launch_classify(sd, 1);
     if (timing) record(ev[2]);
     launch_step_emit(grid_map());
+  }
+  // build_adjacency + label_components + filter_clusters: steppable list and
+  // ordinal map only (cannot overflow: members <= S + 31 K < Mcap)
+  void launch_seg_a2(const vp_pipeline_params& p, bool timing) {
+    const SegDev sd = make_segdev(p.seg, gd.res);
     launch_ccl(sd, grid_map());
     launch_clusters(sd);
     if (timing) record(ev[3]);
@@ -1150,15 +1200,21 @@ void pipeline_run(vp_pipeline* pl, size_t nf, const float* const* xyz, const uin
   for (size_t k = 0; k < nf; ++k) maxn = std::max(maxn, n[k]);
   for (size_t k = 0; k < nf; ++k)
     if (!is_valid_rotation(R + 9 * k)) fail(VP_EINVAL, "clear_rays: pose rotation is not orthonormal");
+  g->use_seg(0);
   g->ensure_points(maxn);
   if (static_cast<uint64_t>(pl->p.ransac.iterations) * kClusterBins > g->seg.cand_cap)
     g->seg.ensure(g->seg.b.Vcap, g->seg.b.Scap, g->seg.b.Icap, pl->p.ransac.iterations, g->gd.nwords);
   g->seg.ensure_dirs(16, g->stream);
+  if (nf >= 2) g->ensure_alt(pl->p.ransac.iterations);
   ck(cudaStreamSynchronize(g->stream), "sync");
   const bool graphs = !g_prof_on && !std::getenv("VP_NO_GRAPH");
+  // frame k-2's slot is reused by frame k: its whole chain must be done
   auto harvest = [&](size_t k) {
-    if (!timings) return;
     const int s = static_cast<int>(k & 1);
+    if (g->h_ctr_s[s]->overflow & kOverflowClusters)
+      fail(VP_ENOMEM, "more than 2048 clusters >= min_cluster_size in one frame");
+    if (g->h_ctr_s[s]->overflow) fail(VP_ENOMEM, "segmentation capacity overflow in a pipelined frame");
+    if (!timings) return;
     float ms = 0.f;
     ck(cudaEventElapsedTime(&ms, pl->ev_start[s], pl->ev_done[s]), "elapsed");
     vp_frame_timing& tm = timings[k];
@@ -1175,6 +1231,7 @@ void pipeline_run(vp_pipeline* pl, size_t nf, const float* const* xyz, const uin
       harvest(k - 2);
     }
     g->set_slot(s);
+    g->use_seg(s);
     g->set_pose(R + 9 * k, t + 3 * k);
     g->fill_static_params();
     if (device_ptrs) {
@@ -1207,33 +1264,42 @@ void pipeline_run(vp_pipeline* pl, size_t nf, const float* const* xyz, const uin
     if (graphs) run_part_graph(pl, 0, g->mstream, map_part); else map_part();
     g->lstream = g->stream;
     ck(cudaEventRecord(pl->ev_map[s], g->mstream), "ev");
-    // segmentation of frame k
+    // segmentation of frame k on the slot's stream: the grid readers first
+    // (occupied scan .. ordinal map), then the CCL .. polygon chain, which
+    // overlaps frame k+1's mapping and the start of its own chain
     ck(cudaStreamWaitEvent(g->stream, pl->ev_map[s], 0), "wait");
-    auto seg_a = [&] {
-      g->launch_seg_a(pl->p, false);
+    auto seg_grid = [&] {
+      g->launch_seg_a1(pl->p, false);
       ck(cudaMemcpyAsync(g->h_ctr, g->ctr, sizeof(Counters), cudaMemcpyDeviceToHost, g->stream), "ctr");
     };
-    auto seg_b = [&] {
+    auto seg_rest = [&] {
+      g->launch_seg_a2(pl->p, false);
       g->launch_seg_b(pl->p, false);
       ck(cudaMemcpyAsync(g->h_ctr, g->ctr, sizeof(Counters), cudaMemcpyDeviceToHost, g->stream), "ctr");
     };
-    if (graphs) run_part_graph(pl, 1, g->stream, seg_a); else seg_a();
+    if (graphs) run_part_graph(pl, 1, g->stream, seg_grid); else seg_grid();
     ck(cudaEventRecord(pl->ev_clu[s], g->stream), "ev");
-    if (graphs) run_part_graph(pl, 2, g->stream, seg_b); else seg_b();
-    ck(cudaEventRecord(pl->ev_done[s], g->stream), "ev");
     // capacity check point: frame k+1 has not touched the grid yet
     ck(cudaEventSynchronize(pl->ev_clu[s]), "sync");
     if (g->h_ctr->overflow) {
       ck(cudaStreamSynchronize(g->stream), "sync");
-      rerun_segment_until_fits(g, pl->p);
+      rerun_segment_until_fits(g, pl->p);  // whole segmentation, synchronous
+      ck(cudaEventRecord(pl->ev_done[s], g->stream), "ev");
+    } else {
+      if (graphs) run_part_graph(pl, 2, g->stream, seg_rest); else seg_rest();
       ck(cudaEventRecord(pl->ev_done[s], g->stream), "ev");
     }
     ++pl->frame;
   }
-  ck(cudaStreamSynchronize(g->stream), "sync");
+  for (int q = 0; q < 2; ++q) {
+    g->use_seg(q);
+    ck(cudaStreamSynchronize(g->stream), "sync");
+  }
   ck(cudaStreamSynchronize(g->mstream), "sync");
   for (size_t k = nf >= 2 ? nf - 2 : 0; k < nf; ++k) harvest(k);
-  if (nf) g->set_slot(static_cast<int>((nf - 1) & 1));
+  const int last = nf ? static_cast<int>((nf - 1) & 1) : 0;
+  g->set_slot(last);
+  g->use_seg(last);  // the final frame's results (callers switch back with use_seg(0))
   g->host_occupied = g->h_ctr->occupied;
 }
 
@@ -2964,6 +3030,7 @@ int vp_pipeline_run(vp_pipeline* pl, size_t n_frames, const float* const* xyz, c
       *out = make_polygons_out(hp);
     }
     pl->grid->set_slot(0);
+    pl->grid->use_seg(0);
   });
 }
 
@@ -2993,6 +3060,7 @@ int vp_pipeline_replay(vp_pipeline* pl, const vp_stream* st, uint64_t first, uin
       *out = make_polygons_out(hp);
     }
     pl->grid->set_slot(0);
+    pl->grid->use_seg(0);
   });
 }
 
