@@ -524,8 +524,8 @@ __global__ void k_clear_apply(GridDesc g, const FrameParams* __restrict__ fp, Co
 __device__ __forceinline__ uint32_t row_bits(const uint32_t* row, int W, int b0) {
   const int wlo = b0 >= 0 ? (b0 >> 5) : -((-b0 + 31) >> 5);
   const int sh = b0 - wlo * 32;
-  const uint32_t lo = (wlo >= 0 && wlo < W) ? row[wlo] : 0u;
-  const uint32_t hi = (wlo + 1 >= 0 && wlo + 1 < W) ? row[wlo + 1] : 0u;
+  const uint32_t lo = (wlo >= 0 && wlo < W) ? __ldg(row + wlo) : 0u;
+  const uint32_t hi = (wlo + 1 >= 0 && wlo + 1 < W) ? __ldg(row + wlo + 1) : 0u;
   return sh ? ((lo >> sh) | (hi << (32 - sh))) : lo;
 }
 

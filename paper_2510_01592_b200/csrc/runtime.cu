@@ -36,6 +36,7 @@ constexpr double kRadToDeg = 57.295779513082320876798;
 constexpr double kDegToRad = 0.017453292519943295769237;
 constexpr double kPi = 3.14159265358979323846;  // == glibc M_PI
 constexpr int kThreads = 256;
+constexpr int kSlots = 3;  // frames in flight in a pipelined run
 
 struct VpFail {
   int code;
@@ -407,11 +408,11 @@ struct vp_grid {
   int cur = 0;
   // Per-frame state in two slots so consecutive frames can be in flight at
   // once (vp_pipeline_run); ctr/h_ctr/d_fp/h_fp/d_pts point at the current slot.
-  Counters* ctr_s[2] = {nullptr, nullptr};
-  Counters* h_ctr_s[2] = {nullptr, nullptr};  // pinned
-  FrameParams* d_fp_s[2] = {nullptr, nullptr};
-  FrameParams* h_fp_s[2] = {nullptr, nullptr};  // pinned
-  float* d_pts_s[2] = {nullptr, nullptr};
+  Counters* ctr_s[kSlots] = {};
+  Counters* h_ctr_s[kSlots] = {};  // pinned
+  FrameParams* d_fp_s[kSlots] = {};
+  FrameParams* h_fp_s[kSlots] = {};  // pinned
+  float* d_pts_s[kSlots] = {};
   int slot = 0;
   Counters* ctr = nullptr;
   Counters* h_ctr = nullptr;
@@ -421,13 +422,17 @@ struct vp_grid {
   unsigned long long* occ_total = nullptr;  // VoxelGrid::occupied_ (device, persistent)
   uint64_t host_occupied = 0;
   cudaStream_t mstream = nullptr;   // mapping stream of pipelined runs
-  // Second segmentation context (pipelined runs): frame k's CCL .. polygon
-  // chain runs on its own stream with its own scratch and ordinal map while
-  // frame k+1 is mapped and starts its own chain. use_seg(s) swaps it in.
-  Seg seg_alt;
-  cudaStream_t stream_alt = nullptr;
-  int32_t* ordmap_alt = nullptr;
-  uint32_t* stbits_alt = nullptr;
+  cudaStream_t fstream = nullptr;   // fork of the mapping stream (integrate grouping || clear_rays)
+  cudaEvent_t fork_ev[2] = {nullptr, nullptr};
+  // Segmentation contexts of the pipelined run's slots: frame k's CCL ..
+  // polygon chain runs on its slot's stream with its own scratch and ordinal
+  // map while later frames are mapped and start their chains. The active
+  // context lives in (seg, gd.ordmap, gd.stbits, stream); pool[i] holds
+  // context i while it is not active. use_seg(s) swaps contexts.
+  Seg seg_pool[kSlots];
+  cudaStream_t stream_pool[kSlots] = {};
+  int32_t* ordmap_pool[kSlots] = {};
+  uint32_t* stbits_pool[kSlots] = {};
   int seg_slot = 0;
   cudaStream_t lstream = nullptr;   // stream the mapping launches go to (stream or mstream)
   // integrate scratch
@@ -460,18 +465,20 @@ struct vp_grid {
     for (auto* p : {occ[0], occ[1]}) if (p) cudaFree(p);
     if (gd.cells) cudaFree(gd.cells);
     if (gd.clr) cudaFree(gd.clr);
-    if (stream_alt) cudaStreamSynchronize(stream_alt);
+    for (int q = 0; q < kSlots; ++q) {
+      if (stream_pool[q]) cudaStreamSynchronize(stream_pool[q]);
+      if (ordmap_pool[q]) cudaFree(ordmap_pool[q]);
+      if (stbits_pool[q]) cudaFree(stbits_pool[q]);
+      seg_pool[q].release();
+    }
     if (gd.ordmap) cudaFree(gd.ordmap);
     if (gd.stbits) cudaFree(gd.stbits);
-    if (ordmap_alt) cudaFree(ordmap_alt);
-    if (stbits_alt) cudaFree(stbits_alt);
-    seg_alt.release();
     if (gmap) cudaFree(gmap);
     if (gbits) cudaFree(gbits);
     sl.release();
     sf.release();
     if (mstream) cudaStreamSynchronize(mstream);
-    for (int q = 0; q < 2; ++q) {
+    for (int q = 0; q < kSlots; ++q) {
       if (ctr_s[q]) cudaFree(ctr_s[q]);
       if (d_fp_s[q]) cudaFree(d_fp_s[q]);
       if (h_ctr_s[q]) cudaFreeHost(h_ctr_s[q]);
@@ -485,7 +492,14 @@ struct vp_grid {
     for (auto& e : ev) if (e) cudaEventDestroy(e);
     if (stream) cudaStreamDestroy(stream);
     if (mstream) cudaStreamDestroy(mstream);
-    if (stream_alt) cudaStreamDestroy(stream_alt);
+    if (fstream) {
+      cudaStreamSynchronize(fstream);
+      cudaStreamDestroy(fstream);
+    }
+    for (auto& e : fork_ev)
+      if (e) cudaEventDestroy(e);
+    for (auto& q : stream_pool)
+      if (q) cudaStreamDestroy(q);
   }
 
   // ------------------------------------------------------------ set-up
@@ -502,7 +516,13 @@ struct vp_grid {
       origin[k] = c[k] - static_cast<double>(e[k]) * (0.5 * res);  // voxel_grid.cpp:23
     }
     ck(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "stream");
-    ck(cudaStreamCreateWithFlags(&mstream, cudaStreamNonBlocking), "stream");
+    {  // the mapping stream carries the pipelined run's critical path: highest priority
+      int lo = 0, hi = 0;
+      ck(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priority range");
+      ck(cudaStreamCreateWithPriority(&mstream, cudaStreamNonBlocking, hi), "stream");
+      ck(cudaStreamCreateWithPriority(&fstream, cudaStreamNonBlocking, hi), "stream");
+      for (auto& e : fork_ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    }
     lstream = stream;
     for (auto& x : ev) ck(cudaEventCreate(&x), "event");
     gd.ex = e[0];
@@ -528,7 +548,7 @@ struct vp_grid {
     ck(cudaMemsetAsync(occ[1], 0, gd.nwords * 4, stream), "memset occ");
     ck(cudaMemsetAsync(gd.ordmap, 0xff, C * 4, stream), "memset ordmap");
     ck(cudaMemsetAsync(gd.stbits, 0, gd.nwords * 4, stream), "memset stbits");
-    for (int q = 0; q < 2; ++q) {
+    for (int q = 0; q < kSlots; ++q) {
       ctr_s[q] = dalloc<Counters>(1);
       ck(cudaMemsetAsync(ctr_s[q], 0, sizeof(Counters), stream), "memset ctr");
       d_fp_s[q] = dalloc<FrameParams>(1);
@@ -597,7 +617,7 @@ struct vp_grid {
     launch_recenter();
     ck(cudaMemsetAsync(occ[0], 0, gd.nwords * 4, stream), "occ");
     ck(cudaMemsetAsync(occ[1], 0, gd.nwords * 4, stream), "occ");
-    for (int q = 0; q < 2; ++q) ck(cudaMemsetAsync(ctr_s[q], 0, sizeof(Counters), stream), "ctr");
+    for (int q = 0; q < kSlots; ++q) ck(cudaMemsetAsync(ctr_s[q], 0, sizeof(Counters), stream), "ctr");
     ck(cudaMemsetAsync(occ_total, 0, 8, stream), "occ total");
     ck(cudaStreamSynchronize(stream), "reset sync");
     cur = 0;
@@ -611,28 +631,33 @@ struct vp_grid {
   // Segmentation context of pipeline slot s (scratch, ordinal map, stream).
   void use_seg(int s) {
     if (s == seg_slot) return;
-    std::swap(seg, seg_alt);
-    std::swap(gd.ordmap, ordmap_alt);
-    std::swap(gd.stbits, stbits_alt);
-    std::swap(stream, stream_alt);
+    std::swap(seg, seg_pool[seg_slot]);  // park the active context
+    std::swap(gd.ordmap, ordmap_pool[seg_slot]);
+    std::swap(gd.stbits, stbits_pool[seg_slot]);
+    std::swap(stream, stream_pool[seg_slot]);
+    std::swap(seg, seg_pool[s]);  // activate s
+    std::swap(gd.ordmap, ordmap_pool[s]);
+    std::swap(gd.stbits, stbits_pool[s]);
+    std::swap(stream, stream_pool[s]);
     seg_slot = s;
   }
-  // The second context, with the first one's capacities.
-  void ensure_alt(int iterations) {
-    if (!stream_alt) {
-      ck(cudaStreamCreateWithFlags(&stream_alt, cudaStreamNonBlocking), "stream");
-      const uint64_t C = gd.ncells;
-      ordmap_alt = dalloc<int32_t>(C);
-      stbits_alt = dalloc<uint32_t>(gd.nwords);
-      ck(cudaMemsetAsync(ordmap_alt, 0xff, C * 4, stream_alt), "memset ordmap");
-      ck(cudaMemsetAsync(stbits_alt, 0, gd.nwords * 4, stream_alt), "memset stbits");
+  // Contexts 1 .. n-1 with context 0's capacities (call with context 0 active).
+  void ensure_contexts(int n, int iterations) {
+    for (int q = 1; q < n; ++q) {
+      if (!stream_pool[q]) {
+        ck(cudaStreamCreateWithFlags(&stream_pool[q], cudaStreamNonBlocking), "stream");
+        const uint64_t C = gd.ncells;
+        ordmap_pool[q] = dalloc<int32_t>(C);
+        stbits_pool[q] = dalloc<uint32_t>(gd.nwords);
+        ck(cudaMemsetAsync(ordmap_pool[q], 0xff, C * 4, stream_pool[q]), "memset ordmap");
+        ck(cudaMemsetAsync(stbits_pool[q], 0, gd.nwords * 4, stream_pool[q]), "memset stbits");
+      }
+      Seg& a = seg_pool[q];
+      a.ensure(std::max(a.b.Vcap, seg.b.Vcap), std::max(a.b.Scap, seg.b.Scap), std::max(a.b.Icap, seg.b.Icap),
+               iterations, gd.nwords);
+      a.ensure_dirs(16, stream_pool[q]);
+      ck(cudaStreamSynchronize(stream_pool[q]), "sync");
     }
-    Seg& a = seg_slot == 0 ? seg_alt : seg;
-    const Seg& m = seg_slot == 0 ? seg : seg_alt;
-    a.ensure(std::max(a.b.Vcap, m.b.Vcap), std::max(a.b.Scap, m.b.Scap), std::max(a.b.Icap, m.b.Icap), iterations,
-             gd.nwords);
-    a.ensure_dirs(16, seg_slot == 0 ? stream_alt : stream);
-    ck(cudaStreamSynchronize(stream_alt), "sync");
   }
   void set_slot(int s) {
     slot = s;
@@ -648,13 +673,13 @@ struct vp_grid {
     uint64_t cap = std::max<uint64_t>(n, 1 << 16);
     cap = std::max<uint64_t>(cap, pcap * 2);
     ck(cudaDeviceSynchronize(), "sync before realloc");
-    for (void* p : {(void*)d_pts_s[0], (void*)d_pts_s[1], (void*)hkey, (void*)hcnt, (void*)hoff,
-                    (void*)groups, (void*)pslot, (void*)prank, (void*)sorted, (void*)dense})
+    for (void* p : {(void*)hkey, (void*)hcnt, (void*)hoff, (void*)groups, (void*)pslot, (void*)prank,
+                    (void*)sorted, (void*)dense})
       if (p) cudaFree(p);
+    for (auto*& p : d_pts_s) dfree(p);
     uint64_t hs = 1;
     while (hs < 2 * cap) hs <<= 1;
-    d_pts_s[0] = dalloc<float>(3 * cap);
-    d_pts_s[1] = dalloc<float>(3 * cap);
+    for (auto*& p : d_pts_s) p = dalloc<float>(3 * cap);
     d_pts = d_pts_s[slot];
     hkey = dalloc<uint32_t>(hs);
     hcnt = dalloc<uint32_t>(hs);
@@ -744,12 +769,21 @@ struct vp_grid {
     LAUNCH(k_clear_apply, grid_for(gd.nwords), kThreads, 0, lstream, gd, d_fp, ctr);
   }
   void launch_integrate(uint64_t n) {
+    launch_integrate_group(n, lstream);
+    launch_integrate_fold(n);
+  }
+  // grouping of the points by voxel (reads only the points): independent of clear_rays
+  void launch_integrate_group(uint64_t n, cudaStream_t st) {
     if (n == 0 && !capturing) return;
     const int gp = grid_for(capturing ? pcap : n);
-    LAUNCH(k_integrate_hash, gp, kThreads, 0, lstream, gd, d_fp, ctr, hkey, hcnt, hmask, groups,
-           pslot, prank);
-    LAUNCH(k_integrate_offsets, gp, kThreads, 0, lstream, ctr, groups, hcnt, hoff);
-    LAUNCH(k_integrate_scatter, gp, kThreads, 0, lstream, d_fp, pslot, prank, hoff, sorted);
+    LAUNCH(k_integrate_hash, gp, kThreads, 0, st, gd, d_fp, ctr, hkey, hcnt, hmask, groups, pslot, prank);
+    LAUNCH(k_integrate_offsets, gp, kThreads, 0, st, ctr, groups, hcnt, hoff);
+    LAUNCH(k_integrate_scatter, gp, kThreads, 0, st, d_fp, pslot, prank, hoff, sorted);
+  }
+  // the ordered fold into the cells: after clear_rays (voxel_grid order)
+  void launch_integrate_fold(uint64_t n) {
+    if (n == 0 && !capturing) return;
+    const int gp = grid_for(capturing ? pcap : n);
     LAUNCH(k_integrate_fold, gp, kThreads, 0, lstream, gd, d_fp, ctr, groups, hkey, hcnt, hoff,
            sorted, dense);
     LAUNCH(k_integrate_fold_dense, 148, 1024, kDenseSmem, lstream, gd, d_fp, ctr, hkey, hcnt, hoff, sorted,
@@ -759,6 +793,19 @@ struct vp_grid {
     LAUNCH(k_recenter, grid_for(gd.nwords), kThreads, 0, lstream, gd, d_fp, ctr);
   }
   void launch_finalize() { LAUNCH(k_map_finalize, 1, 1, 0, lstream, ctr, occ_total); }
+  // clear_rays and the grouping half of integrate_frame in parallel (fork
+  // onto fstream, join before the ordered fold), then recenter, finalize.
+  void launch_mapping_forked(uint64_t n) {
+    ck(cudaEventRecord(fork_ev[0], lstream), "fork");
+    ck(cudaStreamWaitEvent(fstream, fork_ev[0], 0), "fork");
+    launch_integrate_group(n, fstream);
+    ck(cudaEventRecord(fork_ev[1], fstream), "join");
+    launch_clear(n);
+    ck(cudaStreamWaitEvent(lstream, fork_ev[1], 0), "join");
+    launch_integrate_fold(n);
+    launch_recenter();
+    launch_finalize();
+  }
 
   // Occupied scan of the post-recenter bitmap into seg.b.occ_list; ctr->V.
   void launch_occupied_scan() {
@@ -1051,18 +1098,18 @@ struct vp_pipeline {
   uint64_t graph_key = 0;
   uint64_t graph_kernels = 0;
   // pipelined runs: graphs per (slot, part: 0 mapping, 1 seg_a, 2 seg_b)
-  cudaGraphExec_t rx[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
-  uint64_t rkey[2][3] = {{0, 0, 0}, {0, 0, 0}};
-  uint64_t rkern[2][3] = {{0, 0, 0}, {0, 0, 0}};
-  cudaEvent_t ev_start[2] = {nullptr, nullptr}, ev_map[2] = {nullptr, nullptr};
-  cudaEvent_t ev_clu[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr};
+  cudaGraphExec_t rx[kSlots][3] = {};
+  uint64_t rkey[kSlots][3] = {};
+  uint64_t rkern[kSlots][3] = {};
+  cudaEvent_t ev_start[kSlots] = {}, ev_map[kSlots] = {};
+  cudaEvent_t ev_clu[kSlots] = {}, ev_done[kSlots] = {};
   ~vp_pipeline() {
     if (gexec) cudaGraphExecDestroy(gexec);
     for (auto& row : rx)
       for (auto& x : row)
         if (x) cudaGraphExecDestroy(x);
     for (auto* e : {ev_start, ev_map, ev_clu, ev_done})
-      for (int q = 0; q < 2; ++q)
+      for (int q = 0; q < kSlots; ++q)
         if (e[q]) cudaEventDestroy(e[q]);
     delete grid;
   }
@@ -1194,7 +1241,7 @@ void pipeline_run(vp_pipeline* pl, size_t nf, const float* const* xyz, const uin
                   const double* R, const double* t, bool device_ptrs, vp_frame_timing* timings) {
   vp_grid* g = pl->grid;
   for (auto* e : {pl->ev_start, pl->ev_map, pl->ev_clu, pl->ev_done})
-    for (int q = 0; q < 2; ++q)
+    for (int q = 0; q < kSlots; ++q)
       if (!e[q]) ck(cudaEventCreate(&e[q]), "event");
   uint64_t maxn = 0;
   for (size_t k = 0; k < nf; ++k) maxn = std::max(maxn, n[k]);
@@ -1205,15 +1252,24 @@ void pipeline_run(vp_pipeline* pl, size_t nf, const float* const* xyz, const uin
   if (static_cast<uint64_t>(pl->p.ransac.iterations) * kClusterBins > g->seg.cand_cap)
     g->seg.ensure(g->seg.b.Vcap, g->seg.b.Scap, g->seg.b.Icap, pl->p.ransac.iterations, g->gd.nwords);
   g->seg.ensure_dirs(16, g->stream);
-  if (nf >= 2) g->ensure_alt(pl->p.ransac.iterations);
+  const int nslot = static_cast<int>(std::min<size_t>(kSlots, std::max<size_t>(nf, 1)));
+  g->ensure_contexts(nslot, pl->p.ransac.iterations);
   ck(cudaStreamSynchronize(g->stream), "sync");
   const bool graphs = !g_prof_on && !std::getenv("VP_NO_GRAPH");
-  // frame k-2's slot is reused by frame k: its whole chain must be done
+  // frame k-kSlots's slot is reused by frame k: its whole chain must be done
   auto harvest = [&](size_t k) {
-    const int s = static_cast<int>(k & 1);
+    const int s = static_cast<int>(k % kSlots);
     if (g->h_ctr_s[s]->overflow & kOverflowClusters)
       fail(VP_ENOMEM, "more than 2048 clusters >= min_cluster_size in one frame");
     if (g->h_ctr_s[s]->overflow) fail(VP_ENOMEM, "segmentation capacity overflow in a pipelined frame");
+    if (std::getenv("VP_PIPE_STATS")) {  // stage spans of the pipelined frame (diagnostics)
+      float a = 0.f, b = 0.f, c = 0.f;
+      ck(cudaEventElapsedTime(&a, pl->ev_start[s], pl->ev_map[s]), "elapsed");
+      ck(cudaEventElapsedTime(&b, pl->ev_map[s], pl->ev_clu[s]), "elapsed");
+      ck(cudaEventElapsedTime(&c, pl->ev_clu[s], pl->ev_done[s]), "elapsed");
+      std::fprintf(stderr, "frame %zu: map %.1f us, grid readers %.1f us, chain %.1f us\n", k, 1e3 * a, 1e3 * b,
+                   1e3 * c);
+    }
     if (!timings) return;
     float ms = 0.f;
     ck(cudaEventElapsedTime(&ms, pl->ev_start[s], pl->ev_done[s]), "elapsed");
@@ -1225,10 +1281,11 @@ void pipeline_run(vp_pipeline* pl, size_t nf, const float* const* xyz, const uin
     tm.clusters = g->h_ctr_s[s]->K;
   };
   for (size_t k = 0; k < nf; ++k) {
-    const int s = static_cast<int>(k & 1);
-    if (k >= 2) {
+    const int s = static_cast<int>(k % kSlots);
+    const int prev = static_cast<int>((k + kSlots - 1) % kSlots);
+    if (k >= static_cast<size_t>(kSlots)) {
       ck(cudaEventSynchronize(pl->ev_done[s]), "slot sync");
-      harvest(k - 2);
+      harvest(k - kSlots);
     }
     g->set_slot(s);
     g->use_seg(s);
@@ -1250,24 +1307,23 @@ void pipeline_run(vp_pipeline* pl, size_t nf, const float* const* xyz, const uin
       std::memcpy(pl->last_cell, cell, sizeof cell);
     }
     // mapping of frame k: after frame k-1 stopped reading the grid
-    if (k >= 1) ck(cudaStreamWaitEvent(g->mstream, pl->ev_clu[s ^ 1], 0), "wait");
+    if (k >= 1) ck(cudaStreamWaitEvent(g->mstream, pl->ev_clu[prev], 0), "wait");
     ck(cudaEventRecord(pl->ev_start[s], g->mstream), "ev");
     g->lstream = g->mstream;
     auto map_part = [&] {
       g->upload_params();
       g->reset_frame_counters();
-      g->launch_clear(n[k]);
-      g->launch_integrate(n[k]);
-      g->launch_recenter();
-      g->launch_finalize();
+      g->launch_mapping_forked(n[k]);
     };
     if (graphs) run_part_graph(pl, 0, g->mstream, map_part); else map_part();
     g->lstream = g->stream;
     ck(cudaEventRecord(pl->ev_map[s], g->mstream), "ev");
-    // segmentation of frame k on the slot's stream: the grid readers first
-    // (occupied scan .. ordinal map), then the CCL .. polygon chain, which
-    // overlaps frame k+1's mapping and the start of its own chain
-    ck(cudaStreamWaitEvent(g->stream, pl->ev_map[s], 0), "wait");
+    // segmentation of frame k: the grid readers (occupied scan .. ordinal
+    // map) right after the mapping on the high-priority mapping stream (the
+    // critical path: frame k+1's mapping waits for them), then the CCL ..
+    // polygon chain on the slot's stream, overlapping later frames
+    const cudaStream_t slot_stream = g->stream;
+    g->stream = g->mstream;
     auto seg_grid = [&] {
       g->launch_seg_a1(pl->p, false);
       ck(cudaMemcpyAsync(g->h_ctr, g->ctr, sizeof(Counters), cudaMemcpyDeviceToHost, g->stream), "ctr");
@@ -1279,25 +1335,29 @@ void pipeline_run(vp_pipeline* pl, size_t nf, const float* const* xyz, const uin
     };
     if (graphs) run_part_graph(pl, 1, g->stream, seg_grid); else seg_grid();
     ck(cudaEventRecord(pl->ev_clu[s], g->stream), "ev");
+    g->stream = slot_stream;
+    ck(cudaStreamWaitEvent(g->stream, pl->ev_clu[s], 0), "wait");
+    // the chain is enqueued before the host looks at the capacities (it only
+    // reads this slot's buffers, clamped to their capacities, and is redone
+    // below after an overflow)
+    if (graphs) run_part_graph(pl, 2, g->stream, seg_rest); else seg_rest();
+    ck(cudaEventRecord(pl->ev_done[s], g->stream), "ev");
     // capacity check point: frame k+1 has not touched the grid yet
     ck(cudaEventSynchronize(pl->ev_clu[s]), "sync");
     if (g->h_ctr->overflow) {
       ck(cudaStreamSynchronize(g->stream), "sync");
       rerun_segment_until_fits(g, pl->p);  // whole segmentation, synchronous
       ck(cudaEventRecord(pl->ev_done[s], g->stream), "ev");
-    } else {
-      if (graphs) run_part_graph(pl, 2, g->stream, seg_rest); else seg_rest();
-      ck(cudaEventRecord(pl->ev_done[s], g->stream), "ev");
     }
     ++pl->frame;
   }
-  for (int q = 0; q < 2; ++q) {
+  for (int q = 0; q < nslot; ++q) {
     g->use_seg(q);
     ck(cudaStreamSynchronize(g->stream), "sync");
   }
   ck(cudaStreamSynchronize(g->mstream), "sync");
-  for (size_t k = nf >= 2 ? nf - 2 : 0; k < nf; ++k) harvest(k);
-  const int last = nf ? static_cast<int>((nf - 1) & 1) : 0;
+  for (size_t k = nf >= static_cast<size_t>(kSlots) ? nf - kSlots : 0; k < nf; ++k) harvest(k);
+  const int last = nf ? static_cast<int>((nf - 1) % kSlots) : 0;
   g->set_slot(last);
   g->use_seg(last);  // the final frame's results (callers switch back with use_seg(0))
   g->host_occupied = g->h_ctr->occupied;
