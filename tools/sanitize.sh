@@ -1,0 +1,31 @@
+# compute-sanitizer runs (memcheck / racecheck / synccheck / initcheck) over
+# small end-to-end workloads: the smoke stream, a pipelined C2 run of 4
+# frames, the slab path with 3 virtual slabs, the device frame source.
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+S=/usr/local/cuda/bin/compute-sanitizer
+cat > gpurun_out/san_work.py <<'PY'
+import os, sys
+sys.path.insert(0, os.getcwd()); sys.path.insert(0, os.path.join(os.getcwd(), "tests"))
+import numpy as np, torch
+import __graft_entry__ as ge
+from paper_2510_01592_b200 import native, scenes, slabs
+ge.smoke()
+w = scenes.workload("c2", frames=4)
+pl = native.Pipeline(w.resolution, (300, 300, 300), w.frames[0].translation, native.default_params(seed=w.seed))
+pl.run(w.frames)
+ss = [slabs.Slab(0.01, (300, 200, 150), (0.0, 0.0, 0.5), a, b) for a, b in [(0, 100), (100, 103), (103, 300)]]
+comm = slabs.LocalComm(3)
+for f in scenes.stair_frames(3):
+    slabs.slab_frame(ss, comm, torch.from_numpy(np.ascontiguousarray(f.points)).cuda(), f.rotation, f.translation,
+                     native.default_params(seed=5))
+ws = scenes.workload_spec("c2", 1)
+src = scenes.DeviceFrameSource(ws.scene, ws.sensor, ws.seed)
+src.render(ws.poses[0], 0)
+print("sanitizer workload done")
+PY
+for tool in memcheck racecheck synccheck; do
+  VP_NO_GRAPH=1 timeout 1500 $S --tool $tool --print-limit 20 python gpurun_out/san_work.py > gpurun_out/san_$tool.log 2>&1
+  echo "$tool rc=$?" >> gpurun_out/san_$tool.log
+done
+for f in gpurun_out/san_*.log; do tail -n 4 $f; done
