@@ -325,23 +325,114 @@ __global__ void __launch_bounds__(1024) k_integrate_fold_dense(GridDesc g, const
 // then counts unique cells, frees occupied ones and zeroes the mask.
 // ---------------------------------------------------------------------------
 // One thread per ray (voxel_grid.cpp:122-178, the reference's DDA arithmetic
-// verbatim). The loop keeps the cell's 32-bit bitmap word index incrementally
-// and selects the stepped axis without branches; each traversed interior cell
-// is marked with a fire-and-forget RED.OR; lanes of the warp standing in the
-// same cell as their left neighbour this iteration (adjacent pixels near the
-// sensor) skip it. Nothing in the loop waits on memory.
+// verbatim); every traversed interior cell is marked in a clear mask with a
+// fire-and-forget RED.OR, and k_clear_apply then counts unique cells, frees
+// the occupied ones and zeroes the mask. Marking is the bottleneck (L2
+// atomic throughput: without marks the C4 walk takes 0.4 ms instead of 2.0),
+// so it follows the rays' coherence (k_dda_plan's per-frame decision):
+//  * coherent rays (depth images: adjacent lanes walk nearly the same cells
+//    near the sensor): row-layout mask, a lane in the same cell as its left
+//    neighbour this iteration skips the RED;
+//  * incoherent rays (LiDAR patterns): rays walked longest-first (lane
+//    balance), 4x4x2-brick mask, a ray accumulates the bits of the brick it
+//    is in and issues one RED when it leaves it (C4: 2.4 -> 1.4 ms).
 //
-// Per-step work is kept minimal (the kernel is issue/FP64-bound, not
-// memory-bound): the reference loop "visit unless origin or end cell; argmin;
-// step; bounds; t_max[m] += t_delta[m]" is rotated so the origin test runs
-// once (the DDA is monotone per axis: once it left the first cell it never
-// returns, and the first cell is the origin cell whenever the origin lies in
-// the window), the end-cell test is one compare of the cell's bitmap key
-// (word << 5 | bit, injective over the grid's cells), and only the stepped
-// axis' t_max is advanced (one DADD). kSlab adds the owned-x-range logic of a
-// spatial slab.
+// Work binning for unbalanced ray sets. k_dda_keys estimates each ray's DDA
+// length as the L1 cell distance sensor -> end point (original order), bins
+// it (32-step bins), and measures how balanced 32-ray groups are; k_dda_plan
+// turns binning on only when groups would waste > 25 % of their lanes, and
+// k_dda_scatter then lists the rays longest-bin first. The marks are ORs and
+// every count is taken afterwards from the bitmap, so the walk order does
+// not change any result.
+__global__ void k_dda_keys(GridDesc g, const FrameParams* __restrict__ fp, DdaBins* db, uint8_t* bin_of) {
+  __shared__ uint32_t hist[kDdaBins];
+  for (int b = threadIdx.x; b < kDdaBins; b += blockDim.x) hist[b] = 0;
+  __syncthreads();
+  const uint64_t n = fp->n;
+  const double res = g.res;
+  unsigned long long sum = 0, wmax = 0;
+  for (uint64_t i0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u); i0 < n;
+       i0 += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t i = i0 + lane_id();
+    uint32_t st = 0;
+    if (i < n) {
+      const float* pp = fp->pts + 3 * i;
+      const d3 bw = pose_apply(fp->R, fp->t, static_cast<double>(pp[0]), static_cast<double>(pp[1]),
+                               static_cast<double>(pp[2]));
+      if (finite3(bw)) {
+        const double e0 = fabs(bw.x - fp->t[0]) / res, e1 = fabs(bw.y - fp->t[1]) / res,
+                     e2 = fabs(bw.z - fp->t[2]) / res;
+        const double l1 = e0 + e1 + e2 + 3.0;
+        st = l1 < 4.0e9 ? static_cast<uint32_t>(l1) : 0xffffffffu;
+      }
+      const uint32_t b = min(static_cast<uint32_t>(kDdaBins - 1), st >> 5);
+      bin_of[i] = static_cast<uint8_t>(b);
+      atomicAdd(&hist[b], 1u);
+    }
+    const uint32_t mx = __reduce_max_sync(0xffffffffu, st);
+    if (lane_id() == 0) wmax += 32ull * mx;
+    sum += st;
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < kDdaBins; b += blockDim.x)
+    if (hist[b]) atomicAdd(&db->count[b], hist[b]);
+  warp_add_u64(&db->steps, sum);
+  warp_add_u64(&db->warp_max, wmax);
+}
+
+// One warp: decide, and lay the bins out longest first; resets the counts.
+__global__ void k_dda_plan(DdaBins* db) {
+  const unsigned lane = lane_id();
+  const int use = db->steps * 4 < db->warp_max * 3 ? 1 : 0;  // lane efficiency < 75 %
+  uint32_t run = 0;
+  for (int b0 = kDdaBins - 32; b0 >= 0; b0 -= 32) {  // descending bins
+    const int b = b0 + 31 - static_cast<int>(lane);
+    const uint32_t c = db->count[b];
+    uint32_t incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (static_cast<int>(lane) >= o) incl += t;
+    }
+    db->cursor[b] = run + incl - c;
+    run += __shfl_sync(0xffffffffu, incl, 31);
+    db->count[b] = 0;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    db->use = use;
+    db->steps = 0;
+    db->warp_max = 0;
+  }
+}
+
+__global__ void k_dda_scatter(const FrameParams* __restrict__ fp, DdaBins* db, const uint8_t* __restrict__ bin_of,
+                              uint32_t* perm) {
+  if (!db->use) return;
+  const uint64_t n = fp->n;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const int b = bin_of[i];
+    const unsigned peers = __match_any_sync(__activemask(), b);
+    const int leader = __ffs(peers) - 1;
+    uint32_t base = 0;
+    if (static_cast<int>(lane_id()) == leader) base = atomicAdd(&db->cursor[b], static_cast<uint32_t>(__popc(peers)));
+    base = __shfl_sync(peers, base, leader);
+    perm[base + __popc(peers & lanemask_lt())] = static_cast<uint32_t>(i);
+  }
+}
+
+// Per-step work is kept minimal: the reference loop "visit unless origin or
+// end cell; argmin; step; bounds; t_max[m] += t_delta[m]" is rotated so the
+// origin test runs once (the DDA is monotone per axis: once it left the first
+// cell it never returns, and the first cell is the origin cell whenever the
+// origin lies in the window), the end-cell test is one compare of the cell's
+// mask key (word << 5 | bit, injective over the grid's cells), and only the
+// stepped axis' t_max is advanced (one DADD). kSlab adds the owned-x-range
+// logic of a spatial slab.
 template <bool kSlab>
-__device__ __forceinline__ void clear_walk_body(const GridDesc& g, const FrameParams* __restrict__ fp) {
+__device__ __forceinline__ void clear_walk_body(const GridDesc& g, const FrameParams* __restrict__ fp,
+                                                const uint32_t* __restrict__ perm, const DdaBins* db) {
   const uint64_t n = fp->n;
   const double res = g.res;
   const double lo0 = fp->origin_pre[0], lo1 = fp->origin_pre[1], lo2 = fp->origin_pre[2];
@@ -352,13 +443,20 @@ __device__ __forceinline__ void clear_walk_body(const GridDesc& g, const FramePa
   const int oc0 = w2i(a0, lo0, res), oc1 = w2i(a1, lo1, res), oc2 = w2i(a2, lo2, res);
   const int max_steps = g.gex + g.ey + g.ez + 4;
   const int own0 = g.xoff + g.own_lo, own1 = g.xoff + g.own_hi;  // window x owned here
+  uint32_t* __restrict__ clr = g.clr;
+  uint32_t* __restrict__ clrb = g.clrb;
   const uint32_t xstride = static_cast<uint32_t>(g.ey) * static_cast<uint32_t>(g.W);
   const uint32_t ystride = static_cast<uint32_t>(g.W);
-  uint32_t* __restrict__ clr = g.clr;
   const unsigned lane = lane_id();
   const unsigned left = lane ? (1u << (lane - 1)) : 0u;  // the lane to my left
-  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+  // k_dda_plan's decision: incoherent, unbalanced rays (LiDAR patterns) are
+  // walked in length order and accumulate their marks per brick; coherent
+  // rays (depth images) dedup per cell against the neighbouring lane
+  const bool accumulate = db->use != 0;
+  const bool binned = accumulate;
+  for (uint64_t r = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < n;
+       r += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t i = binned ? perm[r] : r;
     const float* pp = fp->pts + 3 * i;
     const d3 bw = pose_apply(fp->R, fp->t, static_cast<double>(pp[0]), static_cast<double>(pp[1]),
                              static_cast<double>(pp[2]));
@@ -412,17 +510,21 @@ __device__ __forceinline__ void clear_walk_body(const GridDesc& g, const FramePa
     VP_INIT(d1, c1, lo1, e1, s1, tm1, td1)
     VP_INIT(d2, c2, lo2, e2, s2, tm2, td2)
 #undef VP_INIT
-    // bitmap key of a cell of this grid: word << 5 | bit (meaningful while c0
+    // brick key of a cell of this grid: word << 5 | bit (meaningful while c0
     // is stored here; the end cell's key only when it is owned here)
     const bool e_here = ec0 >= own0 && ec0 < own1 && static_cast<unsigned>(ec1) < static_cast<unsigned>(g.ey) &&
                         static_cast<unsigned>(ec2) < static_cast<unsigned>(g.ez);
     const uint32_t key_e =
+        e_here ? ((brick_word(g, ec0 - g.xoff, ec1, ec2) << 5) | brick_bit(ec0 - g.xoff, ec1, ec2)) : 0xffffffffu;
+    bool mark = !(c0 == oc0 && c1 == oc1 && c2 == oc2);  // origin cell: first cell only
+    uint32_t aw = 0xffffffffu, ab = 0;  // marks of the current brick, flushed when the ray leaves it
+    // row-layout word index of the current cell (coherent path, incremental)
+    uint32_t row = static_cast<uint32_t>(c0 - g.xoff) * xstride + static_cast<uint32_t>(c1) * ystride;
+    const int dx_row = s0 * static_cast<int>(xstride), dy_row = s1 * static_cast<int>(ystride);
+    const uint32_t key_er =
         e_here ? (((static_cast<uint32_t>(ec0 - g.xoff) * xstride + static_cast<uint32_t>(ec1) * ystride +
                     (static_cast<uint32_t>(ec2) >> 5)) << 5) | (static_cast<uint32_t>(ec2) & 31u))
                : 0xffffffffu;
-    uint32_t row = static_cast<uint32_t>(c0 - g.xoff) * xstride + static_cast<uint32_t>(c1) * ystride;
-    const int dx_row = s0 * static_cast<int>(xstride), dy_row = s1 * static_cast<int>(ystride);
-    bool mark = !(c0 == oc0 && c1 == oc1 && c2 == oc2);  // origin cell: first cell only
     for (int s = 0; s < max_steps; ++s) {
       if (s > 0) {
         // m = argmin t_max, ties to the lower axis (voxel_grid.cpp:170-172)
@@ -458,25 +560,42 @@ __device__ __forceinline__ void clear_walk_body(const GridDesc& g, const FramePa
         if ((s0 > 0 && c0 >= own1) || (s0 < 0 && c0 < own0) || (s0 == 0 && (c0 < own0 || c0 >= own1))) break;
         here = c0 >= own0 && c0 < own1;  // not yet entered: skip
       }
-      const uint32_t w = row + (static_cast<uint32_t>(c2) >> 5);
-      const uint32_t key = (w << 5) | (static_cast<uint32_t>(c2) & 31u);
-      if (mark && here && key != key_e) {
-        // adjacent pixels stand in the same cell as runs of lanes: only the
-        // first lane of each run issues the RED
+      if (!mark || !here) continue;
+      if (accumulate) {  // incoherent rays: one RED per brick the ray crosses
+        const int lx = c0 - g.xoff;
+        const uint32_t w = brick_word(g, lx, c1, c2);
+        const uint32_t bit = brick_bit(lx, c1, c2);
+        if (((w << 5) | bit) == key_e) continue;
+        if (w != aw) {
+          if (ab) atomicOr(clrb + aw, ab);
+          aw = w;
+          ab = 0;
+        }
+        ab |= 1u << bit;
+      } else {  // coherent rays: lanes in the same cell as their left neighbour skip it
+        const uint32_t w = row + (static_cast<uint32_t>(c2) >> 5);
+        const uint32_t key = (w << 5) | (static_cast<uint32_t>(c2) & 31u);
+        if (key == key_er) continue;
         const unsigned act = __activemask();
         const uint32_t prev = __shfl_up_sync(act, key, 1);
         const bool dup = (act & left) && prev == key;
         if (!dup) atomicOr(clr + w, 1u << (c2 & 31));
       }
     }
+    if (ab) atomicOr(clrb + aw, ab);
   }
 }
 
-__global__ void __launch_bounds__(256, 4) k_clear_walk(GridDesc g, const FrameParams* __restrict__ fp) {
-  clear_walk_body<false>(g, fp);
+#ifndef VP_DDA_MINB
+#define VP_DDA_MINB 4
+#endif
+__global__ void __launch_bounds__(256, VP_DDA_MINB) k_clear_walk(GridDesc g, const FrameParams* __restrict__ fp,
+                                                                  const uint32_t* perm, const DdaBins* db) {
+  clear_walk_body<false>(g, fp, perm, db);
 }
-__global__ void __launch_bounds__(256, 4) k_clear_walk_slab(GridDesc g, const FrameParams* __restrict__ fp) {
-  clear_walk_body<true>(g, fp);
+__global__ void __launch_bounds__(256, 4) k_clear_walk_slab(GridDesc g, const FrameParams* __restrict__ fp,
+                                                            const uint32_t* perm, const DdaBins* db) {
+  clear_walk_body<true>(g, fp, perm, db);
 }
 
 __device__ __forceinline__ void zero_cell(Cell* c) {
@@ -487,7 +606,9 @@ __device__ __forceinline__ void zero_cell(Cell* c) {
   c->status = 0;
 }
 
-__global__ void k_clear_apply(GridDesc g, const FrameParams* __restrict__ fp, Counters* ctr) {
+// Row-layout clear mask (coherent rays): one thread per bitmap word.
+__global__ void k_clear_apply(GridDesc g, const FrameParams* __restrict__ fp, Counters* ctr, const DdaBins* db) {
+  if (db->use) return;
   uint32_t* occ = fp->occ_pre;
   unsigned long long cl = 0, fr = 0;
   for (uint64_t w = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; w < g.nwords;
@@ -508,6 +629,45 @@ __global__ void k_clear_apply(GridDesc g, const FrameParams* __restrict__ fp, Co
       const int b = __ffs(f) - 1;
       f &= f - 1;
       zero_cell(g.cells + phys_index(g, fp->off_pre, x, y, z0 + b));
+    }
+  }
+  warp_add_u64(&ctr->cleared, cl);
+  warp_add_u64(&ctr->freed, fr);
+}
+
+// Brick-layout clear mask (incoherent rays): one thread per brick word: count
+// the unique cleared cells, free the occupied ones (the occupancy bits of the
+// brick's 16 (x, y) columns are gathered from the row-layout bitmap, two z
+// bits each), zero the mask.
+__global__ void k_clear_apply_brick(GridDesc g, const FrameParams* __restrict__ fp, Counters* ctr,
+                                    const DdaBins* db) {
+  if (!db->use) return;
+  uint32_t* occ = fp->occ_pre;
+  unsigned long long cl = 0, fr = 0;
+  for (uint64_t w = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; w < g.nbricks;
+       w += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t c = g.clrb[w];
+    if (!c) continue;
+    g.clrb[w] = 0;
+    cl += __popc(c);
+    const uint32_t bz = static_cast<uint32_t>(w % g.bnz);
+    const uint64_t r = w / g.bnz;
+    const int by = static_cast<int>(r % g.bny), bx = static_cast<int>(r / g.bny);
+    const int z0 = static_cast<int>(bz) * 2;
+    const int wz = z0 >> 5, sh = z0 & 31;  // both z of the brick lie in one occupancy word
+    uint32_t cols = c;
+    while (cols) {  // (lx, ly) columns with marks: bits 2k, 2k+1
+      const int k = (__ffs(cols) - 1) >> 1;
+      const uint32_t cm = (c >> (2 * k)) & 3u;
+      cols &= ~(3u << (2 * k));
+      const int x = bx * 4 + (k >> 2), y = by * 4 + (k & 3);
+      uint32_t* ow = occ + (static_cast<uint64_t>(x) * g.ey + y) * g.W + wz;
+      const uint32_t f = (*ow >> sh) & cm;
+      if (!f) continue;
+      atomicAnd(ow, ~(f << sh));  // other bricks share this occupancy word
+      fr += __popc(f);
+      for (int b = 0; b < 2; ++b)
+        if (f & (1u << b)) zero_cell(g.cells + phys_index(g, fp->off_pre, x, y, z0 + b));
     }
   }
   warp_add_u64(&ctr->cleared, cl);

@@ -446,6 +446,9 @@ struct vp_grid {
   uint32_t* prank = nullptr;
   uint32_t* sorted = nullptr;
   uint32_t* dense = nullptr;  // slots of integrate groups > kFoldMax points
+  uint32_t* rperm = nullptr;  // clear_rays: rays in bin order (when binning is on)
+  uint8_t* bin_of = nullptr;  // clear_rays: length bin per ray
+  DdaBins* dbins = nullptr;
   Seg seg;
   cudaEvent_t ev[8];
   // window-sized ordinal map for segmenting a gathered slab steppable list
@@ -465,6 +468,7 @@ struct vp_grid {
     for (auto* p : {occ[0], occ[1]}) if (p) cudaFree(p);
     if (gd.cells) cudaFree(gd.cells);
     if (gd.clr) cudaFree(gd.clr);
+    if (gd.clrb) cudaFree(gd.clrb);
     for (int q = 0; q < kSlots; ++q) {
       if (stream_pool[q]) cudaStreamSynchronize(stream_pool[q]);
       if (ordmap_pool[q]) cudaFree(ordmap_pool[q]);
@@ -487,7 +491,8 @@ struct vp_grid {
     }
     if (occ_total) cudaFree(occ_total);
     for (void* p : {(void*)hkey, (void*)hcnt, (void*)hoff, (void*)groups,
-                    (void*)pslot, (void*)prank, (void*)sorted, (void*)dense})
+                    (void*)pslot, (void*)prank, (void*)sorted, (void*)dense, (void*)rperm, (void*)bin_of,
+                    (void*)dbins})
       if (p) cudaFree(p);
     for (auto& e : ev) if (e) cudaEventDestroy(e);
     if (stream) cudaStreamDestroy(stream);
@@ -537,13 +542,20 @@ struct vp_grid {
     gd.own_hi = e[0];
     gd.gex = e[0];
     gd.cells = dalloc<Cell>(C);
+    gd.bnx = (e[0] + 3) / 4;
+    gd.bny = (e[1] + 3) / 4;
+    gd.bnz = (e[2] + 1) / 2;
+    gd.nbricks = static_cast<uint64_t>(gd.bnx) * gd.bny * gd.bnz;
+    if (gd.nbricks * 32 >= 0xffffffffull) fail(VP_EINVAL, "VoxelGrid: more than 2^32 cells per grid (use slabs)");
     gd.clr = dalloc<uint32_t>(gd.nwords);
+    gd.clrb = dalloc<uint32_t>(gd.nbricks);
     gd.ordmap = dalloc<int32_t>(C);
     gd.stbits = dalloc<uint32_t>(gd.nwords);
     occ[0] = dalloc<uint32_t>(gd.nwords);
     occ[1] = dalloc<uint32_t>(gd.nwords);
     ck(cudaMemsetAsync(gd.cells, 0, C * sizeof(Cell), stream), "memset cells");
     ck(cudaMemsetAsync(gd.clr, 0, gd.nwords * 4, stream), "memset clr");
+    ck(cudaMemsetAsync(gd.clrb, 0, gd.nbricks * 4, stream), "memset clrb");
     ck(cudaMemsetAsync(occ[0], 0, gd.nwords * 4, stream), "memset occ");
     ck(cudaMemsetAsync(occ[1], 0, gd.nwords * 4, stream), "memset occ");
     ck(cudaMemsetAsync(gd.ordmap, 0xff, C * 4, stream), "memset ordmap");
@@ -674,7 +686,7 @@ struct vp_grid {
     cap = std::max<uint64_t>(cap, pcap * 2);
     ck(cudaDeviceSynchronize(), "sync before realloc");
     for (void* p : {(void*)hkey, (void*)hcnt, (void*)hoff, (void*)groups, (void*)pslot, (void*)prank,
-                    (void*)sorted, (void*)dense})
+                    (void*)sorted, (void*)dense, (void*)rperm, (void*)bin_of})
       if (p) cudaFree(p);
     for (auto*& p : d_pts_s) dfree(p);
     uint64_t hs = 1;
@@ -689,6 +701,12 @@ struct vp_grid {
     prank = dalloc<uint32_t>(cap);
     sorted = dalloc<uint32_t>(cap);
     dense = dalloc<uint32_t>(cap / (kFoldMax + 1) + 1);
+    rperm = dalloc<uint32_t>(cap);
+    bin_of = dalloc<uint8_t>(cap);
+    if (!dbins) {
+      dbins = dalloc<DdaBins>(1);
+      ck(cudaMemsetAsync(dbins, 0, sizeof(DdaBins), stream), "dbins");
+    }
     ck(cudaMemsetAsync(hkey, 0xff, hs * 4, stream), "hkey");
     ck(cudaMemsetAsync(hcnt, 0, hs * 4, stream), "hcnt");
     hmask = static_cast<uint32_t>(hs - 1);
@@ -762,11 +780,17 @@ struct vp_grid {
   // the device params), so the same launches can be replayed as a graph.
   void launch_clear(uint64_t n) {
     if (n == 0 && !capturing) return;
+    const int gp = grid_for(capturing ? pcap : n);
+    LAUNCH(k_dda_keys, gp, kThreads, 0, lstream, gd, d_fp, dbins, bin_of);
+    LAUNCH(k_dda_plan, 1, 32, 0, lstream, dbins);
+    LAUNCH(k_dda_scatter, gp, kThreads, 0, lstream, d_fp, dbins, bin_of, rperm);
     if (gd.xoff != 0 || gd.gex != gd.ex)
-      LAUNCH(k_clear_walk_slab, grid_for(capturing ? pcap : n, 148 * 32), kThreads, 0, lstream, gd, d_fp);
+      LAUNCH(k_clear_walk_slab, grid_for(capturing ? pcap : n, 148 * 32), kThreads, 0, lstream, gd, d_fp, rperm,
+             dbins);
     else
-      LAUNCH(k_clear_walk, grid_for(capturing ? pcap : n, 148 * 32), kThreads, 0, lstream, gd, d_fp);
-    LAUNCH(k_clear_apply, grid_for(gd.nwords), kThreads, 0, lstream, gd, d_fp, ctr);
+      LAUNCH(k_clear_walk, grid_for(capturing ? pcap : n, 148 * 32), kThreads, 0, lstream, gd, d_fp, rperm, dbins);
+    LAUNCH(k_clear_apply, grid_for(gd.nwords), kThreads, 0, lstream, gd, d_fp, ctr, dbins);
+    LAUNCH(k_clear_apply_brick, grid_for(gd.nbricks), kThreads, 0, lstream, gd, d_fp, ctr, dbins);
   }
   void launch_integrate(uint64_t n) {
     launch_integrate_group(n, lstream);

@@ -67,7 +67,23 @@ struct GridDesc {
   // x extent (ray clipping and point bounds use the whole window). A plain
   // grid has xoff = 0, own = [0, ex), gex = ex.
   int32_t xoff, own_lo, own_hi, gex;
+  // clear_rays mark bitmap for incoherent rays `clrb` in 4 x 4 x 2 bricks
+  // (one 32-bit word per brick, local coordinates): a ray sets several bits
+  // of a word before it leaves the brick, so it issues one RED per brick
+  // instead of per cell. (Coherent rays use `clr`, occupancy row layout.)
+  uint32_t* clrb;
+  int32_t bnx, bny, bnz;
+  uint64_t nbricks;
 };
+
+__device__ __forceinline__ uint32_t brick_word(const GridDesc& g, int lx, int y, int z) {
+  return (static_cast<uint32_t>(lx >> 2) * static_cast<uint32_t>(g.bny) + static_cast<uint32_t>(y >> 2)) *
+             static_cast<uint32_t>(g.bnz) +
+         static_cast<uint32_t>(z >> 1);
+}
+__device__ __forceinline__ uint32_t brick_bit(int lx, int y, int z) {
+  return (static_cast<uint32_t>(lx & 3) << 3) | (static_cast<uint32_t>(y & 3) << 1) | static_cast<uint32_t>(z & 1);
+}
 
 // Device counters (one struct in device memory, zeroed per frame except
 // `occupied`, which persists like VoxelGrid::occupied_).

@@ -240,6 +240,17 @@ struct MemberRec {
   int32_t pad;
 };
 
+// clear_rays work binning (k_map.cu): rays grouped by estimated DDA length
+// when warps of consecutive rays would be badly unbalanced (LiDAR patterns).
+constexpr int kDdaBins = 64;
+struct DdaBins {
+  uint32_t count[kDdaBins];
+  uint32_t cursor[kDdaBins];
+  unsigned long long steps;     // sum of estimated steps
+  unsigned long long warp_max;  // sum over 32-ray groups of 32 x their longest ray
+  int use;                      // 1: walk rays in bin order (perm), 0: identity
+};
+
 // ---- kernels (k_map.cu)
 __global__ void k_integrate_hash(GridDesc g, const FrameParams* fp, Counters* ctr, uint32_t* hkey,
                                  uint32_t* hcnt, uint32_t hmask, uint32_t* groups, uint32_t* pslot,
@@ -255,9 +266,13 @@ __global__ void k_integrate_fold_dense(GridDesc g, const FrameParams* fp, Counte
                                        uint32_t* hcnt, const uint32_t* hoff, const uint32_t* sorted,
                                        const uint32_t* pslot, const uint32_t* dense);
 constexpr int kDenseSmem = 1024 * 24 + 16384 * 4;  // k_integrate_fold_dense dynamic shared memory
-__global__ void k_clear_walk(GridDesc g, const FrameParams* fp);
-__global__ void k_clear_walk_slab(GridDesc g, const FrameParams* fp);
-__global__ void k_clear_apply(GridDesc g, const FrameParams* fp, Counters* ctr);
+__global__ void k_clear_walk(GridDesc g, const FrameParams* fp, const uint32_t* perm, const DdaBins* db);
+__global__ void k_clear_walk_slab(GridDesc g, const FrameParams* fp, const uint32_t* perm, const DdaBins* db);
+__global__ void k_dda_keys(GridDesc g, const FrameParams* fp, DdaBins* db, uint8_t* bin_of);
+__global__ void k_dda_plan(DdaBins* db);
+__global__ void k_dda_scatter(const FrameParams* fp, DdaBins* db, const uint8_t* bin_of, uint32_t* perm);
+__global__ void k_clear_apply(GridDesc g, const FrameParams* fp, Counters* ctr, const DdaBins* db);
+__global__ void k_clear_apply_brick(GridDesc g, const FrameParams* fp, Counters* ctr, const DdaBins* db);
 __global__ void k_recenter(GridDesc g, const FrameParams* fp, Counters* ctr);
 __global__ void k_map_finalize(Counters* ctr, unsigned long long* occ_total);
 __global__ void k_frame_begin(Counters* ctr, const unsigned long long* occ_total);

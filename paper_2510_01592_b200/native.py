@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "lib", "libvoxplane_b200.so")
+LIB_PATH = os.environ.get("VP_LIB") or os.path.join(PKG, "lib", "libvoxplane_b200.so")  # VP_LIB: experiments only
 
 VP_OK, VP_EINVAL, VP_EEMPTY, VP_ENOMEM, VP_ECUDA, VP_ENODEV = range(6)
 
