@@ -334,7 +334,7 @@ __global__ void __launch_bounds__(1024) k_integrate_fold_dense(GridDesc g, const
 //    near the sensor): row-layout mask, a lane in the same cell as its left
 //    neighbour this iteration skips the RED;
 //  * incoherent rays (LiDAR patterns): rays walked longest-first (lane
-//    balance), 4x4x2-brick mask, a ray accumulates the bits of the brick it
+//    balance), 4x4x4-brick mask (64-bit words), a ray accumulates the bits of the brick it
 //    is in and issues one RED when it leaves it (C4: 2.4 -> 1.4 ms).
 //
 // Work binning for unbalanced ray sets. k_dda_keys estimates each ray's DDA
@@ -427,7 +427,7 @@ __global__ void k_dda_scatter(const FrameParams* __restrict__ fp, DdaBins* db, c
 // origin test runs once (the DDA is monotone per axis: once it left the first
 // cell it never returns, and the first cell is the origin cell whenever the
 // origin lies in the window), the end-cell test is one compare of the cell's
-// mask key (word << 5 | bit, injective over the grid's cells), and only the
+// mask key (word << 5 | bit, or << 6 for bricks; injective over the grid's cells), and only the
 // stepped axis' t_max is advanced (one DADD). kSlab adds the owned-x-range
 // logic of a spatial slab.
 template <bool kSlab>
@@ -444,7 +444,7 @@ __device__ __forceinline__ void clear_walk_body(const GridDesc& g, const FramePa
   const int max_steps = g.gex + g.ey + g.ez + 4;
   const int own0 = g.xoff + g.own_lo, own1 = g.xoff + g.own_hi;  // window x owned here
   uint32_t* __restrict__ clr = g.clr;
-  uint32_t* __restrict__ clrb = g.clrb;
+  unsigned long long* __restrict__ clrb = g.clrb;
   const uint32_t xstride = static_cast<uint32_t>(g.ey) * static_cast<uint32_t>(g.W);
   const uint32_t ystride = static_cast<uint32_t>(g.W);
   const unsigned lane = lane_id();
@@ -515,9 +515,10 @@ __device__ __forceinline__ void clear_walk_body(const GridDesc& g, const FramePa
     const bool e_here = ec0 >= own0 && ec0 < own1 && static_cast<unsigned>(ec1) < static_cast<unsigned>(g.ey) &&
                         static_cast<unsigned>(ec2) < static_cast<unsigned>(g.ez);
     const uint32_t key_e =
-        e_here ? ((brick_word(g, ec0 - g.xoff, ec1, ec2) << 5) | brick_bit(ec0 - g.xoff, ec1, ec2)) : 0xffffffffu;
+        e_here ? ((brick_word(g, ec0 - g.xoff, ec1, ec2) << 6) | brick_bit(ec0 - g.xoff, ec1, ec2)) : 0xffffffffu;
     bool mark = !(c0 == oc0 && c1 == oc1 && c2 == oc2);  // origin cell: first cell only
-    uint32_t aw = 0xffffffffu, ab = 0;  // marks of the current brick, flushed when the ray leaves it
+    uint32_t aw = 0xffffffffu;  // the brick the ray is in, its marks (flushed when it leaves)
+    unsigned long long ab = 0;
     // row-layout word index of the current cell (coherent path, incremental)
     uint32_t row = static_cast<uint32_t>(c0 - g.xoff) * xstride + static_cast<uint32_t>(c1) * ystride;
     const int dx_row = s0 * static_cast<int>(xstride), dy_row = s1 * static_cast<int>(ystride);
@@ -565,13 +566,13 @@ __device__ __forceinline__ void clear_walk_body(const GridDesc& g, const FramePa
         const int lx = c0 - g.xoff;
         const uint32_t w = brick_word(g, lx, c1, c2);
         const uint32_t bit = brick_bit(lx, c1, c2);
-        if (((w << 5) | bit) == key_e) continue;
+        if (((w << 6) | bit) == key_e) continue;
         if (w != aw) {
           if (ab) atomicOr(clrb + aw, ab);
           aw = w;
           ab = 0;
         }
-        ab |= 1u << bit;
+        ab |= 1ull << bit;
       } else {  // coherent rays: lanes in the same cell as their left neighbour skip it
         const uint32_t w = row + (static_cast<uint32_t>(c2) >> 5);
         const uint32_t key = (w << 5) | (static_cast<uint32_t>(c2) & 31u);
@@ -637,7 +638,7 @@ __global__ void k_clear_apply(GridDesc g, const FrameParams* __restrict__ fp, Co
 
 // Brick-layout clear mask (incoherent rays): one thread per brick word: count
 // the unique cleared cells, free the occupied ones (the occupancy bits of the
-// brick's 16 (x, y) columns are gathered from the row-layout bitmap, two z
+// brick's 16 (x, y) columns are gathered from the row-layout bitmap, four z
 // bits each), zero the mask.
 __global__ void k_clear_apply_brick(GridDesc g, const FrameParams* __restrict__ fp, Counters* ctr,
                                     const DdaBins* db) {
@@ -646,27 +647,27 @@ __global__ void k_clear_apply_brick(GridDesc g, const FrameParams* __restrict__ 
   unsigned long long cl = 0, fr = 0;
   for (uint64_t w = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; w < g.nbricks;
        w += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const uint32_t c = g.clrb[w];
+    const unsigned long long c = g.clrb[w];
     if (!c) continue;
     g.clrb[w] = 0;
-    cl += __popc(c);
+    cl += __popcll(c);
     const uint32_t bz = static_cast<uint32_t>(w % g.bnz);
     const uint64_t r = w / g.bnz;
     const int by = static_cast<int>(r % g.bny), bx = static_cast<int>(r / g.bny);
-    const int z0 = static_cast<int>(bz) * 2;
-    const int wz = z0 >> 5, sh = z0 & 31;  // both z of the brick lie in one occupancy word
-    uint32_t cols = c;
-    while (cols) {  // (lx, ly) columns with marks: bits 2k, 2k+1
-      const int k = (__ffs(cols) - 1) >> 1;
-      const uint32_t cm = (c >> (2 * k)) & 3u;
-      cols &= ~(3u << (2 * k));
+    const int z0 = static_cast<int>(bz) * 4;
+    const int wz = z0 >> 5, sh = z0 & 31;  // the brick's 4 z lie in one occupancy word
+    unsigned long long cols = c;
+    while (cols) {  // (lx, ly) columns with marks: bits 4k .. 4k+3
+      const int k = (__ffsll(cols) - 1) >> 2;
+      const uint32_t cm = static_cast<uint32_t>(c >> (4 * k)) & 15u;
+      cols &= ~(15ull << (4 * k));
       const int x = bx * 4 + (k >> 2), y = by * 4 + (k & 3);
       uint32_t* ow = occ + (static_cast<uint64_t>(x) * g.ey + y) * g.W + wz;
       const uint32_t f = (*ow >> sh) & cm;
       if (!f) continue;
       atomicAnd(ow, ~(f << sh));  // other bricks share this occupancy word
       fr += __popc(f);
-      for (int b = 0; b < 2; ++b)
+      for (int b = 0; b < 4; ++b)
         if (f & (1u << b)) zero_cell(g.cells + phys_index(g, fp->off_pre, x, y, z0 + b));
     }
   }

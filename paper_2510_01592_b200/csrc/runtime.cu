@@ -544,18 +544,18 @@ struct vp_grid {
     gd.cells = dalloc<Cell>(C);
     gd.bnx = (e[0] + 3) / 4;
     gd.bny = (e[1] + 3) / 4;
-    gd.bnz = (e[2] + 1) / 2;
+    gd.bnz = (e[2] + 3) / 4;
     gd.nbricks = static_cast<uint64_t>(gd.bnx) * gd.bny * gd.bnz;
-    if (gd.nbricks * 32 >= 0xffffffffull) fail(VP_EINVAL, "VoxelGrid: more than 2^32 cells per grid (use slabs)");
+    if (gd.nbricks * 64 >= 0xffffffffull) fail(VP_EINVAL, "VoxelGrid: more than 2^32 cells per grid (use slabs)");
     gd.clr = dalloc<uint32_t>(gd.nwords);
-    gd.clrb = dalloc<uint32_t>(gd.nbricks);
+    gd.clrb = dalloc<unsigned long long>(gd.nbricks);
     gd.ordmap = dalloc<int32_t>(C);
     gd.stbits = dalloc<uint32_t>(gd.nwords);
     occ[0] = dalloc<uint32_t>(gd.nwords);
     occ[1] = dalloc<uint32_t>(gd.nwords);
     ck(cudaMemsetAsync(gd.cells, 0, C * sizeof(Cell), stream), "memset cells");
     ck(cudaMemsetAsync(gd.clr, 0, gd.nwords * 4, stream), "memset clr");
-    ck(cudaMemsetAsync(gd.clrb, 0, gd.nbricks * 4, stream), "memset clrb");
+    ck(cudaMemsetAsync(gd.clrb, 0, gd.nbricks * 8, stream), "memset clrb");
     ck(cudaMemsetAsync(occ[0], 0, gd.nwords * 4, stream), "memset occ");
     ck(cudaMemsetAsync(occ[1], 0, gd.nwords * 4, stream), "memset occ");
     ck(cudaMemsetAsync(gd.ordmap, 0xff, C * 4, stream), "memset ordmap");

@@ -67,11 +67,11 @@ struct GridDesc {
   // x extent (ray clipping and point bounds use the whole window). A plain
   // grid has xoff = 0, own = [0, ex), gex = ex.
   int32_t xoff, own_lo, own_hi, gex;
-  // clear_rays mark bitmap for incoherent rays `clrb` in 4 x 4 x 2 bricks
-  // (one 32-bit word per brick, local coordinates): a ray sets several bits
+  // clear_rays mark bitmap for incoherent rays `clrb` in 4 x 4 x 4 bricks
+  // (one 64-bit word per brick, local coordinates): a ray sets several bits
   // of a word before it leaves the brick, so it issues one RED per brick
   // instead of per cell. (Coherent rays use `clr`, occupancy row layout.)
-  uint32_t* clrb;
+  unsigned long long* clrb;
   int32_t bnx, bny, bnz;
   uint64_t nbricks;
 };
@@ -79,10 +79,10 @@ struct GridDesc {
 __device__ __forceinline__ uint32_t brick_word(const GridDesc& g, int lx, int y, int z) {
   return (static_cast<uint32_t>(lx >> 2) * static_cast<uint32_t>(g.bny) + static_cast<uint32_t>(y >> 2)) *
              static_cast<uint32_t>(g.bnz) +
-         static_cast<uint32_t>(z >> 1);
+         static_cast<uint32_t>(z >> 2);
 }
 __device__ __forceinline__ uint32_t brick_bit(int lx, int y, int z) {
-  return (static_cast<uint32_t>(lx & 3) << 3) | (static_cast<uint32_t>(y & 3) << 1) | static_cast<uint32_t>(z & 1);
+  return (static_cast<uint32_t>(lx & 3) << 4) | (static_cast<uint32_t>(y & 3) << 2) | static_cast<uint32_t>(z & 3);
 }
 
 // Device counters (one struct in device memory, zeroed per frame except
