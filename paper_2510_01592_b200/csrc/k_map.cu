@@ -454,6 +454,12 @@ __device__ __forceinline__ void clear_walk_body(const GridDesc& g, const FramePa
   // rays (depth images) dedup per cell against the neighbouring lane
   const bool accumulate = db->use != 0;
   const bool binned = accumulate;
+  // the 3x3x3 bricks around the sensor are crossed by every ray: their marks
+  // are gathered in shared memory and flushed once per block
+  __shared__ unsigned long long near_m[27];
+  if (threadIdx.x < 27) near_m[threadIdx.x] = 0;
+  __syncthreads();
+  const int sbx = (oc0 - g.xoff) >> 2, sby = oc1 >> 2, sbz = oc2 >> 2;
   for (uint64_t r = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < n;
        r += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint64_t i = binned ? perm[r] : r;
@@ -519,6 +525,7 @@ __device__ __forceinline__ void clear_walk_body(const GridDesc& g, const FramePa
     bool mark = !(c0 == oc0 && c1 == oc1 && c2 == oc2);  // origin cell: first cell only
     uint32_t aw = 0xffffffffu;  // the brick the ray is in, its marks (flushed when it leaves)
     unsigned long long ab = 0;
+    int anear = -1;  // its index among the sensor's 3x3x3 bricks, or -1
     // row-layout word index of the current cell (coherent path, incremental)
     uint32_t row = static_cast<uint32_t>(c0 - g.xoff) * xstride + static_cast<uint32_t>(c1) * ystride;
     const int dx_row = s0 * static_cast<int>(xstride), dy_row = s1 * static_cast<int>(ystride);
@@ -568,9 +575,15 @@ __device__ __forceinline__ void clear_walk_body(const GridDesc& g, const FramePa
         const uint32_t bit = brick_bit(lx, c1, c2);
         if (((w << 6) | bit) == key_e) continue;
         if (w != aw) {
-          if (ab) atomicOr(clrb + aw, ab);
+          if (ab) {
+            if (anear >= 0) atomicOr(&near_m[anear], ab); else atomicOr(clrb + aw, ab);
+          }
           aw = w;
           ab = 0;
+          const int dbx = (lx >> 2) - sbx, dby = (c1 >> 2) - sby, dbz = (c2 >> 2) - sbz;
+          anear = (dbx >= -1 && dbx <= 1 && dby >= -1 && dby <= 1 && dbz >= -1 && dbz <= 1)
+                      ? (dbx + 1) * 9 + (dby + 1) * 3 + (dbz + 1)
+                      : -1;
         }
         ab |= 1ull << bit;
       } else {  // coherent rays: lanes in the same cell as their left neighbour skip it
@@ -583,7 +596,15 @@ __device__ __forceinline__ void clear_walk_body(const GridDesc& g, const FramePa
         if (!dup) atomicOr(clr + w, 1u << (c2 & 31));
       }
     }
-    if (ab) atomicOr(clrb + aw, ab);
+    if (ab) {
+      if (anear >= 0) atomicOr(&near_m[anear], ab); else atomicOr(clrb + aw, ab);
+    }
+  }
+  __syncthreads();
+  if (accumulate && threadIdx.x < 27 && near_m[threadIdx.x]) {
+    const int k = threadIdx.x;
+    const int bx = sbx + k / 9 - 1, by = sby + (k / 3) % 3 - 1, bz = sbz + k % 3 - 1;
+    atomicOr(clrb + (static_cast<uint32_t>(bx) * g.bny + by) * g.bnz + bz, near_m[k]);
   }
 }
 
