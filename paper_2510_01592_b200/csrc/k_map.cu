@@ -345,6 +345,9 @@ __global__ void __launch_bounds__(1024) k_integrate_fold_dense(GridDesc g, const
 // every count is taken afterwards from the bitmap, so the walk order does
 // not change any result.
 __global__ void k_dda_keys(GridDesc g, const FrameParams* __restrict__ fp, DdaBins* db, uint8_t* bin_of) {
+  // a coherent stream is re-evaluated every 8th frame only (the decision
+  // changes the walk order, never a result)
+  if (!db->use && (db->frame & 7u)) return;
   __shared__ uint32_t hist[kDdaBins];
   for (int b = threadIdx.x; b < kDdaBins; b += blockDim.x) hist[b] = 0;
   __syncthreads();
@@ -383,7 +386,8 @@ __global__ void k_dda_keys(GridDesc g, const FrameParams* __restrict__ fp, DdaBi
 // One warp: decide, and lay the bins out longest first; resets the counts.
 __global__ void k_dda_plan(DdaBins* db) {
   const unsigned lane = lane_id();
-  const int use = db->steps * 4 < db->warp_max * 3 ? 1 : 0;  // lane efficiency < 75 %
+  const bool measured = db->warp_max != 0;  // k_dda_keys ran this frame
+  const int use = measured ? (db->steps * 4 < db->warp_max * 3 ? 1 : 0) : db->use;  // lane efficiency < 75 %
   uint32_t run = 0;
   for (int b0 = kDdaBins - 32; b0 >= 0; b0 -= 32) {  // descending bins
     const int b = b0 + 31 - static_cast<int>(lane);
@@ -403,6 +407,7 @@ __global__ void k_dda_plan(DdaBins* db) {
     db->use = use;
     db->steps = 0;
     db->warp_max = 0;
+    ++db->frame;
   }
 }
 
@@ -454,10 +459,11 @@ __device__ __forceinline__ void clear_walk_body(const GridDesc& g, const FramePa
   // rays (depth images) dedup per cell against the neighbouring lane
   const bool accumulate = db->use != 0;
   const bool binned = accumulate;
-  // the 3x3x3 bricks around the sensor are crossed by every ray: their marks
-  // are gathered in shared memory and flushed once per block
-  __shared__ unsigned long long near_m[27];
-  if (threadIdx.x < 27) near_m[threadIdx.x] = 0;
+  // the kNear^3 bricks around the sensor are crossed by most rays: their
+  // marks are gathered in shared memory and flushed once per block
+  constexpr int kNearR = 1, kNear = 2 * kNearR + 1, kNear3 = kNear * kNear * kNear;
+  __shared__ unsigned long long near_m[kNear3];
+  for (int k = threadIdx.x; k < kNear3; k += blockDim.x) near_m[k] = 0;
   __syncthreads();
   const int sbx = (oc0 - g.xoff) >> 2, sby = oc1 >> 2, sbz = oc2 >> 2;
   for (uint64_t r = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < n;
@@ -525,7 +531,7 @@ __device__ __forceinline__ void clear_walk_body(const GridDesc& g, const FramePa
     bool mark = !(c0 == oc0 && c1 == oc1 && c2 == oc2);  // origin cell: first cell only
     uint32_t aw = 0xffffffffu;  // the brick the ray is in, its marks (flushed when it leaves)
     unsigned long long ab = 0;
-    int anear = -1;  // its index among the sensor's 3x3x3 bricks, or -1
+    int anear = -1;  // its index among the sensor's near bricks, or -1
     // row-layout word index of the current cell (coherent path, incremental)
     uint32_t row = static_cast<uint32_t>(c0 - g.xoff) * xstride + static_cast<uint32_t>(c1) * ystride;
     const int dx_row = s0 * static_cast<int>(xstride), dy_row = s1 * static_cast<int>(ystride);
@@ -581,8 +587,9 @@ __device__ __forceinline__ void clear_walk_body(const GridDesc& g, const FramePa
           aw = w;
           ab = 0;
           const int dbx = (lx >> 2) - sbx, dby = (c1 >> 2) - sby, dbz = (c2 >> 2) - sbz;
-          anear = (dbx >= -1 && dbx <= 1 && dby >= -1 && dby <= 1 && dbz >= -1 && dbz <= 1)
-                      ? (dbx + 1) * 9 + (dby + 1) * 3 + (dbz + 1)
+          anear = (dbx >= -kNearR && dbx <= kNearR && dby >= -kNearR && dby <= kNearR && dbz >= -kNearR &&
+                   dbz <= kNearR)
+                      ? ((dbx + kNearR) * kNear + (dby + kNearR)) * kNear + (dbz + kNearR)
                       : -1;
         }
         ab |= 1ull << bit;
@@ -601,11 +608,12 @@ __device__ __forceinline__ void clear_walk_body(const GridDesc& g, const FramePa
     }
   }
   __syncthreads();
-  if (accumulate && threadIdx.x < 27 && near_m[threadIdx.x]) {
-    const int k = threadIdx.x;
-    const int bx = sbx + k / 9 - 1, by = sby + (k / 3) % 3 - 1, bz = sbz + k % 3 - 1;
-    atomicOr(clrb + (static_cast<uint32_t>(bx) * g.bny + by) * g.bnz + bz, near_m[k]);
-  }
+  for (int k = threadIdx.x; accumulate && k < kNear3; k += blockDim.x)
+    if (near_m[k]) {
+      const int bx = sbx + k / (kNear * kNear) - kNearR, by = sby + (k / kNear) % kNear - kNearR,
+                bz = sbz + k % kNear - kNearR;
+      atomicOr(clrb + (static_cast<uint32_t>(bx) * g.bny + by) * g.bnz + bz, near_m[k]);
+    }
 }
 
 #ifndef VP_DDA_MINB

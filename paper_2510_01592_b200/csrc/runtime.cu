@@ -1127,14 +1127,20 @@ struct vp_pipeline {
   uint64_t rkern[kSlots][3] = {};
   cudaEvent_t ev_start[kSlots] = {}, ev_map[kSlots] = {};
   cudaEvent_t ev_clu[kSlots] = {}, ev_done[kSlots] = {};
+  cudaEvent_t ev_h2d[kSlots] = {};
+  cudaStream_t cstream = nullptr;  // host-to-device copies of upcoming frames
   ~vp_pipeline() {
     if (gexec) cudaGraphExecDestroy(gexec);
     for (auto& row : rx)
       for (auto& x : row)
         if (x) cudaGraphExecDestroy(x);
-    for (auto* e : {ev_start, ev_map, ev_clu, ev_done})
+    for (auto* e : {ev_start, ev_map, ev_clu, ev_done, ev_h2d})
       for (int q = 0; q < kSlots; ++q)
         if (e[q]) cudaEventDestroy(e[q]);
+    if (cstream) {
+      cudaStreamSynchronize(cstream);
+      cudaStreamDestroy(cstream);
+    }
     delete grid;
   }
 };
@@ -1264,9 +1270,21 @@ void run_part_graph(vp_pipeline* pl, int part, cudaStream_t st, F&& enqueue) {
 void pipeline_run(vp_pipeline* pl, size_t nf, const float* const* xyz, const uint64_t* n,
                   const double* R, const double* t, bool device_ptrs, vp_frame_timing* timings) {
   vp_grid* g = pl->grid;
-  for (auto* e : {pl->ev_start, pl->ev_map, pl->ev_clu, pl->ev_done})
+  for (auto* e : {pl->ev_start, pl->ev_map, pl->ev_clu, pl->ev_done, pl->ev_h2d})
     for (int q = 0; q < kSlots; ++q)
       if (!e[q]) ck(cudaEventCreate(&e[q]), "event");
+  if (!pl->cstream) ck(cudaStreamCreateWithFlags(&pl->cstream, cudaStreamNonBlocking), "stream");
+  // host frames are copied ahead on the copy stream, one frame ahead of the
+  // mapping, into the slot's point buffer once that slot's previous frame
+  // has been mapped (copy engine overlaps the compute)
+  auto h2d_ahead = [&](size_t k) {
+    if (device_ptrs || k >= nf) return;
+    const int q = static_cast<int>(k % kSlots);
+    if (k >= static_cast<size_t>(kSlots)) ck(cudaStreamWaitEvent(pl->cstream, pl->ev_map[q], 0), "wait");
+    if (n[k])
+      ck(cudaMemcpyAsync(g->d_pts_s[q], xyz[k], n[k] * 12, cudaMemcpyHostToDevice, pl->cstream), "points h2d");
+    ck(cudaEventRecord(pl->ev_h2d[q], pl->cstream), "ev");
+  };
   uint64_t maxn = 0;
   for (size_t k = 0; k < nf; ++k) maxn = std::max(maxn, n[k]);
   for (size_t k = 0; k < nf; ++k)
@@ -1318,8 +1336,9 @@ void pipeline_run(vp_pipeline* pl, size_t nf, const float* const* xyz, const uin
     if (device_ptrs) {
       g->h_fp->pts = xyz[k];
     } else {
-      if (n[k])
-        ck(cudaMemcpyAsync(g->d_pts, xyz[k], n[k] * 12, cudaMemcpyHostToDevice, g->mstream), "points h2d");
+      if (k == 0) h2d_ahead(0);
+      h2d_ahead(k + 1);
+      ck(cudaStreamWaitEvent(g->mstream, pl->ev_h2d[s], 0), "wait");
       g->h_fp->pts = g->d_pts;
     }
     g->h_fp->n = n[k];
@@ -1380,6 +1399,7 @@ void pipeline_run(vp_pipeline* pl, size_t nf, const float* const* xyz, const uin
     ck(cudaStreamSynchronize(g->stream), "sync");
   }
   ck(cudaStreamSynchronize(g->mstream), "sync");
+  ck(cudaStreamSynchronize(pl->cstream), "sync");
   for (size_t k = nf >= static_cast<size_t>(kSlots) ? nf - kSlots : 0; k < nf; ++k) harvest(k);
   const int last = nf ? static_cast<int>((nf - 1) % kSlots) : 0;
   g->set_slot(last);

@@ -249,6 +249,7 @@ struct DdaBins {
   unsigned long long steps;     // sum of estimated steps
   unsigned long long warp_max;  // sum over 32-ray groups of 32 x their longest ray
   int use;                      // 1: walk rays in bin order (perm), 0: identity
+  uint32_t frame;               // frames planned (a coherent stream is re-measured every 8th)
 };
 
 // ---- kernels (k_map.cu)
