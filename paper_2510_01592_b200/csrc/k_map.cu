@@ -118,10 +118,6 @@ __global__ void k_integrate_scatter(const FrameParams* __restrict__ fp, const ui
   }
 }
 
-// One warp per touched voxel: the point indices are staged in shared memory,
-// ranked (indices are distinct, so rank = number of smaller indices), the
-// points are transformed in parallel, and lane 0 performs the reference's
-// sequential FP64 fold (voxel_grid.cpp:104-110) in ascending point index.
 constexpr int kFoldWarps = 8;
 
 __device__ __forceinline__ void fold_cell(const GridDesc& g, const FrameParams* fp, uint32_t key,
@@ -149,50 +145,116 @@ __device__ __forceinline__ void fold_cell(const GridDesc& g, const FrameParams* 
   }
 }
 
+// Most voxels receive a handful of points: one thread per voxel sorts its
+// (<= kFoldSmall) point indices in registers and folds them; larger groups are
+// listed for the warp-per-voxel pass (<= kFoldMax) or the block pass (dense).
 __global__ void __launch_bounds__(256) k_integrate_fold(GridDesc g, const FrameParams* __restrict__ fp,
                                                         Counters* ctr, const uint32_t* groups,
                                                         uint32_t* hkey, uint32_t* hcnt,
                                                         const uint32_t* hoff, uint32_t* sorted,
-                                                        uint32_t* dense) {
+                                                        uint32_t* medium, uint32_t* dense) {
+  const uint32_t ng = ctr->ngroups;
+  unsigned long long fresh = 0;
+  for (uint32_t gi = blockIdx.x * blockDim.x + threadIdx.x; gi < ng; gi += gridDim.x * blockDim.x) {
+    const uint32_t slot = groups[gi];
+    const uint32_t cnt = hcnt[slot];
+    if (cnt > static_cast<uint32_t>(kFoldSmall)) {
+      if (cnt <= static_cast<uint32_t>(kFoldMax))
+        medium[atomicAdd(&ctr->nmedium, 1u)] = slot;  // warp pass
+      else
+        dense[atomicAdd(&ctr->ndense, 1u)] = slot;  // block pass
+      continue;
+    }
+    const uint32_t key = hkey[slot];
+    const uint32_t* lst = sorted + hoff[slot];
+    uint32_t idx[kFoldSmall];
+#pragma unroll
+    for (int a = 0; a < kFoldSmall; ++a) idx[a] = a < static_cast<int>(cnt) ? lst[a] : 0xffffffffu;
+    // insertion sort (ascending point index = the reference's fold order)
+#pragma unroll
+    for (int a = 1; a < kFoldSmall; ++a) {
+#pragma unroll
+      for (int b = a; b > 0; --b) {
+        const uint32_t lo = min(idx[b - 1], idx[b]), hi = max(idx[b - 1], idx[b]);
+        idx[b - 1] = lo;
+        idx[b] = hi;
+      }
+    }
+    const uint32_t z = key % static_cast<uint32_t>(g.ez);
+    const uint32_t r = key / static_cast<uint32_t>(g.ez);
+    const uint32_t y = r % static_cast<uint32_t>(g.ey);
+    const uint32_t x = r / static_cast<uint32_t>(g.ey);
+    Cell* c = g.cells + phys_index(g, fp->off_pre, x, y, z);
+    double sx = c->sx, sy = c->sy, sz = c->sz;
+    const uint32_t count = c->count;
+#pragma unroll
+    for (int a = 0; a < kFoldSmall; ++a) {
+      if (a >= static_cast<int>(cnt)) break;
+      const float* p = fp->pts + 3 * static_cast<uint64_t>(idx[a]);
+      const d3 w = pose_apply(fp->R, fp->t, static_cast<double>(p[0]), static_cast<double>(p[1]),
+                              static_cast<double>(p[2]));
+      sx += w.x;
+      sy += w.y;
+      sz += w.z;
+    }
+    c->sx = sx;
+    c->sy = sy;
+    c->sz = sz;
+    c->count = count + cnt;
+    c->status = 1;  // VoxelStatus::Occupied
+    if (count == 0) {
+      atomicOr(fp->occ_pre + word_of(g, x, y, z), 1u << (z & 31));
+      ++fresh;
+    }
+    hkey[slot] = kEmptyKey;
+    hcnt[slot] = 0;
+  }
+  warp_add_u64(&ctr->newly, fresh);
+}
+
+// Voxels with kFoldSmall < points <= kFoldMax: one warp per voxel: the point
+// indices are staged in shared memory, ranked (indices are distinct, so rank
+// = number of smaller indices), the points are transformed in parallel, and
+// lane 0 performs the reference's sequential FP64 fold (voxel_grid.cpp:104-110)
+// in ascending point index.
+__global__ void __launch_bounds__(256) k_integrate_fold_medium(GridDesc g, const FrameParams* __restrict__ fp,
+                                                               Counters* ctr, uint32_t* hkey, uint32_t* hcnt,
+                                                               const uint32_t* hoff, const uint32_t* sorted,
+                                                               const uint32_t* medium) {
   __shared__ uint32_t raw[kFoldWarps][kFoldMax];
   __shared__ uint32_t srt[kFoldMax * kFoldWarps];
   __shared__ d3 sw[kFoldWarps][kFoldMax];
-  const uint32_t ng = ctr->ngroups;
+  const uint32_t nm = ctr->nmedium;
   const unsigned lane = lane_id(), wid = threadIdx.x >> 5;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarp = (gridDim.x * blockDim.x) >> 5;
   unsigned long long fresh = 0;
-  for (uint32_t gi = warp; gi < ng; gi += nwarp) {
-    const uint32_t slot = groups[gi];
+  for (uint32_t gi = warp; gi < nm; gi += nwarp) {
+    const uint32_t slot = medium[gi];
     const uint32_t key = hkey[slot];
     const uint32_t cnt = hcnt[slot];
-    uint32_t* lst = sorted + hoff[slot];
-    if (cnt <= static_cast<uint32_t>(kFoldMax)) {
-      for (uint32_t k = lane; k < cnt; k += 32) raw[wid][k] = lst[k];
-      __syncwarp();
-      for (uint32_t k = lane; k < cnt; k += 32) {
-        const uint32_t v = raw[wid][k];
-        uint32_t rank = 0;
-        for (uint32_t q = 0; q < cnt; ++q) rank += raw[wid][q] < v ? 1u : 0u;
-        srt[wid * kFoldMax + rank] = v;
-      }
-      __syncwarp();
-      for (uint32_t k = lane; k < cnt; k += 32) {
-        const float* p = fp->pts + 3 * static_cast<uint64_t>(srt[wid * kFoldMax + k]);
-        sw[wid][k] = pose_apply(fp->R, fp->t, static_cast<double>(p[0]), static_cast<double>(p[1]),
-                                static_cast<double>(p[2]));
-      }
-      __syncwarp();
-      if (lane == 0) fold_cell(g, fp, key, sw[wid], cnt, fresh);
-      __syncwarp();
-    } else {  // dense voxel: k_integrate_fold_dense (block per voxel)
-      if (lane == 0) dense[atomicAdd(&ctr->ndense, 1u)] = slot;
-      continue;
+    const uint32_t* lst = sorted + hoff[slot];
+    for (uint32_t k = lane; k < cnt; k += 32) raw[wid][k] = lst[k];
+    __syncwarp();
+    for (uint32_t k = lane; k < cnt; k += 32) {
+      const uint32_t v = raw[wid][k];
+      uint32_t rank = 0;
+      for (uint32_t q = 0; q < cnt; ++q) rank += raw[wid][q] < v ? 1u : 0u;
+      srt[wid * kFoldMax + rank] = v;
     }
+    __syncwarp();
+    for (uint32_t k = lane; k < cnt; k += 32) {
+      const float* p = fp->pts + 3 * static_cast<uint64_t>(srt[wid * kFoldMax + k]);
+      sw[wid][k] = pose_apply(fp->R, fp->t, static_cast<double>(p[0]), static_cast<double>(p[1]),
+                              static_cast<double>(p[2]));
+    }
+    __syncwarp();
     if (lane == 0) {
+      fold_cell(g, fp, key, sw[wid], cnt, fresh);
       hkey[slot] = kEmptyKey;
       hcnt[slot] = 0;
     }
+    __syncwarp();
   }
   warp_add_u64(&ctr->newly, fresh);
 }

@@ -446,6 +446,7 @@ struct vp_grid {
   uint32_t* prank = nullptr;
   uint32_t* sorted = nullptr;
   uint32_t* dense = nullptr;  // slots of integrate groups > kFoldMax points
+  uint32_t* medium = nullptr;  // slots of integrate groups kFoldSmall < points <= kFoldMax
   uint32_t* rperm = nullptr;  // clear_rays: rays in bin order (when binning is on)
   uint8_t* bin_of = nullptr;  // clear_rays: length bin per ray
   DdaBins* dbins = nullptr;
@@ -491,8 +492,8 @@ struct vp_grid {
     }
     if (occ_total) cudaFree(occ_total);
     for (void* p : {(void*)hkey, (void*)hcnt, (void*)hoff, (void*)groups,
-                    (void*)pslot, (void*)prank, (void*)sorted, (void*)dense, (void*)rperm, (void*)bin_of,
-                    (void*)dbins})
+                    (void*)pslot, (void*)prank, (void*)sorted, (void*)dense, (void*)medium, (void*)rperm,
+                    (void*)bin_of, (void*)dbins})
       if (p) cudaFree(p);
     for (auto& e : ev) if (e) cudaEventDestroy(e);
     if (stream) cudaStreamDestroy(stream);
@@ -686,7 +687,7 @@ struct vp_grid {
     cap = std::max<uint64_t>(cap, pcap * 2);
     ck(cudaDeviceSynchronize(), "sync before realloc");
     for (void* p : {(void*)hkey, (void*)hcnt, (void*)hoff, (void*)groups, (void*)pslot, (void*)prank,
-                    (void*)sorted, (void*)dense, (void*)rperm, (void*)bin_of})
+                    (void*)sorted, (void*)dense, (void*)medium, (void*)rperm, (void*)bin_of})
       if (p) cudaFree(p);
     for (auto*& p : d_pts_s) dfree(p);
     uint64_t hs = 1;
@@ -701,6 +702,7 @@ struct vp_grid {
     prank = dalloc<uint32_t>(cap);
     sorted = dalloc<uint32_t>(cap);
     dense = dalloc<uint32_t>(cap / (kFoldMax + 1) + 1);
+    medium = dalloc<uint32_t>(cap / (kFoldSmall + 1) + 1);
     rperm = dalloc<uint32_t>(cap);
     bin_of = dalloc<uint8_t>(cap);
     if (!dbins) {
@@ -809,7 +811,9 @@ struct vp_grid {
     if (n == 0 && !capturing) return;
     const int gp = grid_for(capturing ? pcap : n);
     LAUNCH(k_integrate_fold, gp, kThreads, 0, lstream, gd, d_fp, ctr, groups, hkey, hcnt, hoff,
-           sorted, dense);
+           sorted, medium, dense);
+    LAUNCH(k_integrate_fold_medium, 148 * 4, kThreads, 0, lstream, gd, d_fp, ctr, hkey, hcnt, hoff, sorted,
+           medium);
     LAUNCH(k_integrate_fold_dense, 148, 1024, kDenseSmem, lstream, gd, d_fp, ctr, hkey, hcnt, hoff, sorted,
            pslot, dense);
   }

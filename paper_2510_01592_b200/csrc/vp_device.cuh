@@ -103,6 +103,7 @@ struct Counters {
   uint32_t surv_max;     // largest hull-survivor set of the frame (diagnostic)
   int32_t ccl_giant;     // root of the sampled largest component after the lattice links
   uint32_t ndense;       // integrate groups with more than kFoldMax points (k_integrate_fold_dense)
+  uint32_t nmedium;      // integrate groups with kFoldSmall < points <= kFoldMax (k_integrate_fold_medium)
 };
 
 constexpr uint32_t kOverflowOcc = 1u;

@@ -14,6 +14,7 @@ constexpr int kClusterBins = 2048;  // clusters handled by the counting sort per
 constexpr int kChunk = 256;         // ordinals per counting-sort chunk (one warp)
 constexpr int kHullSmem = 512;      // survivors sorted in shared memory (6 regions of this size)
 constexpr int kPolyChunk = 1024;    // inlier points per polygon-stage block
+constexpr int kFoldSmall = 24;      // integrate: points per voxel folded by one thread
 constexpr int kFoldMax = 128;       // integrate: points per voxel folded by one warp
 constexpr uint32_t kDenseSort = 16384;  // denser voxels: indices bitonic-sorted in shared memory
 
@@ -262,7 +263,10 @@ __global__ void k_integrate_scatter(const FrameParams* fp, const uint32_t* pslot
                                     const uint32_t* prank, const uint32_t* hoff, uint32_t* sorted);
 __global__ void k_integrate_fold(GridDesc g, const FrameParams* fp, Counters* ctr,
                                  const uint32_t* groups, uint32_t* hkey, uint32_t* hcnt,
-                                 const uint32_t* hoff, uint32_t* sorted, uint32_t* dense);
+                                 const uint32_t* hoff, uint32_t* sorted, uint32_t* medium, uint32_t* dense);
+__global__ void k_integrate_fold_medium(GridDesc g, const FrameParams* fp, Counters* ctr, uint32_t* hkey,
+                                        uint32_t* hcnt, const uint32_t* hoff, const uint32_t* sorted,
+                                        const uint32_t* medium);
 __global__ void k_integrate_fold_dense(GridDesc g, const FrameParams* fp, Counters* ctr, uint32_t* hkey,
                                        uint32_t* hcnt, const uint32_t* hoff, const uint32_t* sorted,
                                        const uint32_t* pslot, const uint32_t* dense);
