@@ -353,6 +353,28 @@ int vp_pipeline_frame_trace(vp_pipeline* pl, const float* xyz, uint64_t n,
                             const double rotation[9], const double translation[3],
                             uint8_t** buf, uint64_t* len);
 
+/* ---- height-map baseline (heightmap.hpp:10-55, heightmap.cpp:9-89) -------
+   The paper's Table I 2.5-D baseline: one height per (x, y) cell, latest
+   measurement wins in point order; segment = BFS region growing over
+   4-neighbours with |dh| < distance_th from seeds in lexicographic order
+   (region id = seed flat index, members in BFS order), then fit_planes,
+   refine_plane (p->refine, p->refine_exact) and make_polygon as the voxel
+   path. Polygons with area < p->min_polygon_area are dropped (run_frames'
+   filter, pipeline.cpp:190-193; pass -inf for plain hm_segment). */
+typedef struct vp_heightmap vp_heightmap;
+int vp_heightmap_create(double resolution, const int32_t extent[2], const double center[2], int device,
+                        vp_heightmap** out);
+void vp_heightmap_destroy(vp_heightmap* hm);
+int vp_hm_integrate(vp_heightmap* hm, const float* xyz, uint64_t n, const double rotation[9],
+                    const double translation[3]);
+/* heights / valid flags of all cells (x-major), host arrays of extent[0]*extent[1] */
+int vp_hm_cells(vp_heightmap* hm, double* heights, uint8_t* valid);
+int vp_hm_segment(vp_heightmap* hm, const vp_pipeline_params* p, vp_polygons_t** out);
+/* The last segment's regions: the visit sequence (all region cells, BFS
+   order per region, host array of >= extent cells) and every cell's region
+   root (its seed's flat index; own index for invalid cells). */
+int vp_hm_regions(vp_heightmap* hm, uint32_t* visit, int32_t* root, uint64_t* nv);
+
 /* ---- frame and polygon formats on the GPU path (frame_io.cpp:91-116,
    polygon_io.cpp:30-47) ---------------------------------------------------
    A VXPF stream (magic "VXPF", u32 version 1, per frame u32 n, 12 f32 pose

@@ -364,6 +364,7 @@ int ref_run_named(const char* name, const char* outdir) {
       tiny();
       c.run.baseline = true;
       c.run.frames = 4;
+      c.output.emit_frames = true;  // the stream, for the height-map parity test
     } else {
       g_err = "unknown run " + n;
       return VP_EINVAL;

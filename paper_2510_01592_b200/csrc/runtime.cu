@@ -3142,6 +3142,177 @@ int vp_pipeline_run(vp_pipeline* pl, size_t n_frames, const float* const* xyz, c
   });
 }
 
+}  // extern "C"
+
+struct vp_heightmap {
+  vp_grid* g = nullptr;  // stream, counters, frame params, segmentation context
+  HmDesc m{};
+  uint32_t ncells = 0;
+  uint32_t* visit = nullptr;
+  uint8_t* flags = nullptr;
+  uint32_t* pos = nullptr;
+  uint32_t* dn = nullptr;  // [0] ncells, [1] frontier size, [2] next frontier size
+  uint32_t nv = 0;         // cells visited by the last segment (region members)
+  ~vp_heightmap() {
+    if (g && g->stream) cudaStreamSynchronize(g->stream);
+    void* ptrs[] = {m.h, m.valid, m.win, m.parent, m.root, m.claim, m.visited, m.spos, visit, flags, pos, dn};
+    for (void* q : ptrs)
+      if (q) cudaFree(q);
+    delete g;
+  }
+};
+
+extern "C" {
+
+int vp_heightmap_create(double res, const int32_t ext[2], const double center[2], int device, vp_heightmap** out) {
+  *out = nullptr;
+  return guard([&] {
+    if (!(res > 0.0) || ext[0] <= 0 || ext[1] <= 0)  // heightmap.cpp:11-12
+      fail(VP_EINVAL, "HeightMap: resolution and extents must be positive");
+    const uint64_t nc = static_cast<uint64_t>(ext[0]) * ext[1];
+    if (4 * nc >= (1ull << 31)) fail(VP_EINVAL, "HeightMap: too many cells");
+    auto* h = new vp_heightmap();
+    struct Del {
+      vp_heightmap*& h;
+      ~Del() { delete h; }
+    } del{h};
+    h->g = new vp_grid();
+    const int32_t ge[3] = {1, 1, 32};
+    const double gc[3] = {0.0, 0.0, 0.0};
+    h->g->init(res, ge, gc, device);
+    h->ncells = static_cast<uint32_t>(nc);
+    HmDesc& m = h->m;
+    m.ex = ext[0];
+    m.ey = ext[1];
+    m.res = res;
+    m.ox = center[0] - static_cast<double>(ext[0]) * (0.5 * res);  // heightmap.cpp:13
+    m.oy = center[1] - static_cast<double>(ext[1]) * (0.5 * res);
+    m.h = dalloc<double>(nc);
+    m.valid = dalloc<uint8_t>(nc);
+    m.win = dalloc<uint32_t>(nc);
+    m.parent = dalloc<int32_t>(nc);
+    m.root = dalloc<int32_t>(nc);
+    m.claim = dalloc<uint32_t>(nc);
+    m.visited = dalloc<uint8_t>(nc);
+    m.spos = dalloc<uint32_t>(nc);
+    h->visit = dalloc<uint32_t>(nc);
+    h->flags = dalloc<uint8_t>(4 * nc);
+    h->pos = dalloc<uint32_t>(4 * nc);
+    h->dn = dalloc<uint32_t>(4);
+    cudaStream_t st = h->g->stream;
+    ck(cudaMemsetAsync(m.h, 0, nc * 8, st), "memset");
+    ck(cudaMemsetAsync(m.valid, 0, nc, st), "memset");
+    ck(cudaMemsetAsync(m.win, 0, nc * 4, st), "memset");
+    const uint32_t d0[4] = {h->ncells, 0, 0, 0};
+    ck(cudaMemcpyAsync(h->dn, d0, 16, cudaMemcpyHostToDevice, st), "dn");
+    // scan scratch for 4 x cells flags
+    const uint32_t cap = static_cast<uint32_t>(4 * nc);
+    h->g->seg.ensure(std::max(h->g->seg.b.Vcap, cap), std::max(h->g->seg.b.Scap, h->ncells),
+                     std::max(h->g->seg.b.Icap, h->ncells), 100, h->g->gd.nwords);
+    ck(cudaStreamSynchronize(st), "sync");
+    *out = h;
+    h = nullptr;
+  });
+}
+
+void vp_heightmap_destroy(vp_heightmap* hm) { delete hm; }
+
+int vp_hm_integrate(vp_heightmap* hm, const float* xyz, uint64_t n, const double R[9], const double t[3]) {
+  return guard([&] {
+    if (!is_valid_rotation(R)) fail(VP_EINVAL, "hm_integrate: pose rotation is not orthonormal");  // :27-28
+    vp_grid* g = hm->g;
+    if (n == 0) return;
+    stage_points(g, xyz, n, false);
+    g->set_pose(R, t);
+    g->upload_params();
+    LAUNCH(k_hm_win, grid_for(n), kThreads, 0, g->stream, hm->m, g->d_fp);
+    LAUNCH(k_hm_write, grid_for(n), kThreads, 0, g->stream, hm->m, g->d_fp);
+    ck(cudaStreamSynchronize(g->stream), "sync");
+  });
+}
+
+int vp_hm_cells(vp_heightmap* hm, double* heights, uint8_t* valid) {
+  return guard([&] {
+    cudaStream_t st = hm->g->stream;
+    ck(cudaMemcpyAsync(heights, hm->m.h, 8ull * hm->ncells, cudaMemcpyDeviceToHost, st), "d2h");
+    ck(cudaMemcpyAsync(valid, hm->m.valid, hm->ncells, cudaMemcpyDeviceToHost, st), "d2h");
+    ck(cudaStreamSynchronize(st), "sync");
+  });
+}
+
+int vp_hm_regions(vp_heightmap* hm, uint32_t* visit, int32_t* root, uint64_t* nv) {
+  return guard([&] {
+    *nv = hm->nv;
+    ck(cudaMemcpyAsync(visit, hm->visit, 4ull * hm->nv, cudaMemcpyDeviceToHost, hm->g->stream), "d2h");
+    ck(cudaMemcpyAsync(root, hm->m.root, 4ull * hm->ncells, cudaMemcpyDeviceToHost, hm->g->stream), "d2h");
+    ck(cudaStreamSynchronize(hm->g->stream), "sync");
+  });
+}
+
+int vp_hm_segment(vp_heightmap* hm, const vp_pipeline_params* p, vp_polygons_t** out) {
+  if (out) *out = nullptr;
+  return guard([&] {
+    vp_grid* g = hm->g;
+    cudaStream_t st = g->stream;
+    const double dth = p->seg.distance_th;
+    const uint32_t nc = hm->ncells;
+    g->reset_frame_counters();
+    // regions = components; roots (component-minimum flat) are the BFS seeds
+    LAUNCH(k_hm_ccl_init, grid_for(nc), kThreads, 0, st, hm->m);
+    LAUNCH(k_hm_ccl_union, grid_for(nc), kThreads, 0, st, hm->m, dth);
+    LAUNCH(k_hm_seed_flags, grid_for(nc), kThreads, 0, st, hm->m, hm->flags);
+    g->launch_flag_scan(hm->flags, hm->dn, nc, hm->pos, hm->dn + 1);
+    LAUNCH(k_hm_seed_emit, grid_for(nc), kThreads, 0, st, hm->m, hm->flags, hm->pos, hm->visit);
+    uint32_t nf = 0;
+    ck(cudaMemcpyAsync(&nf, hm->dn + 1, 4, cudaMemcpyDeviceToHost, st), "d2h");
+    ck(cudaStreamSynchronize(st), "sync");
+    // level-synchronous BFS in the reference's FIFO order
+    uint32_t ls = 0, nv = nf;
+    while (nf) {
+      const uint32_t nt = 4 * nf;
+      LAUNCH(k_hm_claim, grid_for(nt), kThreads, 0, st, hm->m, hm->visit, ls, hm->dn + 1, dth);
+      LAUNCH(k_hm_claimed, grid_for(nt), kThreads, 0, st, hm->m, hm->visit, ls, hm->dn + 1, hm->flags);
+      const uint32_t d3v[1] = {nt};
+      ck(cudaMemcpyAsync(hm->dn + 3, d3v, 4, cudaMemcpyHostToDevice, st), "h2d");
+      g->launch_flag_scan(hm->flags, hm->dn + 3, nt, hm->pos, hm->dn + 2);
+      LAUNCH(k_hm_emit, grid_for(nt), kThreads, 0, st, hm->m, hm->visit, ls, hm->dn + 1, hm->flags, hm->pos);
+      ck(cudaMemcpyAsync(hm->dn + 1, hm->dn + 2, 4, cudaMemcpyDeviceToDevice, st), "d2d");
+      ck(cudaMemcpyAsync(&nf, hm->dn + 2, 4, cudaMemcpyDeviceToHost, st), "d2h");
+      ck(cudaStreamSynchronize(st), "sync");
+      ls = nv;
+      nv += nf;
+    }
+    hm->nv = nv;
+    // regions >= min_cluster_size, members in BFS order, then the voxel path's fitting
+    g->seg.ensure(g->seg.b.Vcap, std::max(g->seg.b.Scap, nv), std::max(g->seg.b.Icap, nv),
+                  std::max(p->ransac.iterations, 1), g->gd.nwords);
+    g->seg.ensure_dirs(16, st);
+    for (int tries = 0;; ++tries) {
+      g->reset_frame_counters();
+      set_counter_u32(g, offsetof(Counters, S), nv);
+      const SegDev sd = make_segdev(p->seg, hm->m.res);
+      const RansacDev rd = make_ransacdev(p->ransac);
+      if (nv) {
+        LAUNCH(k_hm_zero_cnt, grid_for(nv), kThreads, 0, st, nv, g->seg.b);
+        LAUNCH(k_hm_members, grid_for(nv), kThreads, 0, st, hm->m, hm->visit, nv, g->seg.b);
+      }
+      g->launch_clusters(sd);
+      LAUNCH(k_hm_klabel, 8, 256, 0, st, g->ctr, g->seg.b, hm->visit);
+      g->launch_ransac(rd);
+      g->launch_refine(p->ransac.up, p->refine, p->refine_exact);
+      g->launch_polygon(16, p->min_polygon_area);
+      g->read_counters();
+      if (tries > 4 || !g->grow_if_overflow(p->ransac.iterations)) break;
+    }
+    if (g->h_ctr->overflow) fail(VP_ENOMEM, "hm_segment: capacity overflow");
+    if (out) {
+      HostPolys hp;
+      g->download_polygons(hp, false);
+      *out = make_polygons_out(hp);
+    }
+  });
+}
+
 int vp_pipeline_replay(vp_pipeline* pl, const vp_stream* st, uint64_t first, uint64_t count,
                        vp_polygons_t** out, vp_frame_timing* timings) {
   if (out) *out = nullptr;

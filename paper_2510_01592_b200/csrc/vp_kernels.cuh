@@ -253,6 +253,20 @@ struct DdaBins {
   uint32_t frame;               // frames planned (a coherent stream is re-measured every 8th)
 };
 
+// Height-map baseline (k_heightmap.cu): cells x-major, flat = x * ey + y.
+struct HmDesc {
+  double* h;         // height per cell
+  uint8_t* valid;
+  uint32_t* win;     // per frame: last point index + 1
+  int32_t* parent;   // union-find over cells
+  int32_t* root;     // region root (seed flat index) of every cell, after the unions
+  uint32_t* claim;   // BFS: min (frontier position * 4 + step)
+  uint8_t* visited;
+  uint32_t* spos;    // visit position of a region's seed (roots only)
+  int ex, ey;
+  double ox, oy, res;
+};
+
 // ---- kernels (k_map.cu)
 __global__ void k_integrate_hash(GridDesc g, const FrameParams* fp, Counters* ctr, uint32_t* hkey,
                                  uint32_t* hcnt, uint32_t hmask, uint32_t* groups, uint32_t* pslot,
@@ -355,5 +369,20 @@ __global__ void k_owner_init(uint32_t n, SegBufs b);
 __global__ void k_owner_prep(uint32_t n_own, uint32_t n_recv, int64_t own_base, const double* own_mean,
                              const int32_t* flabel, const MemberRec* recv, SegBufs b);
 __global__ void k_klabel_rebase(const Counters* ctr, SegBufs b, int64_t base);
+
+// ---- kernels (k_heightmap.cu)
+__global__ void k_hm_win(HmDesc m, const FrameParams* fp);
+__global__ void k_hm_write(HmDesc m, const FrameParams* fp);
+__global__ void k_hm_ccl_init(HmDesc m);
+__global__ void k_hm_ccl_union(HmDesc m, double dth);
+__global__ void k_hm_seed_flags(HmDesc m, uint8_t* flags);
+__global__ void k_hm_seed_emit(HmDesc m, const uint8_t* flags, const uint32_t* pos, uint32_t* visit);
+__global__ void k_hm_claim(HmDesc m, const uint32_t* visit, uint32_t ls, const uint32_t* nfp, double dth);
+__global__ void k_hm_claimed(HmDesc m, const uint32_t* visit, uint32_t ls, const uint32_t* nfp, uint8_t* flags);
+__global__ void k_hm_emit(HmDesc m, uint32_t* visit, uint32_t ls, const uint32_t* nfp, const uint8_t* flags,
+                          const uint32_t* pos);
+__global__ void k_hm_members(HmDesc m, const uint32_t* visit, uint32_t nv, SegBufs b);
+__global__ void k_hm_zero_cnt(uint32_t nv, SegBufs b);
+__global__ void k_hm_klabel(const Counters* ctr, SegBufs b, const uint32_t* visit);
 
 }  // namespace vp

@@ -487,6 +487,58 @@ def write_polygons(path, polys_ptr):
     check(lib().vp_write_polygons(str(path).encode(), polys_ptr))
 
 
+class HeightMap:
+    """The 2.5-D height-map baseline (heightmap.hpp:10-55) on the GPU."""
+
+    def __init__(self, res, extent, center=(0.0, 0.0), device=0):
+        e = np.asarray(extent, np.int32)
+        c = np.asarray(center, np.float64)
+        self.extent = tuple(int(v) for v in extent)
+        self.h = C.c_void_p()
+        check(lib().vp_heightmap_create(C.c_double(res), _p(e, C.c_int32), _p(c, C.c_double), C.c_int(device),
+                                        C.byref(self.h)))
+
+    def integrate(self, pts, R, t):
+        """hm_integrate (heightmap.cpp:26-38)."""
+        pts = np.ascontiguousarray(pts, np.float32)
+        R, t = _pose(R, t)
+        check(lib().vp_hm_integrate(self.h, _p(pts, C.c_float), C.c_uint64(len(pts)), _p(R, C.c_double),
+                                    _p(t, C.c_double)))
+
+    def cells(self):
+        n = self.extent[0] * self.extent[1]
+        h = np.zeros(n)
+        v = np.zeros(n, np.uint8)
+        check(lib().vp_hm_cells(self.h, _p(h, C.c_double), _p(v, C.c_uint8)))
+        return h.reshape(self.extent), v.reshape(self.extent).astype(bool)
+
+    def segment(self, params: PipelineParams):
+        """hm_segment (heightmap.cpp:40-89) + run_frames' area filter (params.min_polygon_area)."""
+        out = C.POINTER(Polygons)()
+        check(lib().vp_hm_segment(self.h, C.byref(params), C.byref(out)))
+        return polygons_to_py(out)
+
+    def regions(self):
+        """(visit sequence, root per cell) of the last segment()."""
+        n = self.extent[0] * self.extent[1]
+        visit = np.zeros(n, np.uint32)
+        root = np.zeros(n, np.int32)
+        nv = C.c_uint64()
+        check(lib().vp_hm_regions(self.h, _p(visit, C.c_uint32), _p(root, C.c_int32), C.byref(nv)))
+        return visit[:nv.value], root.reshape(self.extent)
+
+    def close(self):
+        if self.h:
+            lib().vp_heightmap_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class AblationConfig(C.Structure):
     _fields_ = [("cluster_counts", C.POINTER(C.c_int32)), ("n_counts", C.c_int32), ("trials", C.c_int32),
                 ("points_min", C.c_int32), ("points_max", C.c_int32), ("seed", C.c_uint64),
