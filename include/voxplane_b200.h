@@ -375,6 +375,24 @@ int vp_hm_segment(vp_heightmap* hm, const vp_pipeline_params* p, vp_polygons_t**
    root (its seed's flat index; own index for invalid cells). */
 int vp_hm_regions(vp_heightmap* hm, uint32_t* visit, int32_t* root, uint64_t* nv);
 
+/* ---- plane IoU scoring (metrics.cpp:19-185; the paper's Table I metric) --
+   match_planes: every (truth, detected) pair within the 20 deg normal gate is
+   projected into the truth plane and rasterised at raster_res (plane_iou,
+   default 0.005 m; one block per pair on the device, integer counts), pairs
+   matched greedily by IoU; matches (capacity min(#detected, #truth)) in
+   truth order. write_iou_report writes the reference's report text. */
+typedef struct {
+  int32_t detected_id, truth_id;
+  double iou;
+} vp_plane_match;
+typedef struct {
+  uint64_t truth_count, detected_count, matched, unmatched_truth, unmatched_detected;
+  double mean_iou, area_weighted_iou;
+} vp_iou_report;
+int vp_match_planes(const vp_polygons_t* detected, const vp_polygons_t* truth, double raster_res, int device,
+                    vp_iou_report* report, vp_plane_match* matches);
+int vp_write_iou_report(const char* path, const vp_iou_report* report, const vp_plane_match* matches);
+
 /* ---- frame and polygon formats on the GPU path (frame_io.cpp:91-116,
    polygon_io.cpp:30-47) ---------------------------------------------------
    A VXPF stream (magic "VXPF", u32 version 1, per frame u32 n, 12 f32 pose

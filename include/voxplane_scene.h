@@ -66,6 +66,12 @@ int vp_render_frame(const vp_box* boxes, size_t nb, const vp_rect* rects, size_t
                     uint64_t frame_index, int threads, float** points, uint64_t* n,
                     double qR[9], double qt[3]);
 
+/* build_scene's ground-truth regions (scene_sim.cpp:23-30, 43-114) for a
+   stock SceneKind: per region the plane (normal xyz, offset; plane_through)
+   and its 4 corners (12 doubles); make_polygon of the corners
+   (vp_make_polygons) gives the truth polygon. Capacity 16 regions. */
+int vp_scene_truth(int kind, double* planes, double* corners, size_t* n);
+
 /* quantize_pose (frame_io.cpp:64-72) + the orthonormality check of
    render_frame (scene_sim.cpp:188-190); returns VP_EINVAL (voxplane_b200.h) if invalid. */
 int vp_quantize_pose(const double R[9], const double t[3], double qR[9], double qt[3]);

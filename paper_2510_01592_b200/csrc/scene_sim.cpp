@@ -368,6 +368,85 @@ int vp_default_trajectory(int kind, int frames, double rate_hz, double* poses) {
   return static_cast<int>(v.size() / 12);
 }
 
+int vp_scene_truth(int kind, double* planes, double* corners, size_t* n) {
+  // build_scene's add_truth regions (scene_sim.cpp:23-30, 43-114): plane_through
+  // (orient_up(normal.normalized()), offset = n . first corner) + 4 corners each
+  const SceneParams p;
+  *n = 0;
+  auto add_truth = [&](V3 nrm, std::initializer_list<V3> cs) {
+    V3 u = normalized(nrm);
+    const double d = dot(u, V3{0, 0, 1});  // orient_up (types.hpp:43-52)
+    const double flip = d < 0.0 ? -1.0 : 1.0;
+    if (d == 0.0) {
+      const double c3[3] = {u.x, u.y, u.z};
+      for (int k = 0; k < 3; ++k) {
+        if (c3[k] > 0.0) break;
+        if (c3[k] < 0.0) {
+          u = scl(-1.0, u);
+          break;
+        }
+      }
+    } else if (flip < 0.0) {
+      u = V3{-u.x, -u.y, -u.z};
+    }
+    const V3 c0 = *cs.begin();
+    double* pl = planes + 4 * *n;
+    pl[0] = u.x;
+    pl[1] = u.y;
+    pl[2] = u.z;
+    pl[3] = dot(u, c0);
+    int k = 0;
+    for (const V3& c : cs) {
+      corners[12 * *n + 3 * k] = c.x;
+      corners[12 * *n + 3 * k + 1] = c.y;
+      corners[12 * *n + 3 * k + 2] = c.z;
+      ++k;
+    }
+    ++*n;
+  };
+  const V3 ux{1, 0, 0}, uz{0, 0, 1}, mx{-1, 0, 0};
+  switch (kind) {
+    case 0: {  // Stair5
+      const double w = 0.5 * p.stair_width;
+      add_truth(uz, {{-p.approach_length, -w, 0}, {0, -w, 0}, {0, w, 0}, {-p.approach_length, w, 0}});
+      for (int k = 0; k < 5; ++k) {
+        const double x0 = k * p.stair_run, x1 = (k + 1) * p.stair_run, z1 = (k + 1) * p.stair_rise;
+        add_truth(uz, {{x0, -w, z1}, {x1, -w, z1}, {x1, w, z1}, {x0, w, z1}});
+        const double z0 = k * p.stair_rise;
+        add_truth(mx, {{x0, -w, z0}, {x0, w, z0}, {x0, w, z1}, {x0, -w, z1}});
+      }
+      return 0;
+    }
+    case 1: {  // SingleStage
+      const double f = 0.5 * p.floor_size;
+      add_truth(uz, {{-f, -f, 0}, {f, -f, 0}, {f, f, 0}, {-f, f, 0}});
+      const double s = 0.5 * p.stage_size, cx = f - s, h = p.stage_height;
+      add_truth(uz, {{cx - s, -f, h}, {cx + s, -f, h}, {cx + s, f, h}, {cx - s, f, h}});
+      return 0;
+    }
+    case 2: {  // Overhang
+      const double fx = 0.5 * p.overhang_floor_x, fy = 0.5 * p.overhang_floor_y;
+      add_truth(uz, {{-fx, -fy, 0}, {fx, -fy, 0}, {fx, fy, 0}, {-fx, fy, 0}});
+      const double ox = 0.5 * p.overhang_depth, oy = fy, cx = fx - ox, h = p.overhang_clearance;
+      add_truth(uz, {{cx - ox, -oy, h}, {cx + ox, -oy, h}, {cx + ox, oy, h}, {cx - ox, oy, h}});
+      return 0;
+    }
+    case 3: {  // SmallObstacle
+      const double f = 0.5 * p.obstacle_floor_size;
+      add_truth(uz, {{-f, -f, 0}, {f, -f, 0}, {f, f, 0}, {-f, f, 0}});
+      const V3 half = scl(0.5, p.obstacle_size);
+      const V3 c{p.obstacle_center_xy.x, p.obstacle_center_xy.y, 0.0};
+      const double z = p.obstacle_size.z;
+      add_truth(uz, {{c.x - half.x, c.y - half.y, z}, {c.x + half.x, c.y - half.y, z},
+                     {c.x + half.x, c.y + half.y, z}, {c.x - half.x, c.y + half.y, z}});
+      return 0;
+    }
+    default:
+      (void)ux;
+      return -1;
+  }
+}
+
 int vp_quantize_pose(const double Rin[9], const double tin[3], double qR[9], double qt[3]) {
   M3 R;  // quantize_pose (frame_io.cpp:64-72)
   for (int i = 0; i < 9; ++i) R.m[i] = static_cast<double>(static_cast<float>(Rin[i]));

@@ -487,6 +487,63 @@ def write_polygons(path, polys_ptr):
     check(lib().vp_write_polygons(str(path).encode(), polys_ptr))
 
 
+def polygons_struct(polys):
+    """A vp_polygons_t view of polygon dicts (normal, offset, label, inlier_count,
+    v3d, area); returns (struct, keep-alive list)."""
+    arr = (Polygon * max(len(polys), 1))()
+    keep = [arr]
+    for q, p in zip(arr, polys):
+        v = np.ascontiguousarray(p["v3d"], np.float64).reshape(-1, 3)
+        v2 = np.ascontiguousarray(p.get("v2d", np.zeros((len(v), 2))), np.float64).reshape(-1, 2)
+        keep += [v, v2]
+        q.plane.normal[:] = tuple(float(x) for x in p["normal"])
+        q.plane.offset = p["offset"]
+        q.plane.inlier_count = p["inlier_count"]
+        q.plane.cluster_label = p["label"]
+        q.nverts = len(v)
+        q.area = p["area"]
+        q.v3d = v.ctypes.data_as(C.POINTER(C.c_double))
+        q.v2d = v2.ctypes.data_as(C.POINTER(C.c_double))
+    return Polygons(len(polys), arr), keep
+
+
+def scene_truth(kind: int, device=0):
+    """build_scene's ground-truth polygons (scene_sim.cpp:23-30, 43-114): the
+    corner sets through make_polygon on the device."""
+    planes = np.zeros(16 * 4)
+    corners = np.zeros(16 * 12)
+    n = C.c_size_t()
+    if lib().vp_scene_truth(C.c_int(kind), _p(planes, C.c_double), _p(corners, C.c_double), C.byref(n)) != 0:
+        raise ValueError(f"unknown scene kind {kind}")
+    models = [dict(normal=tuple(planes[4 * r:4 * r + 3]), offset=planes[4 * r + 3], inlier_count=0, label=r)
+              for r in range(n.value)]
+    return make_polygons(models, [corners[12 * r:12 * r + 12].reshape(4, 3) for r in range(n.value)], device=device)
+
+
+class IoUReport(C.Structure):
+    _fields_ = [("truth_count", C.c_uint64), ("detected_count", C.c_uint64), ("matched", C.c_uint64),
+                ("unmatched_truth", C.c_uint64), ("unmatched_detected", C.c_uint64), ("mean_iou", C.c_double),
+                ("area_weighted_iou", C.c_double)]
+
+
+class PlaneMatch(C.Structure):
+    _fields_ = [("detected_id", C.c_int32), ("truth_id", C.c_int32), ("iou", C.c_double)]
+
+
+def match_planes(detected, truth, raster_res=0.005, report_path=None, device=0):
+    """match_planes (metrics.cpp:114-160) + optional write_iou_report; returns
+    (report dict, [(truth_id, detected_id, iou)])."""
+    d, kd = polygons_struct(detected)
+    t, kt = polygons_struct(truth)
+    rep = IoUReport()
+    m = (PlaneMatch * max(1, min(len(detected), len(truth))))()
+    check(lib().vp_match_planes(C.byref(d), C.byref(t), C.c_double(raster_res), C.c_int(device), C.byref(rep), m))
+    if report_path:
+        check(lib().vp_write_iou_report(str(report_path).encode(), C.byref(rep), m))
+    return ({k: getattr(rep, k) for k, _ in IoUReport._fields_},
+            [(m[i].truth_id, m[i].detected_id, m[i].iou) for i in range(rep.matched)])
+
+
 class HeightMap:
     """The 2.5-D height-map baseline (heightmap.hpp:10-55) on the GPU."""
 

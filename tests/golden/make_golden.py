@@ -6,7 +6,7 @@
   oracle/_ref (ref_run_named("live")).
 * baseline_frames.bin — the stream of the reference's baseline (height-map)
   run, test_pipeline.cpp:183-192, emitted by oracle/_ref ("baseline").
-* pipe_*.polygons_final.txt — the reference's golden outputs copied verbatim
+* pipe_*.polygons_final.txt, pipe_*.iou_report.txt — the reference's golden outputs copied verbatim
   from /root/reference/proj/test_scratch (left there by its own ctest run).
 """
 import ctypes as C
@@ -34,6 +34,7 @@ def main():
     for run in ("pipe_t1", "pipe_stair", "pipe_smallobs", "pipe_rosette", "pipe_baseline"):
         dst = os.path.join(HERE, f"{run}.polygons_final.txt")
         shutil.copyfile(os.path.join(SCRATCH, run, "polygons_final.txt"), dst)
+        shutil.copyfile(os.path.join(SCRATCH, run, "iou_report.txt"), os.path.join(HERE, f"{run}.iou_report.txt"))
     print("golden fixtures written to", HERE)
 
 
