@@ -122,10 +122,8 @@ constexpr int kFoldWarps = 8;
 
 __device__ __forceinline__ void fold_cell(const GridDesc& g, const FrameParams* fp, uint32_t key,
                                           const d3* w, uint32_t cnt, unsigned long long& fresh) {
-  const uint32_t z = key % static_cast<uint32_t>(g.ez);
-  const uint32_t r = key / static_cast<uint32_t>(g.ez);
-  const uint32_t y = r % static_cast<uint32_t>(g.ey);
-  const uint32_t x = r / static_cast<uint32_t>(g.ey);
+  const uint32_t r = fdiv(key, g.fez), z = key - r * static_cast<uint32_t>(g.ez);
+  const uint32_t x = fdiv(r, g.fey), y = r - x * static_cast<uint32_t>(g.ey);
   Cell* c = g.cells + phys_index(g, fp->off_pre, x, y, z);
   double sx = c->sx, sy = c->sy, sz = c->sz;
   const uint32_t count = c->count;
@@ -180,10 +178,8 @@ __global__ void __launch_bounds__(256) k_integrate_fold(GridDesc g, const FrameP
         idx[b] = hi;
       }
     }
-    const uint32_t z = key % static_cast<uint32_t>(g.ez);
-    const uint32_t r = key / static_cast<uint32_t>(g.ez);
-    const uint32_t y = r % static_cast<uint32_t>(g.ey);
-    const uint32_t x = r / static_cast<uint32_t>(g.ey);
+    const uint32_t r = fdiv(key, g.fez), z = key - r * static_cast<uint32_t>(g.ez);
+    const uint32_t x = fdiv(r, g.fey), y = r - x * static_cast<uint32_t>(g.ey);
     Cell* c = g.cells + phys_index(g, fp->off_pre, x, y, z);
     double sx = c->sx, sy = c->sy, sz = c->sz;
     const uint32_t count = c->count;
@@ -280,10 +276,8 @@ __global__ void __launch_bounds__(1024) k_integrate_fold_dense(GridDesc g, const
     const uint32_t slot = dense[di];
     const uint32_t key = hkey[slot];
     const uint32_t cnt = hcnt[slot];
-    const uint32_t z = key % static_cast<uint32_t>(g.ez);
-    const uint32_t r = key / static_cast<uint32_t>(g.ez);
-    const uint32_t y = r % static_cast<uint32_t>(g.ey);
-    const uint32_t x = r / static_cast<uint32_t>(g.ey);
+    const uint32_t r = fdiv(key, g.fez), z = key - r * static_cast<uint32_t>(g.ez);
+    const uint32_t x = fdiv(r, g.fey), y = r - x * static_cast<uint32_t>(g.ey);
     Cell* c = g.cells + phys_index(g, fp->off_pre, x, y, z);
     double sx = 0.0, sy = 0.0, sz = 0.0;
     uint32_t count = 0;
@@ -714,9 +708,10 @@ __global__ void k_clear_apply(GridDesc g, const FrameParams* __restrict__ fp, Co
     if (!f) continue;
     occ[w] = o & ~f;
     fr += __popc(f);
-    const uint64_t row = w / g.W;
-    const int z0 = static_cast<int>(w % g.W) * 32;
-    const int y = static_cast<int>(row % g.ey), x = static_cast<int>(row / g.ey);
+    const uint32_t row = fdiv(static_cast<uint32_t>(w), g.fW);
+    const int z0 = static_cast<int>(static_cast<uint32_t>(w) - row * static_cast<uint32_t>(g.W)) * 32;
+    const uint32_t xr = fdiv(row, g.fey);
+    const int y = static_cast<int>(row - xr * static_cast<uint32_t>(g.ey)), x = static_cast<int>(xr);
     while (f) {
       const int b = __ffs(f) - 1;
       f &= f - 1;
@@ -790,9 +785,10 @@ __global__ void k_recenter(GridDesc g, const FrameParams* __restrict__ fp, Count
   const uint32_t nw = static_cast<uint32_t>(g.nwords);  // < 2^32 (grid creation check)
   const uint32_t W = static_cast<uint32_t>(g.W), ey = static_cast<uint32_t>(g.ey);
   for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < nw; u += gridDim.x * blockDim.x) {
-    const uint32_t row = u / W;
+    const uint32_t row = fdiv(u, g.fW);
     const int wz = static_cast<int>(u - row * W);
-    const int y = static_cast<int>(row % ey), x = static_cast<int>(row / ey);
+    const uint32_t xr = fdiv(row, g.fey);
+    const int y = static_cast<int>(row - xr * ey), x = static_cast<int>(xr);
     // new word: destination (x,y,z) reads source (x+sx, y+sy, z+sz)
     const long long xs = static_cast<long long>(x) + sx, ys = static_cast<long long>(y) + sy;
     uint32_t nv = 0;

@@ -22,10 +22,11 @@ __global__ void k_normals(GridDesc g, const FrameParams* __restrict__ fp, Counte
   const int r = sp.radius;
   for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x) {
     const uint32_t flat = b.occ_list[v];
-    const int z = static_cast<int>(flat % static_cast<uint32_t>(g.ez));
-    const uint32_t rr = flat / static_cast<uint32_t>(g.ez);
-    const int y = static_cast<int>(rr % static_cast<uint32_t>(g.ey));
-    const int x = static_cast<int>(rr / static_cast<uint32_t>(g.ey));
+    const uint32_t rr = fdiv(flat, g.fez);
+    const int z = static_cast<int>(flat - rr * static_cast<uint32_t>(g.ez));
+    const uint32_t xr = fdiv(rr, g.fey);
+    const int y = static_cast<int>(rr - xr * static_cast<uint32_t>(g.ey));
+    const int x = static_cast<int>(xr);
     Cell* own = g.cells + phys_index(g, off, x, y, z);
     const uint32_t oc = own->count;
     const double ocd = static_cast<double>(oc);
@@ -151,10 +152,11 @@ __global__ void k_step_emit(GridDesc g, Counters* ctr, SegBufs b, MapDesc m, int
       continue;
     }
     const uint32_t flat = b.occ_list[v];
-    const int z = static_cast<int>(flat % static_cast<uint32_t>(g.ez));
-    const uint32_t rr = flat / static_cast<uint32_t>(g.ez);
-    const int y = static_cast<int>(rr % static_cast<uint32_t>(g.ey));
-    const int x = static_cast<int>(rr / static_cast<uint32_t>(g.ey));
+    const uint32_t rr = fdiv(flat, g.fez);
+    const int z = static_cast<int>(flat - rr * static_cast<uint32_t>(g.ez));
+    const uint32_t xr = fdiv(rr, g.fey);
+    const int y = static_cast<int>(rr - xr * static_cast<uint32_t>(g.ey));
+    const int x = static_cast<int>(xr);
     b.st_idx[3 * s] = x + xadd;  // xadd: slab -> window x (0 for a plain grid)
     b.st_idx[3 * s + 1] = y;
     b.st_idx[3 * s + 2] = z;
@@ -504,10 +506,11 @@ __global__ void k_occ_gather(GridDesc g, const FrameParams* __restrict__ fp, Cou
   const uint32_t V = min(ctr->V, b.Vcap);
   for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x) {
     const uint32_t flat = b.occ_list[v];
-    const int z = static_cast<int>(flat % static_cast<uint32_t>(g.ez));
-    const uint32_t rr = flat / static_cast<uint32_t>(g.ez);
-    const int y = static_cast<int>(rr % static_cast<uint32_t>(g.ey));
-    const int x = static_cast<int>(rr / static_cast<uint32_t>(g.ey));
+    const uint32_t rr = fdiv(flat, g.fez);
+    const int z = static_cast<int>(flat - rr * static_cast<uint32_t>(g.ez));
+    const uint32_t xr = fdiv(rr, g.fey);
+    const int y = static_cast<int>(rr - xr * static_cast<uint32_t>(g.ey));
+    const int x = static_cast<int>(xr);
     const Cell* c = g.cells + phys_index(g, fp->off_post, x, y, z);
     const double cd = static_cast<double>(c->count);
     b.own_mean[3 * v] = c->sx / cd;

@@ -543,6 +543,9 @@ struct vp_grid {
     gd.own_hi = e[0];
     gd.gex = e[0];
     gd.cells = dalloc<Cell>(C);
+    gd.fW = make_fastdiv(static_cast<uint32_t>(gd.W));
+    gd.fey = make_fastdiv(static_cast<uint32_t>(e[1]));
+    gd.fez = make_fastdiv(static_cast<uint32_t>(e[2]));
     gd.bnx = (e[0] + 3) / 4;
     gd.bny = (e[1] + 3) / 4;
     gd.bnz = (e[2] + 3) / 4;

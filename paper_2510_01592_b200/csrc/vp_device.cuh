@@ -51,6 +51,18 @@ struct FrameParams {
   uint32_t* occ_post;  // after recenter (== occ_pre when no shift)
 };
 
+// Division by a grid-invariant divisor d (ex, ey, ez, W) without the ~20
+// instruction software divide: q = umulhi64(n, ceil(2^64 / d)), exact for
+// every n < 2^32 (the rounding error n * e / 2^64 < 2^-32 < 1 / d).
+struct FastDiv {
+  uint32_t d;
+  uint64_t m;  // 0 for d == 1
+};
+inline FastDiv make_fastdiv(uint32_t d) { return FastDiv{d, d > 1 ? (~0ull / d) + 1 : 0ull}; }
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv& f) {
+  return f.m ? static_cast<uint32_t>(__umul64hi(static_cast<uint64_t>(n), f.m)) : n;
+}
+
 // Static grid description (pointers fixed at creation).
 struct GridDesc {
   Cell* cells;
@@ -74,6 +86,7 @@ struct GridDesc {
   unsigned long long* clrb;
   int32_t bnx, bny, bnz;
   uint64_t nbricks;
+  FastDiv fW, fey, fez;  // W, ey, ez
 };
 
 __device__ __forceinline__ uint32_t brick_word(const GridDesc& g, int lx, int y, int z) {
