@@ -768,65 +768,60 @@ __global__ void k_clear_apply_brick(GridDesc g, const FrameParams* __restrict__ 
 // (2) zeroes the cells of occupied voxels that leave the window, counting them
 // as voxels_dropped.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t row_bits(const uint32_t* row, int W, int b0) {
-  const int wlo = b0 >= 0 ? (b0 >> 5) : -((-b0 + 31) >> 5);
-  const int sh = b0 - wlo * 32;
-  const uint32_t lo = (wlo >= 0 && wlo < W) ? __ldg(row + wlo) : 0u;
-  const uint32_t hi = (wlo + 1 >= 0 && wlo + 1 < W) ? __ldg(row + wlo + 1) : 0u;
-  return sh ? ((lo >> sh) | (hi << (32 - sh))) : lo;
-}
 
 __global__ void k_recenter(GridDesc g, const FrameParams* __restrict__ fp, Counters* ctr) {
   if (!fp->do_shift) return;
-  const uint32_t* oldb = fp->occ_pre;
-  uint32_t* newb = fp->occ_post;
+  const uint32_t* __restrict__ oldb = fp->occ_pre;
+  uint32_t* __restrict__ newb = fp->occ_post;
   const int sx = fp->shift[0], sy = fp->shift[1], sz = fp->shift[2];
   unsigned long long dropped = 0;
   const uint32_t nw = static_cast<uint32_t>(g.nwords);  // < 2^32 (grid creation check)
-  const uint32_t W = static_cast<uint32_t>(g.W), ey = static_cast<uint32_t>(g.ey);
+  const int W = g.W, ey = g.ey, ex = g.ex, ez = g.ez;
   for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < nw; u += gridDim.x * blockDim.x) {
     const uint32_t row = fdiv(u, g.fW);
-    const int wz = static_cast<int>(u - row * W);
+    const int wz = static_cast<int>(u - row * static_cast<uint32_t>(W));
     const uint32_t xr = fdiv(row, g.fey);
-    const int y = static_cast<int>(row - xr * ey), x = static_cast<int>(xr);
-    // new word: destination (x,y,z) reads source (x+sx, y+sy, z+sz)
-    const long long xs = static_cast<long long>(x) + sx, ys = static_cast<long long>(y) + sy;
+    const int y = static_cast<int>(row - xr * static_cast<uint32_t>(ey)), x = static_cast<int>(xr);
+    // new word: destination (x, y, z) reads source (x+sx, y+sy, z+sz), i.e.
+    // bits [32 wz + sz, +32) of source row (x+sx, y+sy), zero outside the row
+    const int xs = x + sx, ys = y + sy;
     uint32_t nv = 0;
-    if (xs >= 0 && xs < g.ex && ys >= 0 && ys < g.ey) {
-      const long long b0 = static_cast<long long>(wz) * 32 + sz;
-      if (b0 > -32 && b0 < static_cast<long long>(g.W) * 32)
-        nv = row_bits(oldb + (static_cast<uint64_t>(xs) * g.ey + ys) * g.W, g.W, static_cast<int>(b0));
+    if (static_cast<unsigned>(xs) < static_cast<unsigned>(ex) && static_cast<unsigned>(ys) < static_cast<unsigned>(ey)) {
+      const uint32_t* src = oldb + (static_cast<uint32_t>(xs) * static_cast<uint32_t>(ey) + static_cast<uint32_t>(ys)) *
+                                       static_cast<uint32_t>(W);
+      const int b0 = wz * 32 + sz;
+      const int wlo = b0 >> 5, sh = b0 & 31;  // floor division (arithmetic shift)
+      const uint32_t lo = (wlo >= 0 && wlo < W) ? __ldg(src + wlo) : 0u;
+      const uint32_t hi = (wlo + 1 >= 0 && wlo + 1 < W) ? __ldg(src + wlo + 1) : 0u;
+      nv = __funnelshift_r(lo, hi, sh);
     }
-    const int zlim = g.ez - wz * 32;
+    const int zlim = ez - wz * 32;
     if (zlim < 32) nv &= (1u << zlim) - 1u;
     newb[u] = nv;
-    // dropped: old bits whose destination leaves the window
-    const uint32_t ov = oldb[u];
-    if (ov) {
-      uint32_t drop;
-      const long long xd = static_cast<long long>(x) - sx, yd = static_cast<long long>(y) - sy;
-      if (xd < 0 || xd >= g.ex || yd < 0 || yd >= g.ey) {
-        drop = ov;
-      } else {
-        // keep bits b with 0 <= 32*wz + b - sz < ez, i.e. b in [blo, bhi)
-        const long long blo = static_cast<long long>(sz) - 32ll * wz;
-        const long long bhi = static_cast<long long>(g.ez) + sz - 32ll * wz;
-        const int lo_b = static_cast<int>(blo < 0 ? 0 : (blo > 32 ? 32 : blo));
-        const int hi_b = static_cast<int>(bhi < 0 ? 0 : (bhi > 32 ? 32 : bhi));
-        uint32_t keep = 0;
-        if (hi_b > lo_b) {
-          const uint32_t upto_hi = hi_b >= 32 ? 0xffffffffu : ((1u << hi_b) - 1u);
-          const uint32_t below_lo = lo_b >= 32 ? 0xffffffffu : ((1u << lo_b) - 1u);
-          keep = upto_hi & ~below_lo;
-        }
-        drop = ov & ~keep;
+    // dropped: old bits whose destination (x-sx, y-sy, z-sz) leaves the window
+    const uint32_t ov = __ldg(oldb + u);
+    if (!ov) continue;
+    uint32_t drop;
+    const int xd = x - sx, yd = y - sy;
+    if (static_cast<unsigned>(xd) >= static_cast<unsigned>(ex) || static_cast<unsigned>(yd) >= static_cast<unsigned>(ey)) {
+      drop = ov;
+    } else {
+      // keep bits b with 0 <= 32*wz + b - sz < ez, i.e. b in [blo, bhi)
+      const int blo = min(max(sz - 32 * wz, 0), 32);
+      const int bhi = min(max(ez + sz - 32 * wz, 0), 32);
+      uint32_t keep = 0;
+      if (bhi > blo) {
+        const uint32_t upto_hi = bhi >= 32 ? 0xffffffffu : ((1u << bhi) - 1u);
+        const uint32_t below_lo = blo >= 32 ? 0xffffffffu : ((1u << blo) - 1u);
+        keep = upto_hi & ~below_lo;
       }
-      dropped += __popc(drop);
-      while (drop) {
-        const int b = __ffs(drop) - 1;
-        drop &= drop - 1;
-        zero_cell(g.cells + phys_index(g, fp->off_pre, x, y, wz * 32 + b));
-      }
+      drop = ov & ~keep;
+    }
+    dropped += __popc(drop);
+    while (drop) {
+      const int b = __ffs(drop) - 1;
+      drop &= drop - 1;
+      zero_cell(g.cells + phys_index(g, fp->off_pre, x, y, wz * 32 + b));
     }
   }
   warp_add_u64(&ctr->dropped, dropped);
