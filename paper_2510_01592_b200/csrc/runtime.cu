@@ -1303,6 +1303,14 @@ void pipeline_run(vp_pipeline* pl, size_t nf, const float* const* xyz, const uin
   g->seg.ensure_dirs(16, g->stream);
   const int nslot = static_cast<int>(std::min<size_t>(kSlots, std::max<size_t>(nf, 1)));
   g->ensure_contexts(nslot, pl->p.ransac.iterations);
+  uint64_t occ_known = g->host_occupied;  // occupancy before frame `known`
+  size_t known = 0;
+  uint32_t cap_min = 0xffffffffu;
+  for (int q = 0; q < nslot; ++q) {
+    g->use_seg(q);
+    cap_min = std::min({cap_min, g->seg.b.Vcap, g->seg.b.Scap});
+  }
+  g->use_seg(0);
   ck(cudaStreamSynchronize(g->stream), "sync");
   const bool graphs = !g_prof_on && !std::getenv("VP_NO_GRAPH");
   // frame k-kSlots's slot is reused by frame k: its whole chain must be done
@@ -1316,8 +1324,14 @@ void pipeline_run(vp_pipeline* pl, size_t nf, const float* const* xyz, const uin
       ck(cudaEventElapsedTime(&a, pl->ev_start[s], pl->ev_map[s]), "elapsed");
       ck(cudaEventElapsedTime(&b, pl->ev_map[s], pl->ev_clu[s]), "elapsed");
       ck(cudaEventElapsedTime(&c, pl->ev_clu[s], pl->ev_done[s]), "elapsed");
-      std::fprintf(stderr, "frame %zu: map %.1f us, grid readers %.1f us, chain %.1f us\n", k, 1e3 * a, 1e3 * b,
-                   1e3 * c);
+      float gap = -1.f;  // mapping stream idle between this frame's readers and the next frame's start
+      if (k + 1 < nf && k + kSlots > k + 1)
+        if (cudaEventElapsedTime(&gap, pl->ev_clu[s], pl->ev_start[(k + 1) % kSlots]) != cudaSuccess) {
+          cudaGetLastError();
+          gap = -1.f;
+        }
+      std::fprintf(stderr, "frame %zu: map %.1f us, grid readers %.1f us, chain %.1f us, gap to next %.1f us\n", k,
+                   1e3 * a, 1e3 * b, 1e3 * c, 1e3 * gap);
     }
     if (!timings) return;
     float ms = 0.f;
@@ -1335,6 +1349,32 @@ void pipeline_run(vp_pipeline* pl, size_t nf, const float* const* xyz, const uin
     if (k >= static_cast<size_t>(kSlots)) {
       ck(cudaEventSynchronize(pl->ev_done[s]), "slot sync");
       harvest(k - kSlots);
+      occ_known = g->h_ctr_s[s]->occupied;  // after frame k - kSlots
+      known = k - kSlots + 1;
+    }
+    // The occupied (and steppable) lists of frame k cannot be longer than the
+    // occupancy known for frame known-1 plus every point integrated since:
+    // grow all contexts before enqueueing if that bound exceeds a capacity,
+    // so no frame in flight can overflow (no host wait per frame).
+    {
+      uint64_t bound = occ_known;
+      for (size_t i = known; i <= k; ++i) bound += n[i];
+      bound = std::min<uint64_t>(bound, g->gd.ncells);
+      if (bound > cap_min) {
+        for (int q = 0; q < nslot; ++q) {
+          g->use_seg(q);
+          ck(cudaStreamSynchronize(g->stream), "sync");
+        }
+        ck(cudaStreamSynchronize(g->mstream), "sync");
+        const uint32_t need = static_cast<uint32_t>(std::max<uint64_t>(bound, 2ull * cap_min));
+        const uint32_t v = static_cast<uint32_t>(std::min<uint64_t>(need, g->gd.ncells));
+        for (int q = 0; q < nslot; ++q) {
+          g->use_seg(q);
+          g->seg.ensure(std::max(g->seg.b.Vcap, v), std::max(g->seg.b.Scap, v), std::max(g->seg.b.Icap, v),
+                        pl->p.ransac.iterations, g->gd.nwords);
+        }
+        cap_min = v;
+      }
     }
     g->set_slot(s);
     g->use_seg(s);
@@ -1392,13 +1432,8 @@ void pipeline_run(vp_pipeline* pl, size_t nf, const float* const* xyz, const uin
     // below after an overflow)
     if (graphs) run_part_graph(pl, 2, g->stream, seg_rest); else seg_rest();
     ck(cudaEventRecord(pl->ev_done[s], g->stream), "ev");
-    // capacity check point: frame k+1 has not touched the grid yet
-    ck(cudaEventSynchronize(pl->ev_clu[s]), "sync");
-    if (g->h_ctr->overflow) {
-      ck(cudaStreamSynchronize(g->stream), "sync");
-      rerun_segment_until_fits(g, pl->p);  // whole segmentation, synchronous
-      ck(cudaEventRecord(pl->ev_done[s], g->stream), "ev");
-    }
+    // no host round trip before the next frame's mapping: the capacities were
+    // sized above for this frame's worst case, and harvest() checks the flags
     ++pl->frame;
   }
   for (int q = 0; q < nslot; ++q) {
