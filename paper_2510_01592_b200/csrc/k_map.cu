@@ -491,17 +491,104 @@ __global__ void k_dda_scatter(const FrameParams* __restrict__ fp, DdaBins* db, c
 // mask key (word << 5 | bit, or << 6 for bricks; injective over the grid's cells), and only the
 // stepped axis' t_max is advanced (one DADD). kSlab adds the owned-x-range
 // logic of a spatial slab.
+// Window constants of one frame's walk (voxel_grid.cpp:122-129).
+struct DdaWin {
+  double lo0, lo1, lo2, hi0, hi1, hi2, a0, a1, a2, res;
+  int oc0, oc1, oc2;  // the sensor's cell
+};
+__device__ __forceinline__ DdaWin dda_window(const GridDesc& g, const FrameParams* __restrict__ fp) {
+  DdaWin w;
+  w.res = g.res;
+  w.lo0 = fp->origin_pre[0];
+  w.lo1 = fp->origin_pre[1];
+  w.lo2 = fp->origin_pre[2];
+  w.hi0 = w.lo0 + static_cast<double>(g.gex) * w.res;
+  w.hi1 = w.lo1 + static_cast<double>(g.ey) * w.res;
+  w.hi2 = w.lo2 + static_cast<double>(g.ez) * w.res;
+  w.a0 = fp->t[0];
+  w.a1 = fp->t[1];
+  w.a2 = fp->t[2];
+  w.oc0 = w2i(w.a0, w.lo0, w.res);
+  w.oc1 = w2i(w.a1, w.lo1, w.res);
+  w.oc2 = w2i(w.a2, w.lo2, w.res);
+  return w;
+}
+
+// One ray's DDA start state: window cell, steps, t_max, t_delta, t1, end cell.
+struct DdaRay {
+  double t1, tm0, tm1, tm2, td0, td1, td2;
+  int c0, c1, c2, s0, s1, s2, ec0, ec1, ec2;
+};
+// walk_segment's clip and initialisation (voxel_grid.cpp:130-168), the
+// reference's arithmetic verbatim; false when the end point is not finite
+// (voxel_grid.cpp:189) or the segment misses the window.
+__device__ __forceinline__ bool dda_setup(const DdaWin& w, const FrameParams* __restrict__ fp, uint64_t i,
+                                          const GridDesc& g, DdaRay& r) {
+  const double res = w.res;
+  const float* pp = fp->pts + 3 * i;
+  const d3 bw = pose_apply(fp->R, fp->t, static_cast<double>(pp[0]), static_cast<double>(pp[1]),
+                           static_cast<double>(pp[2]));
+  if (!finite3(bw)) return false;
+  const double d0 = bw.x - w.a0, d1 = bw.y - w.a1, d2 = bw.z - w.a2;
+  double t0 = 0.0, t1 = 1.0;
+  bool skip = false;
+#define VP_CLIP(dk, ak, lok, hik)                         \
+  if (!skip) {                                           \
+    if (dk == 0.0) {                                     \
+      if (ak < lok || ak >= hik) skip = true;            \
+    } else {                                             \
+      double ta = (lok - ak) / dk;                       \
+      double tb = (hik - ak) / dk;                       \
+      if (ta > tb) {                                     \
+        const double sw = ta;                            \
+        ta = tb;                                         \
+        tb = sw;                                         \
+      }                                                  \
+      t0 = (t0 < ta) ? ta : t0;                          \
+      t1 = (tb < t1) ? tb : t1;                          \
+      if (t0 > t1) skip = true;                          \
+    }                                                    \
+  }
+  VP_CLIP(d0, w.a0, w.lo0, w.hi0)
+  VP_CLIP(d1, w.a1, w.lo1, w.hi1)
+  VP_CLIP(d2, w.a2, w.lo2, w.hi2)
+#undef VP_CLIP
+  if (skip) return false;
+  r.t1 = t1;
+  r.ec0 = w2i(bw.x, w.lo0, res);
+  r.ec1 = w2i(bw.y, w.lo1, res);
+  r.ec2 = w2i(bw.z, w.lo2, res);
+  const double e0 = w.a0 + t0 * d0, e1 = w.a1 + t0 * d1, e2 = w.a2 + t0 * d2;
+  int c0 = w2i(e0, w.lo0, res), c1 = w2i(e1, w.lo1, res), c2 = w2i(e2, w.lo2, res);
+  r.c0 = c0 < 0 ? 0 : (g.gex - 1 < c0 ? g.gex - 1 : c0);  // std::clamp
+  r.c1 = c1 < 0 ? 0 : (g.ey - 1 < c1 ? g.ey - 1 : c1);
+  r.c2 = c2 < 0 ? 0 : (g.ez - 1 < c2 ? g.ez - 1 : c2);
+  r.s0 = r.s1 = r.s2 = 0;
+  r.tm0 = r.tm1 = r.tm2 = CUDART_INF;
+  r.td0 = r.td1 = r.td2 = CUDART_INF;
+#define VP_INIT(dk, ck, lok, ek, sk, tmk, tdk)                                        \
+  if (dk > 0.0) {                                                                     \
+    sk = 1;                                                                           \
+    tmk = t0 + (lok + static_cast<double>(ck + 1) * res - ek) / dk;                   \
+    tdk = res / dk;                                                                   \
+  } else if (dk < 0.0) {                                                              \
+    sk = -1;                                                                          \
+    tmk = t0 + (lok + static_cast<double>(ck) * res - ek) / dk;                       \
+    tdk = res / -dk;                                                                  \
+  }
+  VP_INIT(d0, r.c0, w.lo0, e0, r.s0, r.tm0, r.td0)
+  VP_INIT(d1, r.c1, w.lo1, e1, r.s1, r.tm1, r.td1)
+  VP_INIT(d2, r.c2, w.lo2, e2, r.s2, r.tm2, r.td2)
+#undef VP_INIT
+  return true;
+}
+
 template <bool kSlab>
 __device__ __forceinline__ void clear_walk_body(const GridDesc& g, const FrameParams* __restrict__ fp,
                                                 const uint32_t* __restrict__ perm, const DdaBins* db) {
   const uint64_t n = fp->n;
-  const double res = g.res;
-  const double lo0 = fp->origin_pre[0], lo1 = fp->origin_pre[1], lo2 = fp->origin_pre[2];
-  const double hi0 = lo0 + static_cast<double>(g.gex) * res;
-  const double hi1 = lo1 + static_cast<double>(g.ey) * res;
-  const double hi2 = lo2 + static_cast<double>(g.ez) * res;
-  const double a0 = fp->t[0], a1 = fp->t[1], a2 = fp->t[2];
-  const int oc0 = w2i(a0, lo0, res), oc1 = w2i(a1, lo1, res), oc2 = w2i(a2, lo2, res);
+  const DdaWin wn = dda_window(g, fp);
+  const int oc0 = wn.oc0, oc1 = wn.oc1, oc2 = wn.oc2;
   const int max_steps = g.gex + g.ey + g.ez + 4;
   const int own0 = g.xoff + g.own_lo, own1 = g.xoff + g.own_hi;  // window x owned here
   uint32_t* __restrict__ clr = g.clr;
@@ -525,59 +612,12 @@ __device__ __forceinline__ void clear_walk_body(const GridDesc& g, const FramePa
   for (uint64_t r = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < n;
        r += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint64_t i = binned ? perm[r] : r;
-    const float* pp = fp->pts + 3 * i;
-    const d3 bw = pose_apply(fp->R, fp->t, static_cast<double>(pp[0]), static_cast<double>(pp[1]),
-                             static_cast<double>(pp[2]));
-    if (!finite3(bw)) continue;
-    const double d0 = bw.x - a0, d1 = bw.y - a1, d2 = bw.z - a2;
-    // clip [t0, t1] to the window (voxel_grid.cpp:130-142)
-    double t0 = 0.0, t1 = 1.0;
-    bool skip = false;
-#define VP_CLIP(dk, ak, lok, hik)                         \
-    if (!skip) {                                         \
-      if (dk == 0.0) {                                   \
-        if (ak < lok || ak >= hik) skip = true;          \
-      } else {                                           \
-        double ta = (lok - ak) / dk;                     \
-        double tb = (hik - ak) / dk;                     \
-        if (ta > tb) {                                   \
-          const double sw = ta;                          \
-          ta = tb;                                       \
-          tb = sw;                                       \
-        }                                                \
-        t0 = (t0 < ta) ? ta : t0;                        \
-        t1 = (tb < t1) ? tb : t1;                        \
-        if (t0 > t1) skip = true;                        \
-      }                                                  \
-    }
-    VP_CLIP(d0, a0, lo0, hi0)
-    VP_CLIP(d1, a1, lo1, hi1)
-    VP_CLIP(d2, a2, lo2, hi2)
-#undef VP_CLIP
-    if (skip) continue;
-    const int ec0 = w2i(bw.x, lo0, res), ec1 = w2i(bw.y, lo1, res), ec2 = w2i(bw.z, lo2, res);
-    const double e0 = a0 + t0 * d0, e1 = a1 + t0 * d1, e2 = a2 + t0 * d2;
-    int c0 = w2i(e0, lo0, res), c1 = w2i(e1, lo1, res), c2 = w2i(e2, lo2, res);
-    c0 = c0 < 0 ? 0 : (g.gex - 1 < c0 ? g.gex - 1 : c0);  // std::clamp
-    c1 = c1 < 0 ? 0 : (g.ey - 1 < c1 ? g.ey - 1 : c1);
-    c2 = c2 < 0 ? 0 : (g.ez - 1 < c2 ? g.ez - 1 : c2);
-    int s0 = 0, s1 = 0, s2 = 0;
-    double tm0 = CUDART_INF, tm1 = CUDART_INF, tm2 = CUDART_INF;
-    double td0 = CUDART_INF, td1 = CUDART_INF, td2 = CUDART_INF;
-#define VP_INIT(dk, ck, lok, ek, sk, tmk, tdk)                                        \
-    if (dk > 0.0) {                                                                   \
-      sk = 1;                                                                         \
-      tmk = t0 + (lok + static_cast<double>(ck + 1) * res - ek) / dk;                 \
-      tdk = res / dk;                                                                 \
-    } else if (dk < 0.0) {                                                            \
-      sk = -1;                                                                        \
-      tmk = t0 + (lok + static_cast<double>(ck) * res - ek) / dk;                     \
-      tdk = res / -dk;                                                                \
-    }
-    VP_INIT(d0, c0, lo0, e0, s0, tm0, td0)
-    VP_INIT(d1, c1, lo1, e1, s1, tm1, td1)
-    VP_INIT(d2, c2, lo2, e2, s2, tm2, td2)
-#undef VP_INIT
+    DdaRay ry;
+    if (!dda_setup(wn, fp, i, g, ry)) continue;
+    int c0 = ry.c0, c1 = ry.c1, c2 = ry.c2;
+    const int s0 = ry.s0, s1 = ry.s1, s2 = ry.s2, ec0 = ry.ec0, ec1 = ry.ec1, ec2 = ry.ec2;
+    double tm0 = ry.tm0, tm1 = ry.tm1, tm2 = ry.tm2;
+    const double td0 = ry.td0, td1 = ry.td1, td2 = ry.td2, t1 = ry.t1;
     // brick key of a cell of this grid: word << 5 | bit (meaningful while c0
     // is stored here; the end cell's key only when it is owned here)
     const bool e_here = ec0 >= own0 && ec0 < own1 && static_cast<unsigned>(ec1) < static_cast<unsigned>(g.ey) &&
@@ -672,11 +712,85 @@ __device__ __forceinline__ void clear_walk_body(const GridDesc& g, const FramePa
     }
 }
 
+// Coherent rays on a plain grid (the depth-image case): the warp walks its
+// 32 rays in lockstep -- one loop trip per DDA step of the longest ray, lanes
+// whose ray ended idle -- so the left-neighbour dedup is a full-warp shuffle,
+// and the step is branch-free: argmin, one select per axis, one DADD, the
+// cell's row-mask key advanced incrementally (key = word << 5 | bit =
+// row * 32 + z). Same cells, same order per ray as clear_walk_body.
+constexpr uint32_t kNoMark = 0xffffffffu;
+__device__ __forceinline__ void clear_walk_coherent(const GridDesc& g, const FrameParams* __restrict__ fp) {
+  const uint64_t n = fp->n;
+  const DdaWin wn = dda_window(g, fp);
+  uint32_t* __restrict__ clr = g.clr;
+  const uint32_t xs = static_cast<uint32_t>(g.ey) * static_cast<uint32_t>(g.W) * 32u;
+  const uint32_t ys = static_cast<uint32_t>(g.W) * 32u;
+  const unsigned lane = lane_id();
+  const uint32_t ex0 = static_cast<uint32_t>(g.gex), ex1 = static_cast<uint32_t>(g.ey),
+                 ex2 = static_cast<uint32_t>(g.ez);
+  // warp-uniform ray loop (every lane runs the same trips)
+  for (uint64_t r0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u); r0 < n;
+       r0 += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    DdaRay ry;
+    bool live = r0 + lane < n && dda_setup(wn, fp, r0 + lane, g, ry);
+    uint32_t key = kNoMark, key_e = kNoMark, krow = 0;
+    int c0 = 0, c1 = 0, c2 = 0, s0 = 0, s1 = 0, s2 = 0, dxr = 0, dyr = 0;
+    double tm0 = 0.0, tm1 = 0.0, tm2 = 0.0, td0 = 0.0, td1 = 0.0, td2 = 0.0, t1 = 0.0;
+    if (live) {
+      c0 = ry.c0, c1 = ry.c1, c2 = ry.c2, s0 = ry.s0, s1 = ry.s1, s2 = ry.s2;
+      tm0 = ry.tm0, tm1 = ry.tm1, tm2 = ry.tm2, td0 = ry.td0, td1 = ry.td1, td2 = ry.td2, t1 = ry.t1;
+      krow = static_cast<uint32_t>(c0) * xs + static_cast<uint32_t>(c1) * ys;
+      dxr = s0 * static_cast<int>(xs);
+      dyr = s1 * static_cast<int>(ys);
+      if (static_cast<unsigned>(ry.ec0) < ex0 && static_cast<unsigned>(ry.ec1) < ex1 &&
+          static_cast<unsigned>(ry.ec2) < ex2)
+        key_e = static_cast<uint32_t>(ry.ec0) * xs + static_cast<uint32_t>(ry.ec1) * ys +
+                static_cast<uint32_t>(ry.ec2);
+      // the first cell is visited unless it is the origin cell
+      if (!(c0 == wn.oc0 && c1 == wn.oc1 && c2 == wn.oc2)) key = krow + static_cast<uint32_t>(c2);
+      if (key == key_e) key = kNoMark;
+    }
+    // (a ray never exceeds max_steps here: each step moves one axis
+    // monotonically, so it leaves the window after gex + ey + ez steps)
+    for (;;) {
+      // visit: a lane in the same cell as its left neighbour skips the RED
+      const uint32_t prev = __shfl_up_sync(0xffffffffu, key, 1);
+      if (key != kNoMark && (key != prev || lane == 0)) atomicOr(clr + (key >> 5), 1u << (key & 31u));
+      if (!__any_sync(0xffffffffu, live)) break;
+      // one DDA step, branch-free (an ended lane steps too; its state is
+      // garbage from then on and only `live` / `key` are read):
+      // m = argmin t_max, ties to the lower axis (voxel_grid.cpp:170-172);
+      // min t_max >= t1 is "every t_max >= t1" (no min materialised)
+      const bool m1 = tm1 < tm0;
+      const bool m2 = m1 ? (tm2 < tm1) : (tm2 < tm0);
+      const bool x0 = !m1 && !m2, x1 = m1 && !m2;
+      const bool done = tm0 >= t1 && tm1 >= t1 && tm2 >= t1;
+      if (x0) c0 += s0;
+      if (x1) c1 += s1;
+      if (m2) c2 += s2;
+      if (x0) krow += static_cast<uint32_t>(dxr);
+      if (x1) krow += static_cast<uint32_t>(dyr);
+      if (x0) tm0 += td0;  // t_max[m] += t_delta[m]
+      if (x1) tm1 += td1;
+      if (m2) tm2 += td2;
+      live = live && !done && static_cast<unsigned>(c0) < ex0 && static_cast<unsigned>(c1) < ex1 &&
+             static_cast<unsigned>(c2) < ex2;
+      const uint32_t k = krow + static_cast<uint32_t>(c2);
+      key = (live && k != key_e) ? k : kNoMark;
+    }
+  }
+}
+
 #ifndef VP_DDA_MINB
 #define VP_DDA_MINB 4
 #endif
 __global__ void __launch_bounds__(256, VP_DDA_MINB) k_clear_walk(GridDesc g, const FrameParams* __restrict__ fp,
-                                                                  const uint32_t* perm, const DdaBins* db) {
+                                                                  const uint32_t* perm, const DdaBins* db,
+                                                                  int generic) {
+  if (!db->use && !generic) {
+    clear_walk_coherent(g, fp);
+    return;
+  }
   clear_walk_body<false>(g, fp, perm, db);
 }
 __global__ void __launch_bounds__(256, 4) k_clear_walk_slab(GridDesc g, const FrameParams* __restrict__ fp,

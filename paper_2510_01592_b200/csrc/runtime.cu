@@ -30,6 +30,8 @@ thread_local std::string g_err;
 // CCL variant: 0 = min-neighbour hook + forward-window unions (default),
 // 1 = neighbour sampling + giant skip, 2 = hook + giant skip (same labels)
 int g_ccl_mode = 0;
+// VP_WALK_GENERIC=1 (experiments): coherent rays through the generic walk loop
+const int g_walk_generic = std::getenv("VP_WALK_GENERIC") ? 1 : 0;
 std::atomic<uint64_t> g_launches{0};
 
 constexpr double kRadToDeg = 57.295779513082320876798;
@@ -423,6 +425,7 @@ struct vp_grid {
   uint64_t host_occupied = 0;
   cudaStream_t mstream = nullptr;   // mapping stream of pipelined runs
   cudaStream_t fstream = nullptr;   // fork of the mapping stream (integrate grouping || clear_rays)
+  cudaStream_t pstream = nullptr;   // grid-independent first half of a pipelined frame's mapping
   cudaEvent_t fork_ev[2] = {nullptr, nullptr};
   // Segmentation contexts of the pipelined run's slots: frame k's CCL ..
   // polygon chain runs on its slot's stream with its own scratch and ordinal
@@ -498,6 +501,10 @@ struct vp_grid {
     for (auto& e : ev) if (e) cudaEventDestroy(e);
     if (stream) cudaStreamDestroy(stream);
     if (mstream) cudaStreamDestroy(mstream);
+    if (pstream) {
+      cudaStreamSynchronize(pstream);
+      cudaStreamDestroy(pstream);
+    }
     if (fstream) {
       cudaStreamSynchronize(fstream);
       cudaStreamDestroy(fstream);
@@ -527,6 +534,9 @@ struct vp_grid {
       ck(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priority range");
       ck(cudaStreamCreateWithPriority(&mstream, cudaStreamNonBlocking, hi), "stream");
       ck(cudaStreamCreateWithPriority(&fstream, cudaStreamNonBlocking, hi), "stream");
+      const char* pp = std::getenv("VP_PSTREAM_PRIO");  // experiments: 0 = highest .. lowest
+      const int prio = pp ? std::min(lo, hi + std::atoi(pp)) : hi;
+      ck(cudaStreamCreateWithPriority(&pstream, cudaStreamNonBlocking, prio), "stream");
       for (auto& e : fork_ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     }
     lstream = stream;
@@ -784,6 +794,12 @@ struct vp_grid {
   // Grids are sized by the points capacity (grid-stride loops read n from
   // the device params), so the same launches can be replayed as a graph.
   void launch_clear(uint64_t n) {
+    launch_clear_walk(n);
+    launch_clear_apply(n);
+  }
+  // clear_rays, first half: the DDA walks mark the clear masks (reads only
+  // the points, the pose and the pre-recenter window; touches no cell)
+  void launch_clear_walk(uint64_t n) {
     if (n == 0 && !capturing) return;
     const int gp = grid_for(capturing ? pcap : n);
     LAUNCH(k_dda_keys, gp, kThreads, 0, lstream, gd, d_fp, dbins, bin_of);
@@ -793,7 +809,12 @@ struct vp_grid {
       LAUNCH(k_clear_walk_slab, grid_for(capturing ? pcap : n, 148 * 32), kThreads, 0, lstream, gd, d_fp, rperm,
              dbins);
     else
-      LAUNCH(k_clear_walk, grid_for(capturing ? pcap : n, 148 * 32), kThreads, 0, lstream, gd, d_fp, rperm, dbins);
+      LAUNCH(k_clear_walk, grid_for(capturing ? pcap : n, 148 * 32), kThreads, 0, lstream, gd, d_fp, rperm, dbins,
+             g_walk_generic);
+  }
+  // second half: the marked cells are cleared (and the masks zeroed)
+  void launch_clear_apply(uint64_t n) {
+    if (n == 0 && !capturing) return;
     LAUNCH(k_clear_apply, grid_for(gd.nwords), kThreads, 0, lstream, gd, d_fp, ctr, dbins);
     LAUNCH(k_clear_apply_brick, grid_for(gd.nbricks), kThreads, 0, lstream, gd, d_fp, ctr, dbins);
   }
@@ -827,12 +848,22 @@ struct vp_grid {
   // clear_rays and the grouping half of integrate_frame in parallel (fork
   // onto fstream, join before the ordered fold), then recenter, finalize.
   void launch_mapping_forked(uint64_t n) {
+    launch_mapping_pre(n);
+    launch_mapping_post(n);
+  }
+  // The half of the mapping that touches no cell (DDA walks || grouping):
+  // in a pipelined run it overlaps the previous frame's grid readers.
+  void launch_mapping_pre(uint64_t n) {
     ck(cudaEventRecord(fork_ev[0], lstream), "fork");
     ck(cudaStreamWaitEvent(fstream, fork_ev[0], 0), "fork");
     launch_integrate_group(n, fstream);
     ck(cudaEventRecord(fork_ev[1], fstream), "join");
-    launch_clear(n);
+    launch_clear_walk(n);
     ck(cudaStreamWaitEvent(lstream, fork_ev[1], 0), "join");
+  }
+  // the half that updates the cells: clear, ordered fold, recenter
+  void launch_mapping_post(uint64_t n) {
+    launch_clear_apply(n);
     launch_integrate_fold(n);
     launch_recenter();
     launch_finalize();
@@ -1128,11 +1159,12 @@ struct vp_pipeline {
   cudaGraphExec_t gexec = nullptr;
   uint64_t graph_key = 0;
   uint64_t graph_kernels = 0;
-  // pipelined runs: graphs per (slot, part: 0 mapping, 1 seg_a, 2 seg_b)
-  cudaGraphExec_t rx[kSlots][3] = {};
-  uint64_t rkey[kSlots][3] = {};
-  uint64_t rkern[kSlots][3] = {};
-  cudaEvent_t ev_start[kSlots] = {}, ev_map[kSlots] = {};
+  // pipelined runs: graphs per (slot, part: 0 mapping pre, 1 mapping post,
+  // 2 grid readers, 3 chain)
+  cudaGraphExec_t rx[kSlots][4] = {};
+  uint64_t rkey[kSlots][4] = {};
+  uint64_t rkern[kSlots][4] = {};
+  cudaEvent_t ev_start[kSlots] = {}, ev_pre[kSlots] = {}, ev_map[kSlots] = {};
   cudaEvent_t ev_clu[kSlots] = {}, ev_done[kSlots] = {};
   cudaEvent_t ev_h2d[kSlots] = {};
   cudaStream_t cstream = nullptr;  // host-to-device copies of upcoming frames
@@ -1141,7 +1173,7 @@ struct vp_pipeline {
     for (auto& row : rx)
       for (auto& x : row)
         if (x) cudaGraphExecDestroy(x);
-    for (auto* e : {ev_start, ev_map, ev_clu, ev_done, ev_h2d})
+    for (auto* e : {ev_start, ev_pre, ev_map, ev_clu, ev_done, ev_h2d})
       for (int q = 0; q < kSlots; ++q)
         if (e[q]) cudaEventDestroy(e[q]);
     if (cstream) {
@@ -1268,16 +1300,21 @@ void run_part_graph(vp_pipeline* pl, int part, cudaStream_t st, F&& enqueue) {
   g_launches.fetch_add(pl->rkern[s][part]);
 }
 
-// run_frames (pipeline.cpp:157-245) over a whole stream with two frames in
-// flight: the mapping of frame k+1 (clear/integrate/recenter, on the mapping
-// stream) only has to wait for frame k's segmentation to finish reading the
-// grid (end of seg_a), so it overlaps frame k's fit_planes/refine/make_polygon.
-// The host checks frame k's capacities at that same point, before frame k+1
-// touches the grid, so an overflow is re-run exactly as in the single-frame path.
+// run_frames (pipeline.cpp:157-245) over a whole stream with kSlots frames in
+// flight. Per frame k:
+//   mstream  map_pre(k)  DDA walks || point grouping   after map_post(k-1)
+//   mstream  map_post(k) clear, fold, recenter          after readers(k-1), map_pre(k)
+//   mstream  readers(k)  occupied scan .. ordinal map
+//   slot     chain(k)    CCL .. polygons                 overlaps later frames
+// The critical path is mapping + readers per frame; the chains fill the
+// rest of the GPU. (VP_MAP_SPLIT=1 moves map_pre to its own stream so the
+// walks of frame k+1 overlap frame k's readers: slower on C2, the GPU is
+// already saturated.) Capacities are sized from the occupancy bound before
+// enqueueing, so the host never waits per frame.
 void pipeline_run(vp_pipeline* pl, size_t nf, const float* const* xyz, const uint64_t* n,
                   const double* R, const double* t, bool device_ptrs, vp_frame_timing* timings) {
   vp_grid* g = pl->grid;
-  for (auto* e : {pl->ev_start, pl->ev_map, pl->ev_clu, pl->ev_done, pl->ev_h2d})
+  for (auto* e : {pl->ev_start, pl->ev_pre, pl->ev_map, pl->ev_clu, pl->ev_done, pl->ev_h2d})
     for (int q = 0; q < kSlots; ++q)
       if (!e[q]) ck(cudaEventCreate(&e[q]), "event");
   if (!pl->cstream) ck(cudaStreamCreateWithFlags(&pl->cstream, cudaStreamNonBlocking), "stream");
@@ -1313,6 +1350,11 @@ void pipeline_run(vp_pipeline* pl, size_t nf, const float* const* xyz, const uin
   g->use_seg(0);
   ck(cudaStreamSynchronize(g->stream), "sync");
   const bool graphs = !g_prof_on && !std::getenv("VP_NO_GRAPH");
+  // VP_MAP_SPLIT=1: the mapping's first half on its own stream, overlapping
+  // the previous frame's grid readers (measured slower on C2: the DDA walks
+  // then contend with the critical path), else both halves on the mapping stream
+  const char* split_env = std::getenv("VP_MAP_SPLIT");
+  const cudaStream_t ps = (split_env && split_env[0] == '1') ? g->pstream : g->mstream;
   // frame k-kSlots's slot is reused by frame k: its whole chain must be done
   auto harvest = [&](size_t k) {
     const int s = static_cast<int>(k % kSlots);
@@ -1320,8 +1362,9 @@ void pipeline_run(vp_pipeline* pl, size_t nf, const float* const* xyz, const uin
       fail(VP_ENOMEM, "more than 2048 clusters >= min_cluster_size in one frame");
     if (g->h_ctr_s[s]->overflow) fail(VP_ENOMEM, "segmentation capacity overflow in a pipelined frame");
     if (std::getenv("VP_PIPE_STATS")) {  // stage spans of the pipelined frame (diagnostics)
-      float a = 0.f, b = 0.f, c = 0.f;
-      ck(cudaEventElapsedTime(&a, pl->ev_start[s], pl->ev_map[s]), "elapsed");
+      float a = 0.f, b = 0.f, c = 0.f, a0 = 0.f;
+      ck(cudaEventElapsedTime(&a0, pl->ev_start[s], pl->ev_pre[s]), "elapsed");
+      ck(cudaEventElapsedTime(&a, pl->ev_pre[s], pl->ev_map[s]), "elapsed");
       ck(cudaEventElapsedTime(&b, pl->ev_map[s], pl->ev_clu[s]), "elapsed");
       ck(cudaEventElapsedTime(&c, pl->ev_clu[s], pl->ev_done[s]), "elapsed");
       float gap = -1.f;  // mapping stream idle between this frame's readers and the next frame's start
@@ -1330,8 +1373,10 @@ void pipeline_run(vp_pipeline* pl, size_t nf, const float* const* xyz, const uin
           cudaGetLastError();
           gap = -1.f;
         }
-      std::fprintf(stderr, "frame %zu: map %.1f us, grid readers %.1f us, chain %.1f us, gap to next %.1f us\n", k,
-                   1e3 * a, 1e3 * b, 1e3 * c, 1e3 * gap);
+      std::fprintf(stderr,
+                   "frame %zu: map pre %.1f us, post %.1f us, grid readers %.1f us, chain %.1f us, "
+                   "readers end to next start %.1f us\n",
+                   k, 1e3 * a0, 1e3 * a, 1e3 * b, 1e3 * c, 1e3 * gap);
     }
     if (!timings) return;
     float ms = 0.f;
@@ -1366,6 +1411,7 @@ void pipeline_run(vp_pipeline* pl, size_t nf, const float* const* xyz, const uin
           ck(cudaStreamSynchronize(g->stream), "sync");
         }
         ck(cudaStreamSynchronize(g->mstream), "sync");
+        ck(cudaStreamSynchronize(ps), "sync");
         const uint32_t need = static_cast<uint32_t>(std::max<uint64_t>(bound, 2ull * cap_min));
         const uint32_t v = static_cast<uint32_t>(std::min<uint64_t>(need, g->gd.ncells));
         for (int q = 0; q < nslot; ++q) {
@@ -1385,7 +1431,7 @@ void pipeline_run(vp_pipeline* pl, size_t nf, const float* const* xyz, const uin
     } else {
       if (k == 0) h2d_ahead(0);
       h2d_ahead(k + 1);
-      ck(cudaStreamWaitEvent(g->mstream, pl->ev_h2d[s], 0), "wait");
+      ck(cudaStreamWaitEvent(ps, pl->ev_h2d[s], 0), "wait");
       g->h_fp->pts = g->d_pts;
     }
     g->h_fp->n = n[k];
@@ -1396,16 +1442,26 @@ void pipeline_run(vp_pipeline* pl, size_t nf, const float* const* xyz, const uin
       g->plan_recenter(t + 3 * k, &ss);
       std::memcpy(pl->last_cell, cell, sizeof cell);
     }
-    // mapping of frame k: after frame k-1 stopped reading the grid
-    if (k >= 1) ck(cudaStreamWaitEvent(g->mstream, pl->ev_clu[prev], 0), "wait");
-    ck(cudaEventRecord(pl->ev_start[s], g->mstream), "ev");
-    g->lstream = g->mstream;
-    auto map_part = [&] {
+    // mapping of frame k, first half (DDA walks marking the clear masks ||
+    // grouping the points; no cell touched): on the pre-mapping stream once
+    // frame k-1's mapping has consumed the masks and the grouping buffers,
+    // i.e. concurrently with frame k-1's grid readers
+    if (k >= 1) ck(cudaStreamWaitEvent(ps, pl->ev_map[prev], 0), "wait");
+    ck(cudaEventRecord(pl->ev_start[s], ps), "ev");
+    g->lstream = ps;
+    auto map_pre = [&] {
       g->upload_params();
       g->reset_frame_counters();
-      g->launch_mapping_forked(n[k]);
+      g->launch_mapping_pre(n[k]);
     };
-    if (graphs) run_part_graph(pl, 0, g->mstream, map_part); else map_part();
+    if (graphs) run_part_graph(pl, 0, ps, map_pre); else map_pre();
+    ck(cudaEventRecord(pl->ev_pre[s], ps), "ev");
+    // second half (clear, ordered fold, recenter) on the mapping stream:
+    // after frame k-1's grid readers (stream order) and the first half
+    ck(cudaStreamWaitEvent(g->mstream, pl->ev_pre[s], 0), "wait");
+    g->lstream = g->mstream;
+    auto map_post = [&] { g->launch_mapping_post(n[k]); };
+    if (graphs) run_part_graph(pl, 1, g->mstream, map_post); else map_post();
     g->lstream = g->stream;
     ck(cudaEventRecord(pl->ev_map[s], g->mstream), "ev");
     // segmentation of frame k: the grid readers (occupied scan .. ordinal
@@ -1423,14 +1479,14 @@ void pipeline_run(vp_pipeline* pl, size_t nf, const float* const* xyz, const uin
       g->launch_seg_b(pl->p, false);
       ck(cudaMemcpyAsync(g->h_ctr, g->ctr, sizeof(Counters), cudaMemcpyDeviceToHost, g->stream), "ctr");
     };
-    if (graphs) run_part_graph(pl, 1, g->stream, seg_grid); else seg_grid();
+    if (graphs) run_part_graph(pl, 2, g->stream, seg_grid); else seg_grid();
     ck(cudaEventRecord(pl->ev_clu[s], g->stream), "ev");
     g->stream = slot_stream;
     ck(cudaStreamWaitEvent(g->stream, pl->ev_clu[s], 0), "wait");
     // the chain is enqueued before the host looks at the capacities (it only
     // reads this slot's buffers, clamped to their capacities, and is redone
     // below after an overflow)
-    if (graphs) run_part_graph(pl, 2, g->stream, seg_rest); else seg_rest();
+    if (graphs) run_part_graph(pl, 3, g->stream, seg_rest); else seg_rest();
     ck(cudaEventRecord(pl->ev_done[s], g->stream), "ev");
     // no host round trip before the next frame's mapping: the capacities were
     // sized above for this frame's worst case, and harvest() checks the flags
@@ -1441,6 +1497,7 @@ void pipeline_run(vp_pipeline* pl, size_t nf, const float* const* xyz, const uin
     ck(cudaStreamSynchronize(g->stream), "sync");
   }
   ck(cudaStreamSynchronize(g->mstream), "sync");
+  ck(cudaStreamSynchronize(ps), "sync");
   ck(cudaStreamSynchronize(pl->cstream), "sync");
   for (size_t k = nf >= static_cast<size_t>(kSlots) ? nf - kSlots : 0; k < nf; ++k) harvest(k);
   const int last = nf ? static_cast<int>((nf - 1) % kSlots) : 0;

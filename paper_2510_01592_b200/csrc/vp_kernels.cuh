@@ -285,7 +285,7 @@ __global__ void k_integrate_fold_dense(GridDesc g, const FrameParams* fp, Counte
                                        uint32_t* hcnt, const uint32_t* hoff, const uint32_t* sorted,
                                        const uint32_t* pslot, const uint32_t* dense);
 constexpr int kDenseSmem = 1024 * 24 + 16384 * 4;  // k_integrate_fold_dense dynamic shared memory
-__global__ void k_clear_walk(GridDesc g, const FrameParams* fp, const uint32_t* perm, const DdaBins* db);
+__global__ void k_clear_walk(GridDesc g, const FrameParams* fp, const uint32_t* perm, const DdaBins* db, int generic);
 __global__ void k_clear_walk_slab(GridDesc g, const FrameParams* fp, const uint32_t* perm, const DdaBins* db);
 __global__ void k_dda_keys(GridDesc g, const FrameParams* fp, DdaBins* db, uint8_t* bin_of);
 __global__ void k_dda_plan(DdaBins* db);
