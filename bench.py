@@ -116,8 +116,7 @@ def algorithmic_bytes(c, n_points):
         "k_integrate_hash": 12 * n_points + 8 * n_points,
         "k_integrate_fold": 64 * touched + 12 * n_points,      # cell RMW + points
         "k_recenter": 3 * C_BITS + 32 * dropped,
-        "k_bitmap_count": C_BITS,
-        "k_bitmap_emit": C_BITS + 4 * V,
+        "k_bitmap_compact": C_BITS + 4 * V,
         "k_normals": 32 * V + 4 * V + 72 * V,                  # cells, list in, estimate out
         "k_ccl_hook": 56 * S,
         "k_ccl_compress": 8 * S,
@@ -134,6 +133,28 @@ def algorithmic_bytes(c, n_points):
 
 
 C_BITS = 0  # set from the grid size (cells / 8)
+
+
+def hbm_peak(peaks):
+    """HBM copy bandwidth (GB/s) from the driver-written MEASURED_PEAKS.json:
+    the burst figure (the top kernel is timed alone, one launch at a time in
+    the event profile), else any HBM figure, else the B200_PROFILING fallback."""
+    flat = {}
+
+    def walk(d, pre=""):
+        for k, v in d.items():
+            if isinstance(v, dict):
+                walk(v, pre + k + ".")
+            elif isinstance(v, (int, float)) and not isinstance(v, bool):
+                flat[(pre + k).lower()] = float(v)
+    if isinstance(peaks, dict):
+        walk(peaks)
+    hbm = {k: v for k, v in flat.items() if ("hbm" in k or "dram" in k or "copy" in k) and v > 100}
+    for pick in ("burst", ""):
+        for k, v in sorted(hbm.items()):
+            if pick in k:
+                return v, f"MEASURED_PEAKS.json {k}"
+    return 6650.0, "fallback 6650 (B200_PROFILING.md)"
 
 
 # ------------------------------------------------------------------- ours
@@ -272,12 +293,13 @@ def run_ours(args, rank, world, dist):
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         pass
-    peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak, peak_source = hbm_peak(peaks)
     achieved = per_launch_bytes / per_launch_s / 1e9
-    traffic = None
-    try:  # DRAM bytes of the same kernel from the committed ncu --set full capture
-        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))["dram_bytes_per_launch"]
-        traffic = tr.get(top)
+    traffic, limiter = None, None
+    try:  # DRAM bytes and pipe utilisation of the same kernel from the committed ncu --set full capture
+        nt = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        traffic = nt["dram_bytes_per_launch"].get(top)
+        limiter = nt.get("utilisation_pct", {}).get(top)
     except Exception:
         pass
     # whole-step algorithmic bytes (the survey's frame formula)
@@ -312,8 +334,8 @@ def run_ours(args, rank, world, dist):
         "roofline": {"bound": "hbm", "kernel": top, "achieved": round(achieved, 2), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 5), "traffic": traffic,
                      "alg_bytes_per_launch": round(per_launch_bytes), "us_per_launch": round(per_launch_s * 1e6, 2),
-                     "share_of_step": round(top_ms / prof_total, 4),
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650"},
+                     "share_of_step": round(top_ms / prof_total, 4), "peak_source": peak_source,
+                     "utilisation_pct_ncu": limiter},
         "kernels": {k: {"ms_per_step": round(v[0], 4), "calls": int(v[1])}
                     for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])},
         "clocks": clk.summary(),
@@ -494,7 +516,7 @@ def run_slabs(args, rank, world, dist):
     own_bits = (hi - lo) * ext[1] * ext[2] / 8
     alg = {"k_clear_walk": 12 * n + cleared / 8, "k_clear_apply": 2 * own_bits + 32 * freed,
            "k_integrate_fold": 64 * touched + 12 * n, "k_integrate_hash": 20 * n,
-           "k_bitmap_count": own_bits, "k_bitmap_emit": own_bits + 4 * V, "k_normals": 108 * V,
+           "k_bitmap_compact": own_bits + 4 * V, "k_normals": 108 * V,
            "k_ccl_hook": 56 * S_, "k_ccl_union": 56 * S_, "k_ccl_compress": 8 * S_, "k_ccl_flatten": 12 * S_,
            "k_map_fill": 16 * S_, "k_ransac_count": 24 * padded, "k_extract_count": 24 * padded,
            "k_refine": 48 * inl, "k_poly_hull": 64 * poolv}
@@ -506,7 +528,7 @@ def run_slabs(args, rank, world, dist):
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         pass
-    peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak, peak_source = hbm_peak(peaks)
     achieved = alg[top] / top_calls / (top_ms / top_calls / 1e3) / 1e9
     frame_bytes = 12 * n + 64 * touched + 32 * freed + own_bits + 72 * V + 56 * S_ + 24 * padded + 48 * inl + 64 * poolv
     timed_pts = sum(npts[W:W + K])
@@ -544,7 +566,7 @@ def run_slabs(args, rank, world, dist):
                      "alg_bytes_per_launch": round(alg[top] / top_calls),
                      "us_per_launch": round(top_ms / top_calls * 1e3, 2),
                      "share_of_step": round(top_ms / prof_total, 4),
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650"},
+                     "peak_source": peak_source},
         "kernels_rank0": {k: {"ms_per_frame": round(v[0], 4), "calls": int(v[1])}
                           for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])},
         "clocks": clk.summary(),

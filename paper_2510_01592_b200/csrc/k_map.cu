@@ -807,8 +807,8 @@ __device__ __forceinline__ void zero_cell(Cell* c) {
 }
 
 // Row-layout clear mask (coherent rays): one thread per bitmap word.
-__global__ void k_clear_apply(GridDesc g, const FrameParams* __restrict__ fp, Counters* ctr, const DdaBins* db) {
-  if (db->use) return;
+__device__ __forceinline__ void clear_apply_rows(const GridDesc& g, const FrameParams* __restrict__ fp,
+                                                 Counters* ctr) {
   uint32_t* occ = fp->occ_pre;
   unsigned long long cl = 0, fr = 0;
   for (uint64_t w = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; w < g.nwords;
@@ -840,9 +840,8 @@ __global__ void k_clear_apply(GridDesc g, const FrameParams* __restrict__ fp, Co
 // the unique cleared cells, free the occupied ones (the occupancy bits of the
 // brick's 16 (x, y) columns are gathered from the row-layout bitmap, four z
 // bits each), zero the mask.
-__global__ void k_clear_apply_brick(GridDesc g, const FrameParams* __restrict__ fp, Counters* ctr,
-                                    const DdaBins* db) {
-  if (!db->use) return;
+__device__ __forceinline__ void clear_apply_bricks(const GridDesc& g, const FrameParams* __restrict__ fp,
+                                                   Counters* ctr) {
   uint32_t* occ = fp->occ_pre;
   unsigned long long cl = 0, fr = 0;
   for (uint64_t w = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; w < g.nbricks;
@@ -873,6 +872,11 @@ __global__ void k_clear_apply_brick(GridDesc g, const FrameParams* __restrict__ 
   }
   warp_add_u64(&ctr->cleared, cl);
   warp_add_u64(&ctr->freed, fr);
+}
+
+// One launch for either mask layout (k_dda_plan's decision for this frame).
+__global__ void k_clear_apply(GridDesc g, const FrameParams* __restrict__ fp, Counters* ctr, const DdaBins* db) {
+  if (db->use) clear_apply_bricks(g, fp, ctr); else clear_apply_rows(g, fp, ctr);
 }
 
 // ---------------------------------------------------------------------------
@@ -983,25 +987,34 @@ __global__ void k_frame_begin(Counters* ctr, const unsigned long long* occ_total
 
 // ---------------------------------------------------------------------------
 // occupied_voxels (voxel_grid.cpp:254-263): ordered compaction of the logical
-// bitmap (x, y, z lexicographic) into logical flat indices.
-// 256 threads x 8 words per block.
+// bitmap (x, y, z lexicographic) into logical flat indices, 256 threads x 8
+// words per tile, in one pass (count, decoupled look-back, emit): the grid
+// readers of a pipelined frame are on the critical path, so there is no
+// separate block-sum scan and the bitmap is read once.
 // ---------------------------------------------------------------------------
-__global__ void k_bitmap_count(const FrameParams* __restrict__ fp, uint64_t w_lo, uint64_t nwords,
-                               uint32_t* bsum) {
-  const uint32_t* __restrict__ bits = fp->occ_post + w_lo;
-  const uint64_t w0 = (static_cast<uint64_t>(blockIdx.x) * kScanThreads + threadIdx.x) * kScanItems;
-  uint32_t c = 0;
-#pragma unroll
-  for (int k = 0; k < kScanItems; ++k)
-    if (w0 + k < nwords) c += __popc(bits[w0 + k]);
-  c = block_sum_u32(c);
-  if (threadIdx.x == 0) bsum[blockIdx.x] = c;
+__device__ __forceinline__ uint32_t tile_exclusive(const ScanTiles& st, uint32_t tile, uint32_t epoch,
+                                                   uint32_t c, uint32_t* agg_out) {
+  __shared__ uint32_t s_prefix, s_agg;
+  const uint32_t ex = block_exclusive_u32(c);
+  if (threadIdx.x == blockDim.x - 1) s_agg = ex + c;
+  __syncthreads();
+  const uint32_t agg = s_agg;
+  if (threadIdx.x < 32) {
+    const uint32_t pre = tile_prefix(st, tile, epoch, agg);
+    if (threadIdx.x == 0) s_prefix = pre;
+  }
+  __syncthreads();
+  *agg_out = agg;
+  return s_prefix + ex;
 }
 
-__global__ void k_bitmap_emit(const FrameParams* __restrict__ fp, uint64_t w_lo, uint64_t nwords, int W,
-                              int ez, const uint32_t* boff, uint32_t* out, uint32_t cap) {
+__global__ void __launch_bounds__(kScanThreads) k_bitmap_compact(const FrameParams* __restrict__ fp, uint64_t w_lo,
+                                                                 uint64_t nwords, int W, int ez, ScanTiles st,
+                                                                 uint32_t* out, uint32_t cap, uint32_t* total) {
+  uint32_t tile, epoch;
+  tile_claim(st, tile, epoch);
   const uint32_t* __restrict__ bits = fp->occ_post + w_lo;
-  const uint64_t w0 = (static_cast<uint64_t>(blockIdx.x) * kScanThreads + threadIdx.x) * kScanItems;
+  const uint64_t w0 = (static_cast<uint64_t>(tile) * kScanThreads + threadIdx.x) * kScanItems;
   uint32_t v[kScanItems];
   uint32_t c = 0;
 #pragma unroll
@@ -1009,7 +1022,9 @@ __global__ void k_bitmap_emit(const FrameParams* __restrict__ fp, uint64_t w_lo,
     v[k] = (w0 + k < nwords) ? bits[w0 + k] : 0u;
     c += __popc(v[k]);
   }
-  uint32_t pos = boff[blockIdx.x] + block_exclusive_u32(c);
+  uint32_t agg;
+  uint32_t pos = tile_exclusive(st, tile, epoch, c, &agg);
+  if (tile == st.nb - 1 && threadIdx.x == blockDim.x - 1) *total = pos + c;
 #pragma unroll
   for (int k = 0; k < kScanItems; ++k) {
     uint32_t b = v[k];
@@ -1024,6 +1039,31 @@ __global__ void k_bitmap_emit(const FrameParams* __restrict__ fp, uint64_t w_lo,
       ++pos;
     }
   }
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_flags_compact(const uint8_t* __restrict__ flags,
+                                                                const uint32_t* n_ptr, uint32_t cap, ScanTiles st,
+                                                                uint32_t* pos_out, uint32_t* total) {
+  uint32_t tile, epoch;
+  tile_claim(st, tile, epoch);
+  const uint32_t n = min(*n_ptr, cap);
+  const uint64_t i0 = (static_cast<uint64_t>(tile) * kScanThreads + threadIdx.x) * kScanItems;
+  uint8_t f[kScanItems];
+  uint32_t c = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    f[k] = (i0 + k < n) ? flags[i0 + k] : 0;
+    c += f[k] ? 1u : 0u;
+  }
+  uint32_t agg;
+  uint32_t pos = tile_exclusive(st, tile, epoch, c, &agg);
+  if (tile == st.nb - 1 && threadIdx.x == blockDim.x - 1) *total = pos + c;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k)
+    if (i0 + k < n) {
+      pos_out[i0 + k] = pos;
+      pos += f[k] ? 1u : 0u;
+    }
 }
 
 // Generic ordered compaction of u8 flags: positions[i] = exclusive rank.

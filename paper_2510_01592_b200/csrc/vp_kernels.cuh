@@ -14,7 +14,10 @@ constexpr int kClusterBins = 2048;  // clusters handled by the counting sort per
 constexpr int kChunk = 256;         // ordinals per counting-sort chunk (one warp)
 constexpr int kHullSmem = 512;      // survivors sorted in shared memory (6 regions of this size)
 constexpr int kPolyChunk = 1024;    // inlier points per polygon-stage block
-constexpr int kFoldSmall = 24;      // integrate: points per voxel folded by one thread
+#ifndef VP_FOLD_SMALL
+#define VP_FOLD_SMALL 24
+#endif
+constexpr int kFoldSmall = VP_FOLD_SMALL;  // integrate: points per voxel folded by one thread
 constexpr int kFoldMax = 128;       // integrate: points per voxel folded by one warp
 constexpr uint32_t kDenseSort = 16384;  // denser voxels: indices bitonic-sorted in shared memory
 
@@ -65,6 +68,63 @@ __device__ __forceinline__ uint32_t block_sum_u32(uint32_t v) {
   const uint32_t r = tot;
   __syncthreads();
   return r;
+}
+
+// Single-pass ordered compaction (decoupled look-back): a block takes the
+// next tile in launch order from a ticket counter, publishes its aggregate,
+// and one warp sums its predecessors' published values until it meets an
+// inclusive prefix. Tile words pack [epoch:30 | status:2 | value:32]
+// (status 1 = aggregate, 2 = inclusive); the epoch (ticket / nb + 1) tells a
+// word of this launch from a stale one, so the state is never reset. The
+// ticket counter advances by exactly nb per launch (one launch at a time per
+// ScanTiles, stream order).
+struct ScanTiles {
+  unsigned long long* state;   // nb words, zero-initialised once
+  unsigned long long* ticket;  // persistent launch-order counter
+  uint32_t nb;
+};
+
+// Thread 0 claims the block's tile; every thread gets (tile, epoch).
+__device__ __forceinline__ void tile_claim(const ScanTiles& st, uint32_t& tile, uint32_t& epoch) {
+  __shared__ uint32_t s_t, s_e;
+  if (threadIdx.x == 0) {
+    const unsigned long long t = atomicAdd(st.ticket, 1ull);
+    s_t = static_cast<uint32_t>(t % st.nb);
+    s_e = static_cast<uint32_t>((t / st.nb + 1ull) & 0x3fffffffull);
+  }
+  __syncthreads();
+  tile = s_t;
+  epoch = s_e;
+}
+
+// Called by all 32 lanes of one warp with the tile's aggregate: returns the
+// exclusive prefix of the tile and publishes its inclusive prefix.
+__device__ __forceinline__ uint32_t tile_prefix(const ScanTiles& st, uint32_t tile, uint32_t epoch,
+                                                uint32_t agg) {
+  const unsigned lane = threadIdx.x & 31u;
+  volatile unsigned long long* s = st.state;
+  const unsigned long long E = static_cast<unsigned long long>(epoch) << 34;
+  if (tile == 0) {
+    if (lane == 0) s[0] = E | (2ull << 32) | agg;
+    return 0u;
+  }
+  if (lane == 0) s[tile] = E | (1ull << 32) | agg;
+  uint32_t excl = 0;
+  for (int p = static_cast<int>(tile) - 1;; p -= 32) {
+    const int q = p - static_cast<int>(lane);
+    unsigned long long v;
+    uint32_t status;
+    do {
+      v = q >= 0 ? s[q] : (E | (2ull << 32));  // before tile 0: an inclusive 0
+      status = (v >> 34) == epoch ? static_cast<uint32_t>(v >> 32) & 3u : 0u;
+    } while (__any_sync(0xffffffffu, status == 0u));
+    const unsigned incl = __ballot_sync(0xffffffffu, status == 2u);
+    const int k = incl ? __ffs(incl) - 1 : 31;  // nearest inclusive predecessor
+    excl += __reduce_add_sync(0xffffffffu, static_cast<int>(lane) <= k ? static_cast<uint32_t>(v) : 0u);
+    if (incl) break;
+  }
+  if (lane == 0) s[tile] = E | (2ull << 32) | (excl + agg);
+  return excl;
 }
 
 // Union-find over int32 parent arrays (CCL and the slab boundary merge).
@@ -291,21 +351,21 @@ __global__ void k_dda_keys(GridDesc g, const FrameParams* fp, DdaBins* db, uint8
 __global__ void k_dda_plan(DdaBins* db);
 __global__ void k_dda_scatter(const FrameParams* fp, DdaBins* db, const uint8_t* bin_of, uint32_t* perm);
 __global__ void k_clear_apply(GridDesc g, const FrameParams* fp, Counters* ctr, const DdaBins* db);
-__global__ void k_clear_apply_brick(GridDesc g, const FrameParams* fp, Counters* ctr, const DdaBins* db);
 __global__ void k_recenter(GridDesc g, const FrameParams* fp, Counters* ctr);
 __global__ void k_map_finalize(Counters* ctr, unsigned long long* occ_total);
 __global__ void k_frame_begin(Counters* ctr, const unsigned long long* occ_total);
 __global__ void k_set_statuses(GridDesc g, const FrameParams* fp, const int32_t* idx, const uint8_t* st,
                                uint64_t n);
-__global__ void k_bitmap_count(const FrameParams* fp, uint64_t w_lo, uint64_t nwords, uint32_t* bsum);
-__global__ void k_bitmap_emit(const FrameParams* fp, uint64_t w_lo, uint64_t nwords, int W, int ez,
-                              const uint32_t* boff, uint32_t* out, uint32_t cap);
 __global__ void k_flags_count(const uint8_t* flags, const uint32_t* n_ptr, uint32_t cap,
                               uint32_t* bsum);
 __global__ void k_flags_positions(const uint8_t* flags, const uint32_t* n_ptr, uint32_t cap,
                                   const uint32_t* boff, uint32_t* pos_out);
 __global__ void k_merge_point(GridDesc g, const FrameParams* fp, Counters* ctr, int x, int y, int z,
                               double px, double py, double pz);
+__global__ void k_bitmap_compact(const FrameParams* fp, uint64_t w_lo, uint64_t nwords, int W, int ez,
+                                 ScanTiles st, uint32_t* out, uint32_t cap, uint32_t* total);
+__global__ void k_flags_compact(const uint8_t* flags, const uint32_t* n_ptr, uint32_t cap, ScanTiles st,
+                                uint32_t* pos_out, uint32_t* total);
 __global__ void k_scan_exclusive(uint32_t* a, uint32_t n_static, const uint32_t* n_ptr,
                                  uint32_t* total, uint32_t* total2);
 

@@ -52,8 +52,19 @@ def full(path):
             sm_pct=g("sm__throughput.avg.pct_of_peak_sustained_elapsed"),
             mem_pct=g("gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed"),
             warps_active=g("sm__warps_active.avg.pct_of_peak_sustained_active"),
-            regs=g("launch__registers_per_thread"), stalls=st[:5])
+            regs=g("launch__registers_per_thread"), stalls=st[:5],
+            pipes={k: g(m)[0] for k, m in PIPES.items()})
     return out
+
+
+# what limits a kernel that is not bandwidth-bound: issue slots and pipe utilisation
+PIPES = {"issue": "sm__issue_active.avg.pct_of_peak_sustained_elapsed",
+         "alu": "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+         "fma": "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+         "fp64": "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+         "lsu": "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+         "l2": "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+         "dram": "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"}
 
 
 def to_bytes(v, unit):
@@ -74,7 +85,7 @@ def main(tag):
         for k, (t, n) in sorted(agg.items(), key=lambda kv: -kv[1][0]):
             f.write(f"{k:28s} {n:8d} {t / 1e3:10.1f} {t / 1e3 / n:10.2f} {100 * t / tot:6.1f}%\n")
     fl = full(os.path.join(src, f"{tag}_top.ncu-rep"))
-    traffic = {}
+    traffic, pipes = {}, {}
     with open(os.path.join(dst, f"{tag}_ncu_top.txt"), "w") as f:
         f.write("# ncu --set full --clock-control none, one launch per kernel (C2 frame ~10)\n")
         for k, d in fl.items():
@@ -86,7 +97,10 @@ def main(tag):
             f.write(f"   SM throughput {d['sm_pct'][0]:.1f}%, memory throughput {d['mem_pct'][0]:.1f}%, "
                     f"warps active {d['warps_active'][0]:.1f}%, {int(d['regs'][0])} regs/thread\n")
             f.write("   stalls per issue: " + ", ".join(f"{n}={v:.2f}" for v, n in d["stalls"]) + "\n")
-    json.dump({"source": f"profiles/{tag}_ncu_top.txt", "dram_bytes_per_launch": traffic},
+            pipes[k] = {n: round(v, 1) for n, v in d["pipes"].items() if v is not None}
+            f.write("   utilisation %: " + ", ".join(f"{n} {v}" for n, v in pipes[k].items()) + "\n")
+    json.dump({"source": f"profiles/{tag}_ncu_top.txt", "dram_bytes_per_launch": traffic,
+               "utilisation_pct": pipes},
               open(os.path.join(dst, "ncu_traffic.json"), "w"), indent=1)
     print(open(os.path.join(dst, f"{tag}_kernel_shares.txt")).read())
     print(open(os.path.join(dst, f"{tag}_ncu_top.txt")).read())
