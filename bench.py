@@ -116,7 +116,8 @@ def algorithmic_bytes(c, n_points):
         "k_integrate_hash": 12 * n_points + 8 * n_points,
         "k_integrate_fold": 64 * touched + 12 * n_points,      # cell RMW + points
         "k_recenter": 3 * C_BITS + 32 * dropped,
-        "k_bitmap_compact": C_BITS + 4 * V,
+        "k_bitmap_count": C_BITS,
+        "k_bitmap_emit": C_BITS + 4 * V,
         "k_normals": 32 * V + 4 * V + 72 * V,                  # cells, list in, estimate out
         "k_ccl_hook": 56 * S,
         "k_ccl_compress": 8 * S,
@@ -516,7 +517,7 @@ def run_slabs(args, rank, world, dist):
     own_bits = (hi - lo) * ext[1] * ext[2] / 8
     alg = {"k_clear_walk": 12 * n + cleared / 8, "k_clear_apply": 2 * own_bits + 32 * freed,
            "k_integrate_fold": 64 * touched + 12 * n, "k_integrate_hash": 20 * n,
-           "k_bitmap_compact": own_bits + 4 * V, "k_normals": 108 * V,
+           "k_bitmap_count": own_bits, "k_bitmap_emit": own_bits + 4 * V, "k_normals": 108 * V,
            "k_ccl_hook": 56 * S_, "k_ccl_union": 56 * S_, "k_ccl_compress": 8 * S_, "k_ccl_flatten": 12 * S_,
            "k_map_fill": 16 * S_, "k_ransac_count": 24 * padded, "k_extract_count": 24 * padded,
            "k_refine": 48 * inl, "k_poly_hull": 64 * poolv}

@@ -987,34 +987,25 @@ __global__ void k_frame_begin(Counters* ctr, const unsigned long long* occ_total
 
 // ---------------------------------------------------------------------------
 // occupied_voxels (voxel_grid.cpp:254-263): ordered compaction of the logical
-// bitmap (x, y, z lexicographic) into logical flat indices, 256 threads x 8
-// words per tile, in one pass (count, decoupled look-back, emit): the grid
-// readers of a pipelined frame are on the critical path, so there is no
-// separate block-sum scan and the bitmap is read once.
+// bitmap (x, y, z lexicographic) into logical flat indices.
+// 256 threads x 8 words per block.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t tile_exclusive(const ScanTiles& st, uint32_t tile, uint32_t epoch,
-                                                   uint32_t c, uint32_t* agg_out) {
-  __shared__ uint32_t s_prefix, s_agg;
-  const uint32_t ex = block_exclusive_u32(c);
-  if (threadIdx.x == blockDim.x - 1) s_agg = ex + c;
-  __syncthreads();
-  const uint32_t agg = s_agg;
-  if (threadIdx.x < 32) {
-    const uint32_t pre = tile_prefix(st, tile, epoch, agg);
-    if (threadIdx.x == 0) s_prefix = pre;
-  }
-  __syncthreads();
-  *agg_out = agg;
-  return s_prefix + ex;
+__global__ void k_bitmap_count(const FrameParams* __restrict__ fp, uint64_t w_lo, uint64_t nwords,
+                               uint32_t* bsum) {
+  const uint32_t* __restrict__ bits = fp->occ_post + w_lo;
+  const uint64_t w0 = (static_cast<uint64_t>(blockIdx.x) * kScanThreads + threadIdx.x) * kScanItems;
+  uint32_t c = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k)
+    if (w0 + k < nwords) c += __popc(bits[w0 + k]);
+  c = block_sum_u32(c);
+  if (threadIdx.x == 0) bsum[blockIdx.x] = c;
 }
 
-__global__ void __launch_bounds__(kScanThreads) k_bitmap_compact(const FrameParams* __restrict__ fp, uint64_t w_lo,
-                                                                 uint64_t nwords, int W, int ez, ScanTiles st,
-                                                                 uint32_t* out, uint32_t cap, uint32_t* total) {
-  uint32_t tile, epoch;
-  tile_claim(st, tile, epoch);
+__global__ void k_bitmap_emit(const FrameParams* __restrict__ fp, uint64_t w_lo, uint64_t nwords, int W,
+                              int ez, const uint32_t* boff, uint32_t* out, uint32_t cap) {
   const uint32_t* __restrict__ bits = fp->occ_post + w_lo;
-  const uint64_t w0 = (static_cast<uint64_t>(tile) * kScanThreads + threadIdx.x) * kScanItems;
+  const uint64_t w0 = (static_cast<uint64_t>(blockIdx.x) * kScanThreads + threadIdx.x) * kScanItems;
   uint32_t v[kScanItems];
   uint32_t c = 0;
 #pragma unroll
@@ -1022,9 +1013,7 @@ __global__ void __launch_bounds__(kScanThreads) k_bitmap_compact(const FramePara
     v[k] = (w0 + k < nwords) ? bits[w0 + k] : 0u;
     c += __popc(v[k]);
   }
-  uint32_t agg;
-  uint32_t pos = tile_exclusive(st, tile, epoch, c, &agg);
-  if (tile == st.nb - 1 && threadIdx.x == blockDim.x - 1) *total = pos + c;
+  uint32_t pos = boff[blockIdx.x] + block_exclusive_u32(c);
 #pragma unroll
   for (int k = 0; k < kScanItems; ++k) {
     uint32_t b = v[k];
@@ -1039,31 +1028,6 @@ __global__ void __launch_bounds__(kScanThreads) k_bitmap_compact(const FramePara
       ++pos;
     }
   }
-}
-
-__global__ void __launch_bounds__(kScanThreads) k_flags_compact(const uint8_t* __restrict__ flags,
-                                                                const uint32_t* n_ptr, uint32_t cap, ScanTiles st,
-                                                                uint32_t* pos_out, uint32_t* total) {
-  uint32_t tile, epoch;
-  tile_claim(st, tile, epoch);
-  const uint32_t n = min(*n_ptr, cap);
-  const uint64_t i0 = (static_cast<uint64_t>(tile) * kScanThreads + threadIdx.x) * kScanItems;
-  uint8_t f[kScanItems];
-  uint32_t c = 0;
-#pragma unroll
-  for (int k = 0; k < kScanItems; ++k) {
-    f[k] = (i0 + k < n) ? flags[i0 + k] : 0;
-    c += f[k] ? 1u : 0u;
-  }
-  uint32_t agg;
-  uint32_t pos = tile_exclusive(st, tile, epoch, c, &agg);
-  if (tile == st.nb - 1 && threadIdx.x == blockDim.x - 1) *total = pos + c;
-#pragma unroll
-  for (int k = 0; k < kScanItems; ++k)
-    if (i0 + k < n) {
-      pos_out[i0 + k] = pos;
-      pos += f[k] ? 1u : 0u;
-    }
 }
 
 // Generic ordered compaction of u8 flags: positions[i] = exclusive rank.

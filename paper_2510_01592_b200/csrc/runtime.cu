@@ -32,7 +32,6 @@ thread_local std::string g_err;
 int g_ccl_mode = 0;
 // VP_WALK_GENERIC=1 (experiments): coherent rays through the generic walk loop
 const int g_walk_generic = std::getenv("VP_WALK_GENERIC") ? 1 : 0;
-const int g_compress_blocks = std::getenv("VP_COMPRESS_BLOCKS") ? std::atoi(std::getenv("VP_COMPRESS_BLOCKS")) : 148 * 8;
 std::atomic<uint64_t> g_launches{0};
 
 constexpr double kRadToDeg = 57.295779513082320876798;
@@ -203,9 +202,6 @@ struct Seg {
   SegBufs b{};
   uint32_t* bsum = nullptr;  // scan block sums
   uint32_t bsum_cap = 0;
-  // single-pass compactions (occupied list, steppable flags): tile words for
-  // two scans, then their two tickets
-  unsigned long long* tiles = nullptr;
   double* dirtab = nullptr;
   int dir_n = -1;
   uint32_t hstride = 0;
@@ -218,26 +214,17 @@ struct Seg {
                     b.fid, b.fit_cluster, b.ioff, b.fch_off, b.ccount, b.fit_model, b.fit_meta, b.ref_model, b.inl,
                     b.rch_off, b.rpart, b.rcen,
                     b.proj, b.surv, b.hull, b.basis, b.pch_off, b.pext_dot, b.pext_idx, b.inner,
-                    b.ninner, b.nsurv, b.prec_d, b.prec_i, b.pool, bsum, tiles, dirtab};
+                    b.ninner, b.nsurv, b.prec_d, b.prec_i, b.pool, bsum, dirtab};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     b = SegBufs{};
     bsum = nullptr;
-    tiles = nullptr;
     dirtab = nullptr;
     dir_n = -1;
   }
   void alloc_bsum(uint64_t need_bsum) {
     bsum_cap = static_cast<uint32_t>(need_bsum);
     bsum = dalloc<uint32_t>(2ull * need_bsum);
-    tiles = dalloc<unsigned long long>(2ull * need_bsum + 2);
-    ck(cudaMemset(tiles, 0, (2ull * need_bsum + 2) * sizeof(unsigned long long)), "tiles");
-  }
-  ScanTiles occ_tiles(uint64_t nwords) const {
-    return {tiles, tiles + 2ull * bsum_cap, static_cast<uint32_t>((nwords + kScanPerBlock - 1) / kScanPerBlock)};
-  }
-  ScanTiles step_tiles() const {
-    return {tiles + bsum_cap, tiles + 2ull * bsum_cap + 1, (b.Vcap + kScanPerBlock - 1) / kScanPerBlock};
   }
 
   void ensure(uint32_t vcap, uint32_t scap, uint32_t icap, int iterations, uint64_t nwords) {
@@ -317,7 +304,6 @@ struct Seg {
     } else if (need_bsum > bsum_cap) {
       ++gen;
       dfree(bsum);
-      dfree(tiles);
       alloc_bsum(need_bsum);
     }
   }
@@ -890,9 +876,10 @@ struct vp_grid {
     const uint32_t nb = static_cast<uint32_t>((gd.nwords + kScanPerBlock - 1) / kScanPerBlock);
     const uint64_t w_lo = static_cast<uint64_t>(gd.own_lo) * gd.ey * gd.W;
     const uint64_t w_n = static_cast<uint64_t>(gd.own_hi - gd.own_lo) * gd.ey * gd.W;
-    const ScanTiles st = seg.occ_tiles(gd.nwords);  // st.nb == nb
-    LAUNCH(k_bitmap_compact, nb, kScanThreads, 0, stream, d_fp, w_lo, w_n, gd.W, gd.ez, st, seg.b.occ_list,
-           seg.b.Vcap, &ctr->V);
+    LAUNCH(k_bitmap_count, nb, kScanThreads, 0, stream, d_fp, w_lo, w_n, seg.bsum);
+    LAUNCH(k_scan_exclusive, 1, 1024, 0, stream, seg.bsum, nb, nullptr, &ctr->V, nullptr);
+    LAUNCH(k_bitmap_emit, nb, kScanThreads, 0, stream, d_fp, w_lo, w_n, gd.W, gd.ez, seg.bsum,
+           seg.b.occ_list, seg.b.Vcap);
   }
 
   // flags[0..*n) -> positions, total into *total
@@ -920,9 +907,7 @@ struct vp_grid {
   // normals + classify + steppable list (+ ordinal map)
   void launch_classify(const SegDev& sd, int write_status) {
     LAUNCH(k_normals, kWide, kThreads, 0, stream, gd, d_fp, ctr, sd, seg.b, write_status);
-    const ScanTiles st = seg.step_tiles();
-    LAUNCH(k_flags_compact, st.nb, kScanThreads, 0, stream, seg.b.step_flag, &ctr->V, seg.b.Vcap, st,
-           seg.b.step_pos, &ctr->S);
+    launch_flag_scan(seg.b.step_flag, &ctr->V, seg.b.Vcap, seg.b.step_pos, &ctr->S);
   }
   void launch_step_emit(const MapDesc& m, int xadd = 0) {
     LAUNCH(k_step_emit, kWide, kThreads, 0, stream, gd, ctr, seg.b, m, xadd);
@@ -934,7 +919,7 @@ struct vp_grid {
       // ECL-style atomic-free pre-hooking + compression: most unions then end at
       // the one-load parent check (C2: union pass 400 us -> 80 us)
       LAUNCH(k_ccl_hook, kWide, kThreads, 0, stream, ctr, sd, sb, m);
-      LAUNCH(k_ccl_compress, g_compress_blocks, kThreads, 0, stream, ctr, sb);
+      LAUNCH(k_ccl_compress, kWide, kThreads, 0, stream, ctr, sb);
       LAUNCH(k_ccl_union, kWide, kThreads, 0, stream, ctr, sd, sb, m);
     } else {
       // sampling variants (measured slower on C2 and C5):
@@ -946,7 +931,7 @@ struct vp_grid {
       } else {
         LAUNCH(k_ccl_hook, kWide, kThreads, 0, stream, ctr, sd, sb, m);
       }
-      LAUNCH(k_ccl_compress, g_compress_blocks, kThreads, 0, stream, ctr, sb);
+      LAUNCH(k_ccl_compress, kWide, kThreads, 0, stream, ctr, sb);
       LAUNCH(k_ccl_giant, 1, 1024, 0, stream, ctr, sb);
       LAUNCH(k_ccl_full, kWide, kThreads, 0, stream, ctr, sd, sb, m);
     }

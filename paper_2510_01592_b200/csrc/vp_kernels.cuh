@@ -70,63 +70,6 @@ __device__ __forceinline__ uint32_t block_sum_u32(uint32_t v) {
   return r;
 }
 
-// Single-pass ordered compaction (decoupled look-back): a block takes the
-// next tile in launch order from a ticket counter, publishes its aggregate,
-// and one warp sums its predecessors' published values until it meets an
-// inclusive prefix. Tile words pack [epoch:30 | status:2 | value:32]
-// (status 1 = aggregate, 2 = inclusive); the epoch (ticket / nb + 1) tells a
-// word of this launch from a stale one, so the state is never reset. The
-// ticket counter advances by exactly nb per launch (one launch at a time per
-// ScanTiles, stream order).
-struct ScanTiles {
-  unsigned long long* state;   // nb words, zero-initialised once
-  unsigned long long* ticket;  // persistent launch-order counter
-  uint32_t nb;
-};
-
-// Thread 0 claims the block's tile; every thread gets (tile, epoch).
-__device__ __forceinline__ void tile_claim(const ScanTiles& st, uint32_t& tile, uint32_t& epoch) {
-  __shared__ uint32_t s_t, s_e;
-  if (threadIdx.x == 0) {
-    const unsigned long long t = atomicAdd(st.ticket, 1ull);
-    s_t = static_cast<uint32_t>(t % st.nb);
-    s_e = static_cast<uint32_t>((t / st.nb + 1ull) & 0x3fffffffull);
-  }
-  __syncthreads();
-  tile = s_t;
-  epoch = s_e;
-}
-
-// Called by all 32 lanes of one warp with the tile's aggregate: returns the
-// exclusive prefix of the tile and publishes its inclusive prefix.
-__device__ __forceinline__ uint32_t tile_prefix(const ScanTiles& st, uint32_t tile, uint32_t epoch,
-                                                uint32_t agg) {
-  const unsigned lane = threadIdx.x & 31u;
-  volatile unsigned long long* s = st.state;
-  const unsigned long long E = static_cast<unsigned long long>(epoch) << 34;
-  if (tile == 0) {
-    if (lane == 0) s[0] = E | (2ull << 32) | agg;
-    return 0u;
-  }
-  if (lane == 0) s[tile] = E | (1ull << 32) | agg;
-  uint32_t excl = 0;
-  for (int p = static_cast<int>(tile) - 1;; p -= 32) {
-    const int q = p - static_cast<int>(lane);
-    unsigned long long v;
-    uint32_t status;
-    do {
-      v = q >= 0 ? s[q] : (E | (2ull << 32));  // before tile 0: an inclusive 0
-      status = (v >> 34) == epoch ? static_cast<uint32_t>(v >> 32) & 3u : 0u;
-    } while (__any_sync(0xffffffffu, status == 0u));
-    const unsigned incl = __ballot_sync(0xffffffffu, status == 2u);
-    const int k = incl ? __ffs(incl) - 1 : 31;  // nearest inclusive predecessor
-    excl += __reduce_add_sync(0xffffffffu, static_cast<int>(lane) <= k ? static_cast<uint32_t>(v) : 0u);
-    if (incl) break;
-  }
-  if (lane == 0) s[tile] = E | (2ull << 32) | (excl + agg);
-  return excl;
-}
-
 // Union-find over int32 parent arrays (CCL and the slab boundary merge).
 // Parent pointers only ever move to an ancestor (hooks: root -> smaller root;
 // pointer jumping: node -> grandparent), so every value a thread can observe
@@ -362,10 +305,9 @@ __global__ void k_flags_positions(const uint8_t* flags, const uint32_t* n_ptr, u
                                   const uint32_t* boff, uint32_t* pos_out);
 __global__ void k_merge_point(GridDesc g, const FrameParams* fp, Counters* ctr, int x, int y, int z,
                               double px, double py, double pz);
-__global__ void k_bitmap_compact(const FrameParams* fp, uint64_t w_lo, uint64_t nwords, int W, int ez,
-                                 ScanTiles st, uint32_t* out, uint32_t cap, uint32_t* total);
-__global__ void k_flags_compact(const uint8_t* flags, const uint32_t* n_ptr, uint32_t cap, ScanTiles st,
-                                uint32_t* pos_out, uint32_t* total);
+__global__ void k_bitmap_count(const FrameParams* fp, uint64_t w_lo, uint64_t nwords, uint32_t* bsum);
+__global__ void k_bitmap_emit(const FrameParams* fp, uint64_t w_lo, uint64_t nwords, int W, int ez,
+                              const uint32_t* boff, uint32_t* out, uint32_t cap);
 __global__ void k_scan_exclusive(uint32_t* a, uint32_t n_static, const uint32_t* n_ptr,
                                  uint32_t* total, uint32_t* total2);
 
