@@ -248,7 +248,13 @@ __global__ void __launch_bounds__(256) k_ccl_hook(Counters* ctr, SegDev sp, SegB
     const d3 ni = mk3(__ldg(b.st_normal + 3 * i), __ldg(b.st_normal + 3 * i + 1),
                       __ldg(b.st_normal + 3 * i + 2));
     int best = static_cast<int>(i);
-    for (int r = static_cast<int>(lane); r < nrows; r += 32) {
+    // rows from the back of the window (dx = -w first): ordinals decrease
+    // with r, so once a batch of 32 rows holds an adjacent voxel, no later
+    // batch can hold a smaller one
+    for (int r0 = nrows - 1; r0 >= 0; r0 -= 32) {
+      if (__any_sync(0xffffffffu, best < static_cast<int>(i))) break;
+      const int r = r0 - static_cast<int>(lane);
+      if (r < 0) continue;
       int dx, dy;
       window_row(r, w, span, true, dx, dy);
       const int X = x + dx, Y = y + dy;
