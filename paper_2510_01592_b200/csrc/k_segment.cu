@@ -326,7 +326,9 @@ __global__ void __launch_bounds__(256) k_ccl_union(Counters* ctr, SegDev sp, Seg
       while (bits) {
         bits &= bits - 1;
         ++j;
-        const int pj = __ldcg(parent + j);
+        // L1-cached early-out: a stale parent[j] is an earlier ancestor of j;
+        // if it equals ri, i and j were already in one set (sets only merge)
+        const int pj = __ldca(parent + j);
         if (pj == ri) continue;  // already in i's tree
         if (!adjacent(b, sp, mi, ni, j)) continue;
         const int rj = uf_find(parent, j);
