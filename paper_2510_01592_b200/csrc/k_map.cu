@@ -1071,14 +1071,27 @@ __global__ void k_scan_exclusive(uint32_t* a, uint32_t n_static, const uint32_t*
   __shared__ uint32_t carry;
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
-  for (uint32_t b = 0; b < n; b += blockDim.x) {
-    const uint32_t i = b + threadIdx.x;
-    const uint32_t v = i < n ? a[i] : 0u;
-    const uint32_t ex = block_exclusive_u32(v);
-    const uint32_t c = carry;
-    if (i < n) a[i] = c + ex;
+  // kScanItems consecutive values per thread: one block pass per 8 K values
+  const uint32_t per = blockDim.x * kScanItems;
+  for (uint32_t b = 0; b < n; b += per) {
+    const uint32_t i0 = b + threadIdx.x * kScanItems;
+    uint32_t v[kScanItems];
+    uint32_t sum = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+      v[k] = i0 + k < n ? a[i0 + k] : 0u;
+      sum += v[k];
+    }
+    const uint32_t ex = block_exclusive_u32(sum);
+    uint32_t run = carry + ex;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k)
+      if (i0 + k < n) {
+        a[i0 + k] = run;
+        run += v[k];
+      }
     __syncthreads();
-    if (threadIdx.x == blockDim.x - 1) carry = c + ex + v;
+    if (threadIdx.x == blockDim.x - 1) carry = run;
     __syncthreads();
   }
   if (threadIdx.x == 0) {
