@@ -781,14 +781,98 @@ __device__ __forceinline__ void clear_walk_coherent(const GridDesc& g, const Fra
   }
 }
 
+// Incoherent rays on a plain grid (LiDAR patterns; rays listed longest
+// first by k_dda_scatter): the same branch-free step as the coherent walk,
+// per lane (no cross-lane work), and clear_walk_body's brick accumulation --
+// a ray ORs the bits of the 4x4x4 brick it is in and issues one RED when it
+// leaves it, into shared memory for the 3x3x3 bricks around the sensor.
+__device__ __forceinline__ void clear_walk_bricks(const GridDesc& g, const FrameParams* __restrict__ fp,
+                                                  const uint32_t* __restrict__ perm) {
+  const uint64_t n = fp->n;
+  const DdaWin wn = dda_window(g, fp);
+  unsigned long long* __restrict__ clrb = g.clrb;
+  const uint32_t ex0 = static_cast<uint32_t>(g.gex), ex1 = static_cast<uint32_t>(g.ey),
+                 ex2 = static_cast<uint32_t>(g.ez);
+  constexpr int kNearR = 1, kNear = 2 * kNearR + 1, kNear3 = kNear * kNear * kNear;
+  __shared__ unsigned long long near_m[kNear3];
+  for (int k = threadIdx.x; k < kNear3; k += blockDim.x) near_m[k] = 0;
+  __syncthreads();
+  const int sbx = wn.oc0 >> 2, sby = wn.oc1 >> 2, sbz = wn.oc2 >> 2;
+  for (uint64_t r = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < n;
+       r += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    DdaRay ry;
+    if (!dda_setup(wn, fp, perm[r], g, ry)) continue;
+    int c0 = ry.c0, c1 = ry.c1, c2 = ry.c2;
+    const int s0 = ry.s0, s1 = ry.s1, s2 = ry.s2;
+    double tm0 = ry.tm0, tm1 = ry.tm1, tm2 = ry.tm2;
+    const double td0 = ry.td0, td1 = ry.td1, td2 = ry.td2, t1 = ry.t1;
+    const uint32_t key_e =
+        (static_cast<unsigned>(ry.ec0) < ex0 && static_cast<unsigned>(ry.ec1) < ex1 &&
+         static_cast<unsigned>(ry.ec2) < ex2)
+            ? ((brick_word(g, ry.ec0, ry.ec1, ry.ec2) << 6) | brick_bit(ry.ec0, ry.ec1, ry.ec2))
+            : kNoMark;
+    uint32_t aw = kNoMark;  // the brick the ray is in, its marks (flushed when it leaves)
+    unsigned long long ab = 0;
+    int anear = -1;  // its index among the sensor's near bricks, or -1
+    auto visit = [&] {
+      const uint32_t w = brick_word(g, c0, c1, c2);
+      const uint32_t bit = brick_bit(c0, c1, c2);
+      if (((w << 6) | bit) == key_e) return;
+      if (w != aw) {
+        if (ab) {
+          if (anear >= 0) atomicOr(&near_m[anear], ab); else atomicOr(clrb + aw, ab);
+        }
+        aw = w;
+        ab = 0;
+        const int dbx = (c0 >> 2) - sbx, dby = (c1 >> 2) - sby, dbz = (c2 >> 2) - sbz;
+        anear = (dbx >= -kNearR && dbx <= kNearR && dby >= -kNearR && dby <= kNearR && dbz >= -kNearR &&
+                 dbz <= kNearR)
+                    ? ((dbx + kNearR) * kNear + (dby + kNearR)) * kNear + (dbz + kNearR)
+                    : -1;
+      }
+      ab |= 1ull << bit;
+    };
+    if (!(c0 == wn.oc0 && c1 == wn.oc1 && c2 == wn.oc2)) visit();  // origin cell: first cell only
+    for (;;) {
+      // m = argmin t_max, ties to the lower axis (voxel_grid.cpp:170-172)
+      const bool m1 = tm1 < tm0;
+      const double tm01 = m1 ? tm1 : tm0;
+      const bool m2 = tm2 < tm01;
+      const double tm = m2 ? tm2 : tm01;
+      const bool x0 = !m1 && !m2, x1 = m1 && !m2;
+      c0 += x0 ? s0 : 0;
+      c1 += x1 ? s1 : 0;
+      c2 += m2 ? s2 : 0;
+      if (tm >= t1 || static_cast<unsigned>(c0) >= ex0 || static_cast<unsigned>(c1) >= ex1 ||
+          static_cast<unsigned>(c2) >= ex2)
+        break;
+      const double tn = tm + (m2 ? td2 : (m1 ? td1 : td0));  // t_max[m] += t_delta[m]
+      tm0 = x0 ? tn : tm0;
+      tm1 = x1 ? tn : tm1;
+      tm2 = m2 ? tn : tm2;
+      visit();
+    }
+    if (ab) {
+      if (anear >= 0) atomicOr(&near_m[anear], ab); else atomicOr(clrb + aw, ab);
+    }
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < kNear3; k += blockDim.x)
+    if (near_m[k]) {
+      const int bx = sbx + k / (kNear * kNear) - kNearR, by = sby + (k / kNear) % kNear - kNearR,
+                bz = sbz + k % kNear - kNearR;
+      atomicOr(clrb + (static_cast<uint32_t>(bx) * g.bny + by) * g.bnz + bz, near_m[k]);
+    }
+}
+
 #ifndef VP_DDA_MINB
 #define VP_DDA_MINB 4
 #endif
 __global__ void __launch_bounds__(256, VP_DDA_MINB) k_clear_walk(GridDesc g, const FrameParams* __restrict__ fp,
                                                                   const uint32_t* perm, const DdaBins* db,
                                                                   int generic) {
-  if (!db->use && !generic) {
-    clear_walk_coherent(g, fp);
+  if (!generic) {
+    if (db->use) clear_walk_bricks(g, fp, perm); else clear_walk_coherent(g, fp);
     return;
   }
   clear_walk_body<false>(g, fp, perm, db);

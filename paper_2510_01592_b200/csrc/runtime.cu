@@ -30,7 +30,7 @@ thread_local std::string g_err;
 // CCL variant: 0 = min-neighbour hook + forward-window unions (default),
 // 1 = neighbour sampling + giant skip, 2 = hook + giant skip (same labels)
 int g_ccl_mode = 0;
-// VP_WALK_GENERIC=1 (experiments): coherent rays through the generic walk loop
+// VP_WALK_GENERIC=1 (experiments): plain-grid rays through the generic walk loop
 const int g_walk_generic = std::getenv("VP_WALK_GENERIC") ? 1 : 0;
 std::atomic<uint64_t> g_launches{0};
 
