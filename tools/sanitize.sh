@@ -14,6 +14,9 @@ ge.smoke()
 w = scenes.workload("c2", frames=4)
 pl = native.Pipeline(w.resolution, (300, 300, 300), w.frames[0].translation, native.default_params(seed=w.seed))
 pl.run(w.frames)
+w4 = scenes.workload("c4", frames=2)  # incoherent rays: the brick-mask walk
+pl4 = native.Pipeline(w4.resolution, (300, 300, 200), w4.frames[0].translation, native.default_params(seed=w4.seed))
+pl4.run(w4.frames)
 ss = [slabs.Slab(0.01, (300, 200, 150), (0.0, 0.0, 0.5), a, b) for a, b in [(0, 100), (100, 103), (103, 300)]]
 comm = slabs.LocalComm(3)
 for f in scenes.stair_frames(3):
