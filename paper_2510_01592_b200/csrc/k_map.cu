@@ -752,31 +752,54 @@ __device__ __forceinline__ void clear_walk_coherent(const GridDesc& g, const Fra
     }
     // (a ray never exceeds max_steps here: each step moves one axis
     // monotonically, so it leaves the window after gex + ey + ez steps)
+    uint32_t live_i = live ? 1u : 0u;
     for (;;) {
       // visit: a lane in the same cell as its left neighbour skips the RED
       const uint32_t prev = __shfl_up_sync(0xffffffffu, key, 1);
       if (key != kNoMark && (key != prev || lane == 0)) atomicOr(clr + (key >> 5), 1u << (key & 31u));
       if (!__any_sync(0xffffffffu, live)) break;
       // one DDA step, branch-free (an ended lane steps too; its state is
-      // garbage from then on and only `live` / `key` are read):
-      // m = argmin t_max, ties to the lower axis (voxel_grid.cpp:170-172);
-      // min t_max >= t1 is "every t_max >= t1" (no min materialised)
-      const bool m1 = tm1 < tm0;
-      const bool m2 = m1 ? (tm2 < tm1) : (tm2 < tm0);
-      const bool x0 = !m1 && !m2, x1 = m1 && !m2;
-      const bool done = tm0 >= t1 && tm1 >= t1 && tm2 >= t1;
-      if (x0) c0 += s0;
-      if (x1) c1 += s1;
-      if (m2) c2 += s2;
-      if (x0) krow += static_cast<uint32_t>(dxr);
-      if (x1) krow += static_cast<uint32_t>(dyr);
-      if (x0) tm0 += td0;  // t_max[m] += t_delta[m]
-      if (x1) tm1 += td1;
-      if (m2) tm2 += td2;
-      live = live && !done && static_cast<unsigned>(c0) < ex0 && static_cast<unsigned>(c1) < ex1 &&
-             static_cast<unsigned>(c2) < ex2;
-      const uint32_t k = krow + static_cast<uint32_t>(c2);
-      key = (live && k != key_e) ? k : kNoMark;
+      // garbage from then on and only `live` / `key` are read), written in
+      // PTX so the stepped axis is advanced by predicated adds instead of
+      // selects (the walk is ALU-pipe bound):
+      //   m = argmin t_max, ties to the lower axis (voxel_grid.cpp:170-172):
+      //   m1 = tm1 < tm0, m2 = tm2 < min(tm0, tm1), axis 0 iff !(m1 | m2)
+      //   stop when min t_max >= t1, or the stepped cell leaves the window
+      //   t_max[m] += t_delta[m]; row key += the stepped axis' stride
+      asm("{\n\t"
+          ".reg .pred m1, m2, a, x1, d, ok, lv;\n\t"
+          ".reg .f64 t01;\n\t"
+          ".reg .u32 k;\n\t"
+          "setp.ne.u32 lv, %5, 0;\n\t"
+          "setp.lt.f64 m1, %7, %6;\n\t"
+          "selp.f64 t01, %7, %6, m1;\n\t"
+          "setp.lt.f64 m2, %8, t01;\n\t"
+          "setp.ge.f64 d, t01, %14;\n\t"
+          "setp.ge.and.f64 d, %8, %14, d;\n\t"
+          "or.pred a, m1, m2;\n\t"
+          "and.pred x1, m1, !m2;\n\t"
+          "@!a add.s32 %0, %0, %9;\n\t"
+          "@!a add.s32 %3, %3, %12;\n\t"
+          "@!a add.rn.f64 %6, %6, %15;\n\t"
+          "@x1 add.s32 %1, %1, %10;\n\t"
+          "@x1 add.s32 %3, %3, %13;\n\t"
+          "@x1 add.rn.f64 %7, %7, %16;\n\t"
+          "@m2 add.s32 %2, %2, %11;\n\t"
+          "@m2 add.rn.f64 %8, %8, %17;\n\t"
+          "setp.lt.u32 ok, %0, %18;\n\t"
+          "setp.lt.and.u32 ok, %1, %19, ok;\n\t"
+          "setp.lt.and.u32 ok, %2, %20, ok;\n\t"
+          "and.pred ok, ok, !d;\n\t"
+          "and.pred ok, ok, lv;\n\t"
+          "add.u32 k, %3, %2;\n\t"
+          "setp.ne.and.u32 lv, k, %21, ok;\n\t"
+          "selp.u32 %4, k, 0xffffffff, lv;\n\t"
+          "selp.u32 %5, 1, 0, ok;\n\t"
+          "}"
+          : "+r"(c0), "+r"(c1), "+r"(c2), "+r"(krow), "=r"(key), "+r"(live_i), "+d"(tm0), "+d"(tm1), "+d"(tm2)
+          : "r"(s0), "r"(s1), "r"(s2), "r"(dxr), "r"(dyr), "d"(t1), "d"(td0), "d"(td1), "d"(td2), "r"(ex0),
+            "r"(ex1), "r"(ex2), "r"(key_e));
+      live = live_i != 0;
     }
   }
 }
