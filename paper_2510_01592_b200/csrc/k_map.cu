@@ -804,11 +804,16 @@ __device__ __forceinline__ void clear_walk_coherent(const GridDesc& g, const Fra
   }
 }
 
-// Incoherent rays on a plain grid (LiDAR patterns; rays listed longest
-// first by k_dda_scatter): the same branch-free step as the coherent walk,
-// per lane (no cross-lane work), and clear_walk_body's brick accumulation --
-// a ray ORs the bits of the 4x4x4 brick it is in and issues one RED when it
-// leaves it, into shared memory for the 3x3x3 bricks around the sensor.
+// Incoherent rays (LiDAR patterns; rays listed longest first by
+// k_dda_scatter): a branch-free step per lane (no cross-lane work) and
+// clear_walk_body's brick accumulation -- a ray ORs the bits of the 4x4x4
+// brick it is in and issues one RED when it leaves it, into shared memory
+// for the 3x3x3 bricks around the sensor. kSlab: the grid stores window x
+// [xoff, xoff + ex) and owns [xoff + own_lo, xoff + own_hi); rays are walked
+// in window coordinates from their start (a slab clip would drift in the
+// last bit), marked only inside the owned range, and dropped once they left
+// it in their x direction (the DDA is monotone per axis).
+template <bool kSlab>
 __device__ __forceinline__ void clear_walk_bricks(const GridDesc& g, const FrameParams* __restrict__ fp,
                                                   const uint32_t* __restrict__ perm) {
   const uint64_t n = fp->n;
@@ -816,11 +821,13 @@ __device__ __forceinline__ void clear_walk_bricks(const GridDesc& g, const Frame
   unsigned long long* __restrict__ clrb = g.clrb;
   const uint32_t ex0 = static_cast<uint32_t>(g.gex), ex1 = static_cast<uint32_t>(g.ey),
                  ex2 = static_cast<uint32_t>(g.ez);
+  const int xoff = kSlab ? g.xoff : 0;
+  const int own0 = kSlab ? g.xoff + g.own_lo : 0, own1 = kSlab ? g.xoff + g.own_hi : g.gex;
   constexpr int kNearR = 1, kNear = 2 * kNearR + 1, kNear3 = kNear * kNear * kNear;
   __shared__ unsigned long long near_m[kNear3];
   for (int k = threadIdx.x; k < kNear3; k += blockDim.x) near_m[k] = 0;
   __syncthreads();
-  const int sbx = wn.oc0 >> 2, sby = wn.oc1 >> 2, sbz = wn.oc2 >> 2;
+  const int sbx = (wn.oc0 - xoff) >> 2, sby = wn.oc1 >> 2, sbz = wn.oc2 >> 2;
   for (uint64_t r = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < n;
        r += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     DdaRay ry;
@@ -829,17 +836,20 @@ __device__ __forceinline__ void clear_walk_bricks(const GridDesc& g, const Frame
     const int s0 = ry.s0, s1 = ry.s1, s2 = ry.s2;
     double tm0 = ry.tm0, tm1 = ry.tm1, tm2 = ry.tm2;
     const double td0 = ry.td0, td1 = ry.td1, td2 = ry.td2, t1 = ry.t1;
+    // the end cell's key, when it is stored (and owned) here
     const uint32_t key_e =
-        (static_cast<unsigned>(ry.ec0) < ex0 && static_cast<unsigned>(ry.ec1) < ex1 &&
+        (ry.ec0 >= own0 && ry.ec0 < own1 && static_cast<unsigned>(ry.ec1) < ex1 &&
          static_cast<unsigned>(ry.ec2) < ex2)
-            ? ((brick_word(g, ry.ec0, ry.ec1, ry.ec2) << 6) | brick_bit(ry.ec0, ry.ec1, ry.ec2))
+            ? ((brick_word(g, ry.ec0 - xoff, ry.ec1, ry.ec2) << 6) | brick_bit(ry.ec0 - xoff, ry.ec1, ry.ec2))
             : kNoMark;
     uint32_t aw = kNoMark;  // the brick the ray is in, its marks (flushed when it leaves)
     unsigned long long ab = 0;
     int anear = -1;  // its index among the sensor's near bricks, or -1
     auto visit = [&] {
-      const uint32_t w = brick_word(g, c0, c1, c2);
-      const uint32_t bit = brick_bit(c0, c1, c2);
+      if (kSlab && (c0 < own0 || c0 >= own1)) return;  // not stored here
+      const int lx = c0 - xoff;
+      const uint32_t w = brick_word(g, lx, c1, c2);
+      const uint32_t bit = brick_bit(lx, c1, c2);
       if (((w << 6) | bit) == key_e) return;
       if (w != aw) {
         if (ab) {
@@ -847,7 +857,7 @@ __device__ __forceinline__ void clear_walk_bricks(const GridDesc& g, const Frame
         }
         aw = w;
         ab = 0;
-        const int dbx = (c0 >> 2) - sbx, dby = (c1 >> 2) - sby, dbz = (c2 >> 2) - sbz;
+        const int dbx = (lx >> 2) - sbx, dby = (c1 >> 2) - sby, dbz = (c2 >> 2) - sbz;
         anear = (dbx >= -kNearR && dbx <= kNearR && dby >= -kNearR && dby <= kNearR && dbz >= -kNearR &&
                  dbz <= kNearR)
                     ? ((dbx + kNearR) * kNear + (dby + kNearR)) * kNear + (dbz + kNearR)
@@ -855,6 +865,9 @@ __device__ __forceinline__ void clear_walk_bricks(const GridDesc& g, const Frame
       }
       ab |= 1ull << bit;
     };
+    // a slab skips rays that never reach its owned x-range
+    if (kSlab && ((s0 > 0 && c0 >= own1) || (s0 < 0 && c0 < own0) || (s0 == 0 && (c0 < own0 || c0 >= own1))))
+      continue;
     if (!(c0 == wn.oc0 && c1 == wn.oc1 && c2 == wn.oc2)) visit();  // origin cell: first cell only
     for (;;) {
       // m = argmin t_max, ties to the lower axis (voxel_grid.cpp:170-172)
@@ -869,6 +882,9 @@ __device__ __forceinline__ void clear_walk_bricks(const GridDesc& g, const Frame
       if (tm >= t1 || static_cast<unsigned>(c0) >= ex0 || static_cast<unsigned>(c1) >= ex1 ||
           static_cast<unsigned>(c2) >= ex2)
         break;
+      // a slab never sees the ray again once it left the owned x-range in
+      // its stepping direction
+      if (kSlab && ((s0 > 0 && c0 >= own1) || (s0 < 0 && c0 < own0))) break;
       const double tn = tm + (m2 ? td2 : (m1 ? td1 : td0));  // t_max[m] += t_delta[m]
       tm0 = x0 ? tn : tm0;
       tm1 = x1 ? tn : tm1;
@@ -895,14 +911,14 @@ __global__ void __launch_bounds__(256, VP_DDA_MINB) k_clear_walk(GridDesc g, con
                                                                   const uint32_t* perm, const DdaBins* db,
                                                                   int generic) {
   if (!generic) {
-    if (db->use) clear_walk_bricks(g, fp, perm); else clear_walk_coherent(g, fp);
+    if (db->use) clear_walk_bricks<false>(g, fp, perm); else clear_walk_coherent(g, fp);
     return;
   }
   clear_walk_body<false>(g, fp, perm, db);
 }
 __global__ void __launch_bounds__(256, 4) k_clear_walk_slab(GridDesc g, const FrameParams* __restrict__ fp,
                                                             const uint32_t* perm, const DdaBins* db) {
-  clear_walk_body<true>(g, fp, perm, db);
+  if (db->use) clear_walk_bricks<true>(g, fp, perm); else clear_walk_body<true>(g, fp, perm, db);
 }
 
 __device__ __forceinline__ void zero_cell(Cell* c) {

@@ -181,6 +181,13 @@ def stair_frames(frames=25):
     return render(stock_scene(STAIR5), sensor, default_trajectory(STAIR5, frames, 20.0), 5)
 
 
+def lidar_stair_frames(frames=6, rays=200_000, seed=11):
+    """Stair5 seen by a spherical ray pattern along the Stair5 trajectory:
+    incoherent rays (the brick-mask walk) for tests."""
+    sensor = SensorSpec(kind=1, pattern=spherical_pattern(rays), max_range=4.0)
+    return render(stock_scene(STAIR5), sensor, default_trajectory(STAIR5, frames, 20.0), seed)
+
+
 def stepping_stones():
     """C2 scene: Stair5 plus six 0.3 x 0.3 m stepping stones (0.05-0.15 m) on the approach floor."""
     s = stock_scene(STAIR5)

@@ -67,7 +67,17 @@ def steppable_of_grid(g, params):
                                     [(0, 100), (100, 102), (102, 104), (104, 200), (200, 300)],
                                     [(a, a + 38) for a in range(0, 266, 38)] + [(266, 300)]])
 def test_virtual_slabs_equal_one_grid(ranges):
-    frames = scenes.stair_frames(10)
+    check_slabs(ranges, scenes.stair_frames(10))
+
+
+@pytest.mark.parametrize("ranges", [[(0, 150), (150, 300)], [(0, 100), (100, 102), (102, 104), (104, 200), (200, 300)]])
+def test_virtual_slabs_lidar(ranges):
+    """Incoherent rays: the slab walk's brick-mask path (owned-range marking,
+    rays dropped once they left the slab) against the one-grid walk."""
+    check_slabs(ranges, scenes.lidar_stair_frames(6))
+
+
+def check_slabs(ranges, frames):
     params = native.default_params(seed=5, refine_exact=True)
     g, ref_polys = one_grid(frames, params)
     ref_idx, ref_mean = steppable_of_grid(g, params)
