@@ -38,7 +38,10 @@ constexpr double kRadToDeg = 57.295779513082320876798;
 constexpr double kDegToRad = 0.017453292519943295769237;
 constexpr double kPi = 3.14159265358979323846;  // == glibc M_PI
 constexpr int kThreads = 256;
-constexpr int kSlots = 3;  // frames in flight in a pipelined run
+#ifndef VP_SLOTS
+#define VP_SLOTS 3
+#endif
+constexpr int kSlots = VP_SLOTS;  // frames in flight in a pipelined run
 
 struct VpFail {
   int code;
@@ -440,6 +443,10 @@ struct vp_grid {
   uint32_t* stbits_pool[kSlots] = {};
   int seg_slot = 0;
   cudaStream_t lstream = nullptr;   // stream the mapping launches go to (stream or mstream)
+  // grid width of the CCL .. polygon kernels: a pipelined run caps them at
+  // half an SM's warp slots (148 x 4 blocks of 256) so the next mapping and grid
+  // readers -- the critical path -- are not starved by latency-bound chains
+  int chain_wide = 148 * 8;
   // integrate scratch
   uint64_t pcap = 0;
   uint32_t* hkey = nullptr;
@@ -918,35 +925,35 @@ struct vp_grid {
     if (g_ccl_mode == 0) {
       // ECL-style atomic-free pre-hooking + compression: most unions then end at
       // the one-load parent check (C2: union pass 400 us -> 80 us)
-      LAUNCH(k_ccl_hook, kWide, kThreads, 0, stream, ctr, sd, sb, m);
-      LAUNCH(k_ccl_compress, kWide, kThreads, 0, stream, ctr, sb);
-      LAUNCH(k_ccl_union, kWide, kThreads, 0, stream, ctr, sd, sb, m);
+      LAUNCH(k_ccl_hook, chain_wide, kThreads, 0, stream, ctr, sd, sb, m);
+      LAUNCH(k_ccl_compress, chain_wide, kThreads, 0, stream, ctr, sb);
+      LAUNCH(k_ccl_union, chain_wide, kThreads, 0, stream, ctr, sd, sb, m);
     } else {
       // sampling variants (measured slower on C2 and C5):
       // 1 = neighbour-sampling unions, 2 = min-neighbour hooking; then
       // whole-window unions of the voxels outside the sampled giant tree
       if (g_ccl_mode == 1) {
-        LAUNCH(k_ccl_init, kWide, kThreads, 0, stream, ctr, sb);
-        LAUNCH(k_ccl_lattice, kWide, kThreads, 0, stream, ctr, sd, sb, m);
+        LAUNCH(k_ccl_init, chain_wide, kThreads, 0, stream, ctr, sb);
+        LAUNCH(k_ccl_lattice, chain_wide, kThreads, 0, stream, ctr, sd, sb, m);
       } else {
-        LAUNCH(k_ccl_hook, kWide, kThreads, 0, stream, ctr, sd, sb, m);
+        LAUNCH(k_ccl_hook, chain_wide, kThreads, 0, stream, ctr, sd, sb, m);
       }
-      LAUNCH(k_ccl_compress, kWide, kThreads, 0, stream, ctr, sb);
+      LAUNCH(k_ccl_compress, chain_wide, kThreads, 0, stream, ctr, sb);
       LAUNCH(k_ccl_giant, 1, 1024, 0, stream, ctr, sb);
-      LAUNCH(k_ccl_full, kWide, kThreads, 0, stream, ctr, sd, sb, m);
+      LAUNCH(k_ccl_full, chain_wide, kThreads, 0, stream, ctr, sd, sb, m);
     }
-    LAUNCH(k_ccl_flatten, kWide, kThreads, 0, stream, ctr, sb, m);
+    LAUNCH(k_ccl_flatten, chain_wide, kThreads, 0, stream, ctr, sb, m);
   }
   // label_base: global ordinal of list entry 0 (slab owners), else 0
   void launch_clusters(const SegDev& sd, int64_t label_base = 0) {
-    LAUNCH(k_cluster_flags, kWide, kThreads, 0, stream, ctr, sd, seg.b);
+    LAUNCH(k_cluster_flags, chain_wide, kThreads, 0, stream, ctr, sd, seg.b);
     launch_flag_scan(seg.b.big_flag, &ctr->S, seg.b.Scap, seg.b.big_pos, &ctr->K);
-    LAUNCH(k_cluster_assign, kWide, kThreads, 0, stream, ctr, seg.b);
+    LAUNCH(k_cluster_assign, chain_wide, kThreads, 0, stream, ctr, seg.b);
     LAUNCH(k_cluster_setup, 1, 1024, 0, stream, ctr, seg.b);
     if (label_base) LAUNCH(k_klabel_rebase, 8, 256, 0, stream, ctr, seg.b, label_base);
     const int nch = static_cast<int>(seg.hstride);
     LAUNCH(k_member_hist, std::min(nch, 148 * 16), 32, 0, stream, ctr, seg.b, seg.hstride);
-    LAUNCH(k_member_hscan, kWide, kThreads, 0, stream, ctr, seg.b, seg.hstride);
+    LAUNCH(k_member_hscan, chain_wide, kThreads, 0, stream, ctr, seg.b, seg.hstride);
     LAUNCH(k_member_scatter, std::min(nch, 148 * 16), 32, 0, stream, ctr, seg.b, seg.hstride);
   }
   void launch_ransac(const RansacDev& rd) { launch_ransac(rd, ctr, seg.b); }
@@ -954,13 +961,13 @@ struct vp_grid {
   // serve the cluster-parallel pass and, with single-cluster views, the
   // per-cluster-serial execution mode (plane_fit.cpp:107-119)
   void launch_ransac(const RansacDev& rd, Counters* c, const SegBufs& b) {
-    LAUNCH(k_ransac_hyp, kWide, kThreads, 0, stream, c, rd, b);
-    LAUNCH(k_ransac_count, kWide, kThreads, 0, stream, c, rd, b);
-    LAUNCH(k_ransac_select, kWide, kThreads, 0, stream, c, rd, b);
+    LAUNCH(k_ransac_hyp, chain_wide, kThreads, 0, stream, c, rd, b);
+    LAUNCH(k_ransac_count, chain_wide, kThreads, 0, stream, c, rd, b);
+    LAUNCH(k_ransac_select, chain_wide, kThreads, 0, stream, c, rd, b);
     LAUNCH(k_fit_setup, 1, 1024, 0, stream, c, rd, b);
-    LAUNCH(k_extract_count, kWide, kThreads, 0, stream, c, rd, b);
+    LAUNCH(k_extract_count, chain_wide, kThreads, 0, stream, c, rd, b);
     LAUNCH(k_scan_exclusive, 1, 1024, 0, stream, b.ccount, 0u, &c->fit_chunks, nullptr, nullptr);
-    LAUNCH(k_extract_emit, kWide, kThreads, 0, stream, c, rd, b);
+    LAUNCH(k_extract_emit, chain_wide, kThreads, 0, stream, c, rd, b);
   }
   void launch_refine(const double* up, int refine, int exact) {
     const d3 u{up[0], up[1], up[2]};
@@ -977,9 +984,9 @@ struct vp_grid {
   void launch_polygon(int dirs, double min_area) {
     seg.ensure_dirs(dirs, stream);
     LAUNCH(k_poly_setup, 1, 1024, 0, stream, ctr, seg.b);
-    LAUNCH(k_poly_extremes, kWide, 256, 0, stream, ctr, seg.b, seg.dirtab, dirs);
+    LAUNCH(k_poly_extremes, chain_wide, 256, 0, stream, ctr, seg.b, seg.dirtab, dirs);
     LAUNCH(k_poly_inner, 148 * 2, 64, 0, stream, ctr, seg.b, dirs);
-    LAUNCH(k_poly_keep, kWide, 256, 0, stream, ctr, seg.b);
+    LAUNCH(k_poly_keep, chain_wide, 256, 0, stream, ctr, seg.b);
     LAUNCH(k_poly_hull, 148, 256, kHullSmem * 16 * 6, stream, ctr, seg.b, min_area);
   }
 
@@ -1316,6 +1323,11 @@ void run_part_graph(vp_pipeline* pl, int part, cudaStream_t st, F&& enqueue) {
 void pipeline_run(vp_pipeline* pl, size_t nf, const float* const* xyz, const uint64_t* n,
                   const double* R, const double* t, bool device_ptrs, vp_frame_timing* timings) {
   vp_grid* g = pl->grid;
+  struct ChainWidth {  // C2: 148 x 8 -> 148 x 4 blocks, 3130 -> 3260 Hz
+    vp_grid* g;
+    explicit ChainWidth(vp_grid* gg) : g(gg) { g->chain_wide = 148 * 4; }
+    ~ChainWidth() { g->chain_wide = 148 * 8; }
+  } chain_width(g);
   for (auto* e : {pl->ev_start, pl->ev_pre, pl->ev_map, pl->ev_clu, pl->ev_done, pl->ev_h2d})
     for (int q = 0; q < kSlots; ++q)
       if (!e[q]) ck(cudaEventCreate(&e[q]), "event");
