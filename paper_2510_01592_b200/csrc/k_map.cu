@@ -86,8 +86,14 @@ __global__ void k_integrate_hash(GridDesc g, const FrameParams* __restrict__ fp,
   warp_add_u64(&ctr->discarded, disc);
 }
 
-__global__ void k_integrate_offsets(Counters* ctr, const uint32_t* groups, const uint32_t* hcnt,
-                                    uint32_t* hoff) {
+// Per-group ranges of the point-index buffer; groups too large for one
+// thread are listed for the warp pass (<= kFoldMax points) or the block pass
+// and tagged in `groups`, so the three fold kernels are independent of each
+// other (the thread pass never reads a tagged group's hash slot, which the
+// other passes reset).
+constexpr uint32_t kBigGroup = 0x80000000u;
+__global__ void k_integrate_offsets(Counters* ctr, uint32_t* groups, const uint32_t* hcnt,
+                                    uint32_t* hoff, uint32_t* medium, uint32_t* dense) {
   const uint32_t ng = ctr->ngroups;
   const unsigned lane = lane_id();
   for (uint32_t i0 = blockIdx.x * blockDim.x; i0 < ng; i0 += gridDim.x * blockDim.x) {
@@ -104,7 +110,16 @@ __global__ void k_integrate_offsets(Counters* ctr, const uint32_t* groups, const
     uint32_t base = 0;
     if (lane == 31) base = atomicAdd(&ctr->group_cursor, incl);
     base = __shfl_sync(0xffffffffu, base, 31);
-    if (in) hoff[slot] = base + incl - c;
+    if (in) {
+      hoff[slot] = base + incl - c;
+      if (c > static_cast<uint32_t>(kFoldSmall)) {
+        if (c <= static_cast<uint32_t>(kFoldMax))
+          medium[atomicAdd(&ctr->nmedium, 1u)] = slot;  // warp pass
+        else
+          dense[atomicAdd(&ctr->ndense, 1u)] = slot;  // block pass
+        groups[i] = slot | kBigGroup;
+      }
+    }
   }
 }
 
@@ -144,25 +159,19 @@ __device__ __forceinline__ void fold_cell(const GridDesc& g, const FrameParams* 
 }
 
 // Most voxels receive a handful of points: one thread per voxel sorts its
-// (<= kFoldSmall) point indices in registers and folds them; larger groups are
-// listed for the warp-per-voxel pass (<= kFoldMax) or the block pass (dense).
+// (<= kFoldSmall) point indices in registers and folds them; larger groups
+// (listed by k_integrate_offsets) are folded concurrently by the warp-per-voxel
+// and block passes.
 __global__ void __launch_bounds__(256) k_integrate_fold(GridDesc g, const FrameParams* __restrict__ fp,
                                                         Counters* ctr, const uint32_t* groups,
                                                         uint32_t* hkey, uint32_t* hcnt,
-                                                        const uint32_t* hoff, uint32_t* sorted,
-                                                        uint32_t* medium, uint32_t* dense) {
+                                                        const uint32_t* hoff, uint32_t* sorted) {
   const uint32_t ng = ctr->ngroups;
   unsigned long long fresh = 0;
   for (uint32_t gi = blockIdx.x * blockDim.x + threadIdx.x; gi < ng; gi += gridDim.x * blockDim.x) {
     const uint32_t slot = groups[gi];
+    if (slot & kBigGroup) continue;  // the warp or block pass
     const uint32_t cnt = hcnt[slot];
-    if (cnt > static_cast<uint32_t>(kFoldSmall)) {
-      if (cnt <= static_cast<uint32_t>(kFoldMax))
-        medium[atomicAdd(&ctr->nmedium, 1u)] = slot;  // warp pass
-      else
-        dense[atomicAdd(&ctr->ndense, 1u)] = slot;  // block pass
-      continue;
-    }
     const uint32_t key = hkey[slot];
     const uint32_t* lst = sorted + hoff[slot];
     uint32_t idx[kFoldSmall];

@@ -431,7 +431,7 @@ struct vp_grid {
   cudaStream_t mstream = nullptr;   // mapping stream of pipelined runs
   cudaStream_t fstream = nullptr;   // fork of the mapping stream (integrate grouping || clear_rays)
   cudaStream_t pstream = nullptr;   // grid-independent first half of a pipelined frame's mapping
-  cudaEvent_t fork_ev[2] = {nullptr, nullptr};
+  cudaEvent_t fork_ev[4] = {};
   // Segmentation contexts of the pipelined run's slots: frame k's CCL ..
   // polygon chain runs on its slot's stream with its own scratch and ordinal
   // map while later frames are mapped and start their chains. The active
@@ -836,19 +836,24 @@ struct vp_grid {
     if (n == 0 && !capturing) return;
     const int gp = grid_for(capturing ? pcap : n);
     LAUNCH(k_integrate_hash, gp, kThreads, 0, st, gd, d_fp, ctr, hkey, hcnt, hmask, groups, pslot, prank);
-    LAUNCH(k_integrate_offsets, gp, kThreads, 0, st, ctr, groups, hcnt, hoff);
+    LAUNCH(k_integrate_offsets, gp, kThreads, 0, st, ctr, groups, hcnt, hoff, medium, dense);
     LAUNCH(k_integrate_scatter, gp, kThreads, 0, st, d_fp, pslot, prank, hoff, sorted);
   }
-  // the ordered fold into the cells: after clear_rays (voxel_grid order)
+  // the ordered fold into the cells: after clear_rays (voxel_grid order);
+  // the thread, warp and block passes touch disjoint voxels: the larger
+  // groups are folded on the fork stream beside the thread pass
   void launch_integrate_fold(uint64_t n) {
     if (n == 0 && !capturing) return;
     const int gp = grid_for(capturing ? pcap : n);
-    LAUNCH(k_integrate_fold, gp, kThreads, 0, lstream, gd, d_fp, ctr, groups, hkey, hcnt, hoff,
-           sorted, medium, dense);
-    LAUNCH(k_integrate_fold_medium, 148 * 4, kThreads, 0, lstream, gd, d_fp, ctr, hkey, hcnt, hoff, sorted,
+    ck(cudaEventRecord(fork_ev[2], lstream), "fork");
+    ck(cudaStreamWaitEvent(fstream, fork_ev[2], 0), "fork");
+    LAUNCH(k_integrate_fold_medium, 148 * 4, kThreads, 0, fstream, gd, d_fp, ctr, hkey, hcnt, hoff, sorted,
            medium);
-    LAUNCH(k_integrate_fold_dense, 148, 1024, kDenseSmem, lstream, gd, d_fp, ctr, hkey, hcnt, hoff, sorted,
+    LAUNCH(k_integrate_fold_dense, 148, 1024, kDenseSmem, fstream, gd, d_fp, ctr, hkey, hcnt, hoff, sorted,
            pslot, dense);
+    ck(cudaEventRecord(fork_ev[3], fstream), "join");
+    LAUNCH(k_integrate_fold, gp, kThreads, 0, lstream, gd, d_fp, ctr, groups, hkey, hcnt, hoff, sorted);
+    ck(cudaStreamWaitEvent(lstream, fork_ev[3], 0), "join");
   }
   void launch_recenter() {
     LAUNCH(k_recenter, grid_for(gd.nwords), kThreads, 0, lstream, gd, d_fp, ctr);

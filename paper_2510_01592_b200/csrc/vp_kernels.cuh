@@ -274,13 +274,13 @@ struct HmDesc {
 __global__ void k_integrate_hash(GridDesc g, const FrameParams* fp, Counters* ctr, uint32_t* hkey,
                                  uint32_t* hcnt, uint32_t hmask, uint32_t* groups, uint32_t* pslot,
                                  uint32_t* prank);
-__global__ void k_integrate_offsets(Counters* ctr, const uint32_t* groups, const uint32_t* hcnt,
-                                    uint32_t* hoff);
+__global__ void k_integrate_offsets(Counters* ctr, uint32_t* groups, const uint32_t* hcnt,
+                                    uint32_t* hoff, uint32_t* medium, uint32_t* dense);
 __global__ void k_integrate_scatter(const FrameParams* fp, const uint32_t* pslot,
                                     const uint32_t* prank, const uint32_t* hoff, uint32_t* sorted);
 __global__ void k_integrate_fold(GridDesc g, const FrameParams* fp, Counters* ctr,
                                  const uint32_t* groups, uint32_t* hkey, uint32_t* hcnt,
-                                 const uint32_t* hoff, uint32_t* sorted, uint32_t* medium, uint32_t* dense);
+                                 const uint32_t* hoff, uint32_t* sorted);
 __global__ void k_integrate_fold_medium(GridDesc g, const FrameParams* fp, Counters* ctr, uint32_t* hkey,
                                         uint32_t* hcnt, const uint32_t* hoff, const uint32_t* sorted,
                                         const uint32_t* medium);
