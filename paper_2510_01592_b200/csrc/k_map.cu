@@ -1196,10 +1196,8 @@ __global__ void k_flags_positions(const uint8_t* __restrict__ flags, const uint3
 }
 
 // Single-block exclusive scan of a[0..n) in place; *total = sum (optional
-// also copied to *total2). n is read from n_ptr when non-null.
-__global__ void k_scan_exclusive(uint32_t* a, uint32_t n_static, const uint32_t* n_ptr,
-                                 uint32_t* total, uint32_t* total2) {
-  const uint32_t n = n_ptr ? *n_ptr : n_static;
+// also copied to *total2).
+__device__ __forceinline__ void block_scan_array(uint32_t* a, uint32_t n, uint32_t* total, uint32_t* total2) {
   __shared__ uint32_t carry;
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
@@ -1230,6 +1228,17 @@ __global__ void k_scan_exclusive(uint32_t* a, uint32_t n_static, const uint32_t*
     if (total) *total = carry;
     if (total2) *total2 = carry;
   }
+}
+
+// n is read from n_ptr when non-null.
+__global__ void k_scan_exclusive(uint32_t* a, uint32_t n_static, const uint32_t* n_ptr,
+                                 uint32_t* total, uint32_t* total2) {
+  block_scan_array(a, n_ptr ? *n_ptr : n_static, total, total2);
+}
+
+// Tile sums of a list of min(*n_ptr, cap) items in tiles of `per`.
+__global__ void k_scan_tiles(uint32_t* a, const uint32_t* n_ptr, uint32_t cap, uint32_t per, uint32_t* total) {
+  block_scan_array(a, (min(*n_ptr, cap) + per - 1) / per, total, nullptr);
 }
 
 }  // namespace vp

@@ -13,14 +13,19 @@ namespace vp {
 // acos(d)*kRadToDeg <= theta is evaluated as d >= d*, with d* found on the host
 // by bisection over the host libm acos (exact; A.3).
 // ---------------------------------------------------------------------------
+// Blocks walk the list in tiles of blockDim voxels and write each tile's
+// steppable count to tsum (the steppable compaction's block sums).
 __global__ void k_normals(GridDesc g, const FrameParams* __restrict__ fp, Counters* ctr, SegDev sp,
-                          SegBufs b, int write_status) {
+                          SegBufs b, int write_status, uint32_t* tsum) {
   if (blockIdx.x == 0 && threadIdx.x == 0 && ctr->V > b.Vcap) atomicOr(&ctr->overflow, kOverflowOcc);
   const uint32_t V = min(ctr->V, b.Vcap);
   const uint32_t* occ = fp->occ_post;
   const int32_t* off = fp->off_post;
   const int r = sp.radius;
-  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x) {
+  for (uint32_t t0 = blockIdx.x * blockDim.x; t0 < V; t0 += gridDim.x * blockDim.x) {
+    const uint32_t v = t0 + threadIdx.x;
+    bool step = false;
+    if (v < V) {
     const uint32_t flat = b.occ_list[v];
     const uint32_t rr = fdiv(flat, g.fez);
     const int z = static_cast<int>(flat - rr * static_cast<uint32_t>(g.ez));
@@ -124,7 +129,7 @@ __global__ void k_normals(GridDesc g, const FrameParams* __restrict__ fp, Counte
     }
     double d = valid ? dot3(nrm, sp.up) : 0.0;
     d = d < 0.0 ? 0.0 : (1.0 < d ? 1.0 : d);  // std::clamp(d, 0, 1)
-    const bool step = valid && n >= sp.min_neighbors && d >= sp.dstar;
+    step = valid && n >= sp.min_neighbors && d >= sp.dstar;
     if (write_status) own->status = step ? 2 : 1;  // VoxelStatus::Steppable / Occupied
     b.est_normal[3 * v] = nrm.x;
     b.est_normal[3 * v + 1] = nrm.y;
@@ -137,16 +142,22 @@ __global__ void k_normals(GridDesc g, const FrameParams* __restrict__ fp, Counte
     b.own_count[v] = oc;
     b.own_status[v] = ostatus;
     b.step_flag[v] = step ? 1 : 0;
+    }  // v < V
+    const int c = __syncthreads_count(step);
+    if (threadIdx.x == 0) tsum[t0 / blockDim.x] = static_cast<uint32_t>(c);
   }
 }
 
 // Steppable list in occupied (lexicographic) order -> ordinals; fills the
-// ordinal map used by the CCL window search.
-__global__ void k_step_emit(GridDesc g, Counters* ctr, SegBufs b, MapDesc m, int xadd) {
+// ordinal map used by the CCL window search. Same tiles as k_normals: a
+// voxel's ordinal = its tile's offset (scanned tsum) + its rank in the tile.
+__global__ void k_step_emit(GridDesc g, Counters* ctr, SegBufs b, MapDesc m, int xadd, const uint32_t* toff) {
   const uint32_t V = min(ctr->V, b.Vcap);
-  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x) {
-    if (!b.step_flag[v]) continue;
-    const uint32_t s = b.step_pos[v];
+  for (uint32_t t0 = blockIdx.x * blockDim.x; t0 < V; t0 += gridDim.x * blockDim.x) {
+    const uint32_t v = t0 + threadIdx.x;
+    const bool f = v < V && b.step_flag[v];
+    const uint32_t s = toff[t0 / blockDim.x] + block_exclusive_u32(f ? 1u : 0u);
+    if (!f) continue;
     if (s >= b.Scap) {
       atomicOr(&ctr->overflow, kOverflowStep);
       continue;

@@ -235,7 +235,7 @@ struct Seg {
     const bool need = !b.occ_list || vcap > b.Vcap || scap > b.Scap || icap > b.Icap ||
                       static_cast<uint64_t>(iterations) * kClusterBins > cand_cap;
     const uint64_t need_bsum = std::max<uint64_t>({(nwords + kScanPerBlock - 1) / kScanPerBlock,
-                                                   (vcap + kScanPerBlock - 1) / kScanPerBlock,
+                                                   (vcap + kThreads - 1) / kThreads,
                                                    (scap + kScanPerBlock - 1) / kScanPerBlock}) + 1;
     if (need) {
       ++gen;
@@ -917,12 +917,16 @@ struct vp_grid {
   }
 
   // normals + classify + steppable list (+ ordinal map)
+  // normals + classify (steppable counts per kThreads-voxel tile, scanned:
+  // the tile offsets and ctr->S)
   void launch_classify(const SegDev& sd, int write_status) {
-    LAUNCH(k_normals, kWide, kThreads, 0, stream, gd, d_fp, ctr, sd, seg.b, write_status);
-    launch_flag_scan(seg.b.step_flag, &ctr->V, seg.b.Vcap, seg.b.step_pos, &ctr->S);
+    uint32_t* ts = seg.bsum + seg.bsum_cap;
+    LAUNCH(k_normals, kWide, kThreads, 0, stream, gd, d_fp, ctr, sd, seg.b, write_status, ts);
+    LAUNCH(k_scan_tiles, 1, 1024, 0, stream, ts, &ctr->V, seg.b.Vcap, static_cast<uint32_t>(kThreads), &ctr->S);
   }
+  // the steppable list at the ordinals of launch_classify's tile offsets
   void launch_step_emit(const MapDesc& m, int xadd = 0) {
-    LAUNCH(k_step_emit, kWide, kThreads, 0, stream, gd, ctr, seg.b, m, xadd);
+    LAUNCH(k_step_emit, kWide, kThreads, 0, stream, gd, ctr, seg.b, m, xadd, seg.bsum + seg.bsum_cap);
   }
   // union-find over the steppable list in seg.b (ctr->S set)
   void launch_ccl(const SegDev& sd, const MapDesc& m) { launch_ccl(sd, m, seg.b); }

@@ -310,13 +310,14 @@ __global__ void k_bitmap_emit(const FrameParams* fp, uint64_t w_lo, uint64_t nwo
                               const uint32_t* boff, uint32_t* out, uint32_t cap);
 __global__ void k_scan_exclusive(uint32_t* a, uint32_t n_static, const uint32_t* n_ptr,
                                  uint32_t* total, uint32_t* total2);
+__global__ void k_scan_tiles(uint32_t* a, const uint32_t* n_ptr, uint32_t cap, uint32_t per, uint32_t* total);
 
 // ---- kernels (k_segment.cu)
 __global__ void k_normals(GridDesc g, const FrameParams* fp, Counters* ctr, SegDev sp, SegBufs b,
-                          int write_status);
+                          int write_status, uint32_t* tsum);
 __global__ void k_adjacency(Counters* ctr, SegDev sp, SegBufs b, MapDesc m, const uint64_t* rows,
                             uint32_t* counts, int32_t* cols);
-__global__ void k_step_emit(GridDesc g, Counters* ctr, SegBufs b, MapDesc m, int xadd);
+__global__ void k_step_emit(GridDesc g, Counters* ctr, SegBufs b, MapDesc m, int xadd, const uint32_t* toff);
 __global__ void k_map_fill(Counters* ctr, SegBufs b, MapDesc m);
 __global__ void k_occ_gather(GridDesc g, const FrameParams* fp, Counters* ctr, SegBufs b);
 __global__ void k_ccl_init(Counters* ctr, SegBufs b);
