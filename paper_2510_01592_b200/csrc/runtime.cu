@@ -211,7 +211,7 @@ struct Seg {
 
   void release() {
     void* ptrs[] = {b.occ_list, b.est_normal, b.est_ncount, b.est_valid, b.own_mean, b.own_count,
-                    b.own_status, b.step_flag, b.step_pos, b.st_idx, b.st_mean, b.st_normal,
+                    b.own_status, b.step_flag, b.st_idx, b.st_mean, b.st_normal,
                     b.parent, b.label, b.cnt, b.cid, b.big_flag, b.big_pos, b.klabel, b.ksize,
                     b.kpoff, b.H, b.mx, b.my, b.mz, b.cand, b.cand_cnt, b.win_it, b.win_cnt,
                     b.fid, b.fit_cluster, b.ioff, b.fch_off, b.ccount, b.fit_model, b.fit_meta, b.ref_model, b.inl,
@@ -253,7 +253,6 @@ struct Seg {
       b.own_count = dalloc<uint32_t>(vcap);
       b.own_status = dalloc<uint8_t>(vcap);
       b.step_flag = dalloc<uint8_t>(vcap);
-      b.step_pos = dalloc<uint32_t>(vcap);
       b.st_idx = dalloc<int32_t>(3ull * scap);
       b.st_mean = dalloc<double>(3ull * scap);
       b.st_normal = dalloc<double>(3ull * scap);

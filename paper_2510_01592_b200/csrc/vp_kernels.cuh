@@ -163,7 +163,6 @@ struct SegBufs {
   uint32_t* own_count;
   uint8_t* own_status;
   uint8_t* step_flag;
-  uint32_t* step_pos;
   // steppable (Scap)
   int32_t* st_idx;       // 3*Scap window indices
   double* st_mean;       // 3*Scap
