@@ -1019,7 +1019,11 @@ __global__ void k_clear_apply(GridDesc g, const FrameParams* __restrict__ fp, Co
 // as voxels_dropped.
 // ---------------------------------------------------------------------------
 
-__global__ void k_recenter(GridDesc g, const FrameParams* __restrict__ fp, Counters* ctr) {
+// Blocks walk the bitmap in the occupied scan's tiles (kScanPerBlock words,
+// word k * blockDim + t of a tile by thread t) and leave each tile's
+// popcount of the new bitmap in bsum, so k_bitmap_count skips a shifted frame.
+__global__ void __launch_bounds__(kScanThreads) k_recenter(GridDesc g, const FrameParams* __restrict__ fp,
+                                                           Counters* ctr, uint32_t* bsum) {
   if (!fp->do_shift) return;
   const uint32_t* __restrict__ oldb = fp->occ_pre;
   uint32_t* __restrict__ newb = fp->occ_post;
@@ -1027,52 +1031,58 @@ __global__ void k_recenter(GridDesc g, const FrameParams* __restrict__ fp, Count
   unsigned long long dropped = 0;
   const uint32_t nw = static_cast<uint32_t>(g.nwords);  // < 2^32 (grid creation check)
   const int W = g.W, ey = g.ey, ex = g.ex, ez = g.ez;
-  for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < nw; u += gridDim.x * blockDim.x) {
-    const uint32_t row = fdiv(u, g.fW);
-    const int wz = static_cast<int>(u - row * static_cast<uint32_t>(W));
-    const uint32_t xr = fdiv(row, g.fey);
-    const int y = static_cast<int>(row - xr * static_cast<uint32_t>(ey)), x = static_cast<int>(xr);
-    // new word: destination (x, y, z) reads source (x+sx, y+sy, z+sz), i.e.
-    // bits [32 wz + sz, +32) of source row (x+sx, y+sy), zero outside the row
-    const int xs = x + sx, ys = y + sy;
-    uint32_t nv = 0;
-    if (static_cast<unsigned>(xs) < static_cast<unsigned>(ex) && static_cast<unsigned>(ys) < static_cast<unsigned>(ey)) {
-      const uint32_t* src = oldb + (static_cast<uint32_t>(xs) * static_cast<uint32_t>(ey) + static_cast<uint32_t>(ys)) *
-                                       static_cast<uint32_t>(W);
-      const int b0 = wz * 32 + sz;
-      const int wlo = b0 >> 5, sh = b0 & 31;  // floor division (arithmetic shift)
-      const uint32_t lo = (wlo >= 0 && wlo < W) ? __ldg(src + wlo) : 0u;
-      const uint32_t hi = (wlo + 1 >= 0 && wlo + 1 < W) ? __ldg(src + wlo + 1) : 0u;
-      nv = __funnelshift_r(lo, hi, sh);
-    }
-    const int zlim = ez - wz * 32;
-    if (zlim < 32) nv &= (1u << zlim) - 1u;
-    newb[u] = nv;
-    // dropped: old bits whose destination (x-sx, y-sy, z-sz) leaves the window
-    const uint32_t ov = __ldg(oldb + u);
-    if (!ov) continue;
-    uint32_t drop;
-    const int xd = x - sx, yd = y - sy;
-    if (static_cast<unsigned>(xd) >= static_cast<unsigned>(ex) || static_cast<unsigned>(yd) >= static_cast<unsigned>(ey)) {
-      drop = ov;
-    } else {
-      // keep bits b with 0 <= 32*wz + b - sz < ez, i.e. b in [blo, bhi)
-      const int blo = min(max(sz - 32 * wz, 0), 32);
-      const int bhi = min(max(ez + sz - 32 * wz, 0), 32);
-      uint32_t keep = 0;
-      if (bhi > blo) {
-        const uint32_t upto_hi = bhi >= 32 ? 0xffffffffu : ((1u << bhi) - 1u);
-        const uint32_t below_lo = blo >= 32 ? 0xffffffffu : ((1u << blo) - 1u);
-        keep = upto_hi & ~below_lo;
+  for (uint32_t t0 = blockIdx.x * kScanPerBlock; t0 < nw; t0 += gridDim.x * kScanPerBlock) {
+    uint32_t pc = 0;
+    for (uint32_t u = t0 + threadIdx.x; u < min(nw, t0 + kScanPerBlock); u += kScanThreads) {
+      const uint32_t row = fdiv(u, g.fW);
+      const int wz = static_cast<int>(u - row * static_cast<uint32_t>(W));
+      const uint32_t xr = fdiv(row, g.fey);
+      const int y = static_cast<int>(row - xr * static_cast<uint32_t>(ey)), x = static_cast<int>(xr);
+      // new word: destination (x, y, z) reads source (x+sx, y+sy, z+sz), i.e.
+      // bits [32 wz + sz, +32) of source row (x+sx, y+sy), zero outside the row
+      const int xs = x + sx, ys = y + sy;
+      uint32_t nv = 0;
+      if (static_cast<unsigned>(xs) < static_cast<unsigned>(ex) && static_cast<unsigned>(ys) < static_cast<unsigned>(ey)) {
+        const uint32_t* src = oldb + (static_cast<uint32_t>(xs) * static_cast<uint32_t>(ey) + static_cast<uint32_t>(ys)) *
+                                         static_cast<uint32_t>(W);
+        const int b0 = wz * 32 + sz;
+        const int wlo = b0 >> 5, sh = b0 & 31;  // floor division (arithmetic shift)
+        const uint32_t lo = (wlo >= 0 && wlo < W) ? __ldg(src + wlo) : 0u;
+        const uint32_t hi = (wlo + 1 >= 0 && wlo + 1 < W) ? __ldg(src + wlo + 1) : 0u;
+        nv = __funnelshift_r(lo, hi, sh);
       }
-      drop = ov & ~keep;
+      const int zlim = ez - wz * 32;
+      if (zlim < 32) nv &= (1u << zlim) - 1u;
+      newb[u] = nv;
+      pc += __popc(nv);
+      // dropped: old bits whose destination (x-sx, y-sy, z-sz) leaves the window
+      const uint32_t ov = __ldg(oldb + u);
+      if (!ov) continue;
+      uint32_t drop;
+      const int xd = x - sx, yd = y - sy;
+      if (static_cast<unsigned>(xd) >= static_cast<unsigned>(ex) || static_cast<unsigned>(yd) >= static_cast<unsigned>(ey)) {
+        drop = ov;
+      } else {
+        // keep bits b with 0 <= 32*wz + b - sz < ez, i.e. b in [blo, bhi)
+        const int blo = min(max(sz - 32 * wz, 0), 32);
+        const int bhi = min(max(ez + sz - 32 * wz, 0), 32);
+        uint32_t keep = 0;
+        if (bhi > blo) {
+          const uint32_t upto_hi = bhi >= 32 ? 0xffffffffu : ((1u << bhi) - 1u);
+          const uint32_t below_lo = blo >= 32 ? 0xffffffffu : ((1u << blo) - 1u);
+          keep = upto_hi & ~below_lo;
+        }
+        drop = ov & ~keep;
+      }
+      dropped += __popc(drop);
+      while (drop) {
+        const int b = __ffs(drop) - 1;
+        drop &= drop - 1;
+        zero_cell(g.cells + phys_index(g, fp->off_pre, x, y, wz * 32 + b));
+      }
     }
-    dropped += __popc(drop);
-    while (drop) {
-      const int b = __ffs(drop) - 1;
-      drop &= drop - 1;
-      zero_cell(g.cells + phys_index(g, fp->off_pre, x, y, wz * 32 + b));
-    }
+    pc = block_sum_u32(pc);
+    if (threadIdx.x == 0) bsum[t0 / kScanPerBlock] = pc;
   }
   warp_add_u64(&ctr->dropped, dropped);
 }
@@ -1124,6 +1134,7 @@ __global__ void k_frame_begin(Counters* ctr, const unsigned long long* occ_total
 // ---------------------------------------------------------------------------
 __global__ void k_bitmap_count(const FrameParams* __restrict__ fp, uint64_t w_lo, uint64_t nwords,
                                uint32_t* bsum) {
+  if (fp->do_shift) return;  // k_recenter left the tile counts
   const uint32_t* __restrict__ bits = fp->occ_post + w_lo;
   const uint64_t w0 = (static_cast<uint64_t>(blockIdx.x) * kScanThreads + threadIdx.x) * kScanItems;
   uint32_t c = 0;

@@ -855,7 +855,9 @@ struct vp_grid {
     ck(cudaStreamWaitEvent(lstream, fork_ev[3], 0), "join");
   }
   void launch_recenter() {
-    LAUNCH(k_recenter, grid_for(gd.nwords), kThreads, 0, lstream, gd, d_fp, ctr);
+    // (the tile counts go to the active segmentation context's scan sums)
+    LAUNCH(k_recenter, static_cast<int>(std::min<uint64_t>((gd.nwords + kScanPerBlock - 1) / kScanPerBlock, 148 * 8)),
+           kScanThreads, 0, lstream, gd, d_fp, ctr, seg.bsum);
   }
   void launch_finalize() { LAUNCH(k_map_finalize, 1, 1, 0, lstream, ctr, occ_total); }
   // clear_rays and the grouping half of integrate_frame in parallel (fork

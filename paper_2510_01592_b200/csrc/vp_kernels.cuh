@@ -293,7 +293,7 @@ __global__ void k_dda_keys(GridDesc g, const FrameParams* fp, DdaBins* db, uint8
 __global__ void k_dda_plan(DdaBins* db);
 __global__ void k_dda_scatter(const FrameParams* fp, DdaBins* db, const uint8_t* bin_of, uint32_t* perm);
 __global__ void k_clear_apply(GridDesc g, const FrameParams* fp, Counters* ctr, const DdaBins* db);
-__global__ void k_recenter(GridDesc g, const FrameParams* fp, Counters* ctr);
+__global__ void k_recenter(GridDesc g, const FrameParams* fp, Counters* ctr, uint32_t* bsum);
 __global__ void k_map_finalize(Counters* ctr, unsigned long long* occ_total);
 __global__ void k_frame_begin(Counters* ctr, const unsigned long long* occ_total);
 __global__ void k_set_statuses(GridDesc g, const FrameParams* fp, const int32_t* idx, const uint8_t* st,
