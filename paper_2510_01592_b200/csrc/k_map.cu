@@ -943,25 +943,40 @@ __device__ __forceinline__ void clear_apply_rows(const GridDesc& g, const FrameP
                                                  Counters* ctr) {
   uint32_t* occ = fp->occ_pre;
   unsigned long long cl = 0, fr = 0;
-  for (uint64_t w = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; w < g.nwords;
-       w += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const uint32_t c = g.clr[w];
-    if (!c) continue;
-    g.clr[w] = 0;
-    cl += __popc(c);
-    const uint32_t o = occ[w];
-    uint32_t f = o & c;
-    if (!f) continue;
-    occ[w] = o & ~f;
-    fr += __popc(f);
-    const uint32_t row = fdiv(static_cast<uint32_t>(w), g.fW);
-    const int z0 = static_cast<int>(static_cast<uint32_t>(w) - row * static_cast<uint32_t>(g.W)) * 32;
-    const uint32_t xr = fdiv(row, g.fey);
-    const int y = static_cast<int>(row - xr * static_cast<uint32_t>(g.ey)), x = static_cast<int>(xr);
-    while (f) {
-      const int b = __ffs(f) - 1;
-      f &= f - 1;
-      zero_cell(g.cells + phys_index(g, fp->off_pre, x, y, z0 + b));
+  // four mask words per thread per trip (one 16-byte load; the mask is
+  // mostly zero, so the trip count is what the sweep costs)
+  const uint64_t nq = (g.nwords + 3) / 4;
+  for (uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < nq;
+       q += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    uint32_t cv[4];
+    if (4 * q + 3 < g.nwords) {
+      const uint4 c4 = reinterpret_cast<const uint4*>(g.clr)[q];
+      cv[0] = c4.x, cv[1] = c4.y, cv[2] = c4.z, cv[3] = c4.w;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) cv[k] = 4 * q + k < g.nwords ? g.clr[4 * q + k] : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t c = cv[k];
+      if (!c) continue;
+      const uint64_t w = 4 * q + k;
+      g.clr[w] = 0;
+      cl += __popc(c);
+      const uint32_t o = occ[w];
+      uint32_t f = o & c;
+      if (!f) continue;
+      occ[w] = o & ~f;
+      fr += __popc(f);
+      const uint32_t row = fdiv(static_cast<uint32_t>(w), g.fW);
+      const int z0 = static_cast<int>(static_cast<uint32_t>(w) - row * static_cast<uint32_t>(g.W)) * 32;
+      const uint32_t xr = fdiv(row, g.fey);
+      const int y = static_cast<int>(row - xr * static_cast<uint32_t>(g.ey)), x = static_cast<int>(xr);
+      while (f) {
+        const int b = __ffs(f) - 1;
+        f &= f - 1;
+        zero_cell(g.cells + phys_index(g, fp->off_pre, x, y, z0 + b));
+      }
     }
   }
   warp_add_u64(&ctr->cleared, cl);
