@@ -1147,15 +1147,31 @@ __global__ void k_frame_begin(Counters* ctr, const unsigned long long* occ_total
 // bitmap (x, y, z lexicographic) into logical flat indices.
 // 256 threads x 8 words per block.
 // ---------------------------------------------------------------------------
+// kScanItems (8) consecutive bitmap words from w0: two 16-byte loads when
+// aligned and in range, else word by word (zero past nwords).
+__device__ __forceinline__ void load_words8(const uint32_t* __restrict__ bits, uint64_t w0, uint64_t nwords,
+                                            uint32_t* v) {
+  static_assert(kScanItems == 8, "two uint4 per thread");
+  if (w0 + 8 <= nwords && (reinterpret_cast<uintptr_t>(bits + w0) & 15u) == 0) {
+    const uint4 a = reinterpret_cast<const uint4*>(bits + w0)[0];
+    const uint4 b = reinterpret_cast<const uint4*>(bits + w0)[1];
+    v[0] = a.x, v[1] = a.y, v[2] = a.z, v[3] = a.w, v[4] = b.x, v[5] = b.y, v[6] = b.z, v[7] = b.w;
+  } else {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = (w0 + k < nwords) ? bits[w0 + k] : 0u;
+  }
+}
+
 __global__ void k_bitmap_count(const FrameParams* __restrict__ fp, uint64_t w_lo, uint64_t nwords,
                                uint32_t* bsum) {
   if (fp->do_shift) return;  // k_recenter left the tile counts
   const uint32_t* __restrict__ bits = fp->occ_post + w_lo;
   const uint64_t w0 = (static_cast<uint64_t>(blockIdx.x) * kScanThreads + threadIdx.x) * kScanItems;
+  uint32_t v[kScanItems];
+  load_words8(bits, w0, nwords, v);
   uint32_t c = 0;
 #pragma unroll
-  for (int k = 0; k < kScanItems; ++k)
-    if (w0 + k < nwords) c += __popc(bits[w0 + k]);
+  for (int k = 0; k < kScanItems; ++k) c += __popc(v[k]);
   c = block_sum_u32(c);
   if (threadIdx.x == 0) bsum[blockIdx.x] = c;
 }
@@ -1165,12 +1181,10 @@ __global__ void k_bitmap_emit(const FrameParams* __restrict__ fp, uint64_t w_lo,
   const uint32_t* __restrict__ bits = fp->occ_post + w_lo;
   const uint64_t w0 = (static_cast<uint64_t>(blockIdx.x) * kScanThreads + threadIdx.x) * kScanItems;
   uint32_t v[kScanItems];
+  load_words8(bits, w0, nwords, v);
   uint32_t c = 0;
 #pragma unroll
-  for (int k = 0; k < kScanItems; ++k) {
-    v[k] = (w0 + k < nwords) ? bits[w0 + k] : 0u;
-    c += __popc(v[k]);
-  }
+  for (int k = 0; k < kScanItems; ++k) c += __popc(v[k]);
   uint32_t pos = boff[blockIdx.x] + block_exclusive_u32(c);
 #pragma unroll
   for (int k = 0; k < kScanItems; ++k) {
