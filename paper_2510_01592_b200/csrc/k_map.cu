@@ -879,25 +879,38 @@ __device__ __forceinline__ void clear_walk_bricks(const GridDesc& g, const Frame
       continue;
     if (!(c0 == wn.oc0 && c1 == wn.oc1 && c2 == wn.oc2)) visit();  // origin cell: first cell only
     for (;;) {
-      // m = argmin t_max, ties to the lower axis (voxel_grid.cpp:170-172)
-      const bool m1 = tm1 < tm0;
-      const double tm01 = m1 ? tm1 : tm0;
-      const bool m2 = tm2 < tm01;
-      const double tm = m2 ? tm2 : tm01;
-      const bool x0 = !m1 && !m2, x1 = m1 && !m2;
-      c0 += x0 ? s0 : 0;
-      c1 += x1 ? s1 : 0;
-      c2 += m2 ? s2 : 0;
-      if (tm >= t1 || static_cast<unsigned>(c0) >= ex0 || static_cast<unsigned>(c1) >= ex1 ||
-          static_cast<unsigned>(c2) >= ex2)
-        break;
+      // one DDA step (as in clear_walk_coherent, predicated adds in PTX):
+      // m = argmin t_max, ties to the lower axis (voxel_grid.cpp:170-172);
+      // stop when min t_max >= t1 or the stepped cell leaves the window
+      uint32_t ok;
+      asm("{\n\t"
+          ".reg .pred m1, m2, a, x1, d, p;\n\t"
+          ".reg .f64 t01;\n\t"
+          "setp.lt.f64 m1, %5, %4;\n\t"
+          "selp.f64 t01, %5, %4, m1;\n\t"
+          "setp.lt.f64 m2, %6, t01;\n\t"
+          "setp.ge.f64 d, t01, %10;\n\t"
+          "setp.ge.and.f64 d, %6, %10, d;\n\t"
+          "or.pred a, m1, m2;\n\t"
+          "and.pred x1, m1, !m2;\n\t"
+          "@!a add.s32 %0, %0, %7;\n\t"
+          "@!a add.rn.f64 %4, %4, %11;\n\t"
+          "@x1 add.s32 %1, %1, %8;\n\t"
+          "@x1 add.rn.f64 %5, %5, %12;\n\t"
+          "@m2 add.s32 %2, %2, %9;\n\t"
+          "@m2 add.rn.f64 %6, %6, %13;\n\t"
+          "setp.lt.u32 p, %0, %14;\n\t"
+          "setp.lt.and.u32 p, %1, %15, p;\n\t"
+          "setp.lt.and.u32 p, %2, %16, p;\n\t"
+          "and.pred p, p, !d;\n\t"
+          "selp.u32 %3, 1, 0, p;\n\t"
+          "}"
+          : "+r"(c0), "+r"(c1), "+r"(c2), "=r"(ok), "+d"(tm0), "+d"(tm1), "+d"(tm2)
+          : "r"(s0), "r"(s1), "r"(s2), "d"(t1), "d"(td0), "d"(td1), "d"(td2), "r"(ex0), "r"(ex1), "r"(ex2));
+      if (!ok) break;
       // a slab never sees the ray again once it left the owned x-range in
       // its stepping direction
       if (kSlab && ((s0 > 0 && c0 >= own1) || (s0 < 0 && c0 < own0))) break;
-      const double tn = tm + (m2 ? td2 : (m1 ? td1 : td0));  // t_max[m] += t_delta[m]
-      tm0 = x0 ? tn : tm0;
-      tm1 = x1 ? tn : tm1;
-      tm2 = m2 ? tn : tm2;
       visit();
     }
     if (ab) {
