@@ -306,6 +306,12 @@ def run_ours(args, rank, world, dist):
         limiter = nt.get("utilisation_pct", {}).get(top)
     except Exception:
         pass
+    # DDA cell steps of the step's frames, estimated as the L1 cell distance
+    # sensor -> end point (k_dda_keys' length model; the window clip ignored)
+    dda_steps = 0.0
+    for f in frames:
+        w = f.points.astype(np.float64) @ np.asarray(f.rotation, np.float64).reshape(3, 3).T
+        dda_steps += float(np.nansum(np.abs(w) / wl.resolution))
     # whole-step algorithmic bytes (the survey's frame formula)
     step_bytes = 0.0
     for c, n in zip(per_frame_counters, npts):
@@ -339,7 +345,11 @@ def run_ours(args, rank, world, dist):
                      "unit": "GB/s", "frac": round(achieved / peak, 5), "traffic": traffic,
                      "alg_bytes_per_launch": round(per_launch_bytes), "us_per_launch": round(per_launch_s * 1e6, 2),
                      "share_of_step": round(top_ms / prof_total, 4), "peak_source": peak_source,
-                     "utilisation_pct_ncu": limiter},
+                     "utilisation_pct_ncu": limiter,
+                     # secondary rate of the DDA: cell steps per second
+                     "dda_steps_per_launch_est": round(dda_steps / len(frames)) if top == "k_clear_walk" else None,
+                     "dda_gsteps_per_s": (round(dda_steps / len(frames) / per_launch_s / 1e9, 1)
+                                          if top == "k_clear_walk" else None)},
         "kernels": {k: {"ms_per_step": round(v[0], 4), "calls": int(v[1])}
                     for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])},
         "clocks": clk.summary(),
