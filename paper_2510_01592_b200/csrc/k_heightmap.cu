@@ -125,39 +125,51 @@ __device__ __forceinline__ bool hm_step(const HmDesc& m, uint32_t c, int s, uint
   return true;
 }
 
-// level expansion: frontier visit[ls .. ls+nf); claim = min (pos * 4 + step)
-__global__ void k_hm_claim(HmDesc m, const uint32_t* visit, uint32_t ls, const uint32_t* nfp, double dth) {
-  const uint32_t nf = *nfp;
-  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < 4 * nf; t += gridDim.x * blockDim.x) {
-    const uint32_t c = visit[ls + (t >> 2)];
-    uint32_t nb;
-    if (!hm_step(m, c, static_cast<int>(t & 3), &nb) || m.visited[nb] || !hm_edge(m, c, nb, dth)) continue;
-    atomicMin(m.claim + nb, t);
+// The whole level-synchronous BFS in one block (no host round trip per
+// level): the frontier is visit[ls, ls + nf); a level claims each unvisited
+// neighbour for its smallest (frontier position * 4 + step) (atomicMin),
+// then emits the claimed pairs in that order -- k_hm_claim / k_hm_claimed /
+// k_hm_emit, chained by __syncthreads. dn[1] = seeds in, dn[2] = cells visited out.
+__global__ void __launch_bounds__(1024) k_hm_bfs(HmDesc m, uint32_t* visit, uint32_t* dn, double dth) {
+  __shared__ uint32_t s_base;
+  const uint32_t tid = threadIdx.x;
+  uint32_t ls = 0, nf = dn[1];
+  while (nf) {
+    const uint32_t nt = 4 * nf;
+    for (uint32_t t = tid; t < nt; t += blockDim.x) {
+      const uint32_t c = visit[ls + (t >> 2)];
+      uint32_t nb;
+      if (!hm_step(m, c, static_cast<int>(t & 3), &nb) || m.visited[nb] || !hm_edge(m, c, nb, dth)) continue;
+      atomicMin(m.claim + nb, t);
+    }
+    if (tid == 0) s_base = 0;
+    __syncthreads();
+    const uint32_t le = ls + nf;
+    for (uint32_t b0 = 0; b0 < nt; b0 += blockDim.x) {
+      const uint32_t t = b0 + tid;
+      uint32_t nb = 0;
+      bool f = false;
+      if (t < nt) {
+        const uint32_t c = visit[ls + (t >> 2)];
+        f = hm_step(m, c, static_cast<int>(t & 3), &nb) && !m.visited[nb] && m.claim[nb] == t;
+      }
+      const uint32_t base = s_base;
+      const uint32_t ex = block_exclusive_u32(f ? 1u : 0u);
+      if (f) visit[le + base + ex] = nb;
+      if (tid == blockDim.x - 1) s_base = base + ex + (f ? 1u : 0u);
+      __syncthreads();
+    }
+    const uint32_t nn = s_base;
+    for (uint32_t k = tid; k < nn; k += blockDim.x) {
+      const uint32_t c = visit[le + k];
+      m.visited[c] = 1;
+      m.claim[c] = 0xffffffffu;
+    }
+    __syncthreads();
+    ls = le;
+    nf = nn;
   }
-}
-
-__global__ void k_hm_claimed(HmDesc m, const uint32_t* visit, uint32_t ls, const uint32_t* nfp, uint8_t* flags) {
-  const uint32_t nf = *nfp;
-  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < 4 * nf; t += gridDim.x * blockDim.x) {
-    const uint32_t c = visit[ls + (t >> 2)];
-    uint32_t nb;
-    flags[t] = (hm_step(m, c, static_cast<int>(t & 3), &nb) && !m.visited[nb] && m.claim[nb] == t) ? 1 : 0;
-  }
-}
-
-__global__ void k_hm_emit(HmDesc m, uint32_t* visit, uint32_t ls, const uint32_t* nfp, const uint8_t* flags,
-                          const uint32_t* pos) {
-  const uint32_t nf = *nfp;
-  const uint32_t le = ls + nf;
-  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < 4 * nf; t += gridDim.x * blockDim.x) {
-    if (!flags[t]) continue;
-    const uint32_t c = visit[ls + (t >> 2)];
-    uint32_t nb;
-    hm_step(m, c, static_cast<int>(t & 3), &nb);
-    visit[le + pos[t]] = nb;
-    m.visited[nb] = 1;
-    m.claim[nb] = 0xffffffffu;
-  }
+  if (tid == 0) dn[2] = ls;
 }
 
 // The visit sequence as a "steppable list" for the cluster stage: members

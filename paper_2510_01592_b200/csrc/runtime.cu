@@ -3382,25 +3382,11 @@ int vp_hm_segment(vp_heightmap* hm, const vp_pipeline_params* p, vp_polygons_t**
     LAUNCH(k_hm_seed_flags, grid_for(nc), kThreads, 0, st, hm->m, hm->flags);
     g->launch_flag_scan(hm->flags, hm->dn, nc, hm->pos, hm->dn + 1);
     LAUNCH(k_hm_seed_emit, grid_for(nc), kThreads, 0, st, hm->m, hm->flags, hm->pos, hm->visit);
-    uint32_t nf = 0;
-    ck(cudaMemcpyAsync(&nf, hm->dn + 1, 4, cudaMemcpyDeviceToHost, st), "d2h");
+    // level-synchronous BFS in the reference's FIFO order, all levels in one block
+    LAUNCH(k_hm_bfs, 1, 1024, 0, st, hm->m, hm->visit, hm->dn, dth);
+    uint32_t nv = 0;
+    ck(cudaMemcpyAsync(&nv, hm->dn + 2, 4, cudaMemcpyDeviceToHost, st), "d2h");
     ck(cudaStreamSynchronize(st), "sync");
-    // level-synchronous BFS in the reference's FIFO order
-    uint32_t ls = 0, nv = nf;
-    while (nf) {
-      const uint32_t nt = 4 * nf;
-      LAUNCH(k_hm_claim, grid_for(nt), kThreads, 0, st, hm->m, hm->visit, ls, hm->dn + 1, dth);
-      LAUNCH(k_hm_claimed, grid_for(nt), kThreads, 0, st, hm->m, hm->visit, ls, hm->dn + 1, hm->flags);
-      const uint32_t d3v[1] = {nt};
-      ck(cudaMemcpyAsync(hm->dn + 3, d3v, 4, cudaMemcpyHostToDevice, st), "h2d");
-      g->launch_flag_scan(hm->flags, hm->dn + 3, nt, hm->pos, hm->dn + 2);
-      LAUNCH(k_hm_emit, grid_for(nt), kThreads, 0, st, hm->m, hm->visit, ls, hm->dn + 1, hm->flags, hm->pos);
-      ck(cudaMemcpyAsync(hm->dn + 1, hm->dn + 2, 4, cudaMemcpyDeviceToDevice, st), "d2d");
-      ck(cudaMemcpyAsync(&nf, hm->dn + 2, 4, cudaMemcpyDeviceToHost, st), "d2h");
-      ck(cudaStreamSynchronize(st), "sync");
-      ls = nv;
-      nv += nf;
-    }
     hm->nv = nv;
     // regions >= min_cluster_size, members in BFS order, then the voxel path's fitting
     g->seg.ensure(g->seg.b.Vcap, std::max(g->seg.b.Scap, nv), std::max(g->seg.b.Icap, nv),

@@ -379,10 +379,7 @@ __global__ void k_hm_ccl_init(HmDesc m);
 __global__ void k_hm_ccl_union(HmDesc m, double dth);
 __global__ void k_hm_seed_flags(HmDesc m, uint8_t* flags);
 __global__ void k_hm_seed_emit(HmDesc m, const uint8_t* flags, const uint32_t* pos, uint32_t* visit);
-__global__ void k_hm_claim(HmDesc m, const uint32_t* visit, uint32_t ls, const uint32_t* nfp, double dth);
-__global__ void k_hm_claimed(HmDesc m, const uint32_t* visit, uint32_t ls, const uint32_t* nfp, uint8_t* flags);
-__global__ void k_hm_emit(HmDesc m, uint32_t* visit, uint32_t ls, const uint32_t* nfp, const uint8_t* flags,
-                          const uint32_t* pos);
+__global__ void k_hm_bfs(HmDesc m, uint32_t* visit, uint32_t* dn, double dth);
 __global__ void k_hm_members(HmDesc m, const uint32_t* visit, uint32_t nv, SegBufs b);
 __global__ void k_hm_zero_cnt(uint32_t nv, SegBufs b);
 __global__ void k_hm_klabel(const Counters* ctr, SegBufs b, const uint32_t* visit);
