@@ -38,8 +38,12 @@ constexpr double kRadToDeg = 57.295779513082320876798;
 constexpr double kDegToRad = 0.017453292519943295769237;
 constexpr double kPi = 3.14159265358979323846;  // == glibc M_PI
 constexpr int kThreads = 256;
+#ifndef VP_CHAIN_WIDE
+#define VP_CHAIN_WIDE (148 * 4)
+#endif
+constexpr int kChainWide = VP_CHAIN_WIDE;  // CCL .. polygon grid width in pipelined runs
 #ifndef VP_SLOTS
-#define VP_SLOTS 3
+#define VP_SLOTS 4
 #endif
 constexpr int kSlots = VP_SLOTS;  // frames in flight in a pipelined run
 
@@ -1335,7 +1339,7 @@ void pipeline_run(vp_pipeline* pl, size_t nf, const float* const* xyz, const uin
   vp_grid* g = pl->grid;
   struct ChainWidth {  // C2: 148 x 8 -> 148 x 4 blocks, 3130 -> 3260 Hz
     vp_grid* g;
-    explicit ChainWidth(vp_grid* gg) : g(gg) { g->chain_wide = 148 * 4; }
+    explicit ChainWidth(vp_grid* gg) : g(gg) { g->chain_wide = kChainWide; }
     ~ChainWidth() { g->chain_wide = 148 * 8; }
   } chain_width(g);
   for (auto* e : {pl->ev_start, pl->ev_pre, pl->ev_map, pl->ev_clu, pl->ev_done, pl->ev_h2d})
