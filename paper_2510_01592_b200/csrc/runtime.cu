@@ -213,7 +213,10 @@ struct Seg {
   int dir_n = -1;
   uint32_t hstride = 0;
 
-  void release() {
+  // capacity-dependent buffers (the direction table survives a regrow: a
+  // pipelined run re-captures its graphs after one, and a capture may not
+  // allocate or synchronise)
+  void release_buffers() {
     void* ptrs[] = {b.occ_list, b.est_normal, b.est_ncount, b.est_valid, b.own_mean, b.own_count,
                     b.own_status, b.step_flag, b.st_idx, b.st_mean, b.st_normal,
                     b.parent, b.label, b.cnt, b.cid, b.big_flag, b.big_pos, b.klabel, b.ksize,
@@ -221,11 +224,15 @@ struct Seg {
                     b.fid, b.fit_cluster, b.ioff, b.fch_off, b.ccount, b.fit_model, b.fit_meta, b.ref_model, b.inl,
                     b.rch_off, b.rpart, b.rcen,
                     b.proj, b.surv, b.hull, b.basis, b.pch_off, b.pext_dot, b.pext_idx, b.inner,
-                    b.ninner, b.nsurv, b.prec_d, b.prec_i, b.pool, bsum, dirtab};
+                    b.ninner, b.nsurv, b.prec_d, b.prec_i, b.pool, bsum};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     b = SegBufs{};
     bsum = nullptr;
+  }
+  void release() {
+    release_buffers();
+    if (dirtab) cudaFree(dirtab);
     dirtab = nullptr;
     dir_n = -1;
   }
@@ -243,7 +250,7 @@ struct Seg {
                                                    (scap + kScanPerBlock - 1) / kScanPerBlock}) + 1;
     if (need) {
       ++gen;
-      release();
+      release_buffers();
       b.Vcap = vcap;
       b.Scap = scap;
       b.Mcap = mcap;
@@ -317,6 +324,9 @@ struct Seg {
   void ensure_dirs(int n, cudaStream_t s) {
     if (n == dir_n) return;
     if (n > 64) fail(VP_EINVAL, "make_polygon: at most 64 filter directions supported");
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    ck(cudaStreamIsCapturing(s, &cs), "capture status");
+    if (cs != cudaStreamCaptureStatusNone) fail(VP_ECUDA, "make_polygon: direction table not set before capture");
     std::vector<double> t(2 * 64, 0.0);
     for (int j = 0; j < n; ++j) {  // polygonize.cpp:59-63
       const double a = 2.0 * kPi * j / n;

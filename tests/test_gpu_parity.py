@@ -207,3 +207,21 @@ def test_pipelined_run_c2_matches_frames_and_device_inputs():
     for f in more:
         polys_frame, _ = c.frame(f.points, f.rotation, f.translation)
     assert format_polygons(a2) == format_polygons(polys_frame)
+
+
+def test_pipelined_run_regrows_capacities():
+    """LiDAR frames of ~1 M points: the occupancy bound of the frames in
+    flight exceeds the initial 4 M-voxel capacity, so vp_pipeline_run grows
+    every segmentation context mid-run and re-captures its graphs; the result
+    must still equal the frame-by-frame path."""
+    import torch
+    wl = scenes.workload("c4", frames=8)
+    p = native.default_params(seed=wl.seed)
+    a = native.Pipeline(wl.resolution, wl.extent, wl.frames[0].translation, p)
+    dev = [torch.from_numpy(f.points).cuda() for f in wl.frames]
+    assert sum(len(d) for d in dev[:5]) > (1 << 22)  # frames in flight + the known occupancy
+    polys_run = a.run(wl.frames, device_ptrs=[(d.data_ptr(), len(d)) for d in dev])
+    b = native.Pipeline(wl.resolution, wl.extent, wl.frames[0].translation, p)
+    for f in wl.frames:
+        polys_frame, _ = b.frame(f.points, f.rotation, f.translation)
+    assert format_polygons(polys_run) == format_polygons(polys_frame)
