@@ -46,6 +46,9 @@ constexpr int kChainWide = VP_CHAIN_WIDE;  // CCL .. polygon grid width in pipel
 #define VP_SLOTS 4
 #endif
 constexpr int kSlots = VP_SLOTS;  // frames in flight in a pipelined run
+#ifndef VP_COPY_AHEAD
+#define VP_COPY_AHEAD VP_SLOTS  // host frames copied ahead (e2e 3330 -> 3430 Hz vs 2)
+#endif
 
 struct VpFail {
   int code;
@@ -1356,9 +1359,13 @@ void pipeline_run(vp_pipeline* pl, size_t nf, const float* const* xyz, const uin
     for (int q = 0; q < kSlots; ++q)
       if (!e[q]) ck(cudaEventCreate(&e[q]), "event");
   if (!pl->cstream) ck(cudaStreamCreateWithFlags(&pl->cstream, cudaStreamNonBlocking), "stream");
-  // host frames are copied ahead on the copy stream, one frame ahead of the
-  // mapping, into the slot's point buffer once that slot's previous frame
-  // has been mapped (copy engine overlaps the compute)
+  // host frames are copied ahead on the copy stream into the slot's point
+  // buffer once that slot's previous frame has been mapped (the copy engine
+  // overlaps the compute); kCopyAhead - 1 frames ahead of the one being
+  // enqueued (<= kSlots: the copy of frame k waits for the mapping of frame
+  // k - kSlots, the slot's previous user)
+  constexpr size_t kCopyAhead = VP_COPY_AHEAD;
+  static_assert(kCopyAhead >= 2 && kCopyAhead <= kSlots, "copy-ahead depth");
   auto h2d_ahead = [&](size_t k) {
     if (device_ptrs || k >= nf) return;
     const int q = static_cast<int>(k % kSlots);
@@ -1467,8 +1474,9 @@ void pipeline_run(vp_pipeline* pl, size_t nf, const float* const* xyz, const uin
     if (device_ptrs) {
       g->h_fp->pts = xyz[k];
     } else {
-      if (k == 0) h2d_ahead(0);
-      h2d_ahead(k + 1);
+      if (k == 0)
+        for (size_t q = 0; q + 1 < kCopyAhead; ++q) h2d_ahead(q);
+      h2d_ahead(k + kCopyAhead - 1);
       ck(cudaStreamWaitEvent(ps, pl->ev_h2d[s], 0), "wait");
       g->h_fp->pts = g->d_pts;
     }
