@@ -12,7 +12,10 @@ constexpr int kScanItems = 8;
 constexpr int kScanPerBlock = kScanThreads * kScanItems;  // 2048
 constexpr int kClusterBins = 2048;  // clusters handled by the counting sort per pass
 constexpr int kChunk = 256;         // ordinals per counting-sort chunk (one warp)
-constexpr int kHullSmem = 512;      // survivors sorted in shared memory (6 regions of this size)
+#ifndef VP_HULL_SMEM
+#define VP_HULL_SMEM 1024
+#endif
+constexpr int kHullSmem = VP_HULL_SMEM;  // survivors sorted in shared memory (6 regions of this size)
 constexpr int kPolyChunk = 1024;    // inlier points per polygon-stage block
 #ifndef VP_FOLD_SMALL
 #define VP_FOLD_SMALL 24
