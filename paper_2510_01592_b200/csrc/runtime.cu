@@ -1338,15 +1338,16 @@ void run_part_graph(vp_pipeline* pl, int part, cudaStream_t st, F&& enqueue) {
 
 // run_frames (pipeline.cpp:157-245) over a whole stream with kSlots frames in
 // flight. Per frame k:
-//   mstream  map_pre(k)  DDA walks || point grouping   after map_post(k-1)
+//   pstream  map_pre(k)  DDA walks || point grouping   after map_post(k-1)
 //   mstream  map_post(k) clear, fold, recenter          after readers(k-1), map_pre(k)
 //   mstream  readers(k)  occupied scan .. ordinal map
 //   slot     chain(k)    CCL .. polygons                 overlaps later frames
-// The critical path is mapping + readers per frame; the chains fill the
-// rest of the GPU. (VP_MAP_SPLIT=1 moves map_pre to its own stream so the
-// walks of frame k+1 overlap frame k's readers: slower on C2, the GPU is
-// already saturated.) Capacities are sized from the occupancy bound before
-// enqueueing, so the host never waits per frame.
+// The first half of the mapping touches no cell, so the walks of frame k+1
+// run while frame k's readers scan the grid; the critical path is map_post +
+// readers per frame, the chains (capped at kChainWide blocks) fill the rest of
+// the GPU. VP_MAP_SPLIT=0 puts both halves on the mapping stream (A/B).
+// Capacities are sized from the occupancy bound before enqueueing, so the
+// host never waits per frame.
 void pipeline_run(vp_pipeline* pl, size_t nf, const float* const* xyz, const uint64_t* n,
                   const double* R, const double* t, bool device_ptrs, vp_frame_timing* timings) {
   vp_grid* g = pl->grid;
@@ -1395,11 +1396,11 @@ void pipeline_run(vp_pipeline* pl, size_t nf, const float* const* xyz, const uin
   g->use_seg(0);
   ck(cudaStreamSynchronize(g->stream), "sync");
   const bool graphs = !g_prof_on && !std::getenv("VP_NO_GRAPH");
-  // VP_MAP_SPLIT=1: the mapping's first half on its own stream, overlapping
-  // the previous frame's grid readers (measured slower on C2: the DDA walks
-  // then contend with the critical path), else both halves on the mapping stream
+  // the mapping's first half on its own stream (C2 3610 -> 3760 Hz with four
+  // frames in flight and capped chains; with three and full-width chains it
+  // was slower), VP_MAP_SPLIT=0: both halves on the mapping stream
   const char* split_env = std::getenv("VP_MAP_SPLIT");
-  const cudaStream_t ps = (split_env && split_env[0] == '1') ? g->pstream : g->mstream;
+  const cudaStream_t ps = (split_env && split_env[0] == '0') ? g->mstream : g->pstream;
   // frame k-kSlots's slot is reused by frame k: its whole chain must be done
   auto harvest = [&](size_t k) {
     const int s = static_cast<int>(k % kSlots);
