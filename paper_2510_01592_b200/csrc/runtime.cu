@@ -43,7 +43,7 @@ constexpr int kThreads = 256;
 #endif
 constexpr int kChainWide = VP_CHAIN_WIDE;  // CCL .. polygon grid width in pipelined runs
 #ifndef VP_SLOTS
-#define VP_SLOTS 4
+#define VP_SLOTS 6
 #endif
 constexpr int kSlots = VP_SLOTS;  // frames in flight in a pipelined run
 #ifndef VP_COPY_AHEAD
