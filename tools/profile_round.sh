@@ -6,7 +6,7 @@ cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
 TAG=${TAG:-r01}
 timeout 900 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.log
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-configs \
   > gpurun_out/${TAG}_launch.log 2>&1
 timeout 1200 ncu --set full --clock-control none --import-source on \
