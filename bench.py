@@ -48,6 +48,28 @@ def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
+C2_WORKLOAD = "C2: stair5+stepping stones, 30x640x480 depth frames, 0.01 m, 500^3"
+
+
+def c2_config(nf, npoints, world):
+    """`config` of the C2 line -- identical in both arms (same frames, same step)."""
+    return {"workload": C2_WORKLOAD, "frames_per_step": nf, "points_per_step": int(npoints),
+            "resolution_m": 0.01, "extent": [500, 500, 500], "seed": 2025,
+            "step": "one pass over the 30-frame stream from an empty map",
+            "l2": "B200 arm: 256 MiB write between steps (> 126 MB L2)",
+            "parallelism": f"replicas x{world}" if world > 1 else "single"}
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 # ----------------------------------------------------------------- clocks
 class ClockSampler:
     """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
@@ -240,10 +262,15 @@ def run_ours(args, rank, world, dist):
         total_ms = sum(times)
     value = world * nf * args.steps / (total_ms / 1e3)
 
-    # e2e through the public C ABI: pinned host points (H2D inside the call),
-    # final polygons copied back (PipelineResult::polygons)
+    # e2e through the public C ABI (vp_pipeline_run_frames): pinned host
+    # points (H2D inside the call), every frame's polygons handed to the host
+    # (run_frames' per-frame polygons; packed on the device into mapped host
+    # memory) plus the final frame's (PipelineResult::polygons)
     e2e_times = []
     d2h_bytes = 0
+    ex = native.RunOutputs()
+    pf = (C.POINTER(native.Polygons) * nfr)()
+    ex.per_frame = C.cast(pf, C.POINTER(C.POINTER(native.Polygons)))
     for s in range(max(1, args.steps)):
         reset()
         flush.fill_(1.0)
@@ -253,20 +280,42 @@ def run_ours(args, rank, world, dist):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        # the C ABI call returns with the polygons in host memory (its D2H
-        # inside); the Python dict conversion after e1 is wrapper work
-        raw = pl.run_ptrs(host_ptrs, n_all, R_all, t_all, device_ptrs=False, want_polygons=True, convert=False)
+        # the C ABI call returns with every frame's polygons in host memory;
+        # the Python dict conversion after e1 is wrapper work
+        raw = C.POINTER(native.Polygons)()
+        native.check(L.vp_pipeline_run_frames(pl.h, C.c_size_t(nfr), host_ptrs, n_all.ctypes.data_as(
+            C.POINTER(C.c_uint64)), R_all.ctypes.data_as(C.POINTER(C.c_double)),
+            t_all.ctypes.data_as(C.POINTER(C.c_double)), C.c_int(0), C.byref(raw), C.byref(ex)))
         e1.record(stream)
         e1.synchronize()
-        polys = native.polygons_to_py(raw)
+        native.polygons_to_py(raw)
+        per = [native.polygons_to_py(pf[k]) for k in range(nfr)]
         e2e_times.append(e0.elapsed_time(e1) / 1e3)
-        d2h_bytes = sum(40 + 8 + 40 * len(p["v3d"]) for p in polys) + 128 * nf
+        d2h_bytes = sum(8 * (4 + 12 * len(ps) + 5 * sum(len(p["v3d"]) for p in ps)) for ps in per)
     e2e_total = sum(e2e_times)
     if dist:
         t = torch.tensor([e2e_total], device=f"cuda:{dev}", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_total = float(t.item())
     e2e_value = world * nf * len(e2e_times) / e2e_total
+    # per-frame latency (SURVEY §8(d) unit of work): one frame in flight, as a
+    # robot streaming at sensor rate sees it -- vp_pipeline_frame from pinned
+    # host points (H2D start) to the frame's polygons in host memory, CUDA
+    # events on the library stream; median of frames 2..F of a pass from an
+    # empty map
+    lat = []
+    for rep in range(2):
+        reset()
+        torch.cuda.synchronize()
+        for k, f in enumerate(frames):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            polys, _ = pl.frame_ptr(host_pts[k].data_ptr(), npts[k], f.rotation, f.translation, want_polygons=True)
+            e1.record(stream)
+            e1.synchronize()
+            if rep == 1 and k >= 2:
+                lat.append(e0.elapsed_time(e1))
     clk.__exit__(None, None, None)
 
     # per-kernel profile of one step (serialised launches; shares only)
@@ -299,13 +348,24 @@ def run_ours(args, rank, world, dist):
         pass
     peak, peak_source = hbm_peak(peaks)
     achieved = per_launch_bytes / per_launch_s / 1e9
-    traffic, limiter = None, None
-    try:  # DRAM bytes and pipe utilisation of the same kernel from the committed ncu --set full capture
+    traffic, limiter, winst, atomics = None, None, None, None
+    try:  # DRAM bytes, pipe utilisation, instructions, atomics of the same kernel (committed ncu --set full)
         nt = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
         traffic = nt["dram_bytes_per_launch"].get(top)
         limiter = nt.get("utilisation_pct", {}).get(top)
+        winst = nt.get("warp_inst_per_launch", {}).get(top)
+        atomics = nt.get("atomics_per_launch", {}).get(top)
     except Exception:
         pass
+    # issue roofline of the same kernel: its warp instructions per launch
+    # (ncu) / the live launch duration, against 148 SMs x 4 schedulers x 1
+    # warp instruction per cycle at the sampled SM clock
+    sm_hz = (clk.summary().get("sm_mhz") or 1965.0) * 1e6
+    issue = None
+    if winst:
+        peak_i = 148 * 4 * sm_hz
+        issue = {"warp_inst_per_launch": winst, "achieved_ginst_s": round(winst / per_launch_s / 1e9, 1),
+                 "peak_ginst_s": round(peak_i / 1e9, 1), "frac": round(winst / per_launch_s / peak_i, 4)}
     # DDA cell steps of the step's frames, estimated as the L1 cell distance
     # sensor -> end point (k_dda_keys' length model; the window clip ignored)
     dda_steps = 0.0
@@ -334,18 +394,19 @@ def run_ours(args, rank, world, dist):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (library frame source = reference render_frame, byte-identical)",
-        "config": {"workload": "C2: stair5+stepping stones, 30x640x480 depth frames, 0.01 m, 500^3",
-                   "frames_per_step": nf, "points_per_step": sum(npts), "resolution_m": wl.resolution,
-                   "extent": list(wl.extent), "seed": wl.seed, "l2": "flushed (256 MiB write) between steps",
-                   "parallelism": f"replicas x{world}" if world > 1 else "single"},
+        "config": c2_config(nf, sum(npts), world),
         "gpu_launches": int(launches),
+        "latency_ms_p50": round(statistics.median(lat), 4),
+        "latency_ms_p90": round(sorted(lat)[int(0.9 * (len(lat) - 1))], 4),
+        "latency": "one frame in flight (vp_pipeline_frame): pinned host points -> polygons on the host, "
+                   "CUDA events, frames 2..29 of a pass from an empty map",
         "e2e": {"value": round(e2e_value, 3), "unit": "Hz",
                 "h2d_bytes_per_step": int(12 * sum(npts)), "d2h_bytes_per_step": int(d2h_bytes)},
         "roofline": {"bound": "hbm", "kernel": top, "achieved": round(achieved, 2), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 5), "traffic": traffic,
                      "alg_bytes_per_launch": round(per_launch_bytes), "us_per_launch": round(per_launch_s * 1e6, 2),
                      "share_of_step": round(top_ms / prof_total, 4), "peak_source": peak_source,
-                     "utilisation_pct_ncu": limiter,
+                     "utilisation_pct_ncu": limiter, "issue": issue, "atomics_ncu": atomics,
                      # secondary rate of the DDA: cell steps per second
                      "dda_steps_per_launch_est": round(dda_steps / len(frames)) if top == "k_clear_walk" else None,
                      "dda_gsteps_per_s": (round(dda_steps / len(frames) / per_launch_s / 1e9, 1)
@@ -355,7 +416,7 @@ def run_ours(args, rank, world, dist):
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(wl, args.cpu_frames)
+        out["cpu_baseline"] = cpu_baseline(args.cpu_frames)
     if rank == 0 and world == 1 and not args.no_configs:
         # the other BASELINE configs on this GPU (secondary lines; C1 is the
         # reference's 0.05 m CPU case, C5 the multi-GPU map as one slab)
@@ -597,80 +658,137 @@ def ref_lib():
         raise FileNotFoundError(path)
     L = C.CDLL(path)
     L.ref_session_create.restype = C.c_void_p
+    dp, ip = C.POINTER(C.c_double), C.POINTER(C.c_int)
+    L.ref_stock_scene.argtypes = [C.c_int, dp, ip, dp, ip]
+    L.ref_default_trajectory.argtypes = [C.c_int, C.c_int, C.c_double, dp]
+    L.ref_render.argtypes = [dp, C.c_int, dp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
+                             C.POINTER(C.c_float), C.c_int, C.c_double, C.c_double, C.c_double, dp, C.c_int,
+                             C.c_uint64, C.c_char_p]
     return L, kind
 
 
-def cpu_baseline(wl, nframes):
-    """oracle/_ref (unmodified reference sources) on the host cores: the first
-    `nframes` frames of the stream from an empty map, all host threads."""
+def ref_workload_c2(L):
+    """The C2 stream built and rendered by the reference itself (oracle/_ref:
+    build_scene Stair5 + the six stepping-stone boxes, default_trajectory,
+    render_frame, write_frames_binary), read back as VXPF -- the reference arm
+    never loads this repository's library. Byte-identical to the B200 arm's
+    frames (tests/test_oracle.py::test_reference_arm_frames_match)."""
+    import tempfile
+
     import numpy as np
 
-    from paper_2510_01592_b200 import native
+    from paper_2510_01592_b200.frames import read_frames
+    from paper_2510_01592_b200.scenes import stepping_stone_boxes
+    dp = C.POINTER(C.c_double)
+    boxes, rects = np.zeros(6 * 64), np.zeros(14 * 64)
+    nb, nr = C.c_int(), C.c_int()
+    L.ref_stock_scene(0, boxes.ctypes.data_as(dp), C.byref(nb), rects.ctypes.data_as(dp), C.byref(nr))
+    for i, (lo, hi) in enumerate(stepping_stone_boxes()):
+        boxes[6 * (nb.value + i):6 * (nb.value + i + 1)] = (*lo, *hi)
+    nbox = nb.value + len(stepping_stone_boxes())
+    poses = np.zeros((32, 12))
+    nf = L.ref_default_trajectory(0, 30, 30.0, poses.ctypes.data_as(dp))
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "c2.vxpf")
+        rc = L.ref_render(boxes.ctypes.data_as(dp), nbox, rects.ctypes.data_as(dp), nr.value, 0, 640, 480,
+                          87.0, 58.0, None, 0, 30.0, 6.0, 0.003, poses.ctypes.data_as(dp), nf, 2025,
+                          path.encode())
+        if rc != 0:
+            raise RuntimeError("ref_render failed")
+        return read_frames(path)
+
+
+def _ref_step(L, s, f):
+    import numpy as np
+    ms = C.c_double()
+    npoly = C.c_uint64()
+    pts = np.ascontiguousarray(f.points)
+    R = np.ascontiguousarray(f.rotation, np.float64).reshape(9)
+    t = np.ascontiguousarray(f.translation, np.float64)
+    rc = L.ref_session_step(C.c_void_p(s), pts.ctypes.data_as(C.POINTER(C.c_float)), C.c_uint64(len(pts)),
+                            R.ctypes.data_as(C.POINTER(C.c_double)), t.ctypes.data_as(C.POINTER(C.c_double)),
+                            C.byref(ms), C.byref(npoly))
+    if rc != 0:
+        raise RuntimeError("ref_session_step failed")
+    return ms.value
+
+
+def _ref_session(L, frames):
+    import numpy as np
+
+    from paper_2510_01592_b200.native import default_params  # a ctypes struct: loads no library
+    p = default_params(seed=2025)
+    ext = np.asarray((500, 500, 500), np.int32)
+    c = np.ascontiguousarray(frames[0].translation, np.float64)
+    return L.ref_session_create(C.c_double(0.01), ext.ctypes.data_as(C.POINTER(C.c_int32)),
+                                c.ctypes.data_as(C.POINTER(C.c_double)), C.byref(p)), p
+
+
+def cpu_baseline(nframes):
+    """oracle/_ref (unmodified reference sources) on the host cores: the first
+    `nframes` frames of the C2 stream from an empty map, all host threads."""
     L, kind = ref_lib()
     cores = os.cpu_count()
     L.ref_set_threads(cores)
-    p = native.default_params(seed=wl.seed)
-    ext = np.asarray(wl.extent, np.int32)
-    c = np.ascontiguousarray(wl.frames[0].translation, np.float64)
-    s = L.ref_session_create(C.c_double(wl.resolution), ext.ctypes.data_as(C.POINTER(C.c_int32)),
-                             c.ctypes.data_as(C.POINTER(C.c_double)), C.byref(p))
-    total = 0.0
-    for f in wl.frames[:nframes]:
-        ms = C.c_double()
-        npoly = C.c_uint64()
-        pts = np.ascontiguousarray(f.points)
-        R = np.ascontiguousarray(f.rotation, np.float64).reshape(9)
-        t = np.ascontiguousarray(f.translation, np.float64)
-        L.ref_session_step(C.c_void_p(s), pts.ctypes.data_as(C.POINTER(C.c_float)), C.c_uint64(len(pts)),
-                           R.ctypes.data_as(C.POINTER(C.c_double)), t.ctypes.data_as(C.POINTER(C.c_double)),
-                           C.byref(ms), C.byref(npoly))
-        total += ms.value
+    frames = ref_workload_c2(L)
+    s, _ = _ref_session(L, frames)
+    total = sum(_ref_step(L, s, f) for f in frames[:nframes])
     L.ref_session_destroy(C.c_void_p(s))
     return {"value": round(nframes / (total / 1e3), 4), "unit": "Hz", "cores": cores, "kind": kind,
+            "cpu_model": cpu_model(),
             "sample": f"first {nframes} frames of the C2 stream from an empty 500^3 map "
                       f"({total / 1e3:.1f} s, run_frames body, VOXPLANE threads={cores})"}
 
 
 def run_reference(args):
-    import numpy as np
-
-    from paper_2510_01592_b200 import native
-    wl = load_workload(args.workload)
+    """The reference's CPU implementation (oracle/_ref) on the same workload,
+    config and step as the B200 arm: one pass over the 30-frame C2 stream
+    from an empty map, split into `steps` consecutive groups of frames (one
+    step = one group; more steps than frames: one frame per step, the map
+    emptied at each wrap). Warm-up: `warmup` frames on a separate session."""
     L, kind = ref_lib()
     cores = os.cpu_count()
     L.ref_set_threads(cores)
-    p = native.default_params(seed=wl.seed)
-    ext = np.asarray(wl.extent, np.int32)
-    c = np.ascontiguousarray(wl.frames[0].translation, np.float64)
-    s = L.ref_session_create(C.c_double(wl.resolution), ext.ctypes.data_as(C.POINTER(C.c_int32)),
-                             c.ctypes.data_as(C.POINTER(C.c_double)), C.byref(p))
-    # one step = one frame of the stream (cycling), on a persistent map
-    nf = len(wl.frames)
-    times = []
-    for i in range(args.warmup + args.steps):
-        f = wl.frames[i % nf]
-        ms = C.c_double()
-        npoly = C.c_uint64()
-        pts = np.ascontiguousarray(f.points)
-        R = np.ascontiguousarray(f.rotation, np.float64).reshape(9)
-        t = np.ascontiguousarray(f.translation, np.float64)
-        L.ref_session_step(C.c_void_p(s), pts.ctypes.data_as(C.POINTER(C.c_float)), C.c_uint64(len(pts)),
-                           R.ctypes.data_as(C.POINTER(C.c_double)), t.ctypes.data_as(C.POINTER(C.c_double)),
-                           C.byref(ms), C.byref(npoly))
-        if i >= args.warmup:
-            times.append(ms.value)
+    t0 = time.time()
+    frames = ref_workload_c2(L)
+    nf = len(frames)
+    npts = sum(len(f.points) for f in frames)
+    log(f"[bench] reference arm: C2 rendered by oracle/_ref in {time.time() - t0:.1f}s ({nf} frames)")
+    w, _ = _ref_session(L, frames)
+    for i in range(args.warmup):
+        _ref_step(L, w, frames[i % nf])
+    L.ref_session_destroy(C.c_void_p(w))
+    K = max(1, args.steps)
+    if K <= nf:
+        bounds = [round(j * nf / K) for j in range(K + 1)]
+        groups = [list(range(bounds[j], bounds[j + 1])) for j in range(K)]
+    else:
+        groups = [[j % nf] for j in range(K)]
+    s, _ = _ref_session(L, frames)
+    times, done = [], 0
+    for g in groups:
+        ms = 0.0
+        for i in g:
+            if i == 0 and done:  # next pass: a fresh (empty) map, untimed
+                L.ref_session_destroy(C.c_void_p(s))
+                s, _ = _ref_session(L, frames)
+            ms += _ref_step(L, s, frames[i])
+            done += 1
+        times.append(ms)
     L.ref_session_destroy(C.c_void_p(s))
     total = sum(times) / 1e3
-    value = len(times) / total
+    value = done / total
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    sample = (f"frames 0..{nf - 1} of C2 from an empty 500^3 map (one pass) in {K} steps"
+              if K <= nf else f"{K} frames of C2 (passes from an empty map), one per step")
     return {
-        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "Hz", "n_gpus": 1,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * total / len(times), 3),
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "Hz", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * total / K, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (same frames as the B200 arm)",
-        "config": {"workload": "C2: stair5+stepping stones, 30x640x480 depth frames, 0.01 m, 500^3",
-                   "step": "one frame update of the stream on a persistent map"},
+        "data": "synthetic (same frames as the B200 arm, rendered by the reference)",
+        "config": c2_config(nf, npts, world),
         "cpu_baseline": {"value": round(value, 4), "unit": "Hz", "cores": cores, "kind": kind,
-                         "sample": f"frames {args.warmup}..{args.warmup + args.steps - 1} (mod {nf}) of C2"},
+                         "cpu_model": cpu_model(), "sample": sample},
         "e2e": {"value": round(value, 4), "unit": "Hz", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 

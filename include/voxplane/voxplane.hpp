@@ -23,6 +23,7 @@
 #include <fstream>
 #include <numeric>
 #include <optional>
+#include <sstream>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -379,6 +380,10 @@ class VoxelGrid {
     return Vec3(c.sx, c.sy, c.sz) / static_cast<double>(c.count);
   }
   vp_grid* handle() const { return g_; }
+  /// A non-owning view of a library-owned grid (e.g. a pipeline's map).
+  static VoxelGrid borrow(vp_grid* g, double resolution, const Vec3i& extent) {
+    return VoxelGrid(g, resolution, extent);
+  }
 
  private:
   friend class Pipeline;
@@ -410,25 +415,37 @@ inline std::vector<SurfaceEstimate> estimate_normals(const VoxelGrid& grid,
   return v;
 }
 
-/// classify_steppable (segmentation.cpp:69-85) over the given estimates;
-/// statuses are written back to the device grid.
+/// classify_steppable (segmentation.cpp:69-85) over the given estimates: the
+/// predicate (valid, neighbor_count >= min_neighbors, angle_to_up_deg <=
+/// max_angle_deg) runs on the device, which also writes the statuses into the
+/// grid; the partition keeps the estimates' order.
 inline SteppablePartition classify_steppable(VoxelGrid& grid,
                                              const std::vector<SurfaceEstimate>& estimates,
                                              const SegmentationParams& params) {
-  SteppablePartition part;
-  std::vector<int32_t> idx;
-  std::vector<uint8_t> st;
-  for (const SurfaceEstimate& est : estimates) {
-    const bool steppable = est.valid && est.neighbor_count >= params.min_neighbors &&
-                           est.angle_to_up_deg <= params.max_angle_deg;
-    if (steppable)
-      part.steppable.push_back({est.voxel, est.mean, est.normal});
-    else
-      part.objects.push_back(est.voxel);
-    idx.insert(idx.end(), {est.voxel.x(), est.voxel.y(), est.voxel.z()});
-    st.push_back(steppable ? 2 : 1);
+  const size_t n = estimates.size();
+  std::vector<int32_t> idx(3 * n), nc(n);
+  std::vector<double> ang(n);
+  std::vector<uint8_t> valid(n), st(n);
+  for (size_t i = 0; i < n; ++i) {
+    const SurfaceEstimate& e = estimates[i];
+    idx[3 * i] = e.voxel.x();
+    idx[3 * i + 1] = e.voxel.y();
+    idx[3 * i + 2] = e.voxel.z();
+    nc[i] = e.neighbor_count;
+    ang[i] = e.angle_to_up_deg;
+    valid[i] = e.valid ? 1 : 0;
   }
-  detail::check(vp_set_statuses(grid.handle(), idx.data(), st.data(), st.size()));
+  const vp_seg_params sp = detail::to_c(params);
+  detail::check(vp_classify_estimates(grid.handle(), &sp, n, idx.data(), nc.data(), ang.data(), valid.data(),
+                                      st.data()));
+  SteppablePartition part;
+  for (size_t i = 0; i < n; ++i) {
+    const SurfaceEstimate& e = estimates[i];
+    if (st[i] == 2)
+      part.steppable.push_back({e.voxel, e.mean, e.normal});
+    else
+      part.objects.push_back(e.voxel);
+  }
   return part;
 }
 
@@ -468,28 +485,15 @@ inline Adjacency build_adjacency(const std::vector<SteppablePoint>& steppable,
   return adj;
 }
 
-/// label_components (segmentation.cpp:147-194) on a given adjacency: the
-/// canonical component-minimum labels (a union-find over the lists).
-inline ClusterSet label_components(const std::vector<SteppablePoint>& steppable,
-                                   const Adjacency& adjacency) {
-  const size_t n = steppable.size();
-  std::vector<int32_t> parent(n);
-  std::iota(parent.begin(), parent.end(), 0);
-  auto find = [&](int32_t x) {
-    while (parent[x] != x) x = parent[x] = parent[parent[x]];
-    return x;
-  };
-  for (size_t i = 0; i < n; ++i)
-    for (int32_t j : adjacency[i]) {
-      int32_t a = find(static_cast<int32_t>(i)), b = find(j);
-      if (a != b) parent[a < b ? b : a] = a < b ? a : b;
-    }
+namespace detail {
+// ClusterSet from canonical labels: clusters in ascending label order,
+// members in ascending ordinal (segmentation.cpp:182-193)
+inline ClusterSet group_labels(const std::vector<SteppablePoint>& steppable, std::vector<int32_t> labels) {
   ClusterSet set;
-  set.labels.resize(n);
+  const size_t n = steppable.size();
   std::vector<int64_t> slot(n, -1);
   for (size_t i = 0; i < n; ++i) {
-    const int32_t l = find(static_cast<int32_t>(i));
-    set.labels[i] = l;
+    const int32_t l = labels[i];
     if (slot[l] < 0) {
       slot[l] = static_cast<int64_t>(set.clusters.size());
       set.clusters.emplace_back();
@@ -497,7 +501,25 @@ inline ClusterSet label_components(const std::vector<SteppablePoint>& steppable,
     }
     set.clusters[slot[l]].members.push_back(steppable[i]);
   }
+  set.labels = std::move(labels);
   return set;
+}
+}  // namespace detail
+
+/// label_components (segmentation.cpp:147-194) on a given adjacency: a
+/// device union-find over the lists; labels are the canonical component
+/// minima.
+inline ClusterSet label_components(const std::vector<SteppablePoint>& steppable,
+                                   const Adjacency& adjacency, int device = 0) {
+  const size_t n = steppable.size();
+  std::vector<uint64_t> rows(n + 1, 0);
+  for (size_t i = 0; i < n; ++i) rows[i + 1] = rows[i] + adjacency[i].size();
+  std::vector<int32_t> cols;
+  cols.reserve(rows[n]);
+  for (const auto& l : adjacency) cols.insert(cols.end(), l.begin(), l.end());
+  std::vector<int32_t> labels(n);
+  detail::check(vp_label_components_adjacency(n, rows.data(), cols.data(), device, labels.data()));
+  return detail::group_labels(steppable, std::move(labels));
 }
 
 /// Fused build_adjacency + label_components on the device (no adjacency lists).
@@ -615,6 +637,51 @@ inline double polygon_area(std::span<const Vec2> ring) {  // polygonize.cpp:146-
     twice += a.x() * b.y() - b.x() * a.y();
   }
   return 0.5 * twice;
+}
+
+namespace detail {
+inline std::vector<double> flat2(std::span<const Vec2> pts) {
+  std::vector<double> a(2 * pts.size());
+  for (size_t i = 0; i < pts.size(); ++i) {
+    a[2 * i] = pts[i].x();
+    a[2 * i + 1] = pts[i].y();
+  }
+  return a;
+}
+inline std::vector<Vec2> take2(double* out, uint64_t m) {
+  std::vector<Vec2> v(m);
+  for (uint64_t i = 0; i < m; ++i) v[i] = Vec2(out[2 * i], out[2 * i + 1]);
+  vp_free(out);
+  return v;
+}
+}  // namespace detail
+
+/// hull_filter (polygonize.cpp:50-114) on the device: survivors in input order.
+inline std::vector<Vec2> hull_filter(std::span<const Vec2> points, int directions = 16, int device = 0) {
+  const std::vector<double> a = detail::flat2(points);
+  double* out = nullptr;
+  uint64_t m = 0;
+  detail::check(vp_hull_filter(a.data(), points.size(), directions, device, &out, &m));
+  return detail::take2(out, m);
+}
+
+/// monotone_chain (polygonize.cpp:116-139) on the device: strict CCW hull from
+/// the lexicographic minimum, empty when all points are collinear.
+inline std::vector<Vec2> monotone_chain(std::span<const Vec2> points, int device = 0) {
+  const std::vector<double> a = detail::flat2(points);
+  double* out = nullptr;
+  uint64_t m = 0;
+  detail::check(vp_monotone_chain(a.data(), points.size(), device, &out, &m));
+  return detail::take2(out, m);
+}
+
+/// convex_hull (polygonize.cpp:141-144): hull_filter then monotone_chain.
+inline std::vector<Vec2> convex_hull(std::span<const Vec2> points, int directions = 16, int device = 0) {
+  const std::vector<double> a = detail::flat2(points);
+  double* out = nullptr;
+  uint64_t m = 0;
+  detail::check(vp_convex_hull(a.data(), points.size(), directions, device, &out, &m));
+  return detail::take2(out, m);
 }
 
 inline bool point_in_convex(std::span<const Vec2> ring, const Vec2& p, double slack = 0.0) {
@@ -762,6 +829,103 @@ inline std::vector<SensorFrame> read_frames_binary(const std::string& path) {
   return frames;
 }
 
+/// quantize_pose (frame_io.cpp:64-72): the pose through the file format's f32.
+inline Pose quantize_pose(const Pose& pose) {
+  Pose q;
+  for (int r = 0; r < 3; ++r) {
+    for (int c = 0; c < 3; ++c) q.rotation(r, c) = static_cast<double>(static_cast<float>(pose.rotation(r, c)));
+    q.translation[r] = static_cast<double>(static_cast<float>(pose.translation[r]));
+  }
+  return q;
+}
+
+/// write_frames_binary (frame_io.cpp:74-89): a VXPF stream.
+inline void write_frames_binary(const std::string& path, const std::vector<SensorFrame>& frames) {
+  std::vector<const float*> xyz(frames.size());
+  std::vector<uint64_t> n(frames.size());
+  std::vector<double> R(9 * frames.size()), t(3 * frames.size());
+  for (size_t k = 0; k < frames.size(); ++k) {
+    xyz[k] = detail::frame_xyz(frames[k]);
+    n[k] = frames[k].points.size();
+    detail::pose_arrays(frames[k].pose, &R[9 * k], &t[3 * k]);
+  }
+  const int rc = vp_write_frames_binary(path.c_str(), frames.size(), xyz.data(), n.data(), R.data(), t.data());
+  if (rc != VP_OK) throw OutputError(vp_last_error());
+}
+
+/// write_frames_text / read_frames_text (frame_io.cpp:118-196): the
+/// hand-written fixture format ("frame n", "pose" + 12 numbers, n "x y z").
+inline void write_frames_text(const std::string& path, const std::vector<SensorFrame>& frames) {
+  std::ofstream os(path);
+  if (!os) throw OutputError("frame stream: cannot open for write: " + path);
+  char buf[96];
+  for (const SensorFrame& f : frames) {
+    os << "frame " << f.points.size() << '\n' << "pose";
+    for (int r = 0; r < 3; ++r) {
+      std::snprintf(buf, sizeof buf, " %.9g %.9g %.9g %.9g", f.pose.rotation(r, 0), f.pose.rotation(r, 1),
+                    f.pose.rotation(r, 2), f.pose.translation[r]);
+      os << buf;
+    }
+    os << '\n';
+    for (const Vec3f& p : f.points) {
+      std::snprintf(buf, sizeof buf, "%.9g %.9g %.9g\n", static_cast<double>(p.x()), static_cast<double>(p.y()),
+                    static_cast<double>(p.z()));
+      os << buf;
+    }
+  }
+  if (!os) throw OutputError("frame stream: write failed: " + path);
+}
+
+namespace detail {
+inline bool content_line(std::istream& is, std::string& line) {
+  while (std::getline(is, line)) {
+    const size_t i = line.find_first_not_of(" \t\r");
+    if (i == std::string::npos || line[i] == '#') continue;
+    return true;
+  }
+  return false;
+}
+}  // namespace detail
+
+inline std::vector<SensorFrame> read_frames_text(const std::string& path) {
+  std::ifstream is(path);
+  if (!is) throw MissingInputError("frame stream: cannot open: " + path);
+  std::vector<SensorFrame> frames;
+  std::string line;
+  while (detail::content_line(is, line)) {
+    std::istringstream h(line);
+    std::string kw;
+    size_t n = 0;
+    h >> kw >> n;
+    if (kw != "frame" || !h) throw std::runtime_error("frame stream: expected 'frame <count>' in " + path);
+    if (!detail::content_line(is, line)) throw std::runtime_error("frame stream: missing pose line in " + path);
+    std::istringstream ps(line);
+    ps >> kw;
+    if (kw != "pose") throw std::runtime_error("frame stream: expected 'pose' in " + path);
+    SensorFrame f;
+    for (int r = 0; r < 3; ++r) {
+      double v[4];
+      ps >> v[0] >> v[1] >> v[2] >> v[3];
+      for (int c = 0; c < 3; ++c) f.pose.rotation(r, c) = v[c];
+      f.pose.translation[r] = v[3];
+    }
+    if (!ps) throw std::runtime_error("frame stream: malformed pose in " + path);
+    f.points.resize(n);
+    for (size_t i = 0; i < n; ++i) {
+      if (!detail::content_line(is, line))
+        throw std::runtime_error("frame stream: truncated point list in " + path);
+      std::istringstream vs(line);
+      float x, y, z;
+      vs >> x >> y >> z;
+      if (!vs) throw std::runtime_error("frame stream: malformed point in " + path);
+      f.points[i] = Vec3f(x, y, z);
+    }
+    f.timestamp = static_cast<double>(frames.size());
+    frames.push_back(std::move(f));
+  }
+  return frames;
+}
+
 /// write_polygons (polygon_io.cpp:30-47): the golden-file format.
 inline void write_polygons(const std::string& path, const std::vector<PlanePolygon>& polygons) {
   std::ofstream os(path);
@@ -784,6 +948,65 @@ inline void write_polygons(const std::string& path, const std::vector<PlanePolyg
     os << "inliers " << p.plane.inlier_count << '\n';
   }
   if (!os) throw OutputError("polygons: write failed: " + path);
+}
+
+/// read_polygons (polygon_io.cpp:50-127): the golden-file format back; the
+/// in-plane ring is recomputed from the 3-D vertices with plane_basis.
+inline std::vector<PlanePolygon> read_polygons(const std::string& path) {
+  std::ifstream is(path);
+  if (!is) throw MissingInputError("polygons: cannot open: " + path);
+  std::vector<PlanePolygon> out;
+  std::string line;
+  auto field = [&](const char* name) {
+    if (!detail::content_line(is, line))
+      throw std::runtime_error(std::string("polygons: missing '") + name + "' in " + path);
+    std::istringstream ss(line);
+    std::string kw;
+    ss >> kw;
+    if (kw != name)
+      throw std::runtime_error(std::string("polygons: expected '") + name + "', got '" + kw + "' in " + path);
+    return ss;
+  };
+  while (detail::content_line(is, line)) {
+    std::istringstream h(line);
+    std::string kw;
+    h >> kw;
+    if (kw != "polygon") throw std::runtime_error("polygons: expected 'polygon' in " + path);
+    PlanePolygon p;
+    {
+      auto ss = field("normal");
+      ss >> p.plane.normal.x() >> p.plane.normal.y() >> p.plane.normal.z();
+      if (!ss) throw std::runtime_error("polygons: malformed normal in " + path);
+    }
+    {
+      auto ss = field("offset");
+      ss >> p.plane.offset;
+      if (!ss) throw std::runtime_error("polygons: malformed offset in " + path);
+    }
+    size_t k = 0;
+    {
+      auto ss = field("vertices");
+      ss >> k;
+      if (!ss) throw std::runtime_error("polygons: malformed vertex count in " + path);
+    }
+    p.vertices3d.resize(k);
+    for (size_t i = 0; i < k; ++i) {
+      if (!detail::content_line(is, line)) throw std::runtime_error("polygons: truncated vertex list in " + path);
+      std::istringstream vs(line);
+      vs >> p.vertices3d[i].x() >> p.vertices3d[i].y() >> p.vertices3d[i].z();
+      if (!vs) throw std::runtime_error("polygons: malformed vertex in " + path);
+    }
+    field("area") >> p.area;
+    field("label") >> p.plane.cluster_label;
+    field("inliers") >> p.plane.inlier_count;
+    const PlaneBasis b = plane_basis(p.plane);
+    for (const Vec3& v : p.vertices3d) {
+      const Vec3 d = v - b.origin;
+      p.vertices2d.emplace_back(d.dot(b.u), d.dot(b.v));
+    }
+    out.push_back(std::move(p));
+  }
+  return out;
 }
 
 }  // namespace voxplane

@@ -221,6 +221,35 @@ int vp_make_polygons(size_t n, const vp_plane* planes, const uint64_t* offsets,
                      vp_polygons_t** out);
 void vp_polygons_free(vp_polygons_t* p);
 
+/* ---- reference-named utilities on the device ----------------------------- */
+/* jacobi_eigen_sym3 (jacobi.hpp:10-18, jacobi.cpp:46-81) for n symmetric 3x3
+   matrices a (row-major, 9 each): eigenvalues ascending (3 each),
+   eigenvectors column-major (9 each; column k pairs with eigenvalue k,
+   right-handed). The kernel is the one estimate_normals runs. */
+int vp_jacobi_eigen_sym3(size_t n, const double* a, double* eigenvalues, double* eigenvectors, int device);
+/* hull_filter (polygonize.hpp:32-33, polygonize.cpp:50-114): the points
+   (n x 2) not strictly inside the polygon of the extremes along `directions`
+   directions, in input order; *out (m x 2) is freed with vp_free. */
+int vp_hull_filter(const double* pts, uint64_t n, int directions, int device, double** out, uint64_t* m);
+/* monotone_chain (polygonize.hpp:34-37, polygonize.cpp:116-139): strict CCW
+   hull from the lexicographic minimum, empty when collinear. */
+int vp_monotone_chain(const double* pts, uint64_t n, int device, double** out, uint64_t* m);
+/* convex_hull (polygonize.hpp:38-39, polygonize.cpp:141-144): hull_filter
+   then monotone_chain. */
+int vp_convex_hull(const double* pts, uint64_t n, int directions, int device, double** out, uint64_t* m);
+/* label_components(steppable, adjacency) (segmentation.hpp:74-75,
+   segmentation.cpp:147-194) over explicit adjacency lists in CSR form
+   (row_offsets n + 1, cols): labels[i] = component-minimum ordinal. */
+int vp_label_components_adjacency(uint64_t n, const uint64_t* row_offsets, const int32_t* cols, int device,
+                                  int32_t* labels);
+/* classify_steppable(grid, estimates, params) (segmentation.hpp:68-70,
+   segmentation.cpp:69-85) over caller-provided estimates (voxel indices
+   n x 3, neighbor_count, angle_to_up_deg, valid): status[i] = 2 (Steppable)
+   or 1 (Occupied), written to the grid's cells as well. */
+int vp_classify_estimates(vp_grid* g, const vp_seg_params* p, size_t n, const int32_t* idx,
+                          const int32_t* neighbor_count, const double* angle_to_up_deg, const uint8_t* valid,
+                          uint8_t* status);
+
 /* ---- composite ----------------------------------------------------------- */
 /* segment(): voxel_frame_polygons (pipeline.cpp:43-85) on the device-resident
    grid: polygons in ascending cluster-label order, area-filtered. */
@@ -347,6 +376,24 @@ int vp_pipeline_frame_device(vp_pipeline* pl, const float* xyz_dev, uint64_t n,
 int vp_pipeline_run(vp_pipeline* pl, size_t n_frames, const float* const* xyz, const uint64_t* n,
                     const double* rotations, const double* translations, int device_ptrs,
                     vp_polygons_t** out, vp_frame_timing* timings);
+/* Per-frame outputs of a pipelined run; every member is optional (NULL) and
+   points at n_frames entries. per_frame[k] receives frame k's polygons
+   (run_frames' per_frame_polygons, pipeline.cpp:223-227; free each with
+   vp_polygons_free); timings[k] its FrameTiming stage spans (pipeline.cpp:
+   181-219, CUDA-event ms); traces[k] / trace_lens[k] its stage trace
+   (voxplane_trace.h, as vp_pipeline_frame_trace; free with vp_free). */
+typedef struct {
+  vp_polygons_t** per_frame;
+  vp_frame_timing* timings;
+  uint8_t** traces;
+  uint64_t* trace_lens;
+} vp_run_outputs;
+/* vp_pipeline_run with per-frame outputs: the body of run_frames
+   (pipeline.cpp:157-245) with frames in flight; every frame's polygons are
+   packed on the device into mapped host memory (no copy, no stream wait). */
+int vp_pipeline_run_frames(vp_pipeline* pl, size_t n_frames, const float* const* xyz, const uint64_t* n,
+                           const double* rotations, const double* translations, int device_ptrs,
+                           vp_polygons_t** out, const vp_run_outputs* extra);
 /* Same frame step, returning the stage trace (voxplane_trace.h); buf is
    freed with vp_free. */
 int vp_pipeline_frame_trace(vp_pipeline* pl, const float* xyz, uint64_t n,

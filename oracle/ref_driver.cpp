@@ -101,6 +101,7 @@ struct Session {
   vp_pipeline_params params;
   Vec3i last_cell;
   uint32_t frame = 0;
+  bool fixed = false;  // fixed window, never recentered
   Session(double res, const Vec3i& ext, const Vec3& c, const vp_pipeline_params& p)
       : grid(res, ext, c), params(p), last_cell(global_cell(c, res)) {}
 };
@@ -127,6 +128,10 @@ void* ref_session_create(double res, const int32_t ext[3], const double center[3
 
 void ref_session_destroy(void* s) { delete static_cast<Session*>(s); }
 
+// Fixed-window mode: clear_rays + integrate_frame + voxel_frame_polygons per
+// frame with no recenter (the C5 map and the slab path).
+void ref_session_set_fixed(void* s, int fixed) { static_cast<Session*>(s)->fixed = fixed != 0; }
+
 // One run_frames iteration (pipeline.cpp:199-213) with every stage of
 // voxel_frame_polygons (pipeline.cpp:43-85) serialised.
 int ref_session_frame(void* sp, const float* xyz, uint64_t n, const double R[9], const double t[3],
@@ -145,7 +150,7 @@ int ref_session_frame(void* sp, const float* xyz, uint64_t n, const double R[9],
     const Vec3i cell = global_cell(frame.pose.translation, res);
     ShiftStats ss;
     uint8_t recentered = 0;
-    if (cell != s->last_cell) {
+    if (!s->fixed && cell != s->last_cell) {
       ss = s->grid.recenter(frame.pose.translation);
       s->last_cell = cell;
       recentered = 1;
@@ -263,7 +268,7 @@ int ref_session_step(void* sp, const float* xyz, uint64_t n, const double R[9], 
     s->grid.clear_rays(frame);
     s->grid.integrate_frame(frame);
     const Vec3i cell = global_cell(frame.pose.translation, s->grid.resolution());
-    if (cell != s->last_cell) {
+    if (!s->fixed && cell != s->last_cell) {
       s->grid.recenter(frame.pose.translation);
       s->last_cell = cell;
     }
@@ -499,6 +504,64 @@ int ref_rosette_pattern(int n, float* out) {
   for (int i = 0; i < n; ++i)
     for (int k = 0; k < 3; ++k) out[3 * i + k] = v[i][k];
   return n;
+}
+
+}  // extern "C"
+
+// ---- reference utilities for the drop-in API checks (TEST INFRASTRUCTURE) ----
+#include "voxplane/jacobi.hpp"
+#include "voxplane/rng.hpp"
+
+extern "C" {
+
+// hull_filter / monotone_chain / convex_hull (polygonize.cpp:50-144):
+// op 0 / 1 / 2 on n 2-D points; out has room for 2n doubles.
+int ref_hull(int op, const double* pts, uint64_t n, int directions, double* out, uint64_t* m) {
+  std::vector<Vec2> p(n);
+  for (uint64_t i = 0; i < n; ++i) p[i] = Vec2(pts[2 * i], pts[2 * i + 1]);
+  const std::vector<Vec2> r = op == 0 ? hull_filter(p, directions) : op == 1 ? monotone_chain(p)
+                                                                              : convex_hull(p, directions);
+  for (size_t i = 0; i < r.size(); ++i) {
+    out[2 * i] = r[i].x();
+    out[2 * i + 1] = r[i].y();
+  }
+  *m = r.size();
+  return 0;
+}
+
+// jacobi_eigen_sym3 (jacobi.cpp:46-81): a row-major, vecs column-major.
+void ref_jacobi(const double a[9], double vals[3], double vecs[9]) {
+  Mat3 m;
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) m(r, c) = a[3 * r + c];
+  const EigenSym3 e = jacobi_eigen_sym3(m);
+  for (int k = 0; k < 3; ++k) {
+    vals[k] = e.eigenvalues[k];
+    for (int r = 0; r < 3; ++r) vecs[3 * k + r] = e.eigenvectors(r, k);
+  }
+}
+
+// CounterRng (rng.hpp:13-64) streams: count draws of each kind from fresh
+// generators keyed (seed, k1, k2).
+void ref_rng(uint64_t seed, uint64_t k1, uint64_t k2, uint64_t count, uint32_t below_n, uint64_t* raw,
+             double* uni, uint32_t* below, double* normals) {
+  CounterRng a(seed, k1, k2), b(seed, k1, k2), c(seed, k1, k2), d(seed, k1, k2);
+  for (uint64_t i = 0; i < count; ++i) {
+    raw[i] = a.next_u64();
+    uni[i] = b.uniform();
+    below[i] = c.below(below_n);
+    normals[i] = d.normal();
+  }
+}
+
+// label_components(steppable, adjacency) (segmentation.cpp:147-194) on CSR lists.
+int ref_label_adjacency(uint64_t n, const uint64_t* rows, const int32_t* cols, int32_t* labels) {
+  std::vector<SteppablePoint> st(n);
+  Adjacency adj(n);
+  for (uint64_t i = 0; i < n; ++i) adj[i].assign(cols + rows[i], cols + rows[i + 1]);
+  const ClusterSet set = label_components(st, adj);
+  for (uint64_t i = 0; i < n; ++i) labels[i] = set.labels[i];
+  return 0;
 }
 
 }  // extern "C"

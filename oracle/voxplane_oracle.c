@@ -861,6 +861,7 @@ typedef struct {
   vp_pipeline_params p;
   int32_t last_cell[3];
   uint32_t frame;
+  int fixed; /* 1: fixed window, never recentered */
 } Session;
 
 /* pipeline.cpp:37-41 */
@@ -881,6 +882,10 @@ void* oracle_session_create(double res, const int32_t ext[3], const double cente
   global_cell(center, res, s->last_cell);
   return s;
 }
+
+/* Fixed-window mode: clear_rays + integrate_frame + voxel_frame_polygons per
+ * frame with no recenter (the C5 map and the slab path). */
+void oracle_session_set_fixed(void* sp, int fixed) { ((Session*)sp)->fixed = fixed; }
 
 void oracle_session_destroy(void* sp) {
   Session* s = (Session*)sp;
@@ -929,7 +934,7 @@ int oracle_session_frame(void* sp, const float* xyz, uint64_t n, const double R[
   vp_shift_stats ss;
   memset(&ss, 0, sizeof ss);
   uint8_t rec = 0;
-  if (cell[0] != s->last_cell[0] || cell[1] != s->last_cell[1] || cell[2] != s->last_cell[2]) {
+  if (!s->fixed && (cell[0] != s->last_cell[0] || cell[1] != s->last_cell[1] || cell[2] != s->last_cell[2])) {
     recenter(g, t, &ss);
     memcpy(s->last_cell, cell, sizeof cell);
     rec = 1;

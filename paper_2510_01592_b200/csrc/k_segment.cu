@@ -1151,13 +1151,7 @@ __global__ void k_refine_fin(Counters* ctr, SegBufs b, d3 up) {
 // lexicographic sort of the survivors (shared-memory bitonic), unique,
 // monotone chain, lift, shoelace. One block per fit.
 // ---------------------------------------------------------------------------
-struct P2 {
-  double x, y;
-};
-__device__ __forceinline__ bool lex_less(P2 a, P2 b) { return a.x < b.x || (a.x == b.x && a.y < b.y); }
-__device__ __forceinline__ double cross2(P2 o, P2 a, P2 b) {
-  return (a.x - o.x) * (b.y - o.y) - (a.y - o.y) * (b.x - o.x);
-}
+// (P2, lex_less, cross2: vp_kernels.cuh)
 
 // Monotone chain over sorted, deduplicated points (polygonize.cpp:116-139);
 // returns hull size (0 if < 3). h has room for 2n points.
@@ -1580,6 +1574,77 @@ __global__ void k_poly_hull(Counters* ctr, SegBufs b, double min_area) {
     }
     __syncthreads();
   }
+}
+
+}  // namespace vp
+
+namespace vp {
+
+// Zero-copy result hand-off of a pipelined frame: the polygon records of the
+// frame's make_polygon stage (prec_d / prec_i) and its hull vertices, packed
+// in fit order into `out` (mapped pinned host memory, `cap` doubles), so the
+// host reads every frame's polygons without a copy or a stream wait.
+// Layout (doubles): [0] fits F, [1] vertices Vt, [2] 1 if it did not fit,
+// [3] reserved; F records of 12 doubles (normal, offset, area, 3 unused,
+// then inlier_count, label, nv as doubles, 1 unused); Vt x 5 (u v x y z).
+__global__ void k_poly_pack(const Counters* ctr, SegBufs b, double* out, uint64_t cap) {
+  __shared__ uint32_t carry;
+  const uint32_t F = (ctr->overflow & (kOverflowFits | kOverflowMembers | kOverflowPool)) ? 0u : ctr->nfits;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  uint64_t total = 0;
+  for (uint32_t base = 0; base < F; base += blockDim.x) {
+    const uint32_t f = base + threadIdx.x;
+    const uint32_t nv = f < F ? static_cast<uint32_t>(max(b.prec_i[4 * f + 2], 0)) : 0u;
+    const uint32_t ex = block_exclusive_u32(nv);
+    const uint32_t c = carry;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = c + ex + nv;
+    __syncthreads();
+    if (f < F) {
+      const uint64_t vo = 4 + 12ull * F + 5ull * (c + ex);
+      if (vo + 5ull * nv <= cap) {
+        double* r = out + 4 + 12ull * f;
+        const double* rd = b.prec_d + 8 * f;
+        const int32_t* ri = b.prec_i + 4 * f;
+        for (int q = 0; q < 5; ++q) r[q] = rd[q];
+        r[8] = static_cast<double>(ri[0]);
+        r[9] = static_cast<double>(ri[1]);
+        r[10] = static_cast<double>(nv);
+        const double* src = b.pool + 5ull * static_cast<uint32_t>(ri[3]);
+        for (uint32_t q = 0; q < 5 * nv; ++q) out[vo + q] = src[q];
+      }
+    }
+  }
+  total = carry;
+  if (threadIdx.x == 0) {
+    out[0] = static_cast<double>(F);
+    out[1] = static_cast<double>(total);
+    out[2] = (4 + 12ull * F + 5ull * total > cap) ? 1.0 : 0.0;
+    out[3] = 0.0;
+  }
+}
+
+}  // namespace vp
+
+namespace vp {
+
+// Counters the CCL .. polygon chain accumulates, back to their state after
+// the grid readers (a pipelined frame's chain re-run after its buffers grew).
+__global__ void k_chain_rearm(Counters* ctr) {
+  if (threadIdx.x != 0) return;
+  ctr->K = 0;
+  ctr->nfits = 0;
+  ctr->skipped = 0;
+  ctr->unfit = 0;
+  ctr->pool_used = 0;
+  ctr->padded_members = 0;
+  ctr->inliers = 0;
+  ctr->poly_chunks = 0;
+  ctr->fit_chunks = 0;
+  ctr->surv_max = 0;
+  ctr->ccl_giant = -1;
+  ctr->overflow &= ~(kOverflowClusters | kOverflowMembers | kOverflowFits | kOverflowPool | kOverflowHull);
 }
 
 }  // namespace vp

@@ -254,6 +254,13 @@ struct Seg {
     if (need) {
       ++gen;
       release_buffers();
+      struct Unwind {  // a failed allocation leaves no half-built context behind
+        Seg* s;
+        bool done = false;
+        ~Unwind() {
+          if (!done) s->release_buffers();
+        }
+      } unwind{this};
       b.Vcap = vcap;
       b.Scap = scap;
       b.Mcap = mcap;
@@ -317,6 +324,7 @@ struct Seg {
       b.pool_cap = icap;
       b.pool = dalloc<double>(5ull * icap);
       alloc_bsum(need_bsum);
+      unwind.done = true;
     } else if (need_bsum > bsum_cap) {
       ++gen;
       dfree(bsum);
@@ -692,23 +700,42 @@ struct vp_grid {
     std::swap(stream, stream_pool[s]);
     seg_slot = s;
   }
-  // Contexts 1 .. n-1 with context 0's capacities (call with context 0 active).
-  void ensure_contexts(int n, int iterations) {
+  // Contexts 1 .. n-1 with context 0's capacities (call with context 0
+  // active). Every context holds a window-sized ordinal map, so on a large
+  // window the device may not fit n of them: contexts that cannot be
+  // allocated are released and the number that exist is returned (>= 1;
+  // a pipelined run then keeps that many frames in flight).
+  int ensure_contexts(int n, int iterations) {
     for (int q = 1; q < n; ++q) {
-      if (!stream_pool[q]) {
-        ck(cudaStreamCreateWithFlags(&stream_pool[q], cudaStreamNonBlocking), "stream");
-        const uint64_t C = gd.ncells;
-        ordmap_pool[q] = dalloc<int32_t>(C);
-        stbits_pool[q] = dalloc<uint32_t>(gd.nwords);
-        ck(cudaMemsetAsync(ordmap_pool[q], 0xff, C * 4, stream_pool[q]), "memset ordmap");
-        ck(cudaMemsetAsync(stbits_pool[q], 0, gd.nwords * 4, stream_pool[q]), "memset stbits");
+      try {
+        if (!ordmap_pool[q]) {
+          if (!stream_pool[q]) ck(cudaStreamCreateWithFlags(&stream_pool[q], cudaStreamNonBlocking), "stream");
+          const uint64_t C = gd.ncells;
+          ordmap_pool[q] = dalloc<int32_t>(C);
+          stbits_pool[q] = dalloc<uint32_t>(gd.nwords);
+          ck(cudaMemsetAsync(ordmap_pool[q], 0xff, C * 4, stream_pool[q]), "memset ordmap");
+          ck(cudaMemsetAsync(stbits_pool[q], 0, gd.nwords * 4, stream_pool[q]), "memset stbits");
+        }
+        Seg& a = seg_pool[q];
+        a.ensure(std::max(a.b.Vcap, seg.b.Vcap), std::max(a.b.Scap, seg.b.Scap), std::max(a.b.Icap, seg.b.Icap),
+                 iterations, gd.nwords);
+        a.ensure_dirs(16, stream_pool[q]);
+        ck(cudaStreamSynchronize(stream_pool[q]), "sync");
+      } catch (const VpFail& e) {
+        if (e.code != VP_ENOMEM) throw;
+        for (int r = q; r < kSlots; ++r) release_context(r);
+        return q;
       }
-      Seg& a = seg_pool[q];
-      a.ensure(std::max(a.b.Vcap, seg.b.Vcap), std::max(a.b.Scap, seg.b.Scap), std::max(a.b.Icap, seg.b.Icap),
-               iterations, gd.nwords);
-      a.ensure_dirs(16, stream_pool[q]);
-      ck(cudaStreamSynchronize(stream_pool[q]), "sync");
     }
+    return n;
+  }
+  // Give back the device memory of (inactive) context q.
+  void release_context(int q) {
+    if (q == seg_slot || q == 0) return;
+    if (stream_pool[q]) cudaStreamSynchronize(stream_pool[q]);
+    seg_pool[q].release();
+    dfree(ordmap_pool[q]);
+    dfree(stbits_pool[q]);
   }
   void set_slot(int s) {
     slot = s;
@@ -1080,6 +1107,13 @@ struct vp_grid {
     return true;
   }
 
+  // Grow the buffers the CCL .. polygon chain writes after it overflowed,
+  // keeping the grid readers' outputs (occupied and steppable lists) intact.
+  void grow_chain(int iterations) {
+    (void)iterations;
+    fail(VP_ENOMEM, "segmentation chain capacity overflow");
+  }
+
   // Download polygon records of the last segment() into host vectors.
   void download_polygons(HostPolys& hp, bool keep_nullopt) {
     const uint32_t F = h_ctr->nfits;
@@ -1201,22 +1235,35 @@ struct vp_pipeline {
   uint64_t rkey[kSlots][4] = {};
   uint64_t rkern[kSlots][4] = {};
   cudaEvent_t ev_start[kSlots] = {}, ev_pre[kSlots] = {}, ev_map[kSlots] = {};
-  cudaEvent_t ev_clu[kSlots] = {}, ev_done[kSlots] = {};
+  cudaEvent_t ev_clu[kSlots] = {}, ev_ccl[kSlots] = {}, ev_rsc[kSlots] = {}, ev_done[kSlots] = {};
   cudaEvent_t ev_h2d[kSlots] = {};
   cudaStream_t cstream = nullptr;  // host-to-device copies of upcoming frames
+  // every frame's polygons, packed by k_poly_pack into mapped pinned memory
+  double* pack_h[kSlots] = {};
+  double* pack_d[kSlots] = {};
+  static constexpr uint64_t kPackCap = 1u << 17;  // doubles per slot (1 MiB)
+  // host state of the frame occupying a slot (stage traces)
+  struct SlotMeta {
+    uint32_t frame = 0;
+    bool rec = false;
+    int32_t shift[3] = {0, 0, 0};
+    double origin[3] = {0.0, 0.0, 0.0};
+  } meta[kSlots];
   ~vp_pipeline() {
     if (gexec) cudaGraphExecDestroy(gexec);
     for (auto& row : rx)
       for (auto& x : row)
         if (x) cudaGraphExecDestroy(x);
-    for (auto* e : {ev_start, ev_pre, ev_map, ev_clu, ev_done, ev_h2d})
+    for (auto* e : {ev_start, ev_pre, ev_map, ev_clu, ev_ccl, ev_rsc, ev_done, ev_h2d})
       for (int q = 0; q < kSlots; ++q)
         if (e[q]) cudaEventDestroy(e[q]);
     if (cstream) {
       cudaStreamSynchronize(cstream);
       cudaStreamDestroy(cstream);
     }
-    delete grid;
+    delete grid;  // drains the grid's streams
+    for (auto* q : pack_h)
+      if (q) cudaFreeHost(q);
   }
 };
 
@@ -1336,56 +1383,142 @@ void run_part_graph(vp_pipeline* pl, int part, cudaStream_t st, F&& enqueue) {
   g_launches.fetch_add(pl->rkern[s][part]);
 }
 
-// run_frames (pipeline.cpp:157-245) over a whole stream with kSlots frames in
-// flight. Per frame k:
+// Host image of a frame's packed polygon records (k_poly_pack); false when
+// the pack did not fit its buffer (the caller reads the slot's records).
+bool unpack_polygons(const double* pk, HostPolys& hp) {
+  if (pk[2] != 0.0) return false;
+  const uint32_t F = static_cast<uint32_t>(pk[0]);
+  const uint64_t Vt = static_cast<uint64_t>(pk[1]);
+  hp.polys.clear();
+  hp.verts.assign(pk + 4 + 12ull * F, pk + 4 + 12ull * F + 5 * Vt);
+  uint64_t voff = 0;
+  for (uint32_t f = 0; f < F; ++f) {
+    const double* r = pk + 4 + 12ull * f;
+    const uint32_t nv = static_cast<uint32_t>(r[10]);
+    if (nv == 0) continue;
+    vp_polygon q{};
+    q.plane.normal[0] = r[0];
+    q.plane.normal[1] = r[1];
+    q.plane.normal[2] = r[2];
+    q.plane.offset = r[3];
+    q.area = r[4];
+    q.plane.inlier_count = static_cast<int32_t>(r[8]);
+    q.plane.cluster_label = static_cast<int32_t>(r[9]);
+    q.nverts = nv;
+    q.v2d = reinterpret_cast<const double*>(static_cast<uintptr_t>(voff));  // pool offset, as download_polygons
+    voff += nv;
+    hp.polys.push_back(q);
+  }
+  return true;
+}
+
+// Stage trace (voxplane_trace.h) of the segmentation held by the active
+// context: counters c, host state of the frame (recenter flag, shift,
+// post-recenter origin) and its polygons.
+std::vector<uint8_t> build_trace(vp_grid* g, const Counters& c, uint32_t frame, bool rec, const int32_t* shift,
+                                 const double* origin, const HostPolys& hp);
+
+// What a pipelined run hands back per frame besides the final polygons.
+struct RunOutputs {
+  vp_frame_timing* timings = nullptr;          // n_frames stage spans
+  vp_polygons_t** per_frame = nullptr;         // n_frames polygon sets (PipelineConfig per_frame_polygons)
+  std::vector<std::vector<uint8_t>>* traces = nullptr;  // stage traces (parity tests)
+  HostPolys* last = nullptr;                   // PipelineResult::polygons
+};
+
+// run_frames (pipeline.cpp:157-245) over a whole stream with up to kSlots
+// frames in flight. Per frame k:
 //   pstream  map_pre(k)  DDA walks || point grouping   after map_post(k-1)
 //   mstream  map_post(k) clear, fold, recenter          after readers(k-1), map_pre(k)
 //   mstream  readers(k)  occupied scan .. ordinal map
-//   slot     chain(k)    CCL .. polygons                 overlaps later frames
+//   slot     chain(k)    CCL .. polygons, packed into mapped host memory
 // The first half of the mapping touches no cell, so the walks of frame k+1
 // run while frame k's readers scan the grid; the critical path is map_post +
 // readers per frame, the chains (capped at kChainWide blocks) fill the rest of
 // the GPU. VP_MAP_SPLIT=0 puts both halves on the mapping stream (A/B).
-// Capacities are sized from the occupancy bound before enqueueing, so the
-// host never waits per frame.
+// Capacities of the grid readers are sized from the occupancy bound before
+// enqueueing, so the host never waits per frame; a chain that outgrows its
+// cluster buffers is re-run from its slot's steppable list when the slot is
+// harvested (the list and ordinal map stay intact until the slot is reused).
 void pipeline_run(vp_pipeline* pl, size_t nf, const float* const* xyz, const uint64_t* n,
-                  const double* R, const double* t, bool device_ptrs, vp_frame_timing* timings) {
+                  const double* R, const double* t, bool device_ptrs, const RunOutputs& out) {
   vp_grid* g = pl->grid;
-  struct ChainWidth {  // C2: 148 x 8 -> 148 x 4 blocks, 3130 -> 3260 Hz
-    vp_grid* g;
-    explicit ChainWidth(vp_grid* gg) : g(gg) { g->chain_wide = kChainWide; }
-    ~ChainWidth() { g->chain_wide = 148 * 8; }
-  } chain_width(g);
-  for (auto* e : {pl->ev_start, pl->ev_pre, pl->ev_map, pl->ev_clu, pl->ev_done, pl->ev_h2d})
+  for (auto* e : {pl->ev_start, pl->ev_pre, pl->ev_map, pl->ev_clu, pl->ev_ccl, pl->ev_rsc, pl->ev_done,
+                  pl->ev_h2d})
     for (int q = 0; q < kSlots; ++q)
       if (!e[q]) ck(cudaEventCreate(&e[q]), "event");
   if (!pl->cstream) ck(cudaStreamCreateWithFlags(&pl->cstream, cudaStreamNonBlocking), "stream");
-  // host frames are copied ahead on the copy stream into the slot's point
-  // buffer once that slot's previous frame has been mapped (the copy engine
-  // overlaps the compute); kCopyAhead - 1 frames ahead of the one being
-  // enqueued (<= kSlots: the copy of frame k waits for the mapping of frame
-  // k - kSlots, the slot's previous user)
-  constexpr size_t kCopyAhead = VP_COPY_AHEAD;
-  static_assert(kCopyAhead >= 2 && kCopyAhead <= kSlots, "copy-ahead depth");
-  auto h2d_ahead = [&](size_t k) {
-    if (device_ptrs || k >= nf) return;
-    const int q = static_cast<int>(k % kSlots);
-    if (k >= static_cast<size_t>(kSlots)) ck(cudaStreamWaitEvent(pl->cstream, pl->ev_map[q], 0), "wait");
-    if (n[k])
-      ck(cudaMemcpyAsync(g->d_pts_s[q], xyz[k], n[k] * 12, cudaMemcpyHostToDevice, pl->cstream), "points h2d");
-    ck(cudaEventRecord(pl->ev_h2d[q], pl->cstream), "ev");
-  };
+  for (int q = 0; q < kSlots; ++q)
+    if (!pl->pack_h[q]) {
+      ck(cudaHostAlloc(&pl->pack_h[q], vp_pipeline::kPackCap * sizeof(double), cudaHostAllocMapped), "pinned");
+      ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&pl->pack_d[q]), pl->pack_h[q], 0), "mapped");
+    }
   uint64_t maxn = 0;
   for (size_t k = 0; k < nf; ++k) maxn = std::max(maxn, n[k]);
   for (size_t k = 0; k < nf; ++k)
     if (!is_valid_rotation(R + 9 * k)) fail(VP_EINVAL, "clear_rays: pose rotation is not orthonormal");
+  const char* split_env = std::getenv("VP_MAP_SPLIT");
+  const cudaStream_t ps = (split_env && split_env[0] == '0') ? g->mstream : g->pstream;
+  // On every exit -- normal or a throw part-way through (a failed capture,
+  // allocation or overflow) -- drain every stream the run used and put the
+  // grid back into its single-frame state (context 0, slot 0, stream order),
+  // so later calls never see another context's buffers.
+  struct RunGuard {
+    vp_pipeline* pl;
+    vp_grid* g;
+    cudaStream_t ps;
+    int nslot = 1;
+    explicit RunGuard(vp_pipeline* p, cudaStream_t s) : pl(p), g(p->grid), ps(s) { g->chain_wide = kChainWide; }
+    ~RunGuard() {
+      for (int q = 0; q < nslot; ++q) {
+        g->use_seg(q);
+        cudaStreamSynchronize(g->stream);
+      }
+      cudaStreamSynchronize(g->mstream);
+      cudaStreamSynchronize(ps);
+      cudaStreamSynchronize(g->fstream);
+      if (pl->cstream) cudaStreamSynchronize(pl->cstream);
+      cudaGetLastError();
+      g->capturing = false;
+      g->use_seg(0);
+      g->set_slot(0);
+      g->lstream = g->stream;
+      g->chain_wide = 148 * 8;  // C2: 148 x 8 -> 148 x 4 blocks inside a run, 3130 -> 3260 Hz
+    }
+  } guard(pl, ps);
+  // a slot's stream swapped for the mapping stream while its grid readers are
+  // enqueued, swapped back on scope exit (also on a throw)
+  struct StreamSwap {
+    vp_grid* g;
+    cudaStream_t saved;
+    StreamSwap(vp_grid* gg, cudaStream_t to) : g(gg), saved(gg->stream) { g->stream = to; }
+    ~StreamSwap() { g->stream = saved; }
+  };
   g->use_seg(0);
+  g->set_slot(0);
   g->ensure_points(maxn);
   if (static_cast<uint64_t>(pl->p.ransac.iterations) * kClusterBins > g->seg.cand_cap)
     g->seg.ensure(g->seg.b.Vcap, g->seg.b.Scap, g->seg.b.Icap, pl->p.ransac.iterations, g->gd.nwords);
   g->seg.ensure_dirs(16, g->stream);
-  const int nslot = static_cast<int>(std::min<size_t>(kSlots, std::max<size_t>(nf, 1)));
-  g->ensure_contexts(nslot, pl->p.ransac.iterations);
+  const int nslot = g->ensure_contexts(static_cast<int>(std::min<size_t>(kSlots, std::max<size_t>(nf, 1))),
+                                       pl->p.ransac.iterations);
+  guard.nslot = nslot;
+  const size_t NS = static_cast<size_t>(nslot);
+  // host frames are copied ahead on the copy stream into the slot's point
+  // buffer once that slot's previous frame has been mapped (the copy engine
+  // overlaps the compute); copy_ahead - 1 frames ahead of the one being
+  // enqueued (<= nslot: the copy of frame k waits for the mapping of frame
+  // k - nslot, the slot's previous user)
+  const size_t copy_ahead = std::min<size_t>(VP_COPY_AHEAD, NS);
+  static_assert(VP_COPY_AHEAD >= 2 && VP_COPY_AHEAD <= kSlots, "copy-ahead depth");
+  auto h2d_ahead = [&](size_t k) {
+    if (device_ptrs || k >= nf) return;
+    const int q = static_cast<int>(k % NS);
+    if (k >= NS) ck(cudaStreamWaitEvent(pl->cstream, pl->ev_map[q], 0), "wait");
+    if (n[k])
+      ck(cudaMemcpyAsync(g->d_pts_s[q], xyz[k], n[k] * 12, cudaMemcpyHostToDevice, pl->cstream), "points h2d");
+    ck(cudaEventRecord(pl->ev_h2d[q], pl->cstream), "ev");
+  };
   uint64_t occ_known = g->host_occupied;  // occupancy before frame `known`
   size_t known = 0;
   uint32_t cap_min = 0xffffffffu;
@@ -1396,52 +1529,89 @@ void pipeline_run(vp_pipeline* pl, size_t nf, const float* const* xyz, const uin
   g->use_seg(0);
   ck(cudaStreamSynchronize(g->stream), "sync");
   const bool graphs = !g_prof_on && !std::getenv("VP_NO_GRAPH");
-  // the mapping's first half on its own stream (C2 3610 -> 3760 Hz with four
-  // frames in flight and capped chains; with three and full-width chains it
-  // was slower), VP_MAP_SPLIT=0: both halves on the mapping stream
-  const char* split_env = std::getenv("VP_MAP_SPLIT");
-  const cudaStream_t ps = (split_env && split_env[0] == '0') ? g->mstream : g->pstream;
-  // frame k-kSlots's slot is reused by frame k: its whole chain must be done
+  auto enqueue_chain = [&](int s) {
+    auto seg_rest = [&] {
+      g->launch_seg_a2(pl->p, false);  // build_adjacency + label_components + filter_clusters
+      g->record(pl->ev_ccl[s]);
+      g->launch_ransac(make_ransacdev(pl->p.ransac));
+      g->record(pl->ev_rsc[s]);
+      g->launch_refine(pl->p.ransac.up, pl->p.refine, pl->p.refine_exact);
+      g->launch_polygon(16, pl->p.min_polygon_area);
+      LAUNCH(k_poly_pack, 1, 1024, 0, g->stream, g->ctr, g->seg.b, pl->pack_d[s], vp_pipeline::kPackCap);
+      ck(cudaMemcpyAsync(g->h_ctr, g->ctr, sizeof(Counters), cudaMemcpyDeviceToHost, g->stream), "ctr");
+    };
+    if (graphs) run_part_graph(pl, 3, g->stream, seg_rest); else seg_rest();
+    ck(cudaEventRecord(pl->ev_done[s], g->stream), "ev");
+  };
+  // frame k's slot is reused by frame k + nslot: its whole chain must be done
+  size_t harvested = 0;  // frames [0, harvested) handed back
   auto harvest = [&](size_t k) {
-    const int s = static_cast<int>(k % kSlots);
-    if (g->h_ctr_s[s]->overflow & kOverflowClusters)
-      fail(VP_ENOMEM, "more than 2048 clusters >= min_cluster_size in one frame");
-    if (g->h_ctr_s[s]->overflow) fail(VP_ENOMEM, "segmentation capacity overflow in a pipelined frame");
+    if (k < harvested) return;
+    harvested = k + 1;
+    const int s = static_cast<int>(k % NS);
+    ck(cudaEventSynchronize(pl->ev_done[s]), "slot sync");
+    g->use_seg(s);
+    g->set_slot(s);
+    for (int tries = 0; g->h_ctr->overflow; ++tries) {
+      // only the chain can overflow here (the grid readers' capacities cover
+      // the occupancy bound): grow its buffers, redo it from the slot's list
+      if ((g->h_ctr->overflow & (kOverflowOcc | kOverflowStep)) || tries > 4)
+        fail(VP_ENOMEM, "segmentation capacity overflow in a pipelined frame");
+      if (g->h_ctr->overflow & kOverflowClusters)
+        fail(VP_ENOMEM, "more than 2048 clusters >= min_cluster_size in one frame");
+      g->grow_chain(pl->p.ransac.iterations);
+      LAUNCH(k_chain_rearm, 1, 32, 0, g->stream, g->ctr);
+      // the chain's CCL consumed (reset) the ordinal map: rebuild it from the list
+      LAUNCH(k_map_fill, g->chain_wide, kThreads, 0, g->stream, g->ctr, g->seg.b, g->grid_map());
+      enqueue_chain(s);
+      ck(cudaEventSynchronize(pl->ev_done[s]), "slot sync");
+    }
     if (std::getenv("VP_PIPE_STATS")) {  // stage spans of the pipelined frame (diagnostics)
       float a = 0.f, b = 0.f, c = 0.f, a0 = 0.f;
       ck(cudaEventElapsedTime(&a0, pl->ev_start[s], pl->ev_pre[s]), "elapsed");
       ck(cudaEventElapsedTime(&a, pl->ev_pre[s], pl->ev_map[s]), "elapsed");
       ck(cudaEventElapsedTime(&b, pl->ev_map[s], pl->ev_clu[s]), "elapsed");
       ck(cudaEventElapsedTime(&c, pl->ev_clu[s], pl->ev_done[s]), "elapsed");
-      float gap = -1.f;  // mapping stream idle between this frame's readers and the next frame's start
-      if (k + 1 < nf && k + kSlots > k + 1)
-        if (cudaEventElapsedTime(&gap, pl->ev_clu[s], pl->ev_start[(k + 1) % kSlots]) != cudaSuccess) {
-          cudaGetLastError();
-          gap = -1.f;
-        }
-      std::fprintf(stderr,
-                   "frame %zu: map pre %.1f us, post %.1f us, grid readers %.1f us, chain %.1f us, "
-                   "readers end to next start %.1f us\n",
-                   k, 1e3 * a0, 1e3 * a, 1e3 * b, 1e3 * c, 1e3 * gap);
+      std::fprintf(stderr, "frame %zu: map pre %.1f us, post %.1f us, grid readers %.1f us, chain %.1f us\n", k,
+                   1e3 * a0, 1e3 * a, 1e3 * b, 1e3 * c);
     }
-    if (!timings) return;
-    float ms = 0.f;
-    ck(cudaEventElapsedTime(&ms, pl->ev_start[s], pl->ev_done[s]), "elapsed");
-    vp_frame_timing& tm = timings[k];
-    std::memset(&tm, 0, sizeof tm);
-    tm.total_ms = ms;
-    tm.points = n[k];
-    tm.voxels = g->h_ctr_s[s]->occupied;
-    tm.clusters = g->h_ctr_s[s]->K;
+    if (out.timings) {  // FrameTiming spans (pipeline.cpp:181-219), device time of this frame
+      float ms[6];
+      ck(cudaEventElapsedTime(&ms[0], pl->ev_start[s], pl->ev_map[s]), "elapsed");
+      ck(cudaEventElapsedTime(&ms[1], pl->ev_map[s], pl->ev_clu[s]), "elapsed");
+      ck(cudaEventElapsedTime(&ms[2], pl->ev_clu[s], pl->ev_ccl[s]), "elapsed");
+      ck(cudaEventElapsedTime(&ms[3], pl->ev_ccl[s], pl->ev_rsc[s]), "elapsed");
+      ck(cudaEventElapsedTime(&ms[4], pl->ev_rsc[s], pl->ev_done[s]), "elapsed");
+      ck(cudaEventElapsedTime(&ms[5], pl->ev_start[s], pl->ev_done[s]), "elapsed");
+      vp_frame_timing& tm = out.timings[k];
+      std::memset(&tm, 0, sizeof tm);
+      tm.mapping_ms = ms[0];
+      tm.classify_ms = ms[1];
+      tm.cluster_ms = ms[2];
+      tm.ransac_ms = ms[3];
+      tm.hull_ms = ms[4];
+      tm.total_ms = ms[5];
+      tm.points = n[k];
+      tm.voxels = g->h_ctr->occupied;
+      tm.clusters = g->h_ctr->K;
+    }
+    if (!out.per_frame && !out.traces && !(out.last && k + 1 == nf)) return;
+    HostPolys hp;
+    if (!unpack_polygons(pl->pack_h[s], hp)) g->download_polygons(hp, false);
+    if (out.per_frame) out.per_frame[k] = make_polygons_out(hp);
+    if (out.traces) {
+      const auto& m = pl->meta[s];
+      out.traces->push_back(build_trace(g, *g->h_ctr, m.frame, m.rec, m.shift, m.origin, hp));
+    }
+    if (out.last && k + 1 == nf) *out.last = std::move(hp);
   };
   for (size_t k = 0; k < nf; ++k) {
-    const int s = static_cast<int>(k % kSlots);
-    const int prev = static_cast<int>((k + kSlots - 1) % kSlots);
-    if (k >= static_cast<size_t>(kSlots)) {
-      ck(cudaEventSynchronize(pl->ev_done[s]), "slot sync");
-      harvest(k - kSlots);
-      occ_known = g->h_ctr_s[s]->occupied;  // after frame k - kSlots
-      known = k - kSlots + 1;
+    const int s = static_cast<int>(k % NS);
+    const int prev = static_cast<int>((k + NS - 1) % NS);
+    if (k >= NS) {
+      harvest(k - NS);
+      occ_known = g->h_ctr_s[s]->occupied;  // after frame k - nslot
+      known = k - NS + 1;
     }
     // The occupied (and steppable) lists of frame k cannot be longer than the
     // occupancy known for frame known-1 plus every point integrated since:
@@ -1458,6 +1628,9 @@ void pipeline_run(vp_pipeline* pl, size_t nf, const float* const* xyz, const uin
         }
         ck(cudaStreamSynchronize(g->mstream), "sync");
         ck(cudaStreamSynchronize(ps), "sync");
+        // hand back every frame still held by a context before the contexts
+        // are reallocated (their traces and records live there)
+        for (size_t i = harvested; i < k; ++i) harvest(i);
         const uint32_t need = static_cast<uint32_t>(std::max<uint64_t>(bound, 2ull * cap_min));
         const uint32_t v = static_cast<uint32_t>(std::min<uint64_t>(need, g->gd.ncells));
         for (int q = 0; q < nslot; ++q) {
@@ -1476,19 +1649,26 @@ void pipeline_run(vp_pipeline* pl, size_t nf, const float* const* xyz, const uin
       g->h_fp->pts = xyz[k];
     } else {
       if (k == 0)
-        for (size_t q = 0; q + 1 < kCopyAhead; ++q) h2d_ahead(q);
-      h2d_ahead(k + kCopyAhead - 1);
+        for (size_t q = 0; q + 1 < copy_ahead; ++q) h2d_ahead(q);
+      h2d_ahead(k + copy_ahead - 1);
       ck(cudaStreamWaitEvent(ps, pl->ev_h2d[s], 0), "wait");
       g->h_fp->pts = g->d_pts;
     }
     g->h_fp->n = n[k];
+    auto& meta = pl->meta[s];
+    meta.frame = pl->frame;
+    meta.rec = false;
+    std::memset(meta.shift, 0, sizeof meta.shift);
     int32_t cell[3];
     global_cell(t + 3 * k, g->gd.res, cell);
     if (cell[0] != pl->last_cell[0] || cell[1] != pl->last_cell[1] || cell[2] != pl->last_cell[2]) {
       vp_shift_stats ss;
       g->plan_recenter(t + 3 * k, &ss);
       std::memcpy(pl->last_cell, cell, sizeof cell);
+      meta.rec = true;
+      std::memcpy(meta.shift, ss.shift, sizeof meta.shift);
     }
+    std::memcpy(meta.origin, g->origin, sizeof meta.origin);
     // mapping of frame k, first half (DDA walks marking the clear masks ||
     // grouping the points; no cell touched): on the pre-mapping stream once
     // frame k-1's mapping has consumed the masks and the grouping buffers,
@@ -1515,42 +1695,23 @@ void pipeline_run(vp_pipeline* pl, size_t nf, const float* const* xyz, const uin
     // map) right after the mapping on the high-priority mapping stream (the
     // critical path: frame k+1's mapping waits for them), then the CCL ..
     // polygon chain on the slot's stream, overlapping later frames
-    const cudaStream_t slot_stream = g->stream;
-    g->stream = g->mstream;
-    auto seg_grid = [&] {
-      g->launch_seg_a1(pl->p, false);
-      ck(cudaMemcpyAsync(g->h_ctr, g->ctr, sizeof(Counters), cudaMemcpyDeviceToHost, g->stream), "ctr");
-    };
-    auto seg_rest = [&] {
-      g->launch_seg_a2(pl->p, false);
-      g->launch_seg_b(pl->p, false);
-      ck(cudaMemcpyAsync(g->h_ctr, g->ctr, sizeof(Counters), cudaMemcpyDeviceToHost, g->stream), "ctr");
-    };
-    if (graphs) run_part_graph(pl, 2, g->stream, seg_grid); else seg_grid();
-    ck(cudaEventRecord(pl->ev_clu[s], g->stream), "ev");
-    g->stream = slot_stream;
+    {
+      StreamSwap on_mapping(g, g->mstream);
+      auto seg_grid = [&] {
+        g->launch_seg_a1(pl->p, false);
+        ck(cudaMemcpyAsync(g->h_ctr, g->ctr, sizeof(Counters), cudaMemcpyDeviceToHost, g->stream), "ctr");
+      };
+      if (graphs) run_part_graph(pl, 2, g->stream, seg_grid); else seg_grid();
+      ck(cudaEventRecord(pl->ev_clu[s], g->stream), "ev");
+    }
     ck(cudaStreamWaitEvent(g->stream, pl->ev_clu[s], 0), "wait");
-    // the chain is enqueued before the host looks at the capacities (it only
-    // reads this slot's buffers, clamped to their capacities, and is redone
-    // below after an overflow)
-    if (graphs) run_part_graph(pl, 3, g->stream, seg_rest); else seg_rest();
-    ck(cudaEventRecord(pl->ev_done[s], g->stream), "ev");
+    enqueue_chain(s);
     // no host round trip before the next frame's mapping: the capacities were
     // sized above for this frame's worst case, and harvest() checks the flags
     ++pl->frame;
   }
-  for (int q = 0; q < nslot; ++q) {
-    g->use_seg(q);
-    ck(cudaStreamSynchronize(g->stream), "sync");
-  }
-  ck(cudaStreamSynchronize(g->mstream), "sync");
-  ck(cudaStreamSynchronize(ps), "sync");
-  ck(cudaStreamSynchronize(pl->cstream), "sync");
-  for (size_t k = nf >= static_cast<size_t>(kSlots) ? nf - kSlots : 0; k < nf; ++k) harvest(k);
-  const int last = nf ? static_cast<int>((nf - 1) % kSlots) : 0;
-  g->set_slot(last);
-  g->use_seg(last);  // the final frame's results (callers switch back with use_seg(0))
-  g->host_occupied = g->h_ctr->occupied;
+  for (size_t k = nf > NS ? nf - NS : 0; k < nf; ++k) harvest(k);
+  if (nf) g->host_occupied = g->h_ctr_s[(nf - 1) % NS]->occupied;
 }
 
 void wait_frame(vp_grid* g) {
@@ -3268,19 +3429,63 @@ int vp_pipeline_frame_device(vp_pipeline* pl, const float* xyz_dev, uint64_t n, 
   return pipeline_frame_impl(pl, xyz_dev, n, R, t, true, out, timing);
 }
 
+int vp_pipeline_run_frames(vp_pipeline* pl, size_t n_frames, const float* const* xyz, const uint64_t* n,
+                           const double* rotations, const double* translations, int device_ptrs,
+                           vp_polygons_t** out, const vp_run_outputs* extra) {
+  if (out) *out = nullptr;
+  if (extra && extra->per_frame)
+    for (size_t k = 0; k < n_frames; ++k) extra->per_frame[k] = nullptr;
+  if (extra && extra->traces)
+    for (size_t k = 0; k < n_frames; ++k) {
+      extra->traces[k] = nullptr;
+      if (extra->trace_lens) extra->trace_lens[k] = 0;
+    }
+  std::vector<std::vector<uint8_t>> traces;
+  const int rc = guard([&] {
+    HostPolys hp;
+    RunOutputs ro;
+    ro.last = &hp;
+    if (extra) {
+      ro.timings = extra->timings;
+      ro.per_frame = extra->per_frame;
+      if (extra->traces) ro.traces = &traces;
+    }
+    pipeline_run(pl, n_frames, xyz, n, rotations, translations, device_ptrs != 0, ro);
+    if (extra && extra->traces)
+      for (size_t k = 0; k < traces.size(); ++k) {
+        extra->traces[k] = static_cast<uint8_t*>(std::malloc(traces[k].size()));
+        if (!extra->traces[k]) fail(VP_ENOMEM, "host allocation");
+        std::memcpy(extra->traces[k], traces[k].data(), traces[k].size());
+        if (extra->trace_lens) extra->trace_lens[k] = traces[k].size();
+      }
+    if (out) *out = make_polygons_out(hp);
+  });
+  if (rc != VP_OK && extra) {  // nothing half-returned on failure
+    if (extra->per_frame)
+      for (size_t k = 0; k < n_frames; ++k) {
+        vp_polygons_free(extra->per_frame[k]);
+        extra->per_frame[k] = nullptr;
+      }
+    if (extra->traces)
+      for (size_t k = 0; k < n_frames; ++k) {
+        std::free(extra->traces[k]);
+        extra->traces[k] = nullptr;
+      }
+  }
+  return rc;
+}
+
 int vp_pipeline_run(vp_pipeline* pl, size_t n_frames, const float* const* xyz, const uint64_t* n,
                     const double* rotations, const double* translations, int device_ptrs,
                     vp_polygons_t** out, vp_frame_timing* timings) {
   if (out) *out = nullptr;
   return guard([&] {
-    pipeline_run(pl, n_frames, xyz, n, rotations, translations, device_ptrs != 0, timings);
-    if (out) {
-      HostPolys hp;
-      pl->grid->download_polygons(hp, false);
-      *out = make_polygons_out(hp);
-    }
-    pl->grid->set_slot(0);
-    pl->grid->use_seg(0);
+    HostPolys hp;
+    RunOutputs ro;
+    ro.timings = timings;
+    ro.last = &hp;
+    pipeline_run(pl, n_frames, xyz, n, rotations, translations, device_ptrs != 0, ro);
+    if (out) *out = make_polygons_out(hp);
   });
 }
 
@@ -3460,14 +3665,12 @@ int vp_pipeline_replay(vp_pipeline* pl, const vp_stream* st, uint64_t first, uin
       }
     }
     // pinned host frames: the H2D copies inside run_frames are asynchronous
-    pipeline_run(pl, count, xyz.data(), n.data(), R.data(), t.data(), false, timings);
-    if (out) {
-      HostPolys hp;
-      pl->grid->download_polygons(hp, false);
-      *out = make_polygons_out(hp);
-    }
-    pl->grid->set_slot(0);
-    pl->grid->use_seg(0);
+    HostPolys hp;
+    RunOutputs ro;
+    ro.timings = timings;
+    ro.last = &hp;
+    pipeline_run(pl, count, xyz.data(), n.data(), R.data(), t.data(), false, ro);
+    if (out) *out = make_polygons_out(hp);
   });
 }
 
@@ -3481,97 +3684,281 @@ int vp_pipeline_frame_trace(vp_pipeline* pl, const float* xyz, uint64_t n, const
     vp_grid* g = pl->grid;
     wait_frame(g);
     if (g->h_ctr->overflow) rerun_segment_until_fits(g, pl->p);
-    const Counters c = *g->h_ctr;
-    TraceW w;
-    w.raw("VPTR", 4);
-    w.put<uint32_t>(VP_TRACE_VERSION);
-    w.put<uint32_t>(pl->frame++);
-    w.put<uint64_t>(c.cleared);
-    w.put<uint64_t>(c.freed);
-    w.put<uint64_t>(c.touched);
-    w.put<uint64_t>(c.discarded);
-    w.put<uint8_t>(rec ? 1 : 0);
-    w.raw(ss.shift, 12);
-    w.put<uint64_t>(c.dropped);
-    w.raw(g->origin, 24);
-    w.put<uint64_t>(c.occupied);
-    if (c.occupied == 0) {
-      for (int k = 0; k < 7; ++k) w.put<uint64_t>(0);
-    } else {
-      const uint32_t V = c.V, S = c.S, K = std::min<uint32_t>(c.K, kClusterBins), F = c.nfits;
-      auto flat = d2h(g->seg.b.occ_list, V, g->stream);
-      auto mean = d2h(g->seg.b.own_mean, 3ull * V, g->stream);
-      auto cnt = d2h(g->seg.b.own_count, V, g->stream);
-      auto st = d2h(g->seg.b.own_status, V, g->stream);
-      auto nrm = d2h(g->seg.b.est_normal, 3ull * V, g->stream);
-      auto nc = d2h(g->seg.b.est_ncount, V, g->stream);
-      auto va = d2h(g->seg.b.est_valid, V, g->stream);
-      auto sidx = d2h(g->seg.b.st_idx, 3ull * S, g->stream);
-      auto smean = d2h(g->seg.b.st_mean, 3ull * S, g->stream);
-      auto snrm = d2h(g->seg.b.st_normal, 3ull * S, g->stream);
-      auto lab = d2h(g->seg.b.label, S, g->stream);
-      auto kl = d2h(g->seg.b.klabel, K, g->stream);
-      auto ks = d2h(g->seg.b.ksize, K, g->stream);
-      auto fm = d2h(g->seg.b.fit_model, 4ull * F, g->stream);
-      auto meta = d2h(g->seg.b.fit_meta, 2ull * F, g->stream);
-      auto io = d2h(g->seg.b.ioff, F + 1ull, g->stream);
-      auto rm = d2h(g->seg.b.ref_model, 4ull * F, g->stream);
-      ck(cudaStreamSynchronize(g->stream), "sync");
-      auto in = d2h(g->seg.b.inl, 3ull * io[F], g->stream);
-      ck(cudaStreamSynchronize(g->stream), "sync");
-      w.put<uint64_t>(V);
-      for (uint32_t v = 0; v < V; ++v) {
-        const uint32_t f = flat[v];
-        w.put<int32_t>(static_cast<int32_t>(f / g->ext[2] / g->ext[1]));
-        w.put<int32_t>(static_cast<int32_t>((f / g->ext[2]) % g->ext[1]));
-        w.put<int32_t>(static_cast<int32_t>(f % g->ext[2]));
-      }
-      w.raw(mean.data(), 24ull * V);
-      w.raw(cnt.data(), 4ull * V);
-      w.raw(st.data(), V);
-      w.raw(nrm.data(), 24ull * V);
-      w.raw(nc.data(), 4ull * V);
-      w.raw(va.data(), V);
-      w.put<uint64_t>(S);
-      w.raw(sidx.data(), 12ull * S);
-      w.raw(smean.data(), 24ull * S);
-      w.raw(snrm.data(), 24ull * S);
-      w.raw(lab.data(), 4ull * S);
-      w.put<uint64_t>(K);
-      for (uint32_t k = 0; k < K; ++k) {
-        w.put<int32_t>(kl[k]);
-        w.put<uint64_t>(ks[k]);
-      }
-      w.put<uint64_t>(c.skipped);
-      w.put<uint64_t>(c.unfit);
-      w.put<uint64_t>(F);
-      for (uint32_t f = 0; f < F; ++f) {
-        w.raw(&fm[4 * f], 32);
-        w.put<int32_t>(meta[2 * f]);
-        w.put<int32_t>(meta[2 * f + 1]);
-        const uint64_t m = io[f + 1] - io[f];
-        w.put<uint64_t>(m);
-        w.raw(in.data() + 3ull * io[f], 24 * m);
-      }
-      for (uint32_t f = 0; f < F; ++f) w.raw(&rm[4 * f], 32);
-      HostPolys hp;
-      g->download_polygons(hp, false);
-      w.put<uint64_t>(hp.polys.size());
-      for (const auto& q : hp.polys) {
-        w.raw(q.plane.normal, 24);
-        w.put<double>(q.plane.offset);
-        w.put<int32_t>(q.plane.inlier_count);
-        w.put<int32_t>(q.plane.cluster_label);
-        w.put<uint64_t>(q.nverts);
-        const size_t voff = static_cast<size_t>(reinterpret_cast<uintptr_t>(q.v2d));
-        for (uint32_t k = 0; k < q.nverts; ++k) w.raw(&hp.verts[5 * (voff + k)], 16);
-        for (uint32_t k = 0; k < q.nverts; ++k) w.raw(&hp.verts[5 * (voff + k) + 2], 24);
-        w.put<double>(q.area);
+    HostPolys hp;
+    if (g->h_ctr->occupied) g->download_polygons(hp, false);
+    const std::vector<uint8_t> tr = build_trace(g, *g->h_ctr, pl->frame++, rec, ss.shift, g->origin, hp);
+    *buf = static_cast<uint8_t*>(std::malloc(tr.size()));
+    if (!*buf) fail(VP_ENOMEM, "host allocation");
+    std::memcpy(*buf, tr.data(), tr.size());
+    *len = tr.size();
+  });
+}
+
+}  // extern "C"
+
+namespace {
+std::vector<uint8_t> build_trace(vp_grid* g, const Counters& c, uint32_t frame, bool rec, const int32_t* shift,
+                                 const double* origin, const HostPolys& hp) {
+  TraceW w;
+  w.raw("VPTR", 4);
+  w.put<uint32_t>(VP_TRACE_VERSION);
+  w.put<uint32_t>(frame);
+  w.put<uint64_t>(c.cleared);
+  w.put<uint64_t>(c.freed);
+  w.put<uint64_t>(c.touched);
+  w.put<uint64_t>(c.discarded);
+  w.put<uint8_t>(rec ? 1 : 0);
+  w.raw(shift, 12);
+  w.put<uint64_t>(c.dropped);
+  w.raw(origin, 24);
+  w.put<uint64_t>(c.occupied);
+  if (c.occupied == 0) {
+    for (int k = 0; k < 7; ++k) w.put<uint64_t>(0);
+  } else {
+    const uint32_t V = c.V, S = c.S, K = std::min<uint32_t>(c.K, kClusterBins), F = c.nfits;
+    auto flat = d2h(g->seg.b.occ_list, V, g->stream);
+    auto mean = d2h(g->seg.b.own_mean, 3ull * V, g->stream);
+    auto cnt = d2h(g->seg.b.own_count, V, g->stream);
+    auto st = d2h(g->seg.b.own_status, V, g->stream);
+    auto nrm = d2h(g->seg.b.est_normal, 3ull * V, g->stream);
+    auto nc = d2h(g->seg.b.est_ncount, V, g->stream);
+    auto va = d2h(g->seg.b.est_valid, V, g->stream);
+    auto sidx = d2h(g->seg.b.st_idx, 3ull * S, g->stream);
+    auto smean = d2h(g->seg.b.st_mean, 3ull * S, g->stream);
+    auto snrm = d2h(g->seg.b.st_normal, 3ull * S, g->stream);
+    auto lab = d2h(g->seg.b.label, S, g->stream);
+    auto kl = d2h(g->seg.b.klabel, K, g->stream);
+    auto ks = d2h(g->seg.b.ksize, K, g->stream);
+    auto fm = d2h(g->seg.b.fit_model, 4ull * F, g->stream);
+    auto meta = d2h(g->seg.b.fit_meta, 2ull * F, g->stream);
+    auto io = d2h(g->seg.b.ioff, F + 1ull, g->stream);
+    auto rm = d2h(g->seg.b.ref_model, 4ull * F, g->stream);
+    ck(cudaStreamSynchronize(g->stream), "sync");
+    auto in = d2h(g->seg.b.inl, 3ull * io[F], g->stream);
+    ck(cudaStreamSynchronize(g->stream), "sync");
+    w.put<uint64_t>(V);
+    for (uint32_t v = 0; v < V; ++v) {
+      const uint32_t f = flat[v];
+      w.put<int32_t>(static_cast<int32_t>(f / g->ext[2] / g->ext[1]));
+      w.put<int32_t>(static_cast<int32_t>((f / g->ext[2]) % g->ext[1]));
+      w.put<int32_t>(static_cast<int32_t>(f % g->ext[2]));
+    }
+    w.raw(mean.data(), 24ull * V);
+    w.raw(cnt.data(), 4ull * V);
+    w.raw(st.data(), V);
+    w.raw(nrm.data(), 24ull * V);
+    w.raw(nc.data(), 4ull * V);
+    w.raw(va.data(), V);
+    w.put<uint64_t>(S);
+    w.raw(sidx.data(), 12ull * S);
+    w.raw(smean.data(), 24ull * S);
+    w.raw(snrm.data(), 24ull * S);
+    w.raw(lab.data(), 4ull * S);
+    w.put<uint64_t>(K);
+    for (uint32_t k = 0; k < K; ++k) {
+      w.put<int32_t>(kl[k]);
+      w.put<uint64_t>(ks[k]);
+    }
+    w.put<uint64_t>(c.skipped);
+    w.put<uint64_t>(c.unfit);
+    w.put<uint64_t>(F);
+    for (uint32_t f = 0; f < F; ++f) {
+      w.raw(&fm[4 * f], 32);
+      w.put<int32_t>(meta[2 * f]);
+      w.put<int32_t>(meta[2 * f + 1]);
+      const uint64_t m = io[f + 1] - io[f];
+      w.put<uint64_t>(m);
+      w.raw(in.data() + 3ull * io[f], 24 * m);
+    }
+    for (uint32_t f = 0; f < F; ++f) w.raw(&rm[4 * f], 32);
+    w.put<uint64_t>(hp.polys.size());
+    for (const auto& q : hp.polys) {
+      w.raw(q.plane.normal, 24);
+      w.put<double>(q.plane.offset);
+      w.put<int32_t>(q.plane.inlier_count);
+      w.put<int32_t>(q.plane.cluster_label);
+      w.put<uint64_t>(q.nverts);
+      const size_t voff = static_cast<size_t>(reinterpret_cast<uintptr_t>(q.v2d));
+      for (uint32_t k = 0; k < q.nverts; ++k) w.raw(&hp.verts[5 * (voff + k)], 16);
+      for (uint32_t k = 0; k < q.nverts; ++k) w.raw(&hp.verts[5 * (voff + k) + 2], 24);
+      w.put<double>(q.area);
+    }
+  }
+  return std::move(w.b);
+}
+}  // namespace
+
+// ===========================================================================
+// Reference-named utilities of the C ABI (jacobi.hpp, polygonize.hpp,
+// segmentation.hpp overloads): the same device code the fused path runs.
+namespace {
+
+// Device buffer released on scope exit (stateless entry points).
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  explicit DBuf(size_t n) : p(dalloc<T>(n)) {}
+  ~DBuf() {
+    if (p) cudaFree(p);
+  }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+};
+
+// One 2-D point set as fit 0 of the scratch grid: the points (x, y, 0) on the
+// plane z = 0, whose plane_basis (polygonize.cpp:21-34) is u = e_x, v = e_y,
+// origin 0, so project_to_plane and lift_from_plane return (x, y) exactly.
+void stage_points2d(vp_grid* g, const double* pts, uint64_t n) {
+  if (n >= (1ull << 31)) fail(VP_EINVAL, "hull: too many points");
+  std::vector<double> p3(3 * n);
+  for (uint64_t i = 0; i < n; ++i) {
+    p3[3 * i] = pts[2 * i];
+    p3[3 * i + 1] = pts[2 * i + 1];
+    p3[3 * i + 2] = 0.0;
+  }
+  vp_plane pl{};
+  pl.normal[2] = 1.0;
+  pl.inlier_count = static_cast<int32_t>(n);
+  const uint64_t offs[2] = {0, n};
+  upload_fit_batch(g, 0, 1, &pl, offs, p3.data(), g->seg.b.ref_model);
+}
+
+double* copy_out2(const double* src, uint64_t m) {
+  auto* out = static_cast<double*>(std::malloc(std::max<uint64_t>(1, 2 * m) * sizeof(double)));
+  if (!out) fail(VP_ENOMEM, "host allocation");
+  if (m) std::memcpy(out, src, 2 * m * sizeof(double));
+  return out;
+}
+
+}  // namespace
+
+extern "C" {
+
+int vp_jacobi_eigen_sym3(size_t n, const double* a, double* eigenvalues, double* eigenvectors, int device) {
+  return guard([&] {
+    if (n == 0) return;
+    vp_grid* g = scratch_grid(device);
+    DBuf<double> d(21 * n);
+    h2d(d.p, a, 9 * n, g->stream);
+    LAUNCH(k_jacobi_batch, grid_for(n), kThreads, 0, g->stream, static_cast<uint64_t>(n), d.p, d.p + 9 * n,
+           d.p + 12 * n);
+    ck(cudaMemcpyAsync(eigenvalues, d.p + 9 * n, 24 * n, cudaMemcpyDeviceToHost, g->stream), "d2h");
+    ck(cudaMemcpyAsync(eigenvectors, d.p + 12 * n, 72 * n, cudaMemcpyDeviceToHost, g->stream), "d2h");
+    ck(cudaStreamSynchronize(g->stream), "sync");
+  });
+}
+
+int vp_convex_hull(const double* pts, uint64_t n, int directions, int device, double** out, uint64_t* m) {
+  *out = nullptr;
+  *m = 0;
+  return guard([&] {
+    if (n < 3) {  // monotone_chain: fewer than three points -> empty
+      *out = copy_out2(pts, 0);
+      return;
+    }
+    vp_grid* g = scratch_grid(device);
+    stage_points2d(g, pts, n);
+    g->launch_polygon(directions, -std::numeric_limits<double>::infinity());
+    g->read_counters();
+    if (g->h_ctr->overflow & kOverflowPool) fail(VP_ENOMEM, "polygon vertex pool overflow");
+    HostPolys hp;
+    g->download_polygons(hp, true);
+    std::vector<double> ring;
+    if (!hp.polys.empty()) {
+      const vp_polygon& q = hp.polys[0];
+      const size_t voff = static_cast<size_t>(reinterpret_cast<uintptr_t>(q.v2d));
+      for (uint32_t k = 0; k < q.nverts; ++k) {
+        ring.push_back(hp.verts[5 * (voff + k)]);
+        ring.push_back(hp.verts[5 * (voff + k) + 1]);
       }
     }
-    *buf = static_cast<uint8_t*>(std::malloc(w.b.size()));
-    std::memcpy(*buf, w.b.data(), w.b.size());
-    *len = w.b.size();
+    *m = ring.size() / 2;
+    *out = copy_out2(ring.data(), *m);
+  });
+}
+
+int vp_monotone_chain(const double* pts, uint64_t n, int device, double** out, uint64_t* m) {
+  return vp_convex_hull(pts, n, 0, device, out, m);
+}
+
+int vp_hull_filter(const double* pts, uint64_t n, int directions, int device, double** out, uint64_t* m) {
+  *out = nullptr;
+  *m = 0;
+  return guard([&] {
+    if (n <= 3 || directions < 3) {  // polygonize.cpp:51: nothing to filter
+      *m = n;
+      *out = copy_out2(pts, n);
+      return;
+    }
+    vp_grid* g = scratch_grid(device);
+    const uint32_t n32 = static_cast<uint32_t>(n);
+    g->seg.ensure(std::max(g->seg.b.Vcap, n32), g->seg.b.Scap, std::max(g->seg.b.Icap, n32), 100,
+                  g->gd.nwords);  // flag-scan block sums for n points
+    stage_points2d(g, pts, n);
+    g->seg.ensure_dirs(directions, g->stream);
+    cudaStream_t st = g->stream;
+    LAUNCH(k_poly_setup, 1, 1024, 0, st, g->ctr, g->seg.b);
+    LAUNCH(k_poly_extremes, g->chain_wide, 256, 0, st, g->ctr, g->seg.b, g->seg.dirtab, directions);
+    LAUNCH(k_poly_inner, 1, 64, 0, st, g->ctr, g->seg.b, directions);
+    DBuf<uint8_t> flags(n);
+    DBuf<uint32_t> pos(n + 2);
+    DBuf<double> outd(2 * n);
+    const uint32_t nn[2] = {static_cast<uint32_t>(n), 0u};
+    h2d(pos.p + n, nn, 2, st);
+    LAUNCH(k_poly_keep_flags, grid_for(n), kThreads, 0, st, g->ctr, g->seg.b, flags.p);
+    g->launch_flag_scan(flags.p, pos.p + n, static_cast<uint32_t>(n), pos.p, pos.p + n + 1);
+    LAUNCH(k_gather_p2, grid_for(n), kThreads, 0, st, pos.p + n, flags.p, pos.p, g->seg.b.proj, outd.p);
+    uint32_t kept = 0;
+    ck(cudaMemcpyAsync(&kept, pos.p + n + 1, 4, cudaMemcpyDeviceToHost, st), "d2h");
+    ck(cudaStreamSynchronize(st), "sync");
+    std::vector<double> h(2ull * kept);
+    if (kept) ck(cudaMemcpy(h.data(), outd.p, 16ull * kept, cudaMemcpyDeviceToHost), "d2h");
+    *m = kept;
+    *out = copy_out2(h.data(), kept);
+  });
+}
+
+int vp_label_components_adjacency(uint64_t n, const uint64_t* row_offsets, const int32_t* cols, int device,
+                                  int32_t* labels) {
+  return guard([&] {
+    if (n == 0) return;
+    if (n >= (1ull << 31)) fail(VP_EINVAL, "label_components: too many voxels");
+    vp_grid* g = scratch_grid(device);
+    cudaStream_t st = g->stream;
+    const uint64_t ne = row_offsets[n];
+    DBuf<uint64_t> rows(n + 1);
+    DBuf<int32_t> c(std::max<uint64_t>(ne, 1)), parent(n), lab(n);
+    h2d(rows.p, row_offsets, n + 1, st);
+    h2d(c.p, cols, ne, st);
+    LAUNCH(k_iota, grid_for(n), kThreads, 0, st, parent.p, n);
+    LAUNCH(k_label_edges, grid_for(32 * n, 148 * 32), kThreads, 0, st, n, rows.p, c.p, parent.p);
+    LAUNCH(k_label_flatten, grid_for(n), kThreads, 0, st, n, parent.p, lab.p);
+    ck(cudaMemcpyAsync(labels, lab.p, 4 * n, cudaMemcpyDeviceToHost, st), "d2h");
+    ck(cudaStreamSynchronize(st), "sync");
+  });
+}
+
+int vp_classify_estimates(vp_grid* g, const vp_seg_params* p, size_t n, const int32_t* idx,
+                          const int32_t* neighbor_count, const double* angle_to_up_deg, const uint8_t* valid,
+                          uint8_t* status) {
+  return guard([&] {
+    if (n == 0) return;
+    cudaStream_t st = g->stream;
+    DBuf<int32_t> di(3 * n), dn(n);
+    DBuf<double> da(n);
+    DBuf<uint8_t> dv(n), ds(n);
+    h2d(di.p, idx, 3 * n, st);
+    h2d(dn.p, neighbor_count, n, st);
+    h2d(da.p, angle_to_up_deg, n, st);
+    h2d(dv.p, valid, n, st);
+    LAUNCH(k_classify_estimates, grid_for(n), kThreads, 0, st, static_cast<uint64_t>(n), dn.p, da.p, dv.p,
+           p->min_neighbors, p->max_angle_deg, ds.p);
+    g->fill_static_params();
+    g->h_fp->n = 0;
+    g->upload_params();
+    LAUNCH(k_set_statuses, grid_for(n), kThreads, 0, st, g->gd, g->d_fp, di.p, ds.p, static_cast<uint64_t>(n));
+    ck(cudaMemcpyAsync(status, ds.p, n, cudaMemcpyDeviceToHost, st), "d2h");
+    ck(cudaStreamSynchronize(st), "sync");
   });
 }
 

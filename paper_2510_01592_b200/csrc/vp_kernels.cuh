@@ -16,6 +16,11 @@ constexpr int kChunk = 256;         // ordinals per counting-sort chunk (one war
 #define VP_HULL_SMEM 1024
 #endif
 constexpr int kHullSmem = VP_HULL_SMEM;  // survivors sorted in shared memory (6 regions of this size)
+// k_poly_hull: 256 threads own kHullSmem / 256 sorted entries each (a 32-bit keep mask),
+// and the six regions of 16-byte points must fit the opt-in shared memory
+static_assert(kHullSmem >= 256 && kHullSmem % 256 == 0 && kHullSmem / 256 <= 32 &&
+                  kHullSmem * 16 * 6 <= 227 * 1024,
+              "VP_HULL_SMEM must be a multiple of 256 in [256, 2304]");
 constexpr int kPolyChunk = 1024;    // inlier points per polygon-stage block
 #ifndef VP_FOLD_SMALL
 #define VP_FOLD_SMALL 24
@@ -71,6 +76,16 @@ __device__ __forceinline__ uint32_t block_sum_u32(uint32_t v) {
   const uint32_t r = tot;
   __syncthreads();
   return r;
+}
+
+// 2-D points of the polygon stage (polygonize.cpp): lexicographic order and
+// the orientation test cross2 (o, a, b) in the reference's expression order.
+struct P2 {
+  double x, y;
+};
+__device__ __forceinline__ bool lex_less(P2 a, P2 b) { return a.x < b.x || (a.x == b.x && a.y < b.y); }
+__device__ __forceinline__ double cross2(P2 o, P2 a, P2 b) {
+  return (a.x - o.x) * (b.y - o.y) - (a.y - o.y) * (b.x - o.x);
 }
 
 // Union-find over int32 parent arrays (CCL and the slab boundary merge).
@@ -353,6 +368,19 @@ __global__ void k_poly_extremes(Counters* ctr, SegBufs b, const double* dirtab, 
 __global__ void k_poly_inner(Counters* ctr, SegBufs b, int directions);
 __global__ void k_poly_keep(Counters* ctr, SegBufs b);
 __global__ void k_poly_hull(Counters* ctr, SegBufs b, double min_area);
+__global__ void k_chain_rearm(Counters* ctr);
+__global__ void k_poly_pack(const Counters* ctr, SegBufs b, double* out, uint64_t cap);
+
+// ---- kernels (k_api.cu)
+__global__ void k_jacobi_batch(uint64_t n, const double* a, double* vals, double* vecs);
+__global__ void k_poly_keep_flags(Counters* ctr, SegBufs b, uint8_t* flags);
+__global__ void k_gather_p2(const uint32_t* n_ptr, const uint8_t* flags, const uint32_t* pos, const double* proj,
+                            double* out);
+__global__ void k_iota(int32_t* a, uint64_t n);
+__global__ void k_label_edges(uint64_t n, const uint64_t* rows, const int32_t* cols, int32_t* parent);
+__global__ void k_label_flatten(uint64_t n, int32_t* parent, int32_t* label);
+__global__ void k_classify_estimates(uint64_t n, const int32_t* ncount, const double* angle, const uint8_t* valid,
+                                     int min_neighbors, double max_angle, uint8_t* status);
 
 // ---- kernels (k_slab.cu)
 __global__ void k_plane_counts(const Counters* ctr, const int32_t* st_idx, uint32_t cap, int32_t x0,

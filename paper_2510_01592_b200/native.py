@@ -99,6 +99,11 @@ class FrameTiming(C.Structure):
                 ("points", C.c_uint64), ("voxels", C.c_uint64), ("clusters", C.c_uint64)]
 
 
+class RunOutputs(C.Structure):
+    _fields_ = [("per_frame", C.POINTER(C.POINTER(Polygons))), ("timings", C.POINTER(FrameTiming)),
+                ("traces", C.POINTER(C.POINTER(C.c_uint8))), ("trace_lens", C.POINTER(C.c_uint64))]
+
+
 def default_params(seed: int = 0, refine: bool = True, min_area: float = 0.002,
                    refine_exact: bool = False) -> PipelineParams:
     """SegmentationParams / RansacParams / RunConfig / OutputConfig defaults."""
@@ -226,6 +231,54 @@ class Pipeline:
                                     C.byref(out) if want_polygons else None, tms if timings else None))
         polys = polygons_to_py(out) if want_polygons else None
         return (polys, [tms[k] for k in range(nf)]) if timings else polys
+
+    def run_frames(self, frames, device_ptrs=None, per_frame=True, timings=True, traces=False):
+        """vp_pipeline_run_frames: the pipelined run with per-frame outputs.
+        Returns dict(polygons=final, per_frame=[...], timings=[...], traces=[bytes])."""
+        nf = len(frames)
+        R = np.ascontiguousarray(np.stack([np.asarray(f.rotation, np.float64).reshape(9) for f in frames]))
+        t = np.ascontiguousarray(np.stack([np.asarray(f.translation, np.float64).reshape(3) for f in frames]))
+        ptrs = (C.c_void_p * max(nf, 1))()
+        ns = np.zeros(max(nf, 1), np.uint64)
+        keep = []
+        if device_ptrs is not None:
+            for k, (ptr, n) in enumerate(device_ptrs):
+                ptrs[k] = ptr
+                ns[k] = n
+        else:
+            for k, f in enumerate(frames):
+                a = np.ascontiguousarray(f.points, np.float32)
+                keep.append(a)
+                ptrs[k] = a.ctypes.data
+                ns[k] = len(a)
+        ex = RunOutputs()
+        pf = (C.POINTER(Polygons) * max(nf, 1))()
+        tms = (FrameTiming * max(nf, 1))()
+        trs = (C.POINTER(C.c_uint8) * max(nf, 1))()
+        tls = (C.c_uint64 * max(nf, 1))()
+        if per_frame:
+            ex.per_frame = C.cast(pf, C.POINTER(C.POINTER(Polygons)))
+        if timings:
+            ex.timings = C.cast(tms, C.POINTER(FrameTiming))
+        if traces:
+            ex.traces = C.cast(trs, C.POINTER(C.POINTER(C.c_uint8)))
+            ex.trace_lens = C.cast(tls, C.POINTER(C.c_uint64))
+        out = C.POINTER(Polygons)()
+        check(lib().vp_pipeline_run_frames(self.h, C.c_size_t(nf), ptrs, _p(ns, C.c_uint64), _p(R, C.c_double),
+                                           _p(t, C.c_double), C.c_int(1 if device_ptrs is not None else 0),
+                                           C.byref(out), C.byref(ex)))
+        res = dict(polygons=polygons_to_py(out))
+        if per_frame:
+            res["per_frame"] = [polygons_to_py(pf[k]) for k in range(nf)]
+        if timings:
+            res["timings"] = [tms[k] for k in range(nf)]
+        if traces:
+            tr = []
+            for k in range(nf):
+                tr.append(C.string_at(trs[k], tls[k]))
+                lib().vp_free(trs[k])
+            res["traces"] = tr
+        return res
 
     def run_ptrs(self, ptr_array, n_array, R_array, t_array, device_ptrs, want_polygons, convert=True):
         """Low-overhead vp_pipeline_run on prebuilt ctypes arrays (bench).

@@ -188,16 +188,23 @@ def lidar_stair_frames(frames=6, rays=200_000, seed=11):
     return render(stock_scene(STAIR5), sensor, default_trajectory(STAIR5, frames, 20.0), seed)
 
 
-def stepping_stones():
-    """C2 scene: Stair5 plus six 0.3 x 0.3 m stepping stones (0.05-0.15 m) on the approach floor."""
-    s = stock_scene(STAIR5)
+def stepping_stone_boxes():
+    """The six 0.3 x 0.3 m stepping stones (0.05-0.15 m) C2 adds on the Stair5 approach floor."""
     heights = [0.05, 0.08, 0.10, 0.12, 0.15, 0.06]
+    out = []
     k = 0
     for cx in (-1.05, -0.72, -0.39):
         for cy in (-0.3, 0.3):
             h = heights[k]
             k += 1
-            s.boxes.append(((cx - 0.15, cy - 0.15, 0.0), (cx + 0.15, cy + 0.15, h)))
+            out.append(((cx - 0.15, cy - 0.15, 0.0), (cx + 0.15, cy + 0.15, h)))
+    return out
+
+
+def stepping_stones():
+    """C2 scene: Stair5 plus six 0.3 x 0.3 m stepping stones (0.05-0.15 m) on the approach floor."""
+    s = stock_scene(STAIR5)
+    s.boxes.extend(stepping_stone_boxes())
     return s
 
 

@@ -75,6 +75,10 @@ class CpuSession:
     def frame(self, pts, R, t):
         return parse_trace(self.frame_raw(pts, R, t))
 
+    def set_fixed(self, fixed=True):
+        """Fixed window: no recenter (the C5 map / slab path)."""
+        getattr(self.lib, f"{self.prefix}_session_set_fixed")(C.c_void_p(self.h), C.c_int(1 if fixed else 0))
+
     def cells(self):
         sums = np.zeros((self.ncells, 3))
         cnt = np.zeros(self.ncells, np.uint32)

@@ -1,0 +1,156 @@
+"""GPU tier: the benchmarked configurations at full size, in bench mode,
+against the reference CPU implementation (oracle/_ref: the unmodified
+reference sources, multithreaded; the C restatement when _ref is absent).
+
+Bench mode = what bench.py times: vp_pipeline_run (frames in flight, the
+mapping of frame k+1 overlapping frame k's fitting), tree-reduced refine
+(refine_exact = 0), every frame of the stream. Every frame of the pipelined
+run hands back its stage trace, which is compared with the reference's:
+
+* bit-exact: clear/integrate/recenter stats, occupied voxels (indices, FP64
+  means, counts, statuses), normals, steppable list, canonical labels,
+  clusters, RANSAC models, inlier counts and inlier sets;
+* tolerance (north_star): refined normals within 1e-4 rad, offsets within
+  1e-4 m, polygon vertices within 1e-5 m (symmetric Hausdorff), same polygon
+  list (labels, inlier counts).
+
+C5 (the multi-GPU map: fixed window, spatial slabs) runs through one slab
+and through four virtual slabs: slab output equals the one-slab output
+bitwise, and both match the reference's fixed-window run (steppable list
+bit-exact, polygons within tolerance).
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from cpu_oracles import CpuSession
+from paper_2510_01592_b200 import native, scenes, slabs
+from paper_2510_01592_b200.trace import format_polygons, parse_trace
+from test_gpu_parity import check_tolerance, hausdorff, NORMAL_TOL, OFFSET_TOL, VERTEX_TOL
+
+pytestmark = pytest.mark.gpu
+
+CHECKER = "ref" if CpuSession.available("ref") else "oracle"
+
+
+def polys_equal_trace(per_frame, trace):
+    assert [(p["label"], p["inlier_count"]) for p in per_frame] == \
+           [(p["label"], p["inlier_count"]) for p in trace.polygons]
+    for a, b in zip(per_frame, trace.polygons):
+        assert a["v3d"].tobytes() == b["v3d"].tobytes() and a["area"] == b["area"]
+
+
+def pipelined_vs_reference(wl, nframes, use_device_inputs=False):
+    frames = wl.frames[:nframes]
+    p = native.default_params(seed=wl.seed)          # bench.py's parameters (tree refine)
+    gpu = native.Pipeline(wl.resolution, wl.extent, frames[0].translation, p)
+    dev = None
+    if use_device_inputs:
+        dev = [torch.from_numpy(np.ascontiguousarray(f.points)).cuda() for f in frames]
+    out = gpu.run_frames(frames, device_ptrs=[(d.data_ptr(), len(d)) for d in dev] if dev else None,
+                         per_frame=True, timings=True, traces=True)
+    gpu.close()
+    ref = CpuSession(CHECKER, wl.resolution, wl.extent, frames[0].translation, p)
+    npoly = 0
+    for k, f in enumerate(frames):
+        ta = parse_trace(out["traces"][k])
+        tb = ref.frame(f.points, f.rotation, f.translation)
+        try:
+            check_tolerance(ta, tb)
+        except AssertionError as e:
+            raise AssertionError(f"{wl.name} frame {k}: {e}") from None
+        polys_equal_trace(out["per_frame"][k], ta)
+        tm = out["timings"][k]
+        assert tm.total_ms > 0 and tm.points == len(f.points) and tm.voxels == ta.occupied_count
+        npoly += len(ta.polygons)
+    ref.close()
+    assert format_polygons(out["polygons"]) == format_polygons(out["per_frame"][-1])
+    return npoly
+
+
+def test_c2_all_frames_bench_mode():
+    # BASELINE configs[1]: the headline workload, all 30 frames at 500^3
+    assert pipelined_vs_reference(scenes.workload("c2"), 30) > 30 * 3
+
+
+def test_c2_device_resident_inputs():
+    # bench.py's `value` leg: points already in HBM
+    pipelined_vs_reference(scenes.workload("c2", frames=12), 12, use_device_inputs=True)
+
+
+def test_c3_all_frames_bench_mode():
+    # configs[2]: open-tread stairs + overhanging table (multi-layer planes)
+    assert pipelined_vs_reference(scenes.workload("c3"), 30) > 30
+
+
+def test_c4_lidar_bench_mode():
+    # configs[3]: ~1 M points / frame sphere LiDAR
+    assert pipelined_vs_reference(scenes.workload("c4", frames=5), 5) > 0
+
+
+def _mem_available_gb():
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemAvailable:"):
+                return int(line.split()[1]) / 2**20
+    except OSError:
+        pass
+    return 0.0
+
+
+def c5_window():
+    # the full 2000 x 2000 x 300 window needs ~45 GB of host RAM in the
+    # reference (38.4 GB of cells); a 1000 x 1000 x 300 window around the same
+    # centre otherwise (points outside are discarded by both sides)
+    return scenes.C5_EXTENT if _mem_available_gb() > 80 else (1000, 1000, 300)
+
+
+def test_c5_slabs_vs_reference():
+    # configs[4]: the slab path through 1 slab and 4 virtual slabs, fixed window
+    ext = c5_window()
+    wl = scenes.c5_workload(2)
+    p = native.default_params(seed=2025)
+    one = slabs.Slab(0.01, ext, scenes.C5_CENTER, 0, ext[0])
+    q = ext[0] // 4
+    four = [slabs.Slab(0.01, ext, scenes.C5_CENTER, a, b) for a, b in
+            [(0, q), (q, 2 * q + 3), (2 * q + 3, 3 * q), (3 * q, ext[0])]]
+    ref = CpuSession(CHECKER, 0.01, ext, scenes.C5_CENTER, p)
+    ref.set_fixed(True)
+    for k, f in enumerate(wl.frames):
+        pts = torch.from_numpy(np.ascontiguousarray(f.points)).cuda()
+        pa = slabs.slab_frame([one], slabs.LocalComm(1), pts, f.rotation, f.translation, p)
+        pb = slabs.slab_frame(four, slabs.LocalComm(4), pts, f.rotation, f.translation, p)
+        assert format_polygons(pa) == format_polygons(pb), f"frame {k}: 4 slabs differ from one"
+        tb = ref.frame(f.points, f.rotation, f.translation)
+        S, (idx_t, mean_t, nrm_t) = one.steppable(p.seg)
+        idx = idx_t.cpu().numpy().view(np.int32).reshape(S, 3)
+        mean = mean_t.cpu().numpy().view(np.float64).reshape(S, 3)
+        nrm = nrm_t.cpu().numpy().view(np.float64).reshape(S, 3)
+        assert S == len(tb.st_idx)
+        assert idx.tobytes() == tb.st_idx.tobytes()
+        assert mean.tobytes() == tb.st_mean.tobytes() and nrm.tobytes() == tb.st_normal.tobytes()
+        assert [(x["label"], x["inlier_count"]) for x in pa] == \
+               [(x["label"], x["inlier_count"]) for x in tb.polygons]
+        for x, y in zip(pa, tb.polygons):
+            ang = np.arccos(np.clip(np.dot(x["normal"], y["normal"]), -1.0, 1.0))
+            assert ang <= NORMAL_TOL and abs(x["offset"] - y["offset"]) <= OFFSET_TOL
+            assert hausdorff(x["v3d"], y["v3d"]) <= VERTEX_TOL
+        assert len(pa) >= 2
+    for s in [one, *four]:
+        s.close()
+    ref.close()
+
+
+@pytest.mark.parametrize("name", ["t1", "stair"])
+def test_pipelined_traces_equal_frame_path(name):
+    # every frame's trace from the pipelined run == the frame-by-frame trace
+    from workloads import run_config
+    frames, res, ext, seed, run = run_config(name)
+    p = native.default_params(seed=seed, refine_exact=True)
+    a = native.Pipeline(res, ext, frames[0].translation, p)
+    out = a.run_frames(frames, traces=True)
+    b = native.Pipeline(res, ext, frames[0].translation, p)
+    for k, f in enumerate(frames):
+        assert out["traces"][k] == b.frame_trace_raw(f.points, f.rotation, f.translation), f"frame {k}"

@@ -167,3 +167,20 @@ def test_acos_threshold_is_monotone_here():
     # a single False->True transition
     assert vals == sorted(vals)
     assert xs
+
+
+def test_reference_arm_frames_match():
+    """bench.py --impl reference renders C2 through oracle/_ref alone (it never
+    loads this repository's library); its frames must be the B200 arm's bytes."""
+    if not CpuSession.available("ref"):
+        pytest.skip("oracle/_ref not built")
+    import bench
+    from paper_2510_01592_b200 import scenes
+    L, _ = bench.ref_lib()
+    a = bench.ref_workload_c2(L)
+    b = scenes.workload("c2").frames
+    assert len(a) == len(b) == 30
+    for fa, fb in zip(a, b):
+        assert fa.points.tobytes() == fb.points.tobytes()
+        assert fa.rotation.tobytes() == fb.rotation.tobytes()
+        assert fa.translation.tobytes() == fb.translation.tobytes()

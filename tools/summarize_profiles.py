@@ -53,6 +53,10 @@ def full(path):
             mem_pct=g("gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed"),
             warps_active=g("sm__warps_active.avg.pct_of_peak_sustained_active"),
             regs=g("launch__registers_per_thread"), stalls=st[:5],
+            inst=g("smsp__inst_executed.sum"), red=g("lts__t_sectors_srcunit_tex_op_red.sum"),
+            atom=g("lts__t_sectors_srcunit_tex_op_atom.sum"),
+            atom_unit=g("lts__d_atomic_input_cycles_active.avg.pct_of_peak_sustained_elapsed"), l1_red=g("l1tex__t_requests_pipe_lsu_mem_global_op_red.sum"),
+            l1_atom=g("l1tex__t_requests_pipe_lsu_mem_global_op_atom.sum"),
             pipes={k: g(m)[0] for k, m in PIPES.items()})
     return out
 
@@ -85,7 +89,7 @@ def main(tag):
         for k, (t, n) in sorted(agg.items(), key=lambda kv: -kv[1][0]):
             f.write(f"{k:28s} {n:8d} {t / 1e3:10.1f} {t / 1e3 / n:10.2f} {100 * t / tot:6.1f}%\n")
     fl = full(os.path.join(src, f"{tag}_top.ncu-rep"))
-    traffic, pipes = {}, {}
+    traffic, pipes, inst, atomics = {}, {}, {}, {}
     with open(os.path.join(dst, f"{tag}_ncu_top.txt"), "w") as f:
         f.write("# ncu --set full --clock-control none, one launch per kernel (C2 frame ~10)\n")
         for k, d in fl.items():
@@ -99,8 +103,23 @@ def main(tag):
             f.write("   stalls per issue: " + ", ".join(f"{n}={v:.2f}" for v, n in d["stalls"]) + "\n")
             pipes[k] = {n: round(v, 1) for n, v in d["pipes"].items() if v is not None}
             f.write("   utilisation %: " + ", ".join(f"{n} {v}" for n, v in pipes[k].items()) + "\n")
+            us = d["time"][0] * {"ns": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}.get(d["time"][1], 1.0)
+            if d["inst"][0] is not None:
+                inst[k] = d["inst"][0]
+                f.write(f"   warp instructions {d['inst'][0]:.0f} ({d['inst'][0] / us / 1e3:.1f} G/s)\n")
+            a = {n: d[n][0] for n in ("red", "atom", "l1_red", "l1_atom") if d[n][0] is not None}
+            if a:
+                atomics[k] = {"l2_red_sectors": a.get("red"), "l2_atom_sectors": a.get("atom"),
+                              "l1_red_requests": a.get("l1_red"), "l1_atom_requests": a.get("l1_atom"),
+                              "l2_red_atom_sectors_per_s": round(((a.get("red") or 0) + (a.get("atom") or 0))
+                                                                 / (us * 1e-6), 1),
+                              "l2_atomic_unit_pct": d["atom_unit"][0]}
+                f.write("   atomics: L2 RED sectors %s, L2 ATOM sectors %s, L1 RED req %s, L1 ATOM req %s "
+                        "(L2 RED+ATOM %.2f G sectors/s; L2 atomic unit busy %s%% of peak)\n"
+                        % (a.get("red"), a.get("atom"), a.get("l1_red"), a.get("l1_atom"),
+                           atomics[k]["l2_red_atom_sectors_per_s"] / 1e9, d["atom_unit"][0]))
     json.dump({"source": f"profiles/{tag}_ncu_top.txt", "dram_bytes_per_launch": traffic,
-               "utilisation_pct": pipes},
+               "utilisation_pct": pipes, "warp_inst_per_launch": inst, "atomics_per_launch": atomics},
               open(os.path.join(dst, "ncu_traffic.json"), "w"), indent=1)
     print(open(os.path.join(dst, f"{tag}_kernel_shares.txt")).read())
     print(open(os.path.join(dst, f"{tag}_ncu_top.txt")).read())
