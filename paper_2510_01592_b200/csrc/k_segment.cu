@@ -301,6 +301,18 @@ __global__ void k_ccl_compress(Counters* ctr, SegBufs b) {
     __stcg(b.parent + i, uf_find(b.parent, static_cast<int>(i)));
 }
 
+// One pointer-jumping round over the hook forest (parent[i] <- parent[parent[i]]):
+// two rounds before k_ccl_compress cut the hook chains (C2: up to ~31 deep)
+// by 4x, so compression is no longer one thread's long serial chain.
+__global__ void k_ccl_jump(Counters* ctr, SegBufs b) {
+  const uint32_t S = min(ctr->S, b.Scap);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < S; i += gridDim.x * blockDim.x) {
+    const int p = __ldcg(b.parent + i);
+    const int pp = __ldcg(b.parent + p);
+    if (pp < p) __stcg(b.parent + i, pp);
+  }
+}
+
 // CCL phase 2: every forward edge (i, j > i) as a union. The 4-byte parent[j]
 // is checked against i's cached root before the 48-byte predicate loads, so
 // edges inside an already-joined tree cost one load.
@@ -348,6 +360,299 @@ __global__ void __launch_bounds__(256) k_ccl_union(Counters* ctr, SegDev sp, Seg
       }
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// Edge-balanced variants of k_ccl_hook / k_ccl_union (the default CCL).
+// The row-per-lane kernels above walk a row's present voxels serially: a
+// lane's dependent loads (bitmap word -> ordinal -> parent[j] -> predicate,
+// once per present bit) form a chain of ~20 L2 round trips per voxel, and a
+// plane voxel has ~11 non-empty rows of up to 11 voxels spread over 61 rows.
+// Here the warp first lists its voxel's candidate ordinals in shared memory
+// (one bitmap word + one ordinal load per row, all rows in parallel, then a
+// warp scan of the popcounts), and the lanes then take the candidates 32 at a
+// time, so every voxel costs ~4 dependent round trips whatever its degree.
+// Same edges, same link rule -> the same canonical labels.
+// ---------------------------------------------------------------------------
+constexpr int kCclWarps = 8;     // 256-thread blocks
+constexpr int kCclEdgeBuf = 256; // candidate ordinals per warp and pass
+
+// Lists the present voxels of this lane's row (X, Y, z0..z1) into buf at
+// [pos - base, ...) clipped to [0, kCclEdgeBuf), ascending ordinal.
+__device__ __forceinline__ void ccl_list_row(int32_t* buf, uint32_t bits, int j0, uint32_t pos, uint32_t base) {
+  int j = j0;
+  while (bits) {
+    bits &= bits - 1;
+    if (pos >= base && pos < base + kCclEdgeBuf) buf[pos - base] = j;
+    ++pos;
+    ++j;
+  }
+}
+
+// Row (X, Y) of the window and its z range for voxel (x, y, z), backward or
+// forward half; false when it leaves the map box. Out: present bits and the
+// ordinal of the first present voxel.
+__device__ __forceinline__ uint32_t ccl_row_bits(const MapDesc& m, int w, int span, int r, bool backward, int x,
+                                                 int y, int z, int& j0) {
+  int dx, dy;
+  window_row(r, w, span, backward, dx, dy);
+  const int X = x + dx, Y = y + dy;
+  j0 = 0;
+  if (X < m.lo[0] || X > m.lo[0] + m.dims[0] - 1 || Y < m.lo[1] || Y > m.lo[1] + m.dims[1] - 1) return 0u;
+  const int zlo = m.lo[2], zhi = m.lo[2] + m.dims[2] - 1;
+  int z0, z1;
+  if (dx == 0 && dy == 0) {
+    z0 = backward ? max(z - w, zlo) : z + 1;
+    z1 = backward ? z - 1 : min(z + w, zhi);
+  } else {
+    z0 = max(z - w, zlo);
+    z1 = min(z + w, zhi);
+  }
+  if (z0 > z1) return 0u;
+  const uint32_t bits = m.row_span(X, Y, z0, z1 - z0 + 1);
+  if (bits) j0 = __ldg(m.map + m.slot(X, Y, z0 + __ffs(bits) - 1));
+  return bits;
+}
+
+// Phase 1: parent[i] = the smallest adjacent ordinal j < i, else i. Backward
+// rows are taken 32 at a time in ascending ordinal order (the last rows of
+// the window first), their candidates tested 32 at a time; the first adjacent
+// candidate is the minimum.
+__global__ void __launch_bounds__(256) k_ccl_hook_bal(Counters* ctr, SegDev sp, SegBufs b, MapDesc m) {
+  __shared__ int32_t cand[kCclWarps][kCclEdgeBuf];
+  const uint32_t S = min(ctr->S, b.Scap);
+  const int w = sp.w, span = 2 * w + 1;
+  const int nrows = (w + 1) + w * span;
+  const unsigned lane = lane_id();
+  int32_t* buf = cand[threadIdx.x >> 5];
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarp = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t i = warp; i < S; i += nwarp) {
+    const int x = __ldg(b.st_idx + 3 * i), y = __ldg(b.st_idx + 3 * i + 1), z = __ldg(b.st_idx + 3 * i + 2);
+    const d3 mi = mk3(__ldg(b.st_mean + 3 * i), __ldg(b.st_mean + 3 * i + 1), __ldg(b.st_mean + 3 * i + 2));
+    const d3 ni = mk3(__ldg(b.st_normal + 3 * i), __ldg(b.st_normal + 3 * i + 1),
+                      __ldg(b.st_normal + 3 * i + 2));
+    int best = static_cast<int>(i);
+    for (int r0 = nrows - 1; r0 >= 0 && best == static_cast<int>(i); r0 -= 32) {
+      const int r = r0 - static_cast<int>(lane);
+      int j0 = 0;
+      const uint32_t bits = r >= 0 ? ccl_row_bits(m, w, span, r, true, x, y, z, j0) : 0u;
+      const uint32_t c = __popc(bits);
+      uint32_t incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (static_cast<int>(lane) >= o) incl += t;
+      }
+      const uint32_t E = __shfl_sync(0xffffffffu, incl, 31);
+      for (uint32_t base = 0; base < E && best == static_cast<int>(i); base += kCclEdgeBuf) {
+        ccl_list_row(buf, bits, j0, incl - c, base);
+        __syncwarp();
+        const uint32_t nE = min(E - base, static_cast<uint32_t>(kCclEdgeBuf));
+        for (uint32_t e0 = 0; e0 < nE; e0 += 32) {
+          const uint32_t e = e0 + lane;
+          const bool adj = e < nE && adjacent(b, sp, mi, ni, buf[e]);
+          const unsigned bal = __ballot_sync(0xffffffffu, adj);
+          if (bal) {  // candidates ascend with e: the first adjacent one is the minimum
+            best = buf[e0 + __ffs(bal) - 1];
+            break;
+          }
+        }
+        __syncwarp();
+      }
+    }
+    if (lane == 0) {
+      b.parent[i] = best;
+      b.cnt[i] = 0;
+      b.cid[i] = -1;
+    }
+  }
+}
+
+// Phase 2: every forward edge (i, j > i) as a union, candidates spread over
+// the lanes. Each lane keeps its own view of root(i) (an ancestor: roots only
+// move down); the lanes pool the smallest after every batch.
+__device__ __forceinline__ void ccl_union_bal_body(Counters* ctr, const SegDev& sp, const SegBufs& b,
+                                                   const MapDesc& m) {
+  __shared__ int32_t cand[kCclWarps][kCclEdgeBuf];
+  const uint32_t S = min(ctr->S, b.Scap);
+  const int w = sp.w, span = 2 * w + 1;
+  const int nrows = (w + 1) + w * span;
+  int32_t* parent = b.parent;
+  const unsigned lane = lane_id();
+  int32_t* buf = cand[threadIdx.x >> 5];
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarp = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t i = warp; i < S; i += nwarp) {
+    const int x = __ldg(b.st_idx + 3 * i), y = __ldg(b.st_idx + 3 * i + 1), z = __ldg(b.st_idx + 3 * i + 2);
+    int ri = -1;
+    if (lane == 0) ri = uf_find(parent, static_cast<int>(i));
+    const d3 mi = mk3(__ldg(b.st_mean + 3 * i), __ldg(b.st_mean + 3 * i + 1), __ldg(b.st_mean + 3 * i + 2));
+    const d3 ni = mk3(__ldg(b.st_normal + 3 * i), __ldg(b.st_normal + 3 * i + 1),
+                      __ldg(b.st_normal + 3 * i + 2));
+    for (int r0 = 0; r0 < nrows; r0 += 64) {
+      // two rows per lane per pass (the forward half has 61 rows at w = 5)
+      int ja = 0, jb = 0;
+      const int ra = r0 + static_cast<int>(lane), rb = ra + 32;
+      const uint32_t ba = ra < nrows ? ccl_row_bits(m, w, span, ra, false, x, y, z, ja) : 0u;
+      const uint32_t bb = rb < nrows ? ccl_row_bits(m, w, span, rb, false, x, y, z, jb) : 0u;
+      const uint32_t ca = __popc(ba), c = ca + __popc(bb);
+      uint32_t incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (static_cast<int>(lane) >= o) incl += t;
+      }
+      const uint32_t E = __shfl_sync(0xffffffffu, incl, 31);
+      ri = __reduce_min_sync(0xffffffffu, ri < 0 ? 0x7fffffff : ri);
+      for (uint32_t base = 0; base < E; base += kCclEdgeBuf) {
+        ccl_list_row(buf, ba, ja, incl - c, base);
+        ccl_list_row(buf, bb, jb, incl - c + ca, base);
+        __syncwarp();
+        const uint32_t nE = min(E - base, static_cast<uint32_t>(kCclEdgeBuf));
+        for (uint32_t e = lane; e < nE; e += 32) {
+          const int j = buf[e];
+          // L1-cached early-out: a stale parent[j] is an earlier ancestor of j;
+          // if it equals ri, i and j were already in one set (sets only merge)
+          const int pj = __ldca(parent + j);
+          if (pj == ri) continue;
+          if (!adjacent(b, sp, mi, ni, j)) continue;
+          const int rj = uf_find(parent, j);
+          if (rj == ri) continue;
+          ri = uf_link(parent, ri, rj);
+        }
+        __syncwarp();
+        ri = __reduce_min_sync(0xffffffffu, ri);
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_ccl_union_bal(Counters* ctr, SegDev sp, SegBufs b, MapDesc m) {
+  ccl_union_bal_body(ctr, sp, b, m);
+}
+
+// ---------------------------------------------------------------------------
+// Default CCL after the hook: the hook forest is compressed exactly (every
+// parent[i] = its tree's root), then
+//  k_ccl_pairs        every forward edge (i, j) whose endpoints lie in
+//                     different trees is listed once as a root pair -- no
+//                     unions, no pointer chasing, only the 4-byte parent[j]
+//                     per candidate (C2 frame 10: 2.4 M forward edges, 31 hook
+//                     trees, 11 components: ~20 distinct pairs);
+//  k_ccl_pairs_union  one block unions the listed root pairs (larger root
+//                     under smaller, so each root stays the component minimum);
+//  k_ccl_union_gated  the full edge-balanced union, only if the pair table
+//                     overflowed.
+// k_ccl_flatten then resolves each voxel's root through the (short) root links.
+// ---------------------------------------------------------------------------
+// Pointer chasing to the root with no intermediate writes, then one write of
+// the thread's own entry: every parent[i] ends exactly at its root (the
+// path-halving find of k_ccl_compress can leave a node at a non-root ancestor
+// when two threads rewrite it).
+__global__ void k_ccl_compress_exact(Counters* ctr, SegBufs b) {
+  const uint32_t S = min(ctr->S, b.Scap);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < S; i += gridDim.x * blockDim.x) {
+    int r = __ldcg(b.parent + i);
+    for (;;) {
+      const int n = __ldcg(b.parent + r);
+      if (n >= r) break;
+      r = n;
+    }
+    __stcg(b.parent + i, r);
+  }
+}
+
+constexpr unsigned long long kPairEmpty = ~0ull;
+
+__device__ __forceinline__ void pair_insert(Counters* ctr, const SegBufs& b, int ra, int rb) {
+  const uint32_t lo = static_cast<uint32_t>(min(ra, rb)), hi = static_cast<uint32_t>(max(ra, rb));
+  const unsigned long long key = (static_cast<unsigned long long>(hi) << 32) | lo;
+  const uint32_t mask = b.pair_cap - 1u;
+  uint32_t h = static_cast<uint32_t>((key * 0x9E3779B97F4A7C15ull) >> 40) & mask;
+  for (uint32_t probe = 0; probe <= mask; ++probe, h = (h + 1u) & mask) {
+    const unsigned long long cur = __ldcg(b.pair_key + h);
+    if (cur == key) return;
+    if (cur != kPairEmpty) continue;
+    const unsigned long long old = atomicCAS(b.pair_key + h, kPairEmpty, key);
+    if (old == kPairEmpty) {
+      const uint32_t n = atomicAdd(&ctr->npairs, 1u);
+      if (n < (b.pair_cap >> 1)) b.pair_slot[n] = h; else atomicOr(&ctr->pair_ovf, 1u);
+      return;
+    }
+    if (old == key) return;
+  }
+  atomicOr(&ctr->pair_ovf, 1u);
+}
+
+__global__ void __launch_bounds__(256) k_ccl_pairs(Counters* ctr, SegDev sp, SegBufs b, MapDesc m) {
+  __shared__ int32_t cand[kCclWarps][kCclEdgeBuf];
+  const uint32_t S = min(ctr->S, b.Scap);
+  const int w = sp.w, span = 2 * w + 1;
+  const int nrows = (w + 1) + w * span;
+  const int32_t* parent = b.parent;
+  const unsigned lane = lane_id();
+  int32_t* buf = cand[threadIdx.x >> 5];
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarp = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t i = warp; i < S; i += nwarp) {
+    const int x = __ldg(b.st_idx + 3 * i), y = __ldg(b.st_idx + 3 * i + 1), z = __ldg(b.st_idx + 3 * i + 2);
+    const int ri = __ldg(parent + i);  // exact roots: nothing writes parent in this kernel
+    const d3 mi = mk3(__ldg(b.st_mean + 3 * i), __ldg(b.st_mean + 3 * i + 1), __ldg(b.st_mean + 3 * i + 2));
+    const d3 ni = mk3(__ldg(b.st_normal + 3 * i), __ldg(b.st_normal + 3 * i + 1),
+                      __ldg(b.st_normal + 3 * i + 2));
+    int last = ri;  // the last tree this lane listed a pair with (for this voxel)
+    for (int r0 = 0; r0 < nrows; r0 += 64) {
+      int ja = 0, jb = 0;
+      const int ra = r0 + static_cast<int>(lane), rb = ra + 32;
+      const uint32_t ba = ra < nrows ? ccl_row_bits(m, w, span, ra, false, x, y, z, ja) : 0u;
+      const uint32_t bb = rb < nrows ? ccl_row_bits(m, w, span, rb, false, x, y, z, jb) : 0u;
+      const uint32_t ca = __popc(ba), c = ca + __popc(bb);
+      uint32_t incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (static_cast<int>(lane) >= o) incl += t;
+      }
+      const uint32_t E = __shfl_sync(0xffffffffu, incl, 31);
+      for (uint32_t base = 0; base < E; base += kCclEdgeBuf) {
+        ccl_list_row(buf, ba, ja, incl - c, base);
+        ccl_list_row(buf, bb, jb, incl - c + ca, base);
+        __syncwarp();
+        const uint32_t nE = min(E - base, static_cast<uint32_t>(kCclEdgeBuf));
+        for (uint32_t e = lane; e < nE; e += 32) {
+          const int j = buf[e];
+          const int pj = __ldg(parent + j);
+          if (pj == ri || pj == last) continue;
+          if (!adjacent(b, sp, mi, ni, j)) continue;
+          last = pj;
+          pair_insert(ctr, b, ri, pj);
+        }
+        __syncwarp();
+      }
+    }
+  }
+}
+
+// One block: union of the listed root pairs, then the table is emptied.
+__global__ void __launch_bounds__(1024) k_ccl_pairs_union(Counters* ctr, SegBufs b) {
+  const uint32_t n = min(ctr->npairs, b.pair_cap >> 1);
+  for (uint32_t t = threadIdx.x; t < n; t += blockDim.x) {
+    const unsigned long long key = __ldcg(b.pair_key + b.pair_slot[t]);
+    uf_union(b.parent, static_cast<int>(key & 0xffffffffu), static_cast<int>(key >> 32));
+  }
+  __syncthreads();
+  if (ctr->pair_ovf) {
+    for (uint32_t h = threadIdx.x; h < b.pair_cap; h += blockDim.x) b.pair_key[h] = kPairEmpty;
+  } else {
+    for (uint32_t t = threadIdx.x; t < n; t += blockDim.x) b.pair_key[b.pair_slot[t]] = kPairEmpty;
+  }
+}
+
+// The full union (k_ccl_union_bal) when the pair table overflowed, else nothing.
+__global__ void __launch_bounds__(256) k_ccl_union_gated(Counters* ctr, SegDev sp, SegBufs b, MapDesc m) {
+  if (!ctr->pair_ovf) return;
+  ccl_union_bal_body(ctr, sp, b, m);
 }
 
 // ---------------------------------------------------------------------------
@@ -544,6 +849,10 @@ __global__ void k_occ_gather(GridDesc g, const FrameParams* __restrict__ fp, Cou
 __global__ void k_ccl_flatten(Counters* ctr, SegBufs b, MapDesc m) {
   const uint32_t S = min(ctr->S, b.Scap);
   int32_t* parent = b.parent;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // pair set consumed (k_ccl_pairs_union / _gated ran before)
+    ctr->npairs = 0;
+    ctr->pair_ovf = 0;
+  }
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < S; i += gridDim.x * blockDim.x) {
     const int r = uf_find(parent, static_cast<int>(i));
     b.label[i] = r;
@@ -1282,8 +1591,12 @@ __global__ void k_poly_setup(Counters* ctr, SegBufs b) {
   }
 }
 
+// planar != 0: the points are already 2-D (x, y, 0) with the identity basis
+// (the public hull_filter / monotone_chain / convex_hull): copied verbatim, so
+// a -0.0 coordinate keeps its sign as in the reference (projecting would add
+// +0.0 terms).
 __global__ void __launch_bounds__(256) k_poly_extremes(Counters* ctr, SegBufs b, const double* dirtab,
-                                                       int directions) {
+                                                       int directions, int planar) {
   __shared__ double sdir[128];
   __shared__ double ex_dot[8 * 16];
   __shared__ int ex_idx[8 * 16];
@@ -1300,6 +1613,10 @@ __global__ void __launch_bounds__(256) k_poly_extremes(Counters* ctr, SegBufs b,
     const double* bs = b.basis + 9 * f;
     const d3 u = mk3(bs[0], bs[1], bs[2]), v = mk3(bs[3], bs[4], bs[5]), org = mk3(bs[6], bs[7], bs[8]);
     for (uint64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {  // project_to_plane (:36-44)
+      if (planar) {
+        proj[i] = P2{b.inl[3 * i], b.inl[3 * i + 1]};
+        continue;
+      }
       const d3 d = sub3(mk3(b.inl[3 * i], b.inl[3 * i + 1], b.inl[3 * i + 2]), org);
       proj[i] = P2{dot3(d, u), dot3(d, v)};
     }

@@ -30,6 +30,8 @@ thread_local std::string g_err;
 // CCL variant: 0 = min-neighbour hook + forward-window unions (default),
 // 1 = neighbour sampling + giant skip, 2 = hook + giant skip (same labels)
 int g_ccl_mode = 0;
+// pointer-jumping rounds between hook and compress (VP_CCL_JUMPS, A/B)
+int g_ccl_jumps = getenv("VP_CCL_JUMPS") ? atoi(getenv("VP_CCL_JUMPS")) : 3;
 // VP_WALK_GENERIC=1 (experiments): plain-grid rays through the generic walk loop
 const int g_walk_generic = std::getenv("VP_WALK_GENERIC") ? 1 : 0;
 std::atomic<uint64_t> g_launches{0};
@@ -227,7 +229,7 @@ struct Seg {
                     b.fid, b.fit_cluster, b.ioff, b.fch_off, b.ccount, b.fit_model, b.fit_meta, b.ref_model, b.inl,
                     b.rch_off, b.rpart, b.rcen,
                     b.proj, b.surv, b.hull, b.basis, b.pch_off, b.pext_dot, b.pext_idx, b.inner,
-                    b.ninner, b.nsurv, b.prec_d, b.prec_i, b.pool, bsum};
+                    b.ninner, b.nsurv, b.prec_d, b.prec_i, b.pool, b.pair_key, b.pair_slot, bsum};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     b = SegBufs{};
@@ -323,6 +325,15 @@ struct Seg {
       b.prec_i = dalloc<int32_t>(4 * kClusterBins);
       b.pool_cap = icap;
       b.pool = dalloc<double>(5ull * icap);
+      b.pair_cap = 2048;  // CCL root-pair set (load factor <= 1/2; overflow -> full union)
+      while (b.pair_cap < scap / 4) b.pair_cap <<= 1;
+      if (const char* f = getenv("VP_CCL_PAIR_CAP")) {  // test hook: force (tiny) tables
+        b.pair_cap = 2;
+        while (b.pair_cap < static_cast<uint32_t>(atoi(f))) b.pair_cap <<= 1;
+      }
+      b.pair_key = dalloc<unsigned long long>(b.pair_cap);
+      ck(cudaMemset(b.pair_key, 0xff, 8ull * b.pair_cap), "pair table init");
+      b.pair_slot = dalloc<uint32_t>(b.pair_cap / 2);
       alloc_bsum(need_bsum);
       unwind.done = true;
     } else if (need_bsum > bsum_cap) {
@@ -978,7 +989,26 @@ struct vp_grid {
   void launch_ccl(const SegDev& sd, const MapDesc& m, const SegBufs& sb) {
     if (g_ccl_mode == 0) {
       // ECL-style atomic-free pre-hooking + compression: most unions then end at
-      // the one-load parent check (C2: union pass 400 us -> 80 us)
+      // the one-load parent check (C2: union pass 400 us -> 80 us); candidates
+      // listed per warp and spread over the lanes (k_ccl_*_bal)
+      LAUNCH(k_ccl_hook_bal, chain_wide, 256, 0, stream, ctr, sd, sb, m);
+      if (g_ccl_jumps & 1) LAUNCH(k_ccl_jump, chain_wide, kThreads, 0, stream, ctr, sb);
+      if (g_ccl_jumps & 2) LAUNCH(k_ccl_jump, chain_wide, kThreads, 0, stream, ctr, sb);
+      LAUNCH(k_ccl_compress_exact, chain_wide, kThreads, 0, stream, ctr, sb);
+      // cross-tree edges as a root-pair set, unioned by one block (the full
+      // edge-balanced union only if the set overflowed)
+      LAUNCH(k_ccl_pairs, chain_wide, 256, 0, stream, ctr, sd, sb, m);
+      LAUNCH(k_ccl_pairs_union, 1, 1024, 0, stream, ctr, sb);
+      LAUNCH(k_ccl_union_gated, chain_wide, 256, 0, stream, ctr, sd, sb, m);
+    } else if (g_ccl_mode == 4) {
+      // hook + compression + edge-balanced unions of every forward edge
+      LAUNCH(k_ccl_hook_bal, chain_wide, 256, 0, stream, ctr, sd, sb, m);
+      LAUNCH(k_ccl_jump, chain_wide, kThreads, 0, stream, ctr, sb);
+      LAUNCH(k_ccl_jump, chain_wide, kThreads, 0, stream, ctr, sb);
+      LAUNCH(k_ccl_compress, chain_wide, kThreads, 0, stream, ctr, sb);
+      LAUNCH(k_ccl_union_bal, chain_wide, 256, 0, stream, ctr, sd, sb, m);
+    } else if (g_ccl_mode == 3) {
+      // the same with one window row per lane (round-1 kernels, A/B)
       LAUNCH(k_ccl_hook, chain_wide, kThreads, 0, stream, ctr, sd, sb, m);
       LAUNCH(k_ccl_compress, chain_wide, kThreads, 0, stream, ctr, sb);
       LAUNCH(k_ccl_union, chain_wide, kThreads, 0, stream, ctr, sd, sb, m);
@@ -1035,10 +1065,10 @@ struct vp_grid {
     LAUNCH(k_refine_part1, 148 * 4, 256, 0, stream, ctr, seg.b);
     LAUNCH(k_refine_fin, 8, 256, 0, stream, ctr, seg.b, u);
   }
-  void launch_polygon(int dirs, double min_area) {
+  void launch_polygon(int dirs, double min_area, int planar = 0) {
     seg.ensure_dirs(dirs, stream);
     LAUNCH(k_poly_setup, 1, 1024, 0, stream, ctr, seg.b);
-    LAUNCH(k_poly_extremes, chain_wide, 256, 0, stream, ctr, seg.b, seg.dirtab, dirs);
+    LAUNCH(k_poly_extremes, chain_wide, 256, 0, stream, ctr, seg.b, seg.dirtab, dirs, planar);
     LAUNCH(k_poly_inner, 148 * 2, 64, 0, stream, ctr, seg.b, dirs);
     LAUNCH(k_poly_keep, chain_wide, 256, 0, stream, ctr, seg.b);
     LAUNCH(k_poly_hull, 148, 256, kHullSmem * 16 * 6, stream, ctr, seg.b, min_area);
@@ -1789,7 +1819,7 @@ const char* vp_last_error(void) { return g_err.c_str(); }
 const char* vp_version(void) { return "voxplane_b200 0.1 (sm_100a)"; }
 uint64_t vp_kernel_launch_count(void) { return g_launches.load(); }
 int vp_set_ccl_mode(int mode) {
-  if (mode < 0 || mode > 2) return VP_EINVAL;
+  if (mode < 0 || mode > 4) return VP_EINVAL;
   g_ccl_mode = mode;
   return VP_OK;
 }
@@ -2849,8 +2879,10 @@ void vp_fits_free(vp_fits_t* f) {
 
 namespace {
 // Upload (plane, inlier set) batches as "fits" of the scratch grid.
+// to_ref: the planes go to ref_model (make_polygon input) instead of fit_model
+// (refine input). A selector, not a pointer: ensure() below may reallocate.
 void upload_fit_batch(vp_grid* g, size_t f0, uint32_t F, const vp_plane* planes,
-                      const uint64_t* offsets, const double* inliers, double* model_dst) {
+                      const uint64_t* offsets, const double* inliers, bool to_ref) {
   std::vector<double> fm(4ull * F);
   std::vector<int32_t> meta(2ull * F);
   std::vector<uint32_t> io(F + 1);
@@ -2865,7 +2897,7 @@ void upload_fit_batch(vp_grid* g, size_t f0, uint32_t F, const vp_plane* planes,
   io[F] = static_cast<uint32_t>(offsets[f0 + F] - base);
   const uint32_t tot = io[F];
   g->seg.ensure(g->seg.b.Vcap, g->seg.b.Scap, std::max(g->seg.b.Icap, tot), 100, g->gd.nwords);
-  h2d(model_dst == nullptr ? g->seg.b.fit_model : model_dst, fm.data(), fm.size(), g->stream);
+  h2d(to_ref ? g->seg.b.ref_model : g->seg.b.fit_model, fm.data(), fm.size(), g->stream);
   h2d(g->seg.b.fit_meta, meta.data(), meta.size(), g->stream);
   h2d(g->seg.b.ioff, io.data(), io.size(), g->stream);
   h2d(g->seg.b.inl, inliers + 3 * base, 3ull * tot, g->stream);
@@ -2883,7 +2915,7 @@ int vp_refine_planes(const vp_fits_t* fits, const double up[3], int exact, int d
     vp_grid* g = scratch_grid(device);
     for (size_t f0 = 0; f0 < fits->count; f0 += kClusterBins) {
       const uint32_t F = static_cast<uint32_t>(std::min<size_t>(kClusterBins, fits->count - f0));
-      upload_fit_batch(g, f0, F, fits->models, fits->offsets, fits->inliers, nullptr);
+      upload_fit_batch(g, f0, F, fits->models, fits->offsets, fits->inliers, false);
       g->launch_refine(up, 1, exact);
       auto rm = d2h(g->seg.b.ref_model, 4ull * F, g->stream);
       ck(cudaStreamSynchronize(g->stream), "sync");
@@ -2906,7 +2938,7 @@ int vp_make_polygons(size_t n, const vp_plane* planes, const uint64_t* offsets,
     for (size_t f0 = 0; f0 < n || (f0 == 0 && n == 0); f0 += kClusterBins) {
       if (n == 0) break;
       const uint32_t F = static_cast<uint32_t>(std::min<size_t>(kClusterBins, n - f0));
-      upload_fit_batch(g, f0, F, planes, offsets, inliers, g->seg.b.ref_model);
+      upload_fit_batch(g, f0, F, planes, offsets, inliers, true);
       g->launch_polygon(filter_directions, -std::numeric_limits<double>::infinity());
       g->read_counters();
       if (g->h_ctr->overflow & kOverflowPool) fail(VP_ENOMEM, "polygon vertex pool overflow");
@@ -3820,7 +3852,7 @@ void stage_points2d(vp_grid* g, const double* pts, uint64_t n) {
   pl.normal[2] = 1.0;
   pl.inlier_count = static_cast<int32_t>(n);
   const uint64_t offs[2] = {0, n};
-  upload_fit_batch(g, 0, 1, &pl, offs, p3.data(), g->seg.b.ref_model);
+  upload_fit_batch(g, 0, 1, &pl, offs, p3.data(), true);
 }
 
 double* copy_out2(const double* src, uint64_t m) {
@@ -3858,7 +3890,7 @@ int vp_convex_hull(const double* pts, uint64_t n, int directions, int device, do
     }
     vp_grid* g = scratch_grid(device);
     stage_points2d(g, pts, n);
-    g->launch_polygon(directions, -std::numeric_limits<double>::infinity());
+    g->launch_polygon(directions, -std::numeric_limits<double>::infinity(), 1);
     g->read_counters();
     if (g->h_ctr->overflow & kOverflowPool) fail(VP_ENOMEM, "polygon vertex pool overflow");
     HostPolys hp;
@@ -3898,7 +3930,7 @@ int vp_hull_filter(const double* pts, uint64_t n, int directions, int device, do
     g->seg.ensure_dirs(directions, g->stream);
     cudaStream_t st = g->stream;
     LAUNCH(k_poly_setup, 1, 1024, 0, st, g->ctr, g->seg.b);
-    LAUNCH(k_poly_extremes, g->chain_wide, 256, 0, st, g->ctr, g->seg.b, g->seg.dirtab, directions);
+    LAUNCH(k_poly_extremes, g->chain_wide, 256, 0, st, g->ctr, g->seg.b, g->seg.dirtab, directions, 1);
     LAUNCH(k_poly_inner, 1, 64, 0, st, g->ctr, g->seg.b, directions);
     DBuf<uint8_t> flags(n);
     DBuf<uint32_t> pos(n + 2);

@@ -117,6 +117,8 @@ struct Counters {
   int32_t ccl_giant;     // root of the sampled largest component after the lattice links
   uint32_t ndense;       // integrate groups with more than kFoldMax points (k_integrate_fold_dense)
   uint32_t nmedium;      // integrate groups with kFoldSmall < points <= kFoldMax (k_integrate_fold_medium)
+  uint32_t npairs;       // CCL: distinct adjacent root pairs listed by k_ccl_pairs
+  uint32_t pair_ovf;     // CCL: the pair table overflowed -> k_ccl_union_bal runs the full union
 };
 
 constexpr uint32_t kOverflowOcc = 1u;

@@ -107,11 +107,20 @@ __device__ __forceinline__ int uf_find(int32_t* parent, int v) {
   return par;
 }
 
-// Link two roots (larger under smaller); returns the surviving root.
+// Link two roots (larger under smaller); returns the surviving root. The CAS
+// is tried only when hi still reads as a root: a stale root (already hooked
+// by another thread) is climbed with a plain load. Without the check every
+// late union of two already-joined trees was a failed CAS on one of the few
+// component roots, serialised in its L2 slice (C2: ~74k ATOMs on ~31 roots).
 __device__ __forceinline__ int uf_link(int32_t* parent, int ra, int rb) {
   while (ra != rb) {
     const int lo = ra < rb ? ra : rb;
     const int hi = ra < rb ? rb : ra;
+    const int cur = __ldcg(parent + hi);
+    if (cur != hi) {  // hi was hooked meanwhile: climb without an atomic
+      if (ra == hi) ra = cur; else rb = cur;
+      continue;
+    }
     const int ret = atomicCAS(parent + hi, hi, lo);
     if (ret == hi) return lo;
     if (ra == hi) ra = ret; else rb = ret;  // hi was hooked meanwhile: climb
@@ -235,6 +244,11 @@ struct SegBufs {
   double* pool;          // 5 per vertex: u v x y z
   uint32_t pool_cap;
   uint32_t Vcap, Scap, Mcap, Icap;
+  // CCL root-pair set: open-addressed keys (hi << 32 | lo, ~0 = empty) and the
+  // list of occupied slots (pair_cap / 2 entries)
+  unsigned long long* pair_key;
+  uint32_t* pair_slot;
+  uint32_t pair_cap;     // power of two
 };
 
 // ---- spatial slabs (k_slab.cu)
@@ -339,6 +353,13 @@ __global__ void k_map_fill(Counters* ctr, SegBufs b, MapDesc m);
 __global__ void k_occ_gather(GridDesc g, const FrameParams* fp, Counters* ctr, SegBufs b);
 __global__ void k_ccl_init(Counters* ctr, SegBufs b);
 __global__ void k_ccl_union(Counters* ctr, SegDev sp, SegBufs b, MapDesc m);
+__global__ void k_ccl_hook_bal(Counters* ctr, SegDev sp, SegBufs b, MapDesc m);
+__global__ void k_ccl_jump(Counters* ctr, SegBufs b);
+__global__ void k_ccl_compress_exact(Counters* ctr, SegBufs b);
+__global__ void k_ccl_pairs(Counters* ctr, SegDev sp, SegBufs b, MapDesc m);
+__global__ void k_ccl_pairs_union(Counters* ctr, SegBufs b);
+__global__ void k_ccl_union_gated(Counters* ctr, SegDev sp, SegBufs b, MapDesc m);
+__global__ void k_ccl_union_bal(Counters* ctr, SegDev sp, SegBufs b, MapDesc m);
 __global__ void k_ccl_hook(Counters* ctr, SegDev sp, SegBufs b, MapDesc m);
 __global__ void k_ccl_compress(Counters* ctr, SegBufs b);
 __global__ void k_ccl_lattice(Counters* ctr, SegDev sp, SegBufs b, MapDesc m);
@@ -364,7 +385,7 @@ __global__ void k_refine_part1(Counters* ctr, SegBufs b);
 __global__ void k_refine_cen(Counters* ctr, SegBufs b);
 __global__ void k_refine_fin(Counters* ctr, SegBufs b, d3 up);
 __global__ void k_poly_setup(Counters* ctr, SegBufs b);
-__global__ void k_poly_extremes(Counters* ctr, SegBufs b, const double* dirtab, int directions);
+__global__ void k_poly_extremes(Counters* ctr, SegBufs b, const double* dirtab, int directions, int planar);
 __global__ void k_poly_inner(Counters* ctr, SegBufs b, int directions);
 __global__ void k_poly_keep(Counters* ctr, SegBufs b);
 __global__ void k_poly_hull(Counters* ctr, SegBufs b, double min_area);

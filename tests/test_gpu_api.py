@@ -182,7 +182,7 @@ def random_steppable(rng, n, spread):
     return idx, mean, nrm
 
 
-@pytest.fixture(params=[0, 1, 2], ids=["hook_ccl", "sampling_ccl", "hook_giant_ccl"])
+@pytest.fixture(params=[0, 1, 2, 3, 4], ids=["pairs_ccl", "sampling_ccl", "hook_giant_ccl", "hook_rows_ccl", "hook_union_ccl"])
 def ccl_mode(request):
     native.set_ccl_mode(request.param)
     yield request.param

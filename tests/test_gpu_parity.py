@@ -89,7 +89,7 @@ def test_golden_files_reproduced(name):
     assert format_polygons(polys) == golden_text(run)
 
 
-@pytest.mark.parametrize("ccl_mode", [0, 1, 2], ids=["hook_ccl", "sampling_ccl", "hook_giant_ccl"])
+@pytest.mark.parametrize("ccl_mode", [0, 1, 2, 3, 4], ids=["pairs_ccl", "sampling_ccl", "hook_giant_ccl", "hook_rows_ccl", "hook_union_ccl"])
 def test_stair_every_stage_bit_exact(ccl_mode):
     native.set_ccl_mode(ccl_mode)
     try:
@@ -97,6 +97,21 @@ def test_stair_every_stage_bit_exact(ccl_mode):
         check_bit_exact(frames[:12], gpu, ora)
     finally:
         native.set_ccl_mode(0)
+
+
+def test_ccl_pair_table_overflow_falls_back_to_full_union():
+    # k_ccl_pairs lists cross-tree root pairs in a table; when it overflows the
+    # full union runs instead (VP_CCL_PAIR_CAP forces a 2-slot table)
+    import os
+    import subprocess
+    import sys
+    code = ("import sys; sys.path[:0] = ['tests', '.']; "
+            "import test_gpu_parity as t; "
+            "frames, gpu, ora = t.sessions('stair'); t.check_bit_exact(frames[:8], gpu, ora); print('ok')")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=600,
+                       env=dict(os.environ, VP_CCL_PAIR_CAP="2"))
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-3000:]
 
 
 def hausdorff(a, b):
