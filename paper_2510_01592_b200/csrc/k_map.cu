@@ -17,8 +17,11 @@ namespace vp {
 // ---------------------------------------------------------------------------
 // 0: discarded (non-finite or outside the window), 1: inserted into *key,
 // 2: inside the window but owned by another slab.
+__device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+// box: grows by the point's cell clamped to the grid (local x): every cell its
+// ray can mark lies between the sensor's and this cell, per axis.
 __device__ __forceinline__ int point_key(const GridDesc& g, const FrameParams* fp, uint64_t i,
-                                         uint32_t* key) {
+                                         uint32_t* key, int* box) {
   const float* p = fp->pts + 3 * i;
   const d3 w = pose_apply(fp->R, fp->t, static_cast<double>(p[0]), static_cast<double>(p[1]),
                           static_cast<double>(p[2]));
@@ -26,6 +29,11 @@ __device__ __forceinline__ int point_key(const GridDesc& g, const FrameParams* f
   const int ix = w2i(w.x, fp->origin_pre[0], g.res);  // window coordinates
   const int iy = w2i(w.y, fp->origin_pre[1], g.res);
   const int iz = w2i(w.z, fp->origin_pre[2], g.res);
+  {
+    const int cx = clampi(ix - g.xoff, 0, g.ex - 1), cy = clampi(iy, 0, g.ey - 1), cz = clampi(iz, 0, g.ez - 1);
+    box[0] = min(box[0], cx), box[1] = min(box[1], cy), box[2] = min(box[2], cz);
+    box[3] = max(box[3], cx), box[4] = max(box[4], cy), box[5] = max(box[5], cz);
+  }
   if (ix < 0 || iy < 0 || iz < 0 || ix >= g.gex || iy >= g.ey || iz >= g.ez) return 0;
   const int lx = ix - g.xoff;
   if (lx < g.own_lo || lx >= g.own_hi) return 2;
@@ -39,13 +47,20 @@ __global__ void k_integrate_hash(GridDesc g, const FrameParams* __restrict__ fp,
   const uint64_t n = fp->n;
   unsigned long long disc = 0;
   const unsigned lane = lane_id();
+  int box[6] = {0x7fffffff, 0x7fffffff, 0x7fffffff, -1, -1, -1};
+  if (blockIdx.x == 0 && threadIdx.x == 0 && n) {  // the sensor's cell (rays start there)
+    const int cx = clampi(w2i(fp->t[0], fp->origin_pre[0], g.res) - g.xoff, 0, g.ex - 1);
+    const int cy = clampi(w2i(fp->t[1], fp->origin_pre[1], g.res), 0, g.ey - 1);
+    const int cz = clampi(w2i(fp->t[2], fp->origin_pre[2], g.res), 0, g.ez - 1);
+    box[0] = box[3] = cx, box[1] = box[4] = cy, box[2] = box[5] = cz;
+  }
   for (uint64_t i0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x; i0 < n;
        i0 += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint64_t i = i0 + threadIdx.x;
     uint32_t key = kEmptyKey;
     bool valid = false;
     if (i < n) {
-      const int r = point_key(g, fp, i, &key);
+      const int r = point_key(g, fp, i, &key, box);
       valid = r == 1;
       if (r == 0) ++disc;
       if (r == 2) key = kEmptyKey;
@@ -83,7 +98,25 @@ __global__ void k_integrate_hash(GridDesc g, const FrameParams* __restrict__ fp,
       prank[i] = base + __popc(peers & lanemask_lt());
     }
   }
-  warp_add_u64(&ctr->discarded, disc);
+  block_add_u64(&ctr->discarded, disc);
+  // the block's box -> 6 atomics per block
+  __shared__ int sbox[6];
+  if (threadIdx.x < 6) sbox[threadIdx.x] = threadIdx.x < 3 ? 0x7fffffff : -1;
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const int lo = __reduce_min_sync(0xffffffffu, box[k]), hi = __reduce_max_sync(0xffffffffu, box[3 + k]);
+    if (lane == 0) {
+      atomicMin(&sbox[k], lo);
+      atomicMax(&sbox[3 + k], hi);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    if (sbox[threadIdx.x] != 0x7fffffff) atomicMin(&ctr->box_lo[threadIdx.x], sbox[threadIdx.x]);
+  } else if (threadIdx.x < 6) {
+    if (sbox[threadIdx.x] >= 0) atomicMax(&ctr->box_hi[threadIdx.x - 3], sbox[threadIdx.x]);
+  }
 }
 
 // Per-group ranges of the point-index buffer; groups too large for one
@@ -153,7 +186,7 @@ __device__ __forceinline__ void fold_cell(const GridDesc& g, const FrameParams* 
   c->count = count + cnt;
   c->status = 1;  // VoxelStatus::Occupied
   if (count == 0) {
-    atomicOr(fp->occ_pre + word_of(g, x, y, z), 1u << (z & 31));
+    occ_set(g, fp->occ_pre, fp->off_pre, fp->zb_pre, x, y, z);
     ++fresh;
   }
 }
@@ -208,13 +241,13 @@ __global__ void __launch_bounds__(256) k_integrate_fold(GridDesc g, const FrameP
     c->count = count + cnt;
     c->status = 1;  // VoxelStatus::Occupied
     if (count == 0) {
-      atomicOr(fp->occ_pre + word_of(g, x, y, z), 1u << (z & 31));
+      occ_set(g, fp->occ_pre, fp->off_pre, fp->zb_pre, x, y, z);
       ++fresh;
     }
     hkey[slot] = kEmptyKey;
     hcnt[slot] = 0;
   }
-  warp_add_u64(&ctr->newly, fresh);
+  block_add_u64(&ctr->newly, fresh);
 }
 
 // Voxels with kFoldSmall < points <= kFoldMax: one warp per voxel: the point
@@ -372,7 +405,7 @@ __global__ void __launch_bounds__(1024) k_integrate_fold_dense(GridDesc g, const
       c->count = count + cnt;
       c->status = 1;
       if (count == 0) {
-        atomicOr(fp->occ_pre + word_of(g, x, y, z), 1u << (z & 31));
+        occ_set(g, fp->occ_pre, fp->off_pre, fp->zb_pre, x, y, z);
         atomicAdd(&ctr->newly, 1ull);
       }
       hkey[slot] = kEmptyKey;
@@ -951,166 +984,171 @@ __device__ __forceinline__ void zero_cell(Cell* c) {
   c->status = 0;
 }
 
-// Row-layout clear mask (coherent rays): one thread per bitmap word.
+// The cells the frame's rays can mark: k_integrate_hash's box (use_box), or
+// the whole grid (clear_rays without integrate_frame). Every mark lies in the
+// box, and the apply pass zeroes every mark it visits, so the masks stay zero
+// outside it.
+__device__ __forceinline__ void sweep_box(const GridDesc& g, const Counters* ctr, int use_box, int* lo, int* hi) {
+  if (use_box) {
+    for (int k = 0; k < 3; ++k) lo[k] = ctr->box_lo[k], hi[k] = ctr->box_hi[k];
+  } else {
+    lo[0] = lo[1] = lo[2] = 0;
+    hi[0] = g.ex - 1, hi[1] = g.ey - 1, hi[2] = g.ez - 1;
+  }
+}
+
+// Row-layout clear mask (coherent rays): one thread per mask word of the box.
+// The occupancy of a mask word's 32 cells is 32 ring bits (one or two ring
+// words); freed bits are cleared with atomicAnd (neighbouring mask words share
+// ring words).
 __device__ __forceinline__ void clear_apply_rows(const GridDesc& g, const FrameParams* __restrict__ fp,
-                                                 Counters* ctr) {
+                                                 Counters* ctr, int use_box) {
   uint32_t* occ = fp->occ_pre;
   unsigned long long cl = 0, fr = 0;
-  // four mask words per thread per trip (one 16-byte load; the mask is
-  // mostly zero, so the trip count is what the sweep costs)
-  const uint64_t nq = (g.nwords + 3) / 4;
-  for (uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < nq;
-       q += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    uint32_t cv[4];
-    if (4 * q + 3 < g.nwords) {
-      const uint4 c4 = reinterpret_cast<const uint4*>(g.clr)[q];
-      cv[0] = c4.x, cv[1] = c4.y, cv[2] = c4.z, cv[3] = c4.w;
-    } else {
-#pragma unroll
-      for (int k = 0; k < 4; ++k) cv[k] = 4 * q + k < g.nwords ? g.clr[4 * q + k] : 0u;
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const uint32_t c = cv[k];
+  int lo[3], hi[3];
+  sweep_box(g, ctr, use_box, lo, hi);
+  if (hi[0] >= lo[0]) {
+    const int wz0 = lo[2] >> 5;
+    const uint32_t nwz = static_cast<uint32_t>((hi[2] >> 5) - wz0 + 1);
+    const uint32_t ny = static_cast<uint32_t>(hi[1] - lo[1] + 1);
+    const uint64_t total = static_cast<uint64_t>(hi[0] - lo[0] + 1) * ny * nwz;
+    for (uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < total;
+         q += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+      const uint32_t r = static_cast<uint32_t>(q / nwz);
+      const int wz = wz0 + static_cast<int>(q - static_cast<uint64_t>(r) * nwz);
+      const uint32_t rx = r / ny;
+      const int y = lo[1] + static_cast<int>(r - rx * ny), x = lo[0] + static_cast<int>(rx);
+      const uint64_t w = (static_cast<uint64_t>(x) * g.ey + y) * g.W + wz;
+      const uint32_t c = g.clr[w];
       if (!c) continue;
-      const uint64_t w = 4 * q + k;
       g.clr[w] = 0;
       cl += __popc(c);
-      const uint32_t o = occ[w];
-      uint32_t f = o & c;
+      uint32_t* row = occ_row(g, occ, fp->off_pre, x, y);
+      const int pz = ring_z(g, fp->zb_pre, wz * 32);
+      uint32_t f = ring_bits32(row, g.W, pz) & c;
       if (!f) continue;
-      occ[w] = o & ~f;
+      ring_clear32(row, g.W, pz, f);
       fr += __popc(f);
-      const uint32_t row = fdiv(static_cast<uint32_t>(w), g.fW);
-      const int z0 = static_cast<int>(static_cast<uint32_t>(w) - row * static_cast<uint32_t>(g.W)) * 32;
-      const uint32_t xr = fdiv(row, g.fey);
-      const int y = static_cast<int>(row - xr * static_cast<uint32_t>(g.ey)), x = static_cast<int>(xr);
       while (f) {
         const int b = __ffs(f) - 1;
         f &= f - 1;
-        zero_cell(g.cells + phys_index(g, fp->off_pre, x, y, z0 + b));
+        zero_cell(g.cells + phys_index(g, fp->off_pre, x, y, wz * 32 + b));
       }
     }
   }
-  warp_add_u64(&ctr->cleared, cl);
-  warp_add_u64(&ctr->freed, fr);
+  block_add2_u64(&ctr->cleared, cl, &ctr->freed, fr);
 }
 
-// Brick-layout clear mask (incoherent rays): one thread per brick word: count
-// the unique cleared cells, free the occupied ones (the occupancy bits of the
-// brick's 16 (x, y) columns are gathered from the row-layout bitmap, four z
-// bits each), zero the mask.
+// Brick-layout clear mask (incoherent rays): one thread per brick word of the
+// box: count the unique cleared cells, free the occupied ones (the occupancy
+// of the brick's 16 (x, y) columns: four ring bits each), zero the mask.
 __device__ __forceinline__ void clear_apply_bricks(const GridDesc& g, const FrameParams* __restrict__ fp,
-                                                   Counters* ctr) {
+                                                   Counters* ctr, int use_box) {
   uint32_t* occ = fp->occ_pre;
   unsigned long long cl = 0, fr = 0;
-  for (uint64_t w = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; w < g.nbricks;
-       w += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const unsigned long long c = g.clrb[w];
-    if (!c) continue;
-    g.clrb[w] = 0;
-    cl += __popcll(c);
-    const uint32_t bz = static_cast<uint32_t>(w % g.bnz);
-    const uint64_t r = w / g.bnz;
-    const int by = static_cast<int>(r % g.bny), bx = static_cast<int>(r / g.bny);
-    const int z0 = static_cast<int>(bz) * 4;
-    const int wz = z0 >> 5, sh = z0 & 31;  // the brick's 4 z lie in one occupancy word
-    unsigned long long cols = c;
-    while (cols) {  // (lx, ly) columns with marks: bits 4k .. 4k+3
-      const int k = (__ffsll(cols) - 1) >> 2;
-      const uint32_t cm = static_cast<uint32_t>(c >> (4 * k)) & 15u;
-      cols &= ~(15ull << (4 * k));
-      const int x = bx * 4 + (k >> 2), y = by * 4 + (k & 3);
-      uint32_t* ow = occ + (static_cast<uint64_t>(x) * g.ey + y) * g.W + wz;
-      const uint32_t f = (*ow >> sh) & cm;
-      if (!f) continue;
-      atomicAnd(ow, ~(f << sh));  // other bricks share this occupancy word
-      fr += __popc(f);
-      for (int b = 0; b < 4; ++b)
-        if (f & (1u << b)) zero_cell(g.cells + phys_index(g, fp->off_pre, x, y, z0 + b));
+  int lo[3], hi[3];
+  sweep_box(g, ctr, use_box, lo, hi);
+  if (hi[0] >= lo[0]) {
+    const int bx0 = lo[0] >> 2, by0 = lo[1] >> 2, bz0 = lo[2] >> 2;
+    const uint32_t nbz = static_cast<uint32_t>((hi[2] >> 2) - bz0 + 1);
+    const uint32_t nby = static_cast<uint32_t>((hi[1] >> 2) - by0 + 1);
+    const uint64_t total = static_cast<uint64_t>((hi[0] >> 2) - bx0 + 1) * nby * nbz;
+    for (uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < total;
+         q += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+      const uint32_t r = static_cast<uint32_t>(q / nbz);
+      const int bz = bz0 + static_cast<int>(q - static_cast<uint64_t>(r) * nbz);
+      const uint32_t rbx = r / nby;
+      const int by = by0 + static_cast<int>(r - rbx * nby), bx = bx0 + static_cast<int>(rbx);
+      const uint64_t w = (static_cast<uint64_t>(bx) * g.bny + by) * g.bnz + bz;
+      const unsigned long long c = g.clrb[w];
+      if (!c) continue;
+      g.clrb[w] = 0;
+      cl += __popcll(c);
+      const int z0 = bz * 4;
+      unsigned long long cols = c;
+      while (cols) {  // (lx, ly) columns with marks: bits 4k .. 4k+3
+        const int k = (__ffsll(cols) - 1) >> 2;
+        const uint32_t cm = static_cast<uint32_t>(c >> (4 * k)) & 15u;
+        cols &= ~(15ull << (4 * k));
+        const int x = bx * 4 + (k >> 2), y = by * 4 + (k & 3);
+        uint32_t* row = occ_row(g, occ, fp->off_pre, x, y);
+        const int pz = ring_z(g, fp->zb_pre, z0);
+        const uint32_t f = ring_bits32(row, g.W, pz) & cm;
+        if (!f) continue;
+        ring_clear32(row, g.W, pz, f);  // other bricks share these ring words
+        fr += __popc(f);
+        for (int b = 0; b < 4; ++b)
+          if (f & (1u << b)) zero_cell(g.cells + phys_index(g, fp->off_pre, x, y, z0 + b));
+      }
     }
   }
-  warp_add_u64(&ctr->cleared, cl);
-  warp_add_u64(&ctr->freed, fr);
+  block_add2_u64(&ctr->cleared, cl, &ctr->freed, fr);
 }
 
 // One launch for either mask layout (k_dda_plan's decision for this frame).
-__global__ void k_clear_apply(GridDesc g, const FrameParams* __restrict__ fp, Counters* ctr, const DdaBins* db) {
-  if (db->use) clear_apply_bricks(g, fp, ctr); else clear_apply_rows(g, fp, ctr);
+__global__ void k_clear_apply(GridDesc g, const FrameParams* __restrict__ fp, Counters* ctr, const DdaBins* db,
+                              int use_box) {
+  if (db->use) clear_apply_bricks(g, fp, ctr, use_box); else clear_apply_rows(g, fp, ctr, use_box);
 }
 
 // ---------------------------------------------------------------------------
 // recenter (voxel_grid.cpp:217-252). The host computes the integer shift with
-// the reference's arithmetic; on the device the cell array is toroidal, so a
-// shift only (1) rebuilds the logical bitmap (funnel-shifted gather) and
-// (2) zeroes the cells of occupied voxels that leave the window, counting them
-// as voxels_dropped.
+// the reference's arithmetic and advances the toroidal offsets (cells: off;
+// occupancy ring: off for x and y, zb for z). On the device only the cells
+// that leave the window are touched: one thread per (x, y) row of the
+// pre-shift window -- a row leaving in x or y drops all its occupied cells,
+// any other row the occupied cells of its leaving z range (|sz| bits, one or
+// two ring words); dropped cells are zeroed and their ring bits cleared, so
+// the positions that re-enter the window are empty (voxels_dropped counted).
+// Rows that neither leave nor shift in z are not read at all.
 // ---------------------------------------------------------------------------
-
-// Blocks walk the bitmap in the occupied scan's tiles (kScanPerBlock words,
-// word k * blockDim + t of a tile by thread t) and leave each tile's
-// popcount of the new bitmap in bsum, so k_bitmap_count skips a shifted frame.
-__global__ void __launch_bounds__(kScanThreads) k_recenter(GridDesc g, const FrameParams* __restrict__ fp,
-                                                           Counters* ctr, uint32_t* bsum) {
+__global__ void k_recenter(GridDesc g, const FrameParams* __restrict__ fp, Counters* ctr) {
   if (!fp->do_shift) return;
-  const uint32_t* __restrict__ oldb = fp->occ_pre;
-  uint32_t* __restrict__ newb = fp->occ_post;
+  uint32_t* occ = fp->occ_pre;
   const int sx = fp->shift[0], sy = fp->shift[1], sz = fp->shift[2];
+  const int ex = g.ex, ey = g.ey, ez = g.ez, W = g.W, Wz = g.W << 5;
+  const int zb = fp->zb_pre;
+  // the leaving z range of a row that stays: [zl0, zl1)
+  const int zl0 = sz > 0 ? 0 : max(ez + sz, 0), zl1 = sz > 0 ? min(sz, ez) : ez;
+  const bool zleave = sz != 0;
   unsigned long long dropped = 0;
-  const uint32_t nw = static_cast<uint32_t>(g.nwords);  // < 2^32 (grid creation check)
-  const int W = g.W, ey = g.ey, ex = g.ex, ez = g.ez;
-  for (uint32_t t0 = blockIdx.x * kScanPerBlock; t0 < nw; t0 += gridDim.x * kScanPerBlock) {
-    uint32_t pc = 0;
-    for (uint32_t u = t0 + threadIdx.x; u < min(nw, t0 + kScanPerBlock); u += kScanThreads) {
-      const uint32_t row = fdiv(u, g.fW);
-      const int wz = static_cast<int>(u - row * static_cast<uint32_t>(W));
-      const uint32_t xr = fdiv(row, g.fey);
-      const int y = static_cast<int>(row - xr * static_cast<uint32_t>(ey)), x = static_cast<int>(xr);
-      // new word: destination (x, y, z) reads source (x+sx, y+sy, z+sz), i.e.
-      // bits [32 wz + sz, +32) of source row (x+sx, y+sy), zero outside the row
-      const int xs = x + sx, ys = y + sy;
-      uint32_t nv = 0;
-      if (static_cast<unsigned>(xs) < static_cast<unsigned>(ex) && static_cast<unsigned>(ys) < static_cast<unsigned>(ey)) {
-        const uint32_t* src = oldb + (static_cast<uint32_t>(xs) * static_cast<uint32_t>(ey) + static_cast<uint32_t>(ys)) *
-                                         static_cast<uint32_t>(W);
-        const int b0 = wz * 32 + sz;
-        const int wlo = b0 >> 5, sh = b0 & 31;  // floor division (arithmetic shift)
-        const uint32_t lo = (wlo >= 0 && wlo < W) ? __ldg(src + wlo) : 0u;
-        const uint32_t hi = (wlo + 1 >= 0 && wlo + 1 < W) ? __ldg(src + wlo + 1) : 0u;
-        nv = __funnelshift_r(lo, hi, sh);
-      }
-      const int zlim = ez - wz * 32;
-      if (zlim < 32) nv &= (1u << zlim) - 1u;
-      newb[u] = nv;
-      pc += __popc(nv);
-      // dropped: old bits whose destination (x-sx, y-sy, z-sz) leaves the window
-      const uint32_t ov = __ldg(oldb + u);
-      if (!ov) continue;
-      uint32_t drop;
-      const int xd = x - sx, yd = y - sy;
-      if (static_cast<unsigned>(xd) >= static_cast<unsigned>(ex) || static_cast<unsigned>(yd) >= static_cast<unsigned>(ey)) {
-        drop = ov;
-      } else {
-        // keep bits b with 0 <= 32*wz + b - sz < ez, i.e. b in [blo, bhi)
-        const int blo = min(max(sz - 32 * wz, 0), 32);
-        const int bhi = min(max(ez + sz - 32 * wz, 0), 32);
-        uint32_t keep = 0;
-        if (bhi > blo) {
-          const uint32_t upto_hi = bhi >= 32 ? 0xffffffffu : ((1u << bhi) - 1u);
-          const uint32_t below_lo = blo >= 32 ? 0xffffffffu : ((1u << blo) - 1u);
-          keep = upto_hi & ~below_lo;
+  const uint32_t nrows = static_cast<uint32_t>(ex) * static_cast<uint32_t>(ey);
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += gridDim.x * blockDim.x) {
+    const uint32_t xr = fdiv(r, g.fey);
+    const int y = static_cast<int>(r - xr * static_cast<uint32_t>(ey)), x = static_cast<int>(xr);
+    const bool row_leaves = static_cast<unsigned>(x - sx) >= static_cast<unsigned>(ex) ||
+                            static_cast<unsigned>(y - sy) >= static_cast<unsigned>(ey);
+    if (!row_leaves && !zleave) continue;
+    uint32_t* row = occ_row(g, occ, fp->off_pre, x, y);
+    if (row_leaves) {
+      for (int w = 0; w < W; ++w) {
+        uint32_t v = __ldcg(row + w);
+        if (!v) continue;
+        row[w] = 0u;
+        dropped += __popc(v);
+        while (v) {
+          const int b = __ffs(v) - 1;
+          v &= v - 1;
+          int z = 32 * w + b - zb;  // ring position -> window z
+          if (z < 0) z += Wz;
+          zero_cell(g.cells + phys_index(g, fp->off_pre, x, y, z));
         }
-        drop = ov & ~keep;
       }
-      dropped += __popc(drop);
-      while (drop) {
-        const int b = __ffs(drop) - 1;
-        drop &= drop - 1;
-        zero_cell(g.cells + phys_index(g, fp->off_pre, x, y, wz * 32 + b));
+      continue;
+    }
+    for (int z0 = zl0; z0 < zl1; z0 += 32) {
+      const int len = min(32, zl1 - z0);
+      const int pz = ring_z(g, zb, z0);
+      uint32_t v = ring_bits32(row, W, pz) & (len >= 32 ? 0xffffffffu : ((1u << len) - 1u));
+      if (!v) continue;
+      ring_clear32(row, W, pz, v);
+      dropped += __popc(v);
+      while (v) {
+        const int b = __ffs(v) - 1;
+        v &= v - 1;
+        zero_cell(g.cells + phys_index(g, fp->off_pre, x, y, z0 + b));
       }
     }
-    pc = block_sum_u32(pc);
-    if (threadIdx.x == 0) bsum[t0 / kScanPerBlock] = pc;
   }
   warp_add_u64(&ctr->dropped, dropped);
 }
@@ -1121,7 +1159,7 @@ __global__ void k_merge_point(GridDesc g, const FrameParams* __restrict__ fp, Co
   Cell* c = g.cells + phys_index(g, fp->off_pre, x, y, z);
   if (c->count == 0) {
     ctr->newly += 1;
-    atomicOr(fp->occ_pre + word_of(g, x, y, z), 1u << (z & 31));
+    occ_set(g, fp->occ_pre, fp->off_pre, fp->zb_pre, x, y, z);
   }
   c->sx += px;
   c->sy += py;
@@ -1152,7 +1190,13 @@ __global__ void k_frame_begin(Counters* ctr, const unsigned long long* occ_total
   uint32_t* w = reinterpret_cast<uint32_t*>(ctr);
   for (uint32_t i = threadIdx.x; i < sizeof(Counters) / 4; i += blockDim.x) w[i] = 0u;
   __syncwarp();
-  if (threadIdx.x == 0) ctr->occupied = *occ_total;
+  if (threadIdx.x == 0) {
+    ctr->occupied = *occ_total;
+    for (int k = 0; k < 3; ++k) {
+      ctr->box_lo[k] = 0x7fffffff;
+      ctr->box_hi[k] = -1;
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1175,26 +1219,107 @@ __device__ __forceinline__ void load_words8(const uint32_t* __restrict__ bits, u
   }
 }
 
-__global__ void k_bitmap_count(const FrameParams* __restrict__ fp, uint64_t w_lo, uint64_t nwords,
-                               uint32_t* bsum) {
-  if (fp->do_shift) return;  // k_recenter left the tile counts
-  const uint32_t* __restrict__ bits = fp->occ_post + w_lo;
-  const uint64_t w0 = (static_cast<uint64_t>(blockIdx.x) * kScanThreads + threadIdx.x) * kScanItems;
-  uint32_t v[kScanItems];
-  load_words8(bits, w0, nwords, v);
-  uint32_t c = 0;
+// A block's tile of kScanPerBlock logical words (x, y, z lexicographic: word
+// u = row * W + wz) of the occupancy ring (post-recenter offsets). A ring row
+// is W contiguous words (rotated by zb bits), so the tile's rows are staged in
+// shared memory one row per thread (16-byte loads when W % 4 == 0), and each
+// thread then rotates its kScanItems logical words out of them (logical word
+// wz = 32 ring bits from ring position 32 wz + zb).
+constexpr int kScanStage = kScanPerBlock + 2 * kMaxRowWords;  // a tile's rows: <= 2048 + 2 W words
+
+__device__ __forceinline__ const uint32_t* ring_row_post(const GridDesc& g, const FrameParams* __restrict__ fp,
+                                                         uint32_t row) {
+  const uint32_t xr = fdiv(row, g.fey);
+  return occ_row(g, fp->occ_post, fp->off_post, static_cast<int>(xr),
+                 static_cast<int>(row - xr * static_cast<uint32_t>(g.ey)));
+}
+
+__device__ __forceinline__ void stage_rows(const GridDesc& g, const FrameParams* __restrict__ fp, uint32_t r0,
+                                           uint32_t nr, uint32_t* sm) {
+  const int W = g.W;
+  for (uint32_t rr = threadIdx.x; rr < nr; rr += blockDim.x) {
+    const uint32_t* rp = ring_row_post(g, fp, r0 + rr);
+    uint32_t* d = sm + rr * static_cast<uint32_t>(W);
+    if ((W & 3) == 0) {
+      for (int q = 0; q < W; q += 4) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(rp + q));
+        d[q] = v.x, d[q + 1] = v.y, d[q + 2] = v.z, d[q + 3] = v.w;
+      }
+    } else {
+      for (int q = 0; q < W; ++q) d[q] = __ldg(rp + q);
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void load_tile_logical(const GridDesc& g, const FrameParams* __restrict__ fp,
+                                                  uint64_t u_tile, uint64_t u_end, uint32_t* sm, uint32_t* v) {
+  const int W = g.W;
+  const uint32_t r0 = fdiv(static_cast<uint32_t>(u_tile), g.fW);
+  const uint64_t u_last = min(u_end, u_tile + kScanPerBlock);
+  const uint32_t nr = u_last > u_tile ? fdiv(static_cast<uint32_t>(u_last - 1), g.fW) - r0 + 1 : 0u;
+  stage_rows(g, fp, r0, nr, sm);  // nr * W <= kScanStage (W <= kMaxRowWords)
+  const int zb = fp->zb_post;
+  const uint64_t u0 = u_tile + static_cast<uint64_t>(threadIdx.x) * kScanItems;
+  uint32_t row = fdiv(static_cast<uint32_t>(min(u0, u_last)), g.fW);
+  int wz = static_cast<int>(static_cast<uint32_t>(min(u0, u_last)) - row * static_cast<uint32_t>(W));
 #pragma unroll
-  for (int k = 0; k < kScanItems; ++k) c += __popc(v[k]);
+  for (int k = 0; k < kScanItems; ++k) {
+    if (u0 + k >= u_last) {
+      v[k] = 0u;
+      continue;
+    }
+    if (wz == W) {
+      wz = 0;
+      ++row;
+    }
+    const uint32_t* rs = sm + (row - r0) * static_cast<uint32_t>(W);
+    const int pz = ring_z(g, zb, wz * 32), w = pz >> 5, sh = pz & 31;
+    const uint32_t lo = rs[w];
+    v[k] = sh ? __funnelshift_r(lo, rs[w + 1 == W ? 0 : w + 1], sh) : lo;
+    ++wz;
+  }
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_bitmap_count(GridDesc g, const FrameParams* __restrict__ fp,
+                                                               uint64_t w_lo, uint64_t nwords, uint32_t* bsum) {
+  __shared__ uint32_t sm[kScanStage];
+  const uint64_t u_tile = w_lo + static_cast<uint64_t>(blockIdx.x) * kScanPerBlock;
+  uint32_t c = 0;
+  if (kScanPerBlock % g.W == 0 && w_lo % g.W == 0) {
+    // whole rows per tile: a row's count is its ring row's popcount (rotation-free)
+    const uint32_t r0 = fdiv(static_cast<uint32_t>(u_tile), g.fW);
+    const uint64_t u_last = min(w_lo + nwords, u_tile + kScanPerBlock);
+    const uint32_t nr = u_last > u_tile ? static_cast<uint32_t>((u_last - u_tile) / g.W) : 0u;
+    for (uint32_t rr = threadIdx.x; rr < nr; rr += blockDim.x) {
+      const uint32_t* rp = ring_row_post(g, fp, r0 + rr);
+      if ((g.W & 3) == 0) {
+        for (int q = 0; q < g.W; q += 4) {
+          const uint4 v = __ldg(reinterpret_cast<const uint4*>(rp + q));
+          c += __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+        }
+      } else {
+        for (int q = 0; q < g.W; ++q) c += __popc(__ldg(rp + q));
+      }
+    }
+  } else {
+    uint32_t v[kScanItems];
+    load_tile_logical(g, fp, u_tile, w_lo + nwords, sm, v);
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) c += __popc(v[k]);
+  }
   c = block_sum_u32(c);
   if (threadIdx.x == 0) bsum[blockIdx.x] = c;
 }
 
-__global__ void k_bitmap_emit(const FrameParams* __restrict__ fp, uint64_t w_lo, uint64_t nwords, int W,
-                              int ez, const uint32_t* boff, uint32_t* out, uint32_t cap) {
-  const uint32_t* __restrict__ bits = fp->occ_post + w_lo;
-  const uint64_t w0 = (static_cast<uint64_t>(blockIdx.x) * kScanThreads + threadIdx.x) * kScanItems;
+__global__ void __launch_bounds__(kScanThreads) k_bitmap_emit(GridDesc g, const FrameParams* __restrict__ fp,
+                                                              uint64_t w_lo, uint64_t nwords, const uint32_t* boff,
+                                                              uint32_t* out, uint32_t cap) {
+  __shared__ uint32_t sm[kScanStage];
+  const int W = g.W, ez = g.ez;
+  const uint64_t w0 = static_cast<uint64_t>(blockIdx.x) * kScanPerBlock + static_cast<uint64_t>(threadIdx.x) * kScanItems;
   uint32_t v[kScanItems];
-  load_words8(bits, w0, nwords, v);
+  load_tile_logical(g, fp, w_lo + static_cast<uint64_t>(blockIdx.x) * kScanPerBlock, w_lo + nwords, sm, v);
   uint32_t c = 0;
 #pragma unroll
   for (int k = 0; k < kScanItems; ++k) c += __popc(v[k]);
@@ -1205,7 +1330,7 @@ __global__ void k_bitmap_emit(const FrameParams* __restrict__ fp, uint64_t w_lo,
     if (!b) continue;
     const uint64_t w = w0 + k;
     const uint64_t row = (w + w_lo) / W;
-    const uint32_t zb = static_cast<uint32_t>(w % W) * 32;
+    const uint32_t zb = static_cast<uint32_t>((w + w_lo) % W) * 32;
     while (b) {
       const int t = __ffs(b) - 1;
       b &= b - 1;

@@ -46,19 +46,18 @@ __global__ void k_normals(GridDesc g, const FrameParams* __restrict__ fp, Counte
       // neighbours' cells are independent loads; the sums stay in dx,dy,dz order
       const int za = z - 1, zb = z + 1;
       uint32_t occ3[9];
+      // ring position of z - 1 (or of z at the window's bottom): the three
+      // bits z-1, z, z+1 are one 32-bit ring window
+      const int pz = ring_z(g, fp->zb_post, za >= 0 ? za : z);
 #pragma unroll
       for (int q = 0; q < 9; ++q) {
         const int X = x + q / 3 - 1, Y = y + q % 3 - 1;
         uint32_t bits = 0;
         if (X >= 0 && X < g.ex && Y >= 0 && Y < g.ey) {
-          const uint32_t* row = occ + (static_cast<uint64_t>(X) * g.ey + Y) * g.W;
-          const uint32_t wlo = za >= 0 ? __ldg(row + (za >> 5)) : 0u;
-          const uint32_t whi = (zb < g.ez && (zb >> 5) != (z >> 5)) ? __ldg(row + (zb >> 5)) : 0u;
-          const uint32_t wmid = ((z >> 5) == (za >> 5) && za >= 0) ? wlo : __ldg(row + (z >> 5));
-          const uint32_t b0 = za >= 0 ? ((((za >> 5) == (z >> 5)) ? wmid : wlo) >> (za & 31)) & 1u : 0u;
-          const uint32_t b1 = (wmid >> (z & 31)) & 1u;
-          const uint32_t b2 = zb < g.ez ? ((((zb >> 5) == (z >> 5)) ? wmid : whi) >> (zb & 31)) & 1u : 0u;
-          bits = b0 | (b1 << 1) | (b2 << 2);
+          const uint32_t* row = occ_row(g, const_cast<uint32_t*>(occ), off, X, Y);
+          const uint32_t v = ring_bits32(row, g.W, pz);
+          bits = za >= 0 ? (v & 7u) : ((v << 1) & 6u);
+          if (zb >= g.ez) bits &= 3u;
         }
         occ3[q] = bits;
       }
@@ -87,11 +86,12 @@ __global__ void k_normals(GridDesc g, const FrameParams* __restrict__ fp, Counte
       for (int dy = -r; dy <= r; ++dy) {
         const int Y = y + dy;
         if (Y < 0 || Y >= g.ey) continue;
-        const uint32_t* row = occ + (static_cast<uint64_t>(X) * g.ey + Y) * g.W;
+        const uint32_t* row = occ_row(g, const_cast<uint32_t*>(occ), off, X, Y);
         for (int dz = -r; dz <= r; ++dz) {
           const int Z = z + dz;
           if (Z < 0 || Z >= g.ez) continue;
-          if (!((row[Z >> 5] >> (Z & 31)) & 1u)) continue;
+          const int pz = ring_z(g, fp->zb_post, Z);
+          if (!((__ldcg(row + (pz >> 5)) >> (pz & 31)) & 1u)) continue;
           const Cell* c = g.cells + phys_index(g, off, X, Y, Z);
           const double cd = static_cast<double>(c->count);
           const d3 m = mk3(c->sx / cd, c->sy / cd, c->sz / cd);

@@ -447,7 +447,8 @@ struct vp_grid {
   int32_t ext[3];
   int32_t off[3] = {0, 0, 0};
   uint32_t* occ[2] = {nullptr, nullptr};
-  int cur = 0;
+  int cur = 0;  // always 0: one occupancy ring (occ[1] unused)
+  int32_t zb = 0;  // occupancy ring z offset (window z = 0 at ring position zb)
   // Per-frame state in two slots so consecutive frames can be in flight at
   // once (vp_pipeline_run); ctr/h_ctr/d_fp/h_fp/d_pts point at the current slot.
   Counters* ctr_s[kSlots] = {};
@@ -566,6 +567,7 @@ struct vp_grid {
     const uint64_t C = static_cast<uint64_t>(e[0]) * e[1] * e[2];
     if (C >= (1ull << 32) || static_cast<uint64_t>(e[0]) * e[1] * ((e[2] + 31) / 32) * 32 >= 0xffffffffull)
       fail(VP_EINVAL, "VoxelGrid: more than 2^32 cells per grid (use slabs)");
+    if ((e[2] + 31) / 32 > kMaxRowWords) fail(VP_EINVAL, "VoxelGrid: z extent above 2048 cells");
     check_device(dev);
     device = dev;
     for (int k = 0; k < 3; ++k) {
@@ -610,12 +612,10 @@ struct vp_grid {
     gd.ordmap = dalloc<int32_t>(C);
     gd.stbits = dalloc<uint32_t>(gd.nwords);
     occ[0] = dalloc<uint32_t>(gd.nwords);
-    occ[1] = dalloc<uint32_t>(gd.nwords);
     ck(cudaMemsetAsync(gd.cells, 0, C * sizeof(Cell), stream), "memset cells");
     ck(cudaMemsetAsync(gd.clr, 0, gd.nwords * 4, stream), "memset clr");
     ck(cudaMemsetAsync(gd.clrb, 0, gd.nbricks * 8, stream), "memset clrb");
     ck(cudaMemsetAsync(occ[0], 0, gd.nwords * 4, stream), "memset occ");
-    ck(cudaMemsetAsync(occ[1], 0, gd.nwords * 4, stream), "memset occ");
     ck(cudaMemsetAsync(gd.ordmap, 0xff, C * 4, stream), "memset ordmap");
     ck(cudaMemsetAsync(gd.stbits, 0, gd.nwords * 4, stream), "memset stbits");
     for (int q = 0; q < kSlots; ++q) {
@@ -681,16 +681,15 @@ struct vp_grid {
     // drop everything: a shift larger than the window zeroes every occupied cell
     for (int k = 0; k < 3; ++k) h_fp->shift[k] = ext[k] + 1;
     h_fp->do_shift = 1;
-    h_fp->occ_post = occ[cur ^ 1];
     upload_params();
     reset_frame_counters();
     launch_recenter();
     ck(cudaMemsetAsync(occ[0], 0, gd.nwords * 4, stream), "occ");
-    ck(cudaMemsetAsync(occ[1], 0, gd.nwords * 4, stream), "occ");
     for (int q = 0; q < kSlots; ++q) ck(cudaMemsetAsync(ctr_s[q], 0, sizeof(Counters), stream), "ctr");
     ck(cudaMemsetAsync(occ_total, 0, 8, stream), "occ total");
     ck(cudaStreamSynchronize(stream), "reset sync");
     cur = 0;
+    zb = 0;
     host_occupied = 0;
     for (int k = 0; k < 3; ++k) {
       off[k] = 0;
@@ -804,7 +803,8 @@ struct vp_grid {
       h_fp->shift[k] = 0;
     }
     h_fp->do_shift = 0;
-    h_fp->occ_pre = h_fp->occ_post = occ[cur];
+    h_fp->occ_pre = h_fp->occ_post = occ[0];
+    h_fp->zb_pre = h_fp->zb_post = zb;
   }
   // Host part of recenter (voxel_grid.cpp:217-223) -> post-shift state.
   bool plan_recenter(const double* c, vp_shift_stats* st) {
@@ -837,9 +837,14 @@ struct vp_grid {
       h_fp->off_post[k] = off[k];
       h_fp->shift[k] = s[k];
     }
+    {  // the occupancy ring's z offset moves with the window (mod W * 32)
+      const int64_t wz = static_cast<int64_t>(gd.W) * 32;
+      int64_t o = (static_cast<int64_t>(zb) + s[2]) % wz;
+      if (o < 0) o += wz;
+      zb = static_cast<int32_t>(o);
+      h_fp->zb_post = zb;
+    }
     h_fp->do_shift = 1;
-    h_fp->occ_post = occ[cur ^ 1];
-    cur ^= 1;
     return true;
   }
   void upload_params() {
@@ -858,7 +863,7 @@ struct vp_grid {
   // the device params), so the same launches can be replayed as a graph.
   void launch_clear(uint64_t n) {
     launch_clear_walk(n);
-    launch_clear_apply(n);
+    launch_clear_apply(n, 0);
   }
   // clear_rays, first half: the DDA walks mark the clear masks (reads only
   // the points, the pose and the pre-recenter window; touches no cell)
@@ -876,10 +881,13 @@ struct vp_grid {
              g_walk_generic);
   }
   // second half: the marked cells are cleared (and the masks zeroed)
-  void launch_clear_apply(uint64_t n) {
+  // use_box: sweep only the box k_integrate_hash measured for this frame (the
+  // mapping path), else the whole mask (clear_rays alone)
+  void launch_clear_apply(uint64_t n, int use_box) {
     if (n == 0 && !capturing) return;
-    LAUNCH(k_clear_apply, grid_for(std::max<uint64_t>(gd.nwords, gd.nbricks)), kThreads, 0, lstream, gd, d_fp, ctr,
-           dbins);
+    // 148 x 4 blocks, grid-stride over the box (one counter atomic per block)
+    LAUNCH(k_clear_apply, std::min<int>(148 * 4, grid_for(std::max<uint64_t>(gd.nwords, gd.nbricks))), kThreads, 0,
+           lstream, gd, d_fp, ctr, dbins, use_box);
   }
   void launch_integrate(uint64_t n) {
     launch_integrate_group(n, lstream);
@@ -911,8 +919,7 @@ struct vp_grid {
   }
   void launch_recenter() {
     // (the tile counts go to the active segmentation context's scan sums)
-    LAUNCH(k_recenter, static_cast<int>(std::min<uint64_t>((gd.nwords + kScanPerBlock - 1) / kScanPerBlock, 148 * 8)),
-           kScanThreads, 0, lstream, gd, d_fp, ctr, seg.bsum);
+    LAUNCH(k_recenter, grid_for(static_cast<uint64_t>(gd.ex) * gd.ey), kThreads, 0, lstream, gd, d_fp, ctr);
   }
   void launch_finalize() { LAUNCH(k_map_finalize, 1, 1, 0, lstream, ctr, occ_total); }
   // clear_rays and the grouping half of integrate_frame in parallel (fork
@@ -933,7 +940,7 @@ struct vp_grid {
   }
   // the half that updates the cells: clear, ordered fold, recenter
   void launch_mapping_post(uint64_t n) {
-    launch_clear_apply(n);
+    launch_clear_apply(n, 1);
     launch_integrate_fold(n);
     launch_recenter();
     launch_finalize();
@@ -944,10 +951,10 @@ struct vp_grid {
     const uint32_t nb = static_cast<uint32_t>((gd.nwords + kScanPerBlock - 1) / kScanPerBlock);
     const uint64_t w_lo = static_cast<uint64_t>(gd.own_lo) * gd.ey * gd.W;
     const uint64_t w_n = static_cast<uint64_t>(gd.own_hi - gd.own_lo) * gd.ey * gd.W;
-    LAUNCH(k_bitmap_count, nb, kScanThreads, 0, stream, d_fp, w_lo, w_n, seg.bsum);
+    LAUNCH(k_bitmap_count, nb, kScanThreads, 0, stream, gd, d_fp, w_lo, w_n, seg.bsum);
     LAUNCH(k_scan_exclusive, 1, 1024, 0, stream, seg.bsum, nb, nullptr, &ctr->V, nullptr);
-    LAUNCH(k_bitmap_emit, nb, kScanThreads, 0, stream, d_fp, w_lo, w_n, gd.W, gd.ez, seg.bsum,
-           seg.b.occ_list, seg.b.Vcap);
+    LAUNCH(k_bitmap_emit, nb, kScanThreads, 0, stream, gd, d_fp, w_lo, w_n, seg.bsum, seg.b.occ_list,
+           seg.b.Vcap);
   }
 
   // flags[0..*n) -> positions, total into *total
@@ -1308,10 +1315,7 @@ void enqueue_frame_work(vp_pipeline* pl, uint64_t n) {
   ck(cudaMemcpyAsync(g->d_fp, g->h_fp, sizeof(FrameParams), cudaMemcpyHostToDevice, g->stream), "params");
   g->reset_frame_counters();
   ck(cudaEventRecordWithFlags(g->ev[0], g->stream, evflag), "ev");
-  g->launch_clear(n);
-  g->launch_integrate(n);
-  g->launch_recenter();
-  g->launch_finalize();
+  g->launch_mapping_forked(n);  // walks || grouping, then clear (ray box), fold, recenter
   g->launch_segment(pl->p, true);
   ck(cudaMemcpyAsync(g->h_ctr, g->ctr, sizeof(Counters), cudaMemcpyDeviceToHost, g->stream), "ctr d2h");
 }
@@ -1777,6 +1781,7 @@ void rerun_segment_until_fits(vp_grid* g, const vp_pipeline_params& p) {
       g->h_fp->shift[k] = 0;
     }
     g->h_fp->occ_pre = g->h_fp->occ_post;
+    g->h_fp->zb_pre = g->h_fp->zb_post;
     g->h_fp->do_shift = 0;
     g->h_fp->n = 0;
     const unsigned long long occ = g->h_ctr->occupied;
@@ -1939,8 +1944,9 @@ int vp_update_frame(vp_grid* g, const float* xyz, uint64_t n, const double R[9],
     stage_points(g, xyz, n, false);
     g->upload_params();
     g->reset_frame_counters();
-    g->launch_clear(n);
-    g->launch_integrate(n);
+    g->launch_mapping_pre(n);  // grouping (measures the ray box) || walks
+    g->launch_clear_apply(n, 1);
+    g->launch_integrate_fold(n);
     g->launch_finalize();
     g->read_counters();
     if (cs) {

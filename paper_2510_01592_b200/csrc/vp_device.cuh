@@ -47,8 +47,10 @@ struct FrameParams {
   int32_t off_post[3];
   int32_t shift[3];
   int32_t do_shift;
-  uint32_t* occ_pre;   // occupancy bitmap before recenter
-  uint32_t* occ_post;  // after recenter (== occ_pre when no shift)
+  uint32_t* occ_pre;   // occupancy ring (one buffer: occ_pre == occ_post)
+  uint32_t* occ_post;
+  int32_t zb_pre;      // the ring's z offset during clear/integrate
+  int32_t zb_post;     // after recenter
 };
 
 // Division by a grid-invariant divisor d (ex, ey, ez, W) without the ~20
@@ -117,6 +119,8 @@ struct Counters {
   int32_t ccl_giant;     // root of the sampled largest component after the lattice links
   uint32_t ndense;       // integrate groups with more than kFoldMax points (k_integrate_fold_dense)
   uint32_t nmedium;      // integrate groups with kFoldSmall < points <= kFoldMax (k_integrate_fold_medium)
+  int32_t box_lo[3];     // cells the frame's rays can mark (clamped end-point and
+  int32_t box_hi[3];     // sensor cells, k_integrate_hash): k_clear_apply's sweep box
   uint32_t npairs;       // CCL: distinct adjacent root pairs listed by k_ccl_pairs
   uint32_t pair_ovf;     // CCL: the pair table overflowed -> k_ccl_union_bal runs the full union
 };
@@ -276,6 +280,45 @@ __device__ __forceinline__ uint64_t word_of(const GridDesc& g, int x, int y, int
   return (static_cast<uint64_t>(x) * g.ey + y) * g.W + (z >> 5);
 }
 
+// Occupancy ring: the occupancy bitmap is toroidal like the cells -- row
+// (x, y) is stored at the cells' physical (px, py), and z lives on a ring of
+// W * 32 positions with its own offset zb (the window's z = 0 at ring
+// position zb). Ring positions outside the window are always zero. recenter
+// then only clears the bits of cells that leave the window (leaving planes,
+// leaving rows, the leaving z range of each row) instead of rebuilding the
+// whole bitmap. A slab never recenters: its offsets stay 0 and the ring is
+// the plain logical layout (halo planes are copied word for word).
+__device__ __forceinline__ uint32_t* occ_row(const GridDesc& g, uint32_t* occ, const int32_t* off, int x, int y) {
+  int px = x + off[0];
+  if (px >= g.ex) px -= g.ex;
+  int py = y + off[1];
+  if (py >= g.ey) py -= g.ey;
+  return occ + (static_cast<uint64_t>(px) * g.ey + py) * g.W;
+}
+__device__ __forceinline__ int ring_z(const GridDesc& g, int zb, int z) {
+  const int p = z + zb;
+  return p >= (g.W << 5) ? p - (g.W << 5) : p;
+}
+// 32 ring bits from ring position pz (wrapping around the row)
+__device__ __forceinline__ uint32_t ring_bits32(const uint32_t* row, int W, int pz) {
+  const int w = pz >> 5, sh = pz & 31;
+  const uint32_t lo = __ldcg(row + w);
+  if (!sh) return lo;
+  const uint32_t hi = __ldcg(row + (w + 1 == W ? 0 : w + 1));
+  return __funnelshift_r(lo, hi, sh);
+}
+// clear ring bits m (a 32-bit window at ring position pz): one or two words
+__device__ __forceinline__ void ring_clear32(uint32_t* row, int W, int pz, uint32_t m) {
+  const int w = pz >> 5, sh = pz & 31;
+  if (m << sh) atomicAnd(row + w, ~(m << sh));
+  if (sh && (m >> (32 - sh))) atomicAnd(row + (w + 1 == W ? 0 : w + 1), ~(m >> (32 - sh)));
+}
+__device__ __forceinline__ void occ_set(const GridDesc& g, uint32_t* occ, const int32_t* off, int zb, int x, int y,
+                                        int z) {
+  const int pz = ring_z(g, zb, z);
+  atomicOr(occ_row(g, occ, off, x, y) + (pz >> 5), 1u << (pz & 31));
+}
+
 __device__ __forceinline__ bool in_bounds(const GridDesc& g, int x, int y, int z) {
   return x >= 0 && y >= 0 && z >= 0 && x < g.ex && y < g.ey && z < g.ez;
 }
@@ -303,6 +346,41 @@ __device__ __forceinline__ void warp_add_u64(unsigned long long* c, unsigned lon
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
   if (lane_id() == 0 && v) atomicAdd(c, v);
+}
+
+// Block-wide sum of two counters, one atomic each per block (every thread of
+// the block must call it): a grid of per-warp atomics on one address
+// serialises in its L2 slice.
+__device__ __forceinline__ void block_add2_u64(unsigned long long* c0, unsigned long long v0,
+                                               unsigned long long* c1, unsigned long long v1) {
+  __shared__ unsigned long long s0, s1;
+  if (threadIdx.x == 0) s0 = s1 = 0ull;
+  __syncthreads();
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    v0 += __shfl_down_sync(0xffffffffu, v0, o);
+    v1 += __shfl_down_sync(0xffffffffu, v1, o);
+  }
+  if (lane_id() == 0) {
+    if (v0) atomicAdd(&s0, v0);
+    if (v1) atomicAdd(&s1, v1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (s0) atomicAdd(c0, s0);
+    if (s1) atomicAdd(c1, s1);
+  }
+}
+
+__device__ __forceinline__ void block_add_u64(unsigned long long* c, unsigned long long v) {
+  __shared__ unsigned long long s;
+  if (threadIdx.x == 0) s = 0ull;
+  __syncthreads();
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if (lane_id() == 0 && v) atomicAdd(&s, v);
+  __syncthreads();
+  if (threadIdx.x == 0 && s) atomicAdd(c, s);
 }
 
 __device__ __forceinline__ uint32_t hash_u32(uint32_t k) {

@@ -10,6 +10,7 @@ namespace vp {
 constexpr int kScanThreads = 256;
 constexpr int kScanItems = 8;
 constexpr int kScanPerBlock = kScanThreads * kScanItems;  // 2048
+constexpr int kMaxRowWords = 64;  // occupancy ring row: W = ceil(ez / 32) <= 64 (ez <= 2048)
 constexpr int kClusterBins = 2048;  // clusters handled by the counting sort per pass
 constexpr int kChunk = 256;         // ordinals per counting-sort chunk (one warp)
 #ifndef VP_HULL_SMEM
@@ -324,8 +325,8 @@ __global__ void k_clear_walk_slab(GridDesc g, const FrameParams* fp, const uint3
 __global__ void k_dda_keys(GridDesc g, const FrameParams* fp, DdaBins* db, uint8_t* bin_of);
 __global__ void k_dda_plan(DdaBins* db);
 __global__ void k_dda_scatter(const FrameParams* fp, DdaBins* db, const uint8_t* bin_of, uint32_t* perm);
-__global__ void k_clear_apply(GridDesc g, const FrameParams* fp, Counters* ctr, const DdaBins* db);
-__global__ void k_recenter(GridDesc g, const FrameParams* fp, Counters* ctr, uint32_t* bsum);
+__global__ void k_clear_apply(GridDesc g, const FrameParams* fp, Counters* ctr, const DdaBins* db, int use_box);
+__global__ void k_recenter(GridDesc g, const FrameParams* fp, Counters* ctr);
 __global__ void k_map_finalize(Counters* ctr, unsigned long long* occ_total);
 __global__ void k_frame_begin(Counters* ctr, const unsigned long long* occ_total);
 __global__ void k_set_statuses(GridDesc g, const FrameParams* fp, const int32_t* idx, const uint8_t* st,
@@ -336,8 +337,8 @@ __global__ void k_flags_positions(const uint8_t* flags, const uint32_t* n_ptr, u
                                   const uint32_t* boff, uint32_t* pos_out);
 __global__ void k_merge_point(GridDesc g, const FrameParams* fp, Counters* ctr, int x, int y, int z,
                               double px, double py, double pz);
-__global__ void k_bitmap_count(const FrameParams* fp, uint64_t w_lo, uint64_t nwords, uint32_t* bsum);
-__global__ void k_bitmap_emit(const FrameParams* fp, uint64_t w_lo, uint64_t nwords, int W, int ez,
+__global__ void k_bitmap_count(GridDesc g, const FrameParams* fp, uint64_t w_lo, uint64_t nwords, uint32_t* bsum);
+__global__ void k_bitmap_emit(GridDesc g, const FrameParams* fp, uint64_t w_lo, uint64_t nwords,
                               const uint32_t* boff, uint32_t* out, uint32_t cap);
 __global__ void k_scan_exclusive(uint32_t* a, uint32_t n_static, const uint32_t* n_ptr,
                                  uint32_t* total, uint32_t* total2);
