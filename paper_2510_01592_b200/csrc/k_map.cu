@@ -1012,27 +1012,52 @@ __device__ __forceinline__ void clear_apply_rows(const GridDesc& g, const FrameP
     const uint32_t nwz = static_cast<uint32_t>((hi[2] >> 5) - wz0 + 1);
     const uint32_t ny = static_cast<uint32_t>(hi[1] - lo[1] + 1);
     const uint64_t total = static_cast<uint64_t>(hi[0] - lo[0] + 1) * ny * nwz;
-    for (uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < total;
-         q += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-      const uint32_t r = static_cast<uint32_t>(q / nwz);
-      const int wz = wz0 + static_cast<int>(q - static_cast<uint64_t>(r) * nwz);
-      const uint32_t rx = r / ny;
-      const int y = lo[1] + static_cast<int>(r - rx * ny), x = lo[0] + static_cast<int>(rx);
-      const uint64_t w = (static_cast<uint64_t>(x) * g.ey + y) * g.W + wz;
-      const uint32_t c = g.clr[w];
+    // four mask words per thread and trip, loaded before any is processed
+    // (the sweep is latency-bound: most words are zero)
+    constexpr int kPer = 4;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t q0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q0 < total;
+         q0 += kPer * stride) {
+      uint64_t wq[kPer];
+      uint32_t cq[kPer];
+#pragma unroll
+      for (int k = 0; k < kPer; ++k) {
+        const uint64_t q = q0 + k * stride;
+        wq[k] = ~0ull;
+        cq[k] = 0u;
+        if (q < total) {
+          const uint32_t r = static_cast<uint32_t>(q / nwz);
+          const int wz = wz0 + static_cast<int>(q - static_cast<uint64_t>(r) * nwz);
+          const uint32_t rx = r / ny;
+          const int y = lo[1] + static_cast<int>(r - rx * ny), x = lo[0] + static_cast<int>(rx);
+          wq[k] = (static_cast<uint64_t>(x) * g.ey + y) * g.W + wz;
+          cq[k] = g.clr[wq[k]];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kPer; ++k) {
+      const uint32_t c = cq[k];
       if (!c) continue;
+      const uint64_t w = wq[k];
       g.clr[w] = 0;
+      const uint32_t wrow = fdiv(static_cast<uint32_t>(w), g.fW);
+      const int wz = static_cast<int>(static_cast<uint32_t>(w) - wrow * static_cast<uint32_t>(g.W));
+      const uint32_t wx = fdiv(wrow, g.fey);
+      const int y = static_cast<int>(wrow - wx * static_cast<uint32_t>(g.ey)), x = static_cast<int>(wx);
       cl += __popc(c);
-      uint32_t* row = occ_row(g, occ, fp->off_pre, x, y);
+      const uint64_t ri = ring_row_index(g, fp->off_pre, x, y);
+      uint32_t* row = occ + ri * g.W;
       const int pz = ring_z(g, fp->zb_pre, wz * 32);
       uint32_t f = ring_bits32(row, g.W, pz) & c;
       if (!f) continue;
       ring_clear32(row, g.W, pz, f);
+      atomicSub(g.rowcnt + ri, static_cast<uint32_t>(__popc(f)));
       fr += __popc(f);
       while (f) {
         const int b = __ffs(f) - 1;
         f &= f - 1;
         zero_cell(g.cells + phys_index(g, fp->off_pre, x, y, wz * 32 + b));
+      }
       }
     }
   }
@@ -1071,11 +1096,13 @@ __device__ __forceinline__ void clear_apply_bricks(const GridDesc& g, const Fram
         const uint32_t cm = static_cast<uint32_t>(c >> (4 * k)) & 15u;
         cols &= ~(15ull << (4 * k));
         const int x = bx * 4 + (k >> 2), y = by * 4 + (k & 3);
-        uint32_t* row = occ_row(g, occ, fp->off_pre, x, y);
+        const uint64_t ri = ring_row_index(g, fp->off_pre, x, y);
+        uint32_t* row = occ + ri * g.W;
         const int pz = ring_z(g, fp->zb_pre, z0);
         const uint32_t f = ring_bits32(row, g.W, pz) & cm;
         if (!f) continue;
         ring_clear32(row, g.W, pz, f);  // other bricks share these ring words
+        atomicSub(g.rowcnt + ri, static_cast<uint32_t>(__popc(f)));
         fr += __popc(f);
         for (int b = 0; b < 4; ++b)
           if (f & (1u << b)) zero_cell(g.cells + phys_index(g, fp->off_pre, x, y, z0 + b));
@@ -1119,8 +1146,11 @@ __global__ void k_recenter(GridDesc g, const FrameParams* __restrict__ fp, Count
     const bool row_leaves = static_cast<unsigned>(x - sx) >= static_cast<unsigned>(ex) ||
                             static_cast<unsigned>(y - sy) >= static_cast<unsigned>(ey);
     if (!row_leaves && !zleave) continue;
-    uint32_t* row = occ_row(g, occ, fp->off_pre, x, y);
+    const uint64_t ri = ring_row_index(g, fp->off_pre, x, y);
+    if (!__ldcg(g.rowcnt + ri)) continue;  // an empty row drops nothing
+    uint32_t* row = occ + ri * W;
     if (row_leaves) {
+      g.rowcnt[ri] = 0u;
       for (int w = 0; w < W; ++w) {
         uint32_t v = __ldcg(row + w);
         if (!v) continue;
@@ -1142,6 +1172,7 @@ __global__ void k_recenter(GridDesc g, const FrameParams* __restrict__ fp, Count
       uint32_t v = ring_bits32(row, W, pz) & (len >= 32 ? 0xffffffffu : ((1u << len) - 1u));
       if (!v) continue;
       ring_clear32(row, W, pz, v);
+      g.rowcnt[ri] -= static_cast<uint32_t>(__popc(v));  // this thread owns the row here
       dropped += __popc(v);
       while (v) {
         const int b = __ffs(v) - 1;
@@ -1219,123 +1250,70 @@ __device__ __forceinline__ void load_words8(const uint32_t* __restrict__ bits, u
   }
 }
 
-// A block's tile of kScanPerBlock logical words (x, y, z lexicographic: word
-// u = row * W + wz) of the occupancy ring (post-recenter offsets). A ring row
-// is W contiguous words (rotated by zb bits), so the tile's rows are staged in
-// shared memory one row per thread (16-byte loads when W % 4 == 0), and each
-// thread then rotates its kScanItems logical words out of them (logical word
-// wz = 32 ring bits from ring position 32 wz + zb).
-constexpr int kScanStage = kScanPerBlock + 2 * kMaxRowWords;  // a tile's rows: <= 2048 + 2 W words
-
-__device__ __forceinline__ const uint32_t* ring_row_post(const GridDesc& g, const FrameParams* __restrict__ fp,
-                                                         uint32_t row) {
+// Occupied scan over logical rows (x, y lexicographic; row r's cells are
+// r * ez + z): a block takes kScanPerBlock rows, kScanItems per thread. The
+// count pass sums the rows' occupied counts (rowcnt of the ring row); the
+// emit pass reads only non-empty ring rows and rotates their words into
+// logical z order (logical word wz = 32 ring bits from ring position
+// 32 wz + zb).
+__device__ __forceinline__ uint64_t ring_row_of(const GridDesc& g, const FrameParams* __restrict__ fp, uint32_t row) {
   const uint32_t xr = fdiv(row, g.fey);
-  return occ_row(g, fp->occ_post, fp->off_post, static_cast<int>(xr),
-                 static_cast<int>(row - xr * static_cast<uint32_t>(g.ey)));
-}
-
-__device__ __forceinline__ void stage_rows(const GridDesc& g, const FrameParams* __restrict__ fp, uint32_t r0,
-                                           uint32_t nr, uint32_t* sm) {
-  const int W = g.W;
-  for (uint32_t rr = threadIdx.x; rr < nr; rr += blockDim.x) {
-    const uint32_t* rp = ring_row_post(g, fp, r0 + rr);
-    uint32_t* d = sm + rr * static_cast<uint32_t>(W);
-    if ((W & 3) == 0) {
-      for (int q = 0; q < W; q += 4) {
-        const uint4 v = __ldg(reinterpret_cast<const uint4*>(rp + q));
-        d[q] = v.x, d[q + 1] = v.y, d[q + 2] = v.z, d[q + 3] = v.w;
-      }
-    } else {
-      for (int q = 0; q < W; ++q) d[q] = __ldg(rp + q);
-    }
-  }
-  __syncthreads();
-}
-
-__device__ __forceinline__ void load_tile_logical(const GridDesc& g, const FrameParams* __restrict__ fp,
-                                                  uint64_t u_tile, uint64_t u_end, uint32_t* sm, uint32_t* v) {
-  const int W = g.W;
-  const uint32_t r0 = fdiv(static_cast<uint32_t>(u_tile), g.fW);
-  const uint64_t u_last = min(u_end, u_tile + kScanPerBlock);
-  const uint32_t nr = u_last > u_tile ? fdiv(static_cast<uint32_t>(u_last - 1), g.fW) - r0 + 1 : 0u;
-  stage_rows(g, fp, r0, nr, sm);  // nr * W <= kScanStage (W <= kMaxRowWords)
-  const int zb = fp->zb_post;
-  const uint64_t u0 = u_tile + static_cast<uint64_t>(threadIdx.x) * kScanItems;
-  uint32_t row = fdiv(static_cast<uint32_t>(min(u0, u_last)), g.fW);
-  int wz = static_cast<int>(static_cast<uint32_t>(min(u0, u_last)) - row * static_cast<uint32_t>(W));
-#pragma unroll
-  for (int k = 0; k < kScanItems; ++k) {
-    if (u0 + k >= u_last) {
-      v[k] = 0u;
-      continue;
-    }
-    if (wz == W) {
-      wz = 0;
-      ++row;
-    }
-    const uint32_t* rs = sm + (row - r0) * static_cast<uint32_t>(W);
-    const int pz = ring_z(g, zb, wz * 32), w = pz >> 5, sh = pz & 31;
-    const uint32_t lo = rs[w];
-    v[k] = sh ? __funnelshift_r(lo, rs[w + 1 == W ? 0 : w + 1], sh) : lo;
-    ++wz;
-  }
+  return ring_row_index(g, fp->off_post, static_cast<int>(xr), static_cast<int>(row - xr * static_cast<uint32_t>(g.ey)));
 }
 
 __global__ void __launch_bounds__(kScanThreads) k_bitmap_count(GridDesc g, const FrameParams* __restrict__ fp,
-                                                               uint64_t w_lo, uint64_t nwords, uint32_t* bsum) {
-  __shared__ uint32_t sm[kScanStage];
-  const uint64_t u_tile = w_lo + static_cast<uint64_t>(blockIdx.x) * kScanPerBlock;
+                                                               uint64_t r_lo, uint64_t nrows, uint32_t* bsum) {
+  const uint64_t r0 = static_cast<uint64_t>(blockIdx.x) * kRowsPerBlock + static_cast<uint64_t>(threadIdx.x) * kRowItems;
   uint32_t c = 0;
-  if (kScanPerBlock % g.W == 0 && w_lo % g.W == 0) {
-    // whole rows per tile: a row's count is its ring row's popcount (rotation-free)
-    const uint32_t r0 = fdiv(static_cast<uint32_t>(u_tile), g.fW);
-    const uint64_t u_last = min(w_lo + nwords, u_tile + kScanPerBlock);
-    const uint32_t nr = u_last > u_tile ? static_cast<uint32_t>((u_last - u_tile) / g.W) : 0u;
-    for (uint32_t rr = threadIdx.x; rr < nr; rr += blockDim.x) {
-      const uint32_t* rp = ring_row_post(g, fp, r0 + rr);
-      if ((g.W & 3) == 0) {
-        for (int q = 0; q < g.W; q += 4) {
-          const uint4 v = __ldg(reinterpret_cast<const uint4*>(rp + q));
-          c += __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
-        }
-      } else {
-        for (int q = 0; q < g.W; ++q) c += __popc(__ldg(rp + q));
-      }
-    }
-  } else {
-    uint32_t v[kScanItems];
-    load_tile_logical(g, fp, u_tile, w_lo + nwords, sm, v);
 #pragma unroll
-    for (int k = 0; k < kScanItems; ++k) c += __popc(v[k]);
-  }
+  for (int k = 0; k < kRowItems; ++k)
+    if (r0 + k < nrows) c += __ldg(g.rowcnt + ring_row_of(g, fp, static_cast<uint32_t>(r_lo + r0 + k)));
   c = block_sum_u32(c);
   if (threadIdx.x == 0) bsum[blockIdx.x] = c;
 }
 
+// A non-empty row's ring words in logical z order: from ring word zb / 32
+// (its bits >= zb % 32) to the end, then from word 0 back to that word (its
+// bits < zb % 32); all W + 1 loads are independent (L1-resident row).
 __global__ void __launch_bounds__(kScanThreads) k_bitmap_emit(GridDesc g, const FrameParams* __restrict__ fp,
-                                                              uint64_t w_lo, uint64_t nwords, const uint32_t* boff,
+                                                              uint64_t r_lo, uint64_t nrows, const uint32_t* boff,
                                                               uint32_t* out, uint32_t cap) {
-  __shared__ uint32_t sm[kScanStage];
-  const int W = g.W, ez = g.ez;
-  const uint64_t w0 = static_cast<uint64_t>(blockIdx.x) * kScanPerBlock + static_cast<uint64_t>(threadIdx.x) * kScanItems;
-  uint32_t v[kScanItems];
-  load_tile_logical(g, fp, w_lo + static_cast<uint64_t>(blockIdx.x) * kScanPerBlock, w_lo + nwords, sm, v);
+  const int W = g.W, ez = g.ez, zb = fp->zb_post, Wz = g.W << 5;
+  const int s0 = zb >> 5, sh = zb & 31;
+  const uint64_t r0 = static_cast<uint64_t>(blockIdx.x) * kRowsPerBlock + static_cast<uint64_t>(threadIdx.x) * kRowItems;
+  uint32_t cnt[kRowItems];
+  uint64_t ri[kRowItems];
   uint32_t c = 0;
 #pragma unroll
-  for (int k = 0; k < kScanItems; ++k) c += __popc(v[k]);
+  for (int k = 0; k < kRowItems; ++k) {
+    cnt[k] = 0u;
+    ri[k] = 0;
+    if (r0 + k < nrows) {
+      ri[k] = ring_row_of(g, fp, static_cast<uint32_t>(r_lo + r0 + k));
+      cnt[k] = __ldg(g.rowcnt + ri[k]);
+    }
+    c += cnt[k];
+  }
   uint32_t pos = boff[blockIdx.x] + block_exclusive_u32(c);
 #pragma unroll
-  for (int k = 0; k < kScanItems; ++k) {
-    uint32_t b = v[k];
-    if (!b) continue;
-    const uint64_t w = w0 + k;
-    const uint64_t row = (w + w_lo) / W;
-    const uint32_t zb = static_cast<uint32_t>((w + w_lo) % W) * 32;
-    while (b) {
-      const int t = __ffs(b) - 1;
-      b &= b - 1;
-      if (pos < cap) out[pos] = static_cast<uint32_t>(row * ez + zb + t);
-      ++pos;
+  for (int k = 0; k < kRowItems; ++k) {
+    if (!cnt[k]) continue;
+    const uint32_t* row = fp->occ_post + ri[k] * W;
+    const int64_t base = static_cast<int64_t>(r_lo + r0 + k) * ez;
+    for (int t = 0; t <= W; ++t) {
+      int j = s0 + t;
+      if (j >= W) j -= W;
+      uint32_t b = __ldg(row + j);
+      if (t == 0) b &= ~0u << sh;
+      if (t == W) b &= sh ? ((1u << sh) - 1u) : 0u;
+      // ring position p = 32 j + bit -> window z = p - zb (+ Wz once wrapped)
+      const int zoff = 32 * j - zb + (t < W - s0 ? 0 : Wz);
+      while (b) {
+        const int q = __ffs(b) - 1;
+        b &= b - 1;
+        if (pos < cap) out[pos] = static_cast<uint32_t>(base + zoff + q);
+        ++pos;
+      }
     }
   }
 }

@@ -250,7 +250,7 @@ struct Seg {
     const uint32_t mcap = scap + 32u * kClusterBins;
     const bool need = !b.occ_list || vcap > b.Vcap || scap > b.Scap || icap > b.Icap ||
                       static_cast<uint64_t>(iterations) * kClusterBins > cand_cap;
-    const uint64_t need_bsum = std::max<uint64_t>({(nwords + kScanPerBlock - 1) / kScanPerBlock,
+    const uint64_t need_bsum = std::max<uint64_t>({(nwords + kRowsPerBlock - 1) / kRowsPerBlock,  // >= rows / tile
                                                    (vcap + kThreads - 1) / kThreads,
                                                    (scap + kScanPerBlock - 1) / kScanPerBlock}) + 1;
     if (need) {
@@ -526,6 +526,7 @@ struct vp_grid {
     }
     if (gd.ordmap) cudaFree(gd.ordmap);
     if (gd.stbits) cudaFree(gd.stbits);
+    if (gd.rowcnt) cudaFree(gd.rowcnt);
     if (gmap) cudaFree(gmap);
     if (gbits) cudaFree(gbits);
     sl.release();
@@ -567,7 +568,6 @@ struct vp_grid {
     const uint64_t C = static_cast<uint64_t>(e[0]) * e[1] * e[2];
     if (C >= (1ull << 32) || static_cast<uint64_t>(e[0]) * e[1] * ((e[2] + 31) / 32) * 32 >= 0xffffffffull)
       fail(VP_EINVAL, "VoxelGrid: more than 2^32 cells per grid (use slabs)");
-    if ((e[2] + 31) / 32 > kMaxRowWords) fail(VP_EINVAL, "VoxelGrid: z extent above 2048 cells");
     check_device(dev);
     device = dev;
     for (int k = 0; k < 3; ++k) {
@@ -611,7 +611,9 @@ struct vp_grid {
     gd.clrb = dalloc<unsigned long long>(gd.nbricks);
     gd.ordmap = dalloc<int32_t>(C);
     gd.stbits = dalloc<uint32_t>(gd.nwords);
+    gd.rowcnt = dalloc<uint32_t>(static_cast<uint64_t>(e[0]) * e[1]);
     occ[0] = dalloc<uint32_t>(gd.nwords);
+    ck(cudaMemsetAsync(gd.rowcnt, 0, static_cast<uint64_t>(e[0]) * e[1] * 4, stream), "memset rowcnt");
     ck(cudaMemsetAsync(gd.cells, 0, C * sizeof(Cell), stream), "memset cells");
     ck(cudaMemsetAsync(gd.clr, 0, gd.nwords * 4, stream), "memset clr");
     ck(cudaMemsetAsync(gd.clrb, 0, gd.nbricks * 8, stream), "memset clrb");
@@ -685,6 +687,7 @@ struct vp_grid {
     reset_frame_counters();
     launch_recenter();
     ck(cudaMemsetAsync(occ[0], 0, gd.nwords * 4, stream), "occ");
+    ck(cudaMemsetAsync(gd.rowcnt, 0, static_cast<uint64_t>(gd.ex) * gd.ey * 4, stream), "rowcnt");
     for (int q = 0; q < kSlots; ++q) ck(cudaMemsetAsync(ctr_s[q], 0, sizeof(Counters), stream), "ctr");
     ck(cudaMemsetAsync(occ_total, 0, 8, stream), "occ total");
     ck(cudaStreamSynchronize(stream), "reset sync");
@@ -885,7 +888,8 @@ struct vp_grid {
   // mapping path), else the whole mask (clear_rays alone)
   void launch_clear_apply(uint64_t n, int use_box) {
     if (n == 0 && !capturing) return;
-    // 148 x 4 blocks, grid-stride over the box (one counter atomic per block)
+    // 148 x 4 blocks, grid-stride over the box, four mask loads in flight per
+    // thread; one counter atomic per block
     LAUNCH(k_clear_apply, std::min<int>(148 * 4, grid_for(std::max<uint64_t>(gd.nwords, gd.nbricks))), kThreads, 0,
            lstream, gd, d_fp, ctr, dbins, use_box);
   }
@@ -948,12 +952,13 @@ struct vp_grid {
 
   // Occupied scan of the post-recenter bitmap into seg.b.occ_list; ctr->V.
   void launch_occupied_scan() {
-    const uint32_t nb = static_cast<uint32_t>((gd.nwords + kScanPerBlock - 1) / kScanPerBlock);
-    const uint64_t w_lo = static_cast<uint64_t>(gd.own_lo) * gd.ey * gd.W;
-    const uint64_t w_n = static_cast<uint64_t>(gd.own_hi - gd.own_lo) * gd.ey * gd.W;
-    LAUNCH(k_bitmap_count, nb, kScanThreads, 0, stream, gd, d_fp, w_lo, w_n, seg.bsum);
+    // over the owned logical rows (x, y): row counts, then the non-empty rows
+    const uint64_t r_lo = static_cast<uint64_t>(gd.own_lo) * gd.ey;
+    const uint64_t r_n = static_cast<uint64_t>(gd.own_hi - gd.own_lo) * gd.ey;
+    const uint32_t nb = static_cast<uint32_t>((r_n + kRowsPerBlock - 1) / kRowsPerBlock);
+    LAUNCH(k_bitmap_count, nb, kScanThreads, 0, stream, gd, d_fp, r_lo, r_n, seg.bsum);
     LAUNCH(k_scan_exclusive, 1, 1024, 0, stream, seg.bsum, nb, nullptr, &ctr->V, nullptr);
-    LAUNCH(k_bitmap_emit, nb, kScanThreads, 0, stream, gd, d_fp, w_lo, w_n, seg.bsum, seg.b.occ_list,
+    LAUNCH(k_bitmap_emit, nb, kScanThreads, 0, stream, gd, d_fp, r_lo, r_n, seg.bsum, seg.b.occ_list,
            seg.b.Vcap);
   }
 

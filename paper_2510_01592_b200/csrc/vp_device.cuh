@@ -71,6 +71,8 @@ struct GridDesc {
   uint32_t* clr;
   int32_t* ordmap;
   uint32_t* stbits;  // steppable presence bitmap (logical, occ layout)
+  uint32_t* rowcnt;  // occupied cells per ring row (physical (px, py)): the occupied
+                     // scan reads only non-empty rows (kept by integrate, clear, recenter)
   int32_t ex, ey, ez, W;  // (local) extent and words per (x,y) row
   double res;
   uint64_t ncells;
@@ -313,10 +315,20 @@ __device__ __forceinline__ void ring_clear32(uint32_t* row, int W, int pz, uint3
   if (m << sh) atomicAnd(row + w, ~(m << sh));
   if (sh && (m >> (32 - sh))) atomicAnd(row + (w + 1 == W ? 0 : w + 1), ~(m >> (32 - sh)));
 }
+__device__ __forceinline__ uint64_t ring_row_index(const GridDesc& g, const int32_t* off, int x, int y) {
+  int px = x + off[0];
+  if (px >= g.ex) px -= g.ex;
+  int py = y + off[1];
+  if (py >= g.ey) py -= g.ey;
+  return static_cast<uint64_t>(px) * g.ey + py;
+}
+// a newly occupied cell: its ring bit and its row's count
 __device__ __forceinline__ void occ_set(const GridDesc& g, uint32_t* occ, const int32_t* off, int zb, int x, int y,
                                         int z) {
   const int pz = ring_z(g, zb, z);
-  atomicOr(occ_row(g, occ, off, x, y) + (pz >> 5), 1u << (pz & 31));
+  const uint64_t r = ring_row_index(g, off, x, y);
+  atomicOr(occ + r * g.W + (pz >> 5), 1u << (pz & 31));
+  atomicAdd(g.rowcnt + r, 1u);
 }
 
 __device__ __forceinline__ bool in_bounds(const GridDesc& g, int x, int y, int z) {

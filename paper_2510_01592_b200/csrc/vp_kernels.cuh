@@ -10,7 +10,8 @@ namespace vp {
 constexpr int kScanThreads = 256;
 constexpr int kScanItems = 8;
 constexpr int kScanPerBlock = kScanThreads * kScanItems;  // 2048
-constexpr int kMaxRowWords = 64;  // occupancy ring row: W = ceil(ez / 32) <= 64 (ez <= 2048)
+constexpr int kRowItems = 2;  // occupied scan: ring rows per thread
+constexpr int kRowsPerBlock = kScanThreads * kRowItems;  // 512
 constexpr int kClusterBins = 2048;  // clusters handled by the counting sort per pass
 constexpr int kChunk = 256;         // ordinals per counting-sort chunk (one warp)
 #ifndef VP_HULL_SMEM
