@@ -15,13 +15,14 @@ inside) and the final polygons read back.
 the unmodified /root/reference sources) on the host cores over a bounded
 sample of the same stream.
 
-N > 1 (default C2): the path is a per-robot map whose 5 m window needs no
-slabbing, so ranks run independent replicas of the stream (weak scaling, no
-data-path collective); only the timing barrier / max use torch.distributed.
---workload c5 runs BASELINE configs[4], one 2000x2000x300 window split into
-x-slabs across the ranks (paper_2510_01592_b200/slabs.py: halo
-planes, halo steppable lists, boundary-label merge, cluster gather to the
-owning slab, all over NCCL; strong scaling).
+N > 1 (default C5, BASELINE configs[4]): one 2000x2000x300 window split into
+x-slabs across the ranks, each frame one vp_slab_frame call
+per rank (csrc/slab_frame.cu: frame broadcast, halo planes, halo steppable
+lists, boundary-label merge, cluster gather to the owning slab and the
+polygon gather, all over the library's NCCL communicator; strong scaling).
+--workload c2 with N > 1 runs independent replicas of the per-robot C2 stream
+(weak scaling, no data-path collective: the fallback where slabbing does not
+apply).
 
 At N = 1 the line also carries secondary `configs` (C1, C3, C4 and C5 as one
 slab) measured the same way.
@@ -515,20 +516,30 @@ def run_slabs(args, rank, world, dist):
     ext = scenes.C5_EXTENT
     lo, hi = slabs.split_x(ext[0], world)[rank]
     slab = slabs.Slab(0.01, ext, scenes.C5_CENTER, lo, hi, device=dev)
+    # the timed frames run the library-orchestrated vp_slab_frame over the
+    # library's NCCL communicator; the profiled frame below uses the Python
+    # model of the same protocol (its phase counters feed the roofline)
     comm = slabs.DistComm(dist, dev) if dist else slabs.LocalComm(1)
+    ncomm = slabs.nccl_comm(dist, dev) if dist else None
     params = native.default_params(seed=2025)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{dev}")
     empty = torch.empty(0, dtype=torch.float32, device=f"cuda:{dev}")
     dev_pts = [torch.from_numpy(f.points).to(f"cuda:{dev}") for f in frames] if rank == 0 else None
     host_pts = [torch.from_numpy(f.points).pin_memory() for f in frames] if rank == 0 else None
     npts = [len(f.points) for f in frames] if rank == 0 else [0] * nf
+    if dist:  # every rank passes n to vp_slab_frame
+        nt = torch.tensor(npts, dtype=torch.int64, device=f"cuda:{dev}")
+        dist.broadcast(nt, 0)
+        npts = [int(v) for v in nt.cpu().tolist()]
 
     def rot(i):
         return poses[i][:9].reshape(3, 3), poses[i][9:12]
 
     def step(i, pts):
         R, t = rot(i)
-        return slabs.slab_frame([slab], comm, pts, R, t, params)
+        if ncomm is None:
+            return slabs.frame_local([slab], pts, R, t, params)
+        return slabs.frame(slab, ncomm, pts if rank == 0 else None, npts[i], R, t, params)
 
     for i in range(W):
         step(i, dev_pts[i] if rank == 0 else empty)
@@ -581,6 +592,8 @@ def run_slabs(args, rank, world, dist):
     nk = L.vp_profile_read(names, ms, calls, 128)
     L.vp_profile_enable(0)
     prof = {names[j].decode(): (ms[j], calls[j]) for j in range(nk)}
+    if ncomm is not None:
+        slabs.nccl_comm_destroy(ncomm)
     if rank != 0:
         slab.close()
         return None
@@ -629,9 +642,10 @@ def run_slabs(args, rank, world, dist):
                    "slabs": [list(r) for r in slabs.split_x(ext[0], world)], "timed_frames": f"{W}..{W + K - 1}",
                    "e2e_frames": f"{W}..{W + K - 1} again (revisit)", "points_per_frame": round(timed_pts / K),
                    "l2": "flushed (256 MiB write) between steps; window 38.4 GB >> L2",
-                   "parallelism": f"x-slabs x{world} (halo planes, halo steppable lists, boundary-label "
-                                  "merge and cluster gather to the owner over NCCL)"
-                   if world > 1 else "single slab"},
+                   "parallelism": f"x-slabs x{world}: one vp_slab_frame per rank and frame (halo planes, "
+                                  "halo steppable lists, boundary-label merge, cluster gather to the owner, "
+                                  "polygon gather; library NCCL communicator)"
+                   if world > 1 else "single slab (vp_slab_frame_local)"},
         "gpu_launches": int(launches),
         "e2e": {"value": round(K / (e2e_ms / 1e3), 3), "unit": "Hz",
                 "h2d_bytes_per_step": int(12 * timed_pts / K),
@@ -799,7 +813,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2")
+    ap.add_argument("--workload", default=None, help="c2 (default at N = 1) or c5 (default at N > 1)")
     ap.add_argument("--cpu-frames", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-configs", action="store_true", help="skip the secondary C1/C3/C4/C5 lines")
@@ -822,6 +836,8 @@ def main():
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
         tdist.init_process_group("nccl")
         dist = tdist
+    if args.workload is None:
+        args.workload = "c5" if world > 1 else "c2"
     out = (run_slabs if args.workload == "c5" else run_ours)(args, rank, world, dist)
     if rank == 0:
         print(json.dumps(out))

@@ -338,6 +338,52 @@ int vp_slab_export(vp_grid* g, uint64_t* dest_counts, void** records);
 int vp_slab_segment_owned(vp_grid* g, const vp_pipeline_params* p, const void* recv, uint64_t n_recv,
                           vp_polygons_t** out);
 
+/* ---- one slab frame, orchestrated in the library --------
+   The whole per-frame exchange sequence above (frame broadcast, halo planes,
+   plane counts, halo steppable lists, boundary triples, cluster members,
+   polygon gather to rank 0) as ONE call per rank, over a communicator given
+   as a table of stream-ordered collectives on device buffers -- the library's
+   own NCCL communicator (vp_comm_nccl_create: NVLink / NVSwitch between the
+   GPUs of a node) or any caller-provided implementation with the same
+   semantics (e.g. torch.distributed). */
+typedef struct {
+  int32_t peer;
+  int32_t send;   /* 1 send, 0 receive */
+  void* ptr;      /* device buffer */
+  uint64_t bytes;
+} vp_p2p_op;
+typedef struct {
+  void* ctx;
+  int32_t rank;
+  int32_t nranks;
+  /* stream = the slab grid's cudaStream_t; all buffers are device memory;
+     each returns 0 on success */
+  int (*broadcast)(void* ctx, void* buf, uint64_t bytes, int32_t root, void* stream);
+  int (*allgather)(void* ctx, const void* send, void* recv, uint64_t bytes_per_rank, void* stream);
+  /* point-to-point sends / receives as one group (matched in call order per peer pair) */
+  int (*group)(void* ctx, int32_t n, const vp_p2p_op* ops, void* stream);
+} vp_comm_ops;
+/* NCCL communicator of nranks GPUs (libnccl.so.2 is loaded at run time; one
+   rank per GPU, one process per rank). Rank 0 creates the 128-byte id and the
+   caller hands it to every rank (any host channel). */
+int vp_comm_nccl_unique_id(uint8_t id[128]);
+int vp_comm_nccl_create(const uint8_t id[128], int32_t nranks, int32_t rank, int device, vp_comm_ops* out);
+int vp_comm_nccl_destroy(vp_comm_ops* comm);
+/* One frame on this rank's slab (rank k of the communicator owns slab k; the
+   slabs' x ranges tile the window in rank order): points are rank 0's (host
+   or device; the other ranks pass the same n and NULL); polygons of the
+   whole window in ascending label order on rank 0 (NULL elsewhere) -- equal
+   to run_frames' voxel_frame_polygons on one grid. */
+int vp_slab_frame(vp_grid* slab, const vp_comm_ops* comm, const float* xyz, uint64_t n,
+                  const double rotation[9], const double translation[3], const vp_pipeline_params* p,
+                  vp_polygons_t** out);
+/* The same with n_slabs slabs in this process (virtual slabs, e.g. on one
+   GPU): one host thread per slab runs vp_slab_frame over an in-process
+   communicator (device-to-device copies). */
+int vp_slab_frame_local(vp_grid* const* slabs, int32_t n_slabs, const float* xyz, uint64_t n,
+                        const double rotation[9], const double translation[3], const vp_pipeline_params* p,
+                        vp_polygons_t** out);
+
 /* run_frames state: a grid plus the global-cell recenter trigger
    (pipeline.cpp:165, 174, 199-213). */
 int vp_pipeline_create(double resolution, const int32_t extent[3],

@@ -24,6 +24,10 @@
 
 using namespace vp;
 
+namespace vp {
+void slab_frame_release(vp_grid* g);  // slab_frame.cu
+}
+
 namespace {
 
 thread_local std::string g_err;
@@ -1886,7 +1890,10 @@ int vp_grid_create(double res, const int32_t extent[3], const double center[3], 
   });
 }
 
-void vp_grid_destroy(vp_grid* g) { delete g; }
+void vp_grid_destroy(vp_grid* g) {
+  vp::slab_frame_release(g);
+  delete g;
+}
 
 int vp_grid_info(const vp_grid* g, double origin[3], int32_t extent[3], double* resolution,
                  uint64_t* occupied_count) {
@@ -2967,6 +2974,23 @@ int vp_make_polygons(size_t n, const vp_plane* planes, const uint64_t* offsets,
 }
 
 void vp_polygons_free(vp_polygons_t* p) { std::free(p); }
+
+}  // extern "C"
+
+// Accessors for the slab-frame orchestration (slab_frame.cu).
+namespace vp {
+void set_last_error(const char* msg) { g_err = msg; }
+cudaStream_t slab_stream(vp_grid* g) { return g->stream; }
+void slab_geometry(vp_grid* g, int32_t* xb, int32_t* xe, int32_t* gex, int* device, double* res) {
+  *xb = g->gd.xoff + g->gd.own_lo;
+  *xe = g->gd.xoff + g->gd.own_hi;
+  *gex = g->gd.gex;
+  *device = g->device;
+  *res = g->gd.res;
+}
+}  // namespace vp
+
+extern "C" {
 
 int vp_slab_create(double res, const int32_t window_extent[3], const double center[3],
                    int32_t x_begin, int32_t x_end, int device, vp_grid** out) {

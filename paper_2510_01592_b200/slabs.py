@@ -27,10 +27,17 @@ flat index, voxel_grid.hpp:43-46), one slab per rank. Per frame:
    (vp_slab_segment_owned);
 9. polygons are gathered to rank 0 in slab order (= ascending label order).
 
-The same phase functions drive N virtual slabs in one process (LocalComm:
-exchanges are device copies; used by the single-GPU parity tests) or one slab
-per rank under torch.distributed (DistComm: NCCL broadcast / all-gather /
-send-recv on B200s, gloo in the CPU tests).
+The product path runs the whole sequence inside the library, one call per
+rank and frame (vp_slab_frame, csrc/slab_frame.cu): the exchanges are
+stream-ordered collectives of a communicator table -- the library's NCCL
+communicator (nccl_comm: NVLink / NVSwitch between the GPUs of a node), the
+in-process hub of vp_slab_frame_local (N virtual slabs on one GPU, one host
+thread each), or TorchCommOps (any torch.distributed backend; the CPU-staged
+gloo variant drives two processes on one GPU in the tests).
+
+slab_frame() below is the same sequence written in Python over the
+library's phase functions (LocalComm / DistComm); it is kept as an executable
+model of the protocol for the gloo CPU tests (tests/test_slab_comm.py).
 """
 from __future__ import annotations
 
@@ -529,3 +536,158 @@ def _ranges(slabs, comm):
             _RANGES_CACHE[key] = [tuple(int(v) for v in a.tolist()) for a in allr]
         return _RANGES_CACHE[key]
     return [(s.x_begin, s.x_end) for s in slabs]
+
+
+# ------------------------------------------------- library-orchestrated frame
+class P2POp(C.Structure):
+    _fields_ = [("peer", C.c_int32), ("send", C.c_int32), ("ptr", C.c_void_p), ("bytes", C.c_uint64)]
+
+
+_BCAST = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_int32, C.c_void_p)
+_ALLG = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p)
+_GROUP = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int32, C.POINTER(P2POp), C.c_void_p)
+
+
+class CommOps(C.Structure):
+    """vp_comm_ops: the communicator table vp_slab_frame runs its exchanges on."""
+    _fields_ = [("ctx", C.c_void_p), ("rank", C.c_int32), ("nranks", C.c_int32),
+                ("broadcast", _BCAST), ("allgather", _ALLG), ("group", _GROUP)]
+
+
+def nccl_comm(dist, device: int) -> CommOps:
+    """The library's NCCL communicator over the ranks of `dist` (one GPU each);
+    the 128-byte unique id travels through dist (setup only)."""
+    import torch
+    rank, world = dist.get_rank(), dist.get_world_size()
+    uid = np.zeros(128, np.uint8)
+    if rank == 0:
+        check(lib().vp_comm_nccl_unique_id(_p(uid, C.c_uint8)))
+    t = torch.from_numpy(uid).to(f"cuda:{device}" if dist.get_backend() == "nccl" else "cpu")
+    dist.broadcast(t, 0)
+    uid = np.ascontiguousarray(t.cpu().numpy())
+    ops = CommOps()
+    check(lib().vp_comm_nccl_create(_p(uid, C.c_uint8), C.c_int32(world), C.c_int32(rank), C.c_int(device),
+                                    C.byref(ops)))
+    return ops
+
+
+def nccl_comm_destroy(ops: CommOps) -> None:
+    lib().vp_comm_nccl_destroy(C.byref(ops))
+
+
+class TorchCommOps:
+    """vp_comm_ops implemented with torch.distributed collectives. With a gloo
+    group the device buffers are staged through host tensors (the library's
+    stream is drained first); used to run real slabs in several processes on
+    one GPU, where NCCL refuses duplicate devices."""
+
+    def __init__(self, dist, device: int):
+        import torch
+        self.dist, self.device = dist, device
+        self.rank, self.world = dist.get_rank(), dist.get_world_size()
+        self._torch = torch
+        self.ops = CommOps()
+        self.ops.ctx = None
+        self.ops.rank, self.ops.nranks = self.rank, self.world
+        # keep the callbacks alive as long as this object
+        self._cb = (_BCAST(self._bcast), _ALLG(self._allgather), _GROUP(self._group))
+        self.ops.broadcast, self.ops.allgather, self.ops.group = self._cb
+
+    def _sync(self, stream):
+        # the library's stream: its producers must be done before the copies
+        self._torch.cuda.ExternalStream(stream, device=f"cuda:{self.device}").synchronize()
+
+    def _d2h(self, ptr, nbytes):
+        if not nbytes:
+            return np.empty(0, np.uint8)
+        return DeviceBuffer(ptr, nbytes, self.device).tensor().cpu().numpy()
+
+    def _h2d(self, ptr, buf):
+        if buf.nbytes:
+            DeviceBuffer(ptr, buf.nbytes, self.device).tensor().copy_(self._torch.from_numpy(buf))
+            self._torch.cuda.current_stream(self.device).synchronize()  # before the library stream reads it
+
+    def _bcast(self, ctx, buf, nbytes, root, stream):
+        try:
+            self._sync(stream)
+            h = self._d2h(buf, nbytes) if self.rank == root else np.empty(nbytes, np.uint8)
+            t = self._torch.from_numpy(h)
+            self.dist.broadcast(t, int(root))
+            if self.rank != root:
+                self._h2d(buf, t.numpy())
+            return 0
+        except Exception:  # noqa: BLE001 -- reported to the library as a failed collective
+            return 1
+
+    def _allgather(self, ctx, send, recv, nbytes, stream):
+        try:
+            self._sync(stream)
+            t = self._torch.from_numpy(self._d2h(send, nbytes))
+            outs = [self._torch.empty(nbytes, dtype=self._torch.uint8) for _ in range(self.world)]
+            self.dist.all_gather(outs, t)
+            self._h2d(recv, self._torch.cat(outs).numpy())
+            return 0
+        except Exception:  # noqa: BLE001
+            return 1
+
+    def _group(self, ctx, n, ops, stream):
+        try:
+            self._sync(stream)
+            reqs, recvs = [], []
+            for i in range(n):
+                o = ops[i]
+                if not o.bytes:
+                    continue
+                if o.send:
+                    reqs.append(self.dist.isend(self._torch.from_numpy(self._d2h(o.ptr, o.bytes)), int(o.peer)))
+                else:
+                    t = self._torch.empty(int(o.bytes), dtype=self._torch.uint8)
+                    reqs.append(self.dist.irecv(t, int(o.peer)))
+                    recvs.append((o.ptr, t))
+            for r in reqs:
+                r.wait()
+            for ptr, t in recvs:
+                self._h2d(ptr, t.numpy())
+            return 0
+        except Exception:  # noqa: BLE001
+            return 1
+
+
+def frame(slab: Slab, ops, pts, n: int, R, t, params: native.PipelineParams):
+    """One frame on this rank's slab (vp_slab_frame): rank 0 passes its points
+    (numpy host array or a device tensor), the others None and the same n.
+    Returns the window's polygons on rank 0, else None."""
+    R, t = _pose(R, t)
+    ops_s = ops.ops if isinstance(ops, TorchCommOps) else ops
+    ptr = _points_ptr(pts)
+    out = C.POINTER(native.Polygons)()
+    check(lib().vp_slab_frame(slab.h, C.byref(ops_s), C.c_void_p(ptr), C.c_uint64(n), _p(R, C.c_double),
+                              _p(t, C.c_double), C.byref(params), C.byref(out)))
+    return polygons_to_py(out) if out else None
+
+
+def frame_local(slabs_list, pts, R, t, params: native.PipelineParams):
+    """One frame over N virtual slabs in this process (vp_slab_frame_local)."""
+    R, t = _pose(R, t)
+    arr = (C.c_void_p * len(slabs_list))(*[s.h.value for s in slabs_list])
+    n = _points_len(pts)
+    out = C.POINTER(native.Polygons)()
+    check(lib().vp_slab_frame_local(arr, C.c_int32(len(slabs_list)), C.c_void_p(_points_ptr(pts)), C.c_uint64(n),
+                                    _p(R, C.c_double), _p(t, C.c_double), C.byref(params), C.byref(out)))
+    return polygons_to_py(out)
+
+
+def _points_ptr(pts):
+    if pts is None:
+        return 0
+    if hasattr(pts, "data_ptr"):
+        return pts.data_ptr()
+    return np.ascontiguousarray(pts, np.float32).ctypes.data
+
+
+def _points_len(pts):
+    if pts is None:
+        return 0
+    if hasattr(pts, "data_ptr"):
+        return pts.numel() // 3 if pts.dtype.itemsize == 4 else pts.numel() // 12
+    return len(pts)

@@ -100,6 +100,42 @@ def check_slabs(ranges, frames):
     assert format_polygons(polys) == format_polygons(ref_polys)
 
 
+def check_slabs_library(ranges, frames, device_points=True):
+    """The library-orchestrated frame (vp_slab_frame_local: one host thread per
+    slab, the exchanges as device copies) gives the one-grid polygons."""
+    params = native.default_params(seed=5, refine_exact=True)
+    _, ref_polys = one_grid(frames, params)
+    sl = [slabs.Slab(RES, EXTENT, CENTER, a, b) for a, b in ranges]
+    polys = None
+    for f in frames:
+        pts = torch.from_numpy(np.ascontiguousarray(f.points)).cuda() if device_points else f.points
+        polys = slabs.frame_local(sl, pts, f.rotation, f.translation, params)
+    assert len(ref_polys) >= 3
+    assert format_polygons(polys) == format_polygons(ref_polys)
+    for s in sl:
+        s.close()
+
+
+@pytest.mark.parametrize("ranges", [[(0, 300)], [(0, 150), (150, 300)], [(0, 37), (37, 150), (150, 151), (151, 300)],
+                                    [(a, a + 38) for a in range(0, 266, 38)] + [(266, 300)]])
+def test_library_slab_frame_equals_one_grid(ranges):
+    check_slabs_library(ranges, scenes.stair_frames(10))
+
+
+def test_library_slab_frame_lidar_host_points():
+    check_slabs_library([(0, 100), (100, 102), (102, 104), (104, 200), (200, 300)], scenes.lidar_stair_frames(6),
+                        device_points=False)
+
+
+def test_library_slab_frame_reports_bad_layout():
+    # x ranges that do not tile the window: every slab thread fails, the first error is reported
+    params = native.default_params(seed=5)
+    sl = [slabs.Slab(RES, EXTENT, CENTER, 0, 100), slabs.Slab(RES, EXTENT, CENTER, 120, 300)]
+    f = scenes.stair_frames(1)[0]
+    with pytest.raises(native.InvalidArgument, match="tile the window"):
+        slabs.frame_local(sl, f.points, f.rotation, f.translation, params)
+
+
 def test_slab_window_is_fixed():
     s = slabs.Slab(RES, EXTENT, CENTER, 0, 100)
     from ctypes import byref
