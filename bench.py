@@ -304,7 +304,9 @@ def run_ours(args, rank, world, dist):
     # host points (H2D start) to the frame's polygons in host memory, CUDA
     # events on the library stream; median of frames 2..F of a pass from an
     # empty map
-    lat = []
+    lat, lat_py = [], []
+    L.vp_pipeline_latency_ms.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
+    lat_ms = C.c_double()
     for rep in range(2):
         reset()
         torch.cuda.synchronize()
@@ -316,7 +318,9 @@ def run_ours(args, rank, world, dist):
             e1.record(stream)
             e1.synchronize()
             if rep == 1 and k >= 2:
-                lat.append(e0.elapsed_time(e1))
+                native.check(L.vp_pipeline_latency_ms(pl.h, C.byref(lat_ms)))
+                lat.append(lat_ms.value)           # library events: H2D start -> polygons in host memory
+                lat_py.append(e0.elapsed_time(e1))  # the same seen from Python (plus ctypes + numpy conversion)
     clk.__exit__(None, None, None)
 
     # per-kernel profile of one step (serialised launches; shares only)
@@ -399,8 +403,11 @@ def run_ours(args, rank, world, dist):
         "gpu_launches": int(launches),
         "latency_ms_p50": round(statistics.median(lat), 4),
         "latency_ms_p90": round(sorted(lat)[int(0.9 * (len(lat) - 1))], 4),
+        "latency_ms_p50_python": round(statistics.median(lat_py), 4),
         "latency": "one frame in flight (vp_pipeline_frame): pinned host points -> polygons on the host, "
-                   "CUDA events, frames 2..29 of a pass from an empty map",
+                   "library CUDA events (vp_pipeline_latency_ms: before the points H2D -> polygons assembled in "
+                   "host memory), frames 2..29 of a pass from an empty map; latency_ms_p50_python adds the "
+                   "ctypes call and numpy conversion",
         "e2e": {"value": round(e2e_value, 3), "unit": "Hz",
                 "h2d_bytes_per_step": int(12 * sum(npts)), "d2h_bytes_per_step": int(d2h_bytes)},
         "roofline": {"bound": "hbm", "kernel": top, "achieved": round(achieved, 2), "peak": peak,

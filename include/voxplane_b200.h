@@ -338,6 +338,11 @@ int vp_slab_export(vp_grid* g, uint64_t* dest_counts, void** records);
 int vp_slab_segment_owned(vp_grid* g, const vp_pipeline_params* p, const void* recv, uint64_t n_recv,
                           vp_polygons_t** out);
 
+/* End-to-end latency of the last vp_pipeline_frame / _device call (SURVEY
+   §8(d) unit of work): CUDA events from before the points' H2D copy to after
+   the frame's polygons are assembled in host memory, in milliseconds. */
+int vp_pipeline_latency_ms(const vp_pipeline* pl, double* ms);
+
 /* ---- one slab frame, orchestrated in the library --------
    The whole per-frame exchange sequence above (frame broadcast, halo planes,
    plane counts, halo steppable lists, boundary triples, cluster members,

@@ -10,6 +10,7 @@ namespace vp {
 // One symmetric 3x3 per thread: a row-major (9 per matrix), eigenvalues
 // ascending (3), eigenvectors column-major (9: column k pairs with value k).
 __global__ void k_jacobi_batch(uint64_t n, const double* a, double* vals, double* vecs) {
+  VP_GRID_WAIT();
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     double in[3][3];
@@ -31,6 +32,7 @@ __global__ void k_jacobi_batch(uint64_t n, const double* a, double* vals, double
 // hull_filter keep test (polygonize.cpp:96-107) as flags in input order: a
 // point survives unless strictly inside the inner polygon of its fit.
 __global__ void k_poly_keep_flags(Counters* ctr, SegBufs b, uint8_t* flags) {
+  VP_GRID_WAIT();
   const uint32_t F = ctr->nfits;
   const P2* proj = reinterpret_cast<const P2*>(b.proj);
   for (uint32_t f = 0; f < F; ++f) {
@@ -51,6 +53,7 @@ __global__ void k_poly_keep_flags(Counters* ctr, SegBufs b, uint8_t* flags) {
 // Ordered compaction of flagged 2-D points (positions from a flag scan).
 __global__ void k_gather_p2(const uint32_t* n_ptr, const uint8_t* flags, const uint32_t* pos, const double* proj,
                             double* out) {
+  VP_GRID_WAIT();
   const uint32_t n = *n_ptr;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     if (flags[i]) {
@@ -60,6 +63,7 @@ __global__ void k_gather_p2(const uint32_t* n_ptr, const uint8_t* flags, const u
 }
 
 __global__ void k_iota(int32_t* a, uint64_t n) {
+  VP_GRID_WAIT();
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
     a[i] = static_cast<int32_t>(i);
@@ -69,6 +73,7 @@ __global__ void k_iota(int32_t* a, uint64_t n) {
 // (CSR): every listed edge is a union; the fixed point is the component
 // minimum, the reference's canonical label.
 __global__ void k_label_edges(uint64_t n, const uint64_t* rows, const int32_t* cols, int32_t* parent) {
+  VP_GRID_WAIT();
   const unsigned lane = lane_id();
   const uint64_t warp = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
   const uint64_t nwarp = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -81,6 +86,7 @@ __global__ void k_label_edges(uint64_t n, const uint64_t* rows, const int32_t* c
 }
 
 __global__ void k_label_flatten(uint64_t n, int32_t* parent, int32_t* label) {
+  VP_GRID_WAIT();
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
     label[i] = uf_find(parent, static_cast<int>(i));
@@ -91,6 +97,7 @@ __global__ void k_label_flatten(uint64_t n, int32_t* parent, int32_t* label) {
 // max_angle_deg (inclusive); status 2 (Steppable) or 1 (Occupied) per voxel.
 __global__ void k_classify_estimates(uint64_t n, const int32_t* ncount, const double* angle, const uint8_t* valid,
                                      int min_neighbors, double max_angle, uint8_t* status) {
+  VP_GRID_WAIT();
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
     status[i] = (valid[i] && ncount[i] >= min_neighbors && angle[i] <= max_angle) ? 2 : 1;

@@ -28,6 +28,7 @@ __device__ __forceinline__ bool hm_cell(const HmDesc& m, double px, double py, u
 
 // hm_integrate pass 1: the last point of every cell (heightmap.cpp:26-38)
 __global__ void k_hm_win(HmDesc m, const FrameParams* __restrict__ fp) {
+  VP_GRID_WAIT();
   const uint64_t n = fp->n;
   for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
@@ -42,6 +43,7 @@ __global__ void k_hm_win(HmDesc m, const FrameParams* __restrict__ fp) {
 
 // pass 2: the winner writes its height; the cell becomes valid
 __global__ void k_hm_write(HmDesc m, const FrameParams* __restrict__ fp) {
+  VP_GRID_WAIT();
   const uint64_t n = fp->n;
   for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
@@ -63,6 +65,7 @@ __device__ __forceinline__ bool hm_edge(const HmDesc& m, uint32_t a, uint32_t b,
 }
 
 __global__ void k_hm_ccl_init(HmDesc m) {
+  VP_GRID_WAIT();
   const uint32_t nc = static_cast<uint32_t>(m.ex) * static_cast<uint32_t>(m.ey);
   for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += gridDim.x * blockDim.x) {
     m.parent[c] = static_cast<int32_t>(c);
@@ -73,6 +76,7 @@ __global__ void k_hm_ccl_init(HmDesc m) {
 
 // unions along +x and +y (the 4-neighbour graph is symmetric)
 __global__ void k_hm_ccl_union(HmDesc m, double dth) {
+  VP_GRID_WAIT();
   const uint32_t nc = static_cast<uint32_t>(m.ex) * static_cast<uint32_t>(m.ey);
   for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += gridDim.x * blockDim.x) {
     if (!m.valid[c]) continue;
@@ -88,6 +92,7 @@ __global__ void k_hm_ccl_union(HmDesc m, double dth) {
 // parallel "parent[c] = find(c)" is not a flatten: another thread's pointer
 // jumping may store an intermediate ancestor over it afterwards)
 __global__ void k_hm_seed_flags(HmDesc m, uint8_t* flags) {
+  VP_GRID_WAIT();
   const uint32_t nc = static_cast<uint32_t>(m.ex) * static_cast<uint32_t>(m.ey);
   for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += gridDim.x * blockDim.x) {
     const int r = uf_find(m.parent, static_cast<int>(c));
@@ -97,6 +102,7 @@ __global__ void k_hm_seed_flags(HmDesc m, uint8_t* flags) {
 }
 
 __global__ void k_hm_seed_emit(HmDesc m, const uint8_t* flags, const uint32_t* pos, uint32_t* visit) {
+  VP_GRID_WAIT();
   const uint32_t nc = static_cast<uint32_t>(m.ex) * static_cast<uint32_t>(m.ey);
   for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += gridDim.x * blockDim.x) {
     if (!flags[c]) continue;
@@ -131,6 +137,7 @@ __device__ __forceinline__ bool hm_step(const HmDesc& m, uint32_t c, int s, uint
 // then emits the claimed pairs in that order -- k_hm_claim / k_hm_claimed /
 // k_hm_emit, chained by __syncthreads. dn[1] = seeds in, dn[2] = cells visited out.
 __global__ void __launch_bounds__(1024) k_hm_bfs(HmDesc m, uint32_t* visit, uint32_t* dn, double dth) {
+  VP_GRID_WAIT();
   __shared__ uint32_t s_base;
   const uint32_t tid = threadIdx.x;
   uint32_t ls = 0, nf = dn[1];
@@ -176,6 +183,7 @@ __global__ void __launch_bounds__(1024) k_hm_bfs(HmDesc m, uint32_t* visit, uint
 // (cell centre x, y, height) (heightmap.cpp:61-63), label = visit position of
 // the region's seed, counted per region.
 __global__ void k_hm_members(HmDesc m, const uint32_t* visit, uint32_t nv, SegBufs b) {
+  VP_GRID_WAIT();
   for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < nv; e += gridDim.x * blockDim.x) {
     const uint32_t c = visit[e];
     const uint32_t x = c / static_cast<uint32_t>(m.ey), y = c - x * static_cast<uint32_t>(m.ey);
@@ -190,11 +198,13 @@ __global__ void k_hm_members(HmDesc m, const uint32_t* visit, uint32_t nv, SegBu
 }
 
 __global__ void k_hm_zero_cnt(uint32_t nv, SegBufs b) {
+  VP_GRID_WAIT();
   for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < nv; e += gridDim.x * blockDim.x) b.cnt[e] = 0;
 }
 
 // cluster labels: the seed's flat index (heightmap.cpp:49)
 __global__ void k_hm_klabel(const Counters* ctr, SegBufs b, const uint32_t* visit) {
+  VP_GRID_WAIT();
   const uint32_t K = min(ctr->K, static_cast<uint32_t>(kClusterBins));
   for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < K; k += gridDim.x * blockDim.x)
     b.klabel[k] = static_cast<int32_t>(visit[b.klabel[k]]);

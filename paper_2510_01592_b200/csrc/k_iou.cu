@@ -47,6 +47,7 @@ __device__ __forceinline__ bool in_convex(const double2* ring, uint32_t n, doubl
 // plane_iou raster loop (metrics.cpp:83-95): one block per pair
 __global__ void k_iou_raster(const PairJob* __restrict__ jobs, const double2* __restrict__ rings,
                              unsigned long long* counts) {
+  VP_GRID_WAIT();
   const PairJob j = jobs[blockIdx.x];
   const double2* rd = rings + j.ring_d;
   const double2* rt = rings + j.ring_t;

@@ -44,6 +44,7 @@ __device__ __forceinline__ int point_key(const GridDesc& g, const FrameParams* f
 __global__ void k_integrate_hash(GridDesc g, const FrameParams* __restrict__ fp, Counters* ctr,
                                  uint32_t* hkey, uint32_t* hcnt, uint32_t hmask, uint32_t* groups,
                                  uint32_t* pslot, uint32_t* prank) {
+  VP_GRID_WAIT();
   const uint64_t n = fp->n;
   unsigned long long disc = 0;
   const unsigned lane = lane_id();
@@ -127,6 +128,7 @@ __global__ void k_integrate_hash(GridDesc g, const FrameParams* __restrict__ fp,
 constexpr uint32_t kBigGroup = 0x80000000u;
 __global__ void k_integrate_offsets(Counters* ctr, uint32_t* groups, const uint32_t* hcnt,
                                     uint32_t* hoff, uint32_t* medium, uint32_t* dense) {
+  VP_GRID_WAIT();
   const uint32_t ng = ctr->ngroups;
   const unsigned lane = lane_id();
   for (uint32_t i0 = blockIdx.x * blockDim.x; i0 < ng; i0 += gridDim.x * blockDim.x) {
@@ -158,6 +160,7 @@ __global__ void k_integrate_offsets(Counters* ctr, uint32_t* groups, const uint3
 
 __global__ void k_integrate_scatter(const FrameParams* __restrict__ fp, const uint32_t* pslot,
                                     const uint32_t* prank, const uint32_t* hoff, uint32_t* sorted) {
+  VP_GRID_WAIT();
   const uint64_t n = fp->n;
   for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
@@ -199,6 +202,7 @@ __global__ void __launch_bounds__(256) k_integrate_fold(GridDesc g, const FrameP
                                                         Counters* ctr, const uint32_t* groups,
                                                         uint32_t* hkey, uint32_t* hcnt,
                                                         const uint32_t* hoff, uint32_t* sorted) {
+  VP_GRID_WAIT();
   const uint32_t ng = ctr->ngroups;
   unsigned long long fresh = 0;
   for (uint32_t gi = blockIdx.x * blockDim.x + threadIdx.x; gi < ng; gi += gridDim.x * blockDim.x) {
@@ -259,6 +263,7 @@ __global__ void __launch_bounds__(256) k_integrate_fold_medium(GridDesc g, const
                                                                Counters* ctr, uint32_t* hkey, uint32_t* hcnt,
                                                                const uint32_t* hoff, const uint32_t* sorted,
                                                                const uint32_t* medium) {
+  VP_GRID_WAIT();
   __shared__ uint32_t raw[kFoldWarps][kFoldMax];
   __shared__ uint32_t srt[kFoldMax * kFoldWarps];
   __shared__ d3 sw[kFoldWarps][kFoldMax];
@@ -307,6 +312,7 @@ __global__ void __launch_bounds__(1024) k_integrate_fold_dense(GridDesc g, const
                                                                Counters* ctr, uint32_t* hkey, uint32_t* hcnt,
                                                                const uint32_t* hoff, const uint32_t* sorted,
                                                                const uint32_t* pslot, const uint32_t* dense) {
+  VP_GRID_WAIT();
   extern __shared__ __align__(16) unsigned char smem[];
   d3* w = reinterpret_cast<d3*>(smem);                          // 1024 transformed points
   uint32_t* keys = reinterpret_cast<uint32_t*>(smem + 1024 * sizeof(d3));  // kDenseSort indices
@@ -443,6 +449,7 @@ __global__ void __launch_bounds__(1024) k_integrate_fold_dense(GridDesc g, const
 // every count is taken afterwards from the bitmap, so the walk order does
 // not change any result.
 __global__ void k_dda_keys(GridDesc g, const FrameParams* __restrict__ fp, DdaBins* db, uint8_t* bin_of) {
+  VP_GRID_WAIT();
   // a coherent stream is re-evaluated every 8th frame only (the decision
   // changes the walk order, never a result)
   if (!db->use && (db->frame & 7u)) return;
@@ -483,6 +490,7 @@ __global__ void k_dda_keys(GridDesc g, const FrameParams* __restrict__ fp, DdaBi
 
 // One warp: decide, and lay the bins out longest first; resets the counts.
 __global__ void k_dda_plan(DdaBins* db) {
+  VP_GRID_WAIT();
   const unsigned lane = lane_id();
   const bool measured = db->warp_max != 0;  // k_dda_keys ran this frame
   const int use = measured ? (db->steps * 4 < db->warp_max * 3 ? 1 : 0) : db->use;  // lane efficiency < 75 %
@@ -511,6 +519,7 @@ __global__ void k_dda_plan(DdaBins* db) {
 
 __global__ void k_dda_scatter(const FrameParams* __restrict__ fp, DdaBins* db, const uint8_t* __restrict__ bin_of,
                               uint32_t* perm) {
+  VP_GRID_WAIT();
   if (!db->use) return;
   const uint64_t n = fp->n;
   for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
@@ -965,6 +974,7 @@ __device__ __forceinline__ void clear_walk_bricks(const GridDesc& g, const Frame
 __global__ void __launch_bounds__(256, VP_DDA_MINB) k_clear_walk(GridDesc g, const FrameParams* __restrict__ fp,
                                                                   const uint32_t* perm, const DdaBins* db,
                                                                   int generic) {
+  VP_GRID_WAIT();
   if (!generic) {
     if (db->use) clear_walk_bricks<false>(g, fp, perm); else clear_walk_coherent(g, fp);
     return;
@@ -973,6 +983,7 @@ __global__ void __launch_bounds__(256, VP_DDA_MINB) k_clear_walk(GridDesc g, con
 }
 __global__ void __launch_bounds__(256, 4) k_clear_walk_slab(GridDesc g, const FrameParams* __restrict__ fp,
                                                             const uint32_t* perm, const DdaBins* db) {
+  VP_GRID_WAIT();
   if (db->use) clear_walk_bricks<true>(g, fp, perm); else clear_walk_body<true>(g, fp, perm, db);
 }
 
@@ -1115,6 +1126,7 @@ __device__ __forceinline__ void clear_apply_bricks(const GridDesc& g, const Fram
 // One launch for either mask layout (k_dda_plan's decision for this frame).
 __global__ void k_clear_apply(GridDesc g, const FrameParams* __restrict__ fp, Counters* ctr, const DdaBins* db,
                               int use_box) {
+  VP_GRID_WAIT();
   if (db->use) clear_apply_bricks(g, fp, ctr, use_box); else clear_apply_rows(g, fp, ctr, use_box);
 }
 
@@ -1130,6 +1142,7 @@ __global__ void k_clear_apply(GridDesc g, const FrameParams* __restrict__ fp, Co
 // Rows that neither leave nor shift in z are not read at all.
 // ---------------------------------------------------------------------------
 __global__ void k_recenter(GridDesc g, const FrameParams* __restrict__ fp, Counters* ctr) {
+  VP_GRID_WAIT();
   if (!fp->do_shift) return;
   uint32_t* occ = fp->occ_pre;
   const int sx = fp->shift[0], sy = fp->shift[1], sz = fp->shift[2];
@@ -1187,6 +1200,7 @@ __global__ void k_recenter(GridDesc g, const FrameParams* __restrict__ fp, Count
 // VoxelGrid::merge_point (voxel_grid.cpp:49-57), one point, window index.
 __global__ void k_merge_point(GridDesc g, const FrameParams* __restrict__ fp, Counters* ctr, int x,
                               int y, int z, double px, double py, double pz) {
+  VP_GRID_WAIT();
   Cell* c = g.cells + phys_index(g, fp->off_pre, x, y, z);
   if (c->count == 0) {
     ctr->newly += 1;
@@ -1202,6 +1216,7 @@ __global__ void k_merge_point(GridDesc g, const FrameParams* __restrict__ fp, Co
 // Batch VoxelGrid::set_status (window indices, current toroidal offsets).
 __global__ void k_set_statuses(GridDesc g, const FrameParams* __restrict__ fp, const int32_t* idx,
                                const uint8_t* st, uint64_t n) {
+  VP_GRID_WAIT();
   for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const int x = idx[3 * i], y = idx[3 * i + 1], z = idx[3 * i + 2];
@@ -1210,6 +1225,7 @@ __global__ void k_set_statuses(GridDesc g, const FrameParams* __restrict__ fp, c
 }
 
 __global__ void k_map_finalize(Counters* ctr, unsigned long long* occ_total) {
+  VP_GRID_WAIT();
   const unsigned long long o = *occ_total + ctr->newly - ctr->freed - ctr->dropped;
   *occ_total = o;
   ctr->occupied = o;
@@ -1218,6 +1234,7 @@ __global__ void k_map_finalize(Counters* ctr, unsigned long long* occ_total) {
 
 // Per-frame counter reset (one slot); occupied carries VoxelGrid::occupied_.
 __global__ void k_frame_begin(Counters* ctr, const unsigned long long* occ_total) {
+  VP_GRID_WAIT();
   uint32_t* w = reinterpret_cast<uint32_t*>(ctr);
   for (uint32_t i = threadIdx.x; i < sizeof(Counters) / 4; i += blockDim.x) w[i] = 0u;
   __syncwarp();
@@ -1263,6 +1280,7 @@ __device__ __forceinline__ uint64_t ring_row_of(const GridDesc& g, const FramePa
 
 __global__ void __launch_bounds__(kScanThreads) k_bitmap_count(GridDesc g, const FrameParams* __restrict__ fp,
                                                                uint64_t r_lo, uint64_t nrows, uint32_t* bsum) {
+  VP_GRID_WAIT();
   const uint64_t r0 = static_cast<uint64_t>(blockIdx.x) * kRowsPerBlock + static_cast<uint64_t>(threadIdx.x) * kRowItems;
   uint32_t c = 0;
 #pragma unroll
@@ -1278,6 +1296,7 @@ __global__ void __launch_bounds__(kScanThreads) k_bitmap_count(GridDesc g, const
 __global__ void __launch_bounds__(kScanThreads) k_bitmap_emit(GridDesc g, const FrameParams* __restrict__ fp,
                                                               uint64_t r_lo, uint64_t nrows, const uint32_t* boff,
                                                               uint32_t* out, uint32_t cap) {
+  VP_GRID_WAIT();
   const int W = g.W, ez = g.ez, zb = fp->zb_post, Wz = g.W << 5;
   const int s0 = zb >> 5, sh = zb & 31;
   const uint64_t r0 = static_cast<uint64_t>(blockIdx.x) * kRowsPerBlock + static_cast<uint64_t>(threadIdx.x) * kRowItems;
@@ -1321,6 +1340,7 @@ __global__ void __launch_bounds__(kScanThreads) k_bitmap_emit(GridDesc g, const 
 // Generic ordered compaction of u8 flags: positions[i] = exclusive rank.
 __global__ void k_flags_count(const uint8_t* __restrict__ flags, const uint32_t* n_ptr, uint32_t cap,
                               uint32_t* bsum) {
+  VP_GRID_WAIT();
   const uint32_t n = min(*n_ptr, cap);
   const uint64_t i0 = (static_cast<uint64_t>(blockIdx.x) * kScanThreads + threadIdx.x) * kScanItems;
   uint32_t c = 0;
@@ -1333,6 +1353,7 @@ __global__ void k_flags_count(const uint8_t* __restrict__ flags, const uint32_t*
 
 __global__ void k_flags_positions(const uint8_t* __restrict__ flags, const uint32_t* n_ptr,
                                   uint32_t cap, const uint32_t* boff, uint32_t* pos_out) {
+  VP_GRID_WAIT();
   const uint32_t n = min(*n_ptr, cap);
   const uint64_t i0 = (static_cast<uint64_t>(blockIdx.x) * kScanThreads + threadIdx.x) * kScanItems;
   uint8_t f[kScanItems];
@@ -1389,11 +1410,13 @@ __device__ __forceinline__ void block_scan_array(uint32_t* a, uint32_t n, uint32
 // n is read from n_ptr when non-null.
 __global__ void k_scan_exclusive(uint32_t* a, uint32_t n_static, const uint32_t* n_ptr,
                                  uint32_t* total, uint32_t* total2) {
+  VP_GRID_WAIT();
   block_scan_array(a, n_ptr ? *n_ptr : n_static, total, total2);
 }
 
 // Tile sums of a list of min(*n_ptr, cap) items in tiles of `per`.
 __global__ void k_scan_tiles(uint32_t* a, const uint32_t* n_ptr, uint32_t cap, uint32_t per, uint32_t* total) {
+  VP_GRID_WAIT();
   block_scan_array(a, (min(*n_ptr, cap) + per - 1) / per, total, nullptr);
 }
 

@@ -86,6 +86,7 @@ __device__ __forceinline__ double rng_uniform(CounterRng& r) {
 }
 
 __global__ void k_render_rays(RenderDesc s, float* hits, uint8_t* flag) {
+  VP_GRID_WAIT();
   for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < s.rays;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     d3 ds;
@@ -127,6 +128,7 @@ __global__ void k_render_rays(RenderDesc s, float* hits, uint8_t* flag) {
 
 __global__ void k_render_compact(uint64_t rays, const float* __restrict__ hits, const uint8_t* __restrict__ flag,
                                  const uint32_t* __restrict__ pos, float* out) {
+  VP_GRID_WAIT();
   for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < rays;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     if (!flag[i]) continue;

@@ -17,6 +17,7 @@ namespace vp {
 // steppable count to tsum (the steppable compaction's block sums).
 __global__ void k_normals(GridDesc g, const FrameParams* __restrict__ fp, Counters* ctr, SegDev sp,
                           SegBufs b, int write_status, uint32_t* tsum) {
+  VP_GRID_WAIT();
   if (blockIdx.x == 0 && threadIdx.x == 0 && ctr->V > b.Vcap) atomicOr(&ctr->overflow, kOverflowOcc);
   const uint32_t V = min(ctr->V, b.Vcap);
   const uint32_t* occ = fp->occ_post;
@@ -152,6 +153,7 @@ __global__ void k_normals(GridDesc g, const FrameParams* __restrict__ fp, Counte
 // ordinal map used by the CCL window search. Same tiles as k_normals: a
 // voxel's ordinal = its tile's offset (scanned tsum) + its rank in the tile.
 __global__ void k_step_emit(GridDesc g, Counters* ctr, SegBufs b, MapDesc m, int xadd, const uint32_t* toff) {
+  VP_GRID_WAIT();
   const uint32_t V = min(ctr->V, b.Vcap);
   for (uint32_t t0 = blockIdx.x * blockDim.x; t0 < V; t0 += gridDim.x * blockDim.x) {
     const uint32_t v = t0 + threadIdx.x;
@@ -185,6 +187,7 @@ __global__ void k_step_emit(GridDesc g, Counters* ctr, SegBufs b, MapDesc m, int
 
 // Host-provided steppable list (vp_label_components): fill the map only.
 __global__ void k_map_fill(Counters* ctr, SegBufs b, MapDesc m) {
+  VP_GRID_WAIT();
   const uint32_t S = min(ctr->S, b.Scap);
   for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < S; s += gridDim.x * blockDim.x) {
     const int x = b.st_idx[3 * s], y = b.st_idx[3 * s + 1], z = b.st_idx[3 * s + 2];
@@ -194,6 +197,7 @@ __global__ void k_map_fill(Counters* ctr, SegBufs b, MapDesc m) {
 }
 
 __global__ void k_ccl_init(Counters* ctr, SegBufs b) {
+  VP_GRID_WAIT();
   const uint32_t S = min(ctr->S, b.Scap);
   for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < S; s += gridDim.x * blockDim.x) {
     b.parent[s] = static_cast<int32_t>(s);
@@ -245,6 +249,7 @@ __device__ __forceinline__ bool window_row(int r, int w, int span, bool backward
 // One warp per voxel; the steppable bitmap turns each window row into one
 // word load, and only present voxels are probed.
 __global__ void __launch_bounds__(256) k_ccl_hook(Counters* ctr, SegDev sp, SegBufs b, MapDesc m) {
+  VP_GRID_WAIT();
   const uint32_t S = min(ctr->S, b.Scap);
   const int w = sp.w, span = 2 * w + 1;
   const int nrows = (w + 1) + w * span;
@@ -296,6 +301,7 @@ __global__ void __launch_bounds__(256) k_ccl_hook(Counters* ctr, SegDev sp, SegB
 // SMs in k_ccl_hook are visible; no node changes its own value concurrently
 // except through jumps to an ancestor, which keeps the result a root).
 __global__ void k_ccl_compress(Counters* ctr, SegBufs b) {
+  VP_GRID_WAIT();
   const uint32_t S = min(ctr->S, b.Scap);
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < S; i += gridDim.x * blockDim.x)
     __stcg(b.parent + i, uf_find(b.parent, static_cast<int>(i)));
@@ -305,6 +311,7 @@ __global__ void k_ccl_compress(Counters* ctr, SegBufs b) {
 // two rounds before k_ccl_compress cut the hook chains (C2: up to ~31 deep)
 // by 4x, so compression is no longer one thread's long serial chain.
 __global__ void k_ccl_jump(Counters* ctr, SegBufs b) {
+  VP_GRID_WAIT();
   const uint32_t S = min(ctr->S, b.Scap);
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < S; i += gridDim.x * blockDim.x) {
     const int p = __ldcg(b.parent + i);
@@ -317,6 +324,7 @@ __global__ void k_ccl_jump(Counters* ctr, SegBufs b) {
 // is checked against i's cached root before the 48-byte predicate loads, so
 // edges inside an already-joined tree cost one load.
 __global__ void __launch_bounds__(256) k_ccl_union(Counters* ctr, SegDev sp, SegBufs b, MapDesc m) {
+  VP_GRID_WAIT();
   const uint32_t S = min(ctr->S, b.Scap);
   const int w = sp.w, span = 2 * w + 1;
   const int nrows = (w + 1) + w * span;
@@ -419,6 +427,7 @@ __device__ __forceinline__ uint32_t ccl_row_bits(const MapDesc& m, int w, int sp
 // the window first), their candidates tested 32 at a time; the first adjacent
 // candidate is the minimum.
 __global__ void __launch_bounds__(256) k_ccl_hook_bal(Counters* ctr, SegDev sp, SegBufs b, MapDesc m) {
+  VP_GRID_WAIT();
   __shared__ int32_t cand[kCclWarps][kCclEdgeBuf];
   const uint32_t S = min(ctr->S, b.Scap);
   const int w = sp.w, span = 2 * w + 1;
@@ -529,6 +538,7 @@ __device__ __forceinline__ void ccl_union_bal_body(Counters* ctr, const SegDev& 
 }
 
 __global__ void __launch_bounds__(256) k_ccl_union_bal(Counters* ctr, SegDev sp, SegBufs b, MapDesc m) {
+  VP_GRID_WAIT();
   ccl_union_bal_body(ctr, sp, b, m);
 }
 
@@ -551,6 +561,7 @@ __global__ void __launch_bounds__(256) k_ccl_union_bal(Counters* ctr, SegDev sp,
 // path-halving find of k_ccl_compress can leave a node at a non-root ancestor
 // when two threads rewrite it).
 __global__ void k_ccl_compress_exact(Counters* ctr, SegBufs b) {
+  VP_GRID_WAIT();
   const uint32_t S = min(ctr->S, b.Scap);
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < S; i += gridDim.x * blockDim.x) {
     int r = __ldcg(b.parent + i);
@@ -586,6 +597,7 @@ __device__ __forceinline__ void pair_insert(Counters* ctr, const SegBufs& b, int
 }
 
 __global__ void __launch_bounds__(256) k_ccl_pairs(Counters* ctr, SegDev sp, SegBufs b, MapDesc m) {
+  VP_GRID_WAIT();
   __shared__ int32_t cand[kCclWarps][kCclEdgeBuf];
   const uint32_t S = min(ctr->S, b.Scap);
   const int w = sp.w, span = 2 * w + 1;
@@ -636,6 +648,7 @@ __global__ void __launch_bounds__(256) k_ccl_pairs(Counters* ctr, SegDev sp, Seg
 
 // One block: union of the listed root pairs, then the table is emptied.
 __global__ void __launch_bounds__(1024) k_ccl_pairs_union(Counters* ctr, SegBufs b) {
+  VP_GRID_WAIT();
   const uint32_t n = min(ctr->npairs, b.pair_cap >> 1);
   for (uint32_t t = threadIdx.x; t < n; t += blockDim.x) {
     const unsigned long long key = __ldcg(b.pair_key + b.pair_slot[t]);
@@ -651,6 +664,7 @@ __global__ void __launch_bounds__(1024) k_ccl_pairs_union(Counters* ctr, SegBufs
 
 // The full union (k_ccl_union_bal) when the pair table overflowed, else nothing.
 __global__ void __launch_bounds__(256) k_ccl_union_gated(Counters* ctr, SegDev sp, SegBufs b, MapDesc m) {
+  VP_GRID_WAIT();
   if (!ctr->pair_ovf) return;
   ccl_union_bal_body(ctr, sp, b, m);
 }
@@ -672,6 +686,7 @@ __global__ void __launch_bounds__(256) k_ccl_union_gated(Counters* ctr, SegDev s
 // of its set: labels stay canonical and bit-exact.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_ccl_lattice(Counters* ctr, SegDev sp, SegBufs b, MapDesc m) {
+  VP_GRID_WAIT();
   const uint32_t S = min(ctr->S, b.Scap);
   int32_t* parent = b.parent;
   const int xmax = m.lo[0] + m.dims[0] - 1, ymax = m.lo[1] + m.dims[1] - 1;
@@ -709,6 +724,7 @@ __global__ void __launch_bounds__(256) k_ccl_lattice(Counters* ctr, SegDev sp, S
 // Single block: the most frequent root among up to 1024 evenly spaced voxels
 // (ties to the smaller root) -> ctr->ccl_giant (-1 if there are no voxels).
 __global__ void __launch_bounds__(1024) k_ccl_giant(Counters* ctr, SegBufs b) {
+  VP_GRID_WAIT();
   __shared__ int32_t v[1024];
   __shared__ unsigned long long best;
   const uint32_t S = min(ctr->S, b.Scap);
@@ -748,6 +764,7 @@ __global__ void __launch_bounds__(1024) k_ccl_giant(Counters* ctr, SegBufs b) {
 // Whole-window unions of every voxel outside the giant component (one warp
 // per voxel, one window row per lane).
 __global__ void __launch_bounds__(256) k_ccl_full(Counters* ctr, SegDev sp, SegBufs b, MapDesc m) {
+  VP_GRID_WAIT();
   const uint32_t S = min(ctr->S, b.Scap);
   const int w = sp.w, span = 2 * w + 1;
   const int nrows = span * span;
@@ -800,6 +817,7 @@ __global__ void __launch_bounds__(256) k_ccl_full(Counters* ctr, SegDev sp, SegB
 // pass 1 (cols == nullptr) counts, pass 2 fills rows in ascending ordinal order.
 __global__ void k_adjacency(Counters* ctr, SegDev sp, SegBufs b, MapDesc m, const uint64_t* rows,
                             uint32_t* counts, int32_t* cols) {
+  VP_GRID_WAIT();
   const uint32_t S = min(ctr->S, b.Scap);
   const int w = sp.w;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < S; i += gridDim.x * blockDim.x) {
@@ -827,6 +845,7 @@ __global__ void k_adjacency(Counters* ctr, SegDev sp, SegBufs b, MapDesc m, cons
 // OccupiedVoxel materialisation (voxel_grid.cpp:254-263) for the API.
 __global__ void k_occ_gather(GridDesc g, const FrameParams* __restrict__ fp, Counters* ctr,
                              SegBufs b) {
+  VP_GRID_WAIT();
   const uint32_t V = min(ctr->V, b.Vcap);
   for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x) {
     const uint32_t flat = b.occ_list[v];
@@ -847,6 +866,7 @@ __global__ void k_occ_gather(GridDesc g, const FrameParams* __restrict__ fp, Cou
 
 // Final labels (component minimum), member counts per root, map reset.
 __global__ void k_ccl_flatten(Counters* ctr, SegBufs b, MapDesc m) {
+  VP_GRID_WAIT();
   const uint32_t S = min(ctr->S, b.Scap);
   int32_t* parent = b.parent;
   if (blockIdx.x == 0 && threadIdx.x == 0) {  // pair set consumed (k_ccl_pairs_union / _gated ran before)
@@ -865,6 +885,7 @@ __global__ void k_ccl_flatten(Counters* ctr, SegBufs b, MapDesc m) {
 
 // filter_clusters (segmentation.cpp:196-201): roots with >= min_cluster members.
 __global__ void k_cluster_flags(Counters* ctr, SegDev sp, SegBufs b) {
+  VP_GRID_WAIT();
   const uint32_t S = min(ctr->S, b.Scap);
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < S; i += gridDim.x * blockDim.x)
     b.big_flag[i] = (b.label[i] == static_cast<int32_t>(i) && b.cnt[i] > 0u &&
@@ -874,6 +895,7 @@ __global__ void k_cluster_flags(Counters* ctr, SegDev sp, SegBufs b) {
 }
 
 __global__ void k_cluster_assign(Counters* ctr, SegBufs b) {
+  VP_GRID_WAIT();
   const uint32_t S = min(ctr->S, b.Scap);
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < S; i += gridDim.x * blockDim.x) {
     if (!b.big_flag[i]) continue;
@@ -887,6 +909,7 @@ __global__ void k_cluster_assign(Counters* ctr, SegBufs b) {
 
 // Single block: sizes and warp-padded member offsets of the K clusters.
 __global__ void k_cluster_setup(Counters* ctr, SegBufs b) {
+  VP_GRID_WAIT();
   __shared__ uint32_t carry;
   if (threadIdx.x == 0) {
     carry = 0;
@@ -920,6 +943,7 @@ __global__ void k_cluster_setup(Counters* ctr, SegBufs b) {
 // ordinal inside each cluster = segmentation.cpp:182-193 grouping order).
 // One warp per chunk of kChunk ordinals.
 __global__ void k_member_hist(Counters* ctr, SegBufs b, uint32_t hstride) {
+  VP_GRID_WAIT();
   __shared__ uint32_t hist[kClusterBins];
   const uint32_t S = min(ctr->S, b.Scap);
   const uint32_t K = min(ctr->K, static_cast<uint32_t>(kClusterBins));
@@ -939,6 +963,7 @@ __global__ void k_member_hist(Counters* ctr, SegBufs b, uint32_t hstride) {
 }
 
 __global__ void k_member_hscan(Counters* ctr, SegBufs b, uint32_t hstride) {
+  VP_GRID_WAIT();
   const uint32_t S = min(ctr->S, b.Scap);
   const uint32_t K = min(ctr->K, static_cast<uint32_t>(kClusterBins));
   const uint32_t nch = (S + kChunk - 1) / kChunk;
@@ -963,6 +988,7 @@ __global__ void k_member_hscan(Counters* ctr, SegBufs b, uint32_t hstride) {
 }
 
 __global__ void k_member_scatter(Counters* ctr, SegBufs b, uint32_t hstride) {
+  VP_GRID_WAIT();
   __shared__ uint32_t run[kClusterBins];
   const uint32_t S = min(ctr->S, b.Scap);
   const uint32_t K = min(ctr->K, static_cast<uint32_t>(kClusterBins));
@@ -1003,6 +1029,7 @@ __global__ void k_member_scatter(Counters* ctr, SegBufs b, uint32_t hstride) {
 //     ordered inlier extraction (block scan) in member order.
 // ---------------------------------------------------------------------------
 __global__ void k_ransac_hyp(Counters* ctr, RansacDev rp, SegBufs b) {
+  VP_GRID_WAIT();
   const uint32_t K = min(ctr->K, static_cast<uint32_t>(kClusterBins));
   const uint32_t I = static_cast<uint32_t>(rp.iterations);
   const uint64_t total = static_cast<uint64_t>(K) * I;
@@ -1037,6 +1064,7 @@ __global__ void k_ransac_hyp(Counters* ctr, RansacDev rp, SegBufs b) {
 }
 
 __global__ void k_ransac_count(Counters* ctr, RansacDev rp, SegBufs b) {
+  VP_GRID_WAIT();
   const uint32_t K = min(ctr->K, static_cast<uint32_t>(kClusterBins));
   if (K == 0 || (ctr->overflow & kOverflowMembers)) return;
   const uint32_t nseg = b.kpoff[K] >> 5;
@@ -1093,6 +1121,7 @@ __global__ void k_ransac_count(Counters* ctr, RansacDev rp, SegBufs b) {
 }
 
 __global__ void k_ransac_select(Counters* ctr, RansacDev rp, SegBufs b) {
+  VP_GRID_WAIT();
   const uint32_t K = min(ctr->K, static_cast<uint32_t>(kClusterBins));
   const int I = rp.iterations;
   const unsigned lane = lane_id();
@@ -1133,6 +1162,7 @@ __global__ void k_ransac_select(Counters* ctr, RansacDev rp, SegBufs b) {
 
 // Single block: fit list in cluster order, inlier offsets, FitStats.
 __global__ void k_fit_setup(Counters* ctr, RansacDev rp, SegBufs b) {
+  VP_GRID_WAIT();
   __shared__ uint32_t carry_f, carry_i, n_skip, n_unfit;
   if (threadIdx.x == 0) carry_f = carry_i = n_skip = n_unfit = 0;
   __syncthreads();
@@ -1200,6 +1230,7 @@ __device__ __forceinline__ uint32_t fit_of_chunk(const SegBufs& b, uint32_t F, u
 }
 
 __global__ void k_extract_count(Counters* ctr, RansacDev rp, SegBufs b) {
+  VP_GRID_WAIT();
   if (ctr->overflow & (kOverflowFits | kOverflowMembers)) return;
   const uint32_t F = ctr->nfits, nch = ctr->fit_chunks;
   for (uint32_t c = blockIdx.x; c < nch; c += gridDim.x) {
@@ -1218,6 +1249,7 @@ __global__ void k_extract_count(Counters* ctr, RansacDev rp, SegBufs b) {
 }
 
 __global__ void k_extract_emit(Counters* ctr, RansacDev rp, SegBufs b) {
+  VP_GRID_WAIT();
   if (ctr->overflow & (kOverflowFits | kOverflowMembers)) return;
   __shared__ uint32_t run;
   const uint32_t F = ctr->nfits, nch = ctr->fit_chunks;
@@ -1276,6 +1308,7 @@ __device__ void refine_finish(double cov[3][3], d3 cen, const double* init, d3 u
 // refine_plane with the reference's sequential sums (refine_exact): one
 // thread per fit, bit-identical to plane_fit.cpp:136-143.
 __global__ void k_refine(Counters* ctr, SegBufs b, d3 up, int refine, int exact) {
+  VP_GRID_WAIT();
   const uint32_t F = ctr->nfits;
   if (ctr->overflow & (kOverflowFits | kOverflowMembers)) return;
   for (uint32_t f = blockIdx.x; f < F; f += gridDim.x) {
@@ -1323,6 +1356,7 @@ constexpr uint32_t kRefChunk = 4096;
 
 // Single block: per fit chunk offsets (fits that are not refined get none).
 __global__ void k_refine_setup(Counters* ctr, SegBufs b, int refine) {
+  VP_GRID_WAIT();
   __shared__ uint32_t carry;
   const uint32_t F = min(ctr->nfits, static_cast<uint32_t>(kClusterBins));
   if (threadIdx.x == 0) carry = 0;
@@ -1404,11 +1438,14 @@ __device__ __forceinline__ void refine_part_body(Counters* ctr, SegBufs b) {
   }
 }
 
-__global__ void __launch_bounds__(256) k_refine_part0(Counters* ctr, SegBufs b) { refine_part_body<0>(ctr, b); }
-__global__ void __launch_bounds__(256) k_refine_part1(Counters* ctr, SegBufs b) { refine_part_body<1>(ctr, b); }
+__global__ void __launch_bounds__(256) k_refine_part0(Counters* ctr, SegBufs b) {
+  VP_GRID_WAIT(); refine_part_body<0>(ctr, b); }
+__global__ void __launch_bounds__(256) k_refine_part1(Counters* ctr, SegBufs b) {
+  VP_GRID_WAIT(); refine_part_body<1>(ctr, b); }
 
 // Per fit (one thread): centroid = (sum of chunk sums in chunk order) / n.
 __global__ void k_refine_cen(Counters* ctr, SegBufs b) {
+  VP_GRID_WAIT();
   const uint32_t F = min(ctr->nfits, static_cast<uint32_t>(kClusterBins));
   if (ctr->overflow & (kOverflowFits | kOverflowMembers)) return;
   for (uint32_t f = blockIdx.x * blockDim.x + threadIdx.x; f < F; f += gridDim.x * blockDim.x) {
@@ -1428,6 +1465,7 @@ __global__ void k_refine_cen(Counters* ctr, SegBufs b) {
 // Per fit (one thread): covariance / n -> Jacobi -> rank gate -> orient_up
 // (plane_fit.cpp:133-154); unrefined fits keep the RANSAC model.
 __global__ void k_refine_fin(Counters* ctr, SegBufs b, d3 up) {
+  VP_GRID_WAIT();
   const uint32_t F = min(ctr->nfits, static_cast<uint32_t>(kClusterBins));
   if (ctr->overflow & (kOverflowFits | kOverflowMembers)) return;
   for (uint32_t f = blockIdx.x * blockDim.x + threadIdx.x; f < F; f += gridDim.x * blockDim.x) {
@@ -1552,6 +1590,7 @@ __device__ __forceinline__ uint32_t poly_fit_of_chunk(const SegBufs& b, uint32_t
 }
 
 __global__ void k_poly_setup(Counters* ctr, SegBufs b) {
+  VP_GRID_WAIT();
   __shared__ uint32_t carry;
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
@@ -1597,6 +1636,7 @@ __global__ void k_poly_setup(Counters* ctr, SegBufs b) {
 // +0.0 terms).
 __global__ void __launch_bounds__(256) k_poly_extremes(Counters* ctr, SegBufs b, const double* dirtab,
                                                        int directions, int planar) {
+  VP_GRID_WAIT();
   __shared__ double sdir[128];
   __shared__ double ex_dot[8 * 16];
   __shared__ int ex_idx[8 * 16];
@@ -1680,6 +1720,7 @@ __global__ void __launch_bounds__(256) k_poly_extremes(Counters* ctr, SegBufs b,
 }
 
 __global__ void k_poly_inner(Counters* ctr, SegBufs b, int directions) {
+  VP_GRID_WAIT();
   __shared__ P2 ext[64];
   __shared__ P2 hull_s[130];
   const uint32_t F = ctr->nfits;
@@ -1729,6 +1770,7 @@ __global__ void k_poly_inner(Counters* ctr, SegBufs b, int directions) {
 }
 
 __global__ void __launch_bounds__(256) k_poly_keep(Counters* ctr, SegBufs b) {
+  VP_GRID_WAIT();
   __shared__ P2 inner[130];
   __shared__ uint32_t ni_s;
   const uint32_t F = ctr->nfits, nchunks = ctr->poly_chunks;
@@ -1767,6 +1809,7 @@ __global__ void __launch_bounds__(256) k_poly_keep(Counters* ctr, SegBufs b) {
 }
 
 __global__ void k_poly_hull(Counters* ctr, SegBufs b, double min_area) {
+  VP_GRID_WAIT();
   extern __shared__ P2 sm_pts[];  // kHullSmem points
   __shared__ uint32_t n_uniq, voff;
   __shared__ double area_s;
@@ -1905,6 +1948,7 @@ namespace vp {
 // [3] reserved; F records of 12 doubles (normal, offset, area, 3 unused,
 // then inlier_count, label, nv as doubles, 1 unused); Vt x 5 (u v x y z).
 __global__ void k_poly_pack(const Counters* ctr, SegBufs b, double* out, uint64_t cap) {
+  VP_GRID_WAIT();
   __shared__ uint32_t carry;
   const uint32_t F = (ctr->overflow & (kOverflowFits | kOverflowMembers | kOverflowPool)) ? 0u : ctr->nfits;
   if (threadIdx.x == 0) carry = 0;
@@ -1949,6 +1993,7 @@ namespace vp {
 // Counters the CCL .. polygon chain accumulates, back to their state after
 // the grid readers (a pipelined frame's chain re-run after its buffers grew).
 __global__ void k_chain_rearm(Counters* ctr) {
+  VP_GRID_WAIT();
   if (threadIdx.x != 0) return;
   ctr->K = 0;
   ctr->nfits = 0;

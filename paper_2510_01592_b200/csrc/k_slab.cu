@@ -45,6 +45,7 @@ __device__ __forceinline__ int owner_of(const RankDesc& r, int64_t label) {
 // searches per plane, no atomics.
 __global__ void k_plane_counts(const Counters* ctr, const int32_t* __restrict__ st_idx, uint32_t cap,
                                int32_t x0, int32_t nplanes, uint32_t* counts) {
+  VP_GRID_WAIT();
   const uint32_t S = min(ctr->S, cap);
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < nplanes; p += gridDim.x * blockDim.x) {
     uint32_t lohi[2];
@@ -63,6 +64,7 @@ __global__ void k_plane_counts(const Counters* ctr, const int32_t* __restrict__ 
 }
 
 __global__ void k_fill_i32(int32_t* a, uint64_t n, int32_t v) {
+  VP_GRID_WAIT();
   for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
     a[i] = v;
@@ -70,6 +72,7 @@ __global__ void k_fill_i32(int32_t* a, uint64_t n, int32_t v) {
 
 // Smallest zone entry (local index) of every local component.
 __global__ void k_zone_bmin(const Counters* ctr, SegBufs b, ZoneDesc z, int32_t* bmin) {
+  VP_GRID_WAIT();
   const uint32_t S = min(ctr->S, b.Scap);
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < S; i += gridDim.x * blockDim.x)
     if (zone_of(z, __ldg(b.st_idx + 3ull * i)) >= 0) {
@@ -85,6 +88,7 @@ __global__ void k_zone_bmin(const Counters* ctr, SegBufs b, ZoneDesc z, int32_t*
 // triples does not affect the merge result.
 __global__ void k_zone_triples(const Counters* ctr, SegBufs b, ZoneDesc z, int64_t base,
                                const int32_t* __restrict__ bmin, int32_t* out, uint32_t* nout) {
+  VP_GRID_WAIT();
   const uint32_t S = min(ctr->S, b.Scap);
   const unsigned lane = lane_id();
   const uint32_t stride = gridDim.x * blockDim.x;
@@ -107,6 +111,7 @@ __global__ void k_zone_triples(const Counters* ctr, SegBufs b, ZoneDesc z, int64
 }
 
 __global__ void k_zone_init(int32_t* parent, int32_t* minlab, uint64_t Z) {
+  VP_GRID_WAIT();
   for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < Z;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     parent[i] = static_cast<int32_t>(i);
@@ -116,6 +121,7 @@ __global__ void k_zone_init(int32_t* parent, int32_t* minlab, uint64_t Z) {
 
 // Union of every triple's two zone entries (padding triples have a < 0).
 __global__ void k_zone_union(const int32_t* __restrict__ t, uint64_t n, int32_t* parent) {
+  VP_GRID_WAIT();
   for (uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
        j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const int32_t a = __ldg(t + 3 * j);
@@ -126,6 +132,7 @@ __global__ void k_zone_union(const int32_t* __restrict__ t, uint64_t n, int32_t*
 
 // Canonical label of each joined set: the minimum local label over it.
 __global__ void k_zone_minlab(const int32_t* __restrict__ t, uint64_t n, int32_t* parent, int32_t* minlab) {
+  VP_GRID_WAIT();
   for (uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
        j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     if (__ldg(t + 3 * j) < 0) continue;
@@ -140,6 +147,7 @@ __global__ void k_zone_minlab(const int32_t* __restrict__ t, uint64_t n, int32_t
 __global__ void k_slab_relabel(SegBufs b, ZoneDesc z, int64_t base, uint32_t n_left, uint32_t n_own,
                                const int32_t* __restrict__ bmin, int32_t* parent,
                                const int32_t* __restrict__ minlab, int32_t* flabel) {
+  VP_GRID_WAIT();
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n_own; j += gridDim.x * blockDim.x) {
     const int32_t r = b.label[n_left + j];
     const int32_t bm = bmin[r];
@@ -156,6 +164,7 @@ __global__ void k_slab_relabel(SegBufs b, ZoneDesc z, int64_t base, uint32_t n_l
 // owner, stable-sorted by destination (ascending ordinal inside each).
 __global__ void k_export_hist(uint32_t n_own, const int32_t* __restrict__ flabel, RankDesc rd, int me,
                               uint32_t* H, uint32_t nch, uint32_t* dcount) {
+  VP_GRID_WAIT();
   __shared__ uint32_t hist[kMaxSlabs];
   const unsigned lane = lane_id();
   const int64_t own_lo = rd.ord_lo[me];
@@ -179,6 +188,7 @@ __global__ void k_export_hist(uint32_t n_own, const int32_t* __restrict__ flabel
 __global__ void k_export_scatter(uint32_t n_own, const int32_t* __restrict__ flabel,
                                  const double* __restrict__ mean, RankDesc rd, int me,
                                  const uint32_t* __restrict__ H, uint32_t nch, MemberRec* out) {
+  VP_GRID_WAIT();
   __shared__ uint32_t run[kMaxSlabs];
   const unsigned lane = lane_id();
   const int64_t own_lo = rd.ord_lo[me];
@@ -215,6 +225,7 @@ __global__ void k_export_scatter(uint32_t n_own, const int32_t* __restrict__ fla
 // cluster is owned here get its local root index as label; the others point
 // at themselves with a zero count, so filter_clusters never selects them.
 __global__ void k_owner_init(uint32_t n, SegBufs b) {
+  VP_GRID_WAIT();
   for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
     b.cnt[e] = 0;
     b.cid[e] = -1;
@@ -224,6 +235,7 @@ __global__ void k_owner_init(uint32_t n, SegBufs b) {
 __global__ void k_owner_prep(uint32_t n_own, uint32_t n_recv, int64_t own_base,
                              const double* __restrict__ own_mean, const int32_t* __restrict__ flabel,
                              const MemberRec* __restrict__ recv, SegBufs b) {
+  VP_GRID_WAIT();
   const uint32_t n = n_own + n_recv;
   for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
     int32_t L;
@@ -253,6 +265,7 @@ __global__ void k_owner_prep(uint32_t n_own, uint32_t n_recv, int64_t own_base,
 // Cluster labels back to global ordinals (after k_cluster_setup, before the
 // RANSAC seeds read them).
 __global__ void k_klabel_rebase(const Counters* ctr, SegBufs b, int64_t base) {
+  VP_GRID_WAIT();
   const uint32_t K = min(ctr->K, static_cast<uint32_t>(kClusterBins));
   for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < K; k += gridDim.x * blockDim.x)
     b.klabel[k] = static_cast<int32_t>(b.klabel[k] + base);

@@ -34,6 +34,8 @@ thread_local std::string g_err;
 // CCL variant: 0 = min-neighbour hook + forward-window unions (default),
 // 1 = neighbour sampling + giant skip, 2 = hook + giant skip (same labels)
 int g_ccl_mode = 0;
+// programmatic dependent launch on every LAUNCH (VP_PDL=0 disables, A/B)
+const bool g_pdl = !(getenv("VP_PDL") && atoi(getenv("VP_PDL")) == 0);
 // pointer-jumping rounds between hook and compress (VP_CCL_JUMPS, A/B)
 int g_ccl_jumps = getenv("VP_CCL_JUMPS") ? atoi(getenv("VP_CCL_JUMPS")) : 3;
 // VP_WALK_GENERIC=1 (experiments): plain-grid rays through the generic walk loop
@@ -99,13 +101,27 @@ void prof_end(cudaStream_t s, const char* name) {
   g_prof.push_back(ProfEntry{name, ms, 1});
 }
 
-#define LAUNCH(kernel, grid, block, smem, stream, ...)                         \
+// Every kernel is launched with programmatic stream serialisation (PDL): its
+// launch and block dispatch overlap the previous kernel's tail, and its first
+// statement (VP_GRID_WAIT) holds it until that kernel's writes are visible.
+// Inside a CUDA graph the kernel-to-kernel edges become programmatic edges.
+// VP_PDL=0 launches without the attribute (A/B).
+#define LAUNCH(kernel, grid, block, smem, strm_, ...)                           \
   do {                                                                         \
-    if (g_prof_on) prof_begin(stream);                                         \
-    kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);               \
-    ck(cudaGetLastError(), #kernel);                                           \
+    if (g_prof_on) prof_begin(strm_);                                         \
+    cudaLaunchConfig_t cfg_{};                                                 \
+    cfg_.gridDim = dim3(grid);                                                 \
+    cfg_.blockDim = dim3(block);                                               \
+    cfg_.dynamicSmemBytes = (smem);                                            \
+    cfg_.stream = (strm_);                                                      \
+    cudaLaunchAttribute at_[1];                                                \
+    at_[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;            \
+    at_[0].val.programmaticStreamSerializationAllowed = 1;                     \
+    cfg_.attrs = at_;                                                          \
+    cfg_.numAttrs = g_pdl ? 1 : 0;                                             \
+    ck(cudaLaunchKernelEx(&cfg_, kernel, __VA_ARGS__), #kernel);               \
     g_launches.fetch_add(1, std::memory_order_relaxed);                        \
-    if (g_prof_on) prof_end(stream, #kernel);                                  \
+    if (g_prof_on) prof_end(strm_, #kernel);                                  \
   } while (0)
 
 template <typename T>
@@ -1283,6 +1299,10 @@ struct vp_pipeline {
   cudaEvent_t ev_start[kSlots] = {}, ev_pre[kSlots] = {}, ev_map[kSlots] = {};
   cudaEvent_t ev_clu[kSlots] = {}, ev_ccl[kSlots] = {}, ev_rsc[kSlots] = {}, ev_done[kSlots] = {};
   cudaEvent_t ev_h2d[kSlots] = {};
+  // one frame's latency (vp_pipeline_frame): points H2D start -> polygons
+  // assembled in host memory
+  cudaEvent_t lat_ev[2] = {nullptr, nullptr};
+  float last_latency_ms = 0.0f;
   cudaStream_t cstream = nullptr;  // host-to-device copies of upcoming frames
   // every frame's polygons, packed by k_poly_pack into mapped pinned memory
   double* pack_h[kSlots] = {};
@@ -1296,6 +1316,8 @@ struct vp_pipeline {
     double origin[3] = {0.0, 0.0, 0.0};
   } meta[kSlots];
   ~vp_pipeline() {
+    for (auto e : lat_ev)
+      if (e) cudaEventDestroy(e);
     if (gexec) cudaGraphExecDestroy(gexec);
     for (auto& row : rx)
       for (auto& x : row)
@@ -1373,6 +1395,9 @@ bool pipeline_enqueue(vp_pipeline* pl, const float* xyz, uint64_t n, const doubl
   g->seg.ensure_dirs(16, g->stream);
   g->set_pose(R, t);
   g->fill_static_params();
+  if (!pl->lat_ev[0])
+    for (auto& e : pl->lat_ev) ck(cudaEventCreate(&e), "event");
+  ck(cudaEventRecord(pl->lat_ev[0], g->stream), "event");  // before the points H2D
   stage_points(g, xyz, n, device_ptr);
   int32_t cell[3];
   global_cell(t, g->gd.res, cell);
@@ -2975,6 +3000,10 @@ int vp_make_polygons(size_t n, const vp_plane* planes, const uint64_t* offsets,
 
 void vp_polygons_free(vp_polygons_t* p) { std::free(p); }
 
+int vp_pipeline_latency_ms(const vp_pipeline* pl, double* ms) {
+  return guard([&] { *ms = static_cast<double>(pl->last_latency_ms); });
+}
+
 }  // extern "C"
 
 // Accessors for the slab-frame orchestration (slab_frame.cu).
@@ -3482,6 +3511,10 @@ static int pipeline_frame_impl(vp_pipeline* pl, const float* xyz, uint64_t n, co
       g->download_polygons(hp, false);
       *out = make_polygons_out(hp);
     }
+    // the polygons are in host memory: the frame's end to end latency
+    ck(cudaEventRecord(pl->lat_ev[1], g->stream), "event");
+    ck(cudaEventSynchronize(pl->lat_ev[1]), "event");
+    ck(cudaEventElapsedTime(&pl->last_latency_ms, pl->lat_ev[0], pl->lat_ev[1]), "elapsed");
     ++pl->frame;
   });
 }
