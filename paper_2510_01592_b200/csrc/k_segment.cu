@@ -1,6 +1,8 @@
 // Segmentation kernels: normals + steppability, CCL, cluster gather, RANSAC,
 // refine, polygon. Reference: /root/reference/proj/core/src/{segmentation,
 // jacobi,plane_fit,polygonize}.cpp and pipeline.cpp:43-85.
+#include <cooperative_groups.h>
+
 #include "vp_kernels.cuh"
 
 namespace vp {
@@ -1527,20 +1529,28 @@ __device__ uint32_t chain_sorted(const P2* pts, uint32_t n, P2* h) {
 // live in registers (the pop loop is a serial dependency chain).
 __device__ uint32_t half_chain(const P2* pts, uint32_t n, bool upper, P2* h) {
   uint32_t k = 0;
-  P2 a{0.0, 0.0}, t{0.0, 0.0};
+  // the top three stack entries live in registers (t = h[k-1], a = h[k-2],
+  // a2 = h[k-3]): a pop's next test needs no shared-memory round trip, and the
+  // entry below is fetched while the cross product runs; the next input
+  // point is loaded one step ahead
+  P2 a{0.0, 0.0}, t{0.0, 0.0}, a2{0.0, 0.0};
   if (upper) {
     t = pts[n - 1];
     h[k++] = t;
   }
   const uint32_t m = upper ? n - 1 : n;
+  P2 pn = m ? (upper ? pts[n - 2] : pts[0]) : P2{0.0, 0.0};
   for (uint32_t q = 0; q < m; ++q) {
-    const P2 p = upper ? pts[n - 2 - q] : pts[q];
+    const P2 p = pn;
+    if (q + 1 < m) pn = upper ? pts[n - 3 - q] : pts[q + 1];
     while (k >= 2 && cross2(a, t, p) <= 0.0) {
       --k;
       t = a;
-      if (k >= 2) a = h[k - 2];
+      a = a2;
+      if (k >= 3) a2 = h[k - 3];
     }
     h[k++] = p;
+    a2 = a;
     a = t;
     t = p;
   }
@@ -1576,8 +1586,11 @@ __device__ void bitonic_sort(P2* a, uint32_t n) {
 //  keep    (block / chunk)  survivors: not strictly inside the inner polygon
 //  hull    (block / fit)    lexicographic bitonic sort, unique, monotone chain,
 //                           lift, shoelace, area filter, output record
+// oi != bi: a candidate met again (shuffle-down lanes past the warp's end
+// receive their own value) is not better -- without this every reduction
+// step paid two global loads for the tie-break (C2 polygon stage: 15 us).
 __device__ __forceinline__ bool ext_better(double od, int oi, double bd, int bi, const P2* proj) {
-  return oi >= 0 && (bi < 0 || od > bd || (od == bd && lex_less(proj[oi], proj[bi])));
+  return oi >= 0 && oi != bi && (bi < 0 || od > bd || (od == bd && lex_less(proj[oi], proj[bi])));
 }
 
 __device__ __forceinline__ uint32_t poly_fit_of_chunk(const SegBufs& b, uint32_t F, uint32_t c) {
@@ -1940,6 +1953,363 @@ __global__ void k_poly_hull(Counters* ctr, SegBufs b, double min_area) {
 
 namespace vp {
 
+// ---------------------------------------------------------------------------
+// make_polygon for every fit in ONE kernel (the default polygon stage): a
+// thread-block cluster of kPolyCluster (4) CTAs per fit (fits strided over the
+// clusters of the grid), distributed shared memory between them:
+//  1. every CTA: plane_basis, project_to_plane of its share of the inliers,
+//     per-direction extremes (larger dot, ties to the lexicographically
+//     smaller point -- a total order, so any reduction order gives the
+//     reference's extremes), reduced in the CTA and sent to the leader CTA;
+//  2. leader: final extremes, inner polygon = monotone_chain(extremes);
+//  3. every CTA: reads the inner polygon from the leader (DSMEM), keeps its
+//     points not strictly inside (hull_filter's keep test), appends them to
+//     the leader's shared-memory survivor buffer (DSMEM atomics) and to the
+//     fit's global survivor range;
+//  4. leader: lexicographic bitonic sort, unique, the two monotone chains,
+//     shoelace, area filter, lift, polygon record -- the k_poly_hull body.
+// Replaces the five kernels setup / extremes / inner / keep / hull (kept for
+// the public hull_filter); the survivor set, and so the hull, is identical.
+// ---------------------------------------------------------------------------
+#ifdef VP_POLY_PROFILE
+__device__ unsigned long long g_poly_t[64][16];
+#define VP_PT(k)                                                                              \
+  do {                                                                                        \
+    if (leader && threadIdx.x == 0 && f < 64) {                                               \
+      unsigned long long t_;                                                                  \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                  \
+      g_poly_t[f][k] = t_;                                                                    \
+    }                                                                                         \
+  } while (0)
+#else
+#define VP_PT(k) do {} while (0)
+#endif
+constexpr int kPolyThreads = 512;
+constexpr int kPolyWarps = kPolyThreads / 32;
+
+__device__ __forceinline__ bool ext_better_pt(double od, P2 op, bool ook, double bd, P2 bp, bool bok) {
+  return ook && (!bok || od > bd || (od == bd && lex_less(op, bp)));
+}
+
+__global__ void __cluster_dims__(kPolyCluster, 1, 1) __launch_bounds__(kPolyThreads)
+    k_poly_fused(Counters* ctr, SegBufs b, const double* dirtab, int directions, int planar, double min_area) {
+  VP_GRID_WAIT();
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const unsigned crank = cl.block_rank();
+  const bool leader = crank == 0;
+  extern __shared__ P2 sm_pts[];  // leader: survivors, unique, lower and upper stacks (4 x kHullSmem)
+  __shared__ double sdir[128];
+  __shared__ double wdot[kPolyWarps][16];
+  __shared__ int widx[kPolyWarps][16];
+  __shared__ double cdot[kPolyCluster][64];  // leader: every CTA's extremes
+  __shared__ P2 cpt[kPolyCluster][64];
+  __shared__ int cok[kPolyCluster][64];
+  __shared__ P2 ext_s[64];
+  __shared__ P2 inner_s[130];
+  __shared__ uint32_t ni_s, nsurv_s, n_uniq, voff;
+  __shared__ double area_s, basis_s[9];
+  const uint32_t F = (ctr->overflow & (kOverflowFits | kOverflowMembers)) ? 0u : ctr->nfits;
+  const uint32_t ncl = gridDim.x / kPolyCluster, cid = blockIdx.x / kPolyCluster;
+  for (int j = threadIdx.x; j < 2 * directions && j < 128; j += blockDim.x) sdir[j] = dirtab[j];
+  P2* proj = reinterpret_cast<P2*>(b.proj);
+  const unsigned lane = lane_id(), wid = threadIdx.x >> 5;
+  const uint32_t gtid = crank * kPolyThreads + threadIdx.x, gstride = kPolyCluster * kPolyThreads;
+  for (uint32_t f = cid; f < F; f += ncl) {
+    const uint32_t i0 = b.ioff[f], i1 = b.ioff[f + 1], n = i1 - i0;
+    const double* pl = b.ref_model + 4 * f;
+    if (leader && threadIdx.x == 0) {  // the record (make_polygon: nullopt unless a hull)
+      double* rd = b.prec_d + 8 * f;
+      int32_t* ri = b.prec_i + 4 * f;
+      rd[0] = pl[0], rd[1] = pl[1], rd[2] = pl[2], rd[3] = pl[3], rd[4] = 0.0;
+      ri[0] = b.fit_meta[2 * f], ri[1] = b.fit_meta[2 * f + 1], ri[2] = 0, ri[3] = 0;
+      nsurv_s = 0;
+    }
+    if (n < 3) {
+      cl.sync();
+      continue;
+    }
+    VP_PT(0);
+    if (threadIdx.x == 0) {  // plane_basis (polygonize.cpp:21-34), every CTA
+      const d3 nrm = mk3(pl[0], pl[1], pl[2]);
+      int least = 0;
+      const double an[3] = {fabs(nrm.x), fabs(nrm.y), fabs(nrm.z)};
+      if (an[1] < an[least]) least = 1;
+      if (an[2] < an[least]) least = 2;
+      const d3 axis = mk3(least == 0 ? 1.0 : 0.0, least == 1 ? 1.0 : 0.0, least == 2 ? 1.0 : 0.0);
+      const d3 u = normalized3(sub3(axis, scl3(dot3(nrm, axis), nrm)));
+      const d3 v = cross3(nrm, u);
+      const d3 org = scl3(pl[3], nrm);
+      basis_s[0] = u.x, basis_s[1] = u.y, basis_s[2] = u.z;
+      basis_s[3] = v.x, basis_s[4] = v.y, basis_s[5] = v.z;
+      basis_s[6] = org.x, basis_s[7] = org.y, basis_s[8] = org.z;
+      if (leader) {
+        double* bs = b.basis + 9 * f;
+        for (int k = 0; k < 9; ++k) bs[k] = basis_s[k];
+      }
+    }
+    __syncthreads();
+    const d3 u = mk3(basis_s[0], basis_s[1], basis_s[2]), v = mk3(basis_s[3], basis_s[4], basis_s[5]),
+             org = mk3(basis_s[6], basis_s[7], basis_s[8]);
+    VP_PT(12);
+    // 1. project_to_plane (:36-44) + per-direction extremes of this CTA's points
+    const bool filter = n > 3 && directions >= 3;
+    for (uint32_t i = i0 + gtid; i < i1; i += gstride) {
+      if (planar) {
+        proj[i] = P2{b.inl[3 * i], b.inl[3 * i + 1]};
+      } else {
+        const d3 d = sub3(mk3(b.inl[3 * i], b.inl[3 * i + 1], b.inl[3 * i + 2]), org);
+        proj[i] = P2{dot3(d, u), dot3(d, v)};
+      }
+    }
+    __syncthreads();  // tie-breaks below read other threads' projections
+    VP_PT(8);
+    if (filter) {
+      for (int j0 = 0; j0 < directions; j0 += 16) {
+        const int nd = min(16, directions - j0);
+        double bd[16];
+        int bi[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) bd[q] = -CUDART_INF, bi[q] = -1;
+        for (uint32_t i = i0 + gtid; i < i1; i += gstride) {
+          const P2 q2 = proj[i];  // this thread's own write
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            if (q < nd) {
+              const double dd = q2.x * sdir[2 * (j0 + q)] + q2.y * sdir[2 * (j0 + q) + 1];
+              if (dd > bd[q] || (dd == bd[q] && bi[q] >= 0 && lex_less(q2, proj[bi[q]]))) {
+                bd[q] = dd;
+                bi[q] = static_cast<int>(i);
+              }
+            }
+          }
+        }
+        VP_PT(9);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            const double od = __shfl_down_sync(0xffffffffu, bd[q], o);
+            const int oi = __shfl_down_sync(0xffffffffu, bi[q], o);
+            if (ext_better(od, oi, bd[q], bi[q], proj)) {
+              bd[q] = od;
+              bi[q] = oi;
+            }
+          }
+          if (lane == 0) {
+            wdot[wid][q] = bd[q];
+            widx[wid][q] = bi[q];
+          }
+        }
+        __syncthreads();
+        VP_PT(10);
+        if (threadIdx.x < static_cast<unsigned>(nd)) {  // this CTA's extreme -> the leader
+          const int q = static_cast<int>(threadIdx.x);
+          double best = -CUDART_INF;
+          int bix = -1;
+          for (int w2 = 0; w2 < kPolyWarps; ++w2)
+            if (ext_better(wdot[w2][q], widx[w2][q], best, bix, proj)) {
+              best = wdot[w2][q];
+              bix = widx[w2][q];
+            }
+          double* rdot = cl.map_shared_rank(&cdot[0][0], 0);
+          P2* rpt = cl.map_shared_rank(&cpt[0][0], 0);
+          int* rok = cl.map_shared_rank(&cok[0][0], 0);
+          rdot[crank * 64 + j0 + q] = best;
+          rpt[crank * 64 + j0 + q] = bix >= 0 ? proj[bix] : P2{0.0, 0.0};
+          rok[crank * 64 + j0 + q] = bix >= 0 ? 1 : 0;
+        }
+        __syncthreads();
+        VP_PT(11);
+      }
+    }
+    cl.sync();
+    VP_PT(1);
+    // 2. leader: final extremes and the inner polygon (hull_filter, polygonize.cpp:50-94)
+    if (leader) {
+      if (filter && threadIdx.x < static_cast<unsigned>(directions)) {
+        const int j = static_cast<int>(threadIdx.x);
+        double best = -CUDART_INF;
+        P2 bp{0.0, 0.0};
+        bool bok = false;
+        for (int r = 0; r < kPolyCluster; ++r)
+          if (ext_better_pt(cdot[r][j], cpt[r][j], cok[r][j] != 0, best, bp, bok)) {
+            best = cdot[r][j];
+            bp = cpt[r][j];
+            bok = true;
+          }
+        ext_s[j] = bok ? bp : P2{0.0, 0.0};
+      }
+      __syncthreads();
+      // lexicographic sort of the extremes by rank (ties by direction index),
+      // unique, then monotone_chain over <= 64 points on one thread
+      __shared__ P2 esort[64];
+      if (filter && threadIdx.x < static_cast<unsigned>(directions)) {
+        const int j = static_cast<int>(threadIdx.x);
+        const P2 me = ext_s[j];
+        int r = 0;
+        for (int i = 0; i < directions; ++i) {
+          const P2 o = ext_s[i];
+          r += (lex_less(o, me) || (!lex_less(me, o) && i < j)) ? 1 : 0;
+        }
+        esort[r] = me;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        uint32_t ni = 0;
+        if (filter) {
+          uint32_t m = 0;
+          for (int j = 0; j < directions; ++j)
+            if (m == 0 || !(esort[j].x == esort[m - 1].x && esort[j].y == esort[m - 1].y)) esort[m++] = esort[j];
+          ni = chain_sorted(esort, m, inner_s);
+        }
+        ni_s = ni >= 3 ? ni : 0u;  // < 3: no filtering (hull_filter returns all points)
+      }
+    }
+    cl.sync();
+    VP_PT(2);
+    // 3. every CTA: the keep test against the leader's inner polygon; survivors
+    //    to the leader's shared memory (first kHullSmem) and to global memory
+    if (!leader) {
+      if (threadIdx.x == 0) ni_s = *cl.map_shared_rank(&ni_s, 0);
+      __syncthreads();
+      const P2* rin = cl.map_shared_rank(&inner_s[0], 0);
+      for (uint32_t k = threadIdx.x; k < ni_s; k += blockDim.x) inner_s[k] = rin[k];
+    }
+    __syncthreads();
+    const uint32_t ni = ni_s;
+    uint32_t* rnsurv = cl.map_shared_rank(&nsurv_s, 0);
+    P2* rsurv = cl.map_shared_rank(sm_pts, 0);
+    P2* gsurv = reinterpret_cast<P2*>(b.surv) + 2 * static_cast<uint64_t>(i0);
+    for (uint32_t base = i0 + crank * kPolyThreads + (threadIdx.x & ~31u); base < i1; base += gstride) {
+      const uint32_t i = base + lane;
+      bool keep = false;
+      P2 q{0.0, 0.0};
+      if (i < i1) {
+        q = proj[i];
+        keep = ni == 0;
+        for (uint32_t e = 0; e < ni && !keep; ++e)
+          if (cross2(inner_s[e], inner_s[(e + 1) % ni], q) <= 0.0) keep = true;
+      }
+      const unsigned km = __ballot_sync(0xffffffffu, keep);
+      uint32_t at = 0;
+      if (km) {
+        const int first = __ffs(km) - 1;
+        if (static_cast<int>(lane) == first) at = atomicAdd(rnsurv, static_cast<uint32_t>(__popc(km)));
+        at = __shfl_sync(0xffffffffu, at, first);
+      }
+      if (keep) {
+        const uint32_t k = at + __popc(km & lanemask_lt());
+        gsurv[k] = q;
+        if (k < static_cast<uint32_t>(kHullSmem)) rsurv[k] = q;
+      }
+    }
+    cl.sync();
+    VP_PT(3);
+    // 4. leader: sort, unique, monotone chain, area, lift (k_poly_hull)
+    if (leader) {
+      const uint32_t ns = nsurv_s;
+      if (threadIdx.x == 0) atomicMax(&ctr->surv_max, ns);
+      uint32_t np2 = 1;
+      while (np2 < ns) np2 <<= 1;
+      const bool in_smem = np2 <= static_cast<uint32_t>(kHullSmem);
+      P2* arr = in_smem ? sm_pts : gsurv;
+      P2* hullg = reinterpret_cast<P2*>(b.hull) + 2 * static_cast<uint64_t>(i0);  // the ring (global, <= 2 ns)
+      for (uint32_t i = ns + threadIdx.x; i < np2; i += blockDim.x) arr[i] = P2{CUDART_INF, CUDART_INF};
+      __syncthreads();
+      bitonic_sort(arr, np2);
+      VP_PT(4);
+      if (in_smem) {
+        P2* uq = sm_pts + kHullSmem;
+        P2* lo_st = sm_pts + 2 * kHullSmem;
+        P2* up_st = sm_pts + 3 * kHullSmem;
+        constexpr int kPer = kHullSmem / kPolyThreads;
+        static_assert(kHullSmem % kPolyThreads == 0 && kHullSmem / kPolyThreads <= 32, "survivor slots per thread");
+        uint32_t keep_mask = 0, cnt = 0;
+        const uint32_t j0 = threadIdx.x * kPer;
+#pragma unroll
+        for (int qq = 0; qq < kPer; ++qq) {
+          const uint32_t i = j0 + qq;
+          const bool k = i < ns && (i == 0 || !(arr[i].x == arr[i - 1].x && arr[i].y == arr[i - 1].y));
+          keep_mask |= (k ? 1u : 0u) << qq;
+          cnt += k ? 1u : 0u;
+        }
+        uint32_t pos = block_exclusive_u32(cnt);
+        if (threadIdx.x == blockDim.x - 1) n_uniq = pos + cnt;
+#pragma unroll
+        for (int qq = 0; qq < kPer; ++qq)
+          if ((keep_mask >> qq) & 1u) uq[pos++] = arr[j0 + qq];
+        __syncthreads();
+        const uint32_t mu = n_uniq;
+        if (mu >= 3 && (threadIdx.x == 0 || threadIdx.x == 32)) {
+          const bool upper = threadIdx.x == 32;
+          const uint32_t k = half_chain(uq, mu, upper, upper ? up_st : lo_st);
+          if (upper) voff = k; else area_s = static_cast<double>(k);  // stash sizes
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          uint32_t mh = 0;
+          if (mu >= 3) {
+            const uint32_t kl = static_cast<uint32_t>(area_s), ku = voff;
+            for (uint32_t i = 0; i < kl; ++i) hullg[mh++] = lo_st[i];
+            for (uint32_t i = 1; i + 1 < ku; ++i) hullg[mh++] = up_st[i];
+            if (mh < 3) mh = 0;
+          }
+          n_uniq = mh;
+        }
+        __syncthreads();
+        VP_PT(5);
+      }
+      if (threadIdx.x == 0) {
+        if (!in_smem) {
+          uint32_t m = 0;  // std::unique
+          for (uint32_t i = 0; i < ns; ++i)
+            if (m == 0 || !(arr[i].x == arr[m - 1].x && arr[i].y == arr[m - 1].y)) arr[m++] = arr[i];
+          n_uniq = chain_sorted(arr, m, hullg);
+        }
+        voff = 0xffffffffu;
+        area_s = 0.0;
+        const uint32_t mh = n_uniq;
+        if (mh >= 3) {
+          double twice = 0.0;  // polygon_area (:146-154)
+          for (uint32_t i = 0; i < mh; ++i) {
+            const P2 a = hullg[i], c = hullg[(i + 1) % mh];
+            twice += a.x * c.y - c.x * a.y;
+          }
+          area_s = 0.5 * twice;
+          if (area_s >= min_area) {
+            const uint32_t at = atomicAdd(&ctr->pool_used, mh);
+            if (at + mh <= b.pool_cap) voff = at;
+            else atomicOr(&ctr->overflow, kOverflowPool);
+          }
+        }
+        double* rd = b.prec_d + 8 * f;
+        int32_t* ri = b.prec_i + 4 * f;
+        rd[4] = area_s;
+        ri[2] = (voff != 0xffffffffu) ? static_cast<int32_t>(mh) : 0;
+        ri[3] = static_cast<int32_t>(voff == 0xffffffffu ? 0 : voff);
+      }
+      __syncthreads();
+      const uint32_t m = n_uniq;
+      if (voff != 0xffffffffu) {
+        for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {  // lift_from_plane (:46-48)
+          const P2 q = hullg[i];
+          const d3 p3 = add3(add3(org, scl3(q.x, u)), scl3(q.y, v));
+          double* dst = b.pool + 5 * (static_cast<uint64_t>(voff) + i);
+          dst[0] = q.x;
+          dst[1] = q.y;
+          dst[2] = p3.x;
+          dst[3] = p3.y;
+          dst[4] = p3.z;
+        }
+      }
+    }
+    VP_PT(6);
+    cl.sync();  // the leader's buffers are reused by the next fit
+    VP_PT(7);
+  }
+}
+
 // Zero-copy result hand-off of a pipelined frame: the polygon records of the
 // frame's make_polygon stage (prec_d / prec_i) and its hull vertices, packed
 // in fit order into `out` (mapped pinned host memory, `cap` doubles), so the
@@ -2010,3 +2380,9 @@ __global__ void k_chain_rearm(Counters* ctr) {
 }
 
 }  // namespace vp
+
+#ifdef VP_POLY_PROFILE
+extern "C" int vp_debug_poly_times(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, vp::g_poly_t, sizeof(vp::g_poly_t)) == cudaSuccess ? 0 : 1;
+}
+#endif

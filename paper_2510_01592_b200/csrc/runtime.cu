@@ -34,6 +34,8 @@ thread_local std::string g_err;
 // CCL variant: 0 = min-neighbour hook + forward-window unions (default),
 // 1 = neighbour sampling + giant skip, 2 = hook + giant skip (same labels)
 int g_ccl_mode = 0;
+// polygon stage as five kernels instead of k_poly_fused (VP_POLY_SPLIT=1, A/B)
+const bool g_poly_split = getenv("VP_POLY_SPLIT") && atoi(getenv("VP_POLY_SPLIT")) != 0;
 // programmatic dependent launch on every LAUNCH (VP_PDL=0 disables, A/B)
 const bool g_pdl = !(getenv("VP_PDL") && atoi(getenv("VP_PDL")) == 0);
 // pointer-jumping rounds between hook and compress (VP_CCL_JUMPS, A/B)
@@ -654,6 +656,7 @@ struct vp_grid {
     set_slot(0);
     const uint32_t vcap = static_cast<uint32_t>(std::min<uint64_t>(C, 1u << 22));
     seg.ensure(vcap, vcap, vcap, 100, gd.nwords);
+    ck(cudaFuncSetAttribute(k_poly_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, kPolySmem), "smem attr");
     ck(cudaFuncSetAttribute(k_poly_hull, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             kHullSmem * 16 * 6), "smem attr");
     ck(cudaFuncSetAttribute(k_integrate_fold_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, kDenseSmem),
@@ -1097,8 +1100,16 @@ struct vp_grid {
     LAUNCH(k_refine_part1, 148 * 4, 256, 0, stream, ctr, seg.b);
     LAUNCH(k_refine_fin, 8, 256, 0, stream, ctr, seg.b, u);
   }
+  // make_polygon for every fit: one 8-CTA cluster per fit (k_poly_fused;
+  // VP_POLY_SPLIT=1 runs the five-kernel form setup/extremes/inner/keep/hull)
   void launch_polygon(int dirs, double min_area, int planar = 0) {
     seg.ensure_dirs(dirs, stream);
+    if (!g_poly_split) {
+      const int clusters = chain_wide >= 148 * 8 ? 32 : 16;
+      LAUNCH(k_poly_fused, clusters * kPolyCluster, 512, kPolySmem, stream, ctr, seg.b, seg.dirtab, dirs,
+             planar, min_area);
+      return;
+    }
     LAUNCH(k_poly_setup, 1, 1024, 0, stream, ctr, seg.b);
     LAUNCH(k_poly_extremes, chain_wide, 256, 0, stream, ctr, seg.b, seg.dirtab, dirs, planar);
     LAUNCH(k_poly_inner, 148 * 2, 64, 0, stream, ctr, seg.b, dirs);

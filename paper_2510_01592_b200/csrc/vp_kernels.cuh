@@ -24,6 +24,8 @@ static_assert(kHullSmem >= 256 && kHullSmem % 256 == 0 && kHullSmem / 256 <= 32 
                   kHullSmem * 16 * 6 <= 227 * 1024,
               "VP_HULL_SMEM must be a multiple of 256 in [256, 2304]");
 constexpr int kPolyChunk = 1024;    // inlier points per polygon-stage block
+constexpr int kPolyCluster = 4;     // k_poly_fused: CTAs per fit (one thread-block cluster)
+constexpr int kPolySmem = 4 * kHullSmem * 16;  // k_poly_fused dynamic shared memory (4 x kHullSmem points)
 #ifndef VP_FOLD_SMALL
 #define VP_FOLD_SMALL 24
 #endif
@@ -388,6 +390,7 @@ __global__ void k_refine_cen(Counters* ctr, SegBufs b);
 __global__ void k_refine_fin(Counters* ctr, SegBufs b, d3 up);
 __global__ void k_poly_setup(Counters* ctr, SegBufs b);
 __global__ void k_poly_extremes(Counters* ctr, SegBufs b, const double* dirtab, int directions, int planar);
+__global__ void k_poly_fused(Counters* ctr, SegBufs b, const double* dirtab, int directions, int planar, double min_area);
 __global__ void k_poly_inner(Counters* ctr, SegBufs b, int directions);
 __global__ void k_poly_keep(Counters* ctr, SegBufs b);
 __global__ void k_poly_hull(Counters* ctr, SegBufs b, double min_area);

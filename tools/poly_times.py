@@ -1,0 +1,25 @@
+"""Phase timestamps of k_poly_fused (build with -DVP_POLY_PROFILE, run with
+VP_LIB=<that build>): per fit, ns from the fit's start to each phase end."""
+import ctypes as C
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2510_01592_b200 import native, scenes  # noqa: E402
+
+wl = scenes.workload("c2", frames=12)
+pl = native.Pipeline(wl.resolution, wl.extent, wl.frames[0].translation, native.default_params(seed=wl.seed))
+dev = [torch.from_numpy(f.points).cuda() for f in wl.frames]
+for f, d in zip(wl.frames, dev):
+    pl.frame_device(d.data_ptr(), len(f.points), f.rotation, f.translation)
+out = np.zeros((64, 16), np.uint64)
+native.lib().vp_debug_poly_times(out.ctypes.data_as(C.POINTER(C.c_ulonglong)))
+names = ["start", "ext+sync", "inner+sync", "keep+sync", "sort", "uniq+chains", "area+lift", "end sync", "proj", "extloop", "warpred", "ctared", "basis"]
+for f in range(64):
+    if out[f, 0] == 0:
+        break
+    t = out[f].astype(np.int64) - int(out[f, 0])
+    print(f, " ".join(f"{n}={v / 1e3:.1f}" for n, v in zip(names[1:], t[1:13])))
