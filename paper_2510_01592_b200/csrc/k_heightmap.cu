@@ -205,7 +205,7 @@ __global__ void k_hm_zero_cnt(uint32_t nv, SegBufs b) {
 // cluster labels: the seed's flat index (heightmap.cpp:49)
 __global__ void k_hm_klabel(const Counters* ctr, SegBufs b, const uint32_t* visit) {
   VP_GRID_WAIT();
-  const uint32_t K = min(ctr->K, static_cast<uint32_t>(kClusterBins));
+  const uint32_t K = min(ctr->K, b.Kcap);
   for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < K; k += gridDim.x * blockDim.x)
     b.klabel[k] = static_cast<int32_t>(visit[b.klabel[k]]);
 }

@@ -902,7 +902,7 @@ __global__ void k_cluster_assign(Counters* ctr, SegBufs b) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < S; i += gridDim.x * blockDim.x) {
     if (!b.big_flag[i]) continue;
     const uint32_t k = b.big_pos[i];
-    if (k < static_cast<uint32_t>(kClusterBins)) {
+    if (k < b.Kcap) {
       b.klabel[k] = static_cast<int32_t>(i);
       b.cid[i] = static_cast<int32_t>(k);
     }
@@ -915,10 +915,14 @@ __global__ void k_cluster_setup(Counters* ctr, SegBufs b) {
   __shared__ uint32_t carry;
   if (threadIdx.x == 0) {
     carry = 0;
-    if (ctr->K > static_cast<uint32_t>(kClusterBins)) atomicOr(&ctr->overflow, kOverflowClusters);
+    // more clusters than the buffers hold, or a member-sort histogram above
+    // Hcap: the host grows both (grow_k) and re-runs the chain
+    const uint64_t nch = (static_cast<uint64_t>(min(ctr->S, b.Scap)) + kChunk - 1) / kChunk;
+    if (ctr->K > b.Kcap || static_cast<uint64_t>(min(ctr->K, b.Kcap)) * nch > b.Hcap)
+      atomicOr(&ctr->overflow, kOverflowClusters);
   }
   __syncthreads();
-  const uint32_t K = min(ctr->K, static_cast<uint32_t>(kClusterBins));
+  const uint32_t K = min(ctr->K, b.Kcap);
   for (uint32_t base = 0; base < K; base += blockDim.x) {
     const uint32_t k = base + threadIdx.x;
     uint32_t padded = 0;
@@ -947,28 +951,38 @@ __global__ void k_cluster_setup(Counters* ctr, SegBufs b) {
 __global__ void k_member_hist(Counters* ctr, SegBufs b, uint32_t hstride) {
   VP_GRID_WAIT();
   __shared__ uint32_t hist[kClusterBins];
+  if (ctr->overflow & kOverflowClusters) return;
   const uint32_t S = min(ctr->S, b.Scap);
-  const uint32_t K = min(ctr->K, static_cast<uint32_t>(kClusterBins));
+  const uint32_t K = min(ctr->K, b.Kcap);
   const uint32_t nch = (S + kChunk - 1) / kChunk;
+  // up to kClusterBins clusters: per-chunk bins in shared memory; more: the
+  // chunk's column of H itself (H[k * nch + c], this warp its only writer)
+  const bool big = K > static_cast<uint32_t>(kClusterBins);
+  const uint32_t hs = big ? nch : hstride;
   for (uint32_t c = blockIdx.x; c < nch; c += gridDim.x) {
-    for (uint32_t k = threadIdx.x; k < K; k += blockDim.x) hist[k] = 0;
+    uint32_t* col = big ? b.H + c : hist;
+    const uint32_t step = big ? hs : 1u;
+    for (uint32_t k = threadIdx.x; k < K; k += blockDim.x) col[static_cast<uint64_t>(k) * step] = 0;
     __syncwarp();
     const uint32_t e1 = min(S, (c + 1) * kChunk);
     for (uint32_t e = c * kChunk + threadIdx.x; e < e1; e += blockDim.x) {
       const int32_t k = b.cid[b.label[e]];
-      if (k >= 0) atomicAdd(&hist[k], 1u);
+      if (k >= 0) atomicAdd(&col[static_cast<uint64_t>(k) * step], 1u);
     }
     __syncwarp();
-    for (uint32_t k = threadIdx.x; k < K; k += blockDim.x) b.H[k * hstride + c] = hist[k];
+    if (!big)
+      for (uint32_t k = threadIdx.x; k < K; k += blockDim.x) b.H[static_cast<uint64_t>(k) * hs + c] = hist[k];
     __syncwarp();
   }
 }
 
 __global__ void k_member_hscan(Counters* ctr, SegBufs b, uint32_t hstride) {
   VP_GRID_WAIT();
+  if (ctr->overflow & kOverflowClusters) return;
   const uint32_t S = min(ctr->S, b.Scap);
-  const uint32_t K = min(ctr->K, static_cast<uint32_t>(kClusterBins));
+  const uint32_t K = min(ctr->K, b.Kcap);
   const uint32_t nch = (S + kChunk - 1) / kChunk;
+  const uint64_t hs = K > static_cast<uint32_t>(kClusterBins) ? nch : hstride;  // k_member_hist's layout
   const unsigned lane = lane_id();
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarp = (gridDim.x * blockDim.x) >> 5;
@@ -976,14 +990,14 @@ __global__ void k_member_hscan(Counters* ctr, SegBufs b, uint32_t hstride) {
     uint32_t run = b.kpoff[k];
     for (uint32_t c0 = 0; c0 < nch; c0 += 32) {
       const uint32_t c = c0 + lane;
-      const uint32_t v = c < nch ? b.H[k * hstride + c] : 0u;
+      const uint32_t v = c < nch ? b.H[k * hs + c] : 0u;
       uint32_t incl = v;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
         if (static_cast<int>(lane) >= o) incl += t;
       }
-      if (c < nch) b.H[k * hstride + c] = run + incl - v;
+      if (c < nch) b.H[k * hs + c] = run + incl - v;
       run += __shfl_sync(0xffffffffu, incl, 31);
     }
   }
@@ -991,14 +1005,21 @@ __global__ void k_member_hscan(Counters* ctr, SegBufs b, uint32_t hstride) {
 
 __global__ void k_member_scatter(Counters* ctr, SegBufs b, uint32_t hstride) {
   VP_GRID_WAIT();
-  __shared__ uint32_t run[kClusterBins];
+  __shared__ uint32_t run_s[kClusterBins];
+  if (ctr->overflow & kOverflowClusters) return;
   const uint32_t S = min(ctr->S, b.Scap);
-  const uint32_t K = min(ctr->K, static_cast<uint32_t>(kClusterBins));
+  const uint32_t K = min(ctr->K, b.Kcap);
   const uint32_t nch = (S + kChunk - 1) / kChunk;
   const bool ok = !(ctr->overflow & kOverflowMembers);
   const unsigned lane = lane_id();
+  // up to kClusterBins clusters: the chunk's running offsets in shared memory;
+  // more: in the chunk's column of H (this warp its only reader and writer)
+  const bool big = K > static_cast<uint32_t>(kClusterBins);
   for (uint32_t c = blockIdx.x; c < nch; c += gridDim.x) {
-    for (uint32_t k = lane; k < K; k += 32) run[k] = b.H[k * hstride + c];
+    uint32_t* run = big ? b.H + c : run_s;
+    const uint64_t step = big ? nch : 1u;
+    if (!big)
+      for (uint32_t k = lane; k < K; k += 32) run_s[k] = b.H[static_cast<uint64_t>(k) * hstride + c];
     __syncwarp();
     const uint32_t e1 = min(S, (c + 1) * kChunk);
     for (uint32_t e0 = c * kChunk; e0 < e1; e0 += 32) {
@@ -1006,9 +1027,9 @@ __global__ void k_member_scatter(Counters* ctr, SegBufs b, uint32_t hstride) {
       const int32_t k = e < e1 ? b.cid[b.label[e]] : -1;
       const unsigned peers = __match_any_sync(0xffffffffu, k);
       const int leader = __ffs(peers) - 1;
-      const uint32_t base = k >= 0 ? run[k] : 0u;
+      const uint32_t base = k >= 0 ? run[k * step] : 0u;
       __syncwarp();
-      if (k >= 0 && static_cast<int>(lane) == leader) run[k] = base + __popc(peers);
+      if (k >= 0 && static_cast<int>(lane) == leader) run[k * step] = base + __popc(peers);
       __syncwarp();
       if (k >= 0 && ok) {
         const uint32_t pos = base + __popc(peers & lanemask_lt());
@@ -1032,7 +1053,7 @@ __global__ void k_member_scatter(Counters* ctr, SegBufs b, uint32_t hstride) {
 // ---------------------------------------------------------------------------
 __global__ void k_ransac_hyp(Counters* ctr, RansacDev rp, SegBufs b) {
   VP_GRID_WAIT();
-  const uint32_t K = min(ctr->K, static_cast<uint32_t>(kClusterBins));
+  const uint32_t K = min(ctr->K, b.Kcap);
   const uint32_t I = static_cast<uint32_t>(rp.iterations);
   const uint64_t total = static_cast<uint64_t>(K) * I;
   if (ctr->overflow & kOverflowMembers) return;
@@ -1067,7 +1088,7 @@ __global__ void k_ransac_hyp(Counters* ctr, RansacDev rp, SegBufs b) {
 
 __global__ void k_ransac_count(Counters* ctr, RansacDev rp, SegBufs b) {
   VP_GRID_WAIT();
-  const uint32_t K = min(ctr->K, static_cast<uint32_t>(kClusterBins));
+  const uint32_t K = min(ctr->K, b.Kcap);
   if (K == 0 || (ctr->overflow & kOverflowMembers)) return;
   const uint32_t nseg = b.kpoff[K] >> 5;
   const uint32_t I = static_cast<uint32_t>(rp.iterations);
@@ -1124,7 +1145,7 @@ __global__ void k_ransac_count(Counters* ctr, RansacDev rp, SegBufs b) {
 
 __global__ void k_ransac_select(Counters* ctr, RansacDev rp, SegBufs b) {
   VP_GRID_WAIT();
-  const uint32_t K = min(ctr->K, static_cast<uint32_t>(kClusterBins));
+  const uint32_t K = min(ctr->K, b.Kcap);
   const int I = rp.iterations;
   const unsigned lane = lane_id();
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -1168,7 +1189,7 @@ __global__ void k_fit_setup(Counters* ctr, RansacDev rp, SegBufs b) {
   __shared__ uint32_t carry_f, carry_i, n_skip, n_unfit;
   if (threadIdx.x == 0) carry_f = carry_i = n_skip = n_unfit = 0;
   __syncthreads();
-  const uint32_t K = min(ctr->K, static_cast<uint32_t>(kClusterBins));
+  const uint32_t K = min(ctr->K, b.Kcap);
   for (uint32_t base = 0; base < K; base += blockDim.x) {
     const uint32_t k = base + threadIdx.x;
     int w = -3;
@@ -1360,7 +1381,7 @@ constexpr uint32_t kRefChunk = 4096;
 __global__ void k_refine_setup(Counters* ctr, SegBufs b, int refine) {
   VP_GRID_WAIT();
   __shared__ uint32_t carry;
-  const uint32_t F = min(ctr->nfits, static_cast<uint32_t>(kClusterBins));
+  const uint32_t F = min(ctr->nfits, b.Kcap);
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
   for (uint32_t base = 0; base < F; base += blockDim.x) {
@@ -1396,7 +1417,7 @@ __device__ __forceinline__ void refine_part_body(Counters* ctr, SegBufs b) {
   constexpr int B = 256;
   constexpr int NQ = kPass == 0 ? 3 : 6;
   __shared__ double red[NQ][B];
-  const uint32_t F = min(ctr->nfits, static_cast<uint32_t>(kClusterBins));
+  const uint32_t F = min(ctr->nfits, b.Kcap);
   if (ctr->overflow & (kOverflowFits | kOverflowMembers)) return;
   const uint32_t total = b.rch_off[F];
   for (uint32_t c = blockIdx.x; c < total; c += gridDim.x) {
@@ -1448,7 +1469,7 @@ __global__ void __launch_bounds__(256) k_refine_part1(Counters* ctr, SegBufs b) 
 // Per fit (one thread): centroid = (sum of chunk sums in chunk order) / n.
 __global__ void k_refine_cen(Counters* ctr, SegBufs b) {
   VP_GRID_WAIT();
-  const uint32_t F = min(ctr->nfits, static_cast<uint32_t>(kClusterBins));
+  const uint32_t F = min(ctr->nfits, b.Kcap);
   if (ctr->overflow & (kOverflowFits | kOverflowMembers)) return;
   for (uint32_t f = blockIdx.x * blockDim.x + threadIdx.x; f < F; f += gridDim.x * blockDim.x) {
     double s0 = 0.0, s1 = 0.0, s2 = 0.0;
@@ -1468,7 +1489,7 @@ __global__ void k_refine_cen(Counters* ctr, SegBufs b) {
 // (plane_fit.cpp:133-154); unrefined fits keep the RANSAC model.
 __global__ void k_refine_fin(Counters* ctr, SegBufs b, d3 up) {
   VP_GRID_WAIT();
-  const uint32_t F = min(ctr->nfits, static_cast<uint32_t>(kClusterBins));
+  const uint32_t F = min(ctr->nfits, b.Kcap);
   if (ctr->overflow & (kOverflowFits | kOverflowMembers)) return;
   for (uint32_t f = blockIdx.x * blockDim.x + threadIdx.x; f < F; f += gridDim.x * blockDim.x) {
     const double* init = b.fit_model + 4 * f;

@@ -266,7 +266,7 @@ __global__ void k_owner_prep(uint32_t n_own, uint32_t n_recv, int64_t own_base,
 // RANSAC seeds read them).
 __global__ void k_klabel_rebase(const Counters* ctr, SegBufs b, int64_t base) {
   VP_GRID_WAIT();
-  const uint32_t K = min(ctr->K, static_cast<uint32_t>(kClusterBins));
+  const uint32_t K = min(ctr->K, b.Kcap);
   for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < K; k += gridDim.x * blockDim.x)
     b.klabel[k] = static_cast<int32_t>(b.klabel[k] + base);
 }

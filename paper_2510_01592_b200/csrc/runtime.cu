@@ -268,10 +268,87 @@ struct Seg {
     bsum = dalloc<uint32_t>(2ull * need_bsum);
   }
 
+  // Cluster-count dependent buffers (clusters, members' padding, RANSAC
+  // candidates, fits, polygon records) sized by kcap; the member counting
+  // sort's chunk histogram by hcap. Grown by grow_k when a frame has more
+  // clusters (k_cluster_setup flags kOverflowClusters), keeping every other
+  // buffer -- the occupied and steppable lists stay valid for a chain re-run.
+  uint32_t kcap = kClusterBins;
+  uint64_t hcap = 0;
+  void release_k_buffers() {
+    void* ptrs[] = {b.klabel, b.ksize, b.kpoff, b.H, b.mx, b.my, b.mz, b.cand, b.cand_cnt, b.win_it, b.win_cnt,
+                    b.fid, b.fit_cluster, b.ioff, b.fch_off, b.ccount, b.fit_model, b.fit_meta, b.ref_model,
+                    b.rch_off, b.rpart, b.rcen, b.basis, b.pch_off, b.pext_dot, b.pext_idx, b.inner, b.ninner,
+                    b.nsurv, b.prec_d, b.prec_i};
+    for (void* p : ptrs)
+      if (p) cudaFree(p);
+    b.klabel = nullptr, b.ksize = nullptr, b.kpoff = nullptr, b.H = nullptr, b.mx = b.my = b.mz = nullptr;
+    b.cand = nullptr, b.cand_cnt = nullptr, b.win_it = b.win_cnt = b.fid = nullptr, b.fit_cluster = nullptr;
+    b.ioff = b.fch_off = b.ccount = nullptr, b.fit_model = nullptr, b.fit_meta = nullptr, b.ref_model = nullptr;
+    b.rch_off = nullptr, b.rpart = nullptr, b.rcen = nullptr, b.basis = nullptr, b.pch_off = nullptr;
+    b.pext_dot = nullptr, b.pext_idx = nullptr, b.inner = nullptr, b.ninner = b.nsurv = nullptr;
+    b.prec_d = nullptr, b.prec_i = nullptr;
+  }
+  void alloc_k_buffers(int iterations) {
+    const uint32_t K = kcap;
+    const uint32_t scap = b.Scap, icap = b.Icap;
+    const uint32_t mcap = scap + 32u * K;
+    b.Mcap = mcap;
+    b.Kcap = K;
+    cand_cap = static_cast<uint64_t>(std::max(iterations, 1)) * K;
+    b.klabel = dalloc<int32_t>(K);
+    b.ksize = dalloc<uint32_t>(K);
+    b.kpoff = dalloc<uint32_t>(K + 1);
+    hstride = (scap + kChunk - 1) / kChunk;
+    hcap = std::max<uint64_t>(hcap, static_cast<uint64_t>(std::min(K, static_cast<uint32_t>(kClusterBins))) * hstride);
+    b.H = dalloc<uint32_t>(hcap);
+    b.Hcap = hcap;
+    b.mx = dalloc<double>(mcap);
+    b.my = dalloc<double>(mcap);
+    b.mz = dalloc<double>(mcap);
+    b.cand = dalloc<double>(4 * cand_cap);
+    b.cand_cnt = dalloc<int32_t>(cand_cap);
+    b.win_it = dalloc<int32_t>(K);
+    b.win_cnt = dalloc<int32_t>(K);
+    b.fid = dalloc<int32_t>(K);
+    b.fit_cluster = dalloc<uint32_t>(K);
+    b.ioff = dalloc<uint32_t>(K + 1);
+    b.fch_off = dalloc<uint32_t>(K + 1);
+    b.cch_cap = mcap / kPolyChunk + K + 1;
+    b.ccount = dalloc<uint32_t>(b.cch_cap);
+    b.fit_model = dalloc<double>(4ull * K);
+    b.fit_meta = dalloc<int32_t>(2ull * K);
+    b.ref_model = dalloc<double>(4ull * K);
+    b.rch_off = dalloc<uint32_t>(K + 1);
+    b.rpart = dalloc<double>(8ull * (icap / 4096 + K + 1));
+    b.rcen = dalloc<double>(3ull * K);
+    b.basis = dalloc<double>(9ull * K);
+    b.pch_off = dalloc<uint32_t>(K + 1);
+    b.pch_cap = icap / kPolyChunk + K + 1;
+    b.pext_dot = dalloc<double>(64ull * b.pch_cap);
+    b.pext_idx = dalloc<int32_t>(64ull * b.pch_cap);
+    b.inner = dalloc<double>(2ull * 130 * K);
+    b.ninner = dalloc<uint32_t>(K);
+    b.nsurv = dalloc<uint32_t>(K);
+    b.prec_d = dalloc<double>(8ull * K);
+    b.prec_i = dalloc<int32_t>(4ull * K);
+  }
+  // more clusters than kcap, or a chunk histogram above hcap: K clusters over S
+  // steppable voxels (the counters of the overflowing frame)
+  void grow_k(uint32_t K, uint32_t S, int iterations) {
+    ++gen;
+    uint32_t k = kcap;
+    while (k < K) k *= 2;
+    const uint64_t nch = (static_cast<uint64_t>(S) + kChunk - 1) / kChunk;
+    hcap = std::max<uint64_t>(hcap, static_cast<uint64_t>(K) * nch);  // the member sort's chunk histogram
+    kcap = k;
+    release_k_buffers();
+    alloc_k_buffers(iterations);
+  }
+
   void ensure(uint32_t vcap, uint32_t scap, uint32_t icap, int iterations, uint64_t nwords) {
-    const uint32_t mcap = scap + 32u * kClusterBins;
     const bool need = !b.occ_list || vcap > b.Vcap || scap > b.Scap || icap > b.Icap ||
-                      static_cast<uint64_t>(iterations) * kClusterBins > cand_cap;
+                      static_cast<uint64_t>(iterations) * kcap > cand_cap;
     const uint64_t need_bsum = std::max<uint64_t>({(nwords + kRowsPerBlock - 1) / kRowsPerBlock,  // >= rows / tile
                                                    (vcap + kThreads - 1) / kThreads,
                                                    (scap + kScanPerBlock - 1) / kScanPerBlock}) + 1;
@@ -287,9 +364,7 @@ struct Seg {
       } unwind{this};
       b.Vcap = vcap;
       b.Scap = scap;
-      b.Mcap = mcap;
       b.Icap = icap;
-      cand_cap = static_cast<uint64_t>(std::max(iterations, 1)) * kClusterBins;
       b.occ_list = dalloc<uint32_t>(vcap);
       b.est_normal = dalloc<double>(3ull * vcap);
       b.est_ncount = dalloc<int32_t>(vcap);
@@ -307,44 +382,12 @@ struct Seg {
       b.cid = dalloc<int32_t>(scap);
       b.big_flag = dalloc<uint8_t>(scap);
       b.big_pos = dalloc<uint32_t>(scap);
-      b.klabel = dalloc<int32_t>(kClusterBins);
-      b.ksize = dalloc<uint32_t>(kClusterBins);
-      b.kpoff = dalloc<uint32_t>(kClusterBins + 1);
-      hstride = (scap + kChunk - 1) / kChunk;
-      b.H = dalloc<uint32_t>(static_cast<size_t>(kClusterBins) * hstride);
-      b.mx = dalloc<double>(mcap);
-      b.my = dalloc<double>(mcap);
-      b.mz = dalloc<double>(mcap);
-      b.cand = dalloc<double>(4 * cand_cap);
-      b.cand_cnt = dalloc<int32_t>(cand_cap);
-      b.win_it = dalloc<int32_t>(kClusterBins);
-      b.win_cnt = dalloc<int32_t>(kClusterBins);
-      b.fid = dalloc<int32_t>(kClusterBins);
-      b.fit_cluster = dalloc<uint32_t>(kClusterBins);
-      b.ioff = dalloc<uint32_t>(kClusterBins + 1);
-      b.fch_off = dalloc<uint32_t>(kClusterBins + 1);
-      b.cch_cap = mcap / kPolyChunk + kClusterBins + 1;
-      b.ccount = dalloc<uint32_t>(b.cch_cap);
-      b.fit_model = dalloc<double>(4 * kClusterBins);
-      b.fit_meta = dalloc<int32_t>(2 * kClusterBins);
-      b.ref_model = dalloc<double>(4 * kClusterBins);
-      b.rch_off = dalloc<uint32_t>(kClusterBins + 1);
-      b.rpart = dalloc<double>(8ull * (icap / 4096 + kClusterBins + 1));
-      b.rcen = dalloc<double>(3 * kClusterBins);
+      hcap = 0;  // re-derived from the new steppable capacity
+      alloc_k_buffers(iterations);
       b.inl = dalloc<double>(3ull * icap);
       b.proj = dalloc<double>(2ull * icap);
       b.surv = dalloc<double>(4ull * icap);
       b.hull = dalloc<double>(4ull * icap);
-      b.basis = dalloc<double>(9 * kClusterBins);
-      b.pch_off = dalloc<uint32_t>(kClusterBins + 1);
-      b.pch_cap = icap / kPolyChunk + kClusterBins + 1;
-      b.pext_dot = dalloc<double>(64ull * b.pch_cap);
-      b.pext_idx = dalloc<int32_t>(64ull * b.pch_cap);
-      b.inner = dalloc<double>(2ull * 130 * kClusterBins);
-      b.ninner = dalloc<uint32_t>(kClusterBins);
-      b.nsurv = dalloc<uint32_t>(kClusterBins);
-      b.prec_d = dalloc<double>(8 * kClusterBins);
-      b.prec_i = dalloc<int32_t>(4 * kClusterBins);
       b.pool_cap = icap;
       b.pool = dalloc<double>(5ull * icap);
       b.pair_cap = 2048;  // CCL root-pair set (load factor <= 1/2; overflow -> full union)
@@ -1133,7 +1176,7 @@ struct vp_grid {
   // reads the grid (cells, occupancy) -- everything that can overflow
   void launch_seg_a1(const vp_pipeline_params& p, bool timing) {
     const SegDev sd = make_segdev(p.seg, gd.res);
-    if (!capturing && static_cast<uint64_t>(p.ransac.iterations) * kClusterBins > seg.cand_cap)
+    if (!capturing && static_cast<uint64_t>(p.ransac.iterations) * seg.kcap > seg.cand_cap)
       seg.ensure(seg.b.Vcap, seg.b.Scap, seg.b.Icap, p.ransac.iterations, gd.nwords);
     if (timing) record(ev[1]);
     launch_occupied_scan();
@@ -1167,8 +1210,10 @@ struct vp_grid {
   bool grow_if_overflow(int iterations) {
     const uint32_t of = h_ctr->overflow;
     if (!of) return false;
-    if (of & kOverflowClusters)
-      fail(VP_ENOMEM, "more than 2048 clusters >= min_cluster_size in one frame");
+    if (of & kOverflowClusters) {  // more clusters: only the cluster-sized buffers grow
+      seg.grow_k(h_ctr->K, h_ctr->S, iterations);
+      if (of == kOverflowClusters) return true;
+    }
     uint32_t vcap = seg.b.Vcap, scap = seg.b.Scap, icap = seg.b.Icap;
     const uint64_t C = gd.ncells;
     if (of & kOverflowOcc) vcap = static_cast<uint32_t>(std::min<uint64_t>(C, std::max<uint64_t>(2ull * vcap, h_ctr->V)));
@@ -1183,8 +1228,8 @@ struct vp_grid {
   // Grow the buffers the CCL .. polygon chain writes after it overflowed,
   // keeping the grid readers' outputs (occupied and steppable lists) intact.
   void grow_chain(int iterations) {
-    (void)iterations;
-    fail(VP_ENOMEM, "segmentation chain capacity overflow");
+    if (h_ctr->overflow & ~kOverflowClusters) fail(VP_ENOMEM, "segmentation chain capacity overflow");
+    seg.grow_k(h_ctr->K, h_ctr->S, iterations);  // keeps the steppable list the chain re-runs from
   }
 
   // Download polygon records of the last segment() into host vectors.
@@ -1401,7 +1446,7 @@ bool pipeline_enqueue(vp_pipeline* pl, const float* xyz, uint64_t n, const doubl
   if (!is_valid_rotation(R))  // voxel_grid.cpp:60-61, 183-184
     fail(VP_EINVAL, "clear_rays: pose rotation is not orthonormal");
   g->ensure_points(n);
-  if (static_cast<uint64_t>(pl->p.ransac.iterations) * kClusterBins > g->seg.cand_cap)
+  if (static_cast<uint64_t>(pl->p.ransac.iterations) * g->seg.kcap > g->seg.cand_cap)
     g->seg.ensure(g->seg.b.Vcap, g->seg.b.Scap, g->seg.b.Icap, pl->p.ransac.iterations, g->gd.nwords);
   g->seg.ensure_dirs(16, g->stream);
   g->set_pose(R, t);
@@ -1576,7 +1621,7 @@ void pipeline_run(vp_pipeline* pl, size_t nf, const float* const* xyz, const uin
   g->use_seg(0);
   g->set_slot(0);
   g->ensure_points(maxn);
-  if (static_cast<uint64_t>(pl->p.ransac.iterations) * kClusterBins > g->seg.cand_cap)
+  if (static_cast<uint64_t>(pl->p.ransac.iterations) * g->seg.kcap > g->seg.cand_cap)
     g->seg.ensure(g->seg.b.Vcap, g->seg.b.Scap, g->seg.b.Icap, pl->p.ransac.iterations, g->gd.nwords);
   g->seg.ensure_dirs(16, g->stream);
   const int nslot = g->ensure_contexts(static_cast<int>(std::min<size_t>(kSlots, std::max<size_t>(nf, 1))),
@@ -1636,8 +1681,6 @@ void pipeline_run(vp_pipeline* pl, size_t nf, const float* const* xyz, const uin
       // the occupancy bound): grow its buffers, redo it from the slot's list
       if ((g->h_ctr->overflow & (kOverflowOcc | kOverflowStep)) || tries > 4)
         fail(VP_ENOMEM, "segmentation capacity overflow in a pipelined frame");
-      if (g->h_ctr->overflow & kOverflowClusters)
-        fail(VP_ENOMEM, "more than 2048 clusters >= min_cluster_size in one frame");
       g->grow_chain(pl->p.ransac.iterations);
       LAUNCH(k_chain_rearm, 1, 32, 0, g->stream, g->ctr);
       // the chain's CCL consumed (reset) the ordinal map: rebuild it from the list
@@ -3137,9 +3180,8 @@ int vp_segment_steppable(vp_grid* g, const vp_pipeline_params* p, uint64_t S, co
       g->launch_polygon(16, p->min_polygon_area);
       g->read_counters();
       if (!g->h_ctr->overflow || tries > 4) break;
-      if (g->h_ctr->overflow & kOverflowClusters)
-        fail(VP_ENOMEM, "more than 2048 clusters >= min_cluster_size in one frame");
-      g->seg.ensure(g->seg.b.Vcap, g->seg.b.Scap, 2 * g->seg.b.Icap, p->ransac.iterations, g->gd.nwords);
+      if (g->h_ctr->overflow & kOverflowClusters) g->seg.grow_k(g->h_ctr->K, g->h_ctr->S, p->ransac.iterations);
+      else g->seg.ensure(g->seg.b.Vcap, g->seg.b.Scap, 2 * g->seg.b.Icap, p->ransac.iterations, g->gd.nwords);
     }
     if (out) {
       HostPolys hp;
@@ -3826,7 +3868,7 @@ std::vector<uint8_t> build_trace(vp_grid* g, const Counters& c, uint32_t frame, 
   if (c.occupied == 0) {
     for (int k = 0; k < 7; ++k) w.put<uint64_t>(0);
   } else {
-    const uint32_t V = c.V, S = c.S, K = std::min<uint32_t>(c.K, kClusterBins), F = c.nfits;
+    const uint32_t V = c.V, S = c.S, K = std::min<uint32_t>(c.K, g->seg.b.Kcap), F = c.nfits;
     auto flat = d2h(g->seg.b.occ_list, V, g->stream);
     auto mean = d2h(g->seg.b.own_mean, 3ull * V, g->stream);
     auto cnt = d2h(g->seg.b.own_count, V, g->stream);

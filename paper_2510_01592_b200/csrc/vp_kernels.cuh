@@ -12,7 +12,7 @@ constexpr int kScanItems = 8;
 constexpr int kScanPerBlock = kScanThreads * kScanItems;  // 2048
 constexpr int kRowItems = 2;  // occupied scan: ring rows per thread
 constexpr int kRowsPerBlock = kScanThreads * kRowItems;  // 512
-constexpr int kClusterBins = 2048;  // clusters handled by the counting sort per pass
+constexpr int kClusterBins = 2048;  // initial cluster capacity; the member sort's shared-memory bins
 constexpr int kChunk = 256;         // ordinals per counting-sort chunk (one warp)
 #ifndef VP_HULL_SMEM
 #define VP_HULL_SMEM 1024
@@ -204,7 +204,7 @@ struct SegBufs {
   int32_t* cid;          // cluster index of a big root, else -1
   uint8_t* big_flag;
   uint32_t* big_pos;
-  // clusters (kClusterBins)
+  // clusters (Kcap)
   int32_t* klabel;       // cluster label (= root ordinal)
   uint32_t* ksize;
   uint32_t* kpoff;       // K+1 warp-padded member offsets
@@ -213,7 +213,7 @@ struct SegBufs {
   double* mx;
   double* my;
   double* mz;
-  // RANSAC candidates (kClusterBins x iterations)
+  // RANSAC candidates (Kcap x iterations)
   double* cand;          // 4 per candidate: n.x n.y n.z offset
   int32_t* cand_cnt;     // -1 degenerate
   int32_t* win_it;       // per cluster: winner, -1 unfit, -2 skipped small
@@ -234,7 +234,7 @@ struct SegBufs {
   double* proj;          // 2 * Icap
   double* surv;          // 2 * 2Icap
   double* hull;          // 2 * 2Icap
-  // polygon records (kClusterBins) + vertex pool
+  // polygon records (Kcap) + vertex pool
   double* basis;         // 9 per fit: u, v, origin (plane_basis)
   uint32_t* pch_off;     // per fit chunk offsets (nfits+1)
   double* pext_dot;      // 64 per chunk: per-direction extreme dot
@@ -248,6 +248,8 @@ struct SegBufs {
   double* pool;          // 5 per vertex: u v x y z
   uint32_t pool_cap;
   uint32_t Vcap, Scap, Mcap, Icap;
+  uint32_t Kcap;         // clusters a frame can hold (grown on kOverflowClusters)
+  uint64_t Hcap;         // entries of H (clusters x member-sort chunks)
   // CCL root-pair set: open-addressed keys (hi << 32 | lo, ~0 = empty) and the
   // list of occupied slots (pair_cap / 2 entries)
   unsigned long long* pair_key;

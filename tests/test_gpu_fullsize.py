@@ -15,9 +15,10 @@ run hands back its stage trace, which is compared with the reference's:
   list (labels, inlier counts).
 
 C5 (the multi-GPU map: fixed window, spatial slabs) runs through one slab
-and through four virtual slabs: slab output equals the one-slab output
-bitwise, and both match the reference's fixed-window run (steppable list
-bit-exact, polygons within tolerance).
+and through four virtual slabs driven by the library's vp_slab_frame (one
+host thread per slab): slab output equals the one-slab output bitwise, and
+both match the reference's fixed-window run (steppable list bit-exact,
+polygons within tolerance).
 """
 import os
 
@@ -121,7 +122,7 @@ def test_c5_slabs_vs_reference():
     for k, f in enumerate(wl.frames):
         pts = torch.from_numpy(np.ascontiguousarray(f.points)).cuda()
         pa = slabs.slab_frame([one], slabs.LocalComm(1), pts, f.rotation, f.translation, p)
-        pb = slabs.slab_frame(four, slabs.LocalComm(4), pts, f.rotation, f.translation, p)
+        pb = slabs.frame_local(four, pts, f.rotation, f.translation, p)  # the library-orchestrated frame
         assert format_polygons(pa) == format_polygons(pb), f"frame {k}: 4 slabs differ from one"
         tb = ref.frame(f.points, f.rotation, f.translation)
         S, (idx_t, mean_t, nrm_t) = one.steppable(p.seg)
