@@ -553,8 +553,8 @@ __global__ void __launch_bounds__(256) k_ccl_union_bal(Counters* ctr, SegDev sp,
 //                     per candidate (C2 frame 10: 2.4 M forward edges, 31 hook
 //                     trees, 11 components: ~20 distinct pairs);
 //  k_ccl_pairs_union  one block unions the listed root pairs (larger root
-//                     under smaller, so each root stays the component minimum);
-//  k_ccl_union_gated  the full edge-balanced union, only if the pair table
+//                     under smaller, so each root stays the component minimum),
+//                     or runs the full edge-balanced union if the pair table
 //                     overflowed.
 // k_ccl_flatten then resolves each voxel's root through the (short) root links.
 // ---------------------------------------------------------------------------
@@ -648,9 +648,12 @@ __global__ void __launch_bounds__(256) k_ccl_pairs(Counters* ctr, SegDev sp, Seg
   }
 }
 
-// One block: union of the listed root pairs, then the table is emptied.
-__global__ void __launch_bounds__(1024) k_ccl_pairs_union(Counters* ctr, SegBufs b) {
+// One block: union of the listed root pairs, then the table is emptied. If
+// the table overflowed, the block runs the full edge-balanced union instead
+// (slow -- one block -- but the table holds scap / 8 pairs: C2 frames have ~20).
+__global__ void __launch_bounds__(256) k_ccl_pairs_union(Counters* ctr, SegDev sp, SegBufs b, MapDesc m) {
   VP_GRID_WAIT();
+  if (ctr->pair_ovf) ccl_union_bal_body(ctr, sp, b, m);
   const uint32_t n = min(ctr->npairs, b.pair_cap >> 1);
   for (uint32_t t = threadIdx.x; t < n; t += blockDim.x) {
     const unsigned long long key = __ldcg(b.pair_key + b.pair_slot[t]);
@@ -664,12 +667,6 @@ __global__ void __launch_bounds__(1024) k_ccl_pairs_union(Counters* ctr, SegBufs
   }
 }
 
-// The full union (k_ccl_union_bal) when the pair table overflowed, else nothing.
-__global__ void __launch_bounds__(256) k_ccl_union_gated(Counters* ctr, SegDev sp, SegBufs b, MapDesc m) {
-  VP_GRID_WAIT();
-  if (!ctr->pair_ovf) return;
-  ccl_union_bal_body(ctr, sp, b, m);
-}
 
 // ---------------------------------------------------------------------------
 // Sampling CCL (Afforest-style) for large planar components:
@@ -2340,11 +2337,14 @@ __global__ void __cluster_dims__(kPolyCluster, 1, 1) __launch_bounds__(kPolyThre
 // then inlier_count, label, nv as doubles, 1 unused); Vt x 5 (u v x y z).
 __global__ void k_poly_pack(const Counters* ctr, SegBufs b, double* out, uint64_t cap) {
   VP_GRID_WAIT();
+  // the pack goes over PCIe (mapped pinned memory): every store is spread
+  // over the block so consecutive threads write consecutive doubles (the
+  // serial per-fit copy of round 1 took 34 us for ~10 KB)
   __shared__ uint32_t carry;
+  __shared__ uint32_t voff_s[1024];
   const uint32_t F = (ctr->overflow & (kOverflowFits | kOverflowMembers | kOverflowPool)) ? 0u : ctr->nfits;
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
-  uint64_t total = 0;
   for (uint32_t base = 0; base < F; base += blockDim.x) {
     const uint32_t f = base + threadIdx.x;
     const uint32_t nv = f < F ? static_cast<uint32_t>(max(b.prec_i[4 * f + 2], 0)) : 0u;
@@ -2352,24 +2352,36 @@ __global__ void k_poly_pack(const Counters* ctr, SegBufs b, double* out, uint64_
     const uint32_t c = carry;
     __syncthreads();
     if (threadIdx.x == blockDim.x - 1) carry = c + ex + nv;
+    voff_s[threadIdx.x] = c + ex;
     __syncthreads();
-    if (f < F) {
-      const uint64_t vo = 4 + 12ull * F + 5ull * (c + ex);
-      if (vo + 5ull * nv <= cap) {
-        double* r = out + 4 + 12ull * f;
-        const double* rd = b.prec_d + 8 * f;
-        const int32_t* ri = b.prec_i + 4 * f;
-        for (int q = 0; q < 5; ++q) r[q] = rd[q];
-        r[8] = static_cast<double>(ri[0]);
-        r[9] = static_cast<double>(ri[1]);
-        r[10] = static_cast<double>(nv);
-        const double* src = b.pool + 5ull * static_cast<uint32_t>(ri[3]);
-        for (uint32_t q = 0; q < 5 * nv; ++q) out[vo + q] = src[q];
-      }
+    // records: 12 doubles per fit, the fits of this batch side by side
+    const uint32_t nb = min(blockDim.x, F - base);
+    for (uint32_t e = threadIdx.x; e < 12 * nb; e += blockDim.x) {
+      const uint32_t ff = base + e / 12, q = e % 12;
+      const double* rd = b.prec_d + 8 * ff;
+      const int32_t* ri = b.prec_i + 4 * ff;
+      const uint32_t fnv = static_cast<uint32_t>(max(ri[2], 0));
+      double v = 0.0;
+      if (q < 5) v = rd[q];
+      else if (q == 8) v = static_cast<double>(ri[0]);
+      else if (q == 9) v = static_cast<double>(ri[1]);
+      else if (q == 10) v = static_cast<double>(fnv);
+      if (4 + 12ull * F + 5ull * (voff_s[e / 12] + fnv) <= cap) out[4 + 12ull * ff + q] = v;
     }
+    // vertices, one fit after the other, every thread on consecutive doubles
+    for (uint32_t j = 0; j < nb; ++j) {
+      const uint32_t ff = base + j;
+      const int32_t* ri = b.prec_i + 4 * ff;
+      const uint32_t fnv = static_cast<uint32_t>(max(ri[2], 0));
+      const uint64_t vo = 4 + 12ull * F + 5ull * voff_s[j];
+      if (vo + 5ull * fnv > cap) continue;
+      const double* src = b.pool + 5ull * static_cast<uint32_t>(ri[3]);
+      for (uint32_t q = threadIdx.x; q < 5 * fnv; q += blockDim.x) out[vo + q] = src[q];
+    }
+    __syncthreads();
   }
-  total = carry;
   if (threadIdx.x == 0) {
+    const uint64_t total = carry;
     out[0] = static_cast<double>(F);
     out[1] = static_cast<double>(total);
     out[2] = (4 + 12ull * F + 5ull * total > cap) ? 1.0 : 0.0;

@@ -1073,11 +1073,10 @@ struct vp_grid {
       if (g_ccl_jumps & 1) LAUNCH(k_ccl_jump, chain_wide, kThreads, 0, stream, ctr, sb);
       if (g_ccl_jumps & 2) LAUNCH(k_ccl_jump, chain_wide, kThreads, 0, stream, ctr, sb);
       LAUNCH(k_ccl_compress_exact, chain_wide, kThreads, 0, stream, ctr, sb);
-      // cross-tree edges as a root-pair set, unioned by one block (the full
-      // edge-balanced union only if the set overflowed)
+      // cross-tree edges as a root-pair set, unioned by one block (which runs
+      // the full edge-balanced union instead if the set overflowed)
       LAUNCH(k_ccl_pairs, chain_wide, 256, 0, stream, ctr, sd, sb, m);
-      LAUNCH(k_ccl_pairs_union, 1, 1024, 0, stream, ctr, sb);
-      LAUNCH(k_ccl_union_gated, chain_wide, 256, 0, stream, ctr, sd, sb, m);
+      LAUNCH(k_ccl_pairs_union, 1, 256, 0, stream, ctr, sd, sb, m);
     } else if (g_ccl_mode == 4) {
       // hook + compression + edge-balanced unions of every forward edge
       LAUNCH(k_ccl_hook_bal, chain_wide, 256, 0, stream, ctr, sd, sb, m);
@@ -1362,6 +1361,9 @@ struct vp_pipeline {
   cudaStream_t cstream = nullptr;  // host-to-device copies of upcoming frames
   // every frame's polygons, packed by k_poly_pack into mapped pinned memory
   double* pack_h[kSlots] = {};
+  // the single-frame path's pack (vp_pipeline_frame): no D2H round trip for the polygons
+  double* pack1_h = nullptr;
+  double* pack1_d = nullptr;
   double* pack_d[kSlots] = {};
   static constexpr uint64_t kPackCap = 1u << 17;  // doubles per slot (1 MiB)
   // host state of the frame occupying a slot (stage traces)
@@ -1386,6 +1388,7 @@ struct vp_pipeline {
       cudaStreamDestroy(cstream);
     }
     delete grid;  // drains the grid's streams
+    if (pack1_h) cudaFreeHost(pack1_h);
     for (auto* q : pack_h)
       if (q) cudaFreeHost(q);
   }
@@ -1404,6 +1407,8 @@ void enqueue_frame_work(vp_pipeline* pl, uint64_t n) {
   ck(cudaEventRecordWithFlags(g->ev[0], g->stream, evflag), "ev");
   g->launch_mapping_forked(n);  // walks || grouping, then clear (ray box), fold, recenter
   g->launch_segment(pl->p, true);
+  // the polygons straight into mapped pinned memory (read after the frame's sync)
+  LAUNCH(k_poly_pack, 1, 1024, 0, g->stream, g->ctr, g->seg.b, pl->pack1_d, vp_pipeline::kPackCap);
   ck(cudaMemcpyAsync(g->h_ctr, g->ctr, sizeof(Counters), cudaMemcpyDeviceToHost, g->stream), "ctr d2h");
 }
 
@@ -1453,6 +1458,10 @@ bool pipeline_enqueue(vp_pipeline* pl, const float* xyz, uint64_t n, const doubl
   g->fill_static_params();
   if (!pl->lat_ev[0])
     for (auto& e : pl->lat_ev) ck(cudaEventCreate(&e), "event");
+  if (!pl->pack1_h) {
+    ck(cudaHostAlloc(&pl->pack1_h, vp_pipeline::kPackCap * sizeof(double), cudaHostAllocMapped), "pinned");
+    ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&pl->pack1_d), pl->pack1_h, 0), "mapped");
+  }
   ck(cudaEventRecord(pl->lat_ev[0], g->stream), "event");  // before the points H2D
   stage_points(g, xyz, n, device_ptr);
   int32_t cell[3];
@@ -3557,11 +3566,12 @@ static int pipeline_frame_impl(vp_pipeline* pl, const float* xyz, uint64_t n, co
     pipeline_enqueue(pl, xyz, n, R, t, device_ptr, &ss);
     vp_grid* g = pl->grid;
     wait_frame(g);
-    if (g->h_ctr->overflow) rerun_segment_until_fits(g, pl->p);
+    const bool rerun = g->h_ctr->overflow != 0;
+    if (rerun) rerun_segment_until_fits(g, pl->p);
     fill_timing(g, timing, n);
     if (out) {
       HostPolys hp;
-      g->download_polygons(hp, false);
+      if (rerun || !unpack_polygons(pl->pack1_h, hp)) g->download_polygons(hp, false);
       *out = make_polygons_out(hp);
     }
     // the polygons are in host memory: the frame's end to end latency

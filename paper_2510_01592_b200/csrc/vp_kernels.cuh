@@ -363,8 +363,7 @@ __global__ void k_ccl_hook_bal(Counters* ctr, SegDev sp, SegBufs b, MapDesc m);
 __global__ void k_ccl_jump(Counters* ctr, SegBufs b);
 __global__ void k_ccl_compress_exact(Counters* ctr, SegBufs b);
 __global__ void k_ccl_pairs(Counters* ctr, SegDev sp, SegBufs b, MapDesc m);
-__global__ void k_ccl_pairs_union(Counters* ctr, SegBufs b);
-__global__ void k_ccl_union_gated(Counters* ctr, SegDev sp, SegBufs b, MapDesc m);
+__global__ void k_ccl_pairs_union(Counters* ctr, SegDev sp, SegBufs b, MapDesc m);
 __global__ void k_ccl_union_bal(Counters* ctr, SegDev sp, SegBufs b, MapDesc m);
 __global__ void k_ccl_hook(Counters* ctr, SegDev sp, SegBufs b, MapDesc m);
 __global__ void k_ccl_compress(Counters* ctr, SegBufs b);
