@@ -1869,7 +1869,27 @@ void fill_timing(vp_grid* g, vp_frame_timing* tm, uint64_t n) {
 
 // Re-run only the segmentation part after growing capacities.
 void rerun_segment_until_fits(vp_grid* g, const vp_pipeline_params& p) {
-  for (int tries = 0; tries < 6 && g->grow_if_overflow(p.ransac.iterations); ++tries) {
+  // the frame's mapping counters (ClearStats, UpdateStats, ShiftStats) are
+  // the first run's: a re-run of the segmentation must not reset them
+  const Counters map_ctr = *g->h_ctr;
+  for (int tries = 0; tries < 6; ++tries) {
+    const uint32_t of = g->h_ctr->overflow;
+    // only the chain (CCL .. polygons) overflowed: its buffers grow and it
+    // re-runs from the steppable list, like a pipelined frame's chain -- the
+    // grid readers already wrote this frame's statuses into the cells, so
+    // re-running them would read those instead of the pre-classify ones
+    const bool chain_only = of && !(of & (kOverflowOcc | kOverflowStep));
+    if (!g->grow_if_overflow(p.ransac.iterations)) break;
+    if (chain_only) {
+      LAUNCH(k_chain_rearm, 1, 32, 0, g->stream, g->ctr);
+      // the CCL's flatten consumed (reset) the ordinal map: rebuild it from the list
+      LAUNCH(k_map_fill, g->chain_wide, kThreads, 0, g->stream, g->ctr, g->seg.b, g->grid_map());
+      ck(cudaEventRecord(g->ev[2], g->stream), "ev");
+      g->launch_seg_a2(p, true);
+      g->launch_seg_b(p, true);
+      g->read_counters();
+      continue;
+    }
     // restore the post-map state: the recenter was already applied, so the
     // segmentation reads the post bitmap/offsets; make pre == post.
     for (int k = 0; k < 3; ++k) {
@@ -1881,15 +1901,16 @@ void rerun_segment_until_fits(vp_grid* g, const vp_pipeline_params& p) {
     g->h_fp->zb_pre = g->h_fp->zb_post;
     g->h_fp->do_shift = 0;
     g->h_fp->n = 0;
-    const unsigned long long occ = g->h_ctr->occupied;
     g->upload_params();
     g->reset_frame_counters();
     ck(cudaEventRecord(g->ev[0], g->stream), "ev");
     g->launch_segment(p, true);
     g->read_counters();
-    (void)occ;
   }
   if (g->h_ctr->overflow) fail(VP_ENOMEM, "segmentation capacity overflow persists");
+  Counters& c = *g->h_ctr;
+  c.cleared = map_ctr.cleared, c.freed = map_ctr.freed, c.touched = map_ctr.touched;
+  c.discarded = map_ctr.discarded, c.dropped = map_ctr.dropped, c.newly = map_ctr.newly;
 }
 
 struct TraceW {

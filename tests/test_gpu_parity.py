@@ -114,34 +114,48 @@ def test_ccl_pair_table_overflow_falls_back_to_full_union():
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-3000:]
 
 
-def many_patch_frame(n_side=50, spacing=0.06):
+def many_patch_frame(n_side=47, spacing=0.08):
     """One synthetic frame of n_side^2 separate 3x3-voxel floor patches
-    (2 points per voxel) seen from 1 m above: every patch is its own
+    (2 points per voxel) seen from 0.5 m above: every patch is its own
     steppable cluster (spacing > distance_th)."""
     from types import SimpleNamespace
     pts = []
     for i in range(n_side):
         for j in range(n_side):
-            cx, cy = -1.5 + spacing * i, -1.5 + spacing * j
+            cx, cy = -1.9 + spacing * i, -1.9 + spacing * j
             for dx in (-1, 0, 1):
                 for dy in (-1, 0, 1):
                     for q in (-0.002, 0.002):
                         pts.append((cx + 0.01 * dx + q, cy + 0.01 * dy - q, 0.004 + q))
-    t = np.array([0.0, 0.0, 1.0])
+    t = np.array([0.0, 0.0, 0.5])  # the window is centred on the first pose: z in [-0.1, 1.1)
     pts = np.asarray(pts, np.float64) - t
     return SimpleNamespace(points=np.ascontiguousarray(pts, np.float32), rotation=np.eye(3), translation=t)
 
 
 def test_more_clusters_than_initial_capacity():
-    # 2500 clusters in one frame (> the 2048 the buffers start with): the
+    # 2209 clusters in one frame (> the 2048 the buffers start with): the
     # cluster-sized buffers grow and the chain re-runs; the trace (clusters,
     # RANSAC fits, inlier sets, refined planes, polygons) equals the oracle's
     f = many_patch_frame()
     p = native.default_params(seed=3, refine_exact=True, min_area=1e-6)
     p.seg.min_cluster_size = 5
-    frames, gpu, ora = sessions([f, f], 0.01, (340, 340, 120), 3, params=p)
+    frames, gpu, ora = sessions([f, f], 0.01, (400, 400, 120), 3, params=p)
     t = check_bit_exact(frames, gpu, ora)
-    assert len(t.clusters) == 2500 and len(t.fits) == 2500 and len(t.polygons) > 2048
+    assert len(t.clusters) == 47 * 47 and len(t.fits) > 2048 and len(t.polygons) > 2048
+
+
+def test_more_clusters_than_capacity_pipelined():
+    # the same frames through vp_pipeline_run: the overflowing frame's chain is
+    # grown and re-run when its slot is harvested; traces equal the frame path
+    f = many_patch_frame()
+    p = native.default_params(seed=3, refine_exact=True, min_area=1e-6)
+    p.seg.min_cluster_size = 5
+    frames = [f, f, f]
+    a = native.Pipeline(0.01, (400, 400, 120), f.translation, p)
+    out = a.run_frames(frames, traces=True)
+    b = native.Pipeline(0.01, (400, 400, 120), f.translation, p)
+    for k, fr in enumerate(frames):
+        assert out["traces"][k] == b.frame_trace_raw(fr.points, fr.rotation, fr.translation), f"frame {k}"
 
 
 def hausdorff(a, b):
