@@ -1279,7 +1279,8 @@ __device__ __forceinline__ uint64_t ring_row_of(const GridDesc& g, const FramePa
 }
 
 __global__ void __launch_bounds__(kScanThreads) k_bitmap_count(GridDesc g, const FrameParams* __restrict__ fp,
-                                                               uint64_t r_lo, uint64_t nrows, uint32_t* bsum) {
+                                                               uint64_t r_lo, uint64_t nrows, uint32_t* bsum,
+                                                               Counters* ctr) {
   VP_GRID_WAIT();
   const uint64_t r0 = static_cast<uint64_t>(blockIdx.x) * kRowsPerBlock + static_cast<uint64_t>(threadIdx.x) * kRowItems;
   uint32_t c = 0;
@@ -1288,6 +1289,7 @@ __global__ void __launch_bounds__(kScanThreads) k_bitmap_count(GridDesc g, const
     if (r0 + k < nrows) c += __ldg(g.rowcnt + ring_row_of(g, fp, static_cast<uint32_t>(r_lo + r0 + k)));
   c = block_sum_u32(c);
   if (threadIdx.x == 0) bsum[blockIdx.x] = c;
+  if (last_block_done(&ctr->scan_done[0])) block_scan_array(bsum, gridDim.x, &ctr->V, nullptr);
 }
 
 // A non-empty row's ring words in logical z order: from ring word zb / 32
@@ -1339,7 +1341,7 @@ __global__ void __launch_bounds__(kScanThreads) k_bitmap_emit(GridDesc g, const 
 
 // Generic ordered compaction of u8 flags: positions[i] = exclusive rank.
 __global__ void k_flags_count(const uint8_t* __restrict__ flags, const uint32_t* n_ptr, uint32_t cap,
-                              uint32_t* bsum) {
+                              uint32_t* bsum, uint32_t* total, uint32_t* done) {
   VP_GRID_WAIT();
   const uint32_t n = min(*n_ptr, cap);
   const uint64_t i0 = (static_cast<uint64_t>(blockIdx.x) * kScanThreads + threadIdx.x) * kScanItems;
@@ -1349,6 +1351,7 @@ __global__ void k_flags_count(const uint8_t* __restrict__ flags, const uint32_t*
     if (i0 + k < n) c += flags[i0 + k] ? 1u : 0u;
   c = block_sum_u32(c);
   if (threadIdx.x == 0) bsum[blockIdx.x] = c;
+  if (last_block_done(done)) block_scan_array(bsum, gridDim.x, total, nullptr);
 }
 
 __global__ void k_flags_positions(const uint8_t* __restrict__ flags, const uint32_t* n_ptr,
@@ -1370,41 +1373,6 @@ __global__ void k_flags_positions(const uint8_t* __restrict__ flags, const uint3
       pos_out[i0 + k] = pos;
       pos += f[k] ? 1u : 0u;
     }
-}
-
-// Single-block exclusive scan of a[0..n) in place; *total = sum (optional
-// also copied to *total2).
-__device__ __forceinline__ void block_scan_array(uint32_t* a, uint32_t n, uint32_t* total, uint32_t* total2) {
-  __shared__ uint32_t carry;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  // kScanItems consecutive values per thread: one block pass per 8 K values
-  const uint32_t per = blockDim.x * kScanItems;
-  for (uint32_t b = 0; b < n; b += per) {
-    const uint32_t i0 = b + threadIdx.x * kScanItems;
-    uint32_t v[kScanItems];
-    uint32_t sum = 0;
-#pragma unroll
-    for (int k = 0; k < kScanItems; ++k) {
-      v[k] = i0 + k < n ? a[i0 + k] : 0u;
-      sum += v[k];
-    }
-    const uint32_t ex = block_exclusive_u32(sum);
-    uint32_t run = carry + ex;
-#pragma unroll
-    for (int k = 0; k < kScanItems; ++k)
-      if (i0 + k < n) {
-        a[i0 + k] = run;
-        run += v[k];
-      }
-    __syncthreads();
-    if (threadIdx.x == blockDim.x - 1) carry = run;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    if (total) *total = carry;
-    if (total2) *total2 = carry;
-  }
 }
 
 // n is read from n_ptr when non-null.

@@ -163,7 +163,7 @@ struct vp_frame_source {
   uint8_t* flag = nullptr;
   uint32_t* pos = nullptr;
   uint32_t* bsum = nullptr;
-  uint32_t* nbuf = nullptr;  // [0] rays (n_ptr of the scan), [1] hits
+  uint32_t* nbuf = nullptr;  // [0] rays (n_ptr of the scan), [1] hits, [2] blocks done (fused scan)
   uint32_t nblocks = 0;
   ~vp_frame_source() {
     if (stream) cudaStreamSynchronize(stream);
@@ -214,13 +214,13 @@ int vp_frame_source_create(const vp_box* boxes, size_t nb, const vp_rect* rects,
   s->pos = alloc<uint32_t>(rays);
   s->nblocks = static_cast<uint32_t>((rays + kScanPerBlock - 1) / kScanPerBlock);
   s->bsum = alloc<uint32_t>(s->nblocks + 1);
-  s->nbuf = alloc<uint32_t>(2);
+  s->nbuf = alloc<uint32_t>(3);
   ok = ok && s->boxes && s->rects && s->pattern && s->hits && s->out && s->flag && s->pos && s->bsum && s->nbuf;
   if (ok) {
-    const uint32_t nr32[2] = {static_cast<uint32_t>(rays), 0u};
+    const uint32_t nr32[3] = {static_cast<uint32_t>(rays), 0u, 0u};
     ok = cudaMemcpy(s->boxes, boxes, nb * sizeof(vp_box), cudaMemcpyHostToDevice) == cudaSuccess &&
          cudaMemcpy(s->rects, rects, nr * sizeof(vp_rect), cudaMemcpyHostToDevice) == cudaSuccess &&
-         cudaMemcpy(s->nbuf, nr32, 8, cudaMemcpyHostToDevice) == cudaSuccess &&
+         cudaMemcpy(s->nbuf, nr32, 12, cudaMemcpyHostToDevice) == cudaSuccess &&
          (pinhole || cudaMemcpy(s->pattern, sensor->pattern, 12 * rays, cudaMemcpyHostToDevice) == cudaSuccess);
   }
   if (!ok) {
@@ -252,9 +252,8 @@ int vp_frame_source_render(vp_frame_source* s, const double R[9], const double t
   const uint64_t rays = d.rays;
   const int grid = static_cast<int>(std::min<uint64_t>((rays + 255) / 256, 148ull * 16));
   k_render_rays<<<grid > 0 ? grid : 1, 256, 0, s->stream>>>(d, s->hits, s->flag);
-  k_flags_count<<<s->nblocks ? s->nblocks : 1, kScanThreads, 0, s->stream>>>(s->flag, s->nbuf, static_cast<uint32_t>(rays),
-                                                                            s->bsum);
-  k_scan_exclusive<<<1, 1024, 0, s->stream>>>(s->bsum, s->nblocks, nullptr, s->nbuf + 1, nullptr);
+  k_flags_count<<<s->nblocks ? s->nblocks : 1, kScanThreads, 0, s->stream>>>(
+      s->flag, s->nbuf, static_cast<uint32_t>(rays), s->bsum, s->nbuf + 1, s->nbuf + 2);  // + the block-sum scan
   k_flags_positions<<<s->nblocks ? s->nblocks : 1, kScanThreads, 0, s->stream>>>(
       s->flag, s->nbuf, static_cast<uint32_t>(rays), s->bsum, s->pos);
   k_render_compact<<<grid > 0 ? grid : 1, 256, 0, s->stream>>>(rays, s->hits, s->flag, s->pos, s->out);

@@ -149,6 +149,8 @@ __global__ void k_normals(GridDesc g, const FrameParams* __restrict__ fp, Counte
     const int c = __syncthreads_count(step);
     if (threadIdx.x == 0) tsum[t0 / blockDim.x] = static_cast<uint32_t>(c);
   }
+  // the last block scans the tile counts: tile offsets and ctr->S
+  if (last_block_done(&ctr->scan_done[1])) block_scan_array(tsum, (V + blockDim.x - 1) / blockDim.x, &ctr->S, nullptr);
 }
 
 // Steppable list in occupied (lexicographic) order -> ordinals; fills the

@@ -1022,8 +1022,7 @@ struct vp_grid {
     const uint64_t r_lo = static_cast<uint64_t>(gd.own_lo) * gd.ey;
     const uint64_t r_n = static_cast<uint64_t>(gd.own_hi - gd.own_lo) * gd.ey;
     const uint32_t nb = static_cast<uint32_t>((r_n + kRowsPerBlock - 1) / kRowsPerBlock);
-    LAUNCH(k_bitmap_count, nb, kScanThreads, 0, stream, gd, d_fp, r_lo, r_n, seg.bsum);
-    LAUNCH(k_scan_exclusive, 1, 1024, 0, stream, seg.bsum, nb, nullptr, &ctr->V, nullptr);
+    LAUNCH(k_bitmap_count, nb, kScanThreads, 0, stream, gd, d_fp, r_lo, r_n, seg.bsum, ctr);  // + scan
     LAUNCH(k_bitmap_emit, nb, kScanThreads, 0, stream, gd, d_fp, r_lo, r_n, seg.bsum, seg.b.occ_list,
            seg.b.Vcap);
   }
@@ -1033,8 +1032,7 @@ struct vp_grid {
                         uint32_t* total) {
     const uint32_t nb = (cap + kScanPerBlock - 1) / kScanPerBlock;
     uint32_t* bs = seg.bsum + seg.bsum_cap;
-    LAUNCH(k_flags_count, nb, kScanThreads, 0, stream, flags, n_ptr, cap, bs);
-    LAUNCH(k_scan_exclusive, 1, 1024, 0, stream, bs, nb, nullptr, total, nullptr);
+    LAUNCH(k_flags_count, nb, kScanThreads, 0, stream, flags, n_ptr, cap, bs, total, &ctr->scan_done[2]);  // + scan
     LAUNCH(k_flags_positions, nb, kScanThreads, 0, stream, flags, n_ptr, cap, bs, pos);
   }
 
@@ -1055,8 +1053,7 @@ struct vp_grid {
   // the tile offsets and ctr->S)
   void launch_classify(const SegDev& sd, int write_status) {
     uint32_t* ts = seg.bsum + seg.bsum_cap;
-    LAUNCH(k_normals, kWide, kThreads, 0, stream, gd, d_fp, ctr, sd, seg.b, write_status, ts);
-    LAUNCH(k_scan_tiles, 1, 1024, 0, stream, ts, &ctr->V, seg.b.Vcap, static_cast<uint32_t>(kThreads), &ctr->S);
+    LAUNCH(k_normals, kWide, kThreads, 0, stream, gd, d_fp, ctr, sd, seg.b, write_status, ts);  // + tile scan
   }
   // the steppable list at the ordinals of launch_classify's tile offsets
   void launch_step_emit(const MapDesc& m, int xadd = 0) {

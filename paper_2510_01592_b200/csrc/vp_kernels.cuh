@@ -61,6 +61,58 @@ __device__ __forceinline__ uint32_t block_exclusive_u32(uint32_t v) {
   return r;
 }
 
+// Single-block exclusive scan of a[0..n) in place; *total = sum (optional
+// also copied to *total2).
+__device__ __forceinline__ void block_scan_array(uint32_t* a, uint32_t n, uint32_t* total, uint32_t* total2) {
+  __shared__ uint32_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  // kScanItems consecutive values per thread: one block pass per 8 K values
+  const uint32_t per = blockDim.x * kScanItems;
+  for (uint32_t b = 0; b < n; b += per) {
+    const uint32_t i0 = b + threadIdx.x * kScanItems;
+    uint32_t v[kScanItems];
+    uint32_t sum = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+      v[k] = i0 + k < n ? __ldcg(a + i0 + k) : 0u;
+      sum += v[k];
+    }
+    const uint32_t ex = block_exclusive_u32(sum);
+    uint32_t run = carry + ex;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k)
+      if (i0 + k < n) {
+        a[i0 + k] = run;
+        run += v[k];
+      }
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = run;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    if (total) *total = carry;
+    if (total2) *total2 = carry;
+  }
+}
+
+// True in the block that finishes last (every block of the grid must call
+// it, after writing its results): the fused count kernels then scan the
+// per-block sums in that block instead of a separate single-block launch.
+// `done` is reset by that block.
+__device__ __forceinline__ bool last_block_done(uint32_t* done) {
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    last = atomicAdd(done, 1u) == gridDim.x - 1;
+    if (last) *done = 0u;
+  }
+  __syncthreads();
+  if (last) __threadfence();
+  return last;
+}
+
 __device__ __forceinline__ uint32_t block_sum_u32(uint32_t v) {
   __shared__ uint32_t ws[32];
   __shared__ uint32_t tot;
@@ -337,12 +389,13 @@ __global__ void k_frame_begin(Counters* ctr, const unsigned long long* occ_total
 __global__ void k_set_statuses(GridDesc g, const FrameParams* fp, const int32_t* idx, const uint8_t* st,
                                uint64_t n);
 __global__ void k_flags_count(const uint8_t* flags, const uint32_t* n_ptr, uint32_t cap,
-                              uint32_t* bsum);
+                              uint32_t* bsum, uint32_t* total, uint32_t* done);
 __global__ void k_flags_positions(const uint8_t* flags, const uint32_t* n_ptr, uint32_t cap,
                                   const uint32_t* boff, uint32_t* pos_out);
 __global__ void k_merge_point(GridDesc g, const FrameParams* fp, Counters* ctr, int x, int y, int z,
                               double px, double py, double pz);
-__global__ void k_bitmap_count(GridDesc g, const FrameParams* fp, uint64_t w_lo, uint64_t nwords, uint32_t* bsum);
+__global__ void k_bitmap_count(GridDesc g, const FrameParams* fp, uint64_t w_lo, uint64_t nwords, uint32_t* bsum,
+                               Counters* ctr);
 __global__ void k_bitmap_emit(GridDesc g, const FrameParams* fp, uint64_t w_lo, uint64_t nwords,
                               const uint32_t* boff, uint32_t* out, uint32_t cap);
 __global__ void k_scan_exclusive(uint32_t* a, uint32_t n_static, const uint32_t* n_ptr,
