@@ -1094,7 +1094,11 @@ __global__ void k_ransac_count(Counters* ctr, RansacDev rp, SegBufs b) {
   const unsigned lane = lane_id();
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarp = (gridDim.x * blockDim.x) >> 5;
-  for (uint32_t sg = warp; sg < nseg; sg += nwarp) {
+  // one warp per (32-member segment, 32 candidates): C2's ~850 segments x 100
+  // candidates as ~3400 independent warps instead of 850 long loops
+  const uint32_t ncb = (I + 31) >> 5;
+  for (uint32_t wi = warp; wi < nseg * ncb; wi += nwarp) {
+    const uint32_t sg = wi / ncb, cb = wi - sg * ncb;
     const uint32_t start = sg << 5;
     uint32_t lo = 0, hi = K;  // largest k with kpoff[k] <= start
     while (hi - lo > 1) {
@@ -1109,7 +1113,8 @@ __global__ void k_ransac_count(Counters* ctr, RansacDev rp, SegBufs b) {
     const d3 p = in ? mk3(b.mx[start + lane], b.my[start + lane], b.mz[start + lane])
                     : mk3(0.0, 0.0, 0.0);
     const uint64_t cbase = static_cast<uint64_t>(k) * I;
-    for (uint32_t c0 = 0; c0 < I; c0 += 32) {
+    {
+      const uint32_t c0 = cb << 5;
       // candidate c0 + lane held by this lane, broadcast by shuffles
       const uint32_t mine_t = c0 + lane;
       int valid = 0;
@@ -1374,7 +1379,7 @@ __global__ void k_refine(Counters* ctr, SegBufs b, d3 up, int refine, int exact)
 // (one block each) reduce in a fixed-shape tree; each fit then sums its chunk
 // partials in chunk order. Deterministic; within the north_star tolerance of
 // the reference's sequential sums.
-constexpr uint32_t kRefChunk = 4096;
+constexpr uint32_t kRefChunk = kRefineChunk;  // 512: C2's ~3 k-inlier fits spread over ~60 blocks instead of ~9
 
 // Single block: per fit chunk offsets (fits that are not refined get none).
 __global__ void k_refine_setup(Counters* ctr, SegBufs b, int refine) {
@@ -1460,22 +1465,35 @@ __device__ __forceinline__ void refine_part_body(Counters* ctr, SegBufs b) {
   }
 }
 
+__device__ __forceinline__ void refine_cen_body(const Counters* ctr, const SegBufs& b);
+__device__ __forceinline__ void refine_fin_body(const Counters* ctr, const SegBufs& b, d3 up);
+
+// Each pass's last block to finish runs the per-fit step that needs all of
+// the fit's chunk partials: centroids after pass 0, covariance -> Jacobi ->
+// model after pass 1 (one launch each fewer).
 __global__ void __launch_bounds__(256) k_refine_part0(Counters* ctr, SegBufs b) {
-  VP_GRID_WAIT(); refine_part_body<0>(ctr, b); }
-__global__ void __launch_bounds__(256) k_refine_part1(Counters* ctr, SegBufs b) {
-  VP_GRID_WAIT(); refine_part_body<1>(ctr, b); }
+  VP_GRID_WAIT();
+  refine_part_body<0>(ctr, b);
+  if (last_block_done(&ctr->scan_done[3]) && !(ctr->overflow & (kOverflowFits | kOverflowMembers)))
+    refine_cen_body(ctr, b);
+}
+__global__ void __launch_bounds__(256) k_refine_part1(Counters* ctr, SegBufs b, d3 up) {
+  VP_GRID_WAIT();
+  refine_part_body<1>(ctr, b);
+  if (last_block_done(&ctr->scan_done[4]) && !(ctr->overflow & (kOverflowFits | kOverflowMembers)))
+    refine_fin_body(ctr, b, up);
+}
 
 // Per fit (one thread): centroid = (sum of chunk sums in chunk order) / n.
-__global__ void k_refine_cen(Counters* ctr, SegBufs b) {
-  VP_GRID_WAIT();
+// (a block-strided loop over the fits: run by the last block of pass 0)
+__device__ __forceinline__ void refine_cen_body(const Counters* ctr, const SegBufs& b) {
   const uint32_t F = min(ctr->nfits, b.Kcap);
-  if (ctr->overflow & (kOverflowFits | kOverflowMembers)) return;
-  for (uint32_t f = blockIdx.x * blockDim.x + threadIdx.x; f < F; f += gridDim.x * blockDim.x) {
+  for (uint32_t f = threadIdx.x; f < F; f += blockDim.x) {
     double s0 = 0.0, s1 = 0.0, s2 = 0.0;
     for (uint32_t c = b.rch_off[f]; c < b.rch_off[f + 1]; ++c) {
-      s0 += b.rpart[8ull * c];
-      s1 += b.rpart[8ull * c + 1];
-      s2 += b.rpart[8ull * c + 2];
+      s0 += __ldcg(b.rpart + 8ull * c);
+      s1 += __ldcg(b.rpart + 8ull * c + 1);
+      s2 += __ldcg(b.rpart + 8ull * c + 2);
     }
     const double dn = static_cast<double>(b.ioff[f + 1] - b.ioff[f]);
     b.rcen[3 * f] = s0 / dn;
@@ -1486,11 +1504,10 @@ __global__ void k_refine_cen(Counters* ctr, SegBufs b) {
 
 // Per fit (one thread): covariance / n -> Jacobi -> rank gate -> orient_up
 // (plane_fit.cpp:133-154); unrefined fits keep the RANSAC model.
-__global__ void k_refine_fin(Counters* ctr, SegBufs b, d3 up) {
-  VP_GRID_WAIT();
+// (run by the last block of pass 1)
+__device__ __forceinline__ void refine_fin_body(const Counters* ctr, const SegBufs& b, d3 up) {
   const uint32_t F = min(ctr->nfits, b.Kcap);
-  if (ctr->overflow & (kOverflowFits | kOverflowMembers)) return;
-  for (uint32_t f = blockIdx.x * blockDim.x + threadIdx.x; f < F; f += gridDim.x * blockDim.x) {
+  for (uint32_t f = threadIdx.x; f < F; f += blockDim.x) {
     const double* init = b.fit_model + 4 * f;
     double* out = b.ref_model + 4 * f;
     if (b.rch_off[f] == b.rch_off[f + 1]) {
@@ -1501,7 +1518,7 @@ __global__ void k_refine_fin(Counters* ctr, SegBufs b, d3 up) {
     double a[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     for (uint32_t c = b.rch_off[f]; c < b.rch_off[f + 1]; ++c)
 #pragma unroll
-      for (int k = 0; k < 6; ++k) a[k] += b.rpart[8ull * c + k];
+      for (int k = 0; k < 6; ++k) a[k] += __ldcg(b.rpart + 8ull * c + k);
     const double dn = static_cast<double>(b.ioff[f + 1] - b.ioff[f]);
     double cv[3][3];
     cv[0][0] = a[0] / dn;

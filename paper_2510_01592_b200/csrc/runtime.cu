@@ -320,7 +320,7 @@ struct Seg {
     b.fit_meta = dalloc<int32_t>(2ull * K);
     b.ref_model = dalloc<double>(4ull * K);
     b.rch_off = dalloc<uint32_t>(K + 1);
-    b.rpart = dalloc<double>(8ull * (icap / 4096 + K + 1));
+    b.rpart = dalloc<double>(8ull * (icap / kRefineChunk + K + 1));
     b.rcen = dalloc<double>(3ull * K);
     b.basis = dalloc<double>(9ull * K);
     b.pch_off = dalloc<uint32_t>(K + 1);
@@ -1134,12 +1134,10 @@ struct vp_grid {
       return;
     }
     LAUNCH(k_refine_setup, 1, 1024, 0, stream, ctr, seg.b, refine);
-    LAUNCH(k_refine_part0, 148 * 4, 256, 0, stream, ctr, seg.b);
-    LAUNCH(k_refine_cen, 8, 256, 0, stream, ctr, seg.b);
-    LAUNCH(k_refine_part1, 148 * 4, 256, 0, stream, ctr, seg.b);
-    LAUNCH(k_refine_fin, 8, 256, 0, stream, ctr, seg.b, u);
+    LAUNCH(k_refine_part0, 148 * 4, 256, 0, stream, ctr, seg.b);     // + centroids (last block)
+    LAUNCH(k_refine_part1, 148 * 4, 256, 0, stream, ctr, seg.b, u);  // + covariance, Jacobi, model
   }
-  // make_polygon for every fit: one 8-CTA cluster per fit (k_poly_fused;
+  // make_polygon for every fit: one 4-CTA cluster per fit (k_poly_fused;
   // VP_POLY_SPLIT=1 runs the five-kernel form setup/extremes/inner/keep/hull)
   void launch_polygon(int dirs, double min_area, int planar = 0) {
     seg.ensure_dirs(dirs, stream);

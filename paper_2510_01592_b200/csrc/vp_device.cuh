@@ -123,7 +123,7 @@ struct Counters {
   uint32_t nmedium;      // integrate groups with kFoldSmall < points <= kFoldMax (k_integrate_fold_medium)
   int32_t box_lo[3];     // cells the frame's rays can mark (clamped end-point and
   int32_t box_hi[3];     // sensor cells, k_integrate_hash): k_clear_apply's sweep box
-  uint32_t scan_done[4]; // blocks finished per fused count+scan kernel (the last one scans; reset by it)
+  uint32_t scan_done[8]; // blocks finished per kernel with a last-block step (reset by that block)
   uint32_t npairs;       // CCL: distinct adjacent root pairs listed by k_ccl_pairs
   uint32_t pair_ovf;     // CCL: the pair table overflowed -> k_ccl_union_bal runs the full union
 };

@@ -24,6 +24,7 @@ static_assert(kHullSmem >= 256 && kHullSmem % 256 == 0 && kHullSmem / 256 <= 32 
                   kHullSmem * 16 * 6 <= 227 * 1024,
               "VP_HULL_SMEM must be a multiple of 256 in [256, 2304]");
 constexpr int kPolyChunk = 1024;    // inlier points per polygon-stage block
+constexpr uint32_t kRefineChunk = 512;  // inliers per refine_plane tree chunk (one block each)
 constexpr int kPolyCluster = 4;     // k_poly_fused: CTAs per fit (one thread-block cluster)
 constexpr int kPolySmem = 4 * kHullSmem * 16;  // k_poly_fused dynamic shared memory (4 x kHullSmem points)
 #ifndef VP_FOLD_SMALL
@@ -439,9 +440,7 @@ __global__ void k_extract_emit(Counters* ctr, RansacDev rp, SegBufs b);
 __global__ void k_refine(Counters* ctr, SegBufs b, d3 up, int refine, int exact);
 __global__ void k_refine_setup(Counters* ctr, SegBufs b, int refine);
 __global__ void k_refine_part0(Counters* ctr, SegBufs b);
-__global__ void k_refine_part1(Counters* ctr, SegBufs b);
-__global__ void k_refine_cen(Counters* ctr, SegBufs b);
-__global__ void k_refine_fin(Counters* ctr, SegBufs b, d3 up);
+__global__ void k_refine_part1(Counters* ctr, SegBufs b, d3 up);
 __global__ void k_poly_setup(Counters* ctr, SegBufs b);
 __global__ void k_poly_extremes(Counters* ctr, SegBufs b, const double* dirtab, int directions, int planar);
 __global__ void k_poly_fused(Counters* ctr, SegBufs b, const double* dirtab, int directions, int planar, double min_area);
