@@ -1141,9 +1141,25 @@ __global__ void k_clear_apply(GridDesc g, const FrameParams* __restrict__ fp, Co
 // the positions that re-enter the window are empty (voxels_dropped counted).
 // Rows that neither leave nor shift in z are not read at all.
 // ---------------------------------------------------------------------------
-__global__ void k_recenter(GridDesc g, const FrameParams* __restrict__ fp, Counters* ctr) {
+__device__ __forceinline__ void recenter_body(const GridDesc& g, const FrameParams* __restrict__ fp, Counters* ctr);
+
+// occ_total != nullptr: the last block also finishes the frame's mapping
+// (k_map_finalize's occupied bookkeeping), one launch fewer.
+__device__ __forceinline__ void map_finalize_body(Counters* ctr, unsigned long long* occ_total) {
+  const unsigned long long o = __ldcg(occ_total) + __ldcg(&ctr->newly) - __ldcg(&ctr->freed) - __ldcg(&ctr->dropped);
+  *occ_total = o;
+  ctr->occupied = o;
+  ctr->touched = __ldcg(&ctr->ngroups);
+}
+
+__global__ void k_recenter(GridDesc g, const FrameParams* __restrict__ fp, Counters* ctr,
+                           unsigned long long* occ_total) {
   VP_GRID_WAIT();
-  if (!fp->do_shift) return;
+  if (fp->do_shift) recenter_body(g, fp, ctr);
+  if (occ_total && last_block_done(&ctr->scan_done[7]) && threadIdx.x == 0) map_finalize_body(ctr, occ_total);
+}
+
+__device__ __forceinline__ void recenter_body(const GridDesc& g, const FrameParams* __restrict__ fp, Counters* ctr) {
   uint32_t* occ = fp->occ_pre;
   const int sx = fp->shift[0], sy = fp->shift[1], sz = fp->shift[2];
   const int ex = g.ex, ey = g.ey, ez = g.ez, W = g.W, Wz = g.W << 5;
@@ -1226,10 +1242,7 @@ __global__ void k_set_statuses(GridDesc g, const FrameParams* __restrict__ fp, c
 
 __global__ void k_map_finalize(Counters* ctr, unsigned long long* occ_total) {
   VP_GRID_WAIT();
-  const unsigned long long o = *occ_total + ctr->newly - ctr->freed - ctr->dropped;
-  *occ_total = o;
-  ctr->occupied = o;
-  ctr->touched = ctr->ngroups;
+  map_finalize_body(ctr, occ_total);
 }
 
 // Per-frame counter reset (one slot); occupied carries VoxelGrid::occupied_.

@@ -895,6 +895,8 @@ __global__ void k_cluster_flags(Counters* ctr, SegDev sp, SegBufs b) {
                         : 0;
 }
 
+__device__ __forceinline__ void cluster_setup_body(Counters* ctr, const SegBufs& b);
+
 __global__ void k_cluster_assign(Counters* ctr, SegBufs b) {
   VP_GRID_WAIT();
   const uint32_t S = min(ctr->S, b.Scap);
@@ -906,11 +908,12 @@ __global__ void k_cluster_assign(Counters* ctr, SegBufs b) {
       b.cid[i] = static_cast<int32_t>(k);
     }
   }
+  if (last_block_done(&ctr->scan_done[5])) cluster_setup_body(ctr, b);  // sizes, member offsets
 }
 
-// Single block: sizes and warp-padded member offsets of the K clusters.
-__global__ void k_cluster_setup(Counters* ctr, SegBufs b) {
-  VP_GRID_WAIT();
+// Single block: sizes and warp-padded member offsets of the K clusters (the
+// last block of k_cluster_assign).
+__device__ __forceinline__ void cluster_setup_body(Counters* ctr, const SegBufs& b) {
   __shared__ uint32_t carry;
   if (threadIdx.x == 0) {
     carry = 0;
@@ -1147,8 +1150,16 @@ __global__ void k_ransac_count(Counters* ctr, RansacDev rp, SegBufs b) {
   }
 }
 
+__device__ __forceinline__ void fit_setup_body(Counters* ctr, const RansacDev& rp, const SegBufs& b);
+__device__ __forceinline__ void ransac_select_body(Counters* ctr, const RansacDev& rp, const SegBufs& b);
+
 __global__ void k_ransac_select(Counters* ctr, RansacDev rp, SegBufs b) {
   VP_GRID_WAIT();
+  ransac_select_body(ctr, rp, b);
+  if (last_block_done(&ctr->scan_done[6])) fit_setup_body(ctr, rp, b);  // fit list, inlier offsets
+}
+
+__device__ __forceinline__ void ransac_select_body(Counters* ctr, const RansacDev& rp, const SegBufs& b) {
   const uint32_t K = min(ctr->K, b.Kcap);
   const int I = rp.iterations;
   const unsigned lane = lane_id();
@@ -1187,9 +1198,9 @@ __global__ void k_ransac_select(Counters* ctr, RansacDev rp, SegBufs b) {
   }
 }
 
-// Single block: fit list in cluster order, inlier offsets, FitStats.
-__global__ void k_fit_setup(Counters* ctr, RansacDev rp, SegBufs b) {
-  VP_GRID_WAIT();
+// Single block: fit list in cluster order, inlier offsets, FitStats (the last
+// block of k_ransac_select).
+__device__ __forceinline__ void fit_setup_body(Counters* ctr, const RansacDev& rp, const SegBufs& b) {
   __shared__ uint32_t carry_f, carry_i, n_skip, n_unfit;
   if (threadIdx.x == 0) carry_f = carry_i = n_skip = n_unfit = 0;
   __syncthreads();

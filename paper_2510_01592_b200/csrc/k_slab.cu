@@ -262,7 +262,7 @@ __global__ void k_owner_prep(uint32_t n_own, uint32_t n_recv, int64_t own_base,
   }
 }
 
-// Cluster labels back to global ordinals (after k_cluster_setup, before the
+// Cluster labels back to global ordinals (after the cluster setup, before the
 // RANSAC seeds read them).
 __global__ void k_klabel_rebase(const Counters* ctr, SegBufs b, int64_t base) {
   VP_GRID_WAIT();

@@ -271,7 +271,7 @@ struct Seg {
   // Cluster-count dependent buffers (clusters, members' padding, RANSAC
   // candidates, fits, polygon records) sized by kcap; the member counting
   // sort's chunk histogram by hcap. Grown by grow_k when a frame has more
-  // clusters (k_cluster_setup flags kOverflowClusters), keeping every other
+  // clusters (the cluster setup flags kOverflowClusters), keeping every other
   // buffer -- the occupied and steppable lists stay valid for a chain re-run.
   uint32_t kcap = kClusterBins;
   uint64_t hcap = 0;
@@ -987,9 +987,10 @@ struct vp_grid {
     LAUNCH(k_integrate_fold, gp, kThreads, 0, lstream, gd, d_fp, ctr, groups, hkey, hcnt, hoff, sorted);
     ck(cudaStreamWaitEvent(lstream, fork_ev[3], 0), "join");
   }
-  void launch_recenter() {
-    // (the tile counts go to the active segmentation context's scan sums)
-    LAUNCH(k_recenter, grid_for(static_cast<uint64_t>(gd.ex) * gd.ey), kThreads, 0, lstream, gd, d_fp, ctr);
+  // finalize: the last block also does k_map_finalize's bookkeeping
+  void launch_recenter(bool finalize = false) {
+    LAUNCH(k_recenter, grid_for(static_cast<uint64_t>(gd.ex) * gd.ey), kThreads, 0, lstream, gd, d_fp, ctr,
+           finalize ? occ_total : nullptr);
   }
   void launch_finalize() { LAUNCH(k_map_finalize, 1, 1, 0, lstream, ctr, occ_total); }
   // clear_rays and the grouping half of integrate_frame in parallel (fork
@@ -1012,8 +1013,7 @@ struct vp_grid {
   void launch_mapping_post(uint64_t n) {
     launch_clear_apply(n, 1);
     launch_integrate_fold(n);
-    launch_recenter();
-    launch_finalize();
+    launch_recenter(true);  // + finalize
   }
 
   // Occupied scan of the post-recenter bitmap into seg.b.occ_list; ctr->V.
@@ -1106,8 +1106,7 @@ struct vp_grid {
   void launch_clusters(const SegDev& sd, int64_t label_base = 0) {
     LAUNCH(k_cluster_flags, chain_wide, kThreads, 0, stream, ctr, sd, seg.b);
     launch_flag_scan(seg.b.big_flag, &ctr->S, seg.b.Scap, seg.b.big_pos, &ctr->K);
-    LAUNCH(k_cluster_assign, chain_wide, kThreads, 0, stream, ctr, seg.b);
-    LAUNCH(k_cluster_setup, 1, 1024, 0, stream, ctr, seg.b);
+    LAUNCH(k_cluster_assign, chain_wide, kThreads, 0, stream, ctr, seg.b);  // + cluster setup (last block)
     if (label_base) LAUNCH(k_klabel_rebase, 8, 256, 0, stream, ctr, seg.b, label_base);
     const int nch = static_cast<int>(seg.hstride);
     LAUNCH(k_member_hist, std::min(nch, 148 * 16), 32, 0, stream, ctr, seg.b, seg.hstride);
@@ -1121,8 +1120,7 @@ struct vp_grid {
   void launch_ransac(const RansacDev& rd, Counters* c, const SegBufs& b) {
     LAUNCH(k_ransac_hyp, chain_wide, kThreads, 0, stream, c, rd, b);
     LAUNCH(k_ransac_count, chain_wide, kThreads, 0, stream, c, rd, b);
-    LAUNCH(k_ransac_select, chain_wide, kThreads, 0, stream, c, rd, b);
-    LAUNCH(k_fit_setup, 1, 1024, 0, stream, c, rd, b);
+    LAUNCH(k_ransac_select, chain_wide, kThreads, 0, stream, c, rd, b);  // + fit setup (last block)
     LAUNCH(k_extract_count, chain_wide, kThreads, 0, stream, c, rd, b);
     LAUNCH(k_scan_exclusive, 1, 1024, 0, stream, b.ccount, 0u, &c->fit_chunks, nullptr, nullptr);
     LAUNCH(k_extract_emit, chain_wide, kThreads, 0, stream, c, rd, b);

@@ -384,7 +384,7 @@ __global__ void k_dda_keys(GridDesc g, const FrameParams* fp, DdaBins* db, uint8
 __global__ void k_dda_plan(DdaBins* db);
 __global__ void k_dda_scatter(const FrameParams* fp, DdaBins* db, const uint8_t* bin_of, uint32_t* perm);
 __global__ void k_clear_apply(GridDesc g, const FrameParams* fp, Counters* ctr, const DdaBins* db, int use_box);
-__global__ void k_recenter(GridDesc g, const FrameParams* fp, Counters* ctr);
+__global__ void k_recenter(GridDesc g, const FrameParams* fp, Counters* ctr, unsigned long long* occ_total);
 __global__ void k_map_finalize(Counters* ctr, unsigned long long* occ_total);
 __global__ void k_frame_begin(Counters* ctr, const unsigned long long* occ_total);
 __global__ void k_set_statuses(GridDesc g, const FrameParams* fp, const int32_t* idx, const uint8_t* st,
@@ -427,14 +427,12 @@ __global__ void k_ccl_full(Counters* ctr, SegDev sp, SegBufs b, MapDesc m);
 __global__ void k_ccl_flatten(Counters* ctr, SegBufs b, MapDesc m);
 __global__ void k_cluster_flags(Counters* ctr, SegDev sp, SegBufs b);
 __global__ void k_cluster_assign(Counters* ctr, SegBufs b);
-__global__ void k_cluster_setup(Counters* ctr, SegBufs b);
 __global__ void k_member_hist(Counters* ctr, SegBufs b, uint32_t hstride);
 __global__ void k_member_hscan(Counters* ctr, SegBufs b, uint32_t hstride);
 __global__ void k_member_scatter(Counters* ctr, SegBufs b, uint32_t hstride);
 __global__ void k_ransac_hyp(Counters* ctr, RansacDev rp, SegBufs b);
 __global__ void k_ransac_count(Counters* ctr, RansacDev rp, SegBufs b);
 __global__ void k_ransac_select(Counters* ctr, RansacDev rp, SegBufs b);
-__global__ void k_fit_setup(Counters* ctr, RansacDev rp, SegBufs b);
 __global__ void k_extract_count(Counters* ctr, RansacDev rp, SegBufs b);
 __global__ void k_extract_emit(Counters* ctr, RansacDev rp, SegBufs b);
 __global__ void k_refine(Counters* ctr, SegBufs b, d3 up, int refine, int exact);
