@@ -814,6 +814,72 @@ def run_reference(args):
     }
 
 
+def run_reference_c5(args):
+    """The reference's CPU implementation (oracle/_ref) on C5, the workload of
+    the N > 1 line: the reference renders the C5 frames itself (ref_render:
+    the same scene, sphere-LiDAR pattern, lawnmower poses and seed), runs a
+    fixed 2000 x 2000 x 300 window (38.4 GB of cells in host RAM) with all
+    host threads, one warm-up frame (map pre-population), then times up to two
+    frames (a C5 frame takes tens of seconds on the host)."""
+    import tempfile
+
+    import numpy as np
+
+    from paper_2510_01592_b200.frames import read_frames
+    from paper_2510_01592_b200.native import default_params  # a ctypes struct: loads no library
+    from paper_2510_01592_b200.scenes import C5_CENTER, C5_EXTENT, c5_poses, c5_scene, spherical_pattern
+    L, kind = ref_lib()
+    cores = os.cpu_count()
+    L.ref_set_threads(cores)
+    W, K = min(max(args.warmup, 0), 1), min(max(args.steps, 1), 2)
+    nf = W + K
+    sc = c5_scene()
+    boxes = np.asarray([(*lo, *hi) for lo, hi in sc.boxes], np.float64).reshape(-1)
+    rects = np.asarray([(*np.asarray(R, np.float64).reshape(9), *t, hu, hv) for R, t, hu, hv in sc.rects],
+                       np.float64).reshape(-1)
+    pat = np.ascontiguousarray(spherical_pattern(1_000_000), np.float32)
+    poses = np.ascontiguousarray(c5_poses(nf), np.float64)
+    dp = C.POINTER(C.c_double)
+    t0 = time.time()
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "c5.vxpf")
+        rc = L.ref_render(boxes.ctypes.data_as(dp), len(sc.boxes), rects.ctypes.data_as(dp), len(sc.rects), 1, 0, 0,
+                          0.0, 0.0, pat.ctypes.data_as(C.POINTER(C.c_float)), len(pat), 10.0, 10.0, 0.003,
+                          poses.ctypes.data_as(dp), nf, 2025, path.encode())
+        if rc != 0:
+            raise RuntimeError("ref_render failed")
+        frames = read_frames(path)
+    log(f"[bench] reference arm: C5 rendered by oracle/_ref in {time.time() - t0:.1f}s ({nf} frames)")
+    p = default_params(seed=2025)
+    ext = np.asarray(C5_EXTENT, np.int32)
+    c = np.asarray(C5_CENTER, np.float64)
+    L.ref_session_create.restype = C.c_void_p
+    sess = L.ref_session_create(C.c_double(0.01), ext.ctypes.data_as(C.POINTER(C.c_int32)),
+                                c.ctypes.data_as(dp), C.byref(p))
+    L.ref_session_set_fixed(C.c_void_p(sess), C.c_int(1))
+    for i in range(W):
+        _ref_step(L, sess, frames[i])
+    times = [_ref_step(L, sess, frames[W + i]) for i in range(K)]
+    L.ref_session_destroy(C.c_void_p(sess))
+    total = sum(times) / 1e3
+    value = K / total
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    npts = sum(len(f.points) for f in frames[W:])
+    sample = f"{W} warm-up + {K} timed C5 frames (fixed 2000x2000x300 window), one frame per step"
+    return {
+        "impl": "reference", "metric": METRIC, "value": round(value, 5), "unit": "Hz", "n_gpus": world,
+        "steps": K, "warmup": W, "ms_per_step": round(1e3 * total / K, 3), "ms_per_frame": round(1e3 * total / K, 3),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (same scene, pattern, poses and seed as the B200 arm, rendered by the reference)",
+        "config": {"workload": "C5: 20x20x3 m two-level map (floor, mezzanine, 2 stairs, 10 tables), "
+                               "2000x2000x300 at 0.01 m, lawnmower sphere-LiDAR frames",
+                   "points_per_frame": round(npts / K), "parallelism": "host threads"},
+        "cpu_baseline": {"value": round(value, 5), "unit": "Hz", "cores": cores, "kind": kind,
+                         "cpu_model": cpu_model(), "sample": sample},
+        "e2e": {"value": round(value, 5), "unit": "Hz", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -827,11 +893,13 @@ def main():
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if args.workload is None:
+        args.workload = "c5" if world > 1 else "c2"
     if args.impl == "reference":
         if rank != 0:
             return 0
         try:
-            out = run_reference(args)
+            out = run_reference_c5(args) if args.workload == "c5" else run_reference(args)
         except FileNotFoundError as e:
             out = {"impl": "reference", "unavailable": f"reference build missing: {e}"}
         print(json.dumps(out))
@@ -843,8 +911,6 @@ def main():
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
         tdist.init_process_group("nccl")
         dist = tdist
-    if args.workload is None:
-        args.workload = "c5" if world > 1 else "c2"
     out = (run_slabs if args.workload == "c5" else run_ours)(args, rank, world, dist)
     if rank == 0:
         print(json.dumps(out))
