@@ -25,6 +25,17 @@ for f in scenes.stair_frames(3):
 ws = scenes.workload_spec("c2", 1)
 src = scenes.DeviceFrameSource(ws.scene, ws.sensor, ws.seed)
 src.render(ws.poses[0], 0)
+# round 2: the library-orchestrated slab frame (one host thread per slab)
+ss2 = [slabs.Slab(0.01, (300, 200, 150), (0.0, 0.0, 0.5), a, b) for a, b in [(0, 120), (120, 300)]]
+for f in scenes.stair_frames(2):
+    slabs.frame_local(ss2, f.points, f.rotation, f.translation, native.default_params(seed=5))
+# more clusters than the initial capacity (the cluster buffers grow, the chain re-runs)
+from test_gpu_parity import many_patch_frame
+f = many_patch_frame()
+p = native.default_params(seed=3, refine_exact=False, min_area=1e-6)
+p.seg.min_cluster_size = 5
+pm = native.Pipeline(0.01, (400, 400, 120), f.translation, p)
+pm.frame(f.points, f.rotation, f.translation)
 print("sanitizer workload done")
 PY
 for tool in memcheck racecheck synccheck; do
