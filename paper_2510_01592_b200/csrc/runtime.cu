@@ -5,6 +5,7 @@
 // whose data-dependent sizes live in device counters, so the host never waits
 // mid-frame; it synchronises once to read the result records.
 #include <algorithm>
+#include <chrono>
 #include <atomic>
 #include <cmath>
 #include <cstdio>
@@ -265,7 +266,9 @@ struct Seg {
   }
   void alloc_bsum(uint64_t need_bsum) {
     bsum_cap = static_cast<uint32_t>(need_bsum);
-    bsum = dalloc<uint32_t>(2ull * need_bsum);
+    // three regions: occupied-scan tile sums | steppable tile offsets (kept for
+    // step_emit, also on a chain re-run) | flag scans (clusters)
+    bsum = dalloc<uint32_t>(3ull * need_bsum);
   }
 
   // Cluster-count dependent buffers (clusters, members' padding, RANSAC
@@ -1031,7 +1034,7 @@ struct vp_grid {
   void launch_flag_scan(const uint8_t* flags, const uint32_t* n_ptr, uint32_t cap, uint32_t* pos,
                         uint32_t* total) {
     const uint32_t nb = (cap + kScanPerBlock - 1) / kScanPerBlock;
-    uint32_t* bs = seg.bsum + seg.bsum_cap;
+    uint32_t* bs = seg.bsum + 2ull * seg.bsum_cap;
     LAUNCH(k_flags_count, nb, kScanThreads, 0, stream, flags, n_ptr, cap, bs, total, &ctr->scan_done[2]);  // + scan
     LAUNCH(k_flags_positions, nb, kScanThreads, 0, stream, flags, n_ptr, cap, bs, pos);
   }
@@ -1166,7 +1169,10 @@ struct vp_grid {
   }
   // occupied_voxels .. classify_steppable + ordinal map: the last stage that
   // reads the grid (cells, occupancy) -- everything that can overflow
-  void launch_seg_a1(const vp_pipeline_params& p, bool timing) {
+  // with_step_emit = false: the steppable list / ordinal map are left to the
+  // caller (the pipelined run enqueues them with the chain, off the mapping
+  // stream: they read only this context's lists)
+  void launch_seg_a1(const vp_pipeline_params& p, bool timing, bool with_step_emit = true) {
     const SegDev sd = make_segdev(p.seg, gd.res);
     if (!capturing && static_cast<uint64_t>(p.ransac.iterations) * seg.kcap > seg.cand_cap)
       seg.ensure(seg.b.Vcap, seg.b.Scap, seg.b.Icap, p.ransac.iterations, gd.nwords);
@@ -1174,7 +1180,7 @@ struct vp_grid {
     launch_occupied_scan();
     launch_classify(sd, 1);
     if (timing) record(ev[2]);
-    launch_step_emit(grid_map());
+    if (with_step_emit) launch_step_emit(grid_map());
   }
   // build_adjacency + label_components + filter_clusters: steppable list and
   // ordinal map only (cannot overflow: members <= S + 31 K < Mcap)
@@ -1568,6 +1574,8 @@ struct RunOutputs {
 // harvested (the list and ordinal map stay intact until the slot is reused).
 void pipeline_run(vp_pipeline* pl, size_t nf, const float* const* xyz, const uint64_t* n,
                   const double* R, const double* t, bool device_ptrs, const RunOutputs& out) {
+  const auto run_t0 = std::chrono::steady_clock::now();
+  double host_wait_us = 0.0;
   vp_grid* g = pl->grid;
   for (auto* e : {pl->ev_start, pl->ev_pre, pl->ev_map, pl->ev_clu, pl->ev_ccl, pl->ev_rsc, pl->ev_done,
                   pl->ev_h2d})
@@ -1657,6 +1665,7 @@ void pipeline_run(vp_pipeline* pl, size_t nf, const float* const* xyz, const uin
   const bool graphs = !g_prof_on && !std::getenv("VP_NO_GRAPH");
   auto enqueue_chain = [&](int s) {
     auto seg_rest = [&] {
+      g->launch_step_emit(g->grid_map());  // steppable list + ordinal map (lists only, off the mapping stream)
       g->launch_seg_a2(pl->p, false);  // build_adjacency + label_components + filter_clusters
       g->record(pl->ev_ccl[s]);
       g->launch_ransac(make_ransacdev(pl->p.ransac));
@@ -1675,7 +1684,11 @@ void pipeline_run(vp_pipeline* pl, size_t nf, const float* const* xyz, const uin
     if (k < harvested) return;
     harvested = k + 1;
     const int s = static_cast<int>(k % NS);
-    ck(cudaEventSynchronize(pl->ev_done[s]), "slot sync");
+    {
+      const auto w0 = std::chrono::steady_clock::now();
+      ck(cudaEventSynchronize(pl->ev_done[s]), "slot sync");
+      host_wait_us += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - w0).count();
+    }
     g->use_seg(s);
     g->set_slot(s);
     for (int tries = 0; g->h_ctr->overflow; ++tries) {
@@ -1685,8 +1698,8 @@ void pipeline_run(vp_pipeline* pl, size_t nf, const float* const* xyz, const uin
         fail(VP_ENOMEM, "segmentation capacity overflow in a pipelined frame");
       g->grow_chain(pl->p.ransac.iterations);
       LAUNCH(k_chain_rearm, 1, 32, 0, g->stream, g->ctr);
-      // the chain's CCL consumed (reset) the ordinal map: rebuild it from the list
-      LAUNCH(k_map_fill, g->chain_wide, kThreads, 0, g->stream, g->ctr, g->seg.b, g->grid_map());
+      // (the chain starts with the steppable list: it rebuilds the ordinal
+      // map the first run's CCL consumed)
       enqueue_chain(s);
       ck(cudaEventSynchronize(pl->ev_done[s]), "slot sync");
     }
@@ -1822,7 +1835,7 @@ void pipeline_run(vp_pipeline* pl, size_t nf, const float* const* xyz, const uin
     {
       StreamSwap on_mapping(g, g->mstream);
       auto seg_grid = [&] {
-        g->launch_seg_a1(pl->p, false);
+        g->launch_seg_a1(pl->p, false, false);  // the cell readers only: the next mapping waits for them
         ck(cudaMemcpyAsync(g->h_ctr, g->ctr, sizeof(Counters), cudaMemcpyDeviceToHost, g->stream), "ctr");
       };
       if (graphs) run_part_graph(pl, 2, g->stream, seg_grid); else seg_grid();
@@ -1836,6 +1849,10 @@ void pipeline_run(vp_pipeline* pl, size_t nf, const float* const* xyz, const uin
   }
   for (size_t k = nf > NS ? nf - NS : 0; k < nf; ++k) harvest(k);
   if (nf) g->host_occupied = g->h_ctr_s[(nf - 1) % NS]->occupied;
+  if (std::getenv("VP_PIPE_STATS"))  // host-bound run: the harvests never wait
+    std::fprintf(stderr, "pipeline_run: %zu frames, host waited %.1f us in harvests (%.1f us/frame), wall %.1f us\n",
+                 nf, host_wait_us, nf ? host_wait_us / nf : 0.0,
+                 std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - run_t0).count());
 }
 
 void wait_frame(vp_grid* g) {
