@@ -431,12 +431,12 @@ def run_ours(args, rank, world, dist):
         out["configs"] = {}
         for name in ("c1", "c3", "c4"):
             try:
-                out["configs"][name] = measure_stream(name, 3, 2, dev)
+                out["configs"][name] = measure_stream(name, 5, 3, dev, not args.no_cpu_baseline)
             except Exception as e:  # report, do not lose the headline line
                 out["configs"][name] = {"error": repr(e)[:200]}
         try:
             a5 = argparse.Namespace(**vars(args))
-            a5.steps, a5.warmup = 3, 3
+            a5.steps, a5.warmup = 6, 3
             r5 = run_slabs(a5, 0, 1, None)
             out["configs"]["c5"] = {k: r5[k] for k in ("value", "ms_per_frame", "points_per_s", "e2e", "config")}
         except Exception as e:
@@ -445,10 +445,11 @@ def run_ours(args, rank, world, dist):
 
 
 # ------------------------------------------- other BASELINE configs (N=1)
-def measure_stream(name, steps, warmup, dev):
+def measure_stream(name, steps, warmup, dev, with_cpu=True):
     """Frames/s and points/s of one BASELINE config on one GPU: the stream from
     an empty map per step (device-resident inputs; L2 flushed between steps),
-    plus the same through the C ABI with pinned host inputs (e2e)."""
+    plus the same through the C ABI with pinned host inputs (e2e), and
+    oracle/_ref on the host cores over a bounded prefix of the same frames."""
     import numpy as np
     import torch
 
@@ -491,10 +492,42 @@ def measure_stream(name, steps, warmup, dev):
     te = timed(host_ptrs, False, steps)
     pl.close()
     ms = sum(t) / len(t)
-    return {"workload": name, "frames_per_step": nf, "points_per_frame": round(sum(npts) / nf),
-            "resolution_m": wl.resolution, "extent": list(wl.extent), "value_hz": round(nf / (ms / 1e3), 2),
-            "ms_per_frame": round(ms / nf, 4), "points_per_s": round(sum(npts) / (ms / 1e3), 1),
-            "e2e_hz": round(nf / (sum(te) / len(te) / 1e3), 2), "steps": steps, "warmup": warmup}
+    r = {"workload": name, "frames_per_step": nf, "points_per_frame": round(sum(npts) / nf),
+         "resolution_m": wl.resolution, "extent": list(wl.extent), "value_hz": round(nf / (ms / 1e3), 2),
+         "ms_per_frame": round(ms / nf, 4), "points_per_s": round(sum(npts) / (ms / 1e3), 1),
+         "e2e_hz": round(nf / (sum(te) / len(te) / 1e3), 2), "steps": steps, "warmup": warmup}
+    if with_cpu:
+        try:
+            r["cpu_baseline"] = cpu_baseline_stream(wl)
+        except Exception as e:  # the reference library is optional on the box
+            r["cpu_baseline"] = {"error": repr(e)[:200]}
+    return r
+
+
+def cpu_baseline_stream(wl, budget_s=8.0):
+    """oracle/_ref on the host cores (all threads) over the first frames of a
+    secondary config's stream from an empty map, stopping once `budget_s` of
+    reference time is spent (the same frames the B200 line runs)."""
+    import numpy as np
+
+    from paper_2510_01592_b200.native import default_params  # a ctypes struct: loads no library
+    L, kind = ref_lib()
+    cores = os.cpu_count()
+    L.ref_set_threads(cores)
+    p = default_params(seed=wl.seed)
+    ext = np.asarray(wl.extent, np.int32)
+    c = np.ascontiguousarray(wl.frames[0].translation, np.float64)
+    s = L.ref_session_create(C.c_double(wl.resolution), ext.ctypes.data_as(C.POINTER(C.c_int32)),
+                             c.ctypes.data_as(C.POINTER(C.c_double)), C.byref(p))
+    total, n = 0.0, 0
+    for f in wl.frames:
+        total += _ref_step(L, s, f)
+        n += 1
+        if total / 1e3 >= budget_s:
+            break
+    L.ref_session_destroy(C.c_void_p(s))
+    return {"value": round(n / (total / 1e3), 4), "unit": "Hz", "cores": cores, "kind": kind,
+            "sample": f"first {n} of {len(wl.frames)} frames from an empty map ({total / 1e3:.1f} s)"}
 
 
 # ------------------------------------------------------ C5: spatial slabs
