@@ -1495,41 +1495,95 @@ __global__ void __launch_bounds__(256) k_refine_part1(Counters* ctr, SegBufs b, 
     refine_fin_body(ctr, b, up);
 }
 
-// Per fit (one thread): centroid = (sum of chunk sums in chunk order) / n.
-// (a block-strided loop over the fits: run by the last block of pass 0)
-__device__ __forceinline__ void refine_cen_body(const Counters* ctr, const SegBufs& b) {
-  const uint32_t F = min(ctr->nfits, b.Kcap);
-  for (uint32_t f = threadIdx.x; f < F; f += blockDim.x) {
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-    for (uint32_t c = b.rch_off[f]; c < b.rch_off[f + 1]; ++c) {
-      s0 += __ldcg(b.rpart + 8ull * c);
-      s1 += __ldcg(b.rpart + 8ull * c + 1);
-      s2 += __ldcg(b.rpart + 8ull * c + 2);
+// The fits' chunk partials are summed in the last block of each pass: one
+// thread per fit in chunk order, or -- for a fit with more than kRefSerial
+// chunks (a C5 floor has ~1500) -- the whole block: thread t sums chunks
+// t, t + 256, .. in order, then a fixed 256-leaf tree. The shape depends only
+// on the chunk count, so the result is deterministic.
+constexpr uint32_t kRefSerial = 64;
+
+template <int NQ>
+__device__ __forceinline__ void refine_block_sum(const double* rpart, uint32_t c0, uint32_t c1, double* out) {
+  __shared__ double red[NQ][256];
+  double q[NQ];
+#pragma unroll
+  for (int k = 0; k < NQ; ++k) q[k] = 0.0;
+  for (uint32_t c = c0 + threadIdx.x; c < c1; c += 256)
+#pragma unroll
+    for (int k = 0; k < NQ; ++k) q[k] += __ldcg(rpart + 8ull * c + k);
+#pragma unroll
+  for (int k = 0; k < NQ; ++k) red[k][threadIdx.x] = q[k];
+  __syncthreads();
+  for (int h = 128; h > 0; h >>= 1) {
+    if (static_cast<int>(threadIdx.x) < h)
+#pragma unroll
+      for (int k = 0; k < NQ; ++k) red[k][threadIdx.x] = red[k][threadIdx.x] + red[k][threadIdx.x + h];
+    __syncthreads();
+  }
+#pragma unroll
+  for (int k = 0; k < NQ; ++k) out[k] = red[k][0];
+  __syncthreads();
+}
+
+// Calls fn(f, sums) for every fit: serial sums by the fit's thread, block sums
+// for the large fits (batches of 256 fits, large ones listed in fit order).
+template <int NQ, class Fn>
+__device__ __forceinline__ void refine_fit_sums(const SegBufs& b, uint32_t F, Fn fn) {
+  __shared__ uint32_t big[256];
+  __shared__ uint32_t nbig;
+  for (uint32_t base = 0; base < F; base += 256) {
+    const uint32_t f = base + threadIdx.x;
+    uint32_t c0 = 0, c1 = 0;
+    if (f < F) c0 = b.rch_off[f], c1 = b.rch_off[f + 1];
+    const bool large = f < F && c1 - c0 > kRefSerial;
+    if (f < F && !large) {
+      double a[NQ];
+#pragma unroll
+      for (int k = 0; k < NQ; ++k) a[k] = 0.0;
+      for (uint32_t c = c0; c < c1; ++c)
+#pragma unroll
+        for (int k = 0; k < NQ; ++k) a[k] += __ldcg(b.rpart + 8ull * c + k);
+      fn(f, a, c1 - c0);
     }
-    const double dn = static_cast<double>(b.ioff[f + 1] - b.ioff[f]);
-    b.rcen[3 * f] = s0 / dn;
-    b.rcen[3 * f + 1] = s1 / dn;
-    b.rcen[3 * f + 2] = s2 / dn;
+    const uint32_t at = block_exclusive_u32(large ? 1u : 0u);
+    if (large) big[at] = f;
+    if (threadIdx.x == 255) nbig = at + (large ? 1u : 0u);
+    __syncthreads();
+    const uint32_t nb = nbig;
+    for (uint32_t j = 0; j < nb; ++j) {
+      const uint32_t g = big[j];
+      double a[NQ];
+      refine_block_sum<NQ>(b.rpart, b.rch_off[g], b.rch_off[g + 1], a);
+      if (threadIdx.x == 0) fn(g, a, b.rch_off[g + 1] - b.rch_off[g]);
+    }
+    __syncthreads();
   }
 }
 
-// Per fit (one thread): covariance / n -> Jacobi -> rank gate -> orient_up
+// Per fit: centroid = (sum of chunk sums) / n (run by the last block of pass 0).
+__device__ __forceinline__ void refine_cen_body(const Counters* ctr, const SegBufs& b) {
+  const uint32_t F = min(ctr->nfits, b.Kcap);
+  refine_fit_sums<3>(b, F, [&](uint32_t f, const double* s, uint32_t) {
+    const double dn = static_cast<double>(b.ioff[f + 1] - b.ioff[f]);
+    b.rcen[3 * f] = s[0] / dn;
+    b.rcen[3 * f + 1] = s[1] / dn;
+    b.rcen[3 * f + 2] = s[2] / dn;
+  });
+}
+
+// Per fit: covariance / n -> Jacobi -> rank gate -> orient_up
 // (plane_fit.cpp:133-154); unrefined fits keep the RANSAC model.
 // (run by the last block of pass 1)
 __device__ __forceinline__ void refine_fin_body(const Counters* ctr, const SegBufs& b, d3 up) {
   const uint32_t F = min(ctr->nfits, b.Kcap);
-  for (uint32_t f = threadIdx.x; f < F; f += blockDim.x) {
+  refine_fit_sums<6>(b, F, [&](uint32_t f, const double* a, uint32_t nch) {
     const double* init = b.fit_model + 4 * f;
     double* out = b.ref_model + 4 * f;
-    if (b.rch_off[f] == b.rch_off[f + 1]) {
+    if (nch == 0) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) out[q] = init[q];
-      continue;
+      return;
     }
-    double a[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    for (uint32_t c = b.rch_off[f]; c < b.rch_off[f + 1]; ++c)
-#pragma unroll
-      for (int k = 0; k < 6; ++k) a[k] += __ldcg(b.rpart + 8ull * c + k);
     const double dn = static_cast<double>(b.ioff[f + 1] - b.ioff[f]);
     double cv[3][3];
     cv[0][0] = a[0] / dn;
@@ -1539,7 +1593,7 @@ __device__ __forceinline__ void refine_fin_body(const Counters* ctr, const SegBu
     cv[1][2] = cv[2][1] = a[4] / dn;
     cv[2][2] = a[5] / dn;
     refine_finish(cv, mk3(b.rcen[3 * f], b.rcen[3 * f + 1], b.rcen[3 * f + 2]), init, up, out);
-  }
+  });
 }
 
 // ---------------------------------------------------------------------------
@@ -2002,6 +2056,251 @@ __global__ void k_poly_hull(Counters* ctr, SegBufs b, double min_area) {
 namespace vp {
 
 // ---------------------------------------------------------------------------
+// Wide passes of make_polygon for the large fits (n > kPolyBig inliers: a C5
+// floor has ~800 k, which one 4-CTA cluster projected, reduced and tested for
+// ~1.1 ms): the fits' 1024-point chunks are spread over the whole grid.
+//  k_poly_wide_ext : plane_basis, project_to_plane and the per-direction
+//                    extremes of a chunk; the last chunk of a fit to finish
+//                    reduces the chunks' extremes and builds the inner polygon
+//  k_poly_wide_keep: hull_filter's keep test of a chunk, survivors appended to
+//                    the fit's survivor range
+// k_poly_fused then runs only the hull (sort, unique, chains, area, lift) of
+// these fits. The extremes are a total order (larger dot, ties to the
+// lexicographically smaller point) and the survivors are sorted before the
+// chain, so the result equals the one-cluster form bit for bit.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void plane_basis9(const double* pl, double* bs) {  // polygonize.cpp:21-34
+  const d3 nrm = mk3(pl[0], pl[1], pl[2]);
+  int least = 0;
+  const double an[3] = {fabs(nrm.x), fabs(nrm.y), fabs(nrm.z)};
+  if (an[1] < an[least]) least = 1;
+  if (an[2] < an[least]) least = 2;
+  const d3 axis = mk3(least == 0 ? 1.0 : 0.0, least == 1 ? 1.0 : 0.0, least == 2 ? 1.0 : 0.0);
+  const d3 u = normalized3(sub3(axis, scl3(dot3(nrm, axis), nrm)));
+  const d3 v = cross3(nrm, u);
+  const d3 org = scl3(pl[3], nrm);
+  bs[0] = u.x, bs[1] = u.y, bs[2] = u.z;
+  bs[3] = v.x, bs[4] = v.y, bs[5] = v.z;
+  bs[6] = org.x, bs[7] = org.y, bs[8] = org.z;
+}
+
+__device__ __forceinline__ bool ext_better_pt(double od, P2 op, bool ook, double bd, P2 bp, bool bok) {
+  return ook && (!bok || od > bd || (od == bd && lex_less(op, bp)));
+}
+
+__device__ __forceinline__ bool poly_wide_fit(uint32_t n) { return n > kPolyBig; }
+
+// Calls fn(f, chunk id, chunk of the fit, chunks of the fit) for every chunk
+// of the large fits, block-strided over the grid. The chunk table is built
+// by every block in shared memory (batches of 256 fits, one block scan each:
+// no setup launch); chunk ids are global across batches.
+template <class Fn>
+__device__ __forceinline__ void poly_wide_chunks(const SegBufs& b, uint32_t F, Fn fn) {
+  __shared__ uint32_t off[257];
+  uint32_t base_c = 0;
+  for (uint32_t base = 0; base < F; base += 256) {
+    const uint32_t f = base + threadIdx.x;
+    const uint32_t n = f < F ? b.ioff[f + 1] - b.ioff[f] : 0u;
+    const uint32_t nch = poly_wide_fit(n) ? (n + kPolyChunk - 1) / kPolyChunk : 0u;
+    const uint32_t ex = block_exclusive_u32(nch);
+    off[threadIdx.x] = ex;
+    if (threadIdx.x == 255) off[256] = ex + nch;
+    __syncthreads();
+    const uint32_t tot = off[256];
+    const uint32_t first = (blockIdx.x + gridDim.x - base_c % gridDim.x) % gridDim.x;
+    for (uint32_t c = first; c < tot; c += gridDim.x) {
+      uint32_t lo = 0, hi = 256;  // largest j with off[j] <= c (a fit with chunks)
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (off[mid] <= c) lo = mid; else hi = mid;
+      }
+      fn(base + lo, base_c + c, c - off[lo], off[lo + 1] - off[lo]);
+    }
+    base_c += tot;
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(256) k_poly_wide_ext(Counters* ctr, SegBufs b, const double* dirtab,
+                                                       int directions, int planar) {
+  VP_GRID_WAIT();
+  __shared__ double sdir[128];
+  __shared__ double bs[9];
+  __shared__ double ex_dot[8 * 16];
+  __shared__ int ex_idx[8 * 16];
+  __shared__ bool last;
+  __shared__ P2 esort[64];
+  __shared__ P2 inner_s[130];
+  const uint32_t F = (ctr->overflow & (kOverflowFits | kOverflowMembers)) ? 0u : ctr->nfits;
+  for (int j = threadIdx.x; j < 2 * directions && j < 128; j += blockDim.x) sdir[j] = dirtab[j];
+  P2* proj = reinterpret_cast<P2*>(b.proj);
+  const unsigned lane = lane_id(), wid = threadIdx.x >> 5;
+  const bool filter = directions >= 3;  // n > kPolyBig > 3
+  poly_wide_chunks(b, F, [&](uint32_t f, uint32_t cg, uint32_t lc, uint32_t nch) {
+    const uint64_t i0 = b.ioff[f] + static_cast<uint64_t>(lc) * kPolyChunk;
+    const uint64_t i1 = min(static_cast<uint64_t>(b.ioff[f + 1]), i0 + kPolyChunk);
+    if (threadIdx.x == 0) plane_basis9(b.ref_model + 4 * f, bs);
+    __syncthreads();
+    const d3 u = mk3(bs[0], bs[1], bs[2]), v = mk3(bs[3], bs[4], bs[5]), org = mk3(bs[6], bs[7], bs[8]);
+    for (uint64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {  // project_to_plane (:36-44)
+      if (planar) {
+        proj[i] = P2{b.inl[3 * i], b.inl[3 * i + 1]};
+      } else {
+        const d3 d = sub3(mk3(b.inl[3 * i], b.inl[3 * i + 1], b.inl[3 * i + 2]), org);
+        proj[i] = P2{dot3(d, u), dot3(d, v)};
+      }
+    }
+    __syncthreads();
+    if (filter) {
+      for (int j0 = 0; j0 < directions; j0 += 16) {
+        const int nd = min(16, directions - j0);
+        double bd[16];
+        int bi[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) bd[q] = -CUDART_INF, bi[q] = -1;
+        for (uint64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+          const P2 q2 = proj[i];
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            if (q < nd) {
+              const double dd = q2.x * sdir[2 * (j0 + q)] + q2.y * sdir[2 * (j0 + q) + 1];
+              if (dd > bd[q] || (dd == bd[q] && bi[q] >= 0 && lex_less(q2, proj[bi[q]]))) {
+                bd[q] = dd;
+                bi[q] = static_cast<int>(i);
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            const double od = __shfl_down_sync(0xffffffffu, bd[q], o);
+            const int oi = __shfl_down_sync(0xffffffffu, bi[q], o);
+            if (ext_better(od, oi, bd[q], bi[q], proj)) {
+              bd[q] = od;
+              bi[q] = oi;
+            }
+          }
+          if (lane == 0) {
+            ex_dot[wid * 16 + q] = bd[q];
+            ex_idx[wid * 16 + q] = bi[q];
+          }
+        }
+        __syncthreads();
+        if (threadIdx.x < static_cast<unsigned>(nd)) {
+          const int q = static_cast<int>(threadIdx.x);
+          double best = -CUDART_INF;
+          int bix = -1;
+          for (unsigned w2 = 0; w2 < (blockDim.x >> 5); ++w2)
+            if (ext_better(ex_dot[w2 * 16 + q], ex_idx[w2 * 16 + q], best, bix, proj)) {
+              best = ex_dot[w2 * 16 + q];
+              bix = ex_idx[w2 * 16 + q];
+            }
+          b.pext_dot[static_cast<uint64_t>(cg) * 64 + j0 + q] = best;
+          b.pext_idx[static_cast<uint64_t>(cg) * 64 + j0 + q] = bix;
+        }
+        __syncthreads();
+      }
+    }
+    // the fit's last chunk to finish: final extremes, inner polygon
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      last = atomicAdd(&b.pdone[f], 1u) == nch - 1;
+      if (last) b.pdone[f] = 0u;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    if (filter && threadIdx.x < static_cast<unsigned>(directions)) {
+      // other blocks' projections: read through L2 (a line straddling two
+      // chunks may sit stale in this SM's L1)
+      const int j = static_cast<int>(threadIdx.x);
+      double best = -CUDART_INF;
+      P2 bp{0.0, 0.0};
+      bool bok = false;
+      for (uint32_t c = cg - lc; c < cg - lc + nch; ++c) {
+        const double od = __ldcg(b.pext_dot + static_cast<uint64_t>(c) * 64 + j);
+        const int oi = __ldcg(b.pext_idx + static_cast<uint64_t>(c) * 64 + j);
+        if (oi < 0) continue;
+        const P2 op{__ldcg(&proj[oi].x), __ldcg(&proj[oi].y)};
+        if (ext_better_pt(od, op, true, best, bp, bok)) {
+          best = od;
+          bp = op;
+          bok = true;
+        }
+      }
+      const P2 me = bok ? bp : P2{0.0, 0.0};
+      inner_s[j] = me;  // staging: the extremes by direction
+    }
+    __syncthreads();
+    if (filter && threadIdx.x < static_cast<unsigned>(directions)) {  // rank sort, ties by direction
+      const int j = static_cast<int>(threadIdx.x);
+      const P2 me = inner_s[j];
+      int r = 0;
+      for (int i = 0; i < directions; ++i) {
+        const P2 o = inner_s[i];
+        r += (lex_less(o, me) || (!lex_less(me, o) && i < j)) ? 1 : 0;
+      }
+      esort[r] = me;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t ni = 0;
+      if (filter) {
+        uint32_t m = 0;
+        for (int j = 0; j < directions; ++j)
+          if (m == 0 || !(esort[j].x == esort[m - 1].x && esort[j].y == esort[m - 1].y)) esort[m++] = esort[j];
+        ni = chain_sorted(esort, m, inner_s);
+        for (uint32_t k = 0; k < ni; ++k) reinterpret_cast<P2*>(b.inner)[130 * f + k] = inner_s[k];
+      }
+      b.ninner[f] = ni >= 3 ? ni : 0u;  // < 3: no filtering (hull_filter returns all points)
+      b.nsurv[f] = 0u;
+    }
+    __syncthreads();
+  });
+}
+
+__global__ void __launch_bounds__(256) k_poly_wide_keep(Counters* ctr, SegBufs b) {
+  VP_GRID_WAIT();
+  __shared__ P2 inner[130];
+  __shared__ uint32_t ni_s;
+  const uint32_t F = (ctr->overflow & (kOverflowFits | kOverflowMembers)) ? 0u : ctr->nfits;
+  const P2* proj = reinterpret_cast<const P2*>(b.proj);
+  poly_wide_chunks(b, F, [&](uint32_t f, uint32_t, uint32_t lc, uint32_t) {
+    if (threadIdx.x == 0) ni_s = b.ninner[f];
+    __syncthreads();
+    const uint32_t ni = ni_s;
+    for (uint32_t k = threadIdx.x; k < ni; k += blockDim.x) inner[k] = reinterpret_cast<const P2*>(b.inner)[130 * f + k];
+    __syncthreads();
+    const uint64_t i0 = b.ioff[f] + static_cast<uint64_t>(lc) * kPolyChunk;
+    const uint64_t i1 = min(static_cast<uint64_t>(b.ioff[f + 1]), i0 + kPolyChunk);
+    P2* surv = reinterpret_cast<P2*>(b.surv) + 2 * static_cast<uint64_t>(b.ioff[f]);
+    for (uint64_t base = i0; base < i1; base += blockDim.x) {
+      const uint64_t i = base + threadIdx.x;
+      bool keep = false;
+      P2 q{0.0, 0.0};
+      if (i < i1) {
+        q = proj[i];
+        keep = ni == 0;
+        for (uint32_t e = 0; e < ni && !keep; ++e)
+          if (cross2(inner[e], inner[(e + 1) % ni], q) <= 0.0) keep = true;
+      }
+      const unsigned km = __ballot_sync(0xffffffffu, keep);
+      uint32_t at = 0;
+      if (km) {
+        const int first = __ffs(km) - 1;
+        if (static_cast<int>(lane_id()) == first) at = atomicAdd(&b.nsurv[f], static_cast<uint32_t>(__popc(km)));
+        at = __shfl_sync(0xffffffffu, at, first);
+      }
+      if (keep) surv[at + __popc(km & lanemask_lt())] = q;
+    }
+    __syncthreads();
+  });
+}
+
+// ---------------------------------------------------------------------------
 // make_polygon for every fit in ONE kernel (the default polygon stage): a
 // thread-block cluster of kPolyCluster (4) CTAs per fit (fits strided over the
 // clusters of the grid), distributed shared memory between them:
@@ -2035,9 +2334,6 @@ __device__ unsigned long long g_poly_t[64][16];
 constexpr int kPolyThreads = 512;
 constexpr int kPolyWarps = kPolyThreads / 32;
 
-__device__ __forceinline__ bool ext_better_pt(double od, P2 op, bool ook, double bd, P2 bp, bool bok) {
-  return ook && (!bok || od > bd || (od == bd && lex_less(op, bp)));
-}
 
 __global__ void __cluster_dims__(kPolyCluster, 1, 1) __launch_bounds__(kPolyThreads)
     k_poly_fused(Counters* ctr, SegBufs b, const double* dirtab, int directions, int planar, double min_area) {
@@ -2079,18 +2375,7 @@ __global__ void __cluster_dims__(kPolyCluster, 1, 1) __launch_bounds__(kPolyThre
     }
     VP_PT(0);
     if (threadIdx.x == 0) {  // plane_basis (polygonize.cpp:21-34), every CTA
-      const d3 nrm = mk3(pl[0], pl[1], pl[2]);
-      int least = 0;
-      const double an[3] = {fabs(nrm.x), fabs(nrm.y), fabs(nrm.z)};
-      if (an[1] < an[least]) least = 1;
-      if (an[2] < an[least]) least = 2;
-      const d3 axis = mk3(least == 0 ? 1.0 : 0.0, least == 1 ? 1.0 : 0.0, least == 2 ? 1.0 : 0.0);
-      const d3 u = normalized3(sub3(axis, scl3(dot3(nrm, axis), nrm)));
-      const d3 v = cross3(nrm, u);
-      const d3 org = scl3(pl[3], nrm);
-      basis_s[0] = u.x, basis_s[1] = u.y, basis_s[2] = u.z;
-      basis_s[3] = v.x, basis_s[4] = v.y, basis_s[5] = v.z;
-      basis_s[6] = org.x, basis_s[7] = org.y, basis_s[8] = org.z;
+      plane_basis9(pl, basis_s);
       if (leader) {
         double* bs = b.basis + 9 * f;
         for (int k = 0; k < 9; ++k) bs[k] = basis_s[k];
@@ -2100,6 +2385,19 @@ __global__ void __cluster_dims__(kPolyCluster, 1, 1) __launch_bounds__(kPolyThre
     const d3 u = mk3(basis_s[0], basis_s[1], basis_s[2]), v = mk3(basis_s[3], basis_s[4], basis_s[5]),
              org = mk3(basis_s[6], basis_s[7], basis_s[8]);
     VP_PT(12);
+    // a large fit: projection, extremes and keep test ran in k_poly_wide_ext /
+    // k_poly_wide_keep; only the hull is left (uniform over the cluster)
+    const bool wide = poly_wide_fit(n);
+    P2* gsurv = reinterpret_cast<P2*>(b.surv) + 2 * static_cast<uint64_t>(i0);
+    if (wide) {
+      if (leader && threadIdx.x == 0) nsurv_s = b.nsurv[f];
+      __syncthreads();
+      if (leader) {
+        const uint32_t ns = nsurv_s;
+        for (uint32_t k = threadIdx.x; k < ns && k < static_cast<uint32_t>(kHullSmem); k += blockDim.x)
+          sm_pts[k] = gsurv[k];
+      }
+    } else {
     // 1. project_to_plane (:36-44) + per-direction extremes of this CTA's points
     const bool filter = n > 3 && directions >= 3;
     for (uint32_t i = i0 + gtid; i < i1; i += gstride) {
@@ -2228,7 +2526,6 @@ __global__ void __cluster_dims__(kPolyCluster, 1, 1) __launch_bounds__(kPolyThre
     const uint32_t ni = ni_s;
     uint32_t* rnsurv = cl.map_shared_rank(&nsurv_s, 0);
     P2* rsurv = cl.map_shared_rank(sm_pts, 0);
-    P2* gsurv = reinterpret_cast<P2*>(b.surv) + 2 * static_cast<uint64_t>(i0);
     for (uint32_t base = i0 + crank * kPolyThreads + (threadIdx.x & ~31u); base < i1; base += gstride) {
       const uint32_t i = base + lane;
       bool keep = false;
@@ -2253,6 +2550,7 @@ __global__ void __cluster_dims__(kPolyCluster, 1, 1) __launch_bounds__(kPolyThre
       }
     }
     cl.sync();
+    }  // !wide
     VP_PT(3);
     // 4. leader: sort, unique, monotone chain, area, lift (k_poly_hull)
     if (leader) {

@@ -252,7 +252,7 @@ struct Seg {
                     b.fid, b.fit_cluster, b.ioff, b.fch_off, b.ccount, b.fit_model, b.fit_meta, b.ref_model, b.inl,
                     b.rch_off, b.rpart, b.rcen,
                     b.proj, b.surv, b.hull, b.basis, b.pch_off, b.pext_dot, b.pext_idx, b.inner,
-                    b.ninner, b.nsurv, b.prec_d, b.prec_i, b.pool, b.pair_key, b.pair_slot, bsum};
+                    b.ninner, b.nsurv, b.pdone, b.prec_d, b.prec_i, b.pool, b.pair_key, b.pair_slot, bsum};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     b = SegBufs{};
@@ -282,14 +282,14 @@ struct Seg {
     void* ptrs[] = {b.klabel, b.ksize, b.kpoff, b.H, b.mx, b.my, b.mz, b.cand, b.cand_cnt, b.win_it, b.win_cnt,
                     b.fid, b.fit_cluster, b.ioff, b.fch_off, b.ccount, b.fit_model, b.fit_meta, b.ref_model,
                     b.rch_off, b.rpart, b.rcen, b.basis, b.pch_off, b.pext_dot, b.pext_idx, b.inner, b.ninner,
-                    b.nsurv, b.prec_d, b.prec_i};
+                    b.nsurv, b.pdone, b.prec_d, b.prec_i};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     b.klabel = nullptr, b.ksize = nullptr, b.kpoff = nullptr, b.H = nullptr, b.mx = b.my = b.mz = nullptr;
     b.cand = nullptr, b.cand_cnt = nullptr, b.win_it = b.win_cnt = b.fid = nullptr, b.fit_cluster = nullptr;
     b.ioff = b.fch_off = b.ccount = nullptr, b.fit_model = nullptr, b.fit_meta = nullptr, b.ref_model = nullptr;
     b.rch_off = nullptr, b.rpart = nullptr, b.rcen = nullptr, b.basis = nullptr, b.pch_off = nullptr;
-    b.pext_dot = nullptr, b.pext_idx = nullptr, b.inner = nullptr, b.ninner = b.nsurv = nullptr;
+    b.pext_dot = nullptr, b.pext_idx = nullptr, b.inner = nullptr, b.ninner = b.nsurv = b.pdone = nullptr;
     b.prec_d = nullptr, b.prec_i = nullptr;
   }
   void alloc_k_buffers(int iterations) {
@@ -333,6 +333,8 @@ struct Seg {
     b.inner = dalloc<double>(2ull * 130 * K);
     b.ninner = dalloc<uint32_t>(K);
     b.nsurv = dalloc<uint32_t>(K);
+    b.pdone = dalloc<uint32_t>(K);
+    ck(cudaMemset(b.pdone, 0, 4ull * K), "memset pdone");
     b.prec_d = dalloc<double>(8ull * K);
     b.prec_i = dalloc<int32_t>(4ull * K);
   }
@@ -1138,11 +1140,15 @@ struct vp_grid {
     LAUNCH(k_refine_part0, 148 * 4, 256, 0, stream, ctr, seg.b);     // + centroids (last block)
     LAUNCH(k_refine_part1, 148 * 4, 256, 0, stream, ctr, seg.b, u);  // + covariance, Jacobi, model
   }
-  // make_polygon for every fit: one 4-CTA cluster per fit (k_poly_fused;
-  // VP_POLY_SPLIT=1 runs the five-kernel form setup/extremes/inner/keep/hull)
+  // make_polygon for every fit: one 4-CTA cluster per fit (k_poly_fused),
+  // after the passes over the inliers of the fits above kPolyBig on the whole
+  // GPU (VP_POLY_SPLIT=1: the five-kernel form setup/extremes/inner/keep/hull)
   void launch_polygon(int dirs, double min_area, int planar = 0) {
     seg.ensure_dirs(dirs, stream);
     if (!g_poly_split) {
+      // the large fits' projection / extremes / keep test over the whole GPU
+      LAUNCH(k_poly_wide_ext, 148 * 4, 256, 0, stream, ctr, seg.b, seg.dirtab, dirs, planar);
+      LAUNCH(k_poly_wide_keep, 148 * 4, 256, 0, stream, ctr, seg.b);
       const int clusters = chain_wide >= 148 * 8 ? 32 : 16;
       LAUNCH(k_poly_fused, clusters * kPolyCluster, 512, kPolySmem, stream, ctr, seg.b, seg.dirtab, dirs,
              planar, min_area);

@@ -24,6 +24,7 @@ static_assert(kHullSmem >= 256 && kHullSmem % 256 == 0 && kHullSmem / 256 <= 32 
                   kHullSmem * 16 * 6 <= 227 * 1024,
               "VP_HULL_SMEM must be a multiple of 256 in [256, 2304]");
 constexpr int kPolyChunk = 1024;    // inlier points per polygon-stage block
+constexpr uint32_t kPolyBig = 16384;  // fits with more inliers: projection, extremes and keep test over the whole GPU
 constexpr uint32_t kRefineChunk = 512;  // inliers per refine_plane tree chunk (one block each)
 constexpr int kPolyCluster = 4;     // k_poly_fused: CTAs per fit (one thread-block cluster)
 constexpr int kPolySmem = 4 * kHullSmem * 16;  // k_poly_fused dynamic shared memory (4 x kHullSmem points)
@@ -295,6 +296,7 @@ struct SegBufs {
   double* inner;         // 2*130 per fit: inner polygon
   uint32_t* ninner;
   uint32_t* nsurv;       // survivors per fit
+  uint32_t* pdone;       // per fit chunk tickets of the wide polygon passes (reset by the last chunk)
   uint32_t pch_cap;
   double* prec_d;        // 8 per fit: normal(3) offset area
   int32_t* prec_i;       // 4 per fit: inlier_count label nv voff
@@ -441,6 +443,8 @@ __global__ void k_refine_part0(Counters* ctr, SegBufs b);
 __global__ void k_refine_part1(Counters* ctr, SegBufs b, d3 up);
 __global__ void k_poly_setup(Counters* ctr, SegBufs b);
 __global__ void k_poly_extremes(Counters* ctr, SegBufs b, const double* dirtab, int directions, int planar);
+__global__ void k_poly_wide_ext(Counters* ctr, SegBufs b, const double* dirtab, int directions, int planar);
+__global__ void k_poly_wide_keep(Counters* ctr, SegBufs b);
 __global__ void k_poly_fused(Counters* ctr, SegBufs b, const double* dirtab, int directions, int planar, double min_area);
 __global__ void k_poly_inner(Counters* ctr, SegBufs b, int directions);
 __global__ void k_poly_keep(Counters* ctr, SegBufs b);

@@ -10,11 +10,22 @@ import torch  # noqa: E402
 
 from paper_2510_01592_b200 import native, scenes  # noqa: E402
 
-wl = scenes.workload("c2", frames=12)
-pl = native.Pipeline(wl.resolution, wl.extent, wl.frames[0].translation, native.default_params(seed=wl.seed))
-dev = [torch.from_numpy(f.points).cuda() for f in wl.frames]
-for f, d in zip(wl.frames, dev):
-    pl.frame_device(d.data_ptr(), len(f.points), f.rotation, f.translation)
+from paper_2510_01592_b200 import slabs  # noqa: E402
+
+name = sys.argv[1] if len(sys.argv) > 1 else "c2"
+if name == "c5":  # one slab over the C5 window, library-orchestrated frames
+    wl = scenes.workload("c5", frames=int(sys.argv[2]) if len(sys.argv) > 2 else 6)
+    sl = slabs.Slab(wl.resolution, wl.extent, scenes.C5_CENTER, 0, wl.extent[0])
+    p = native.default_params(seed=wl.seed)
+    for f in wl.frames:
+        polys = slabs.frame_local([sl], torch.from_numpy(f.points).cuda(), f.rotation, f.translation, p)
+    print("polygons", len(polys), "counters", sl.counters())
+else:
+    wl = scenes.workload("c2", frames=12)
+    pl = native.Pipeline(wl.resolution, wl.extent, wl.frames[0].translation, native.default_params(seed=wl.seed))
+    dev = [torch.from_numpy(f.points).cuda() for f in wl.frames]
+    for f, d in zip(wl.frames, dev):
+        pl.frame_device(d.data_ptr(), len(f.points), f.rotation, f.translation)
 out = np.zeros((64, 16), np.uint64)
 native.lib().vp_debug_poly_times(out.ctypes.data_as(C.POINTER(C.c_ulonglong)))
 names = ["start", "ext+sync", "inner+sync", "keep+sync", "sort", "uniq+chains", "area+lift", "end sync", "proj", "extloop", "warpred", "ctared", "basis"]
