@@ -489,11 +489,11 @@ __global__ void k_dda_keys(GridDesc g, const FrameParams* __restrict__ fp, DdaBi
 }
 
 // One warp: decide, and lay the bins out longest first; resets the counts.
-__global__ void k_dda_plan(DdaBins* db) {
+__global__ void k_dda_plan(DdaBins* db, int force, int long_steps) {
   VP_GRID_WAIT();
   const unsigned lane = lane_id();
   const bool measured = db->warp_max != 0;  // k_dda_keys ran this frame
-  const int use = measured ? (db->steps * 4 < db->warp_max * 3 ? 1 : 0) : db->use;  // lane efficiency < 75 %
+  int use = measured ? (db->steps * 4 < db->warp_max * 3 ? 1 : 0) : db->use;  // lane efficiency < 75 %
   uint32_t run = 0;
   for (int b0 = kDdaBins - 32; b0 >= 0; b0 -= 32) {  // descending bins
     const int b = b0 + 31 - static_cast<int>(lane);
@@ -509,6 +509,10 @@ __global__ void k_dda_plan(DdaBins* db) {
     db->count[b] = 0;
   }
   __syncwarp();
+  // long rays (mean estimated steps per ray above long_steps): few cells are
+  // shared with the neighbouring lane, and one RED per brick beats one per cell
+  if (measured && long_steps > 0 && run && db->steps > static_cast<unsigned long long>(long_steps) * run) use = 1;
+  if (force >= 0) use = force;
   if (lane == 0) {
     db->use = use;
     db->steps = 0;
@@ -769,10 +773,16 @@ __device__ __forceinline__ void clear_walk_body(const GridDesc& g, const FramePa
 // and the step is branch-free: argmin, one select per axis, one DADD, the
 // cell's row-mask key advanced incrementally (key = word << 5 | bit =
 // row * 32 + z). Same cells, same order per ray as clear_walk_body.
+// kSlab: as in clear_walk_bricks below (window-coordinate walk, marks only in
+// the owned x-range, a lane ends once its ray left it); the row key of a cell
+// outside the stored range is meaningless (uint32 wrap) and never used.
 constexpr uint32_t kNoMark = 0xffffffffu;
+template <bool kSlab>
 __device__ __forceinline__ void clear_walk_coherent(const GridDesc& g, const FrameParams* __restrict__ fp) {
   const uint64_t n = fp->n;
   const DdaWin wn = dda_window(g, fp);
+  const int xoff = kSlab ? g.xoff : 0;
+  const int own0 = kSlab ? g.xoff + g.own_lo : 0, own1 = kSlab ? g.xoff + g.own_hi : g.gex;
   uint32_t* __restrict__ clr = g.clr;
   const uint32_t xs = static_cast<uint32_t>(g.ey) * static_cast<uint32_t>(g.W) * 32u;
   const uint32_t ys = static_cast<uint32_t>(g.W) * 32u;
@@ -790,16 +800,22 @@ __device__ __forceinline__ void clear_walk_coherent(const GridDesc& g, const Fra
     if (live) {
       c0 = ry.c0, c1 = ry.c1, c2 = ry.c2, s0 = ry.s0, s1 = ry.s1, s2 = ry.s2;
       tm0 = ry.tm0, tm1 = ry.tm1, tm2 = ry.tm2, td0 = ry.td0, td1 = ry.td1, td2 = ry.td2, t1 = ry.t1;
-      krow = static_cast<uint32_t>(c0) * xs + static_cast<uint32_t>(c1) * ys;
+      krow = static_cast<uint32_t>(c0 - xoff) * xs + static_cast<uint32_t>(c1) * ys;
       dxr = s0 * static_cast<int>(xs);
       dyr = s1 * static_cast<int>(ys);
-      if (static_cast<unsigned>(ry.ec0) < ex0 && static_cast<unsigned>(ry.ec1) < ex1 &&
-          static_cast<unsigned>(ry.ec2) < ex2)
-        key_e = static_cast<uint32_t>(ry.ec0) * xs + static_cast<uint32_t>(ry.ec1) * ys +
+      if (ry.ec0 >= own0 && ry.ec0 < own1 && static_cast<unsigned>(ry.ec0) < ex0 &&
+          static_cast<unsigned>(ry.ec1) < ex1 && static_cast<unsigned>(ry.ec2) < ex2)
+        key_e = static_cast<uint32_t>(ry.ec0 - xoff) * xs + static_cast<uint32_t>(ry.ec1) * ys +
                 static_cast<uint32_t>(ry.ec2);
       // the first cell is visited unless it is the origin cell
       if (!(c0 == wn.oc0 && c1 == wn.oc1 && c2 == wn.oc2)) key = krow + static_cast<uint32_t>(c2);
       if (key == key_e) key = kNoMark;
+      if (kSlab) {
+        // a ray that never reaches the owned range; a first cell outside it
+        if ((s0 > 0 && c0 >= own1) || (s0 < 0 && c0 < own0) || (s0 == 0 && (c0 < own0 || c0 >= own1)))
+          live = false, key = kNoMark;
+        if (c0 < own0 || c0 >= own1) key = kNoMark;
+      }
     }
     // (a ray never exceeds max_steps here: each step moves one axis
     // monotonically, so it leaves the window after gex + ey + ez steps)
@@ -851,6 +867,11 @@ __device__ __forceinline__ void clear_walk_coherent(const GridDesc& g, const Fra
           : "r"(s0), "r"(s1), "r"(s2), "r"(dxr), "r"(dyr), "d"(t1), "d"(td0), "d"(td1), "d"(td2), "r"(ex0),
             "r"(ex1), "r"(ex2), "r"(key_e));
       live = live_i != 0;
+      if (kSlab) {
+        // left the owned range in its x direction: done; not yet in it: no mark
+        if ((s0 > 0 && c0 >= own1) || (s0 < 0 && c0 < own0)) live = false, key = kNoMark;
+        if (c0 < own0 || c0 >= own1) key = kNoMark;
+      }
     }
   }
 }
@@ -976,7 +997,7 @@ __global__ void __launch_bounds__(256, VP_DDA_MINB) k_clear_walk(GridDesc g, con
                                                                   int generic) {
   VP_GRID_WAIT();
   if (!generic) {
-    if (db->use) clear_walk_bricks<false>(g, fp, perm); else clear_walk_coherent(g, fp);
+    if (db->use) clear_walk_bricks<false>(g, fp, perm); else clear_walk_coherent<false>(g, fp);
     return;
   }
   clear_walk_body<false>(g, fp, perm, db);
@@ -984,7 +1005,7 @@ __global__ void __launch_bounds__(256, VP_DDA_MINB) k_clear_walk(GridDesc g, con
 __global__ void __launch_bounds__(256, 4) k_clear_walk_slab(GridDesc g, const FrameParams* __restrict__ fp,
                                                             const uint32_t* perm, const DdaBins* db) {
   VP_GRID_WAIT();
-  if (db->use) clear_walk_bricks<true>(g, fp, perm); else clear_walk_body<true>(g, fp, perm, db);
+  if (db->use) clear_walk_bricks<true>(g, fp, perm); else clear_walk_coherent<true>(g, fp);
 }
 
 __device__ __forceinline__ void zero_cell(Cell* c) {
@@ -1022,23 +1043,22 @@ __device__ __forceinline__ void clear_apply_rows(const GridDesc& g, const FrameP
     const int wz0 = lo[2] >> 5;
     const uint32_t nwz = static_cast<uint32_t>((hi[2] >> 5) - wz0 + 1);
     const uint32_t ny = static_cast<uint32_t>(hi[1] - lo[1] + 1);
-    const uint64_t total = static_cast<uint64_t>(hi[0] - lo[0] + 1) * ny * nwz;
+    const uint32_t total = static_cast<uint32_t>(hi[0] - lo[0] + 1) * ny * nwz;  // < 2^27 mask words
     // four mask words per thread and trip, loaded before any is processed
     // (the sweep is latency-bound: most words are zero)
     constexpr int kPer = 4;
-    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    for (uint64_t q0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q0 < total;
-         q0 += kPer * stride) {
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t q0 = blockIdx.x * blockDim.x + threadIdx.x; q0 < total; q0 += kPer * stride) {
       uint64_t wq[kPer];
       uint32_t cq[kPer];
 #pragma unroll
       for (int k = 0; k < kPer; ++k) {
-        const uint64_t q = q0 + k * stride;
+        const uint32_t q = q0 + k * stride;
         wq[k] = ~0ull;
         cq[k] = 0u;
         if (q < total) {
-          const uint32_t r = static_cast<uint32_t>(q / nwz);
-          const int wz = wz0 + static_cast<int>(q - static_cast<uint64_t>(r) * nwz);
+          const uint32_t r = q / nwz;
+          const int wz = wz0 + static_cast<int>(q - r * nwz);
           const uint32_t rx = r / ny;
           const int y = lo[1] + static_cast<int>(r - rx * ny), x = lo[0] + static_cast<int>(rx);
           wq[k] = (static_cast<uint64_t>(x) * g.ey + y) * g.W + wz;
@@ -1088,25 +1108,46 @@ __device__ __forceinline__ void clear_apply_bricks(const GridDesc& g, const Fram
     const int bx0 = lo[0] >> 2, by0 = lo[1] >> 2, bz0 = lo[2] >> 2;
     const uint32_t nbz = static_cast<uint32_t>((hi[2] >> 2) - bz0 + 1);
     const uint32_t nby = static_cast<uint32_t>((hi[1] >> 2) - by0 + 1);
-    const uint64_t total = static_cast<uint64_t>((hi[0] >> 2) - bx0 + 1) * nby * nbz;
-    for (uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < total;
-         q += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-      const uint32_t r = static_cast<uint32_t>(q / nbz);
-      const int bz = bz0 + static_cast<int>(q - static_cast<uint64_t>(r) * nbz);
-      const uint32_t rbx = r / nby;
-      const int by = by0 + static_cast<int>(r - rbx * nby), bx = bx0 + static_cast<int>(rbx);
-      const uint64_t w = (static_cast<uint64_t>(bx) * g.bny + by) * g.bnz + bz;
-      const unsigned long long c = g.clrb[w];
+    // (< 2^26 brick words in a grid: 32-bit index arithmetic; four mask
+    // words per thread and trip loaded before any is processed -- the sweep is
+    // latency-bound, most words are zero; C5's box is the whole 150 MB mask)
+    const uint32_t total = static_cast<uint32_t>((hi[0] >> 2) - bx0 + 1) * nby * nbz;
+    constexpr int kPer = 4;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t q0 = blockIdx.x * blockDim.x + threadIdx.x; q0 < total; q0 += kPer * stride) {
+      uint64_t wq[kPer];
+      unsigned long long cq[kPer];
+      int bxq[kPer], byq[kPer], bzq[kPer];
+#pragma unroll
+      for (int k = 0; k < kPer; ++k) {
+        const uint32_t q = q0 + k * stride;
+        cq[k] = 0ull;
+        bxq[k] = byq[k] = bzq[k] = 0;
+        wq[k] = 0;
+        if (q < total) {
+          const uint32_t r = q / nbz;
+          bzq[k] = bz0 + static_cast<int>(q - r * nbz);
+          const uint32_t rbx = r / nby;
+          byq[k] = by0 + static_cast<int>(r - rbx * nby);
+          bxq[k] = bx0 + static_cast<int>(rbx);
+          wq[k] = (static_cast<uint64_t>(bxq[k]) * g.bny + byq[k]) * g.bnz + bzq[k];
+          cq[k] = g.clrb[wq[k]];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kPer; ++k) {
+      const unsigned long long c = cq[k];
       if (!c) continue;
-      g.clrb[w] = 0;
+      const int bx = bxq[k], by = byq[k], bz = bzq[k];
+      g.clrb[wq[k]] = 0;
       cl += __popcll(c);
       const int z0 = bz * 4;
       unsigned long long cols = c;
       while (cols) {  // (lx, ly) columns with marks: bits 4k .. 4k+3
-        const int k = (__ffsll(cols) - 1) >> 2;
-        const uint32_t cm = static_cast<uint32_t>(c >> (4 * k)) & 15u;
-        cols &= ~(15ull << (4 * k));
-        const int x = bx * 4 + (k >> 2), y = by * 4 + (k & 3);
+        const int kc = (__ffsll(cols) - 1) >> 2;
+        const uint32_t cm = static_cast<uint32_t>(c >> (4 * kc)) & 15u;
+        cols &= ~(15ull << (4 * kc));
+        const int x = bx * 4 + (kc >> 2), y = by * 4 + (kc & 3);
         const uint64_t ri = ring_row_index(g, fp->off_pre, x, y);
         uint32_t* row = occ + ri * g.W;
         const int pz = ring_z(g, fp->zb_pre, z0);
@@ -1115,8 +1156,9 @@ __device__ __forceinline__ void clear_apply_bricks(const GridDesc& g, const Fram
         ring_clear32(row, g.W, pz, f);  // other bricks share these ring words
         atomicSub(g.rowcnt + ri, static_cast<uint32_t>(__popc(f)));
         fr += __popc(f);
-        for (int b = 0; b < 4; ++b)
-          if (f & (1u << b)) zero_cell(g.cells + phys_index(g, fp->off_pre, x, y, z0 + b));
+        for (int bb = 0; bb < 4; ++bb)
+          if (f & (1u << bb)) zero_cell(g.cells + phys_index(g, fp->off_pre, x, y, z0 + bb));
+      }
       }
     }
   }

@@ -2129,6 +2129,8 @@ __global__ void __launch_bounds__(256) k_poly_wide_ext(Counters* ctr, SegBufs b,
   __shared__ double ex_dot[8 * 16];
   __shared__ int ex_idx[8 * 16];
   __shared__ bool last;
+  __shared__ double rdot[16][16];
+  __shared__ int ridx[16][16];
   __shared__ P2 esort[64];
   __shared__ P2 inner_s[130];
   const uint32_t F = (ctr->overflow & (kOverflowFits | kOverflowMembers)) ? 0u : ctr->nfits;
@@ -2213,28 +2215,56 @@ __global__ void __launch_bounds__(256) k_poly_wide_ext(Counters* ctr, SegBufs b,
     __syncthreads();
     if (!last) return;
     __threadfence();
-    if (filter && threadIdx.x < static_cast<unsigned>(directions)) {
-      // other blocks' projections: read through L2 (a line straddling two
-      // chunks may sit stale in this SM's L1)
-      const int j = static_cast<int>(threadIdx.x);
-      double best = -CUDART_INF;
-      P2 bp{0.0, 0.0};
-      bool bok = false;
-      for (uint32_t c = cg - lc; c < cg - lc + nch; ++c) {
-        const double od = __ldcg(b.pext_dot + static_cast<uint64_t>(c) * 64 + j);
-        const int oi = __ldcg(b.pext_idx + static_cast<uint64_t>(c) * 64 + j);
-        if (oi < 0) continue;
-        const P2 op{__ldcg(&proj[oi].x), __ldcg(&proj[oi].y)};
-        if (ext_better_pt(od, op, true, best, bp, bok)) {
-          best = od;
-          bp = op;
-          bok = true;
+    if (filter) {
+      // 16 directions at a time, each over 16 strided parts of the fit's
+      // chunks, then the 16 parts; the points only for ties (the order is
+      // total, so any reduction shape gives the same extreme). Other blocks'
+      // results and projections are read through L2 (a line straddling two
+      // chunks may sit stale in this SM's L1).
+      const uint32_t c0 = cg - lc;
+      for (int j0 = 0; j0 < directions; j0 += 16) {
+        const int j = j0 + static_cast<int>(threadIdx.x & 15u);
+        const uint32_t part = threadIdx.x >> 4;
+        double best = -CUDART_INF;
+        int bix = -1;
+        if (j < directions) {
+          for (uint32_t c = c0 + part; c < c0 + nch; c += 16) {
+            const double od = __ldcg(b.pext_dot + static_cast<uint64_t>(c) * 64 + j);
+            const int oi = __ldcg(b.pext_idx + static_cast<uint64_t>(c) * 64 + j);
+            if (oi < 0) continue;
+            if (bix < 0 || od > best) {
+              best = od;
+              bix = oi;
+            } else if (od == best && oi != bix) {
+              const P2 po{__ldcg(&proj[oi].x), __ldcg(&proj[oi].y)}, pb{__ldcg(&proj[bix].x), __ldcg(&proj[bix].y)};
+              if (lex_less(po, pb)) bix = oi;
+            }
+          }
         }
+        rdot[part][threadIdx.x & 15u] = best;
+        ridx[part][threadIdx.x & 15u] = bix;
+        __syncthreads();
+        if (threadIdx.x < 16u && j < directions) {
+          double bb = -CUDART_INF;
+          int bi2 = -1;
+          for (int q = 0; q < 16; ++q) {
+            const double od = rdot[q][threadIdx.x];
+            const int oi = ridx[q][threadIdx.x];
+            if (oi < 0) continue;
+            if (bi2 < 0 || od > bb) {
+              bb = od;
+              bi2 = oi;
+            } else if (od == bb && oi != bi2) {
+              const P2 po{__ldcg(&proj[oi].x), __ldcg(&proj[oi].y)}, pb{__ldcg(&proj[bi2].x), __ldcg(&proj[bi2].y)};
+              if (lex_less(po, pb)) bi2 = oi;
+            }
+          }
+          // staging: the extremes by direction
+          inner_s[j] = bi2 >= 0 ? P2{__ldcg(&proj[bi2].x), __ldcg(&proj[bi2].y)} : P2{0.0, 0.0};
+        }
+        __syncthreads();
       }
-      const P2 me = bok ? bp : P2{0.0, 0.0};
-      inner_s[j] = me;  // staging: the extremes by direction
     }
-    __syncthreads();
     if (filter && threadIdx.x < static_cast<unsigned>(directions)) {  // rank sort, ties by direction
       const int j = static_cast<int>(threadIdx.x);
       const P2 me = inner_s[j];

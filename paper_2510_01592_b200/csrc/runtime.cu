@@ -43,6 +43,12 @@ const bool g_pdl = !(getenv("VP_PDL") && atoi(getenv("VP_PDL")) == 0);
 int g_ccl_jumps = getenv("VP_CCL_JUMPS") ? atoi(getenv("VP_CCL_JUMPS")) : 3;
 // VP_WALK_GENERIC=1 (experiments): plain-grid rays through the generic walk loop
 const int g_walk_generic = std::getenv("VP_WALK_GENERIC") ? 1 : 0;
+// DDA walk mode (A/B): -1 k_dda_plan decides, 0 coherent lockstep, 1 bricks
+const int g_dda_force = std::getenv("VP_DDA_FORCE") ? std::atoi(std::getenv("VP_DDA_FORCE")) : -1;
+// mean estimated DDA steps per ray above which the plan walks bricks, for
+// windows whose clear mask is larger than kDdaL2Mask (VP_DDA_LONG: any window)
+const int g_dda_long = std::getenv("VP_DDA_LONG") ? std::atoi(std::getenv("VP_DDA_LONG")) : -1;
+constexpr uint64_t kDdaL2Mask = 64ull << 20;
 std::atomic<uint64_t> g_launches{0};
 
 constexpr double kRadToDeg = 57.295779513082320876798;
@@ -945,7 +951,12 @@ struct vp_grid {
     if (n == 0 && !capturing) return;
     const int gp = grid_for(capturing ? pcap : n);
     LAUNCH(k_dda_keys, gp, kThreads, 0, lstream, gd, d_fp, dbins, bin_of);
-    LAUNCH(k_dda_plan, 1, 32, 0, lstream, dbins);
+    // a window mask beyond L2 (C5: 150 MB): one row-layout RED per cell is a
+    // DRAM round trip, the brick walk issues one per brick (C5 walk 1.5 ->
+    // 0.85 ms; C2-C4 windows keep the lane-balance rule: C2 83 vs 200 us)
+    const uint64_t mask_bytes = static_cast<uint64_t>(gd.gex) * gd.ey * gd.ez / 8;
+    const int long_steps = g_dda_long >= 0 ? g_dda_long : (mask_bytes > kDdaL2Mask ? 128 : 0);
+    LAUNCH(k_dda_plan, 1, 32, 0, lstream, dbins, g_dda_force, long_steps);
     LAUNCH(k_dda_scatter, gp, kThreads, 0, lstream, d_fp, dbins, bin_of, rperm);
     if (gd.xoff != 0 || gd.gex != gd.ex)
       LAUNCH(k_clear_walk_slab, grid_for(capturing ? pcap : n, 148 * 32), kThreads, 0, lstream, gd, d_fp, rperm,

@@ -383,7 +383,7 @@ constexpr int kDenseSmem = 1024 * 24 + 16384 * 4;  // k_integrate_fold_dense dyn
 __global__ void k_clear_walk(GridDesc g, const FrameParams* fp, const uint32_t* perm, const DdaBins* db, int generic);
 __global__ void k_clear_walk_slab(GridDesc g, const FrameParams* fp, const uint32_t* perm, const DdaBins* db);
 __global__ void k_dda_keys(GridDesc g, const FrameParams* fp, DdaBins* db, uint8_t* bin_of);
-__global__ void k_dda_plan(DdaBins* db);
+__global__ void k_dda_plan(DdaBins* db, int force, int long_steps);
 __global__ void k_dda_scatter(const FrameParams* fp, DdaBins* db, const uint8_t* bin_of, uint32_t* perm);
 __global__ void k_clear_apply(GridDesc g, const FrameParams* fp, Counters* ctr, const DdaBins* db, int use_box);
 __global__ void k_recenter(GridDesc g, const FrameParams* fp, Counters* ctr, unsigned long long* occ_total);
