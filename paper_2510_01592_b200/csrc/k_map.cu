@@ -638,6 +638,16 @@ __device__ __forceinline__ bool dda_setup(const DdaWin& w, const FrameParams* __
   return true;
 }
 
+// 64-bit OR into shared memory as two native 32-bit ATOMS.OR (a 64-bit
+// atomicOr on shared memory compiles to a CAS spin loop, which the rays
+// near the sensor contend on)
+__device__ __forceinline__ void smem_or64(unsigned long long* p, unsigned long long v) {
+  uint32_t* h = reinterpret_cast<uint32_t*>(p);
+  const uint32_t lo = static_cast<uint32_t>(v), hi = static_cast<uint32_t>(v >> 32);
+  if (lo) atomicOr(h, lo);
+  if (hi) atomicOr(h + 1, hi);
+}
+
 template <bool kSlab>
 __device__ __forceinline__ void clear_walk_body(const GridDesc& g, const FrameParams* __restrict__ fp,
                                                 const uint32_t* __restrict__ perm, const DdaBins* db) {
@@ -733,7 +743,7 @@ __device__ __forceinline__ void clear_walk_body(const GridDesc& g, const FramePa
         if (((w << 6) | bit) == key_e) continue;
         if (w != aw) {
           if (ab) {
-            if (anear >= 0) atomicOr(&near_m[anear], ab); else atomicOr(clrb + aw, ab);
+            if (anear >= 0) smem_or64(&near_m[anear], ab); else atomicOr(clrb + aw, ab);
           }
           aw = w;
           ab = 0;
@@ -755,7 +765,7 @@ __device__ __forceinline__ void clear_walk_body(const GridDesc& g, const FramePa
       }
     }
     if (ab) {
-      if (anear >= 0) atomicOr(&near_m[anear], ab); else atomicOr(clrb + aw, ab);
+      if (anear >= 0) smem_or64(&near_m[anear], ab); else atomicOr(clrb + aw, ab);
     }
   }
   __syncthreads();
@@ -925,7 +935,7 @@ __device__ __forceinline__ void clear_walk_bricks(const GridDesc& g, const Frame
       if (((w << 6) | bit) == key_e) return;
       if (w != aw) {
         if (ab) {
-          if (anear >= 0) atomicOr(&near_m[anear], ab); else atomicOr(clrb + aw, ab);
+          if (anear >= 0) smem_or64(&near_m[anear], ab); else atomicOr(clrb + aw, ab);
         }
         aw = w;
         ab = 0;
@@ -977,7 +987,7 @@ __device__ __forceinline__ void clear_walk_bricks(const GridDesc& g, const Frame
       visit();
     }
     if (ab) {
-      if (anear >= 0) atomicOr(&near_m[anear], ab); else atomicOr(clrb + aw, ab);
+      if (anear >= 0) smem_or64(&near_m[anear], ab); else atomicOr(clrb + aw, ab);
     }
   }
   __syncthreads();
