@@ -1695,6 +1695,46 @@ __device__ __forceinline__ bool ext_better(double od, int oi, double bd, int bi,
   return oi >= 0 && oi != bi && (bi < 0 || od > bd || (od == bd && lex_less(proj[oi], proj[bi])));
 }
 
+// Warp-wide extreme of one direction (every lane gets the result): the
+// largest dot as the max of an order-preserving 64-bit key (-0.0 folded
+// into +0.0 so key equality is double equality), then -- only when several
+// lanes hold that dot -- the lexicographically smallest of their points.
+// The same total order as ext_better, without a load per shuffle step.
+__device__ __forceinline__ unsigned long long ext_key(double d) {
+  const unsigned long long u = static_cast<unsigned long long>(__double_as_longlong(d + 0.0));
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+__device__ __forceinline__ void warp_ext_max(double& bd, int& bi, const P2* proj) {
+  const unsigned long long key = ext_key(bd);
+  unsigned long long m = key;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long t = __shfl_xor_sync(0xffffffffu, m, o);
+    m = t > m ? t : m;
+  }
+  const unsigned tied = __ballot_sync(0xffffffffu, bi >= 0 && key == m);
+  if (!tied) {
+    bd = -CUDART_INF;
+    bi = -1;
+    return;
+  }
+  int win = __ffs(tied) - 1;
+  if (tied & (tied - 1)) {  // equal dots: lexicographic tie-break
+    const P2 mine = bi >= 0 ? proj[bi] : P2{0.0, 0.0};
+    P2 pw{__shfl_sync(0xffffffffu, mine.x, win), __shfl_sync(0xffffffffu, mine.y, win)};
+    for (unsigned rest = tied & (tied - 1); rest; rest &= rest - 1) {
+      const int l = __ffs(rest) - 1;
+      const P2 pl{__shfl_sync(0xffffffffu, mine.x, l), __shfl_sync(0xffffffffu, mine.y, l)};
+      if (lex_less(pl, pw)) {
+        win = l;
+        pw = pl;
+      }
+    }
+  }
+  bd = __shfl_sync(0xffffffffu, bd, win);
+  bi = __shfl_sync(0xffffffffu, bi, win);
+}
+
 __device__ __forceinline__ uint32_t poly_fit_of_chunk(const SegBufs& b, uint32_t F, uint32_t c) {
   uint32_t lo = 0, hi = F;  // largest f with pch_off[f] <= c
   while (hi - lo > 1) {
@@ -2175,15 +2215,7 @@ __global__ void __launch_bounds__(256) k_poly_wide_ext(Counters* ctr, SegBufs b,
         }
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            const double od = __shfl_down_sync(0xffffffffu, bd[q], o);
-            const int oi = __shfl_down_sync(0xffffffffu, bi[q], o);
-            if (ext_better(od, oi, bd[q], bi[q], proj)) {
-              bd[q] = od;
-              bi[q] = oi;
-            }
-          }
+          warp_ext_max(bd[q], bi[q], proj);
           if (lane == 0) {
             ex_dot[wid * 16 + q] = bd[q];
             ex_idx[wid * 16 + q] = bi[q];
@@ -2463,15 +2495,7 @@ __global__ void __cluster_dims__(kPolyCluster, 1, 1) __launch_bounds__(kPolyThre
         VP_PT(9);
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            const double od = __shfl_down_sync(0xffffffffu, bd[q], o);
-            const int oi = __shfl_down_sync(0xffffffffu, bi[q], o);
-            if (ext_better(od, oi, bd[q], bi[q], proj)) {
-              bd[q] = od;
-              bi[q] = oi;
-            }
-          }
+          warp_ext_max(bd[q], bi[q], proj);
           if (lane == 0) {
             wdot[wid][q] = bd[q];
             widx[wid][q] = bi[q];
@@ -2586,6 +2610,9 @@ __global__ void __cluster_dims__(kPolyCluster, 1, 1) __launch_bounds__(kPolyThre
     if (leader) {
       const uint32_t ns = nsurv_s;
       if (threadIdx.x == 0) atomicMax(&ctr->surv_max, ns);
+#ifdef VP_POLY_PROFILE
+      if (threadIdx.x == 0 && f < 64) g_poly_t[f][13] = n, g_poly_t[f][14] = ns;
+#endif
       uint32_t np2 = 1;
       while (np2 < ns) np2 <<= 1;
       const bool in_smem = np2 <= static_cast<uint32_t>(kHullSmem);

@@ -33,4 +33,4 @@ for f in range(64):
     if out[f, 0] == 0:
         break
     t = out[f].astype(np.int64) - int(out[f, 0])
-    print(f, " ".join(f"{n}={v / 1e3:.1f}" for n, v in zip(names[1:], t[1:13])))
+    print(f, f"n={int(out[f, 13])} surv={int(out[f, 14])}", " ".join(f"{n}={v / 1e3:.1f}" for n, v in zip(names[1:], t[1:13])))
