@@ -409,7 +409,9 @@ int vp_pipeline_counters(vp_pipeline* pl, uint64_t out[16]);
    (values of the last call that read them back). */
 int vp_grid_counters(vp_grid* g, uint64_t out[16]);
 /* One frame of run_frames: clear_rays, integrate_frame, recenter-if-moved,
-   voxel_frame_polygons. out may be NULL (polygons stay on the device). */
+   voxel_frame_polygons. out may be NULL (polygons stay on the device);
+   timing may be NULL (the per-stage device times cost six event queries,
+   ~17 us of host time per frame). */
 int vp_pipeline_frame(vp_pipeline* pl, const float* xyz, uint64_t n, const double rotation[9],
                       const double translation[3], vp_polygons_t** out,
                       vp_frame_timing* timing);

@@ -2618,9 +2618,41 @@ __global__ void __cluster_dims__(kPolyCluster, 1, 1) __launch_bounds__(kPolyThre
       const bool in_smem = np2 <= static_cast<uint32_t>(kHullSmem);
       P2* arr = in_smem ? sm_pts : gsurv;
       P2* hullg = reinterpret_cast<P2*>(b.hull) + 2 * static_cast<uint64_t>(i0);  // the ring (global, <= 2 ns)
-      for (uint32_t i = ns + threadIdx.x; i < np2; i += blockDim.x) arr[i] = P2{CUDART_INF, CUDART_INF};
-      __syncthreads();
-      bitonic_sort(arr, np2);
+      if (in_smem && ns <= static_cast<uint32_t>(kPolyThreads)) {
+        // one point per thread: rank sort (lexicographic, ties by position)
+        // through the lower-stack region, one pass instead of the bitonic
+        // network's log^2 passes and barriers
+        // The comparisons run on order-preserving integer keys of the
+        // coordinates (ext_key: -0.0 folded into +0.0, so key order and
+        // equality are the doubles' <, ==) -- integer compares issue at full
+        // rate where the FP64 compares of lex_less do not.
+        P2* tmp = sm_pts + 2 * kHullSmem;
+        ulonglong2* keys = reinterpret_cast<ulonglong2*>(sm_pts + 3 * kHullSmem);
+        P2 me{0.0, 0.0};
+        ulonglong2 mk{0ull, 0ull};
+        if (threadIdx.x < ns) {
+          me = arr[threadIdx.x];
+          mk = make_ulonglong2(ext_key(me.x), ext_key(me.y));
+          keys[threadIdx.x] = mk;
+        }
+        __syncthreads();
+        if (threadIdx.x < ns) {
+          uint32_t r = 0;
+#pragma unroll 8
+          for (uint32_t j = 0; j < ns; ++j) {
+            const ulonglong2 o = keys[j];
+            r += (o.x < mk.x || (o.x == mk.x && (o.y < mk.y || (o.y == mk.y && j < threadIdx.x)))) ? 1u : 0u;
+          }
+          tmp[r] = me;
+        }
+        __syncthreads();
+        if (threadIdx.x < ns) arr[threadIdx.x] = tmp[threadIdx.x];
+        __syncthreads();
+      } else {
+        for (uint32_t i = ns + threadIdx.x; i < np2; i += blockDim.x) arr[i] = P2{CUDART_INF, CUDART_INF};
+        __syncthreads();
+        bitonic_sort(arr, np2);
+      }
       VP_PT(4);
       if (in_smem) {
         P2* uq = sm_pts + kHullSmem;

@@ -3610,22 +3610,47 @@ static int pipeline_frame_impl(vp_pipeline* pl, const float* xyz, uint64_t n, co
                                vp_frame_timing* timing) {
   if (out) *out = nullptr;
   return guard([&] {
+    // VP_LAT_STATS: where one frame's latency goes (host phases, GPU gaps)
+    static const bool lat_stats = std::getenv("VP_LAT_STATS") != nullptr;
+    using clk = std::chrono::steady_clock;
+    const auto h0 = clk::now();
     vp_shift_stats ss;
     pipeline_enqueue(pl, xyz, n, R, t, device_ptr, &ss);
+    const auto h1 = clk::now();
     vp_grid* g = pl->grid;
     wait_frame(g);
+    const auto h2 = clk::now();
     const bool rerun = g->h_ctr->overflow != 0;
     if (rerun) rerun_segment_until_fits(g, pl->p);
     fill_timing(g, timing, n);
+    const auto h2b = clk::now();
+    clk::time_point h2c = h2b;
     if (out) {
       HostPolys hp;
       if (rerun || !unpack_polygons(pl->pack1_h, hp)) g->download_polygons(hp, false);
+      h2c = clk::now();
       *out = make_polygons_out(hp);
     }
+    const auto h3 = clk::now();
     // the polygons are in host memory: the frame's end to end latency
     ck(cudaEventRecord(pl->lat_ev[1], g->stream), "event");
     ck(cudaEventSynchronize(pl->lat_ev[1]), "event");
     ck(cudaEventElapsedTime(&pl->last_latency_ms, pl->lat_ev[0], pl->lat_ev[1]), "elapsed");
+    if (lat_stats) {
+      const auto us = [](clk::time_point a, clk::time_point b) {
+        return std::chrono::duration<double, std::micro>(b - a).count();
+      };
+      float head = 0.0f, body = 0.0f, tail = 0.0f;
+      cudaEventElapsedTime(&head, pl->lat_ev[0], g->ev[0]);
+      cudaEventElapsedTime(&body, g->ev[0], g->ev[5]);
+      cudaEventElapsedTime(&tail, g->ev[5], pl->lat_ev[1]);
+      std::fprintf(stderr,
+                   "[lat] frame %u: %.1f us | host enqueue %.1f, wait %.1f, timing %.1f, unpack %.1f, out %.1f, "
+                   "end event %.1f | gpu head %.1f, body %.1f, tail %.1f\n",
+                   pl->frame, 1e3 * pl->last_latency_ms, us(h0, h1), us(h1, h2), us(h2, h2b), us(h2b, h2c),
+                   us(h2c, h3), us(h3, clk::now()),
+                   1e3 * head, 1e3 * body, 1e3 * tail);
+    }
     ++pl->frame;
   });
 }

@@ -195,15 +195,17 @@ class Pipeline:
                                       C.byref(out) if want_polygons else None, C.byref(tm)))
         return (polygons_to_py(out) if want_polygons else None), tm
 
-    def frame_ptr(self, pts_host_ptr: int, n: int, R, t, want_polygons=True):
-        """vp_pipeline_frame on a raw host pointer (e.g. pinned memory)."""
+    def frame_ptr(self, pts_host_ptr: int, n: int, R, t, want_polygons=True, want_timing=True):
+        """vp_pipeline_frame on a raw host pointer (e.g. pinned memory); the
+        stage timings (FrameTiming, six event queries) only when wanted."""
         R, t = _pose(R, t)
         out = C.POINTER(Polygons)()
         tm = FrameTiming()
         check(lib().vp_pipeline_frame(self.h, C.c_void_p(pts_host_ptr), C.c_uint64(n),
                                       _p(R, C.c_double), _p(t, C.c_double),
-                                      C.byref(out) if want_polygons else None, C.byref(tm)))
-        return (polygons_to_py(out) if want_polygons else None), tm
+                                      C.byref(out) if want_polygons else None,
+                                      C.byref(tm) if want_timing else None))
+        return (polygons_to_py(out) if want_polygons else None), (tm if want_timing else None)
 
     def run(self, frames, device_ptrs=None, want_polygons=True, timings=False):
         """vp_pipeline_run: run_frames over a list of Frames (host arrays), or

@@ -17,7 +17,7 @@ host = [torch.from_numpy(f.points).pin_memory() for f in wl.frames]
 dev = [torch.empty_like(h, device="cuda") for h in host]
 L = native.lib()
 L.vp_pipeline_latency_ms.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
-lat, dspan, h2d = [], [], []
+lat, dspan, h2d, parts = [], [], [], []
 ms = C.c_double()
 for rep in range(2):
     pl.reset(wl.frames[0].translation)
@@ -27,6 +27,7 @@ for rep in range(2):
         if rep == 1 and k >= 2:
             lat.append(ms.value)
             dspan.append(tm.total_ms)
+            parts.append((tm.mapping_ms, tm.classify_ms, tm.cluster_ms, tm.ransac_ms, tm.hull_ms))
 s = torch.cuda.Stream()
 for k in range(2, 30):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -38,3 +39,5 @@ for k in range(2, 30):
     h2d.append(e0.elapsed_time(e1))
 print(f"latency p50 {statistics.median(lat):.4f} ms, device span p50 {statistics.median(dspan):.4f} ms, "
       f"points H2D p50 {statistics.median(h2d):.4f} ms ({len(wl.frames[5].points) * 12 / 1e6:.2f} MB)")
+names = ("mapping", "classify", "cluster", "ransac", "refine+hull")
+print("device stages p50 (ms): " + ", ".join(f"{n} {statistics.median(p[i] for p in parts):.4f}" for i, n in enumerate(names)))
