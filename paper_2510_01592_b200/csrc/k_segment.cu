@@ -662,6 +662,17 @@ __global__ void __launch_bounds__(256) k_ccl_pairs_union(Counters* ctr, SegDev s
     uf_union(b.parent, static_cast<int>(key & 0xffffffffu), static_cast<int>(key >> 32));
   }
   __syncthreads();
+  // the pair roots now form chains (larger root under smaller, in pair
+  // order: C4's many small hook trees made them thousands deep, and every
+  // voxel of k_ccl_flatten chased them): point each straight at its root
+  __threadfence_block();
+  for (uint32_t t = threadIdx.x; t < n; t += blockDim.x) {
+    const unsigned long long key = __ldcg(b.pair_key + b.pair_slot[t]);
+    const int a = static_cast<int>(key & 0xffffffffu), c = static_cast<int>(key >> 32);
+    __stcg(b.parent + a, uf_find(b.parent, a));
+    __stcg(b.parent + c, uf_find(b.parent, c));
+  }
+  __syncthreads();
   if (ctr->pair_ovf) {
     for (uint32_t h = threadIdx.x; h < b.pair_cap; h += blockDim.x) b.pair_key[h] = kPairEmpty;
   } else {
