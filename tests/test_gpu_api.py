@@ -320,6 +320,56 @@ def test_refine_exact_and_tree():
         assert np.arccos(np.clip(ne @ nt, -1, 1)) <= 1e-4 and abs(oe - ot) <= 1e-4
 
 
+def _oracle_polygon(L, pl, pts):
+    P = native.Plane()
+    P.normal[:] = tuple(pl["normal"])
+    P.offset = pl["offset"]
+    v2 = np.zeros(2 * len(pts))
+    v3 = np.zeros(3 * len(pts))
+    area = C.c_double()
+    pts = np.ascontiguousarray(pts, float)
+    nv = L.oracle_make_polygon(C.byref(P), C.c_size_t(len(pts)), pts.ctypes.data_as(C.POINTER(C.c_double)),
+                               16, v2.ctypes.data_as(C.POINTER(C.c_double)),
+                               v3.ctypes.data_as(C.POINTER(C.c_double)), C.byref(area))
+    return nv, v2[:2 * nv], v3[:3 * nv], area.value
+
+
+def test_make_polygon_large_fits_vs_oracle():
+    """Fits above the wide-pass threshold (16 384 inliers: chunked extremes
+    and keep test over the grid) next to small ones, with exact ties: lattice
+    points put many points on the same extreme line (key-reduction and
+    lexicographic tie-breaks), duplicated points, and survivor sets on both
+    sides of the rank-sort (512) and shared-memory (1024) limits."""
+    rng = np.random.default_rng(21)
+    L = CpuSession.load("oracle")
+    planes, sets = [], []
+
+    def add(pts, normal=(0, 0, 1.0), offset=0.0):
+        n = np.asarray(normal, float)
+        planes.append(dict(normal=n / np.linalg.norm(n), offset=offset, inlier_count=len(pts), label=len(planes)))
+        sets.append(np.ascontiguousarray(pts, float))
+
+    g = np.stack(np.meshgrid(np.arange(150), np.arange(140), indexing="ij"), -1).reshape(-1, 2) * 0.01
+    add(np.c_[g, np.zeros(len(g))])                                   # 21 000-point lattice square
+    disk = g[((g - 0.7) ** 2).sum(1) < 0.49]
+    add(np.c_[disk, np.full(len(disk), 0.3)], offset=0.3)             # lattice disk: hundreds of survivors
+    add(np.r_[np.c_[g, np.zeros(len(g))], np.c_[g, np.zeros(len(g))]])  # every point twice
+    add(rng.normal(size=(70000, 3)), normal=(0.3, -0.2, 0.9), offset=0.1)
+    add(rng.uniform(-1, 1, (150000, 3)), normal=(1.0, 0.0, 0.0))
+    add(rng.normal(size=(300, 3)))                                    # a small fit beside them
+    theta = rng.uniform(0, 2 * np.pi, 40000)
+    add(np.c_[np.cos(theta), np.sin(theta), np.zeros(40000)])         # points on a circle: every point survives
+    got = native.make_polygons(planes, sets)
+    assert len(got) == len(planes)
+    for pl, pts, gp in zip(planes, sets, got):
+        nv, v2, v3, area = _oracle_polygon(L, pl, pts)
+        assert len(gp["v2d"]) == nv
+        if nv:
+            assert gp["v2d"].tobytes() == v2.tobytes()
+            assert gp["v3d"].tobytes() == v3.tobytes()
+            assert gp["area"] == area
+
+
 def test_make_polygon_square_and_vs_oracle():
     # test_polygonize.cpp:105-117: unit square -> CCW from the lex-min vertex, area 1
     sq = np.array([[0, 0, 0], [1, 0, 0], [1, 1, 0], [0, 1, 0], [0.5, 0.5, 0], [0.25, 0.75, 0]], float)

@@ -36,6 +36,11 @@ p = native.default_params(seed=3, refine_exact=False, min_area=1e-6)
 p.seg.min_cluster_size = 5
 pm = native.Pipeline(0.01, (400, 400, 120), f.translation, p)
 pm.frame(f.points, f.rotation, f.translation)
+# round 2: fits above the wide-pass threshold (k_poly_wide_ext / _keep), lattice ties
+g = np.stack(np.meshgrid(np.arange(150), np.arange(140), indexing="ij"), -1).reshape(-1, 2) * 0.01
+lat = np.c_[g, np.zeros(len(g))]
+native.make_polygons([dict(normal=np.array([0, 0, 1.0]), offset=0.0), dict(normal=np.array([0.3, -0.2, 0.9]) / np.linalg.norm([0.3, -0.2, 0.9]), offset=0.1)],
+                     [lat, np.random.default_rng(1).normal(size=(40000, 3))])
 print("sanitizer workload done")
 PY
 for tool in memcheck racecheck synccheck; do
