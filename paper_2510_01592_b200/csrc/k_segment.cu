@@ -2770,6 +2770,7 @@ __global__ void k_poly_pack(const Counters* ctr, SegBufs b, double* out, uint64_
   // serial per-fit copy of round 1 took 34 us for ~10 KB)
   __shared__ uint32_t carry;
   __shared__ uint32_t voff_s[1024];
+  __shared__ uint32_t src_s[1024];
   const uint32_t F = (ctr->overflow & (kOverflowFits | kOverflowMembers | kOverflowPool)) ? 0u : ctr->nfits;
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
@@ -2781,6 +2782,7 @@ __global__ void k_poly_pack(const Counters* ctr, SegBufs b, double* out, uint64_
     __syncthreads();
     if (threadIdx.x == blockDim.x - 1) carry = c + ex + nv;
     voff_s[threadIdx.x] = c + ex;
+    src_s[threadIdx.x] = f < F ? static_cast<uint32_t>(b.prec_i[4 * f + 3]) : 0u;
     __syncthreads();
     // records: 12 doubles per fit, the fits of this batch side by side
     const uint32_t nb = min(blockDim.x, F - base);
@@ -2796,15 +2798,20 @@ __global__ void k_poly_pack(const Counters* ctr, SegBufs b, double* out, uint64_
       else if (q == 10) v = static_cast<double>(fnv);
       if (4 + 12ull * F + 5ull * (voff_s[e / 12] + fnv) <= cap) out[4 + 12ull * ff + q] = v;
     }
-    // vertices, one fit after the other, every thread on consecutive doubles
-    for (uint32_t j = 0; j < nb; ++j) {
-      const uint32_t ff = base + j;
-      const int32_t* ri = b.prec_i + 4 * ff;
-      const uint32_t fnv = static_cast<uint32_t>(max(ri[2], 0));
-      const uint64_t vo = 4 + 12ull * F + 5ull * voff_s[j];
-      if (vo + 5ull * fnv > cap) continue;
-      const double* src = b.pool + 5ull * static_cast<uint32_t>(ri[3]);
-      for (uint32_t q = threadIdx.x; q < 5 * fnv; q += blockDim.x) out[vo + q] = src[q];
+    // vertices of every fit of the batch in one pass, consecutive threads on
+    // consecutive doubles (a thread finds its fit by binary search in the
+    // batch's vertex offsets; a fit-by-fit loop paid a dependent record load
+    // per fit); a pack beyond cap is flagged below and not read
+    const uint32_t vb = voff_s[0], ve = carry;
+    const uint64_t ob = 4 + 12ull * F + 5ull * vb;
+    for (uint32_t e = threadIdx.x; e < 5 * (ve - vb); e += blockDim.x) {
+      const uint32_t vtx = vb + e / 5;
+      uint32_t lo = 0, hi = nb;  // largest j with voff_s[j] <= vtx
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (voff_s[mid] <= vtx) lo = mid; else hi = mid;
+      }
+      if (ob + e < cap) out[ob + e] = b.pool[5ull * (src_s[lo] + (vtx - voff_s[lo])) + e % 5];
     }
     __syncthreads();
   }
