@@ -1640,12 +1640,24 @@ __device__ uint32_t chain_sorted(const P2* pts, uint32_t n, P2* h) {
 // the upper part only down to `lower`, i.e. never below pts[n-1], so
 // hull = L + U[1 .. |U|-1) is exactly its output. The top two stack entries
 // live in registers (the pop loop is a serial dependency chain).
+#ifdef VP_POLY_PROFILE
+__device__ unsigned long long g_chain_stats[4];  // tests, points, cycles
+#endif
 __device__ uint32_t half_chain(const P2* pts, uint32_t n, bool upper, P2* h) {
   uint32_t k = 0;
+#ifdef VP_POLY_PROFILE
+  const long long c_start = clock64();
+  unsigned long long ntests = 0;
+#define VP_CHAIN_TEST() ++ntests
+#else
+#define VP_CHAIN_TEST() do {} while (0)
+#endif
   // the top three stack entries live in registers (t = h[k-1], a = h[k-2],
   // a2 = h[k-3]): a pop's next test needs no shared-memory round trip, and the
   // entry below is fetched while the cross product runs; the next input
-  // point is loaded one step ahead
+  // point is loaded one step ahead. (Profiled, VP_POLY_PROFILE, C2: ~1.1
+  // tests per point at ~260 cycles each on one warp; evaluating the test that
+  // follows a pop speculatively alongside did not change it.)
   P2 a{0.0, 0.0}, t{0.0, 0.0}, a2{0.0, 0.0};
   if (upper) {
     t = pts[n - 1];
@@ -1656,7 +1668,9 @@ __device__ uint32_t half_chain(const P2* pts, uint32_t n, bool upper, P2* h) {
   for (uint32_t q = 0; q < m; ++q) {
     const P2 p = pn;
     if (q + 1 < m) pn = upper ? pts[n - 3 - q] : pts[q + 1];
-    while (k >= 2 && cross2(a, t, p) <= 0.0) {
+    while (k >= 2) {
+      VP_CHAIN_TEST();
+      if (!(cross2(a, t, p) <= 0.0)) break;
       --k;
       t = a;
       a = a2;
@@ -1667,6 +1681,11 @@ __device__ uint32_t half_chain(const P2* pts, uint32_t n, bool upper, P2* h) {
     a = t;
     t = p;
   }
+#ifdef VP_POLY_PROFILE
+  atomicAdd(&g_chain_stats[0], ntests);
+  atomicAdd(&g_chain_stats[1], static_cast<unsigned long long>(m));
+  atomicAdd(&g_chain_stats[2], static_cast<unsigned long long>(clock64() - c_start));
+#endif
   return k;
 }
 
@@ -2392,7 +2411,7 @@ __global__ void __launch_bounds__(256) k_poly_wide_keep(Counters* ctr, SegBufs b
 // the public hull_filter); the survivor set, and so the hull, is identical.
 // ---------------------------------------------------------------------------
 #ifdef VP_POLY_PROFILE
-__device__ unsigned long long g_poly_t[64][16];
+__device__ unsigned long long g_poly_t[64][20];
 #define VP_PT(k)                                                                              \
   do {                                                                                        \
     if (leader && threadIdx.x == 0 && f < 64) {                                               \
@@ -2686,6 +2705,7 @@ __global__ void __cluster_dims__(kPolyCluster, 1, 1) __launch_bounds__(kPolyThre
         for (int qq = 0; qq < kPer; ++qq)
           if ((keep_mask >> qq) & 1u) uq[pos++] = arr[j0 + qq];
         __syncthreads();
+        VP_PT(15);
         const uint32_t mu = n_uniq;
         if (mu >= 3 && (threadIdx.x == 0 || threadIdx.x == 32)) {
           const bool upper = threadIdx.x == 32;
@@ -2693,6 +2713,7 @@ __global__ void __cluster_dims__(kPolyCluster, 1, 1) __launch_bounds__(kPolyThre
           if (upper) voff = k; else area_s = static_cast<double>(k);  // stash sizes
         }
         __syncthreads();
+        VP_PT(16);
         if (threadIdx.x == 0) {
           uint32_t mh = 0;
           if (mu >= 3) {
@@ -2850,6 +2871,11 @@ __global__ void k_chain_rearm(Counters* ctr) {
 }  // namespace vp
 
 #ifdef VP_POLY_PROFILE
+#ifdef VP_POLY_PROFILE
+extern "C" int vp_debug_chain_stats(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, vp::g_chain_stats, sizeof(vp::g_chain_stats)) == cudaSuccess ? 0 : 1;
+}
+#endif
 extern "C" int vp_debug_poly_times(unsigned long long* out) {
   return cudaMemcpyFromSymbol(out, vp::g_poly_t, sizeof(vp::g_poly_t)) == cudaSuccess ? 0 : 1;
 }

@@ -210,6 +210,8 @@ SegDev make_segdev(const vp_seg_params& p, double res) {
   s.dstar = angle_threshold(p.max_angle_deg);
   s.up = d3{p.up[0], p.up[1], p.up[2]};
   s.w = std::max(1, static_cast<int>(std::ceil(p.distance_th / res)));
+  // a window row (2w + 1 cells along z) is read as one 32-bit bitmap span
+  if (s.w > 15) fail(VP_EINVAL, "segment: distance_th / resolution above 15 cells is not supported");
   s.d2_th = p.distance_th * p.distance_th;
   s.cos_th = std::cos(p.adjacency_angle_deg * kDegToRad);
   s.min_cluster = p.min_cluster_size;

@@ -26,11 +26,18 @@ else:
     dev = [torch.from_numpy(f.points).cuda() for f in wl.frames]
     for f, d in zip(wl.frames, dev):
         pl.frame_device(d.data_ptr(), len(f.points), f.rotation, f.translation)
-out = np.zeros((64, 16), np.uint64)
+out = np.zeros((64, 20), np.uint64)
 native.lib().vp_debug_poly_times(out.ctypes.data_as(C.POINTER(C.c_ulonglong)))
 names = ["start", "ext+sync", "inner+sync", "keep+sync", "sort", "uniq+chains", "area+lift", "end sync", "proj", "extloop", "warpred", "ctared", "basis"]
 for f in range(64):
     if out[f, 0] == 0:
         break
     t = out[f].astype(np.int64) - int(out[f, 0])
-    print(f, f"n={int(out[f, 13])} surv={int(out[f, 14])}", " ".join(f"{n}={v / 1e3:.1f}" for n, v in zip(names[1:], t[1:13])))
+    print(f, f"n={int(out[f, 13])} surv={int(out[f, 14])}", " ".join(f"{n}={v / 1e3:.1f}" for n, v in zip(names[1:], t[1:13])),
+          f"uniq={t[15] / 1e3:.1f} chains={t[16] / 1e3:.1f}")
+
+if hasattr(native.lib(), "vp_debug_chain_stats"):
+    cs = np.zeros(4, np.uint64)
+    native.lib().vp_debug_chain_stats(cs.ctypes.data_as(C.POINTER(C.c_ulonglong)))
+    print(f"half chains: {int(cs[1])} points, {int(cs[0])} pop tests, {int(cs[2])} cycles "
+          f"({cs[2] / max(cs[1], 1):.0f} cycles/point, {cs[2] / max(cs[0], 1):.0f} cycles/test)")
