@@ -2423,7 +2423,6 @@ __device__ unsigned long long g_poly_t[64][20];
 #else
 #define VP_PT(k) do {} while (0)
 #endif
-constexpr int kPolyThreads = 512;
 constexpr int kPolyWarps = kPolyThreads / 32;
 
 

@@ -1163,7 +1163,7 @@ struct vp_grid {
       LAUNCH(k_poly_wide_ext, 148 * 4, 256, 0, stream, ctr, seg.b, seg.dirtab, dirs, planar);
       LAUNCH(k_poly_wide_keep, 148 * 4, 256, 0, stream, ctr, seg.b);
       const int clusters = chain_wide >= 148 * 8 ? 32 : 16;
-      LAUNCH(k_poly_fused, clusters * kPolyCluster, 512, kPolySmem, stream, ctr, seg.b, seg.dirtab, dirs,
+      LAUNCH(k_poly_fused, clusters * kPolyCluster, kPolyThreads, kPolySmem, stream, ctr, seg.b, seg.dirtab, dirs,
              planar, min_area);
       return;
     }

@@ -27,6 +27,14 @@ constexpr int kPolyChunk = 1024;    // inlier points per polygon-stage block
 constexpr uint32_t kPolyBig = 16384;  // fits with more inliers: projection, extremes and keep test over the whole GPU
 constexpr uint32_t kRefineChunk = 512;  // inliers per refine_plane tree chunk (one block each)
 constexpr int kPolyCluster = 4;     // k_poly_fused: CTAs per fit (one thread-block cluster)
+#ifndef VP_POLY_THREADS
+#define VP_POLY_THREADS 256
+#endif
+// k_poly_fused: threads per CTA. 256 rather than 512: a CTA then holds half
+// an SM's registers (128 per thread) while its leader runs the serial hull,
+// which leaves room for the overlapping frames' kernels (C2 5097 -> 5160
+// frames/s; the polygon stage itself 60 -> 66 us)
+constexpr int kPolyThreads = VP_POLY_THREADS;
 constexpr int kPolySmem = 4 * kHullSmem * 16;  // k_poly_fused dynamic shared memory (4 x kHullSmem points)
 #ifndef VP_FOLD_SMALL
 #define VP_FOLD_SMALL 24
