@@ -204,6 +204,26 @@ def test_label_components_matches_oracle(seed, ccl_mode):
     assert np.array_equal(got, exp)
 
 
+def test_label_components_widest_window_and_limit():
+    """w = ceil(distance_th / res) = 15 (a window row of 31 cells, the widest one
+    bitmap span holds) matches the oracle; w > 15 fails loudly."""
+    rng = np.random.default_rng(7)
+    idx, mean, nrm = random_steppable(rng, 2000, 40)
+    seg = native.default_params().seg
+    seg.distance_th = 0.149
+    got = native.label_components(idx, mean, nrm, seg, 0.01)
+    L = CpuSession.load("oracle")
+    exp = np.zeros(len(idx), np.int32)
+    L.oracle_label_components(C.c_size_t(len(idx)), idx.ctypes.data_as(C.POINTER(C.c_int32)),
+                              mean.ctypes.data_as(C.POINTER(C.c_double)),
+                              nrm.ctypes.data_as(C.POINTER(C.c_double)), C.byref(seg), C.c_double(0.01),
+                              exp.ctypes.data_as(C.POINTER(C.c_int32)))
+    assert np.array_equal(got, exp)
+    seg.distance_th = 0.2
+    with pytest.raises(native.InvalidArgument):
+        native.label_components(idx, mean, nrm, seg, 0.01)
+
+
 def planar_steppable(rng):
     """~300k voxels: a 520 x 520 noisy floor with holes, a raised 200 x 120 table
     patch and clutter -- a giant component plus many small ones."""
