@@ -2676,8 +2676,27 @@ __global__ void __cluster_dims__(kPolyCluster, 1, 1) __launch_bounds__(kPolyThre
           uint32_t r = 0;
 #pragma unroll 8
           for (uint32_t j = 0; j < ns; ++j) {
+            // (o.x, o.y, j) < (mk.x, mk.y, tid) as one 160-bit borrow chain
+            // (five subtract-with-borrow steps instead of ~13 compares and
+            // predicate ops): b = 0xffffffff if less, else 0
             const ulonglong2 o = keys[j];
-            r += (o.x < mk.x || (o.x == mk.x && (o.y < mk.y || (o.y == mk.y && j < threadIdx.x)))) ? 1u : 0u;
+            uint32_t bw;
+            asm("{\n\t"
+                ".reg .u32 d;\n\t"
+                "sub.cc.u32 d, %1, %2;\n\t"
+                "subc.cc.u32 d, %3, %4;\n\t"
+                "subc.cc.u32 d, %5, %6;\n\t"
+                "subc.cc.u32 d, %7, %8;\n\t"
+                "subc.cc.u32 d, %9, %10;\n\t"
+                "subc.u32 %0, 0, 0;\n\t"
+                "}"
+                : "=r"(bw)
+                : "r"(j), "r"(static_cast<uint32_t>(threadIdx.x)), "r"(static_cast<uint32_t>(o.y)),
+                  "r"(static_cast<uint32_t>(mk.y)), "r"(static_cast<uint32_t>(o.y >> 32)),
+                  "r"(static_cast<uint32_t>(mk.y >> 32)), "r"(static_cast<uint32_t>(o.x)),
+                  "r"(static_cast<uint32_t>(mk.x)), "r"(static_cast<uint32_t>(o.x >> 32)),
+                  "r"(static_cast<uint32_t>(mk.x >> 32)));
+            r -= bw;
           }
           tmp[r] = me;
         }
